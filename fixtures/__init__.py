@@ -1,0 +1,233 @@
+"""Seeded synthetic workloads shared by the oracle tests, the GPU tests and bench.py.
+
+This module holds NO arithmetic of the method (no convolution, coupling,
+encode, decode or classifier).  It only defines
+
+  * the architecture descriptors (workload definitions),
+  * a counter-based splitmix64 generator,
+  * the canonical flat parameter layout both sides parse independently,
+  * seeded inputs x ~ U[0,1) and per-group drop indices.
+
+Both the oracle (oracle/) and the CUDA path (paper_2106_06445_b200/) receive
+the arrays produced here; neither imports the other.
+
+Input recipe:
+  - images x[B, k, C, H, W] fp32, i.i.d. U[0,1) (PAPER.md:393-426 use MNIST /
+    CIFAR-10 images; values in [0,1) as ToTensor produces);
+  - weights per SURVEY §8a "Weight init" with gain gamma = 0.1;
+  - drop index per group j_b = (uint32)(splitmix64_at(seed, b) >> 32) % k:
+    one uniformly random main worker lost per group ("one of the
+    k workers", "randomly select an input x_a").
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+MASK64 = (1 << 64) - 1
+GOLDEN = 0x9E3779B97F4A7C15
+STREAM_MUL = 0xD1B54A32D192ED03
+
+
+# --------------------------------------------------------------------------
+# splitmix64 (counter based: the i-th output needs no previous state)
+# --------------------------------------------------------------------------
+def splitmix64_at(seed: int, idx):
+    """(idx+1)-th output of splitmix64 seeded with `seed` (vectorised over idx).
+
+    z_i = seed + (i+1)*GOLDEN;  z ^= z>>30; z *= 0xBF58476D1CE4E5B9;
+    z ^= z>>27; z *= 0x94D049BB133111EB; z ^= z>>31.
+    """
+    idx = np.asarray(idx, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = np.uint64(seed & MASK64) + (idx + np.uint64(1)) * np.uint64(GOLDEN)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    return z
+
+
+def stream_seed(seed: int, tensor_id: int) -> int:
+    return (seed ^ ((tensor_id * STREAM_MUL) & MASK64)) & MASK64
+
+
+def uniform01(seed: int, tensor_id: int, n: int) -> np.ndarray:
+    """n draws u = (z >> 11) * 2^-53 in [0,1), float64."""
+    z = splitmix64_at(stream_seed(seed, tensor_id), np.arange(n, dtype=np.uint64))
+    return (z >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+
+
+def uniform_f32(seed: int, tensor_id: int, n: int, lo: float, hi: float) -> np.ndarray:
+    u = uniform01(seed, tensor_id, n)
+    return (lo + (hi - lo) * u).astype(np.float32)
+
+
+# --------------------------------------------------------------------------
+# Architecture descriptors (readings Q1-Q6 in DESIGN.md)
+# --------------------------------------------------------------------------
+@dataclass(frozen=True)
+class Stage:
+    squeeze_before: int  # 1: apply psi (space-to-depth r=2) before the blocks
+    n_blocks: int
+    mid: int             # hidden width m of F = conv3x3(c->m) -> act -> conv3x3(m->c)
+
+
+@dataclass(frozen=True)
+class Arch:
+    name: str
+    in_c: int
+    in_h: int
+    in_w: int
+    stages: tuple
+    act: str = "relu"            # "relu" | "identity"
+    first_orient: int = 0        # 0: block 0 does s_B += F(s_A); 1: s_A += F(s_B)
+    heads: tuple = (10,)         # classes per linear head g_t
+    gamma: float = 0.1           # gain on W2
+    has_encoder: int = 0         # learned encoder (Arch E) params appended
+
+    def stage_shapes(self):
+        """[(C, H, W, c=C/2, m, n_blocks)] of each stage after its squeeze."""
+        C, H, W = self.in_c, self.in_h, self.in_w
+        out = []
+        for st in self.stages:
+            if st.squeeze_before:
+                C, H, W = C * 4, H // 2, W // 2
+            out.append((C, H, W, C // 2, st.mid, st.n_blocks))
+        return out
+
+    @property
+    def d(self) -> int:
+        C, H, W, *_ = self.stage_shapes()[-1]
+        return C * H * W
+
+    @property
+    def act_id(self) -> int:
+        return {"relu": 0, "identity": 2}[self.act]
+
+
+ARCH_T = Arch("T", 3, 8, 8, (Stage(1, 2, 16),))
+ARCH_M = Arch("M", 1, 28, 28, (Stage(1, 2, 32), Stage(1, 2, 64)))
+ARCH_C = Arch("C", 3, 32, 32, (Stage(1, 9, 64), Stage(1, 9, 128), Stage(1, 9, 256)))
+# Rotation pin (App. A.1) as three additive-coupling shears.
+ARCH_R = Arch("R", 2, 1, 1, (Stage(0, 3, 1),), act="identity", first_orient=1, heads=())
+ARCHS = {a.name: a for a in (ARCH_T, ARCH_M, ARCH_C, ARCH_R)}
+
+
+def linear_variant(arch: Arch) -> Arch:
+    """Same shapes, identity activation (P1: h is linear when biases are 0)."""
+    return Arch(arch.name + "lin", arch.in_c, arch.in_h, arch.in_w, arch.stages,
+                act="identity", first_orient=arch.first_orient, heads=arch.heads,
+                gamma=arch.gamma, has_encoder=arch.has_encoder)
+
+
+# --------------------------------------------------------------------------
+# Canonical flat parameter layout
+#   for stage s, block t:  W1[m][c][3][3], b1[m], W2[c][m][3][3], b2[c]
+#   then per head:         Wg[classes][d], bg[classes]
+# --------------------------------------------------------------------------
+def param_tensors(arch: Arch):
+    """[(name, shape, lo, hi)] in canonical order."""
+    out = []
+    for s, (C, H, W, c, m, nb) in enumerate(arch.stage_shapes()):
+        a1 = math.sqrt(6.0 / (9 * c))
+        a2 = arch.gamma * math.sqrt(3.0 / (9 * m))
+        for t in range(nb):
+            out.append((f"s{s}b{t}.W1", (m, c, 3, 3), -a1, a1))
+            out.append((f"s{s}b{t}.b1", (m,), -0.01, 0.01))
+            out.append((f"s{s}b{t}.W2", (c, m, 3, 3), -a2, a2))
+            out.append((f"s{s}b{t}.b2", (c,), -0.01, 0.01))
+    d = arch.d
+    ag = math.sqrt(3.0 / d)
+    for i, ncls in enumerate(arch.heads):
+        out.append((f"g{i}.W", (ncls, d), -ag, ag))
+        out.append((f"g{i}.b", (ncls,), -0.01, 0.01))
+    return out
+
+
+def n_params(arch: Arch) -> int:
+    return int(sum(np.prod(s) for _, s, _, _ in param_tensors(arch)))
+
+
+def make_weights(arch: Arch, seed: int, zero_bias: bool = False) -> np.ndarray:
+    """Flat fp32 parameter vector in canonical order (one splitmix64 stream per tensor)."""
+    parts = []
+    for tid, (name, shape, lo, hi) in enumerate(param_tensors(arch)):
+        n = int(np.prod(shape))
+        if zero_bias and (name.endswith(".b1") or name.endswith(".b2") or name.endswith(".b")):
+            parts.append(np.zeros(n, np.float32))
+        else:
+            parts.append(uniform_f32(seed, tid + 1, n, lo, hi))
+    return np.concatenate(parts) if parts else np.zeros(0, np.float32)
+
+
+def split_params(arch: Arch, flat: np.ndarray) -> dict:
+    """Views into the flat vector by canonical name (layout bookkeeping only)."""
+    out, off = {}, 0
+    for name, shape, _, _ in param_tensors(arch):
+        n = int(np.prod(shape))
+        out[name] = flat[off:off + n].reshape(shape)
+        off += n
+    assert off == flat.size
+    return out
+
+
+def rotation_params(theta: float, seed: int = 7) -> np.ndarray:
+    """ARCH_R parameters realising R(theta) as shears A,B,A.
+
+    Centre taps carry the shear; the 8 off-centre taps are random and must be
+    ignored by zero padding of the 1x1 image.
+    """
+    flat = make_weights(ARCH_R, seed)
+    p = split_params(ARCH_R, flat)
+    shear = [-math.tan(theta / 2), math.sin(theta), -math.tan(theta / 2)]
+    for t in range(3):
+        p[f"s0b{t}.W1"][0, 0, 1, 1] = 1.0
+        p[f"s0b{t}.b1"][:] = 0.0
+        p[f"s0b{t}.W2"][0, 0, 1, 1] = shear[t]
+        p[f"s0b{t}.b2"][:] = 0.0
+    return flat
+
+
+# --------------------------------------------------------------------------
+# Inputs and drops
+# --------------------------------------------------------------------------
+def make_inputs(arch: Arch, B: int, k: int, seed: int) -> np.ndarray:
+    n = B * k * arch.in_c * arch.in_h * arch.in_w
+    return uniform_f32(seed, 0, n, 0.0, 1.0).reshape(B, k, arch.in_c, arch.in_h, arch.in_w)
+
+
+def make_drops(B: int, k: int, seed: int) -> np.ndarray:
+    """j_b = (uint32)(splitmix64_at(seed, b) >> 32) % k, int32[B]."""
+    z = splitmix64_at(seed & MASK64, np.arange(B, dtype=np.uint64))
+    return ((z >> np.uint64(32)) % np.uint64(k)).astype(np.int32)
+
+
+def group_of(q, k: int):
+    """Query q -> (group b, slot i) = (q div k, q mod k)."""
+    q = np.asarray(q, dtype=np.int64)
+    return q // k, q % k
+
+
+# --------------------------------------------------------------------------
+# Named workloads = BASELINE.json configs
+# --------------------------------------------------------------------------
+@dataclass(frozen=True)
+class Config:
+    name: str
+    arch: Arch
+    k: int
+    B: int
+    seed_w: int
+    seed_x: int
+    seed_drop: int
+    note: str = ""
+
+
+CONFIGS = {
+    "C1": Config("C1", ARCH_T, 2, 4, 11, 1, 101, "k=2 tiny 2-block net on 3x8x8, 4 groups"),
+    "C2": Config("C2", ARCH_M, 4, 256, 12, 2, 102, "k=4 MNIST-shaped 1x28x28, 256 groups"),
+    "C3": Config("C3", ARCH_C, 10, 1024, 13, 3, 103,
+                 "k=10 CIFAR-shaped 3x32x32 full-depth h, exact h^-1 parity encode, 1024 groups"),
+}
