@@ -1,0 +1,175 @@
+/*
+ * codedinv.h -- C ABI of the B200-native Coded-InvNet hot path (arXiv 2106.06445).
+ *
+ * The library computes coded inference f = g o h over groups of k queries with one
+ * parity worker (n = k + 1, c_{1,j} = 1/k):
+ *   (1) h on the k main queries
+ *   (2) exact encode x_p = h^-1((1/k) sum_i h(x_i))
+ *   (3) h on the parity query                         PAPER.md:205 (every worker runs f, :330)
+ *   (4) decode h(x_j) = k h(x_p) - sum_{i!=j} h(x_i)
+ *   (5) linear heads g_t + argmax
+ *
+ * Conventions (all entry points):
+ *   - Tensor arguments are DEVICE pointers (except the *_host entry point), owned by the
+ *     caller, contiguous, fp32 (int32 for drop / labels), 16-byte aligned.
+ *   - Layouts: images NCHW [n][in_c][in_h][in_w]; features h [n][d] are the NCHW flatten of
+ *     the final state (d = C*H*W, h is dimension preserving);
+ *     groups are [B][k][...]: query q belongs to group q / k, slot q % k.
+ *   - Every call is asynchronous on `stream` (no hidden device sync) except ci_model_create,
+ *     ci_model_destroy, ci_check and ci_serve_group_host.  Hot calls do not allocate: the
+ *     caller passes a workspace of at least ci_workspace_size() bytes.  One workspace per
+ *     concurrent stream.
+ *   - Host-checkable errors (NULL/misaligned pointers, k < 1, B < 1, n < 0, head out of range,
+ *     workspace too small, dims mismatch) return synchronously with nothing enqueued.
+ *     Out-of-range drop indices found on the device are clamped to "no drop", counted in a
+ *     flag inside the workspace, and reported by ci_check() as CI_ERR_INVALID_ARG.
+ *   - CUDA launch failures map to CI_ERR_CUDA; ci_last_error() returns the thread-local text
+ *     of the last non-OK status.
+ *   - ci_model_t is immutable after create and safe to use from several streams.
+ *   - Determinism: results are bitwise reproducible for the same (device, precision, n);
+ *     F's accumulation order per output does not depend on tile position, so ci_inverse_h
+ *     undoes ci_forward_h up to fp32 rounding of the coupling adds.
+ */
+#ifndef CODEDINV_H_
+#define CODEDINV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define CI_API __attribute__((visibility("default")))
+#else
+#define CI_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+struct CUstream_st;
+typedef struct CUstream_st* ci_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef struct ci_model ci_model_t; /* opaque: packed device weights for h and heads */
+
+typedef enum {
+    CI_OK = 0,
+    CI_ERR_INVALID_ARG = 1,
+    CI_ERR_INVALID_SHAPE = 2, /* SPEC.md:40 InvalidShape */
+    CI_ERR_DIM_MISMATCH = 3,  /* SPEC.md:115 DimensionMismatch */
+    CI_ERR_UNSUPPORTED = 4,   /* arch/precision combination not built */
+    CI_ERR_WORKSPACE = 5,     /* workspace NULL or smaller than ci_workspace_size() */
+    CI_ERR_CUDA = 6
+} ci_status_t;
+
+typedef enum {
+    /* fp32 state, every conv operand split bf16 hi + lo, 3 tcgen05 MMAs per product
+     * (hi*hi + hi*lo + lo*hi), fp32 TMEM accumulators: the parity mode (<= 1e-3 vs oracle). */
+    CI_PREC_FP32 = 0,
+    /* fp32 state, bf16 operands, 1 tcgen05 MMA per product, fp32 TMEM accumulators. */
+    CI_PREC_BF16 = 1,
+    /* fp32 CUDA-core direct convolution (no tensor cores): a GPU cross-check mode. */
+    CI_PREC_SIMT = 2
+} ci_precision_t;
+
+typedef enum { CI_ENC_EXACT = 0 } ci_encode_mode_t;
+
+typedef struct {
+    int32_t squeeze_before; /* 1: psi (space-to-depth r=2) before this stage's blocks */
+    int32_t n_blocks;       /* additive coupling blocks in the stage */
+    int32_t mid_channels;   /* m: F = conv3x3(c->m) -> act -> conv3x3(m->c), c = C/2 */
+} ci_stage_t;
+
+typedef struct {
+    int32_t in_c, in_h, in_w; /* input image shape */
+    int32_t n_stages;         /* 1..4 */
+    ci_stage_t stage[4];
+    int32_t act;              /* 0 = ReLU, 2 = identity */
+    int32_t first_orientation;/* 0: block 0 of each stage does s_B += F(s_A); 1: s_A += F(s_B) */
+    int32_t n_heads;          /* 0..4 linear heads g_t */
+    int32_t head_classes[4];
+} ci_arch_t;
+
+/* Thread-local description of the last non-OK status (never NULL). */
+CI_API const char* ci_last_error(void);
+
+/* Build a model on `device` from the canonical flat fp32 parameter vector (host memory,
+ * copied; the caller keeps ownership):
+ *   per stage s, block t: W1[m][c][3][3], b1[m], W2[c][m][3][3], b2[c]
+ *   then per head t:      W[classes][d], b[classes]
+ * n_params must equal the count implied by `arch` (else CI_ERR_DIM_MISMATCH). */
+CI_API ci_status_t ci_model_create(const ci_arch_t* arch, const float* host_params, size_t n_params,
+                            ci_precision_t precision, int device, ci_model_t** out);
+CI_API void ci_model_destroy(ci_model_t* model);
+
+CI_API int64_t ci_feature_dim(const ci_model_t* model); /* d; -1 if model == NULL */
+
+/* Bytes of workspace needed by any call with up to B groups of k (or n = B * k images). */
+CI_API ci_status_t ci_workspace_size(const ci_model_t* model, int32_t k, int64_t B, size_t* bytes);
+
+/* Synchronise `stream` and report device-side flags recorded in `ws` (drop index out of
+ * range), then clear them. */
+CI_API ci_status_t ci_check(const ci_model_t* model, void* ws, size_t ws_bytes, ci_stream_t stream);
+
+/* h on n images: x [n][in_c][in_h][in_w] -> h [n][d].  x and h must not overlap.
+ * (SPEC.md:111-118 `forward`) */
+CI_API ci_status_t ci_forward_h(const ci_model_t* model, const float* x, float* h, int64_t n, void* ws,
+                         size_t ws_bytes, ci_stream_t stream);
+
+/* Exact inverse by reverse coupling: h [n][d] -> x [n][in_c][in_h][in_w]
+ * (blocks in reverse order, s_B -= F(s_A) / s_A -= F(s_B), psi^-1; SPEC.md:120-128 `inverse`;
+ * closed form, iteration count 0). */
+CI_API ci_status_t ci_inverse_h(const ci_model_t* model, const float* h, float* x, int64_t n, void* ws,
+                         size_t ws_bytes, ci_stream_t stream);
+
+/* Exact encode of B groups: m_b = (1/k) sum_{i<k} h[b][i] (fp32 sum in ascending i, then /k),
+ * x_parity[b] = h^-1(m_b).  h [B][k][d]; x_parity [B][in_c][in_h][in_w]; mean_out [B][d] or
+ * NULL.  (PAPER.md:125-127 Enc(x1,x2) = f^-1((f(x1)+f(x2))/2); :241 c_{1,j} = 1/k) */
+CI_API ci_status_t ci_encode(const ci_model_t* model, ci_encode_mode_t mode, int32_t k, int64_t B,
+                      const float* h, float* x_parity, float* mean_out, void* ws, size_t ws_bytes,
+                      ci_stream_t stream);
+
+/* In-place decode of B groups: for each b with j = drop[b] in [0,k):
+ *   h[b][j] = k * h_parity[b] - sum_{i != j, ascending} h[b][i]
+ * drop[b] = -1 leaves group b untouched; other values are flagged (see ci_check) and ignored.
+ * h [B][k][d], h_parity [B][d], drop [B] int32.  d must be a multiple of 4.
+ * (App. C: one scalar-vector multiply, k-1 subtractions) */
+CI_API ci_status_t ci_decode(int32_t k, int64_t B, int64_t d, float* h, const float* h_parity,
+                      const int32_t* drop, void* ws, size_t ws_bytes, ci_stream_t stream);
+
+/* Linear head t on n feature rows: logits [n][C_t] = z W_t^T + b_t (fp32),
+ * labels [n] = smallest index attaining the max (or NULL). */
+CI_API ci_status_t ci_classify(const ci_model_t* model, int32_t head, const float* z, int64_t n,
+                        float* logits, int32_t* labels, ci_stream_t stream);
+
+/* The whole coded path for B groups (steps 1-5 above) on one GPU:
+ *   x [B][k][in_c][in_h][in_w], drop [B]
+ *   h_out [B][k][d]     : h(x), with slot drop[b] replaced by its decoded estimate
+ *   h_parity [B][d]     : h(x_p)
+ *   x_parity [B][in_c][in_h][in_w] or NULL : the encoded query x_p
+ *   logits [n_heads][B][k][C_t] (heads packed one after another), labels [n_heads][B][k]
+ *   (either may be NULL to skip the heads) */
+CI_API ci_status_t ci_serve_group(const ci_model_t* model, ci_encode_mode_t mode, int32_t k, int64_t B,
+                           const float* x, const int32_t* drop, float* h_out, float* h_parity,
+                           float* x_parity, float* logits, int32_t* labels, void* ws,
+                           size_t ws_bytes, ci_stream_t stream);
+
+/* Same as ci_serve_group with HOST buffers (x, drop in; h_out, h_parity, logits, labels out;
+ * any output may be NULL).  Stages inputs into the workspace (which must be sized by
+ * ci_workspace_size_host), runs the path, copies outputs back and synchronises `stream`.
+ * Host buffers should be pinned for full PCIe bandwidth. */
+CI_API ci_status_t ci_workspace_size_host(const ci_model_t* model, int32_t k, int64_t B, size_t* bytes);
+CI_API ci_status_t ci_serve_group_host(const ci_model_t* model, ci_encode_mode_t mode, int32_t k,
+                                int64_t B, const float* x_host, const int32_t* drop_host,
+                                float* h_out_host, float* h_parity_host, float* logits_host,
+                                int32_t* labels_host, void* ws, size_t ws_bytes,
+                                ci_stream_t stream);
+
+/* Per-group drop indices generated on the device, bit-identical to the fixtures' host
+ * generator: drop[b] = (uint32)(splitmix64_at(seed, b) >> 32) % k (counter-based splitmix64;
+ * one uniformly random lost main worker per group). */
+CI_API ci_status_t ci_make_drops(int32_t k, int64_t B, uint64_t seed, int32_t* drop, ci_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CODEDINV_H_ */

@@ -1,0 +1,37 @@
+/*
+ * codedinv_testing.h -- test-only entry points of libcodedinv (not part of the serving ABI).
+ *
+ * They expose the tcgen05 building blocks of the convolution kernels so tests can pin the
+ * descriptor encodings the implicit 3x3 convolution depends on, and measure the raw MMA
+ * issue rate on the device.  Same conventions as codedinv.h (device pointers, async on
+ * `stream`, synchronous host-side argument errors).
+ */
+#ifndef CODEDINV_TESTING_H_
+#define CODEDINV_TESTING_H_
+
+#include "codedinv.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* One UMMA GEMM D[128][N] (fp32) = sum over nk K=16 steps of A-rows x B^T on tcgen05:
+ *   A [RA][KA] bf16 row-major (K contiguous), B [N][KB] bf16 row-major, D [128][N] fp32.
+ *   mode 0: step j uses A channels [16j, 16j+16) of rows shift..shift+127 and B columns
+ *           [16j, 16j+16)   (row-shifted start address, K-planes at LBO = RA*16 B);
+ *   mode 1: KA = 8; step j uses A channels 0..7 of rows shift+2j+i (K-half 0) and
+ *           shift+2j+1+i (K-half 1) against B columns [16j, 16j+16) (LBO = 16 B).
+ * Requires 16 <= N <= 256, N % 16 == 0, KA % 8 == 0, KB % 16 == 0, shift + 127 + 2nk < RA. */
+CI_API ci_status_t ci_test_umma_gemm(const uint16_t* A, int32_t RA, int32_t KA, const uint16_t* B,
+                                     int32_t N, int32_t KB, int32_t shift, int32_t mode, int32_t nk,
+                                     float* D, ci_stream_t stream);
+
+/* `nblocks` CTAs each issue `iters` back-to-back 128 x N x 16 bf16 MMAs from shared memory
+ * (SS mode) and record the issue-to-completion SM cycles in cycles[nblocks] (int64). */
+CI_API ci_status_t ci_test_umma_rate(int32_t N, int32_t iters, int32_t nblocks, int64_t* cycles,
+                                     ci_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CODEDINV_TESTING_H_ */

@@ -1,0 +1,206 @@
+"""Thin ctypes binding of libcodedinv.so (include/codedinv.h).
+
+Argument marshalling only: every step of the coded path runs in the library's CUDA
+kernels.  Tensors are torch CUDA tensors (device memory / streams come from PyTorch);
+the host-buffer entry point takes numpy arrays.  If the shared library is missing this
+module raises at import time -- there is no fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcodedinv.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+CI_OK, CI_ERR_INVALID_ARG, CI_ERR_INVALID_SHAPE, CI_ERR_DIM_MISMATCH, CI_ERR_UNSUPPORTED, \
+    CI_ERR_WORKSPACE, CI_ERR_CUDA = range(7)
+CI_PREC_FP32, CI_PREC_BF16, CI_PREC_SIMT = 0, 1, 2
+CI_ENC_EXACT = 0
+PRECISIONS = {"fp32": CI_PREC_FP32, "bf16": CI_PREC_BF16, "simt": CI_PREC_SIMT}
+
+EXPORTS = ["ci_last_error", "ci_model_create", "ci_model_destroy", "ci_feature_dim",
+           "ci_workspace_size", "ci_check", "ci_forward_h", "ci_inverse_h", "ci_encode",
+           "ci_decode", "ci_classify", "ci_serve_group", "ci_workspace_size_host",
+           "ci_serve_group_host", "ci_make_drops"]
+TESTING_EXPORTS = ["ci_test_umma_gemm", "ci_test_umma_rate"]  # include/codedinv_testing.h
+
+
+class CiStage(ctypes.Structure):
+    _fields_ = [("squeeze_before", ctypes.c_int32), ("n_blocks", ctypes.c_int32),
+                ("mid_channels", ctypes.c_int32)]
+
+
+class CiArch(ctypes.Structure):
+    _fields_ = [("in_c", ctypes.c_int32), ("in_h", ctypes.c_int32), ("in_w", ctypes.c_int32),
+                ("n_stages", ctypes.c_int32), ("stage", CiStage * 4), ("act", ctypes.c_int32),
+                ("first_orientation", ctypes.c_int32), ("n_heads", ctypes.c_int32),
+                ("head_classes", ctypes.c_int32 * 4)]
+
+
+_P, _I32, _I64, _SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+_sig = {
+    "ci_last_error": (ctypes.c_char_p, []),
+    "ci_model_create": (_I32, [_P, _P, _SZ, _I32, ctypes.c_int, _P]),
+    "ci_model_destroy": (None, [_P]),
+    "ci_feature_dim": (_I64, [_P]),
+    "ci_workspace_size": (_I32, [_P, _I32, _I64, _P]),
+    "ci_check": (_I32, [_P, _P, _SZ, _P]),
+    "ci_forward_h": (_I32, [_P, _P, _P, _I64, _P, _SZ, _P]),
+    "ci_inverse_h": (_I32, [_P, _P, _P, _I64, _P, _SZ, _P]),
+    "ci_encode": (_I32, [_P, _I32, _I32, _I64, _P, _P, _P, _P, _SZ, _P]),
+    "ci_decode": (_I32, [_I32, _I64, _I64, _P, _P, _P, _P, _SZ, _P]),
+    "ci_classify": (_I32, [_P, _I32, _P, _I64, _P, _P, _P]),
+    "ci_serve_group": (_I32, [_P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "ci_workspace_size_host": (_I32, [_P, _I32, _I64, _P]),
+    "ci_serve_group_host": (_I32, [_P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "ci_make_drops": (_I32, [_I32, _I64, ctypes.c_uint64, _P, _P]),
+    "ci_test_umma_gemm": (_I32, [_P, _I32, _I32, _P, _I32, _I32, _I32, _I32, _I32, _P, _P]),
+    "ci_test_umma_rate": (_I32, [_I32, _I32, _I32, _P, _P]),
+}
+for _name, (_res, _args) in _sig.items():
+    _f = getattr(_lib, _name)
+    _f.restype, _f.argtypes = _res, _args
+
+
+class CiError(RuntimeError):
+    def __init__(self, status, where):
+        super().__init__(f"{where}: status {status}: {_lib.ci_last_error().decode()}")
+        self.status = status
+
+
+def _check(status, where):
+    if status != CI_OK:
+        raise CiError(status, where)
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data_as(ctypes.c_void_p)
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def to_ci_arch(arch) -> CiArch:
+    a = CiArch()
+    a.in_c, a.in_h, a.in_w = arch.in_c, arch.in_h, arch.in_w
+    a.n_stages = len(arch.stages)
+    for i, st in enumerate(arch.stages):
+        a.stage[i].squeeze_before, a.stage[i].n_blocks, a.stage[i].mid_channels = \
+            st.squeeze_before, st.n_blocks, st.mid
+    a.act = arch.act_id
+    a.first_orientation = arch.first_orient
+    a.n_heads = len(arch.heads)
+    for i, c in enumerate(arch.heads):
+        a.head_classes[i] = c
+    return a
+
+
+class Model:
+    """Owns a ci_model_t.  `params` is the canonical flat fp32 vector (numpy)."""
+
+    def __init__(self, arch, params, precision="fp32", device=0):
+        self.arch = arch
+        self.precision = precision
+        p = np.ascontiguousarray(params, dtype=np.float32)
+        self._carch = to_ci_arch(arch)
+        h = ctypes.c_void_p()
+        _check(_lib.ci_model_create(ctypes.byref(self._carch), _ptr(p), p.size,
+                                    PRECISIONS[precision], device, ctypes.byref(h)), "ci_model_create")
+        self._h = h
+        self.d = int(_lib.ci_feature_dim(h))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.ci_model_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    # ---- workspace
+    def workspace_size(self, k, B):
+        n = ctypes.c_size_t()
+        _check(_lib.ci_workspace_size(self._h, k, B, ctypes.byref(n)), "ci_workspace_size")
+        return n.value
+
+    def workspace_size_host(self, k, B):
+        n = ctypes.c_size_t()
+        _check(_lib.ci_workspace_size_host(self._h, k, B, ctypes.byref(n)), "ci_workspace_size_host")
+        return n.value
+
+    def workspace(self, k, B, host=False):
+        import torch
+        n = self.workspace_size_host(k, B) if host else self.workspace_size(k, B)
+        return torch.zeros(n, dtype=torch.uint8, device="cuda")
+
+    # ---- ABI calls (same names as the C entry points)
+    def ci_forward_h(self, x, h, ws, stream=None):
+        _check(_lib.ci_forward_h(self._h, _ptr(x), _ptr(h), x.shape[0], _ptr(ws), ws.numel(),
+                                 _stream(stream)), "ci_forward_h")
+
+    def ci_inverse_h(self, h, x, ws, stream=None):
+        _check(_lib.ci_inverse_h(self._h, _ptr(h), _ptr(x), h.shape[0], _ptr(ws), ws.numel(),
+                                 _stream(stream)), "ci_inverse_h")
+
+    def ci_encode(self, h, x_parity, ws, mean_out=None, stream=None):
+        B, k = h.shape[0], h.shape[1]
+        _check(_lib.ci_encode(self._h, CI_ENC_EXACT, k, B, _ptr(h), _ptr(x_parity), _ptr(mean_out),
+                              _ptr(ws), ws.numel(), _stream(stream)), "ci_encode")
+
+    def ci_classify(self, head, z, logits, labels=None, stream=None):
+        _check(_lib.ci_classify(self._h, head, _ptr(z), z.shape[0], _ptr(logits), _ptr(labels),
+                                _stream(stream)), "ci_classify")
+
+    def ci_serve_group(self, x, drop, h_out, h_parity, ws, x_parity=None, logits=None, labels=None,
+                       stream=None):
+        B, k = x.shape[0], x.shape[1]
+        _check(_lib.ci_serve_group(self._h, CI_ENC_EXACT, k, B, _ptr(x), _ptr(drop), _ptr(h_out),
+                                   _ptr(h_parity), _ptr(x_parity), _ptr(logits), _ptr(labels),
+                                   _ptr(ws), ws.numel(), _stream(stream)), "ci_serve_group")
+
+    def ci_serve_group_host(self, x, drop, h_out, h_parity, logits, labels, ws, stream=None):
+        B, k = x.shape[0], x.shape[1]
+        _check(_lib.ci_serve_group_host(self._h, CI_ENC_EXACT, k, B, _ptr(x), _ptr(drop), _ptr(h_out),
+                                        _ptr(h_parity), _ptr(logits), _ptr(labels), _ptr(ws), ws.numel(),
+                                        _stream(stream)), "ci_serve_group_host")
+
+    def ci_check(self, ws, stream=None):
+        _check(_lib.ci_check(self._h, _ptr(ws), ws.numel(), _stream(stream)), "ci_check")
+
+
+def ci_decode(h, h_parity, drop, ws, stream=None):
+    B, k, d = h.shape
+    _check(_lib.ci_decode(k, B, d, _ptr(h), _ptr(h_parity), _ptr(drop), _ptr(ws), ws.numel(),
+                          _stream(stream)), "ci_decode")
+
+
+def ci_make_drops(k, B, seed, drop, stream=None):
+    _check(_lib.ci_make_drops(k, B, seed, _ptr(drop), _stream(stream)), "ci_make_drops")
+
+
+def ci_last_error() -> str:
+    return _lib.ci_last_error().decode()
+
+
+# ---- test-only entry points (include/codedinv_testing.h)
+def ci_test_umma_gemm(A, B, N, shift, mode, nk, D, stream=None):
+    _check(_lib.ci_test_umma_gemm(_ptr(A), A.shape[0], A.shape[1], _ptr(B), N, B.shape[1], shift, mode,
+                                  nk, _ptr(D), _stream(stream)), "ci_test_umma_gemm")
+
+
+def ci_test_umma_rate(N, iters, nblocks, cycles, stream=None):
+    _check(_lib.ci_test_umma_rate(N, iters, nblocks, _ptr(cycles), _stream(stream)), "ci_test_umma_rate")

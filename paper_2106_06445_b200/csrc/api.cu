@@ -1,0 +1,452 @@
+// C ABI of libcodedinv: argument validation, model packing, workspace carving and the
+// orchestration of the coded path (see include/codedinv.h for the contract).
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+
+#include "ci_internal.h"
+
+namespace ci {
+
+static thread_local char g_err[512] = "no error";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+ci_status_t cuda_status(cudaError_t e, const char* what) {
+    set_error("CUDA error %d (%s) in %s", (int)e, cudaGetErrorString(e), what);
+    return CI_ERR_CUDA;
+}
+
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+// ---------------------------------------------------------------------------
+// workspace layout
+// ---------------------------------------------------------------------------
+static constexpr size_t kAlign = 256;
+static size_t up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+struct WsLayout {
+    size_t flag = 0, scratch = 0, mean = 0, xp = 0, hidden = 0, total = 0;
+};
+
+static constexpr int64_t kSimtChunk = 1024;
+
+static WsLayout ws_layout(const Model* m, int32_t k, int64_t B) {
+    WsLayout L;
+    int64_t n = B * (int64_t)k;
+    size_t off = 0;
+    L.flag = off; off += up(256);
+    L.scratch = off; off += up(sizeof(float) * (size_t)(std::max<int64_t>(n, 1) * m->d));
+    L.mean = off; off += up(sizeof(float) * (size_t)(std::max<int64_t>(B, 1) * m->d));
+    L.xp = off; off += up(sizeof(float) * (size_t)(std::max<int64_t>(B, 1) * m->din));
+    L.hidden = off;
+    if (m->prec == CI_PREC_SIMT)
+        off += up(sizeof(float) * (size_t)(std::min<int64_t>(std::max<int64_t>(n, 1), kSimtChunk) * m->max_hidden));
+    L.total = off;
+    return L;
+}
+
+template <class T>
+static T* at(void* ws, size_t off) { return reinterpret_cast<T*>(reinterpret_cast<char*>(ws) + off); }
+
+// ---------------------------------------------------------------------------
+// h / h^-1 orchestration (both precisions share the stage-boundary permutations)
+// ---------------------------------------------------------------------------
+static ci_status_t run_stage_blocks(const Model* m, int s, float* state, int64_t n, bool inverse,
+                                    float* hidden, cudaStream_t st) {
+    const StageInfo& S = m->st[s];
+    if (m->umma) return umma_stage(m, s, state, n, inverse, st);
+    const int64_t per = (int64_t)S.C * S.H * S.W, half = (int64_t)S.c * S.H * S.W;
+    for (int tt = 0; tt < S.nb; tt++) {
+        int t = inverse ? S.nb - 1 - tt : tt;
+        const float* blk = m->d_params + m->blk_off[m->blk_first[s] + t];
+        const float* W1 = blk;
+        const float* b1 = W1 + (int64_t)S.m * S.c * 9;
+        const float* W2 = b1 + S.m;
+        const float* b2 = W2 + (int64_t)S.c * S.m * 9;
+        int orient = (m->arch.first_orientation + t) & 1;
+        int64_t src_off = orient == 0 ? 0 : half, dst_off = orient == 0 ? half : 0;
+        for (int64_t i0 = 0; i0 < n; i0 += kSimtChunk) {
+            int64_t nc = std::min<int64_t>(kSimtChunk, n - i0);
+            CI_CUDA(launch_conv_simt(state + i0 * per + src_off, per, S.c, S.H, S.W, W1, b1, S.m,
+                                     hidden, (int64_t)S.m * S.H * S.W, nc, 0, m->arch.act, st));
+            CI_CUDA(launch_conv_simt(hidden, (int64_t)S.m * S.H * S.W, S.m, S.H, S.W, W2, b2, S.c,
+                                     state + i0 * per + dst_off, per, nc, inverse ? 2 : 1, 0, st));
+        }
+    }
+    return CI_OK;
+}
+
+static ci_status_t forward_impl(const Model* m, const float* x, float* h, int64_t n, void* ws,
+                                const WsLayout& L, cudaStream_t st) {
+    if (n == 0) return CI_OK;
+    float* scratch = at<float>(ws, L.scratch);
+    float* hidden = at<float>(ws, L.hidden);
+    // stage s starts with a copy (psi or identity) into buffer buf[s]; last buffer = h
+    const int S = m->n_stages;
+    const float* src = x;
+    int C = m->arch.in_c, H = m->arch.in_h, W = m->arch.in_w;
+    for (int s = 0; s < S; s++) {
+        float* dst = ((S - 1 - s) % 2 == 0) ? h : scratch;
+        CI_CUDA(launch_permute(src, dst, n, C, H, W, m->st[s].squeeze ? 1 : 0, st));
+        C = m->st[s].C; H = m->st[s].H; W = m->st[s].W;
+        ci_status_t r = run_stage_blocks(m, s, dst, n, false, hidden, st);
+        if (r != CI_OK) return r;
+        src = dst;
+    }
+    return CI_OK;
+}
+
+static ci_status_t inverse_impl(const Model* m, const float* h, float* x, int64_t n, void* ws,
+                                const WsLayout& L, cudaStream_t st) {
+    if (n == 0) return CI_OK;
+    float* scratch = at<float>(ws, L.scratch);
+    float* hidden = at<float>(ws, L.hidden);
+    const int S = m->n_stages;
+    // copies: 1 initial + 1 after each stage -> S + 1 copies, the last one lands in x
+    int ncopy = S + 1, ci = 0;
+    auto target = [&](int i) { return ((ncopy - 1 - i) % 2 == 0) ? x : scratch; };
+    float* cur = target(ci++);
+    const StageInfo& L3 = m->st[S - 1];
+    CI_CUDA(launch_permute(h, cur, n, L3.C, L3.H, L3.W, 0, st));
+    for (int s = S - 1; s >= 0; s--) {
+        ci_status_t r = run_stage_blocks(m, s, cur, n, true, hidden, st);
+        if (r != CI_OK) return r;
+        float* nxt = target(ci++);
+        const StageInfo& Si = m->st[s];
+        CI_CUDA(launch_permute(cur, nxt, n, Si.C, Si.H, Si.W, Si.squeeze ? 2 : 0, st));
+        cur = nxt;
+    }
+    return CI_OK;
+}
+
+}  // namespace ci
+
+using namespace ci;
+
+// ===========================================================================
+// exported C ABI
+// ===========================================================================
+extern "C" {
+
+const char* ci_last_error(void) { return g_err; }
+
+ci_status_t ci_model_create(const ci_arch_t* arch, const float* host_params, size_t n_params,
+                            ci_precision_t precision, int device, ci_model_t** out) {
+    if (!arch || !host_params || !out) { set_error("NULL argument"); return CI_ERR_INVALID_ARG; }
+    *out = nullptr;
+    if (precision != CI_PREC_FP32 && precision != CI_PREC_BF16 && precision != CI_PREC_SIMT) {
+        set_error("unknown precision %d", (int)precision);
+        return CI_ERR_INVALID_ARG;
+    }
+    const ci_arch_t& a = *arch;
+    if (a.n_stages < 1 || a.n_stages > 4 || a.in_c < 1 || a.in_h < 1 || a.in_w < 1 ||
+        a.n_heads < 0 || a.n_heads > 4 || (a.act != 0 && a.act != 2)) {
+        set_error("invalid arch descriptor");
+        return CI_ERR_INVALID_SHAPE;
+    }
+    Model* m = new Model();
+    m->arch = a;
+    m->prec = precision;
+    m->device = device;
+    m->n_stages = a.n_stages;
+    int C = a.in_c, H = a.in_h, W = a.in_w;
+    int64_t off = 0;
+    for (int s = 0; s < a.n_stages; s++) {
+        const ci_stage_t& sg = a.stage[s];
+        if (sg.squeeze_before) {
+            if (H % 2 || W % 2) { delete m; set_error("psi needs even H, W"); return CI_ERR_INVALID_SHAPE; }
+            C *= 4; H /= 2; W /= 2;
+        }
+        if (C % 2 || sg.n_blocks < 1 || sg.mid_channels < 1) {
+            delete m; set_error("stage %d: odd channel count or empty stage", s); return CI_ERR_INVALID_SHAPE;
+        }
+        StageInfo& S = m->st[s];
+        S.C = C; S.H = H; S.W = W; S.c = C / 2; S.m = sg.mid_channels; S.nb = sg.n_blocks;
+        S.squeeze = sg.squeeze_before;
+        m->blk_first.push_back((int)m->blk_off.size());
+        for (int t = 0; t < S.nb; t++) {
+            m->blk_off.push_back(off);
+            off += (int64_t)S.m * S.c * 9 + S.m + (int64_t)S.c * S.m * 9 + S.c;
+        }
+        m->max_hidden = std::max<int64_t>(m->max_hidden, (int64_t)S.m * H * W);
+    }
+    m->d = (int64_t)C * H * W;
+    m->din = (int64_t)a.in_c * a.in_h * a.in_w;
+    if (m->d != m->din) { delete m; set_error("h must be dimension preserving"); return CI_ERR_INVALID_SHAPE; }
+    for (int t = 0; t < a.n_heads; t++) {
+        if (a.head_classes[t] < 1 || a.head_classes[t] > 16) {
+            delete m; set_error("head %d: classes must be in [1,16]", t); return CI_ERR_INVALID_SHAPE;
+        }
+        m->head_off[t] = off;
+        off += (int64_t)a.head_classes[t] * m->d + a.head_classes[t];
+    }
+    m->n_params = off;
+    if ((size_t)off != n_params) {
+        delete m;
+        set_error("n_params %zu != %lld implied by arch", n_params, (long long)off);
+        return CI_ERR_DIM_MISMATCH;
+    }
+    if (m->d % 4) { delete m; set_error("d must be a multiple of 4"); return CI_ERR_INVALID_SHAPE; }
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) { delete m; return cuda_status(e, "cudaSetDevice"); }
+    e = cudaMalloc(&m->d_params, sizeof(float) * (size_t)off);
+    if (e != cudaSuccess) { delete m; return cuda_status(e, "cudaMalloc params"); }
+    e = cudaMemcpy(m->d_params, host_params, sizeof(float) * (size_t)off, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) { cudaFree(m->d_params); delete m; return cuda_status(e, "cudaMemcpy params"); }
+    for (int t = 0; t < a.n_heads; t++) {
+        size_t nh = (size_t)a.head_classes[t] * (m->d + 1);
+        e = cudaMalloc(&m->d_head[t], sizeof(float) * nh);
+        if (e == cudaSuccess)
+            e = cudaMemcpy(m->d_head[t], host_params + m->head_off[t], sizeof(float) * nh, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) { ci_model_destroy(reinterpret_cast<ci_model_t*>(m)); return cuda_status(e, "head weights"); }
+    }
+    if (precision != CI_PREC_SIMT) {
+        ci_status_t r = umma_prepare(m, host_params);
+        if (r != CI_OK) { ci_model_destroy(reinterpret_cast<ci_model_t*>(m)); return r; }
+        m->umma = true;
+    }
+    *out = reinterpret_cast<ci_model_t*>(m);
+    return CI_OK;
+}
+
+void ci_model_destroy(ci_model_t* model) {
+    Model* m = reinterpret_cast<Model*>(model);
+    if (!m) return;
+    umma_release(m);
+    cudaFree(m->d_params);
+    for (int t = 0; t < 4; t++) cudaFree(m->d_head[t]);
+    delete m;
+}
+
+int64_t ci_feature_dim(const ci_model_t* model) {
+    const Model* m = reinterpret_cast<const Model*>(model);
+    return m ? m->d : -1;
+}
+
+ci_status_t ci_workspace_size(const ci_model_t* model, int32_t k, int64_t B, size_t* bytes) {
+    const Model* m = reinterpret_cast<const Model*>(model);
+    if (!m || !bytes || k < 1 || B < 0) { set_error("invalid argument"); return CI_ERR_INVALID_ARG; }
+    *bytes = ws_layout(m, k, B).total;
+    return CI_OK;
+}
+
+#define CI_MODEL_OR_FAIL(mv, model)                                          \
+    const Model* mv = reinterpret_cast<const Model*>(model);                 \
+    if (!mv) { set_error("NULL model"); return CI_ERR_INVALID_ARG; }
+
+static ci_status_t check_ws(const WsLayout& L, void* ws, size_t ws_bytes) {
+    if (!ws || !aligned16(ws) || ws_bytes < L.total) {
+        set_error("workspace %p of %zu bytes; need %zu (16-byte aligned)", ws, ws_bytes, L.total);
+        return CI_ERR_WORKSPACE;
+    }
+    return CI_OK;
+}
+
+ci_status_t ci_check(const ci_model_t* model, void* ws, size_t ws_bytes, ci_stream_t stream) {
+    (void)model;
+    if (!ws || ws_bytes < 256) { set_error("workspace too small"); return CI_ERR_WORKSPACE; }
+    int flag = 0;
+    CI_CUDA(cudaMemcpyAsync(&flag, ws, sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    CI_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    if (flag) {
+        CI_CUDA(cudaMemsetAsync(ws, 0, sizeof(int), (cudaStream_t)stream));
+        CI_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+        set_error("%d group(s) had a drop index outside [-1, k)", flag);
+        return CI_ERR_INVALID_ARG;
+    }
+    return CI_OK;
+}
+
+ci_status_t ci_forward_h(const ci_model_t* model, const float* x, float* h, int64_t n, void* ws,
+                         size_t ws_bytes, ci_stream_t stream) {
+    CI_MODEL_OR_FAIL(m, model);
+    if (n < 0 || (n > 0 && (!x || !h || !aligned16(x) || !aligned16(h)))) {
+        set_error("invalid x/h/n"); return CI_ERR_INVALID_ARG;
+    }
+    WsLayout L = ws_layout(m, 1, n);
+    ci_status_t r = check_ws(L, ws, ws_bytes);
+    if (r != CI_OK) return r;
+    return forward_impl(m, x, h, n, ws, L, (cudaStream_t)stream);
+}
+
+ci_status_t ci_inverse_h(const ci_model_t* model, const float* h, float* x, int64_t n, void* ws,
+                         size_t ws_bytes, ci_stream_t stream) {
+    CI_MODEL_OR_FAIL(m, model);
+    if (n < 0 || (n > 0 && (!x || !h || !aligned16(x) || !aligned16(h)))) {
+        set_error("invalid x/h/n"); return CI_ERR_INVALID_ARG;
+    }
+    WsLayout L = ws_layout(m, 1, n);
+    ci_status_t r = check_ws(L, ws, ws_bytes);
+    if (r != CI_OK) return r;
+    return inverse_impl(m, h, x, n, ws, L, (cudaStream_t)stream);
+}
+
+ci_status_t ci_encode(const ci_model_t* model, ci_encode_mode_t mode, int32_t k, int64_t B,
+                      const float* h, float* x_parity, float* mean_out, void* ws, size_t ws_bytes,
+                      ci_stream_t stream) {
+    CI_MODEL_OR_FAIL(m, model);
+    if (mode != CI_ENC_EXACT) { set_error("only CI_ENC_EXACT is built"); return CI_ERR_UNSUPPORTED; }
+    if (k < 1 || B < 0 || (B > 0 && (!h || !x_parity || !aligned16(h) || !aligned16(x_parity))) ||
+        (mean_out && !aligned16(mean_out))) {
+        set_error("invalid argument"); return CI_ERR_INVALID_ARG;
+    }
+    WsLayout L = ws_layout(m, k, B);
+    ci_status_t r = check_ws(L, ws, ws_bytes);
+    if (r != CI_OK) return r;
+    cudaStream_t st = (cudaStream_t)stream;
+    float* mean = mean_out ? mean_out : at<float>(ws, L.mean);
+    CI_CUDA(launch_mean(h, mean, k, B, m->d, st));
+    return inverse_impl(m, mean, x_parity, B, ws, L, st);
+}
+
+ci_status_t ci_decode(int32_t k, int64_t B, int64_t d, float* h, const float* h_parity,
+                      const int32_t* drop, void* ws, size_t ws_bytes, ci_stream_t stream) {
+    if (k < 1 || B < 0 || d < 0 || d % 4 ||
+        (B > 0 && (!h || !h_parity || !drop || !aligned16(h) || !aligned16(h_parity)))) {
+        set_error("invalid argument"); return CI_ERR_INVALID_ARG;
+    }
+    if (!ws || ws_bytes < 256 || !aligned16(ws)) { set_error("workspace too small"); return CI_ERR_WORKSPACE; }
+    CI_CUDA(launch_decode(h, h_parity, drop, k, B, d, reinterpret_cast<int*>(ws), (cudaStream_t)stream));
+    return CI_OK;
+}
+
+ci_status_t ci_classify(const ci_model_t* model, int32_t head, const float* z, int64_t n,
+                        float* logits, int32_t* labels, ci_stream_t stream) {
+    CI_MODEL_OR_FAIL(m, model);
+    if (head < 0 || head >= m->arch.n_heads) { set_error("head %d out of range", head); return CI_ERR_INVALID_ARG; }
+    if (n < 0 || (n > 0 && (!z || !aligned16(z)))) { set_error("invalid z/n"); return CI_ERR_INVALID_ARG; }
+    const float* W = m->d_head[head];
+    const float* b = W + (int64_t)m->arch.head_classes[head] * m->d;
+    CI_CUDA(launch_classify(z, n, m->d, W, b, m->arch.head_classes[head], logits, labels,
+                            (cudaStream_t)stream));
+    return CI_OK;
+}
+
+static ci_status_t serve_impl(const Model* m, int32_t k, int64_t B, const float* x,
+                              const int32_t* drop, float* h_out, float* h_parity, float* x_parity,
+                              float* logits, int32_t* labels, void* ws, const WsLayout& L,
+                              cudaStream_t st) {
+    const int64_t n = B * (int64_t)k;
+    ci_status_t r = forward_impl(m, x, h_out, n, ws, L, st);             // (1) h on main queries
+    if (r != CI_OK) return r;
+    float* mean = at<float>(ws, L.mean);
+    float* xp = x_parity ? x_parity : at<float>(ws, L.xp);
+    CI_CUDA(launch_mean(h_out, mean, k, B, m->d, st));                   // (2) encode: mean ...
+    r = inverse_impl(m, mean, xp, B, ws, L, st);                          //     ... then h^-1
+    if (r != CI_OK) return r;
+    r = forward_impl(m, xp, h_parity, B, ws, L, st);                      // (3) h on parity query
+    if (r != CI_OK) return r;
+    CI_CUDA(launch_decode(h_out, h_parity, drop, k, B, m->d, at<int>(ws, L.flag), st));  // (4)
+    if (logits || labels) {                                               // (5) heads
+        int64_t lo = 0;
+        for (int t = 0; t < m->arch.n_heads; t++) {
+            const float* W = m->d_head[t];
+            const float* b = W + (int64_t)m->arch.head_classes[t] * m->d;
+            CI_CUDA(launch_classify(h_out, n, m->d, W, b, m->arch.head_classes[t],
+                                    logits ? logits + lo : nullptr, labels ? labels + t * n : nullptr, st));
+            lo += n * m->arch.head_classes[t];
+        }
+    }
+    return CI_OK;
+}
+
+ci_status_t ci_serve_group(const ci_model_t* model, ci_encode_mode_t mode, int32_t k, int64_t B,
+                           const float* x, const int32_t* drop, float* h_out, float* h_parity,
+                           float* x_parity, float* logits, int32_t* labels, void* ws,
+                           size_t ws_bytes, ci_stream_t stream) {
+    CI_MODEL_OR_FAIL(m, model);
+    if (mode != CI_ENC_EXACT) { set_error("only CI_ENC_EXACT is built"); return CI_ERR_UNSUPPORTED; }
+    if (k < 1 || B < 0) { set_error("k must be >= 1 and B >= 0"); return CI_ERR_INVALID_ARG; }
+    if (B > 0 && (!x || !drop || !h_out || !h_parity || !aligned16(x) || !aligned16(h_out) ||
+                  !aligned16(h_parity) || (x_parity && !aligned16(x_parity)))) {
+        set_error("invalid pointer argument"); return CI_ERR_INVALID_ARG;
+    }
+    WsLayout L = ws_layout(m, k, B);
+    ci_status_t r = check_ws(L, ws, ws_bytes);
+    if (r != CI_OK) return r;
+    if (B == 0) return CI_OK;
+    return serve_impl(m, k, B, x, drop, h_out, h_parity, x_parity, logits, labels, ws, L,
+                      (cudaStream_t)stream);
+}
+
+// --- host-buffer variant: staging areas appended after the device workspace ---------------
+struct HostLayout {
+    WsLayout dev;
+    size_t x = 0, drop = 0, h = 0, p = 0, logits = 0, labels = 0, total = 0;
+};
+
+static HostLayout host_layout(const Model* m, int32_t k, int64_t B) {
+    HostLayout H;
+    H.dev = ws_layout(m, k, B);
+    int64_t n = B * (int64_t)k;
+    int64_t ncls = 0;
+    for (int t = 0; t < m->arch.n_heads; t++) ncls += m->arch.head_classes[t];
+    size_t off = H.dev.total;
+    H.x = off; off += up(sizeof(float) * (size_t)(n * m->din));
+    H.drop = off; off += up(sizeof(int32_t) * (size_t)B);
+    H.h = off; off += up(sizeof(float) * (size_t)(n * m->d));
+    H.p = off; off += up(sizeof(float) * (size_t)(B * m->d));
+    H.logits = off; off += up(sizeof(float) * (size_t)(n * ncls));
+    H.labels = off; off += up(sizeof(int32_t) * (size_t)(n * m->arch.n_heads));
+    H.total = off;
+    return H;
+}
+
+ci_status_t ci_workspace_size_host(const ci_model_t* model, int32_t k, int64_t B, size_t* bytes) {
+    const Model* m = reinterpret_cast<const Model*>(model);
+    if (!m || !bytes || k < 1 || B < 0) { set_error("invalid argument"); return CI_ERR_INVALID_ARG; }
+    *bytes = host_layout(m, k, B).total;
+    return CI_OK;
+}
+
+ci_status_t ci_serve_group_host(const ci_model_t* model, ci_encode_mode_t mode, int32_t k,
+                                int64_t B, const float* x_host, const int32_t* drop_host,
+                                float* h_out_host, float* h_parity_host, float* logits_host,
+                                int32_t* labels_host, void* ws, size_t ws_bytes,
+                                ci_stream_t stream) {
+    CI_MODEL_OR_FAIL(m, model);
+    if (mode != CI_ENC_EXACT) { set_error("only CI_ENC_EXACT is built"); return CI_ERR_UNSUPPORTED; }
+    if (k < 1 || B < 0 || (B > 0 && (!x_host || !drop_host))) { set_error("invalid argument"); return CI_ERR_INVALID_ARG; }
+    HostLayout H = host_layout(m, k, B);
+    if (!ws || !aligned16(ws) || ws_bytes < H.total) {
+        set_error("host workspace %zu bytes; need %zu", ws_bytes, H.total); return CI_ERR_WORKSPACE;
+    }
+    if (B == 0) return CI_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t n = B * (int64_t)k;
+    int64_t ncls = 0;
+    for (int t = 0; t < m->arch.n_heads; t++) ncls += m->arch.head_classes[t];
+    float* dx = at<float>(ws, H.x);
+    int32_t* ddrop = at<int32_t>(ws, H.drop);
+    float* dh = at<float>(ws, H.h);
+    float* dp = at<float>(ws, H.p);
+    float* dl = at<float>(ws, H.logits);
+    int32_t* dlab = at<int32_t>(ws, H.labels);
+    CI_CUDA(cudaMemcpyAsync(dx, x_host, sizeof(float) * n * m->din, cudaMemcpyHostToDevice, st));
+    CI_CUDA(cudaMemcpyAsync(ddrop, drop_host, sizeof(int32_t) * B, cudaMemcpyHostToDevice, st));
+    ci_status_t r = serve_impl(m, k, B, dx, ddrop, dh, dp, nullptr, dl, dlab, ws, H.dev, st);
+    if (r != CI_OK) return r;
+    if (h_out_host) CI_CUDA(cudaMemcpyAsync(h_out_host, dh, sizeof(float) * n * m->d, cudaMemcpyDeviceToHost, st));
+    if (h_parity_host) CI_CUDA(cudaMemcpyAsync(h_parity_host, dp, sizeof(float) * B * m->d, cudaMemcpyDeviceToHost, st));
+    if (logits_host && ncls) CI_CUDA(cudaMemcpyAsync(logits_host, dl, sizeof(float) * n * ncls, cudaMemcpyDeviceToHost, st));
+    if (labels_host && m->arch.n_heads)
+        CI_CUDA(cudaMemcpyAsync(labels_host, dlab, sizeof(int32_t) * n * m->arch.n_heads, cudaMemcpyDeviceToHost, st));
+    CI_CUDA(cudaStreamSynchronize(st));
+    return CI_OK;
+}
+
+ci_status_t ci_make_drops(int32_t k, int64_t B, uint64_t seed, int32_t* drop, ci_stream_t stream) {
+    if (k < 1 || B < 0 || (B > 0 && !drop)) { set_error("invalid argument"); return CI_ERR_INVALID_ARG; }
+    CI_CUDA(launch_make_drops(k, B, seed, drop, (cudaStream_t)stream));
+    return CI_OK;
+}
+
+}  // extern "C"

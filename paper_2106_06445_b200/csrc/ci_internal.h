@@ -1,0 +1,87 @@
+// Internal declarations of libcodedinv (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "codedinv.h"
+
+namespace ci {
+
+void set_error(const char* fmt, ...);
+ci_status_t cuda_status(cudaError_t e, const char* what);
+
+#define CI_CUDA(call)                                              \
+    do {                                                           \
+        cudaError_t e_ = (call);                                   \
+        if (e_ != cudaSuccess) return ::ci::cuda_status(e_, #call); \
+    } while (0)
+
+#define CI_CHECK_LAUNCH(what)                                      \
+    do {                                                           \
+        cudaError_t e_ = cudaGetLastError();                       \
+        if (e_ != cudaSuccess) return ::ci::cuda_status(e_, what); \
+    } while (0)
+
+struct StageInfo {
+    int C, H, W;   // state shape after the stage's squeeze
+    int c, m, nb;  // half channels, hidden width, blocks
+    int squeeze;   // psi before the stage
+};
+
+// Packed tcgen05 operands of one conv (see k_umma.cu for the layout).
+struct PackedConv {
+    int64_t off_hi = 0;   // element offset (bf16) into Model::d_wpack
+    int64_t off_lo = 0;   // lo split (CI_PREC_FP32 only)
+    int64_t bias_off = 0; // float offset into Model::d_bias
+};
+
+struct Model {
+    ci_arch_t arch;
+    ci_precision_t prec;
+    int device;
+    int n_stages;
+    StageInfo st[4];
+    int64_t d, din;
+    int64_t n_params;
+    float* d_params = nullptr;               // canonical flat fp32 params on device
+    std::vector<int64_t> blk_off;            // offset of W1 of block (s,t), flattened
+    std::vector<int> blk_first;              // first block index of each stage
+    int64_t head_off[4] = {0, 0, 0, 0};
+    float* d_head[4] = {nullptr, nullptr, nullptr, nullptr};  // 16-B aligned copy: W [C][d], then b [C]
+    int64_t max_hidden = 0;                  // max m*H*W over stages (SIMT scratch)
+    // tcgen05 path
+    uint16_t* d_wpack = nullptr;             // packed bf16 weights (hi [+ lo])
+    float* d_bias = nullptr;                 // padded biases
+    std::vector<PackedConv> pk1, pk2;        // per block: conv1, conv2
+    bool umma = false;
+};
+
+// ---- kernels (launchers) ------------------------------------------------------
+// permutation copy between stage layouts: mode 0 identity, 1 psi, 2 psi^-1
+// in: [n][C][H][W] of the SOURCE layout.  C,H,W are the source shape.
+cudaError_t launch_permute(const float* in, float* out, int64_t n, int C, int H, int W, int mode,
+                           cudaStream_t s);
+// SIMT conv3x3 (NCHW, fp32): out = act(conv(in) + b)   (mode 0)
+//                            out += conv(in) + b       (mode 1)
+//                            out -= conv(in) + b       (mode 2)
+cudaError_t launch_conv_simt(const float* in, int64_t in_stride, int Cin, int H, int W,
+                             const float* Wt, const float* b, int Cout, float* out,
+                             int64_t out_stride, int64_t n, int mode, int act, cudaStream_t s);
+cudaError_t launch_mean(const float* h, float* m, int k, int64_t B, int64_t d, cudaStream_t s);
+cudaError_t launch_decode(float* h, const float* p, const int32_t* drop, int k, int64_t B,
+                          int64_t d, int* flag, cudaStream_t s);
+cudaError_t launch_classify(const float* z, int64_t n, int64_t d, const float* W, const float* b,
+                            int C, float* logits, int32_t* labels, cudaStream_t s);
+cudaError_t launch_make_drops(int k, int64_t B, uint64_t seed, int32_t* drop, cudaStream_t s);
+
+// tcgen05 path (k_umma.cu)
+ci_status_t umma_prepare(Model* m, const float* host_params);
+void umma_release(Model* m);
+// Runs one stage (all blocks) on the fp32 NCHW state `state` [n][C][H][W] in place.
+ci_status_t umma_stage(const Model* m, int stage, float* state, int64_t n, bool inverse,
+                       cudaStream_t s);
+
+}  // namespace ci

@@ -1,0 +1,231 @@
+// HBM-bound kernels of the coded path: encode-mean (K7), decode (K8), linear heads +
+// argmax (K9) and the device drop-index generator (K12).
+//
+// Roofline: mean reads k*d*4 B and writes d*4 B per group; decode reads
+// (k-1)*d*4 + d*4 + 4 B and writes d*4 B per group.  Both are pure streams: float4
+// loads, one thread per (group, 4 features), grid sized to 148 SMs x resident blocks.
+#include "ci_internal.h"
+
+namespace ci {
+
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+// m[b][e] = (sum_{i=0}^{k-1} h[b][i][e]) / k ; fp32 sum in ascending i, then one division
+// (SURVEY Q7 reading; c_{1,j} = 1/k).
+template <int KMAX>
+__global__ void __launch_bounds__(256) k_mean(const float4* __restrict__ h, float4* __restrict__ m,
+                                              int k, int64_t B, int64_t d4) {
+    const int64_t total = B * d4;
+    const float fk = (float)k;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        int64_t b = idx / d4, e = idx - b * d4;
+        const float4* src = h + b * k * d4 + e;
+        float4 v[KMAX > 0 ? KMAX : 1];
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (KMAX > 0) {
+#pragma unroll
+            for (int i = 0; i < KMAX; i++)
+                if (i < k) v[i] = ld_stream(src + i * d4);
+#pragma unroll
+            for (int i = 0; i < KMAX; i++)
+                if (i < k) {
+                    acc.x = __fadd_rn(acc.x, v[i].x); acc.y = __fadd_rn(acc.y, v[i].y);
+                    acc.z = __fadd_rn(acc.z, v[i].z); acc.w = __fadd_rn(acc.w, v[i].w);
+                }
+        } else {
+            for (int i = 0; i < k; i++) {
+                float4 t = ld_stream(src + i * d4);
+                acc.x = __fadd_rn(acc.x, t.x); acc.y = __fadd_rn(acc.y, t.y);
+                acc.z = __fadd_rn(acc.z, t.z); acc.w = __fadd_rn(acc.w, t.w);
+            }
+        }
+        m[idx] = make_float4(__fdiv_rn(acc.x, fk), __fdiv_rn(acc.y, fk), __fdiv_rn(acc.z, fk),
+                             __fdiv_rn(acc.w, fk));
+    }
+}
+
+static int grid_for(int64_t total, int block) {
+    int64_t g = (total + block - 1) / block;
+    int64_t cap = 148 * (2048 / block) * 4;  // 4 waves of fully resident blocks
+    if (g > cap) g = cap;
+    return (int)(g < 1 ? 1 : g);
+}
+
+cudaError_t launch_mean(const float* h, float* m, int k, int64_t B, int64_t d, cudaStream_t s) {
+    int64_t d4 = d / 4, total = B * d4;
+    if (total == 0) return cudaSuccess;
+    int g = grid_for(total, 256);
+    auto H = reinterpret_cast<const float4*>(h);
+    auto M = reinterpret_cast<float4*>(m);
+    if (k <= 4) k_mean<4><<<g, 256, 0, s>>>(H, M, k, B, d4);
+    else if (k <= 10) k_mean<10><<<g, 256, 0, s>>>(H, M, k, B, d4);
+    else if (k <= 16) k_mean<16><<<g, 256, 0, s>>>(H, M, k, B, d4);
+    else k_mean<0><<<g, 256, 0, s>>>(H, M, k, B, d4);
+    return cudaGetLastError();
+}
+
+// h[b][j] = k * p[b] - sum_{i != j, ascending} h[b][i]   for j = drop[b] in [0,k)
+// (App. C).  In place; only slot j is written.
+template <int KMAX>
+__global__ void __launch_bounds__(256) k_decode(float4* __restrict__ h, const float4* __restrict__ p,
+                                                const int32_t* __restrict__ drop, int k, int64_t B,
+                                                int64_t d4, int* __restrict__ flag) {
+    const int64_t total = B * d4;
+    const float fk = (float)k;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        int64_t b = idx / d4, e = idx - b * d4;
+        int j = __ldg(drop + b);
+        if (j < 0) continue;
+        if (j >= k) {
+            if (e == 0) atomicAdd(flag, 1);
+            continue;
+        }
+        float4* g = h + b * k * d4 + e;
+        float4 pv = ld_stream(p + b * d4 + e);
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (KMAX > 0) {
+            float4 v[KMAX > 0 ? KMAX : 1];
+#pragma unroll
+            for (int i = 0; i < KMAX; i++)
+                if (i < k && i != j) v[i] = ld_stream(g + i * d4);
+#pragma unroll
+            for (int i = 0; i < KMAX; i++)
+                if (i < k && i != j) {
+                    acc.x = __fadd_rn(acc.x, v[i].x); acc.y = __fadd_rn(acc.y, v[i].y);
+                    acc.z = __fadd_rn(acc.z, v[i].z); acc.w = __fadd_rn(acc.w, v[i].w);
+                }
+        } else {
+            for (int i = 0; i < k; i++) {
+                if (i == j) continue;
+                float4 t = ld_stream(g + i * d4);
+                acc.x = __fadd_rn(acc.x, t.x); acc.y = __fadd_rn(acc.y, t.y);
+                acc.z = __fadd_rn(acc.z, t.z); acc.w = __fadd_rn(acc.w, t.w);
+            }
+        }
+        g[j * d4] = make_float4(__fmaf_rn(fk, pv.x, -acc.x), __fmaf_rn(fk, pv.y, -acc.y),
+                                __fmaf_rn(fk, pv.z, -acc.z), __fmaf_rn(fk, pv.w, -acc.w));
+    }
+}
+
+cudaError_t launch_decode(float* h, const float* p, const int32_t* drop, int k, int64_t B,
+                          int64_t d, int* flag, cudaStream_t s) {
+    int64_t d4 = d / 4, total = B * d4;
+    if (total == 0) return cudaSuccess;
+    int g = grid_for(total, 256);
+    auto H = reinterpret_cast<float4*>(h);
+    auto P = reinterpret_cast<const float4*>(p);
+    if (k <= 4) k_decode<4><<<g, 256, 0, s>>>(H, P, drop, k, B, d4, flag);
+    else if (k <= 10) k_decode<10><<<g, 256, 0, s>>>(H, P, drop, k, B, d4, flag);
+    else if (k <= 16) k_decode<16><<<g, 256, 0, s>>>(H, P, drop, k, B, d4, flag);
+    else k_decode<0><<<g, 256, 0, s>>>(H, P, drop, k, B, d4, flag);
+    return cudaGetLastError();
+}
+
+// logits[r][c] = sum_e W[c][e] z[r][e] + b[c]; label = first argmax.
+// One warp handles ROWS rows; lanes stride the feature axis with float4 loads; W (C x d)
+// is read through L1 once per ROWS rows.  Fixed reduction tree -> deterministic.
+constexpr int CLS_ROWS = 4;
+constexpr int CLS_CMAX = 16;
+__global__ void __launch_bounds__(256) k_classify(const float* __restrict__ z, int64_t n, int64_t d,
+                                                  const float* __restrict__ W,
+                                                  const float* __restrict__ bias, int C,
+                                                  float* __restrict__ logits,
+                                                  int32_t* __restrict__ labels) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t d4 = d >> 2;
+    for (int64_t r0 = warp * CLS_ROWS; r0 < n; r0 += nwarps * CLS_ROWS) {
+        float acc[CLS_ROWS][CLS_CMAX];
+#pragma unroll
+        for (int r = 0; r < CLS_ROWS; r++)
+#pragma unroll
+            for (int c = 0; c < CLS_CMAX; c++) acc[r][c] = 0.f;
+        for (int64_t e = lane; e < d4; e += 32) {
+            float4 zv[CLS_ROWS];
+#pragma unroll
+            for (int r = 0; r < CLS_ROWS; r++)
+                zv[r] = (r0 + r < n) ? ld_stream(reinterpret_cast<const float4*>(z + (r0 + r) * d) + e)
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int c = 0; c < CLS_CMAX; c++) {
+                if (c >= C) break;
+                float4 w = __ldg(reinterpret_cast<const float4*>(W + (int64_t)c * d) + e);
+#pragma unroll
+                for (int r = 0; r < CLS_ROWS; r++) {
+                    float a = acc[r][c];
+                    a = fmaf(w.x, zv[r].x, a);
+                    a = fmaf(w.y, zv[r].y, a);
+                    a = fmaf(w.z, zv[r].z, a);
+                    a = fmaf(w.w, zv[r].w, a);
+                    acc[r][c] = a;
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < CLS_ROWS; r++)
+#pragma unroll
+            for (int c = 0; c < CLS_CMAX; c++) {
+                if (c >= C) break;
+                float v = acc[r][c];
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+                acc[r][c] = v;
+            }
+        if (lane == 0) {
+#pragma unroll
+            for (int r = 0; r < CLS_ROWS; r++) {
+                int64_t row = r0 + r;
+                if (row >= n) break;
+                int best = 0;
+                float bv = 0.f;
+#pragma unroll
+                for (int c = 0; c < CLS_CMAX; c++) {
+                    if (c >= C) break;
+                    float v = acc[r][c] + __ldg(bias + c);
+                    if (logits) logits[row * C + c] = v;
+                    if (c == 0 || v > bv) { bv = v; best = c; }
+                }
+                if (labels) labels[row] = best;
+            }
+        }
+    }
+}
+
+cudaError_t launch_classify(const float* z, int64_t n, int64_t d, const float* W, const float* b,
+                            int C, float* logits, int32_t* labels, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    int64_t warps = (n + CLS_ROWS - 1) / CLS_ROWS;
+    int64_t blocks = (warps * 32 + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    k_classify<<<(unsigned)blocks, 256, 0, s>>>(z, n, d, W, b, C, logits, labels);
+    return cudaGetLastError();
+}
+
+// drop[b] = (uint32)(splitmix64_at(seed, b) >> 32) % k   (bit-identical to fixtures.make_drops)
+__global__ void k_make_drops(int k, int64_t B, uint64_t seed, int32_t* __restrict__ drop) {
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < B;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t z = seed + (uint64_t)(b + 1) * 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z = z ^ (z >> 31);
+        drop[b] = (int32_t)((uint32_t)(z >> 32) % (uint32_t)k);
+    }
+}
+
+cudaError_t launch_make_drops(int k, int64_t B, uint64_t seed, int32_t* drop, cudaStream_t s) {
+    if (B == 0) return cudaSuccess;
+    k_make_drops<<<grid_for(B, 256), 256, 0, s>>>(k, B, seed, drop);
+    return cudaGetLastError();
+}
+
+}  // namespace ci

@@ -1,0 +1,140 @@
+// Test-only probes of the tcgen05 building blocks (include/codedinv_testing.h):
+//  * ci_test_umma_gemm: one 128 x N x (16*nk) UMMA with the descriptor tricks the conv
+//    kernel relies on (row-shifted start address; LBO = 16 B pairing adjacent rows),
+//    checked against a host reference by tests/test_gpu_umma.py;
+//  * ci_test_umma_rate: back-to-back MMA issue rate per SM for a given N.
+#include <stdio.h>
+
+#include "ci_internal.h"
+#include "codedinv_testing.h"
+#include "umma.cuh"
+
+namespace ci {
+using namespace umma;
+
+// A: [RA][KA] bf16 row-major in global; B: [N][KB] bf16 row-major.  SMEM planes of 8 channels:
+// plane p holds rows 0..R-1 at 16-B stride (uniform, SBO = 128).
+__global__ void __launch_bounds__(128) k_umma_gemm(const uint16_t* __restrict__ A, int RA, int KA,
+                                                   const uint16_t* __restrict__ B, int N, int KB,
+                                                   int shift, int mode, int nk, float* __restrict__ D) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tmem_base;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int pa = KA / 8, pb = KB / 8;
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + (size_t)pa * RA * 16;
+    // fill planes (generic proxy)
+    for (int i = tid; i < RA * pa; i += 128) {
+        int r = i / pa, p = i % pa;
+        *reinterpret_cast<uint4*>(sA + ((size_t)p * RA + r) * 16) =
+            *reinterpret_cast<const uint4*>(A + (size_t)r * KA + p * 8);
+    }
+    for (int i = tid; i < N * pb; i += 128) {
+        int r = i / pb, p = i % pb;
+        *reinterpret_cast<uint4*>(sB + ((size_t)p * N + r) * 16) =
+            *reinterpret_cast<const uint4*>(B + (size_t)r * KB + p * 8);
+    }
+    fence_proxy_async();
+    if (warp == 0) tmem_alloc(&tmem_base, 256);
+    if (tid == 0) { mbar_init(&bar, 1); fence_mbar_init(); }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = tmem_base;
+    if (warp == 0 && elect_one()) {
+        const uint32_t idesc = idesc_bf16(128, N);
+        for (int j = 0; j < nk; j++) {
+            uint64_t ad, bd;
+            if (mode == 0) {  // K-halves = planes 2j, 2j+1
+                ad = smem_desc(smem_u32(sA) + (uint32_t)(2 * j * RA + shift) * 16, RA * 16, 128);
+            } else {          // K-halves = rows r and r+1 of plane 0 (LBO = 16 B); step j moves 2 rows
+                ad = smem_desc(smem_u32(sA) + (uint32_t)(shift + 2 * j) * 16, 16, 128);
+            }
+            bd = smem_desc(smem_u32(sB) + (uint32_t)(2 * j * N) * 16, N * 16, 128);
+            mma_bf16(tmem, ad, bd, idesc, j > 0);
+        }
+        commit(&bar);
+    }
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    fence_after();
+    for (int c = 0; c < N; c += 8) {
+        float v[8];
+        tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + c, v);
+        tmem_wait_ld();
+        for (int q = 0; q < 8; q++) D[(size_t)(warp * 32 + (tid & 31)) * N + c + q] = v[q];
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, 256);
+}
+
+__global__ void __launch_bounds__(128) k_umma_rate(int N, int iters, long long* __restrict__ cycles) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tmem_base;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    // A: 2 planes x (128 + 64) rows, B: 2 planes x 256 rows (zeros are fine)
+    for (int i = tid; i < (2 * 192 + 2 * 256) * 4; i += 128) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+    fence_proxy_async();
+    if (warp == 0) tmem_alloc(&tmem_base, 512);
+    if (tid == 0) { mbar_init(&bar, 1); fence_mbar_init(); }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = tmem_base;
+    if (warp == 0 && elect_one()) {
+        const uint32_t idesc = idesc_bf16(128, N);
+        const uint32_t a0 = smem_u32(smem), b0 = a0 + 2 * 192 * 16;
+        long long t0 = clock64();
+        for (int j = 0; j < iters; j++) {
+            uint64_t ad = smem_desc(a0 + (uint32_t)(j & 63) * 16, 192 * 16, 128);
+            uint64_t bd = smem_desc(b0, 256 * 16, 128);
+            mma_bf16(tmem + (uint32_t)((j & 1) * 256), ad, bd, idesc, 1);
+        }
+        commit(&bar);
+        mbar_wait(&bar, 0);
+        long long t1 = clock64();
+        cycles[blockIdx.x] = t1 - t0;
+    }
+    __syncwarp();
+    fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+}  // namespace ci
+
+using namespace ci;
+
+extern "C" {
+
+ci_status_t ci_test_umma_gemm(const uint16_t* A, int32_t RA, int32_t KA, const uint16_t* B, int32_t N,
+                              int32_t KB, int32_t shift, int32_t mode, int32_t nk, float* D,
+                              ci_stream_t stream) {
+    if (N < 16 || N > 256 || N % 16 || KA % 8 || KB % 16 || nk < 1 || shift < 0) {
+        set_error("bad probe shape");
+        return CI_ERR_INVALID_ARG;
+    }
+    size_t smem = (size_t)(KA / 8) * RA * 16 + (size_t)(KB / 8) * N * 16;
+    CI_CUDA(cudaFuncSetAttribute(k_umma_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_umma_gemm<<<1, 128, smem, (cudaStream_t)stream>>>(A, RA, KA, B, N, KB, shift, mode, nk, D);
+    CI_CHECK_LAUNCH("k_umma_gemm");
+    return CI_OK;
+}
+
+ci_status_t ci_test_umma_rate(int32_t N, int32_t iters, int32_t nblocks, int64_t* cycles,
+                              ci_stream_t stream) {
+    if (N < 16 || N > 256 || N % 16 || iters < 1 || nblocks < 1) {
+        set_error("bad probe shape");
+        return CI_ERR_INVALID_ARG;
+    }
+    size_t smem = (2 * 192 + 2 * 256) * 16;
+    CI_CUDA(cudaFuncSetAttribute(k_umma_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_umma_rate<<<nblocks, 128, smem, (cudaStream_t)stream>>>(N, iters, (long long*)cycles);
+    CI_CHECK_LAUNCH("k_umma_rate");
+    return CI_OK;
+}
+
+}  // extern "C"

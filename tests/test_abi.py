@@ -1,0 +1,88 @@
+"""CPU-only checks of the C-ABI library: it builds/loads, exports every symbol that
+include/codedinv.h declares, and rejects host-checkable bad arguments without a GPU."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import fixtures as fx
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def ci():
+    from paper_2106_06445_b200 import build
+    build.build()
+    from paper_2106_06445_b200 import codedinv
+    return codedinv
+
+
+def declared_symbols(header="*"):
+    import glob
+    syms = set()
+    for h in glob.glob(os.path.join(ROOT, "include", header + ".h")):
+        syms |= set(re.findall(r"CI_API[^;(]*?\b(ci_\w+)\s*\(", open(h).read()))
+    return sorted(syms)
+
+
+def test_header_declares_the_north_star_entry_points():
+    syms = declared_symbols("codedinv")
+    for name in ("ci_forward_h", "ci_inverse_h", "ci_encode", "ci_decode", "ci_classify",
+                 "ci_serve_group"):
+        assert name in syms
+
+
+def test_library_exports_every_declared_symbol(ci):
+    lib = ctypes.CDLL(ci.LIB_PATH)
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+    assert sorted(ci.EXPORTS + ci.TESTING_EXPORTS) == declared_symbols()
+
+
+def test_library_is_sm100a(ci):
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", ci.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_host_side_argument_errors(ci):
+    lib = ci._lib
+    # bad arch -> synchronous error before any device work
+    a = ci.to_ci_arch(fx.ARCH_T)
+    a.n_stages = 0
+    h = ctypes.c_void_p()
+    p = np.zeros(4, np.float32)
+    st = lib.ci_model_create(ctypes.byref(a), p.ctypes.data_as(ctypes.c_void_p), 4, 0, 0, ctypes.byref(h))
+    assert st == ci.CI_ERR_INVALID_SHAPE and "arch" in ci.ci_last_error()
+    # parameter count mismatch
+    a = ci.to_ci_arch(fx.ARCH_T)
+    st = lib.ci_model_create(ctypes.byref(a), p.ctypes.data_as(ctypes.c_void_p), 4, 0, 0, ctypes.byref(h))
+    assert st == ci.CI_ERR_DIM_MISMATCH
+    # unknown precision
+    st = lib.ci_model_create(ctypes.byref(a), p.ctypes.data_as(ctypes.c_void_p), 4, 9, 0, ctypes.byref(h))
+    assert st == ci.CI_ERR_INVALID_ARG
+    # decode: k < 1, misaligned, null workspace
+    assert lib.ci_decode(0, 1, 4, None, None, None, None, 0, None) == ci.CI_ERR_INVALID_ARG
+    assert lib.ci_decode(2, 1, 6, None, None, None, None, 0, None) == ci.CI_ERR_INVALID_ARG
+    buf = (ctypes.c_float * 64)()
+    addr = ctypes.addressof(buf)
+    assert lib.ci_decode(2, 1, 4, ctypes.c_void_p(addr), ctypes.c_void_p(addr + 32),
+                         ctypes.c_void_p(addr), None, 0, None) == ci.CI_ERR_WORKSPACE
+    # NULL model
+    assert lib.ci_feature_dim(None) == -1
+    assert lib.ci_forward_h(None, None, None, 1, None, 0, None) == ci.CI_ERR_INVALID_ARG
+    assert lib.ci_make_drops(0, 1, 1, None, None) == ci.CI_ERR_INVALID_ARG
+
+
+def test_binding_has_no_cpu_fallback():
+    """The product package never imports the oracle (or numpy math for the path)."""
+    pkg = os.path.join(ROOT, "paper_2106_06445_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".h", ".cpp")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in src.replace("no CPU fallback", ""), f
