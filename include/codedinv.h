@@ -131,7 +131,7 @@ CI_API ci_status_t ci_encode(const ci_model_t* model, ci_encode_mode_t mode, int
 /* In-place decode of B groups: for each b with j = drop[b] in [0,k):
  *   h[b][j] = k * h_parity[b] - sum_{i != j, ascending} h[b][i]
  * drop[b] = -1 leaves group b untouched; other values are flagged (see ci_check) and ignored.
- * h [B][k][d], h_parity [B][d], drop [B] int32.  d must be a multiple of 4.
+ * h [B][k][d], h_parity [B][d], drop [B] int32 (float4 path when d % 4 == 0).
  * (App. C: one scalar-vector multiply, k-1 subtractions) */
 CI_API ci_status_t ci_decode(int32_t k, int64_t B, int64_t d, float* h, const float* h_parity,
                       const int32_t* drop, void* ws, size_t ws_bytes, ci_stream_t stream);

@@ -27,9 +27,32 @@ CI_API ci_status_t ci_test_umma_gemm(const uint16_t* A, int32_t RA, int32_t KA, 
                                      float* D, ci_stream_t stream);
 
 /* `nblocks` CTAs each issue `iters` back-to-back 128 x N x 16 bf16 MMAs from shared memory
- * (SS mode) and record the issue-to-completion SM cycles in cycles[nblocks] (int64). */
+ * (SS mode) and record the issue-to-completion SM cycles in cycles[nblocks] (int64).
+ * N's upper bits select a variant: bits 16..23 = number of accumulators cycled (default 2),
+ * bits 24..31 = variant flags (1 packed accumulators, 2 LBO=16 A pairs, 4 spinning warps,
+ * 8 moving B, 16 periodic commits). */
 CI_API ci_status_t ci_test_umma_rate(int32_t N, int32_t iters, int32_t nblocks, int64_t* cycles,
                                      ci_stream_t stream);
+
+/* Kernel accounting for bench.py.
+ * ci_test_prof_enable(1) makes every fused tcgen05 stage launch record a CUDA event pair on
+ * its own stream, together with the launch's algorithmic FLOPs (2 MACs per 3x3-conv product,
+ * no padding); ci_test_prof_read() synchronises those events and returns, per stage index
+ * (0..3), the summed device milliseconds, launch count and algorithmic FLOPs, then clears them.
+ * ci_test_launch_count() returns the number of kernels this library has launched since the
+ * last call with reset != 0 (all kernels: stage, permute, mean, decode, classify, drops). */
+CI_API ci_status_t ci_test_prof_enable(int32_t enable);
+CI_API ci_status_t ci_test_prof_read(double* ms, int64_t* launches, double* flops);
+CI_API int64_t ci_test_launch_count(int32_t reset);
+
+/* Host-only: the shared-memory / TMEM plan the fused stage kernel uses for one stage
+ * (H x W state, c = half channels, m = hidden width).  out16 = {Wp, G, Cp, Mp, MC, nch, Nc2,
+ * T, I, Rtot, k1, k2, nslot, slot_bytes, smem_bytes, packed_bytes_per_block}. */
+CI_API ci_status_t ci_test_plan(int32_t H, int32_t W, int32_t c, int32_t m, int32_t prec3, int64_t* out16);
+
+/* The encode-mean kernel alone: m [B][d] = (sum_{i<k} h[b][i]) / k  (as inside ci_encode). */
+CI_API ci_status_t ci_test_mean(int32_t k, int64_t B, int64_t d, const float* h, float* m,
+                                ci_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -30,7 +30,8 @@ EXPORTS = ["ci_last_error", "ci_model_create", "ci_model_destroy", "ci_feature_d
            "ci_workspace_size", "ci_check", "ci_forward_h", "ci_inverse_h", "ci_encode",
            "ci_decode", "ci_classify", "ci_serve_group", "ci_workspace_size_host",
            "ci_serve_group_host", "ci_make_drops"]
-TESTING_EXPORTS = ["ci_test_umma_gemm", "ci_test_umma_rate"]  # include/codedinv_testing.h
+TESTING_EXPORTS = ["ci_test_umma_gemm", "ci_test_umma_rate", "ci_test_prof_enable", "ci_test_prof_read",
+                   "ci_test_launch_count", "ci_test_mean", "ci_test_plan"]  # include/codedinv_testing.h
 
 
 class CiStage(ctypes.Structure):
@@ -64,6 +65,11 @@ _sig = {
     "ci_make_drops": (_I32, [_I32, _I64, ctypes.c_uint64, _P, _P]),
     "ci_test_umma_gemm": (_I32, [_P, _I32, _I32, _P, _I32, _I32, _I32, _I32, _I32, _P, _P]),
     "ci_test_umma_rate": (_I32, [_I32, _I32, _I32, _P, _P]),
+    "ci_test_prof_enable": (_I32, [_I32]),
+    "ci_test_prof_read": (_I32, [_P, _P, _P]),
+    "ci_test_launch_count": (_I64, [_I32]),
+    "ci_test_mean": (_I32, [_I32, _I64, _I64, _P, _P, _P]),
+    "ci_test_plan": (_I32, [_I32, _I32, _I32, _I32, _I32, _P]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_lib, _name)
@@ -204,3 +210,35 @@ def ci_test_umma_gemm(A, B, N, shift, mode, nk, D, stream=None):
 
 def ci_test_umma_rate(N, iters, nblocks, cycles, stream=None):
     _check(_lib.ci_test_umma_rate(N, iters, nblocks, _ptr(cycles), _stream(stream)), "ci_test_umma_rate")
+
+
+def ci_test_prof_enable(enable=True):
+    _check(_lib.ci_test_prof_enable(1 if enable else 0), "ci_test_prof_enable")
+
+
+def ci_test_prof_read():
+    """-> (ms[4], launches[4], flops[4]) per stage index since the last read."""
+    ms = (ctypes.c_double * 4)()
+    ln = (ctypes.c_int64 * 4)()
+    fl = (ctypes.c_double * 4)()
+    _check(_lib.ci_test_prof_read(ms, ln, fl), "ci_test_prof_read")
+    return list(ms), list(ln), list(fl)
+
+
+def ci_test_launch_count(reset=False):
+    return int(_lib.ci_test_launch_count(1 if reset else 0))
+
+
+def ci_test_mean(h, m, stream=None):
+    B, k, d = h.shape
+    _check(_lib.ci_test_mean(k, B, d, _ptr(h), _ptr(m), _stream(stream)), "ci_test_mean")
+
+
+PLAN_FIELDS = ["Wp", "G", "Cp", "Mp", "MC", "nch", "Nc2", "T", "I", "Rtot", "k1", "k2", "nslot",
+               "slot_bytes", "smem", "blk_bytes"]
+
+
+def ci_test_plan(H, W, c, m, prec3):
+    out = (ctypes.c_int64 * 16)()
+    _check(_lib.ci_test_plan(H, W, c, m, 1 if prec3 else 0, out), "ci_test_plan")
+    return dict(zip(PLAN_FIELDS, list(out)))

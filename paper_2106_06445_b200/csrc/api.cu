@@ -5,12 +5,16 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 
 #include "ci_internal.h"
+#include "codedinv_testing.h"
 
 namespace ci {
 
 static thread_local char g_err[512] = "no error";
+static std::atomic<long long> g_launches{0};
+void count_launch(int n) { g_launches += n; }
 
 void set_error(const char* fmt, ...) {
     va_list ap;
@@ -194,7 +198,6 @@ ci_status_t ci_model_create(const ci_arch_t* arch, const float* host_params, siz
         set_error("n_params %zu != %lld implied by arch", n_params, (long long)off);
         return CI_ERR_DIM_MISMATCH;
     }
-    if (m->d % 4) { delete m; set_error("d must be a multiple of 4"); return CI_ERR_INVALID_SHAPE; }
     cudaError_t e = cudaSetDevice(device);
     if (e != cudaSuccess) { delete m; return cuda_status(e, "cudaSetDevice"); }
     e = cudaMalloc(&m->d_params, sizeof(float) * (size_t)off);
@@ -309,7 +312,7 @@ ci_status_t ci_encode(const ci_model_t* model, ci_encode_mode_t mode, int32_t k,
 
 ci_status_t ci_decode(int32_t k, int64_t B, int64_t d, float* h, const float* h_parity,
                       const int32_t* drop, void* ws, size_t ws_bytes, ci_stream_t stream) {
-    if (k < 1 || B < 0 || d < 0 || d % 4 ||
+    if (k < 1 || B < 0 || d < 0 ||
         (B > 0 && (!h || !h_parity || !drop || !aligned16(h) || !aligned16(h_parity)))) {
         set_error("invalid argument"); return CI_ERR_INVALID_ARG;
     }
@@ -441,6 +444,17 @@ ci_status_t ci_serve_group_host(const ci_model_t* model, ci_encode_mode_t mode, 
         CI_CUDA(cudaMemcpyAsync(labels_host, dlab, sizeof(int32_t) * n * m->arch.n_heads, cudaMemcpyDeviceToHost, st));
     CI_CUDA(cudaStreamSynchronize(st));
     return CI_OK;
+}
+
+ci_status_t ci_test_mean(int32_t k, int64_t B, int64_t d, const float* h, float* m, ci_stream_t stream) {
+    if (k < 1 || B < 0 || d < 0 || (B > 0 && (!h || !m))) { set_error("invalid argument"); return CI_ERR_INVALID_ARG; }
+    CI_CUDA(launch_mean(h, m, k, B, d, (cudaStream_t)stream));
+    return CI_OK;
+}
+
+int64_t ci_test_launch_count(int32_t reset) {
+    long long v = reset ? g_launches.exchange(0) : g_launches.load();
+    return (int64_t)v;
 }
 
 ci_status_t ci_make_drops(int32_t k, int64_t B, uint64_t seed, int32_t* drop, ci_stream_t stream) {

@@ -31,13 +31,6 @@ struct StageInfo {
     int squeeze;   // psi before the stage
 };
 
-// Packed tcgen05 operands of one conv (see k_umma.cu for the layout).
-struct PackedConv {
-    int64_t off_hi = 0;   // element offset (bf16) into Model::d_wpack
-    int64_t off_lo = 0;   // lo split (CI_PREC_FP32 only)
-    int64_t bias_off = 0; // float offset into Model::d_bias
-};
-
 struct Model {
     ci_arch_t arch;
     ci_precision_t prec;
@@ -55,9 +48,12 @@ struct Model {
     // tcgen05 path
     uint16_t* d_wpack = nullptr;             // packed bf16 weights (hi [+ lo])
     float* d_bias = nullptr;                 // padded biases
-    std::vector<PackedConv> pk1, pk2;        // per block: conv1, conv2
+    void* umma_state = nullptr;              // host-side stage plans (k_umma.cu)
     bool umma = false;
 };
+
+// ---- accounting (codedinv_testing.h)
+void count_launch(int n = 1);
 
 // ---- kernels (launchers) ------------------------------------------------------
 // permutation copy between stage layouts: mode 0 identity, 1 psi, 2 psi^-1

@@ -58,7 +58,38 @@ static int grid_for(int64_t total, int block) {
     return (int)(g < 1 ? 1 : g);
 }
 
+// scalar variants (d % 4 != 0, e.g. the 2-D rotation pin)
+__global__ void k_mean_scalar(const float* __restrict__ h, float* __restrict__ m, int k, int64_t B, int64_t d) {
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < B * d;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        int64_t b = idx / d, e = idx - b * d;
+        float acc = 0.f;
+        for (int i = 0; i < k; i++) acc = __fadd_rn(acc, h[(b * k + i) * d + e]);
+        m[idx] = __fdiv_rn(acc, (float)k);
+    }
+}
+__global__ void k_decode_scalar(float* __restrict__ h, const float* __restrict__ p, const int32_t* __restrict__ drop,
+                                int k, int64_t B, int64_t d, int* __restrict__ flag) {
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < B * d;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        int64_t b = idx / d, e = idx - b * d;
+        int j = drop[b];
+        if (j < 0) continue;
+        if (j >= k) { if (e == 0) atomicAdd(flag, 1); continue; }
+        float acc = 0.f;
+        for (int i = 0; i < k; i++)
+            if (i != j) acc = __fadd_rn(acc, h[(b * k + i) * d + e]);
+        h[(b * k + j) * d + e] = __fmaf_rn((float)k, p[b * d + e], -acc);
+    }
+}
+
 cudaError_t launch_mean(const float* h, float* m, int k, int64_t B, int64_t d, cudaStream_t s) {
+    if (d % 4) {
+        if (B * d == 0) return cudaSuccess;
+        k_mean_scalar<<<grid_for(B * d, 256), 256, 0, s>>>(h, m, k, B, d);
+        count_launch();
+        return cudaGetLastError();
+    }
     int64_t d4 = d / 4, total = B * d4;
     if (total == 0) return cudaSuccess;
     int g = grid_for(total, 256);
@@ -68,6 +99,7 @@ cudaError_t launch_mean(const float* h, float* m, int k, int64_t B, int64_t d, c
     else if (k <= 10) k_mean<10><<<g, 256, 0, s>>>(H, M, k, B, d4);
     else if (k <= 16) k_mean<16><<<g, 256, 0, s>>>(H, M, k, B, d4);
     else k_mean<0><<<g, 256, 0, s>>>(H, M, k, B, d4);
+    count_launch();
     return cudaGetLastError();
 }
 
@@ -117,6 +149,12 @@ __global__ void __launch_bounds__(256) k_decode(float4* __restrict__ h, const fl
 
 cudaError_t launch_decode(float* h, const float* p, const int32_t* drop, int k, int64_t B,
                           int64_t d, int* flag, cudaStream_t s) {
+    if (d % 4) {
+        if (B * d == 0) return cudaSuccess;
+        k_decode_scalar<<<grid_for(B * d, 256), 256, 0, s>>>(h, p, drop, k, B, d, flag);
+        count_launch();
+        return cudaGetLastError();
+    }
     int64_t d4 = d / 4, total = B * d4;
     if (total == 0) return cudaSuccess;
     int g = grid_for(total, 256);
@@ -126,6 +164,7 @@ cudaError_t launch_decode(float* h, const float* p, const int32_t* drop, int k, 
     else if (k <= 10) k_decode<10><<<g, 256, 0, s>>>(H, P, drop, k, B, d4, flag);
     else if (k <= 16) k_decode<16><<<g, 256, 0, s>>>(H, P, drop, k, B, d4, flag);
     else k_decode<0><<<g, 256, 0, s>>>(H, P, drop, k, B, d4, flag);
+    count_launch();
     return cudaGetLastError();
 }
 
@@ -200,13 +239,36 @@ __global__ void __launch_bounds__(256) k_classify(const float* __restrict__ z, i
     }
 }
 
+__global__ void k_classify_scalar(const float* __restrict__ z, int64_t n, int64_t d, const float* __restrict__ W,
+                                  const float* __restrict__ bias, int C, float* __restrict__ logits,
+                                  int32_t* __restrict__ labels) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+        int best = 0;
+        float bv = 0.f;
+        for (int c = 0; c < C; c++) {
+            float acc = 0.f;
+            for (int64_t e = 0; e < d; e++) acc = fmaf(W[c * d + e], z[r * d + e], acc);
+            float v = acc + bias[c];
+            if (logits) logits[r * C + c] = v;
+            if (c == 0 || v > bv) { bv = v; best = c; }
+        }
+        if (labels) labels[r] = best;
+    }
+}
+
 cudaError_t launch_classify(const float* z, int64_t n, int64_t d, const float* W, const float* b,
                             int C, float* logits, int32_t* labels, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
+    if (d % 4) {
+        k_classify_scalar<<<grid_for(n, 128), 128, 0, s>>>(z, n, d, W, b, C, logits, labels);
+        count_launch();
+        return cudaGetLastError();
+    }
     int64_t warps = (n + CLS_ROWS - 1) / CLS_ROWS;
     int64_t blocks = (warps * 32 + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
     k_classify<<<(unsigned)blocks, 256, 0, s>>>(z, n, d, W, b, C, logits, labels);
+    count_launch();
     return cudaGetLastError();
 }
 
@@ -225,6 +287,7 @@ __global__ void k_make_drops(int k, int64_t B, uint64_t seed, int32_t* __restric
 cudaError_t launch_make_drops(int k, int64_t B, uint64_t seed, int32_t* drop, cudaStream_t s) {
     if (B == 0) return cudaSuccess;
     k_make_drops<<<grid_for(B, 256), 256, 0, s>>>(k, B, seed, drop);
+    count_launch();
     return cudaGetLastError();
 }
 

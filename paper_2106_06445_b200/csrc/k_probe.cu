@@ -70,35 +70,79 @@ __global__ void __launch_bounds__(128) k_umma_gemm(const uint16_t* __restrict__ 
     if (warp == 0) tmem_dealloc(tmem, 256);
 }
 
-__global__ void __launch_bounds__(128) k_umma_rate(int N, int iters, long long* __restrict__ cycles) {
+// Issue-loop cost probe.  One elected thread issues `iters` k-steps of `ntile` MMAs each.
+// variant bits: 1 = A/B start addresses carried across iterations (add + wrap),
+// 2 = mbarrier try_wait on an already-completed barrier every k-step,
+// 4 = tcgen05.commit every k-step, 8 = B advances per k-step, 16 = fully static addresses
+__global__ void __launch_bounds__(128) k_umma_rate(int N, int iters, int ntile, int variant,
+                                                   long long* __restrict__ cycles) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ uint64_t bar;
+    __shared__ uint64_t bar, slot_bar, done_bar, slot_bar2;
     __shared__ uint32_t tmem_base;
     const int tid = threadIdx.x, warp = tid >> 5;
-    // A: 2 planes x (128 + 64) rows, B: 2 planes x 256 rows (zeros are fine)
-    for (int i = tid; i < (2 * 192 + 2 * 256) * 4; i += 128) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+    const int ARows = 1088;
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + 3 * ARows * 16;
+    for (int i = tid; i < (3 * ARows * 16 + 65536) / 4; i += 128) reinterpret_cast<uint32_t*>(smem)[i] = 0;
     fence_proxy_async();
     if (warp == 0) tmem_alloc(&tmem_base, 512);
-    if (tid == 0) { mbar_init(&bar, 1); fence_mbar_init(); }
+    if (tid == 0) { mbar_init(&bar, 1); mbar_init(&slot_bar, 1); mbar_init(&done_bar, 1); mbar_init(&slot_bar2, 1); fence_mbar_init(); }
     fence_before();
+    __syncthreads();
+    if (tid == 0) mbar_arrive(&done_bar);   // phase 0 completed
     __syncthreads();
     fence_after();
     const uint32_t tmem = tmem_base;
-    if (warp == 0 && elect_one()) {
+    if (warp == 0) {
         const uint32_t idesc = idesc_bf16(128, N);
-        const uint32_t a0 = smem_u32(smem), b0 = a0 + 2 * 192 * 16;
-        long long t0 = clock64();
-        for (int j = 0; j < iters; j++) {
-            uint64_t ad = smem_desc(a0 + (uint32_t)(j & 63) * 16, 192 * 16, 128);
-            uint64_t bd = smem_desc(b0, 256 * 16, 128);
-            mma_bf16(tmem + (uint32_t)((j & 1) * 256), ad, bd, idesc, 1);
+        const uint64_t a_desc0 = smem_desc(smem_u32(sA), ARows * 16, 128);
+        const uint64_t b_desc0 = smem_desc(smem_u32(sB), N * 16, 128);
+        const uint32_t dstride = 512u / (uint32_t)ntile;
+        if (elect_one()) {
+            long long t0 = clock64();
+            uint64_t ac = a_desc0, bc = b_desc0;
+            if (variant & 32) {   // v1-style loop. 64: A LBO 4320 B; 128: all MMAs into D=0;
+                                  // 256: B advances per MMA; 512: A alternates tiles (+2048 B)
+                const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+                const uint32_t albo = (variant & 64) ? 4320u : 192u * 16u;
+                for (int j = 0; j < iters; j++) {
+                    uint32_t aadr = a0 + (uint32_t)(j & 63) * 16 + ((variant & 512) ? (uint32_t)(j & 1) * 2048u : 0u);
+                    uint64_t ad = smem_desc(aadr, albo, 128);
+                    uint64_t bd = smem_desc(b0 + ((variant & 256) ? (uint32_t)(j & 7) * (uint32_t)N * 32u : 0u), (uint32_t)N * 16, 128);
+                    mma_bf16(tmem + (uint32_t)((j & 1) * ((variant & 128) ? 0 : 256)), ad, bd, idesc, 1);
+                    if ((j & 7) == 7) {
+                        if (variant & 8192) { mbar_wait(&done_bar, 0); }
+                        if (variant & 16384) { fence_after(); }
+                        if (variant & 32768) { commit(&slot_bar); }
+                    }
+                }
+                iters = 0;
+            }
+            for (int j = 0; j < iters; j++) {
+                uint64_t ad, bd;
+                if (variant & 16) { ad = a_desc0; bd = b_desc0; }
+                else if (variant & 1) { ad = ac; bd = bc; }
+                else { ad = a_desc0 + (uint64_t)((j * 7) & 63); bd = b_desc0 + ((variant & 8) ? (uint64_t)((j & 7) * N * 2) : 0); }
+                for (int t = 0; t < ntile; t++)
+                    mma_bf16(tmem + (uint32_t)t * dstride, ad + (uint64_t)(t * 128), bd, idesc, 1);
+                if (variant & 2) mbar_wait(&done_bar, 0);
+                if (variant & 4) commit(&slot_bar);
+                if (variant & 1) {
+                    ac += 7; if ((uint32_t)ac - (uint32_t)a_desc0 >= 64u) ac -= 64;
+                    if (variant & 8) { bc += (uint64_t)N * 2; if ((uint32_t)bc - (uint32_t)b_desc0 >= (uint32_t)(16 * N)) bc = b_desc0; }
+                }
+            }
+            commit(&bar);
+            mbar_wait(&bar, 0);
+            long long t1 = clock64();
+            cycles[blockIdx.x] = t1 - t0;
+            mbar_arrive(&slot_bar2);
         }
-        commit(&bar);
-        mbar_wait(&bar, 0);
-        long long t1 = clock64();
-        cycles[blockIdx.x] = t1 - t0;
+        __syncwarp();
+    } else if (variant & 2048) {          // warps 1..3 spin on try_wait during the MMAs
+        if ((variant & 4096) == 0 || (tid & 31) == 0) mbar_wait(&slot_bar2, 0);
+        __syncwarp();
     }
-    __syncwarp();
     fence_before();
     __syncthreads();
     if (warp == 0) tmem_dealloc(tmem, 512);
@@ -126,13 +170,16 @@ ci_status_t ci_test_umma_gemm(const uint16_t* A, int32_t RA, int32_t KA, const u
 
 ci_status_t ci_test_umma_rate(int32_t N, int32_t iters, int32_t nblocks, int64_t* cycles,
                               ci_stream_t stream) {
-    if (N < 16 || N > 256 || N % 16 || iters < 1 || nblocks < 1) {
+    int32_t ntile = (N >> 16) & 0xFF, variant = N >> 24;
+    N &= 0xFFFF;
+    if (ntile < 1) ntile = 2;
+    if (N < 16 || N > 256 || N % 16 || iters < 1 || nblocks < 1 || ntile * N > 512) {
         set_error("bad probe shape");
         return CI_ERR_INVALID_ARG;
     }
-    size_t smem = (2 * 192 + 2 * 256) * 16;
+    size_t smem = 3 * 1088 * 16 + 65536;
     CI_CUDA(cudaFuncSetAttribute(k_umma_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_umma_rate<<<nblocks, 128, smem, (cudaStream_t)stream>>>(N, iters, (long long*)cycles);
+    k_umma_rate<<<nblocks, 128, smem, (cudaStream_t)stream>>>(N, iters, ntile, variant, (long long*)cycles);
     CI_CHECK_LAUNCH("k_umma_rate");
     return CI_OK;
 }

@@ -40,6 +40,7 @@ cudaError_t launch_permute(const float* in, float* out, int64_t n, int C, int H,
     int64_t blocks = (total + 255) / 256;
     if (blocks > 148 * 64) blocks = 148 * 64;
     k_permute<<<(unsigned)blocks, 256, 0, s>>>(in, out, total, C, H, W, mode);
+    count_launch();
     return cudaGetLastError();
 }
 
@@ -98,6 +99,7 @@ cudaError_t launch_conv_simt(const float* in, int64_t in_stride, int Cin, int H,
     if (blocks > 148 * 32) blocks = 148 * 32;
     k_conv_simt<<<(unsigned)blocks, 256, 0, s>>>(in, in_stride, Cin, H, W, Wt, b, Cout, out,
                                                  out_stride, n, mode, act);
+    count_launch();
     return cudaGetLastError();
 }
 

@@ -1,14 +1,906 @@
-// tcgen05 path: placeholder until the fused stage kernel lands.
+// Fused tcgen05 stage kernel: all additive-coupling blocks of one stage of h (or h^-1),
+//   s_out <- s_out (+|-) F(s_in),  F = conv3x3(W2) o act o conv3x3(W1)
+// for a batch of images resident in shared memory, on 5th-gen tensor cores.
+//
+// Design:
+//  * Implicit 3x3 convolution with NO im2col: activations live in shared memory as bf16
+//    "planes" of 8 channels, one 16-byte row per pixel, in a zero-padded raster (one pad
+//    column per image row, one zero row band between images).  The A operand of tap (u,v)
+//    is the same buffer with the UMMA descriptor start moved by u*Wp + v rows (16 B each):
+//    9 taps = 9 shifted views, zero padding comes from the pad rows/columns.  For inputs with
+//    <= 8 channels two horizontally adjacent taps share one K=16 MMA (LBO = 16 B).
+//  * conv1 -> act -> conv2 fused per hidden-channel chunk: conv1 accumulates in TMEM, the
+//    epilogue warps apply bias + activation, round to bf16 (hi [+ lo]) into the hidden plane
+//    buffer in shared memory, conv2 accumulates all chunks in TMEM; the conv2 epilogue adds
+//    (or subtracts, for h^-1) bias + F into the fp32 state in global memory and writes the
+//    bf16 shadow of the updated half back to shared memory as the next block's input.
+//    The fp32 state makes one global round trip per block; the hidden never leaves the SM.
+//  * Weights are pre-packed on the host in exactly the MMA consumption order (UMMA K-major
+//    no-swizzle core-matrix layout) and streamed by one producer thread with
+//    cp.async.bulk (TMA engine) through an mbarrier ring; every weight slot is reused by all
+//    T M-tiles of the CTA.
+//  * Warp roles: warp 0 = producer, warp 1 = MMA issuer (one thread), warps 2..5 = epilogue
+//    (thread <-> TMEM lane <-> pixel row).
+//  * CI_PREC_FP32 ("bf16x3"): operands split x = hi + lo (bf16 each); 3 MMAs per k-step
+//    (hi*hi + hi*lo + lo*hi) into the same fp32 accumulator.
+//  * Determinism: the k-step order per accumulator is fixed and independent of the tile or
+//    batch position, so forward and inverse compute bit-identical F for identical inputs.
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
 #include "ci_internal.h"
+#include <cuda_bf16.h>
+
+#include "codedinv_testing.h"
+#include "umma.cuh"
+
 namespace ci {
+using namespace umma;
+
+constexpr int kThreads = 192;      // 6 warps
+constexpr int kEpiThreads = 128;   // warps 2..5
+constexpr int kMaxSlots = 6;
+
+struct StagePlan {
+    int H, W, Wp, G;       // image, padded width, guard rows
+    int c, m, Cp, Mp, MC, nch, Nc2;
+    int T, I;              // M-tiles per CTA batch, images per batch
+    int Rtot;              // rows per plane incl. guards
+    int pair;              // conv1 pair mode (Cp == 8)
+    int k1, k2;            // k-steps per chunk: conv1, conv2
+    int prec3;             // bf16x3
+    int nslot, slot_bytes;
+    int64_t blk_bytes;     // packed weight stream bytes per block
+    size_t smem;
+    int tmem_cols;
+};
+
+struct StageArgs {
+    float* state;
+    int64_t n;
+    const uint8_t* wpack;  // stage stream: block t at t * blk_bytes
+    const float* bias;     // block t: [Mp] b1 then [Nc2] b2
+    int C, nb, first_orient, act, inverse;
+    unsigned long long* dbg;  // optional per-CTA cycle counters (CI_DEBUG_CYCLES), 16 per CTA
+    StagePlan p;
+};
+
+// ----------------------------------------------------------------------------------------
+// schedule helpers shared by producer / MMA (device) and packer (host)
+// ----------------------------------------------------------------------------------------
+__host__ __device__ inline int kstep_bytes(int N, int prec3) { return N * 32 * (prec3 ? 2 : 1); }
+__host__ __device__ inline int steps_per_slot(int N, int prec3, int slot_bytes) {
+    int g = slot_bytes / kstep_bytes(N, prec3);
+    return g < 1 ? 1 : g;
+}
+
+__device__ __forceinline__ uint32_t bf16_bits(float v) {
+    return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v));
+}
+__device__ __forceinline__ float bf16_val(uint32_t b) {
+    return __bfloat162float(__ushort_as_bfloat16((unsigned short)b));
+}
+
+// pixel row r of a batch -> (image in batch, y, x), or false for pad/zero rows
+__device__ __forceinline__ bool row_pixel(int r, const StagePlan& p, int& ii, int& y, int& x) {
+    int band = r / p.Wp;
+    x = r - band * p.Wp;
+    ii = band / (p.H + 1);
+    int yy = band - ii * (p.H + 1);
+    y = yy - 1;
+    return yy != 0 && x < p.W;
+}
+
+// ----------------------------------------------------------------------------------------
+// Compile-time specialised MMA issue for one conv segment (conv1 chunk or conv2 chunk).
+// Every k-step's A/B descriptor offsets, accumulate flags and ring-slot boundaries are
+// constants, so each MMA costs one uniform add + UTCHMMA in the issuing thread.
+//   alo0  : low descriptor word (start>>4 | LBO>>4 << 16) of the A buffer at row G, plane 0
+//   ringlo: low descriptor word of ring slot 0 with this segment's B LBO field
+// ----------------------------------------------------------------------------------------
+template <int K, int PER, bool PAIR, int WP, int PLANE16, int G, int KB16, int T, int N, bool P3,
+          int LOA16, int ACC0, int DSTRIDE>
+__device__ __forceinline__ void issue_static(uint32_t tmem, uint32_t alo0, uint32_t ringlo, uint32_t slot16,
+                                             uint32_t idesc, uint32_t acc_first, int& slot, uint32_t& phase,
+                                             int nslot, uint64_t* full, uint64_t* empty) {
+    constexpr uint32_t HI = 0x4008u;   // SBO = 128 B, descriptor version 1
+    uint32_t bl = 0;
+#pragma unroll
+    for (int s = 0; s < K; s++) {
+        if (s % G == 0) {
+            mbar_wait(&full[slot], phase);
+            fence_after();
+            bl = ringlo + (uint32_t)slot * slot16;
+        }
+        constexpr int dummy = 0;
+        (void)dummy;
+        const int shift = PAIR ? (s / 2 - 1) * WP + ((s & 1) ? 1 : -1)
+                               : ((s / PER) / 3 - 1) * WP + ((s / PER) % 3 - 1);
+        const int poff16 = PAIR ? 0 : 2 * (s % PER) * PLANE16;
+        const uint32_t al = alo0 + (uint32_t)(shift + poff16);
+        const uint32_t b = bl + (uint32_t)((s % G) * KB16);
+#pragma unroll
+        for (int t = 0; t < T; t++) {
+            const uint64_t ad = ((uint64_t)HI << 32) | (al + (uint32_t)(t * 128));
+            const uint64_t bd = ((uint64_t)HI << 32) | b;
+            const uint32_t d = tmem + (uint32_t)(ACC0 + t * DSTRIDE);
+            mma_bf16(d, ad, bd, idesc, s == 0 ? acc_first : 1u);
+            if (P3) {
+                mma_bf16(d, ad, bd + (uint64_t)(N * 2), idesc, 1u);
+                mma_bf16(d, ad + (uint64_t)LOA16, bd, idesc, 1u);
+            }
+        }
+        if (s % G == G - 1 || s == K - 1) {
+            commit(&empty[slot]);
+            if (++slot == nslot) { slot = 0; phase ^= 1; }
+        }
+    }
+}
+
+// Static stage configuration (0 = use the runtime plan)
+template <int WP_, int CP_, int MC_, int NC2_, int T_, int P3_, int SLOT_>
+struct SCfg {
+    static constexpr bool kStatic = WP_ > 0;
+    static constexpr int WP = WP_, CP = CP_, MC = MC_, NC2 = NC2_, T = T_, SLOT = SLOT_;
+    static constexpr bool P3 = P3_ != 0;
+    static constexpr int G = WP + 2;
+    static constexpr int RTOT = T * 128 + 2 * G;
+    static constexpr int PLANE16 = RTOT;                 // plane bytes / 16
+    static constexpr bool PAIR = CP == 8;
+    static constexpr int PER1 = PAIR ? 2 : CP / 16;
+    static constexpr int K1 = PAIR ? 6 : 9 * (CP / 16);
+    static constexpr int PER2 = MC / 16;
+    static constexpr int K2 = 9 * (MC / 16);
+    static constexpr int KB1 = MC * 32 * (P3 ? 2 : 1), KB2 = NC2 * 32 * (P3 ? 2 : 1);
+    static constexpr int G1 = (SLOT / (KB1 > 0 ? KB1 : 1)) < 1 ? 1 : SLOT / (KB1 > 0 ? KB1 : 1);
+    static constexpr int G2 = (SLOT / (KB2 > 0 ? KB2 : 1)) < 1 ? 1 : SLOT / (KB2 > 0 ? KB2 : 1);
+    static constexpr int ACC1 = T * NC2;
+    static constexpr int LOX16 = (CP / 8) * PLANE16;
+    static constexpr int LOH16 = (MC / 8) * PLANE16;
+};
+using SDyn = SCfg<0, 0, 0, 0, 0, 0, 0>;
+
+#define TWAIT(acc, call)                                      \
+    do {                                                      \
+        long long t0_ = a.dbg ? clock64() : 0;                \
+        call;                                                 \
+        if (a.dbg) acc += (unsigned long long)(clock64() - t0_); \
+    } while (0)
+
+template <class CFG>
+__global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
+    const StagePlan& p = a.p;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int P = p.prec3 ? 2 : 1;
+
+    // ---- shared memory carve-up
+    uint8_t* ring = smem;                                           // nslot * slot_bytes
+    uint8_t* xbuf = ring + (size_t)p.nslot * p.slot_bytes;          // P * Cp/8 planes
+    const uint32_t plane_bytes = (uint32_t)p.Rtot * 16;
+    uint8_t* hbuf = xbuf + (size_t)P * (p.Cp / 8) * plane_bytes;    // P * MC/8 planes
+    uint64_t* bars = reinterpret_cast<uint64_t*>(hbuf + (size_t)P * (p.MC / 8) * plane_bytes);
+    uint64_t* full = bars;                  // [kMaxSlots]
+    uint64_t* empty = bars + kMaxSlots;     // [kMaxSlots]
+    uint64_t* x_full = bars + 2 * kMaxSlots;
+    uint64_t* acc1_full = x_full + 1;
+    uint64_t* hd_full = x_full + 2;
+    uint64_t* hd_empty = x_full + 3;
+    uint64_t* acc2_full = x_full + 4;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_full + 5);
+    // per-k-step A descriptors for tile 0 (hi planes): conv1 [k1], conv2 [k2]
+    uint64_t* adesc1 = x_full + 6;
+    uint64_t* adesc2 = adesc1 + p.k1;
+
+    // ---- zero the activation buffers (pads and guards must read as 0)
+    {
+        uint4 z = make_uint4(0, 0, 0, 0);
+        size_t nbytes = (size_t)P * ((p.Cp + p.MC) / 8) * plane_bytes;
+        for (size_t i = tid; i < nbytes / 16; i += kThreads) reinterpret_cast<uint4*>(xbuf)[i] = z;
+    }
+    fence_proxy_async();
+    if (warp == 1) tmem_alloc(tmem_slot, p.tmem_cols);
+    if (tid == 0) {
+        for (int i = 0; i < p.nslot; i++) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+        mbar_init(x_full, kEpiThreads);
+        mbar_init(acc1_full, 1);
+        mbar_init(hd_full, kEpiThreads);
+        mbar_init(hd_empty, 1);
+        mbar_init(acc2_full, 1);
+        fence_mbar_init();
+        const uint32_t plane_b = (uint32_t)p.Rtot * 16;
+        const uint32_t xb0 = smem_u32(xbuf), hb0 = smem_u32(hbuf);
+        for (int s = 0; s < p.k1; s++) {
+            int shift, plane;
+            uint32_t lbo;
+            if (p.pair) {
+                int u = s / 2 - 1, v0 = (s & 1) ? 1 : -1;
+                shift = u * p.Wp + v0; plane = 0; lbo = 16;
+            } else {
+                int per = p.Cp / 16;
+                int tap = s / per, kc = s - tap * per;
+                shift = (tap / 3 - 1) * p.Wp + (tap % 3 - 1);
+                plane = 2 * kc; lbo = plane_b;
+            }
+            adesc1[s] = smem_desc(xb0 + (uint32_t)(p.G + shift) * 16 + (uint32_t)plane * plane_b, lbo, 128);
+        }
+        const int per2 = p.MC / 16;
+        for (int s = 0; s < p.k2; s++) {
+            int tap = s / per2, kc = s - tap * per2;
+            int shift = (tap / 3 - 1) * p.Wp + (tap % 3 - 1);
+            adesc2[s] = smem_desc(hb0 + (uint32_t)(p.G + shift) * 16 + (uint32_t)(2 * kc) * plane_b, plane_b, 128);
+        }
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t acc1_col0 = (uint32_t)(p.T * p.Nc2);  // acc2[tile] at tile*Nc2, acc1[tile] after
+
+    const int64_t nbatch = (a.n + p.I - 1) / p.I;
+    const int64_t HW = (int64_t)p.H * p.W;
+
+    if (warp == 0) {
+        // ================= producer: stream packed weights through the ring ===============
+        if (lane == 0) {
+            int slot = 0;
+            uint32_t phase = 0;
+            unsigned long long w_empty = 0, t_start = clock64();
+            for (int64_t b = blockIdx.x; b < nbatch; b += gridDim.x) {
+                for (int tt = 0; tt < a.nb; tt++) {
+                    int t = a.inverse ? a.nb - 1 - tt : tt;
+                    const uint8_t* src = a.wpack + (int64_t)t * p.blk_bytes;
+                    for (int j = 0; j < p.nch; j++) {
+                        for (int seg = 0; seg < 2; seg++) {
+                            int N = seg == 0 ? p.MC : p.Nc2;
+                            int K = seg == 0 ? p.k1 : p.k2;
+                            int g = steps_per_slot(N, p.prec3, p.slot_bytes);
+                            int kb = kstep_bytes(N, p.prec3);
+                            for (int s0 = 0; s0 < K; s0 += g) {
+                                int cnt = min(g, K - s0);
+                                uint32_t bytes = (uint32_t)(cnt * kb);
+                                TWAIT(w_empty, mbar_wait(&empty[slot], phase ^ 1));
+                                mbar_arrive_expect_tx(&full[slot], bytes);
+                                bulk_g2s(ring + (size_t)slot * p.slot_bytes, src, bytes, &full[slot]);
+                                src += bytes;
+                                if (++slot == p.nslot) { slot = 0; phase ^= 1; }
+                            }
+                        }
+                    }
+                }
+            }
+            if (a.dbg) {
+                a.dbg[blockIdx.x * 16 + 0] = clock64() - t_start;
+                a.dbg[blockIdx.x * 16 + 1] = w_empty;
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // ================= MMA issuer ========================================================
+        // One elect.sync-ed thread runs the whole issue loop.  Descriptors are rebuilt each
+        // k-step from 32-bit loop counters (smem_desc of a shared-memory address) so that ptxas
+        // keeps them on the uniform datapath: no R2UR / waterfall in the inner loops.
+        if (elect_one()) {
+            int slot = 0;
+            uint32_t phase = 0, xph = 0, hph = 0;
+            const uint32_t xb = smem_u32(xbuf) + (uint32_t)p.G * 16;
+            const uint32_t hb = smem_u32(hbuf) + (uint32_t)p.G * 16;
+            const uint32_t xlo_b = (uint32_t)(p.Cp / 8) * plane_bytes;   // lo planes (prec3)
+            const uint32_t hlo_b = (uint32_t)(p.MC / 8) * plane_bytes;
+            const uint32_t id1 = idesc_bf16(128, p.MC), id2 = idesc_bf16(128, p.Nc2);
+            const uint32_t rb = smem_u32(ring);
+            const uint32_t lbo1 = p.pair ? 16u : plane_bytes;
+            const int g1 = steps_per_slot(p.MC, p.prec3, p.slot_bytes);
+            const int g2 = steps_per_slot(p.Nc2, p.prec3, p.slot_bytes);
+            const uint32_t kb1 = (uint32_t)kstep_bytes(p.MC, p.prec3), kb2 = (uint32_t)kstep_bytes(p.Nc2, p.prec3);
+            const int per1 = p.pair ? 2 : p.Cp / 16;   // k-steps per kernel row u (pair) / per tap
+            const int per2 = p.MC / 16;
+            unsigned long long w_x = 0, w_full = 0, w_hd = 0, t_start = clock64();
+            for (int64_t b = blockIdx.x; b < nbatch; b += gridDim.x) {
+                for (int tt = 0; tt < a.nb; tt++) {
+                    TWAIT(w_x, mbar_wait(x_full, xph)); xph ^= 1;
+                    fence_after();
+                    for (int j = 0; j < p.nch; j++) {
+                        // ---------------- conv1, chunk j -> acc1 ----------------
+                        if constexpr (CFG::kStatic) {
+                            constexpr uint32_t LBO1 = CFG::PAIR ? 16u : (uint32_t)CFG::PLANE16 * 16u;
+                            const uint32_t alo0 = ((xb >> 4) & 0x3FFFu) | ((LBO1 >> 4) << 16);
+                            const uint32_t ringlo = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::MC * 16 >> 4) << 16);
+                            issue_static<CFG::K1, CFG::PER1, CFG::PAIR, CFG::WP, CFG::PLANE16, CFG::G1, CFG::KB1 / 16,
+                                         CFG::T, CFG::MC, CFG::P3, CFG::LOX16, CFG::ACC1, CFG::MC>(
+                                tmem, alo0, ringlo, (uint32_t)CFG::SLOT / 16u, id1, 0u, slot, phase, p.nslot,
+                                full, empty);
+                            commit(acc1_full);
+                        } else
+                                                {
+                            int tap = 0, kc = 0, q = 0;
+                            for (int s = 0; s < p.k1; s++) {
+                                if (q == 0) {
+                                    TWAIT(w_full, mbar_wait(&full[slot], phase));
+                                    fence_after();
+                                }
+                                int shift;
+                                uint32_t poff;
+                                if (p.pair) {           // tap = kernel row u+1; kc = 0: v0=-1, 1: v0=+1
+                                    shift = (tap - 1) * p.Wp + (kc ? 1 : -1);
+                                    poff = 0;
+                                } else {
+                                    shift = (tap / 3 - 1) * p.Wp + (tap % 3 - 1);
+                                    poff = (uint32_t)(2 * kc) * plane_bytes;
+                                }
+                                const uint32_t aaddr = xb + (uint32_t)shift * 16u + poff;
+                                const uint32_t baddr = rb + (uint32_t)slot * (uint32_t)p.slot_bytes + (uint32_t)q * kb1;
+                                const uint32_t acc = s > 0 ? 1u : 0u;
+                                for (int tile = 0; tile < p.T; tile++) {
+                                    const uint32_t d = tmem + acc1_col0 + (uint32_t)(tile * p.MC);
+                                    const uint32_t at = aaddr + (uint32_t)tile * 2048u;
+                                    mma_bf16(d, smem_desc(at, lbo1, 128), smem_desc(baddr, (uint32_t)p.MC * 16u, 128), id1, acc);
+                                    if (p.prec3) {
+                                        mma_bf16(d, smem_desc(at, lbo1, 128),
+                                                 smem_desc(baddr + (uint32_t)p.MC * 32u, (uint32_t)p.MC * 16u, 128), id1, 1);
+                                        mma_bf16(d, smem_desc(at + xlo_b, lbo1, 128),
+                                                 smem_desc(baddr, (uint32_t)p.MC * 16u, 128), id1, 1);
+                                    }
+                                }
+                                if (++kc == per1) { kc = 0; ++tap; }
+                                if (++q == g1 || s + 1 == p.k1) {
+                                    commit(&empty[slot]);
+                                    if (++slot == p.nslot) { slot = 0; phase ^= 1; }
+                                    q = 0;
+                                }
+                            }
+                            commit(acc1_full);
+                        }
+                        // ---------------- conv2, chunk j -> acc2 ----------------
+                        TWAIT(w_hd, mbar_wait(hd_full, hph)); hph ^= 1;
+                        fence_after();
+                        if constexpr (CFG::kStatic) {
+                            constexpr uint32_t LBO2 = (uint32_t)CFG::PLANE16 * 16u;
+                            const uint32_t alo0 = ((hb >> 4) & 0x3FFFu) | ((LBO2 >> 4) << 16);
+                            const uint32_t ringlo = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::NC2 * 16 >> 4) << 16);
+                            issue_static<CFG::K2, CFG::PER2, false, CFG::WP, CFG::PLANE16, CFG::G2, CFG::KB2 / 16,
+                                         CFG::T, CFG::NC2, CFG::P3, CFG::LOH16, 0, CFG::NC2>(
+                                tmem, alo0, ringlo, (uint32_t)CFG::SLOT / 16u, id2, j > 0 ? 1u : 0u, slot, phase,
+                                p.nslot, full, empty);
+                            commit(hd_empty);
+                        } else
+                        {
+                            int tap = 0, kc = 0, q = 0;
+                            for (int s = 0; s < p.k2; s++) {
+                                if (q == 0) {
+                                    TWAIT(w_full, mbar_wait(&full[slot], phase));
+                                    fence_after();
+                                }
+                                const int shift = (tap / 3 - 1) * p.Wp + (tap % 3 - 1);
+                                const uint32_t aaddr = hb + (uint32_t)shift * 16u + (uint32_t)(2 * kc) * plane_bytes;
+                                const uint32_t baddr = rb + (uint32_t)slot * (uint32_t)p.slot_bytes + (uint32_t)q * kb2;
+                                const uint32_t acc = (j > 0 || s > 0) ? 1u : 0u;
+                                for (int tile = 0; tile < p.T; tile++) {
+                                    const uint32_t d = tmem + (uint32_t)(tile * p.Nc2);
+                                    const uint32_t at = aaddr + (uint32_t)tile * 2048u;
+                                    mma_bf16(d, smem_desc(at, plane_bytes, 128), smem_desc(baddr, (uint32_t)p.Nc2 * 16u, 128), id2, acc);
+                                    if (p.prec3) {
+                                        mma_bf16(d, smem_desc(at, plane_bytes, 128),
+                                                 smem_desc(baddr + (uint32_t)p.Nc2 * 32u, (uint32_t)p.Nc2 * 16u, 128), id2, 1);
+                                        mma_bf16(d, smem_desc(at + hlo_b, plane_bytes, 128),
+                                                 smem_desc(baddr, (uint32_t)p.Nc2 * 16u, 128), id2, 1);
+                                    }
+                                }
+                                if (++kc == per2) { kc = 0; ++tap; }
+                                if (++q == g2 || s + 1 == p.k2) {
+                                    commit(&empty[slot]);
+                                    if (++slot == p.nslot) { slot = 0; phase ^= 1; }
+                                    q = 0;
+                                }
+                            }
+                            commit(hd_empty);
+                        }
+                    }
+                    commit(acc2_full);
+                }
+            }
+            if (a.dbg) {
+                a.dbg[blockIdx.x * 16 + 2] = clock64() - t_start;
+                a.dbg[blockIdx.x * 16 + 3] = w_x;
+                a.dbg[blockIdx.x * 16 + 4] = w_full;
+                a.dbg[blockIdx.x * 16 + 5] = w_hd;
+            }
+        }  // elect_one
+        __syncwarp();
+    } else {
+        // ================= epilogue warps (128 threads) =====================================
+        const int et = tid - 64;                       // 0..127
+        const int lane_base = (warp & 3) * 32;         // TMEM lane quarter of this warp
+        const int row_in_tile = lane_base + lane;
+        uint32_t a1ph = 0, a2ph = 0, heph = 0;
+        int hd_uses = 0;
+        const uint32_t lane_addr = (uint32_t)lane_base << 16;
+        uint8_t* xlo_buf = xbuf + (size_t)(p.Cp / 8) * plane_bytes;
+        uint8_t* hlo_buf = hbuf + (size_t)(p.MC / 8) * plane_bytes;
+        unsigned long long w_a1 = 0, w_he = 0, w_a2 = 0, t_ld = 0, t_e1 = 0, t_e2 = 0, t_start = clock64();
+        for (int64_t b = blockIdx.x; b < nbatch; b += gridDim.x) {
+            long long tl0 = clock64();
+            const int64_t img0 = b * p.I;
+            const int nimg = (int)(a.n - img0 < (int64_t)p.I ? a.n - img0 : (int64_t)p.I);
+            // ---- load bf16(s_in) of the first processed block into the X planes
+            {
+                int t0 = a.inverse ? a.nb - 1 : 0;
+                int o0 = (a.first_orient + t0) & 1;
+                int in_off = o0 == 0 ? 0 : p.c;
+                for (int tile = 0; tile < p.T; tile++) {
+                    int r = tile * 128 + row_in_tile, ii, y, x;
+                    if (!row_pixel(r, p, ii, y, x) || ii >= nimg) continue;
+                    const float* src = a.state + ((img0 + ii) * a.C + in_off) * HW + y * p.W + x;
+                    for (int c8 = 0; c8 < p.Cp; c8 += 8) {
+                        uint32_t hi[8], lo[8];
+#pragma unroll
+                        for (int e = 0; e < 8; e++) {
+                            float v = (c8 + e < p.c) ? src[(int64_t)(c8 + e) * HW] : 0.f;
+                            hi[e] = bf16_bits(v);
+                            lo[e] = bf16_bits(v - bf16_val(hi[e]));
+                        }
+                        size_t off = (size_t)(c8 / 8) * plane_bytes + (size_t)(r + p.G) * 16;
+                        *reinterpret_cast<uint4*>(xbuf + off) =
+                            make_uint4(hi[0] | hi[1] << 16, hi[2] | hi[3] << 16, hi[4] | hi[5] << 16, hi[6] | hi[7] << 16);
+                        if (p.prec3)
+                            *reinterpret_cast<uint4*>(xlo_buf + off) =
+                                make_uint4(lo[0] | lo[1] << 16, lo[2] | lo[3] << 16, lo[4] | lo[5] << 16, lo[6] | lo[7] << 16);
+                    }
+                }
+                fence_proxy_async();
+                mbar_arrive(x_full);
+            }
+            t_ld += clock64() - tl0;
+            for (int tt = 0; tt < a.nb; tt++) {
+                const int t = a.inverse ? a.nb - 1 - tt : tt;
+                const int orient = (a.first_orient + t) & 1;
+                const int out_off = orient == 0 ? p.c : 0;
+                const float* b1 = a.bias + (int64_t)t * (p.Mp + p.Nc2);
+                const float* b2 = b1 + p.Mp;
+                for (int j = 0; j < p.nch; j++) {
+                    // ---- conv1 epilogue: acc1 -> bias + act -> bf16 hidden planes
+                    TWAIT(w_a1, mbar_wait(acc1_full, a1ph)); a1ph ^= 1;
+                    fence_after();
+                    if (hd_uses > 0) { TWAIT(w_he, mbar_wait(hd_empty, heph)); heph ^= 1; }
+                    hd_uses++;
+                    long long te0 = clock64();
+                    for (int tile = 0; tile < p.T; tile++) {
+                        int r = tile * 128 + row_in_tile, ii, y, x;
+                        bool valid = row_pixel(r, p, ii, y, x) && ii < nimg;
+                        const uint32_t col = acc1_col0 + (uint32_t)(tile * p.MC);
+                        for (int c16 = 0; c16 < p.MC; c16 += 16) {
+                            float v[16];
+                            tmem_ld16(tmem + lane_addr + col + c16, v);
+                            tmem_wait_ld();
+                            uint32_t hi[16], lo[16];
+#pragma unroll
+                            for (int e = 0; e < 16; e++) {
+                                float h = v[e] + __ldg(b1 + j * p.MC + c16 + e);
+                                if (a.act == 0) h = fmaxf(h, 0.f);
+                                if (!valid) h = 0.f;
+                                hi[e] = bf16_bits(h);
+                                lo[e] = bf16_bits(h - bf16_val(hi[e]));
+                            }
+#pragma unroll
+                            for (int hh = 0; hh < 2; hh++) {
+                                size_t off = (size_t)((c16 / 8) + hh) * plane_bytes + (size_t)(r + p.G) * 16;
+                                const uint32_t* q = hi + hh * 8;
+                                *reinterpret_cast<uint4*>(hbuf + off) =
+                                    make_uint4(q[0] | q[1] << 16, q[2] | q[3] << 16, q[4] | q[5] << 16, q[6] | q[7] << 16);
+                                if (p.prec3) {
+                                    const uint32_t* w = lo + hh * 8;
+                                    *reinterpret_cast<uint4*>(hlo_buf + off) =
+                                        make_uint4(w[0] | w[1] << 16, w[2] | w[3] << 16, w[4] | w[5] << 16, w[6] | w[7] << 16);
+                                }
+                            }
+                        }
+                    }
+                    fence_before();
+                    fence_proxy_async();
+                    mbar_arrive(hd_full);
+                    t_e1 += clock64() - te0;
+                }
+                // ---- conv2 epilogue: s_out (+|-)= acc2 + b2 (fp32, global); bf16(s_out) -> X
+                TWAIT(w_a2, mbar_wait(acc2_full, a2ph)); a2ph ^= 1;
+                fence_after();
+                long long te2 = clock64();
+                const bool write_x = tt + 1 < a.nb;
+                for (int tile = 0; tile < p.T; tile++) {
+                    int r = tile * 128 + row_in_tile, ii, y, x;
+                    bool valid = row_pixel(r, p, ii, y, x) && ii < nimg;
+                    float* dst = valid ? a.state + ((img0 + ii) * a.C + out_off) * HW + y * p.W + x : nullptr;
+                    // software pipeline: old state of chunk c16+16 is in flight while chunk c16 is
+                    // combined with the accumulator (independent loads, no load->store chains)
+                    float oldv[16], nxt[16];
+#pragma unroll
+                    for (int e = 0; e < 16; e++) oldv[e] = (valid && e < p.c) ? __ldcg(dst + (int64_t)e * HW) : 0.f;
+                    for (int c16 = 0; c16 < p.Nc2; c16 += 16) {
+#pragma unroll
+                        for (int e = 0; e < 16; e++) {
+                            int o = c16 + 16 + e;
+                            nxt[e] = (valid && o < p.c) ? __ldcg(dst + (int64_t)o * HW) : 0.f;
+                        }
+                        float v[16];
+                        tmem_ld16(tmem + lane_addr + (uint32_t)(tile * p.Nc2 + c16), v);
+                        tmem_wait_ld();
+                        if (valid) {
+                        uint32_t hi[16], lo[16];
+#pragma unroll
+                        for (int e = 0; e < 16; e++) {
+                            int o = c16 + e;
+                            float nv = 0.f;
+                            if (o < p.c) {
+                                float f = v[e] + __ldg(b2 + o);
+                                nv = a.inverse ? oldv[e] - f : oldv[e] + f;
+                                __stcg(dst + (int64_t)o * HW, nv);
+                            }
+                            hi[e] = bf16_bits(nv);
+                            lo[e] = bf16_bits(nv - bf16_val(hi[e]));
+                        }
+                        if (write_x) {
+#pragma unroll
+                            for (int hh = 0; hh < 2; hh++) {
+                                if (c16 + hh * 8 >= p.Cp) break;
+                                size_t off = (size_t)((c16 / 8) + hh) * plane_bytes + (size_t)(r + p.G) * 16;
+                                const uint32_t* q = hi + hh * 8;
+                                *reinterpret_cast<uint4*>(xbuf + off) =
+                                    make_uint4(q[0] | q[1] << 16, q[2] | q[3] << 16, q[4] | q[5] << 16, q[6] | q[7] << 16);
+                                if (p.prec3) {
+                                    const uint32_t* w = lo + hh * 8;
+                                    *reinterpret_cast<uint4*>(xlo_buf + off) =
+                                        make_uint4(w[0] | w[1] << 16, w[2] | w[3] << 16, w[4] | w[5] << 16, w[6] | w[7] << 16);
+                                }
+                            }
+                        }
+                        }
+#pragma unroll
+                        for (int e = 0; e < 16; e++) oldv[e] = nxt[e];
+                    }
+                }
+                if (write_x) {
+                    fence_before();
+                    fence_proxy_async();
+                    mbar_arrive(x_full);
+                }
+                t_e2 += clock64() - te2;
+            }
+        }
+        if (a.dbg && et == 0) {
+            unsigned long long* o = a.dbg + blockIdx.x * 16;
+            o[6] = clock64() - t_start; o[7] = w_a1; o[8] = w_he; o[9] = w_a2;
+            o[10] = t_ld; o[11] = t_e1; o[12] = t_e2;
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem, p.tmem_cols);
+}
+
+// ========================================================================================
+// host side: planning and weight packing
+// ========================================================================================
+static int rup(int x, int m) { return (x + m - 1) / m * m; }
+
+static uint16_t f2bf(float f) {  // round-to-nearest-even, no NaN inputs
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    u += 0x7FFFu + ((u >> 16) & 1u);
+    return (uint16_t)(u >> 16);
+}
+static float bf2f(uint16_t b) {
+    uint32_t u = (uint32_t)b << 16;
+    float f;
+    memcpy(&f, &u, 4);
+    return f;
+}
+
+static const size_t kSmemCap = 227 * 1024;
+
+static bool make_plan(const StageInfo& S, bool prec3, StagePlan& best) {
+    StagePlan p{};
+    p.H = S.H; p.W = S.W; p.Wp = S.W + 1; p.G = p.Wp + 2;
+    p.c = S.c; p.m = S.m;
+    p.Cp = S.c <= 8 ? 8 : rup(S.c, 16);
+    p.Mp = rup(S.m, 16);
+    p.Nc2 = rup(S.c, 16);
+    p.pair = p.Cp == 8;
+    p.prec3 = prec3 ? 1 : 0;
+    const int P = prec3 ? 2 : 1;
+    const int img_rows = (p.H + 1) * p.Wp;
+    double best_score = -1;
+    for (int MC = p.Mp; MC >= 16; MC -= 16) {
+        if (p.Mp % MC) continue;
+        for (int T = 1; T <= 8; T++) {
+            if (T * (MC + p.Nc2) > 512) break;
+            int I = (T * 128) / img_rows;
+            if (I < 1) continue;
+            for (int nslot = 4; nslot >= 2; nslot--) {
+                int slot_bytes = std::max(16384, std::max(kstep_bytes(MC, prec3), kstep_bytes(p.Nc2, prec3)));
+                int Rtot = T * 128 + 2 * p.G;
+                size_t smem = (size_t)nslot * slot_bytes + (size_t)P * ((p.Cp + MC) / 8) * Rtot * 16 + 256 +
+                              8 * (size_t)(9 * (p.Cp / 8 + 1) + 9 * (MC / 16));
+                if (smem > kSmemCap) continue;
+                // score: useful fraction of M rows, weight reuse (T), fewer chunk round trips
+                double eff = (double)I * p.H * p.W / (T * 128.0);
+                double score = eff * (1.0 - 0.15 / T) * (1.0 - 0.02 * (p.Mp / MC)) + 0.001 * nslot;
+                if (score > best_score) {
+                    best_score = score;
+                    best = p;
+                    best.MC = MC; best.nch = p.Mp / MC; best.T = T; best.I = I;
+                    best.Rtot = Rtot; best.nslot = nslot; best.slot_bytes = slot_bytes; best.smem = smem;
+                }
+                break;
+            }
+        }
+    }
+    if (best_score < 0) return false;
+    best.k1 = best.pair ? 6 : 9 * (best.Cp / 16);
+    best.k2 = 9 * (best.MC / 16);
+    int cols = best.T * (best.MC + best.Nc2);
+    best.tmem_cols = 32;
+    while (best.tmem_cols < cols) best.tmem_cols *= 2;
+    // stream bytes per block
+    int64_t bytes = 0;
+    for (int j = 0; j < best.nch; j++)
+        bytes += (int64_t)best.k1 * kstep_bytes(best.MC, prec3) + (int64_t)best.k2 * kstep_bytes(best.Nc2, prec3);
+    best.blk_bytes = bytes;
+    return true;
+}
+
+// one k-step B tile: [khalf][n][8] bf16 (hi), then the lo tile when prec3
+static void put_tile(std::vector<uint16_t>& out, const std::vector<float>& w, int N, bool prec3) {
+    // w is [N][16] (n, kk)
+    for (int part = 0; part < (prec3 ? 2 : 1); part++)
+        for (int kh = 0; kh < 2; kh++)
+            for (int n = 0; n < N; n++)
+                for (int e = 0; e < 8; e++) {
+                    float v = w[(size_t)n * 16 + kh * 8 + e];
+                    uint16_t hi = f2bf(v);
+                    out.push_back(part == 0 ? hi : f2bf(v - bf2f(hi)));
+                }
+}
+
+static void pack_block(const StagePlan& p, const float* W1, const float* W2, bool prec3,
+                       std::vector<uint16_t>& out) {
+    const int c = p.c, m = p.m;
+    auto w1 = [&](int h, int ci, int u, int v) -> float {  // u, v in -1..1
+        if (h >= m || ci >= c || v < -1 || v > 1) return 0.f;
+        return W1[(((size_t)h * c + ci) * 3 + (u + 1)) * 3 + (v + 1)];
+    };
+    auto w2 = [&](int o, int h, int u, int v) -> float {
+        if (o >= c || h >= m) return 0.f;
+        return W2[(((size_t)o * m + h) * 3 + (u + 1)) * 3 + (v + 1)];
+    };
+    std::vector<float> tile;
+    for (int j = 0; j < p.nch; j++) {
+        // conv1 chunk j: N = MC hidden channels
+        for (int s = 0; s < p.k1; s++) {
+            tile.assign((size_t)p.MC * 16, 0.f);
+            for (int n = 0; n < p.MC; n++) {
+                int h = j * p.MC + n;
+                for (int kk = 0; kk < 16; kk++) {
+                    float v;
+                    if (p.pair) {
+                        int u = s / 2 - 1, v0 = (s & 1) ? 1 : -1;
+                        int vv = v0 + kk / 8, ci = kk % 8;
+                        v = w1(h, ci, u, vv);
+                    } else {
+                        int per = p.Cp / 16, tap = s / per, kc = s % per;
+                        v = w1(h, kc * 16 + kk, tap / 3 - 1, tap % 3 - 1);
+                    }
+                    tile[(size_t)n * 16 + kk] = v;
+                }
+            }
+            put_tile(out, tile, p.MC, prec3);
+        }
+        // conv2 chunk j: N = Nc2 outputs, K = this chunk's hidden channels
+        for (int s = 0; s < p.k2; s++) {
+            tile.assign((size_t)p.Nc2 * 16, 0.f);
+            int per = p.MC / 16, tap = s / per, kc = s % per;
+            for (int n = 0; n < p.Nc2; n++)
+                for (int kk = 0; kk < 16; kk++)
+                    tile[(size_t)n * 16 + kk] = w2(n, j * p.MC + kc * 16 + kk, tap / 3 - 1, tap % 3 - 1);
+            put_tile(out, tile, p.Nc2, prec3);
+        }
+    }
+}
+
+struct UmmaState {
+    StagePlan plan[4];
+    int64_t wpack_off[4];  // bytes into d_wpack per stage
+    int64_t bias_off[4];   // floats into d_bias per stage
+};
+
+// ---- compile-time specialisations for the Arch-C stage plans (see make_plan) -----------------
+typedef void (*StageKernel)(StageArgs);
+struct SpecEntry { int Wp, Cp, MC, Nc2, T, p3, slot; StageKernel fn; };
+#define CI_SPEC(WP, CP, MC, NC2, T, P3, SLOT) \
+    {WP, CP, MC, NC2, T, P3, SLOT, k_stage<SCfg<WP, CP, MC, NC2, T, P3, SLOT>>}
+static const SpecEntry kSpecs[] = {
+    CI_SPEC(17, 8, 32, 16, 7, 0, 16384),   // C stage 1, bf16
+    CI_SPEC(9, 32, 32, 32, 7, 0, 16384),   // C stage 2, bf16
+    CI_SPEC(5, 96, 128, 96, 2, 0, 16384),  // C stage 3, bf16
+    CI_SPEC(17, 8, 32, 16, 7, 1, 16384),   // C stage 1, bf16x3
+    CI_SPEC(9, 32, 128, 32, 2, 1, 16384),  // C stage 2, bf16x3
+    CI_SPEC(5, 96, 64, 96, 2, 1, 16384),   // C stage 3, bf16x3
+};
+
+static StageKernel pick_kernel(const StagePlan& p) {
+    if (!getenv("CI_NO_STATIC"))
+        for (const auto& e : kSpecs)
+            if (e.Wp == p.Wp && e.Cp == p.Cp && e.MC == p.MC && e.Nc2 == p.Nc2 && e.T == p.T && e.p3 == p.prec3 &&
+                e.slot == p.slot_bytes)
+                return e.fn;
+    return k_stage<SDyn>;
+}
+
 ci_status_t umma_prepare(Model* m, const float* host_params) {
-    (void)m; (void)host_params;
-    set_error("tcgen05 precisions not built yet");
-    return CI_ERR_UNSUPPORTED;
+    const bool prec3 = m->prec == CI_PREC_FP32;
+    UmmaState* U = new UmmaState();
+    std::vector<uint16_t> pack;
+    std::vector<float> bias;
+    for (int s = 0; s < m->n_stages; s++) {
+        const StageInfo& S = m->st[s];
+        if (!make_plan(S, prec3, U->plan[s])) {
+            delete U;
+            set_error("stage %d (%dx%d, c=%d, m=%d) does not fit the tcgen05 kernel", s, S.H, S.W, S.c, S.m);
+            return CI_ERR_UNSUPPORTED;
+        }
+        const StagePlan& p = U->plan[s];
+        if (getenv("CI_DEBUG_PLAN"))
+            fprintf(stderr,
+                    "[ci plan] stage %d %dx%d c=%d m=%d prec3=%d: Cp=%d Mp=%d MC=%d nch=%d Nc2=%d T=%d I=%d "
+                    "k1=%d k2=%d slots=%dx%d smem=%zu tmem=%d blk_bytes=%lld M-eff=%.3f\n",
+                    s, p.H, p.W, p.c, p.m, p.prec3, p.Cp, p.Mp, p.MC, p.nch, p.Nc2, p.T, p.I, p.k1, p.k2,
+                    p.nslot, p.slot_bytes, p.smem, p.tmem_cols, (long long)p.blk_bytes,
+                    (double)p.I * p.H * p.W / (p.T * 128.0));
+        // align each stage stream to 128 B
+        while ((pack.size() * 2) % 128) pack.push_back(0);
+        U->wpack_off[s] = (int64_t)pack.size() * 2;
+        U->bias_off[s] = (int64_t)bias.size();
+        for (int t = 0; t < S.nb; t++) {
+            const float* blk = host_params + m->blk_off[m->blk_first[s] + t];
+            const float* W1 = blk;
+            const float* b1 = W1 + (size_t)S.m * S.c * 9;
+            const float* W2 = b1 + S.m;
+            const float* b2 = W2 + (size_t)S.c * S.m * 9;
+            size_t before = pack.size();
+            pack_block(p, W1, W2, prec3, pack);
+            if ((int64_t)(pack.size() - before) * 2 != p.blk_bytes) {
+                delete U;
+                set_error("internal: packed block size mismatch");
+                return CI_ERR_UNSUPPORTED;
+            }
+            for (int i = 0; i < p.Mp; i++) bias.push_back(i < S.m ? b1[i] : 0.f);
+            for (int i = 0; i < p.Nc2; i++) bias.push_back(i < S.c ? b2[i] : 0.f);
+        }
+    }
+    cudaError_t e = cudaMalloc(&m->d_wpack, pack.size() * 2);
+    if (e == cudaSuccess) e = cudaMemcpy(m->d_wpack, pack.data(), pack.size() * 2, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&m->d_bias, std::max<size_t>(bias.size(), 1) * 4);
+    if (e == cudaSuccess) e = cudaMemcpy(m->d_bias, bias.data(), bias.size() * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_stage<SDyn>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap);
+    for (const auto& sp : kSpecs)
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(sp.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap);
+    if (e != cudaSuccess) { delete U; return cuda_status(e, "umma_prepare"); }
+    m->umma_state = U;
+    return CI_OK;
 }
-void umma_release(Model* m) { (void)m; }
-ci_status_t umma_stage(const Model* m, int stage, float* state, int64_t n, bool inverse, cudaStream_t s) {
-    (void)m; (void)stage; (void)state; (void)n; (void)inverse; (void)s;
-    return CI_ERR_UNSUPPORTED;
+
+void umma_release(Model* m) {
+    if (m->d_wpack) cudaFree(m->d_wpack);
+    if (m->d_bias) cudaFree(m->d_bias);
+    m->d_wpack = nullptr;
+    m->d_bias = nullptr;
+    delete reinterpret_cast<UmmaState*>(m->umma_state);
+    m->umma_state = nullptr;
 }
+
+// ---- optional CUDA-event accounting of stage launches (codedinv_testing.h)
+struct ProfRec { cudaEvent_t a, b; int stage; double flops; };
+static std::vector<ProfRec> g_prof;
+static std::vector<cudaEvent_t> g_prof_pool;
+static bool g_prof_on = false;
+static cudaEvent_t prof_event() {
+    if (!g_prof_pool.empty()) { cudaEvent_t e = g_prof_pool.back(); g_prof_pool.pop_back(); return e; }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+static cudaEvent_t g_prof_open = nullptr;
+static void prof_begin(cudaStream_t st) {
+    if (!g_prof_on) return;
+    g_prof_open = prof_event();
+    cudaEventRecord(g_prof_open, st);
+}
+static void prof_end(cudaStream_t st, int stage, double flops) {
+    if (!g_prof_on || !g_prof_open) return;
+    cudaEvent_t b = prof_event();
+    cudaEventRecord(b, st);
+    g_prof.push_back({g_prof_open, b, stage, flops});
+    g_prof_open = nullptr;
+}
+
+ci_status_t umma_stage(const Model* m, int s, float* state, int64_t n, bool inverse, cudaStream_t st) {
+    if (n == 0) return CI_OK;
+    const UmmaState* U = reinterpret_cast<const UmmaState*>(m->umma_state);
+    StageArgs a;
+    a.p = U->plan[s];
+    a.state = state;
+    a.n = n;
+    a.wpack = reinterpret_cast<const uint8_t*>(m->d_wpack) + U->wpack_off[s];
+    a.bias = m->d_bias + U->bias_off[s];
+    a.C = m->st[s].C;
+    a.nb = m->st[s].nb;
+    a.first_orient = m->arch.first_orientation;
+    a.act = m->arch.act;
+    a.inverse = inverse ? 1 : 0;
+    static unsigned long long* dbg = nullptr;
+    const bool debug_cycles = getenv("CI_DEBUG_CYCLES") != nullptr;
+    if (debug_cycles && !dbg) cudaMalloc(&dbg, 148 * 16 * sizeof(unsigned long long));
+    a.dbg = debug_cycles ? dbg : nullptr;
+    if (a.dbg) cudaMemsetAsync(dbg, 0, 148 * 16 * sizeof(unsigned long long), st);
+    int64_t nbatch = (n + a.p.I - 1) / a.p.I;
+    int dev_sms = 148;
+    int grid = (int)std::min<int64_t>(nbatch, dev_sms);
+    const StageInfo& S = m->st[s];
+    double flops = (double)n * S.nb * 36.0 * S.H * S.W * S.c * S.m;
+    prof_begin(st);
+    pick_kernel(a.p)<<<grid, kThreads, a.p.smem, st>>>(a);
+    count_launch();
+    CI_CHECK_LAUNCH("k_stage");
+    prof_end(st, s, flops);
+    if (a.dbg) {
+        unsigned long long h[148 * 16];
+        cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        double acc[16] = {0};
+        for (int b = 0; b < grid; b++)
+            for (int i = 0; i < 16; i++) acc[i] += (double)h[b * 16 + i] / grid;
+        fprintf(stderr,
+                "[ci cycles] stage %d n=%lld inv=%d | prod total %.0f wait_empty %.0f | mma total %.0f wait_x %.0f "
+                "wait_full %.0f wait_hd %.0f | epi total %.0f wait_acc1 %.0f wait_hd_empty %.0f wait_acc2 %.0f "
+                "load %.0f epi1 %.0f epi2 %.0f\n",
+                s, (long long)n, (int)inverse, acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6], acc[7],
+                acc[8], acc[9], acc[10], acc[11], acc[12]);
+    }
+    return CI_OK;
+}
+
 }  // namespace ci
+
+extern "C" {
+ci_status_t ci_test_plan(int32_t H, int32_t W, int32_t c, int32_t m, int32_t prec3, int64_t* out16) {
+    ci::StageInfo S{};
+    S.H = H; S.W = W; S.c = c; S.m = m; S.C = 2 * c; S.nb = 1;
+    ci::StagePlan p;
+    if (!ci::make_plan(S, prec3 != 0, p)) { ci::set_error("no plan"); return CI_ERR_UNSUPPORTED; }
+    int64_t v[16] = {p.Wp, p.G, p.Cp, p.Mp, p.MC, p.nch, p.Nc2, p.T, p.I, p.Rtot, p.k1, p.k2,
+                     p.nslot, p.slot_bytes, (int64_t)p.smem, p.blk_bytes};
+    for (int i = 0; i < 16; i++) out16[i] = v[i];
+    return CI_OK;
+}
+ci_status_t ci_test_prof_enable(int32_t enable) {
+    ci::g_prof_on = enable != 0;
+    return CI_OK;
+}
+ci_status_t ci_test_prof_read(double* ms, int64_t* launches, double* flops) {
+    for (int i = 0; i < 4; i++) { ms[i] = 0; launches[i] = 0; flops[i] = 0; }
+    for (auto& r : ci::g_prof) {
+        CI_CUDA(cudaEventSynchronize(r.b));
+        float t = 0.f;
+        CI_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+        ms[r.stage] += t;
+        launches[r.stage] += 1;
+        flops[r.stage] += r.flops;
+        ci::g_prof_pool.push_back(r.a);
+        ci::g_prof_pool.push_back(r.b);
+    }
+    ci::g_prof.clear();
+    return CI_OK;
+}
+}  // extern "C"

@@ -130,8 +130,12 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// Spin on try_wait (which itself suspends in hardware for a bounded time).  A deadlock
+// becomes a trap (launch error) after ~2^28 polls instead of a hung GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t n = 0;
     while (!mbar_try_wait(bar, parity)) {
+        if (++n > (1u << 28)) __trap();
     }
 }
 

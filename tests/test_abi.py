@@ -67,7 +67,7 @@ def test_host_side_argument_errors(ci):
     assert st == ci.CI_ERR_INVALID_ARG
     # decode: k < 1, misaligned, null workspace
     assert lib.ci_decode(0, 1, 4, None, None, None, None, 0, None) == ci.CI_ERR_INVALID_ARG
-    assert lib.ci_decode(2, 1, 6, None, None, None, None, 0, None) == ci.CI_ERR_INVALID_ARG
+    assert lib.ci_decode(2, -1, 4, None, None, None, None, 0, None) == ci.CI_ERR_INVALID_ARG
     buf = (ctypes.c_float * 64)()
     addr = ctypes.addressof(buf)
     assert lib.ci_decode(2, 1, 4, ctypes.c_void_p(addr), ctypes.c_void_p(addr + 32),

@@ -239,7 +239,9 @@ def test_round_trip_and_determinism(ci, prec):
     assert torch.equal(h1, h2)
     err = relerr(xr.cpu().numpy(), x.reshape(37, -1))
     print(f"[round-trip {prec}] {err:.3g}")
-    assert err < 1e-5
+    # fp32 state: the coupling round trip is exact up to fp32 rounding of the adds, which
+    # then perturbs later F inputs slightly; bf16 operands turn those into bf16 flips.
+    assert err < (1e-5 if prec != "bf16" else 3e-3)
 
 
 @pytest.mark.parametrize("prec", PRECS)
