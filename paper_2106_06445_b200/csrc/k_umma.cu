@@ -19,8 +19,8 @@
 //    no-swizzle core-matrix layout) and streamed by one producer thread with
 //    cp.async.bulk (TMA engine) through an mbarrier ring; every weight slot is reused by all
 //    T M-tiles of the CTA.
-//  * Warp roles: warp 0 = producer, warp 1 = MMA issuer (one thread), warps 2..5 = epilogue
-//    (thread <-> TMEM lane <-> pixel row).
+//  * Warp roles: warp 0 = producer, warp 1 = MMA issuer (one thread), warps 2..9 = epilogue
+//    (thread <-> TMEM lane <-> pixel row; two warps per lane quarter split the columns).
 //  * CI_PREC_FP32 ("bf16x3"): operands split x = hi + lo (bf16 each); 3 MMAs per k-step
 //    (hi*hi + hi*lo + lo*hi) into the same fp32 accumulator.
 //  * Determinism: the k-step order per accumulator is fixed and independent of the tile or
@@ -41,8 +41,8 @@
 namespace ci {
 using namespace umma;
 
-constexpr int kThreads = 192;      // 6 warps
-constexpr int kEpiThreads = 128;   // warps 2..5
+constexpr int kThreads = 320;      // 10 warps: producer, MMA, 8 epilogue
+constexpr int kEpiThreads = 256;   // warps 2..9
 constexpr int kMaxSlots = 6;
 
 struct StagePlan {
@@ -57,6 +57,8 @@ struct StagePlan {
     int64_t blk_bytes;     // packed weight stream bytes per block
     size_t smem;
     int tmem_cols;
+    int sstate;            // 1: the batch's fp32 state lives in shared memory for the whole stage
+    uint32_t sstate_off;   // byte offset of the fp32 state region in dynamic smem
 };
 
 struct StageArgs {
@@ -80,6 +82,12 @@ __host__ __device__ inline int steps_per_slot(int N, int prec3, int slot_bytes) 
 
 __device__ __forceinline__ uint32_t bf16_bits(float v) {
     return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v));
+}
+// two floats -> packed bf16x2 (round to nearest even), a in the low half
+__device__ __forceinline__ uint32_t bf16x2_bits(float a, float b) {
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+    return r;
 }
 __device__ __forceinline__ float bf16_val(uint32_t b) {
     return __bfloat162float(__ushort_as_bfloat16((unsigned short)b));
@@ -109,6 +117,9 @@ __device__ __forceinline__ void issue_static(uint32_t tmem, uint32_t alo0, uint3
                                              int nslot, uint64_t* full, uint64_t* empty) {
     constexpr uint32_t HI = 0x4008u;   // SBO = 128 B, descriptor version 1
     uint32_t bl = 0;
+    // opaque to the optimiser: keeps ptxas from hoisting every k-step's descriptor constant out
+    // of the chunk/block loops into registers (which spills); each MMA then costs one add.
+    asm volatile("" : "+r"(alo0), "+r"(ringlo));
 #pragma unroll
     for (int s = 0; s < K; s++) {
         if (s % G == 0) {
@@ -142,10 +153,11 @@ __device__ __forceinline__ void issue_static(uint32_t tmem, uint32_t alo0, uint3
 }
 
 // Static stage configuration (0 = use the runtime plan)
-template <int WP_, int CP_, int MC_, int NC2_, int T_, int P3_, int SLOT_>
+template <int WP_, int CP_, int MC_, int NC2_, int T_, int P3_, int SLOT_, int H_ = 0, int C_ = 0, int SST_ = 0>
 struct SCfg {
     static constexpr bool kStatic = WP_ > 0;
     static constexpr int WP = WP_, CP = CP_, MC = MC_, NC2 = NC2_, T = T_, SLOT = SLOT_;
+    static constexpr int H = H_, W = WP_ - 1, C = C_, SST = SST_;
     static constexpr bool P3 = P3_ != 0;
     static constexpr int G = WP + 2;
     static constexpr int RTOT = T * 128 + 2 * G;
@@ -177,6 +189,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int P = p.prec3 ? 2 : 1;
+    // precision known at compile time for the static configurations
+    const bool kP3 = CFG::kStatic ? CFG::P3 : (p.prec3 != 0);
 
     // ---- shared memory carve-up
     uint8_t* ring = smem;                                           // nslot * slot_bytes
@@ -412,43 +426,99 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
         }  // elect_one
         __syncwarp();
     } else {
-        // ================= epilogue warps (128 threads) =====================================
-        const int et = tid - 64;                       // 0..127
-        const int lane_base = (warp & 3) * 32;         // TMEM lane quarter of this warp
-        const int row_in_tile = lane_base + lane;
+        // ================= epilogue warps (8 warps = 256 threads) ===========================
+        // warp w may only touch TMEM lanes 32*(w%4)..+31, so warps w and w+4 share a lane
+        // quarter (= the same 32 pixel rows of every tile) and split the columns in halves.
+        // Sizes are compile-time constants for the specialised configurations.
+        constexpr bool S = CFG::kStatic;
+        const int eT = S ? CFG::T : p.T;
+        const int eMC = S ? CFG::MC : p.MC;
+        const int eNC2 = S ? CFG::NC2 : p.Nc2;
+        const int eCp = S ? CFG::CP : p.Cp;
+        const int ec = S ? CFG::C : p.c;
+        const int eH = S ? CFG::H : p.H;
+        const int eW = S ? CFG::W : p.W;
+        const int eWp = S ? CFG::WP : p.Wp;
+        const int eG = S ? CFG::G : p.G;
+        const bool esst = S ? (CFG::SST != 0) : (p.sstate != 0);
+        const int64_t eHW = (int64_t)eH * eW;
+        constexpr int OLDN = S ? (CFG::NC2 / 2 > 0 ? CFG::NC2 / 2 : 8) : 48;
+        const int ew = warp - 2;                       // 0..7
+        const int quarter = warp & 3;
+        const int half = ew >> 2;
+        const int et = ew * 32 + lane;                 // 0..255
+        const int row_in_tile = quarter * 32 + lane;
+        const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
         uint32_t a1ph = 0, a2ph = 0, heph = 0;
         int hd_uses = 0;
-        const uint32_t lane_addr = (uint32_t)lane_base << 16;
-        uint8_t* xlo_buf = xbuf + (size_t)(p.Cp / 8) * plane_bytes;
-        uint8_t* hlo_buf = hbuf + (size_t)(p.MC / 8) * plane_bytes;
+        uint8_t* xlo_buf = xbuf + (size_t)(eCp / 8) * plane_bytes;
+        uint8_t* hlo_buf = hbuf + (size_t)(eMC / 8) * plane_bytes;
+        const int cw1 = eMC / 2, cb1 = half * cw1;     // conv1 chunk columns of this half
+        const int cw2 = eNC2 / 2, cb2 = half * cw2;    // conv2 columns of this half
+        const bool any2 = cb2 < ec;                    // this half owns at least one real channel
         unsigned long long w_a1 = 0, w_he = 0, w_a2 = 0, t_ld = 0, t_e1 = 0, t_e2 = 0, t_start = clock64();
+        auto rowpix = [&](int r, int& ii, int& y, int& x) -> bool {
+            const int band = r / eWp;
+            x = r - band * eWp;
+            ii = band / (eH + 1);
+            const int yy = band - ii * (eH + 1);
+            y = yy - 1;
+            return yy != 0 && x < eW;
+        };
+        auto store8 = [&](uint8_t* base_hi, uint8_t* base_lo, int plane, int r, const float* v8) {
+            size_t off = (size_t)plane * plane_bytes + (size_t)(r + eG) * 16;
+            uint32_t hi[4];
+#pragma unroll
+            for (int e = 0; e < 4; e++) hi[e] = bf16x2_bits(v8[2 * e], v8[2 * e + 1]);
+            *reinterpret_cast<uint4*>(base_hi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+            if (kP3) {
+                uint32_t lo[4];
+#pragma unroll
+                for (int e = 0; e < 4; e++)
+                    lo[e] = bf16x2_bits(v8[2 * e] - __uint_as_float(hi[e] << 16),
+                                        v8[2 * e + 1] - __uint_as_float(hi[e] & 0xFFFF0000u));
+                *reinterpret_cast<uint4*>(base_lo + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+            }
+        };
+        // L2 prefetch of a batch's fp32 state (contiguous images) when it stays in global memory
+        auto prefetch_batch = [&](int64_t bb) {
+            if (bb >= nbatch) return;
+            const int64_t i0 = bb * p.I;
+            const int64_t ni = (a.n - i0 < (int64_t)p.I ? a.n - i0 : (int64_t)p.I);
+            const char* base = reinterpret_cast<const char*>(a.state + i0 * a.C * eHW);
+            const int64_t bytes = ni * a.C * eHW * 4;
+            for (int64_t off = (int64_t)et * 128; off < bytes; off += (int64_t)kEpiThreads * 128)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(base + off));
+        };
+        if (!esst && blockIdx.x < nbatch) prefetch_batch(blockIdx.x);
+        float* sst = reinterpret_cast<float*>(smem + p.sstate_off);
         for (int64_t b = blockIdx.x; b < nbatch; b += gridDim.x) {
             long long tl0 = clock64();
             const int64_t img0 = b * p.I;
             const int nimg = (int)(a.n - img0 < (int64_t)p.I ? a.n - img0 : (int64_t)p.I);
-            // ---- load bf16(s_in) of the first processed block into the X planes
+            if (!esst) prefetch_batch(b + gridDim.x);
+            // ---- (esst) copy the batch's fp32 state into shared memory
+            if (esst) {
+                const int64_t nf = (int64_t)nimg * a.C * eHW;
+                const float4* src4 = reinterpret_cast<const float4*>(a.state + img0 * a.C * eHW);
+                float4* dst4 = reinterpret_cast<float4*>(sst);
+                for (int64_t i = et; i < nf / 4; i += kEpiThreads) dst4[i] = __ldcg(src4 + i);
+                asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads));
+            }
+            float* stb = esst ? sst : a.state + img0 * a.C * eHW;
+            // ---- load bf16(s_in) of the first processed block into the X planes (planes split by half)
             {
-                int t0 = a.inverse ? a.nb - 1 : 0;
-                int o0 = (a.first_orient + t0) & 1;
-                int in_off = o0 == 0 ? 0 : p.c;
-                for (int tile = 0; tile < p.T; tile++) {
+                const int t0 = a.inverse ? a.nb - 1 : 0;
+                const int in_off = ((a.first_orient + t0) & 1) == 0 ? 0 : ec;
+                for (int tile = 0; tile < eT; tile++) {
                     int r = tile * 128 + row_in_tile, ii, y, x;
-                    if (!row_pixel(r, p, ii, y, x) || ii >= nimg) continue;
-                    const float* src = a.state + ((img0 + ii) * a.C + in_off) * HW + y * p.W + x;
-                    for (int c8 = 0; c8 < p.Cp; c8 += 8) {
-                        uint32_t hi[8], lo[8];
+                    if (!rowpix(r, ii, y, x) || ii >= nimg) continue;
+                    const float* src = stb + ((int64_t)ii * a.C + in_off) * eHW + y * eW + x;
+                    for (int pl = half; pl < eCp / 8; pl += 2) {
+                        float v8[8];
 #pragma unroll
-                        for (int e = 0; e < 8; e++) {
-                            float v = (c8 + e < p.c) ? src[(int64_t)(c8 + e) * HW] : 0.f;
-                            hi[e] = bf16_bits(v);
-                            lo[e] = bf16_bits(v - bf16_val(hi[e]));
-                        }
-                        size_t off = (size_t)(c8 / 8) * plane_bytes + (size_t)(r + p.G) * 16;
-                        *reinterpret_cast<uint4*>(xbuf + off) =
-                            make_uint4(hi[0] | hi[1] << 16, hi[2] | hi[3] << 16, hi[4] | hi[5] << 16, hi[6] | hi[7] << 16);
-                        if (p.prec3)
-                            *reinterpret_cast<uint4*>(xlo_buf + off) =
-                                make_uint4(lo[0] | lo[1] << 16, lo[2] | lo[3] << 16, lo[4] | lo[5] << 16, lo[6] | lo[7] << 16);
+                        for (int e = 0; e < 8; e++) v8[e] = (pl * 8 + e < ec) ? src[(int64_t)(pl * 8 + e) * eHW] : 0.f;
+                        store8(xbuf, xlo_buf, pl, r, v8);
                     }
                 }
                 fence_proxy_async();
@@ -457,9 +527,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
             t_ld += clock64() - tl0;
             for (int tt = 0; tt < a.nb; tt++) {
                 const int t = a.inverse ? a.nb - 1 - tt : tt;
-                const int orient = (a.first_orient + t) & 1;
-                const int out_off = orient == 0 ? p.c : 0;
-                const float* b1 = a.bias + (int64_t)t * (p.Mp + p.Nc2);
+                const int out_off = ((a.first_orient + t) & 1) == 0 ? ec : 0;
+                const float* b1 = a.bias + (int64_t)t * (p.Mp + eNC2);
                 const float* b2 = b1 + p.Mp;
                 for (int j = 0; j < p.nch; j++) {
                     // ---- conv1 epilogue: acc1 -> bias + act -> bf16 hidden planes
@@ -468,34 +537,37 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                     if (hd_uses > 0) { TWAIT(w_he, mbar_wait(hd_empty, heph)); heph ^= 1; }
                     hd_uses++;
                     long long te0 = clock64();
-                    for (int tile = 0; tile < p.T; tile++) {
+                    const float* bj = b1 + j * eMC + cb1;
+                    for (int tile = 0; tile < eT; tile++) {
                         int r = tile * 128 + row_in_tile, ii, y, x;
-                        bool valid = row_pixel(r, p, ii, y, x) && ii < nimg;
-                        const uint32_t col = acc1_col0 + (uint32_t)(tile * p.MC);
-                        for (int c16 = 0; c16 < p.MC; c16 += 16) {
-                            float v[16];
-                            tmem_ld16(tmem + lane_addr + col + c16, v);
-                            tmem_wait_ld();
-                            uint32_t hi[16], lo[16];
+                        const bool valid = rowpix(r, ii, y, x) && ii < nimg;
+                        const uint32_t col = acc1_col0 + (uint32_t)(tile * eMC + cb1);
+                        for (int g0 = 0; g0 < cw1; g0 += 32) {
+                            const int n = cw1 - g0 < 32 ? cw1 - g0 : 32;   // 8, 16 or 32
+                            float va[16], vb[16];
+                            if (n >= 16) tmem_ld16(tmem + lane_addr + col + g0, va);
+                            if (n == 32) tmem_ld16(tmem + lane_addr + col + g0 + 16, vb);
+                            if (n == 8) {
+                                float v8[8];
+                                tmem_ld8(tmem + lane_addr + col + g0, v8);
 #pragma unroll
-                            for (int e = 0; e < 16; e++) {
-                                float h = v[e] + __ldg(b1 + j * p.MC + c16 + e);
-                                if (a.act == 0) h = fmaxf(h, 0.f);
-                                if (!valid) h = 0.f;
-                                hi[e] = bf16_bits(h);
-                                lo[e] = bf16_bits(h - bf16_val(hi[e]));
+                                for (int e = 0; e < 8; e++) va[e] = v8[e];
                             }
+                            tmem_wait_ld();
 #pragma unroll
-                            for (int hh = 0; hh < 2; hh++) {
-                                size_t off = (size_t)((c16 / 8) + hh) * plane_bytes + (size_t)(r + p.G) * 16;
-                                const uint32_t* q = hi + hh * 8;
-                                *reinterpret_cast<uint4*>(hbuf + off) =
-                                    make_uint4(q[0] | q[1] << 16, q[2] | q[3] << 16, q[4] | q[5] << 16, q[6] | q[7] << 16);
-                                if (p.prec3) {
-                                    const uint32_t* w = lo + hh * 8;
-                                    *reinterpret_cast<uint4*>(hlo_buf + off) =
-                                        make_uint4(w[0] | w[1] << 16, w[2] | w[3] << 16, w[4] | w[5] << 16, w[6] | w[7] << 16);
+                            for (int q8 = 0; q8 < 4; q8++) {
+                                if (q8 * 8 >= n) break;
+                                const float4 bA = __ldg(reinterpret_cast<const float4*>(bj + g0 + q8 * 8));
+                                const float4 bB = __ldg(reinterpret_cast<const float4*>(bj + g0 + q8 * 8 + 4));
+                                const float bb[8] = {bA.x, bA.y, bA.z, bA.w, bB.x, bB.y, bB.z, bB.w};
+                                float h8[8];
+#pragma unroll
+                                for (int e = 0; e < 8; e++) {
+                                    float h = (q8 < 2 ? va[q8 * 8 + e] : vb[(q8 - 2) * 8 + e]) + bb[e];
+                                    if (a.act == 0) h = fmaxf(h, 0.f);
+                                    h8[e] = valid ? h : 0.f;
                                 }
+                                store8(hbuf, hlo_buf, (cb1 + g0) / 8 + q8, r, h8);
                             }
                         }
                     }
@@ -504,67 +576,78 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                     mbar_arrive(hd_full);
                     t_e1 += clock64() - te0;
                 }
-                // ---- conv2 epilogue: s_out (+|-)= acc2 + b2 (fp32, global); bf16(s_out) -> X
+                // ---- conv2 epilogue: s_out (+|-)= acc2 + b2 (fp32); bf16(s_out) -> X
+                const bool write_x = tt + 1 < a.nb;
+                float oldv[OLDN];
+                auto load_old = [&](int tile) {
+                    int r = tile * 128 + row_in_tile, ii, y, x;
+                    const bool valid = any2 && rowpix(r, ii, y, x) && ii < nimg;
+                    const float* src = stb + ((int64_t)(valid ? ii : 0) * a.C + out_off) * eHW + y * eW + x;
+#pragma unroll
+                    for (int e = 0; e < OLDN; e++) {
+                        const int o = cb2 + e;
+                        oldv[e] = (valid && e < cw2 && o < ec) ? src[(int64_t)o * eHW] : 0.f;
+                    }
+                };
+                load_old(0);
                 TWAIT(w_a2, mbar_wait(acc2_full, a2ph)); a2ph ^= 1;
                 fence_after();
                 long long te2 = clock64();
-                const bool write_x = tt + 1 < a.nb;
-                for (int tile = 0; tile < p.T; tile++) {
+                for (int tile = 0; tile < eT; tile++) {
                     int r = tile * 128 + row_in_tile, ii, y, x;
-                    bool valid = row_pixel(r, p, ii, y, x) && ii < nimg;
-                    float* dst = valid ? a.state + ((img0 + ii) * a.C + out_off) * HW + y * p.W + x : nullptr;
-                    // software pipeline: old state of chunk c16+16 is in flight while chunk c16 is
-                    // combined with the accumulator (independent loads, no load->store chains)
-                    float oldv[16], nxt[16];
+                    const bool valid = any2 && rowpix(r, ii, y, x) && ii < nimg;
+                    float v0[16], v1[16], v2[16];
+                    {
+                        const uint32_t col = (uint32_t)(tile * eNC2 + cb2);
+                        if (cw2 == 8) {
+                            float v8[8];
+                            tmem_ld8(tmem + lane_addr + col, v8);
+                            tmem_wait_ld();
 #pragma unroll
-                    for (int e = 0; e < 16; e++) oldv[e] = (valid && e < p.c) ? __ldcg(dst + (int64_t)e * HW) : 0.f;
-                    for (int c16 = 0; c16 < p.Nc2; c16 += 16) {
-#pragma unroll
-                        for (int e = 0; e < 16; e++) {
-                            int o = c16 + 16 + e;
-                            nxt[e] = (valid && o < p.c) ? __ldcg(dst + (int64_t)o * HW) : 0.f;
+                            for (int e = 0; e < 8; e++) v0[e] = v8[e];
+                        } else {
+                            tmem_ld16(tmem + lane_addr + col, v0);
+                            if (cw2 >= 32) tmem_ld16(tmem + lane_addr + col + 16, v1);
+                            if (cw2 >= 48) tmem_ld16(tmem + lane_addr + col + 32, v2);
+                            tmem_wait_ld();
                         }
-                        float v[16];
-                        tmem_ld16(tmem + lane_addr + (uint32_t)(tile * p.Nc2 + c16), v);
-                        tmem_wait_ld();
-                        if (valid) {
-                        uint32_t hi[16], lo[16];
-#pragma unroll
-                        for (int e = 0; e < 16; e++) {
-                            int o = c16 + e;
-                            float nv = 0.f;
-                            if (o < p.c) {
-                                float f = v[e] + __ldg(b2 + o);
-                                nv = a.inverse ? oldv[e] - f : oldv[e] + f;
-                                __stcg(dst + (int64_t)o * HW, nv);
-                            }
-                            hi[e] = bf16_bits(nv);
-                            lo[e] = bf16_bits(nv - bf16_val(hi[e]));
-                        }
-                        if (write_x) {
-#pragma unroll
-                            for (int hh = 0; hh < 2; hh++) {
-                                if (c16 + hh * 8 >= p.Cp) break;
-                                size_t off = (size_t)((c16 / 8) + hh) * plane_bytes + (size_t)(r + p.G) * 16;
-                                const uint32_t* q = hi + hh * 8;
-                                *reinterpret_cast<uint4*>(xbuf + off) =
-                                    make_uint4(q[0] | q[1] << 16, q[2] | q[3] << 16, q[4] | q[5] << 16, q[6] | q[7] << 16);
-                                if (p.prec3) {
-                                    const uint32_t* w = lo + hh * 8;
-                                    *reinterpret_cast<uint4*>(xlo_buf + off) =
-                                        make_uint4(w[0] | w[1] << 16, w[2] | w[3] << 16, w[4] | w[5] << 16, w[6] | w[7] << 16);
-                                }
-                            }
-                        }
-                        }
-#pragma unroll
-                        for (int e = 0; e < 16; e++) oldv[e] = nxt[e];
                     }
+                    if (valid) {
+                        float* dst = stb + ((int64_t)ii * a.C + out_off) * eHW + y * eW + x;
+#pragma unroll
+                        for (int q8 = 0; q8 < 6; q8++) {
+                            if (q8 * 8 >= cw2 || q8 * 8 >= OLDN) break;
+                            if (cb2 + q8 * 8 >= ec && !(write_x && (cb2 + q8 * 8) < eCp)) break;
+                            float n8[8];
+#pragma unroll
+                            for (int e = 0; e < 8; e++) {
+                                const int o = cb2 + q8 * 8 + e;
+                                const float acc = q8 < 2 ? v0[q8 * 8 + e] : (q8 < 4 ? v1[(q8 - 2) * 8 + e] : v2[(q8 - 4) * 8 + e]);
+                                float nv = 0.f;
+                                if (o < ec) {
+                                    const float f = acc + __ldg(b2 + o);
+                                    nv = a.inverse ? oldv[q8 * 8 + e] - f : oldv[q8 * 8 + e] + f;
+                                    dst[(int64_t)o * eHW] = nv;
+                                }
+                                n8[e] = nv;
+                            }
+                            if (write_x && (cb2 + q8 * 8) < eCp) store8(xbuf, xlo_buf, (cb2 + q8 * 8) / 8, r, n8);
+                        }
+                    }
+                    if (tile + 1 < eT) load_old(tile + 1);
                 }
                 if (write_x) {
                     fence_before();
                     fence_proxy_async();
                     mbar_arrive(x_full);
+                }
+                if (esst && !write_x) {   // last block of the stage: state back to global
+                    asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads));
+                    const int64_t nf = (int64_t)nimg * a.C * eHW;
+                    float4* dst4 = reinterpret_cast<float4*>(a.state + img0 * a.C * eHW);
+                    const float4* src4 = reinterpret_cast<const float4*>(sst);
+                    for (int64_t i = et; i < nf / 4; i += kEpiThreads) __stcg(dst4 + i, src4[i]);
+                    asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads));
                 }
                 t_e2 += clock64() - te2;
             }
@@ -624,6 +707,7 @@ static bool make_plan(const StageInfo& S, bool prec3, StagePlan& best) {
                 size_t smem = (size_t)nslot * slot_bytes + (size_t)P * ((p.Cp + MC) / 8) * Rtot * 16 + 256 +
                               8 * (size_t)(9 * (p.Cp / 8 + 1) + 9 * (MC / 16));
                 if (smem > kSmemCap) continue;
+
                 // score: useful fraction of M rows, weight reuse (T), fewer chunk round trips
                 double eff = (double)I * p.H * p.W / (T * 128.0);
                 double score = eff * (1.0 - 0.15 / T) * (1.0 - 0.02 * (p.Mp / MC)) + 0.001 * nslot;
@@ -632,12 +716,20 @@ static bool make_plan(const StageInfo& S, bool prec3, StagePlan& best) {
                     best = p;
                     best.MC = MC; best.nch = p.Mp / MC; best.T = T; best.I = I;
                     best.Rtot = Rtot; best.nslot = nslot; best.slot_bytes = slot_bytes; best.smem = smem;
+
                 }
                 break;
             }
         }
     }
     if (best_score < 0) return false;
+    {   // second pass: keep the batch's fp32 state in shared memory when it still fits
+        const size_t state_bytes = (size_t)best.I * 2 * best.c * best.H * best.W * 4;
+        const size_t off = (best.smem + 127) / 128 * 128;
+        best.sstate_off = (uint32_t)off;
+        best.sstate = off + state_bytes <= kSmemCap ? 1 : 0;
+        if (best.sstate) best.smem = off + state_bytes;
+    }
     best.k1 = best.pair ? 6 : 9 * (best.Cp / 16);
     best.k2 = 9 * (best.MC / 16);
     int cols = best.T * (best.MC + best.Nc2);
@@ -717,23 +809,23 @@ struct UmmaState {
 
 // ---- compile-time specialisations for the Arch-C stage plans (see make_plan) -----------------
 typedef void (*StageKernel)(StageArgs);
-struct SpecEntry { int Wp, Cp, MC, Nc2, T, p3, slot; StageKernel fn; };
-#define CI_SPEC(WP, CP, MC, NC2, T, P3, SLOT) \
-    {WP, CP, MC, NC2, T, P3, SLOT, k_stage<SCfg<WP, CP, MC, NC2, T, P3, SLOT>>}
+struct SpecEntry { int Wp, Cp, MC, Nc2, T, p3, slot, H, c, sst; StageKernel fn; };
+#define CI_SPEC(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST) \
+    {WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, k_stage<SCfg<WP, CP, MC, NC2, T, P3, SLOT, H, C, SST>>}
 static const SpecEntry kSpecs[] = {
-    CI_SPEC(17, 8, 32, 16, 7, 0, 16384),   // C stage 1, bf16
-    CI_SPEC(9, 32, 32, 32, 7, 0, 16384),   // C stage 2, bf16
-    CI_SPEC(5, 96, 128, 96, 2, 0, 16384),  // C stage 3, bf16
-    CI_SPEC(17, 8, 32, 16, 7, 1, 16384),   // C stage 1, bf16x3
-    CI_SPEC(9, 32, 128, 32, 2, 1, 16384),  // C stage 2, bf16x3
-    CI_SPEC(5, 96, 64, 96, 2, 1, 16384),   // C stage 3, bf16x3
+    CI_SPEC(17, 8, 32, 16, 7, 0, 16384, 16, 6, 1),   // C stage 1, bf16
+    CI_SPEC(9, 32, 32, 32, 7, 0, 16384, 8, 24, 0),   // C stage 2, bf16
+    CI_SPEC(5, 96, 128, 96, 2, 0, 16384, 4, 96, 0),  // C stage 3, bf16
+    CI_SPEC(17, 8, 32, 16, 7, 1, 16384, 16, 6, 0),   // C stage 1, bf16x3
+    CI_SPEC(9, 32, 128, 32, 2, 1, 16384, 8, 24, 0),  // C stage 2, bf16x3
+    CI_SPEC(5, 96, 64, 96, 2, 1, 16384, 4, 96, 0),   // C stage 3, bf16x3
 };
 
 static StageKernel pick_kernel(const StagePlan& p) {
     if (!getenv("CI_NO_STATIC"))
         for (const auto& e : kSpecs)
             if (e.Wp == p.Wp && e.Cp == p.Cp && e.MC == p.MC && e.Nc2 == p.Nc2 && e.T == p.T && e.p3 == p.prec3 &&
-                e.slot == p.slot_bytes)
+                e.slot == p.slot_bytes && e.H == p.H && e.c == p.c && e.sst == p.sstate)
                 return e.fn;
     return k_stage<SDyn>;
 }

@@ -119,23 +119,24 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
+// try_wait with a suspend-time hint: the thread sleeps in hardware until the phase completes
+// (woken by the arrival) or the hint (ns) expires, instead of burning issue slots polling.
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
     uint32_t ok;
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}\n"
         : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
         : "memory");
     return ok != 0;
 }
-// Spin on try_wait (which itself suspends in hardware for a bounded time).  A deadlock
-// becomes a trap (launch error) after ~2^28 polls instead of a hung GPU.
+// A deadlock becomes a trap (launch error) after ~2^22 suspended waits instead of a hung GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     uint32_t n = 0;
     while (!mbar_try_wait(bar, parity)) {
-        if (++n > (1u << 28)) __trap();
+        if (++n > (1u << 22)) __trap();
     }
 }
 
