@@ -11,6 +11,8 @@ N > 1: launched by torchrun, one process per GPU; groups are sharded across rank
 rank serves its own 1024 groups, no collective on the data path: "scaling": "weak");
 timing is a barrier + synchronize bracket, device-timed with CUDA events, max over ranks.
 Inputs rotate over 4 resident buffer sets (x + outputs ~1 GB > 126 MB L2).
+Rank r serves global groups [r*1024, (r+1)*1024) of each workload (fixtures.shard; the
+N>1 host logic is covered by tests/test_multiproc.py with gloo, world size 2).
 """
 from __future__ import annotations
 
@@ -174,14 +176,13 @@ def main():
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
 
-    # rank r serves its own B groups (seeded per rank); NBUF rotating buffer sets
-    xs = [torch.from_numpy(fx.make_inputs(arch, B, k, cfg.seed_x + 7919 * (rank * NBUF + i))).to(dev)
+    # group-sharded data parallelism: rank r serves global groups [r*B, (r+1)*B) of each of
+    # NBUF rotating global workloads (counter-based slices: no rank generates others' groups)
+    b0, b1 = fx.shard(rank, world, B)
+    xs = [torch.from_numpy(fx.make_inputs_slice(arch, b0, b1, k, cfg.seed_x + 7919 * i)).to(dev)
           for i in range(NBUF)]
-    drops = []
-    for i in range(NBUF):
-        dt_ = torch.empty(B, dtype=torch.int32, device=dev)
-        ci.ci_make_drops(k, B, cfg.seed_drop + 7919 * (rank * NBUF + i), dt_)
-        drops.append(dt_)
+    drops = [torch.from_numpy(fx.make_drops_slice(b0, b1, k, cfg.seed_drop + 7919 * i)).to(dev)
+             for i in range(NBUF)]
     hs = [torch.empty(B, k, d, device=dev) for _ in range(NBUF)]
     ps = [torch.empty(B, d, device=dev) for _ in range(NBUF)]
     ncls = sum(arch.heads)
@@ -299,8 +300,8 @@ def main():
     if not args.no_e2e:
         model = main_run["model"]
         wsh = model.workspace(k, B, host=True)
-        xh = torch.from_numpy(fx.make_inputs(arch, B, k, cfg.seed_x + rank)).pin_memory()
-        dh = torch.from_numpy(fx.make_drops(B, k, cfg.seed_drop + rank)).pin_memory()
+        xh = torch.from_numpy(fx.make_inputs_slice(arch, b0, b1, k, cfg.seed_x)).pin_memory()
+        dh = torch.from_numpy(fx.make_drops_slice(b0, b1, k, cfg.seed_drop)).pin_memory()
         hh = torch.empty(B, k, d).pin_memory()
         ph = torch.empty(B, d).pin_memory()
         lgh = torch.empty(B * k * ncls).pin_memory()

@@ -198,6 +198,27 @@ def make_inputs(arch: Arch, B: int, k: int, seed: int) -> np.ndarray:
     return uniform_f32(seed, 0, n, 0.0, 1.0).reshape(B, k, arch.in_c, arch.in_h, arch.in_w)
 
 
+def make_inputs_slice(arch: Arch, b0: int, b1: int, k: int, seed: int) -> np.ndarray:
+    """Groups [b0, b1) of make_inputs(arch, B, k, seed) for any B >= b1, generated directly
+    (counter-based stream: element e of the global tensor is splitmix64_at(stream, e))."""
+    per = k * arch.in_c * arch.in_h * arch.in_w
+    idx = np.arange(b0 * per, b1 * per, dtype=np.uint64)
+    z = splitmix64_at(stream_seed(seed, 0), idx)
+    u = (z >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+    return u.astype(np.float32).reshape(b1 - b0, k, arch.in_c, arch.in_h, arch.in_w)
+
+
+def make_drops_slice(b0: int, b1: int, k: int, seed: int) -> np.ndarray:
+    z = splitmix64_at(seed & MASK64, np.arange(b0, b1, dtype=np.uint64))
+    return ((z >> np.uint64(32)) % np.uint64(k)).astype(np.int32)
+
+
+def shard(rank: int, world: int, groups_per_rank: int):
+    """Group-sharded data parallelism: rank r serves global groups [r*B, (r+1)*B)."""
+    assert 0 <= rank < world
+    return rank * groups_per_rank, (rank + 1) * groups_per_rank
+
+
 def make_drops(B: int, k: int, seed: int) -> np.ndarray:
     """j_b = (uint32)(splitmix64_at(seed, b) >> 32) % k, int32[B]."""
     z = splitmix64_at(seed & MASK64, np.arange(B, dtype=np.uint64))
