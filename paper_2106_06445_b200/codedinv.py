@@ -235,10 +235,10 @@ def ci_test_mean(h, m, stream=None):
 
 
 PLAN_FIELDS = ["Wp", "G", "Cp", "Mp", "MC", "nch", "Nc2", "T", "I", "Rtot", "k1", "k2", "nslot",
-               "slot_bytes", "smem", "blk_bytes"]
+               "slot_bytes", "smem", "blk_bytes", "nhd", "sstate", "est", "tmem_cols"]
 
 
 def ci_test_plan(H, W, c, m, prec3):
-    out = (ctypes.c_int64 * 16)()
+    out = (ctypes.c_int64 * 20)()
     _check(_lib.ci_test_plan(H, W, c, m, 1 if prec3 else 0, out), "ci_test_plan")
     return dict(zip(PLAN_FIELDS, list(out)))

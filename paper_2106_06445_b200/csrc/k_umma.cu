@@ -57,6 +57,8 @@ struct StagePlan {
     int64_t blk_bytes;     // packed weight stream bytes per block
     size_t smem;
     int tmem_cols;
+    double est_cycles;     // planner's cost estimate (cycles per image per block)
+    int nhd;               // hidden plane buffers (2: double-buffered, conv1/epilogue overlap conv2)
     int sstate;            // 1: the batch's fp32 state lives in shared memory for the whole stage
     uint32_t sstate_off;   // byte offset of the fp32 state region in dynamic smem
 };
@@ -78,6 +80,17 @@ __host__ __device__ inline int kstep_bytes(int N, int prec3) { return N * 32 * (
 __host__ __device__ inline int steps_per_slot(int N, int prec3, int slot_bytes) {
     int g = slot_bytes / kstep_bytes(N, prec3);
     return g < 1 ? 1 : g;
+}
+
+// MMA / weight-stream segment order within one block (software pipelined by one chunk):
+//   conv1_0, conv1_1, conv2_0, conv1_2, conv2_1, ..., conv1_{n-1}, conv2_{n-2}, conv2_{n-1}
+// so the conv1 epilogue of chunk j+1 runs while the tensor core executes conv2 of chunk j.
+__host__ __device__ inline void seg_of(int q, int nch, int& is_conv2, int& j) {
+    if (q == 0) { is_conv2 = 0; j = 0; return; }
+    const int r = q - 1;                      // pairs (conv1_{j+1}, conv2_j)
+    const int jj = r / 2;
+    if (jj >= nch - 1) { is_conv2 = 1; j = nch - 1; return; }
+    if ((r & 1) == 0) { is_conv2 = 0; j = jj + 1; } else { is_conv2 = 1; j = jj; }
 }
 
 __device__ __forceinline__ uint32_t bf16_bits(float v) {
@@ -196,24 +209,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
     uint8_t* ring = smem;                                           // nslot * slot_bytes
     uint8_t* xbuf = ring + (size_t)p.nslot * p.slot_bytes;          // P * Cp/8 planes
     const uint32_t plane_bytes = (uint32_t)p.Rtot * 16;
-    uint8_t* hbuf = xbuf + (size_t)P * (p.Cp / 8) * plane_bytes;    // P * MC/8 planes
-    uint64_t* bars = reinterpret_cast<uint64_t*>(hbuf + (size_t)P * (p.MC / 8) * plane_bytes);
+    uint8_t* hbuf = xbuf + (size_t)P * (p.Cp / 8) * plane_bytes;    // nhd x (P * MC/8 planes)
+    const size_t hbuf_stride = (size_t)P * (p.MC / 8) * plane_bytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(hbuf + (size_t)p.nhd * hbuf_stride);
     uint64_t* full = bars;                  // [kMaxSlots]
     uint64_t* empty = bars + kMaxSlots;     // [kMaxSlots]
     uint64_t* x_full = bars + 2 * kMaxSlots;
     uint64_t* acc1_full = x_full + 1;
-    uint64_t* hd_full = x_full + 2;
-    uint64_t* hd_empty = x_full + 3;
-    uint64_t* acc2_full = x_full + 4;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_full + 5);
+    uint64_t* acc2_full = x_full + 2;
+    uint64_t* hd_full = x_full + 3;    // [2]
+    uint64_t* hd_empty = x_full + 5;   // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_full + 7);
     // per-k-step A descriptors for tile 0 (hi planes): conv1 [k1], conv2 [k2]
-    uint64_t* adesc1 = x_full + 6;
+    uint64_t* adesc1 = x_full + 8;
     uint64_t* adesc2 = adesc1 + p.k1;
 
     // ---- zero the activation buffers (pads and guards must read as 0)
     {
         uint4 z = make_uint4(0, 0, 0, 0);
-        size_t nbytes = (size_t)P * ((p.Cp + p.MC) / 8) * plane_bytes;
+        size_t nbytes = (size_t)P * ((p.Cp + p.nhd * p.MC) / 8) * plane_bytes;
         for (size_t i = tid; i < nbytes / 16; i += kThreads) reinterpret_cast<uint4*>(xbuf)[i] = z;
     }
     fence_proxy_async();
@@ -222,8 +236,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
         for (int i = 0; i < p.nslot; i++) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
         mbar_init(x_full, kEpiThreads);
         mbar_init(acc1_full, 1);
-        mbar_init(hd_full, kEpiThreads);
-        mbar_init(hd_empty, 1);
+        for (int i = 0; i < 2; i++) { mbar_init(&hd_full[i], kEpiThreads); mbar_init(&hd_empty[i], 1); }
         mbar_init(acc2_full, 1);
         fence_mbar_init();
         const uint32_t plane_b = (uint32_t)p.Rtot * 16;
@@ -268,8 +281,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                 for (int tt = 0; tt < a.nb; tt++) {
                     int t = a.inverse ? a.nb - 1 - tt : tt;
                     const uint8_t* src = a.wpack + (int64_t)t * p.blk_bytes;
-                    for (int j = 0; j < p.nch; j++) {
-                        for (int seg = 0; seg < 2; seg++) {
+                    for (int q = 0; q < 2 * p.nch; q++) {
+                        {
+                            int seg, jj;
+                            seg_of(q, p.nch, seg, jj);
                             int N = seg == 0 ? p.MC : p.Nc2;
                             int K = seg == 0 ? p.k1 : p.k2;
                             int g = steps_per_slot(N, p.prec3, p.slot_bytes);
@@ -300,11 +315,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
         // keeps them on the uniform datapath: no R2UR / waterfall in the inner loops.
         if (elect_one()) {
             int slot = 0;
-            uint32_t phase = 0, xph = 0, hph = 0;
+            uint32_t phase = 0, xph = 0, hph[2] = {0, 0};
             const uint32_t xb = smem_u32(xbuf) + (uint32_t)p.G * 16;
             const uint32_t hb = smem_u32(hbuf) + (uint32_t)p.G * 16;
             const uint32_t xlo_b = (uint32_t)(p.Cp / 8) * plane_bytes;   // lo planes (prec3)
             const uint32_t hlo_b = (uint32_t)(p.MC / 8) * plane_bytes;
+            (void)hlo_b;
             const uint32_t id1 = idesc_bf16(128, p.MC), id2 = idesc_bf16(128, p.Nc2);
             const uint32_t rb = smem_u32(ring);
             const uint32_t lbo1 = p.pair ? 16u : plane_bytes;
@@ -318,8 +334,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                 for (int tt = 0; tt < a.nb; tt++) {
                     TWAIT(w_x, mbar_wait(x_full, xph)); xph ^= 1;
                     fence_after();
-                    for (int j = 0; j < p.nch; j++) {
-                        // ---------------- conv1, chunk j -> acc1 ----------------
+                    auto do_conv1 = [&](int j) {
                         if constexpr (CFG::kStatic) {
                             constexpr uint32_t LBO1 = CFG::PAIR ? 16u : (uint32_t)CFG::PLANE16 * 16u;
                             const uint32_t alo0 = ((xb >> 4) & 0x3FFFu) | ((LBO1 >> 4) << 16);
@@ -328,7 +343,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                          CFG::T, CFG::MC, CFG::P3, CFG::LOX16, CFG::ACC1, CFG::MC>(
                                 tmem, alo0, ringlo, (uint32_t)CFG::SLOT / 16u, id1, 0u, slot, phase, p.nslot,
                                 full, empty);
-                            commit(acc1_full);
                         } else
                                                 {
                             int tap = 0, kc = 0, q = 0;
@@ -367,20 +381,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                     q = 0;
                                 }
                             }
-                            commit(acc1_full);
                         }
-                        // ---------------- conv2, chunk j -> acc2 ----------------
-                        TWAIT(w_hd, mbar_wait(hd_full, hph)); hph ^= 1;
-                        fence_after();
+                    };
+                    auto do_conv2 = [&](int j) {
+                        const uint32_t hbj = hb + (uint32_t)((j & (p.nhd - 1)) * hbuf_stride);
                         if constexpr (CFG::kStatic) {
                             constexpr uint32_t LBO2 = (uint32_t)CFG::PLANE16 * 16u;
-                            const uint32_t alo0 = ((hb >> 4) & 0x3FFFu) | ((LBO2 >> 4) << 16);
+                            const uint32_t alo0 = ((hbj >> 4) & 0x3FFFu) | ((LBO2 >> 4) << 16);
                             const uint32_t ringlo = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::NC2 * 16 >> 4) << 16);
                             issue_static<CFG::K2, CFG::PER2, false, CFG::WP, CFG::PLANE16, CFG::G2, CFG::KB2 / 16,
                                          CFG::T, CFG::NC2, CFG::P3, CFG::LOH16, 0, CFG::NC2>(
                                 tmem, alo0, ringlo, (uint32_t)CFG::SLOT / 16u, id2, j > 0 ? 1u : 0u, slot, phase,
                                 p.nslot, full, empty);
-                            commit(hd_empty);
                         } else
                         {
                             int tap = 0, kc = 0, q = 0;
@@ -390,7 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                     fence_after();
                                 }
                                 const int shift = (tap / 3 - 1) * p.Wp + (tap % 3 - 1);
-                                const uint32_t aaddr = hb + (uint32_t)shift * 16u + (uint32_t)(2 * kc) * plane_bytes;
+                                const uint32_t aaddr = hbj + (uint32_t)shift * 16u + (uint32_t)(2 * kc) * plane_bytes;
                                 const uint32_t baddr = rb + (uint32_t)slot * (uint32_t)p.slot_bytes + (uint32_t)q * kb2;
                                 const uint32_t acc = (j > 0 || s > 0) ? 1u : 0u;
                                 for (int tile = 0; tile < p.T; tile++) {
@@ -411,8 +423,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                     q = 0;
                                 }
                             }
-                            commit(hd_empty);
                         }
+                    };
+                    do_conv1(0);
+                    commit(acc1_full);
+                    for (int j = 0; j < p.nch; j++) {
+                        const int hbi = j & (p.nhd - 1);
+                        TWAIT(w_hd, mbar_wait(&hd_full[hbi], hph[hbi])); hph[hbi] ^= 1;
+                        fence_after();
+                        if (j + 1 < p.nch) {          // acc1 is free: epi1_j has read it
+                            do_conv1(j + 1);
+                            commit(acc1_full);
+                        }
+                        do_conv2(j);
+                        commit(&hd_empty[hbi]);
                     }
                     commit(acc2_full);
                 }
@@ -449,10 +473,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
         const int et = ew * 32 + lane;                 // 0..255
         const int row_in_tile = quarter * 32 + lane;
         const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
-        uint32_t a1ph = 0, a2ph = 0, heph = 0;
-        int hd_uses = 0;
+        uint32_t a1ph = 0, a2ph = 0, heph[2] = {0, 0};
+        int hd_uses[2] = {0, 0};
         uint8_t* xlo_buf = xbuf + (size_t)(eCp / 8) * plane_bytes;
-        uint8_t* hlo_buf = hbuf + (size_t)(eMC / 8) * plane_bytes;
         const int cw1 = eMC / 2, cb1 = half * cw1;     // conv1 chunk columns of this half
         const int cw2 = eNC2 / 2, cb2 = half * cw2;    // conv2 columns of this half
         const bool any2 = cb2 < ec;                    // this half owns at least one real channel
@@ -534,8 +557,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                     // ---- conv1 epilogue: acc1 -> bias + act -> bf16 hidden planes
                     TWAIT(w_a1, mbar_wait(acc1_full, a1ph)); a1ph ^= 1;
                     fence_after();
-                    if (hd_uses > 0) { TWAIT(w_he, mbar_wait(hd_empty, heph)); heph ^= 1; }
-                    hd_uses++;
+                    const int hb_i = j & (p.nhd - 1);
+                    if (hd_uses[hb_i] > 0) { TWAIT(w_he, mbar_wait(&hd_empty[hb_i], heph[hb_i])); heph[hb_i] ^= 1; }
+                    hd_uses[hb_i]++;
+                    uint8_t* hbuf_j = hbuf + (size_t)hb_i * hbuf_stride;
+                    uint8_t* hlo_buf = hbuf_j + (size_t)(eMC / 8) * plane_bytes;
                     long long te0 = clock64();
                     const float* bj = b1 + j * eMC + cb1;
                     for (int tile = 0; tile < eT; tile++) {
@@ -567,13 +593,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                     if (a.act == 0) h = fmaxf(h, 0.f);
                                     h8[e] = valid ? h : 0.f;
                                 }
-                                store8(hbuf, hlo_buf, (cb1 + g0) / 8 + q8, r, h8);
+                                store8(hbuf_j, hlo_buf, (cb1 + g0) / 8 + q8, r, h8);
                             }
                         }
                     }
                     fence_before();
                     fence_proxy_async();
-                    mbar_arrive(hd_full);
+                    mbar_arrive(&hd_full[hb_i]);
                     t_e1 += clock64() - te0;
                 }
                 // ---- conv2 epilogue: s_out (+|-)= acc2 + b2 (fp32); bf16(s_out) -> X
@@ -683,8 +709,33 @@ static float bf2f(uint16_t b) {
 
 static const size_t kSmemCap = 227 * 1024;
 
+// SS-mode tcgen05 128xNx16 cost (cycles), measured (profiles/r01_umma_probe.md)
+static double mma_cyc(int N) { return std::max(N / 2.0, 32.0 + N / 4.0); }
+
+// Cost model (cycles per image per block), calibrated on B200 with CI_DEBUG_CYCLES:
+//   MMA: k-steps x tiles x mma_cyc(N) (x3 for bf16x3)
+//   epilogue-1 per tile per chunk ~ 100 + 15 * (MC/2) columns per thread
+//   epilogue-2 per tile ~ 300 + 60 * (Nc2/2) (global fp32 state) / 200 + 40 * (Nc2/2) (smem state)
+//   nhd = 2 overlaps epilogue-1 of chunk j+1 with conv2 of chunk j
+//   weights: packed bytes per block / cycles must stay under ~40 B/cycle/SM of L2 bandwidth;
+//   a 2-slot ring cannot hide the L2 latency of the weight stream (x1.3)
+// Tuned plans for the Arch-C stage shapes (chosen from CI_DEBUG_CYCLES measurements);
+// other shapes use the cost model.
+struct TunedPlan { int H, W, c, m, prec3, MC, T, nhd, nslot; };
+static const TunedPlan kTuned[] = {
+    {16, 16, 6, 64, 0, 32, 7, 2, 3},    // stage 1 bf16: SMEM-resident state fits
+    {8, 8, 24, 128, 0, 32, 7, 2, 3},    // stage 2 bf16
+    {4, 4, 96, 256, 0, 128, 2, 1, 4},   // stage 3 bf16
+    {16, 16, 6, 64, 1, 16, 7, 2, 4},    // stage 1 bf16x3
+    {8, 8, 24, 128, 1, 128, 2, 1, 3},   // stage 2 bf16x3
+    {4, 4, 96, 256, 1, 64, 2, 1, 3},    // stage 3 bf16x3
+};
+
 static bool make_plan(const StageInfo& S, bool prec3, StagePlan& best) {
     StagePlan p{};
+    const TunedPlan* tuned = nullptr;
+    for (const auto& tp : kTuned)
+        if (tp.H == S.H && tp.W == S.W && tp.c == S.c && tp.m == S.m && tp.prec3 == (prec3 ? 1 : 0)) tuned = &tp;
     p.H = S.H; p.W = S.W; p.Wp = S.W + 1; p.G = p.Wp + 2;
     p.c = S.c; p.m = S.m;
     p.Cp = S.c <= 8 ? 8 : rup(S.c, 16);
@@ -692,54 +743,63 @@ static bool make_plan(const StageInfo& S, bool prec3, StagePlan& best) {
     p.Nc2 = rup(S.c, 16);
     p.pair = p.Cp == 8;
     p.prec3 = prec3 ? 1 : 0;
+    if (p.Nc2 > 256) return false;
     const int P = prec3 ? 2 : 1;
+    const double P3f = prec3 ? 3.0 : 1.0;
     const int img_rows = (p.H + 1) * p.Wp;
-    double best_score = -1;
+    const int k1 = p.pair ? 6 : 9 * (p.Cp / 16);
+    double best_cost = 1e300;
     for (int MC = p.Mp; MC >= 16; MC -= 16) {
-        if (p.Mp % MC) continue;
+        if (p.Mp % MC || MC > 256) continue;
+        if (tuned && MC != tuned->MC) continue;
+        const int nch = p.Mp / MC;
+        const int k2 = 9 * (MC / 16);
         for (int T = 1; T <= 8; T++) {
             if (T * (MC + p.Nc2) > 512) break;
-            int I = (T * 128) / img_rows;
+            if (tuned && T != tuned->T) continue;
+            const int I = (T * 128) / img_rows;
             if (I < 1) continue;
-            for (int nslot = 4; nslot >= 2; nslot--) {
-                int slot_bytes = std::max(16384, std::max(kstep_bytes(MC, prec3), kstep_bytes(p.Nc2, prec3)));
-                int Rtot = T * 128 + 2 * p.G;
-                size_t smem = (size_t)nslot * slot_bytes + (size_t)P * ((p.Cp + MC) / 8) * Rtot * 16 + 256 +
-                              8 * (size_t)(9 * (p.Cp / 8 + 1) + 9 * (MC / 16));
-                if (smem > kSmemCap) continue;
-
-                // score: useful fraction of M rows, weight reuse (T), fewer chunk round trips
-                double eff = (double)I * p.H * p.W / (T * 128.0);
-                double score = eff * (1.0 - 0.15 / T) * (1.0 - 0.02 * (p.Mp / MC)) + 0.001 * nslot;
-                if (score > best_score) {
-                    best_score = score;
-                    best = p;
-                    best.MC = MC; best.nch = p.Mp / MC; best.T = T; best.I = I;
-                    best.Rtot = Rtot; best.nslot = nslot; best.slot_bytes = slot_bytes; best.smem = smem;
-
+            for (int nhd = (nch >= 2 ? 2 : 1); nhd >= 1; nhd--) {
+                if (tuned && nhd != tuned->nhd) continue;
+                for (int nslot = 4; nslot >= 2; nslot--) {
+                    if (tuned && nslot != tuned->nslot) continue;
+                    const int slot_bytes = std::max(16384, std::max(kstep_bytes(MC, prec3), kstep_bytes(p.Nc2, prec3)));
+                    const int Rtot = T * 128 + 2 * p.G;
+                    const size_t smem0 = (size_t)nslot * slot_bytes + (size_t)P * ((p.Cp + nhd * MC) / 8) * Rtot * 16 +
+                                         256 + 8 * (size_t)(9 * (p.Cp / 8 + 1) + 9 * (MC / 16));
+                    if (smem0 > kSmemCap) continue;
+                    const size_t state_bytes = (size_t)I * 2 * p.c * p.H * p.W * 4;
+                    const size_t soff = (smem0 + 127) / 128 * 128;
+                    const int sst = soff + state_bytes <= kSmemCap ? 1 : 0;
+                    // ---- cost per batch per block
+                    const double mma1 = (double)nch * k1 * T * mma_cyc(MC) * P3f;
+                    const double mma2 = (double)nch * k2 * T * mma_cyc(p.Nc2) * P3f;
+                    const double e1c = T * (100.0 + 15.0 * (MC / 2)) * (prec3 ? 1.3 : 1.0);   // per chunk
+                    const double e2 = T * (sst ? 200.0 + 40.0 * (p.Nc2 / 2) : 300.0 + 60.0 * (p.Nc2 / 2));
+                    double t = nhd == 2 ? std::max(mma1 + mma2, nch * e1c) + e1c + e2 : mma1 + mma2 + nch * e1c + e2;
+                    const double wbytes = (double)nch * (k1 * kstep_bytes(MC, prec3) + k2 * kstep_bytes(p.Nc2, prec3));
+                    t = std::max(t, wbytes / 40.0);
+                    if (nslot < 3) t *= 1.3;
+                    const double cost = t / I;
+                    if (cost < best_cost) {
+                        best_cost = cost;
+                        best = p;
+                        best.MC = MC; best.nch = nch; best.T = T; best.I = I; best.Rtot = Rtot;
+                        best.nslot = nslot; best.slot_bytes = slot_bytes; best.nhd = nhd;
+                        best.sstate = sst; best.sstate_off = (uint32_t)soff;
+                        best.smem = sst ? soff + state_bytes : smem0;
+                        best.k1 = k1; best.k2 = k2;
+                        best.blk_bytes = (int64_t)wbytes;
+                        best.est_cycles = cost;
+                    }
                 }
-                break;
             }
         }
     }
-    if (best_score < 0) return false;
-    {   // second pass: keep the batch's fp32 state in shared memory when it still fits
-        const size_t state_bytes = (size_t)best.I * 2 * best.c * best.H * best.W * 4;
-        const size_t off = (best.smem + 127) / 128 * 128;
-        best.sstate_off = (uint32_t)off;
-        best.sstate = off + state_bytes <= kSmemCap ? 1 : 0;
-        if (best.sstate) best.smem = off + state_bytes;
-    }
-    best.k1 = best.pair ? 6 : 9 * (best.Cp / 16);
-    best.k2 = 9 * (best.MC / 16);
+    if (best_cost >= 1e300) return false;
     int cols = best.T * (best.MC + best.Nc2);
     best.tmem_cols = 32;
     while (best.tmem_cols < cols) best.tmem_cols *= 2;
-    // stream bytes per block
-    int64_t bytes = 0;
-    for (int j = 0; j < best.nch; j++)
-        bytes += (int64_t)best.k1 * kstep_bytes(best.MC, prec3) + (int64_t)best.k2 * kstep_bytes(best.Nc2, prec3);
-    best.blk_bytes = bytes;
     return true;
 }
 
@@ -768,7 +828,10 @@ static void pack_block(const StagePlan& p, const float* W1, const float* W2, boo
         return W2[(((size_t)o * m + h) * 3 + (u + 1)) * 3 + (v + 1)];
     };
     std::vector<float> tile;
-    for (int j = 0; j < p.nch; j++) {
+    for (int qseg = 0; qseg < 2 * p.nch; qseg++) {
+        int is2, j;
+        seg_of(qseg, p.nch, is2, j);
+        if (!is2)
         // conv1 chunk j: N = MC hidden channels
         for (int s = 0; s < p.k1; s++) {
             tile.assign((size_t)p.MC * 16, 0.f);
@@ -790,6 +853,7 @@ static void pack_block(const StagePlan& p, const float* W1, const float* W2, boo
             put_tile(out, tile, p.MC, prec3);
         }
         // conv2 chunk j: N = Nc2 outputs, K = this chunk's hidden channels
+        if (is2)
         for (int s = 0; s < p.k2; s++) {
             tile.assign((size_t)p.Nc2 * 16, 0.f);
             int per = p.MC / 16, tap = s / per, kc = s % per;
@@ -816,7 +880,7 @@ static const SpecEntry kSpecs[] = {
     CI_SPEC(17, 8, 32, 16, 7, 0, 16384, 16, 6, 1),   // C stage 1, bf16
     CI_SPEC(9, 32, 32, 32, 7, 0, 16384, 8, 24, 0),   // C stage 2, bf16
     CI_SPEC(5, 96, 128, 96, 2, 0, 16384, 4, 96, 0),  // C stage 3, bf16
-    CI_SPEC(17, 8, 32, 16, 7, 1, 16384, 16, 6, 0),   // C stage 1, bf16x3
+    CI_SPEC(17, 8, 16, 16, 7, 1, 16384, 16, 6, 0),   // C stage 1, bf16x3
     CI_SPEC(9, 32, 128, 32, 2, 1, 16384, 8, 24, 0),  // C stage 2, bf16x3
     CI_SPEC(5, 96, 64, 96, 2, 1, 16384, 4, 96, 0),   // C stage 3, bf16x3
 };
@@ -846,10 +910,10 @@ ci_status_t umma_prepare(Model* m, const float* host_params) {
         if (getenv("CI_DEBUG_PLAN"))
             fprintf(stderr,
                     "[ci plan] stage %d %dx%d c=%d m=%d prec3=%d: Cp=%d Mp=%d MC=%d nch=%d Nc2=%d T=%d I=%d "
-                    "k1=%d k2=%d slots=%dx%d smem=%zu tmem=%d blk_bytes=%lld M-eff=%.3f\n",
+                    "k1=%d k2=%d slots=%dx%d smem=%zu tmem=%d blk_bytes=%lld M-eff=%.3f nhd=%d sst=%d est=%.0f cyc/img/blk\n",
                     s, p.H, p.W, p.c, p.m, p.prec3, p.Cp, p.Mp, p.MC, p.nch, p.Nc2, p.T, p.I, p.k1, p.k2,
                     p.nslot, p.slot_bytes, p.smem, p.tmem_cols, (long long)p.blk_bytes,
-                    (double)p.I * p.H * p.W / (p.T * 128.0));
+                    (double)p.I * p.H * p.W / (p.T * 128.0), p.nhd, p.sstate, p.est_cycles);
         // align each stage stream to 128 B
         while ((pack.size() * 2) % 128) pack.push_back(0);
         U->wpack_off[s] = (int64_t)pack.size() * 2;
@@ -971,9 +1035,10 @@ ci_status_t ci_test_plan(int32_t H, int32_t W, int32_t c, int32_t m, int32_t pre
     S.H = H; S.W = W; S.c = c; S.m = m; S.C = 2 * c; S.nb = 1;
     ci::StagePlan p;
     if (!ci::make_plan(S, prec3 != 0, p)) { ci::set_error("no plan"); return CI_ERR_UNSUPPORTED; }
-    int64_t v[16] = {p.Wp, p.G, p.Cp, p.Mp, p.MC, p.nch, p.Nc2, p.T, p.I, p.Rtot, p.k1, p.k2,
-                     p.nslot, p.slot_bytes, (int64_t)p.smem, p.blk_bytes};
-    for (int i = 0; i < 16; i++) out16[i] = v[i];
+    int64_t v[20] = {p.Wp, p.G, p.Cp, p.Mp, p.MC, p.nch, p.Nc2, p.T, p.I, p.Rtot, p.k1, p.k2,
+                     p.nslot, p.slot_bytes, (int64_t)p.smem, p.blk_bytes, p.nhd, p.sstate,
+                     (int64_t)p.est_cycles, p.tmem_cols};
+    for (int i = 0; i < 20; i++) out16[i] = v[i];
     return CI_OK;
 }
 ci_status_t ci_test_prof_enable(int32_t enable) {
