@@ -58,6 +58,8 @@ struct StagePlan {
     size_t smem;
     int tmem_cols;
     double est_cycles;     // planner's cost estimate (cycles per image per block)
+    int hst;               // conv2 "horizontal tap stacking": N = 3 taps x 8 outputs (c <= 8),
+                           // 3 vertical k-steps per 16 hidden channels, col2im in the epilogue
     int nhd;               // hidden plane buffers (2: double-buffered, conv1/epilogue overlap conv2)
     int sstate;            // 1: the batch's fp32 state lives in shared memory for the whole stage
     uint32_t sstate_off;   // byte offset of the fp32 state region in dynamic smem
@@ -124,7 +126,7 @@ __device__ __forceinline__ bool row_pixel(int r, const StagePlan& p, int& ii, in
 //   ringlo: low descriptor word of ring slot 0 with this segment's B LBO field
 // ----------------------------------------------------------------------------------------
 template <int K, int PER, bool PAIR, int WP, int PLANE16, int G, int KB16, int T, int N, bool P3,
-          int LOA16, int ACC0, int DSTRIDE>
+          int LOA16, int ACC0, int DSTRIDE, bool HSTK = false>
 __device__ __forceinline__ void issue_static(uint32_t tmem, uint32_t alo0, uint32_t ringlo, uint32_t slot16,
                                              uint32_t idesc, uint32_t acc_first, int& slot, uint32_t& phase,
                                              int nslot, uint64_t* full, uint64_t* empty) {
@@ -143,7 +145,7 @@ __device__ __forceinline__ void issue_static(uint32_t tmem, uint32_t alo0, uint3
         constexpr int dummy = 0;
         (void)dummy;
         const int shift = PAIR ? (s / 2 - 1) * WP + ((s & 1) ? 1 : -1)
-                               : ((s / PER) / 3 - 1) * WP + ((s / PER) % 3 - 1);
+                               : (HSTK ? (s / PER - 1) * WP : ((s / PER) / 3 - 1) * WP + ((s / PER) % 3 - 1));
         const int poff16 = PAIR ? 0 : 2 * (s % PER) * PLANE16;
         const uint32_t al = alo0 + (uint32_t)(shift + poff16);
         const uint32_t b = bl + (uint32_t)((s % G) * KB16);
@@ -166,8 +168,10 @@ __device__ __forceinline__ void issue_static(uint32_t tmem, uint32_t alo0, uint3
 }
 
 // Static stage configuration (0 = use the runtime plan)
-template <int WP_, int CP_, int MC_, int NC2_, int T_, int P3_, int SLOT_, int H_ = 0, int C_ = 0, int SST_ = 0>
+template <int WP_, int CP_, int MC_, int NC2_, int T_, int P3_, int SLOT_, int H_ = 0, int C_ = 0, int SST_ = 0,
+          int HST_ = 0>
 struct SCfg {
+    static constexpr bool HST = HST_ != 0;
     static constexpr bool kStatic = WP_ > 0;
     static constexpr int WP = WP_, CP = CP_, MC = MC_, NC2 = NC2_, T = T_, SLOT = SLOT_;
     static constexpr int H = H_, W = WP_ - 1, C = C_, SST = SST_;
@@ -179,7 +183,7 @@ struct SCfg {
     static constexpr int PER1 = PAIR ? 2 : CP / 16;
     static constexpr int K1 = PAIR ? 6 : 9 * (CP / 16);
     static constexpr int PER2 = MC / 16;
-    static constexpr int K2 = 9 * (MC / 16);
+    static constexpr int K2 = (HST ? 3 : 9) * (MC / 16);
     static constexpr int KB1 = MC * 32 * (P3 ? 2 : 1), KB2 = NC2 * 32 * (P3 ? 2 : 1);
     static constexpr int G1 = (SLOT / (KB1 > 0 ? KB1 : 1)) < 1 ? 1 : SLOT / (KB1 > 0 ? KB1 : 1);
     static constexpr int G2 = (SLOT / (KB2 > 0 ? KB2 : 1)) < 1 ? 1 : SLOT / (KB2 > 0 ? KB2 : 1);
@@ -188,6 +192,7 @@ struct SCfg {
     static constexpr int LOH16 = (MC / 8) * PLANE16;
 };
 using SDyn = SCfg<0, 0, 0, 0, 0, 0, 0>;
+constexpr int kXchgBytes = 8 * 4 * 2 * 8 * 4;   // hst boundary exchange: [T<=8][quarter][2][8] fp32
 
 #define TWAIT(acc, call)                                      \
     do {                                                      \
@@ -211,7 +216,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
     const uint32_t plane_bytes = (uint32_t)p.Rtot * 16;
     uint8_t* hbuf = xbuf + (size_t)P * (p.Cp / 8) * plane_bytes;    // nhd x (P * MC/8 planes)
     const size_t hbuf_stride = (size_t)P * (p.MC / 8) * plane_bytes;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(hbuf + (size_t)p.nhd * hbuf_stride);
+    float* xchg = reinterpret_cast<float*>(hbuf + (size_t)p.nhd * hbuf_stride);     // hst exchange
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(xchg) + kXchgBytes);
     uint64_t* full = bars;                  // [kMaxSlots]
     uint64_t* empty = bars + kMaxSlots;     // [kMaxSlots]
     uint64_t* x_full = bars + 2 * kMaxSlots;
@@ -390,7 +396,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             const uint32_t alo0 = ((hbj >> 4) & 0x3FFFu) | ((LBO2 >> 4) << 16);
                             const uint32_t ringlo = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::NC2 * 16 >> 4) << 16);
                             issue_static<CFG::K2, CFG::PER2, false, CFG::WP, CFG::PLANE16, CFG::G2, CFG::KB2 / 16,
-                                         CFG::T, CFG::NC2, CFG::P3, CFG::LOH16, 0, CFG::NC2>(
+                                         CFG::T, CFG::NC2, CFG::P3, CFG::LOH16, 0, CFG::NC2, CFG::HST>(
                                 tmem, alo0, ringlo, (uint32_t)CFG::SLOT / 16u, id2, j > 0 ? 1u : 0u, slot, phase,
                                 p.nslot, full, empty);
                         } else
@@ -401,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                     TWAIT(w_full, mbar_wait(&full[slot], phase));
                                     fence_after();
                                 }
-                                const int shift = (tap / 3 - 1) * p.Wp + (tap % 3 - 1);
+                                const int shift = p.hst ? (tap - 1) * p.Wp : (tap / 3 - 1) * p.Wp + (tap % 3 - 1);
                                 const uint32_t aaddr = hbj + (uint32_t)shift * 16u + (uint32_t)(2 * kc) * plane_bytes;
                                 const uint32_t baddr = rb + (uint32_t)slot * (uint32_t)p.slot_bytes + (uint32_t)q * kb2;
                                 const uint32_t acc = (j > 0 || s > 0) ? 1u : 0u;
@@ -465,6 +471,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
         const int eWp = S ? CFG::WP : p.Wp;
         const int eG = S ? CFG::G : p.G;
         const bool esst = S ? (CFG::SST != 0) : (p.sstate != 0);
+        const bool ehst = S ? CFG::HST : (p.hst != 0);
         const int64_t eHW = (int64_t)eH * eW;
         constexpr int OLDN = S ? (CFG::NC2 / 2 > 0 ? CFG::NC2 / 2 : 8) : 48;
         const int ew = warp - 2;                       // 0..7
@@ -604,6 +611,77 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                 }
                 // ---- conv2 epilogue: s_out (+|-)= acc2 + b2 (fp32); bf16(s_out) -> X
                 const bool write_x = tt + 1 < a.nb;
+                if (ehst) {
+                    // ---- horizontal tap stacking: acc2 row r holds Z_v[r][o] at column (v+1)*8+o;
+                    // out[p][o] = Z_-1[p-1][o] + Z_0[p][o] + Z_+1[p+1][o]  (col2im over v).
+                    // Rows are lanes: neighbours come from warp shuffles, warp-boundary rows from
+                    // a small shared-memory exchange.  The two warp halves take alternate tiles.
+                    TWAIT(w_a2, mbar_wait(acc2_full, a2ph)); a2ph ^= 1;
+                    fence_after();
+                    long long te2h = clock64();
+                    {
+                        for (int tile = half; tile < eT; tile += 2) {
+                            float za[16], zb[8];
+                            const uint32_t col = (uint32_t)(tile * eNC2);
+                            tmem_ld16(tmem + lane_addr + col, za);
+                            tmem_ld8(tmem + lane_addr + col + 16, zb);
+                            tmem_wait_ld();
+                            float* xq = xchg + ((tile * 4 + quarter) * 2) * 8;
+                            if (lane == 31) {
+#pragma unroll
+                                for (int o = 0; o < 8; o++) xq[o] = za[o];        // Z_-1 of the last row
+                            }
+                            if (lane == 0) {
+#pragma unroll
+                                for (int o = 0; o < 8; o++) xq[8 + o] = zb[o];    // Z_+1 of the first row
+                            }
+                        }
+                        asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+                        for (int tile = half; tile < eT; tile += 2) {
+                            int r = tile * 128 + row_in_tile, ii, y, x;
+                            const bool valid = rowpix(r, ii, y, x) && ii < nimg;
+                            float za[16], zb[8];
+                            const uint32_t col = (uint32_t)(tile * eNC2);
+                            tmem_ld16(tmem + lane_addr + col, za);
+                            tmem_ld8(tmem + lane_addr + col + 16, zb);
+                            tmem_wait_ld();
+                            float left[8], right[8];
+#pragma unroll
+                            for (int o = 0; o < 8; o++) {
+                                left[o] = __shfl_up_sync(0xffffffffu, za[o], 1);
+                                right[o] = __shfl_down_sync(0xffffffffu, zb[o], 1);
+                            }
+                            if (lane == 0) {
+                                const int tq = quarter > 0 ? tile : tile - 1, qq = quarter > 0 ? quarter - 1 : 3;
+#pragma unroll
+                                for (int o = 0; o < 8; o++) left[o] = tq >= 0 ? xchg[((tq * 4 + qq) * 2) * 8 + o] : 0.f;
+                            }
+                            if (lane == 31) {
+                                const int tq = quarter < 3 ? tile : tile + 1, qq = quarter < 3 ? quarter + 1 : 0;
+#pragma unroll
+                                for (int o = 0; o < 8; o++) right[o] = tq < eT ? xchg[((tq * 4 + qq) * 2 + 1) * 8 + o] : 0.f;
+                            }
+                            if (valid) {
+                                float* dst = stb + ((int64_t)ii * a.C + out_off) * eHW + y * eW + x;
+                                float n8[8];
+#pragma unroll
+                                for (int o = 0; o < 8; o++) {
+                                    float nv = 0.f;
+                                    if (o < ec) {
+                                        const float f = (left[o] + za[8 + o] + right[o]) + __ldg(b2 + o);
+                                        const float old = dst[(int64_t)o * eHW];
+                                        nv = a.inverse ? old - f : old + f;
+                                        dst[(int64_t)o * eHW] = nv;
+                                    }
+                                    n8[o] = nv;
+                                }
+                                if (write_x) store8(xbuf, xlo_buf, 0, r, n8);
+                            }
+                        }
+                        asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+                    }
+                    t_e2 += clock64() - te2h;
+                } else {
                 float oldv[OLDN];
                 auto load_old = [&](int tile) {
                     int r = tile * 128 + row_in_tile, ii, y, x;
@@ -662,6 +740,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                     }
                     if (tile + 1 < eT) load_old(tile + 1);
                 }
+                t_e2 += clock64() - te2;
+                }
                 if (write_x) {
                     fence_before();
                     fence_proxy_async();
@@ -675,7 +755,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                     for (int64_t i = et; i < nf / 4; i += kEpiThreads) __stcg(dst4 + i, src4[i]);
                     asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads));
                 }
-                t_e2 += clock64() - te2;
             }
         }
         if (a.dbg && et == 0) {
@@ -740,7 +819,8 @@ static bool make_plan(const StageInfo& S, bool prec3, StagePlan& best) {
     p.c = S.c; p.m = S.m;
     p.Cp = S.c <= 8 ? 8 : rup(S.c, 16);
     p.Mp = rup(S.m, 16);
-    p.Nc2 = rup(S.c, 16);
+    p.hst = S.c <= 8 ? 1 : 0;
+    p.Nc2 = p.hst ? 32 : rup(S.c, 16);
     p.pair = p.Cp == 8;
     p.prec3 = prec3 ? 1 : 0;
     if (p.Nc2 > 256) return false;
@@ -753,7 +833,7 @@ static bool make_plan(const StageInfo& S, bool prec3, StagePlan& best) {
         if (p.Mp % MC || MC > 256) continue;
         if (tuned && MC != tuned->MC) continue;
         const int nch = p.Mp / MC;
-        const int k2 = 9 * (MC / 16);
+        const int k2 = (p.hst ? 3 : 9) * (MC / 16);
         for (int T = 1; T <= 8; T++) {
             if (T * (MC + p.Nc2) > 512) break;
             if (tuned && T != tuned->T) continue;
@@ -766,7 +846,7 @@ static bool make_plan(const StageInfo& S, bool prec3, StagePlan& best) {
                     const int slot_bytes = std::max(16384, std::max(kstep_bytes(MC, prec3), kstep_bytes(p.Nc2, prec3)));
                     const int Rtot = T * 128 + 2 * p.G;
                     const size_t smem0 = (size_t)nslot * slot_bytes + (size_t)P * ((p.Cp + nhd * MC) / 8) * Rtot * 16 +
-                                         256 + 8 * (size_t)(9 * (p.Cp / 8 + 1) + 9 * (MC / 16));
+                                         256 + kXchgBytes + 8 * (size_t)(9 * (p.Cp / 8 + 1) + 9 * (MC / 16));
                     if (smem0 > kSmemCap) continue;
                     const size_t state_bytes = (size_t)I * 2 * p.c * p.H * p.W * 4;
                     const size_t soff = (smem0 + 127) / 128 * 128;
@@ -858,8 +938,13 @@ static void pack_block(const StagePlan& p, const float* W1, const float* W2, boo
             tile.assign((size_t)p.Nc2 * 16, 0.f);
             int per = p.MC / 16, tap = s / per, kc = s % per;
             for (int n = 0; n < p.Nc2; n++)
-                for (int kk = 0; kk < 16; kk++)
-                    tile[(size_t)n * 16 + kk] = w2(n, j * p.MC + kc * 16 + kk, tap / 3 - 1, tap % 3 - 1);
+                for (int kk = 0; kk < 16; kk++) {
+                    const int h = j * p.MC + kc * 16 + kk;
+                    if (p.hst)   // column n = (v+1)*8 + o, k-step row u = tap-1
+                        tile[(size_t)n * 16 + kk] = n < 24 ? w2(n % 8, h, tap - 1, n / 8 - 1) : 0.f;
+                    else
+                        tile[(size_t)n * 16 + kk] = w2(n, h, tap / 3 - 1, tap % 3 - 1);
+                }
             put_tile(out, tile, p.Nc2, prec3);
         }
     }
@@ -875,12 +960,12 @@ struct UmmaState {
 typedef void (*StageKernel)(StageArgs);
 struct SpecEntry { int Wp, Cp, MC, Nc2, T, p3, slot, H, c, sst; StageKernel fn; };
 #define CI_SPEC(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST) \
-    {WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, k_stage<SCfg<WP, CP, MC, NC2, T, P3, SLOT, H, C, SST>>}
+    {WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, k_stage<SCfg<WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, ((C) <= 8)>>}
 static const SpecEntry kSpecs[] = {
-    CI_SPEC(17, 8, 32, 16, 7, 0, 16384, 16, 6, 1),   // C stage 1, bf16
+    CI_SPEC(17, 8, 32, 32, 7, 0, 16384, 16, 6, 1),   // C stage 1, bf16 (hst)
     CI_SPEC(9, 32, 32, 32, 7, 0, 16384, 8, 24, 0),   // C stage 2, bf16
     CI_SPEC(5, 96, 128, 96, 2, 0, 16384, 4, 96, 0),  // C stage 3, bf16
-    CI_SPEC(17, 8, 16, 16, 7, 1, 16384, 16, 6, 0),   // C stage 1, bf16x3
+    CI_SPEC(17, 8, 16, 32, 7, 1, 16384, 16, 6, 0),   // C stage 1, bf16x3 (hst)
     CI_SPEC(9, 32, 128, 32, 2, 1, 16384, 8, 24, 0),  // C stage 2, bf16x3
     CI_SPEC(5, 96, 64, 96, 2, 1, 16384, 4, 96, 0),   // C stage 3, bf16x3
 };
