@@ -85,7 +85,7 @@ class Arch:
     first_orient: int = 0        # 0: block 0 does s_B += F(s_A); 1: s_A += F(s_B)
     heads: tuple = (10,)         # classes per linear head g_t
     gamma: float = 0.1           # gain on W2 (SURVEY §8a)
-    has_encoder: int = 0         # learned encoder (Arch E) params appended
+    encoder: tuple = ()          # learned encoder (Arch E): (c1, mid); () = none
 
     def stage_shapes(self):
         """[(C, H, W, c=C/2, m, n_blocks)] of each stage after its squeeze."""
@@ -112,20 +112,28 @@ ARCH_M = Arch("M", 1, 28, 28, (Stage(1, 2, 32), Stage(1, 2, 64)))
 ARCH_C = Arch("C", 3, 32, 32, (Stage(1, 9, 64), Stage(1, 9, 128), Stage(1, 9, 256)))
 # Rotation pin (App. A.1) as three additive-coupling shears.
 ARCH_R = Arch("R", 2, 1, 1, (Stage(0, 3, 1),), act="identity", first_orient=1, heads=())
-ARCHS = {a.name: a for a in (ARCH_T, ARCH_M, ARCH_C, ARCH_R)}
+# Arch C + light learned encoder (Arch E) + multitask heads fine 10 / coarse 2
+# (PAPER.md:697-698): config C4.
+ARCH_CE = Arch("CE", 3, 32, 32, ARCH_C.stages, heads=(10, 2), encoder=(16, 64))
+# small encoder arch for fast oracle pins / GPU parity
+ARCH_TE = Arch("TE", 3, 8, 8, ARCH_T.stages, heads=(10, 2), encoder=(4, 8))
+ARCHS = {a.name: a for a in (ARCH_T, ARCH_M, ARCH_C, ARCH_R, ARCH_CE, ARCH_TE)}
 
 
 def linear_variant(arch: Arch) -> Arch:
     """Same shapes, identity activation (P1: h is linear when biases are 0)."""
     return Arch(arch.name + "lin", arch.in_c, arch.in_h, arch.in_w, arch.stages,
                 act="identity", first_orient=arch.first_orient, heads=arch.heads,
-                gamma=arch.gamma, has_encoder=arch.has_encoder)
+                gamma=arch.gamma, encoder=arch.encoder)
 
 
 # --------------------------------------------------------------------------
 # Canonical flat parameter layout
 #   for stage s, block t:  W1[m][c][3][3], b1[m], W2[c][m][3][3], b2[c]
 #   then per head:         Wg[classes][d], bg[classes]
+#   then (learned encoder, Arch E):  E1.W[c1][in_c][3][3], E1.b[c1],
+#        E2.W[mid][4c1][3][3], E2.b[mid], E3.W[4c1][mid][3][3], E3.b[4c1],
+#        E4.W[in_c][c1][3][3], E4.b[in_c]
 # --------------------------------------------------------------------------
 def param_tensors(arch: Arch):
     """[(name, shape, lo, hi)] in canonical order."""
@@ -143,6 +151,14 @@ def param_tensors(arch: Arch):
     for i, ncls in enumerate(arch.heads):
         out.append((f"g{i}.W", (ncls, d), -ag, ag))
         out.append((f"g{i}.b", (ncls,), -0.01, 0.01))
+    if arch.encoder:
+        c1, mid = arch.encoder
+        ci = arch.in_c
+        for nm, co, cin, gain in (("E1", c1, ci, 6.0), ("E2", mid, 4 * c1, 6.0), ("E3", 4 * c1, mid, 6.0),
+                                  ("E4", ci, c1, 3.0)):
+            a = math.sqrt(gain / (9 * cin))
+            out.append((f"{nm}.W", (co, cin, 3, 3), -a, a))
+            out.append((f"{nm}.b", (co,), -0.01, 0.01))
     return out
 
 
@@ -251,4 +267,6 @@ CONFIGS = {
     "C2": Config("C2", ARCH_M, 4, 256, 12, 2, 102, "k=4 MNIST-shaped 1x28x28, 256 groups"),
     "C3": Config("C3", ARCH_C, 10, 1024, 13, 3, 103,
                  "k=10 CIFAR-shaped 3x32x32 full-depth h, exact h^-1 parity encode, 1024 groups"),
+    "C4": Config("C4", ARCH_CE, 10, 1024, 14, 4, 104,
+                 "k=10 CIFAR-shaped, light learned encoder replaces h^-1, multitask heads 10 + 2"),
 }

@@ -32,7 +32,8 @@ class OrArch(ctypes.Structure):
                 ("n_stages", ctypes.c_int), ("squeeze", ctypes.c_int * 4),
                 ("n_blocks", ctypes.c_int * 4), ("mid", ctypes.c_int * 4),
                 ("act", ctypes.c_int), ("first_orient", ctypes.c_int),
-                ("n_heads", ctypes.c_int), ("head_classes", ctypes.c_int * 4)]
+                ("n_heads", ctypes.c_int), ("head_classes", ctypes.c_int * 4),
+                ("enc_c1", ctypes.c_int), ("enc_mid", ctypes.c_int)]
 
 
 def to_orarch(arch) -> OrArch:
@@ -46,6 +47,8 @@ def to_orarch(arch) -> OrArch:
     a.n_heads = len(arch.heads)
     for i, c in enumerate(arch.heads):
         a.head_classes[i] = c
+    if arch.encoder:
+        a.enc_c1, a.enc_mid = arch.encoder
     return a
 
 
@@ -65,7 +68,8 @@ def lib():
         L.oracle_mean.argtypes = [ctypes.c_int, ctypes.c_long, ctypes.c_long, P, P]
         L.oracle_decode.argtypes = [ctypes.c_int, ctypes.c_long, ctypes.c_long, P, P, P, P]
         L.oracle_classify.argtypes = [P, P, ctypes.c_int, ctypes.c_long, P, P, P]
-        L.oracle_serve_group.argtypes = [P, P, ctypes.c_int, ctypes.c_long, P, P] + [P] * 9 + [ctypes.c_int]
+        L.oracle_serve_group.argtypes = [P, P, ctypes.c_int, ctypes.c_long, P, P] + [P] * 9 + [ctypes.c_int, ctypes.c_int]
+        L.oracle_encode_learned.argtypes = [P, P, ctypes.c_int, ctypes.c_long, P, P, ctypes.c_int]
         _lib = L
     return _lib
 
@@ -163,8 +167,19 @@ def classify(arch, params, head, z):
     return logits, labels
 
 
-def serve_group(arch, params, x, drop, nthreads=None):
-    """Whole coded path (exact encode).  x [B, k, C, H, W] fp32, drop [B] int32.
+def encode_learned(arch, params, x, nthreads=None):
+    """Learned encoder (Arch E): x [B, k, C, H, W] -> x_p [B, C, H, W] (f64)."""
+    x = _f64(x)
+    B, k = x.shape[:2]
+    a, p = to_orarch(arch), _f32(params)
+    out = np.empty((B, arch.in_c, arch.in_h, arch.in_w))
+    lib().oracle_encode_learned(ctypes.byref(a), _p(p), k, B, _p(x), _p(out), nthreads or default_threads())
+    return out
+
+
+def serve_group(arch, params, x, drop, nthreads=None, learned=False):
+    """Whole coded path (exact encode, or the learned encoder when learned=True).
+    x [B, k, C, H, W] fp32, drop [B] int32.
 
     Returns dict of f64 arrays: H, m, xp, P, R, logits[t], labels[t],
     logits_n[t], labels_n[t]  (t over heads)."""
@@ -182,7 +197,7 @@ def serve_group(arch, params, x, drop, nthreads=None):
     labels_n = np.empty(max(n * len(arch.heads), 1), np.int32)
     lib().oracle_serve_group(ctypes.byref(a), _p(p), k, B, _p(x), _p(drop), _p(H), _p(m), _p(xp), _p(P),
                              _p(R), _p(logits), _p(labels), _p(logits_n), _p(labels_n),
-                             nthreads or default_threads())
+                             nthreads or default_threads(), 1 if learned else 0)
     out = dict(H=H, m=m, xp=xp, P=P, R=R, logits=[], labels=[], logits_n=[], labels_n=[])
     lo = 0
     for t, C in enumerate(arch.heads):

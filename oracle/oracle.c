@@ -29,6 +29,12 @@
  *                           934-936 App. C)
  *   classify .............. linear heads g_t(z) = W_t z + b_t, label = first argmax
  *
+ *   learned encode ........ light encoder with a weight-shared first layer on each of the k
+ *                           inputs, averaged after that layer (reading
+ *                           Q13), then a small U-Net-style tail:
+ *                             e_i = ReLU(conv(E1, x_i)); m = (1/k) sum_i e_i; z = psi(m);
+ *                             z = ReLU(conv(E2, z)); z = ReLU(conv(E3, z));
+ *                             u = psi^-1(z) + m; x_p = conv(E4, u)     (SURVEY §8a Arch E)
  *
  * Parity pins: see tests/test_oracle_pins.py (every function here is pinned; none
  * is "parity unpinned").
@@ -49,6 +55,7 @@ typedef struct {
     int first_orient; /* 0: block 0 updates s_B, 1: block 0 updates s_A */
     int n_heads;
     int head_classes[4];
+    int enc_c1, enc_mid; /* learned encoder widths; 0 = no encoder */
 } or_arch_t;
 
 /* ------------------------------------------------------------------------ */
@@ -333,6 +340,78 @@ void oracle_classify(const or_arch_t* a, const float* params, int head, long n, 
     }
 }
 
+static long encoder_offset(const or_arch_t* a) {
+    long off = head_offset(a, a->n_heads);
+    return off;
+}
+
+/* Learned encoder on one group: x [k][in_c][H][W] (f64) -> xp [in_c][H][W] */
+static void encode_one(const or_arch_t* a, const float* params, int k, const double* x, double* xp) {
+    const int ci = a->in_c, H = a->in_h, W = a->in_w, c1 = a->enc_c1, mid = a->enc_mid;
+    const long HW = (long)H * W, hw4 = HW / 4;
+    const float* E1W = params + encoder_offset(a);
+    const float* E1b = E1W + (long)c1 * ci * 9;
+    const float* E2W = E1b + c1;
+    const float* E2b = E2W + (long)mid * 4 * c1 * 9;
+    const float* E3W = E2b + mid;
+    const float* E3b = E3W + (long)4 * c1 * mid * 9;
+    const float* E4W = E3b + 4 * c1;
+    const float* E4b = E4W + (long)ci * c1 * 9;
+    double* e = (double*)malloc(sizeof(double) * c1 * HW);
+    double* m = (double*)calloc((size_t)c1 * HW, sizeof(double));
+    double* z = (double*)malloc(sizeof(double) * 4 * c1 * hw4);
+    double* z2 = (double*)malloc(sizeof(double) * (mid > 4 * c1 ? mid : 4 * c1) * hw4);
+    double* u = (double*)malloc(sizeof(double) * c1 * HW);
+    for (int i = 0; i < k; i++) {                       /* weight-shared first layer */
+        oracle_conv3x3(x + (long)i * ci * HW, ci, H, W, E1W, E1b, c1, e);
+        for (long q = 0; q < c1 * HW; q++) m[q] += e[q] > 0.0 ? e[q] : 0.0;
+    }
+    for (long q = 0; q < c1 * HW; q++) m[q] /= (double)k; /* average after the first layer */
+    oracle_psi(m, c1, H, W, z);                          /* [4c1][H/2][W/2] */
+    oracle_conv3x3(z, 4 * c1, H / 2, W / 2, E2W, E2b, mid, z2);
+    for (long q = 0; q < mid * hw4; q++) z2[q] = z2[q] > 0.0 ? z2[q] : 0.0;
+    oracle_conv3x3(z2, mid, H / 2, W / 2, E3W, E3b, 4 * c1, z);
+    for (long q = 0; q < 4 * c1 * hw4; q++) z[q] = z[q] > 0.0 ? z[q] : 0.0;
+    oracle_psi_inv(z, 4 * c1, H / 2, W / 2, u);          /* [c1][H][W] */
+    for (long q = 0; q < c1 * HW; q++) u[q] += m[q];    /* skip connection */
+    oracle_conv3x3(u, c1, H, W, E4W, E4b, ci, xp);
+    free(e); free(m); free(z); free(z2); free(u);
+}
+
+typedef struct {
+    const or_arch_t* a;
+    const float* params;
+    int k;
+    const double* x;
+    double* xp;
+    long lo, hi;
+} enc_job_t;
+
+static void* run_enc(void* p) {
+    enc_job_t* j = (enc_job_t*)p;
+    long din = (long)j->a->in_c * j->a->in_h * j->a->in_w;
+    for (long b = j->lo; b < j->hi; b++) encode_one(j->a, j->params, j->k, j->x + b * j->k * din, j->xp + b * din);
+    return NULL;
+}
+
+/* Learned encode of B groups: x [B][k][in_c][H][W] (f64) -> x_parity [B][in_c][H][W] */
+int oracle_encode_learned(const or_arch_t* a, const float* params, int k, long B, const double* x,
+                          double* xp, int nthreads) {
+    if (a->enc_c1 <= 0) return -1;
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > B) nthreads = (int)(B > 0 ? B : 1);
+    if (nthreads > 256) nthreads = 256;
+    pthread_t th[256];
+    enc_job_t jobs[256];
+    for (int t = 0; t < nthreads; t++) {
+        jobs[t].a = a; jobs[t].params = params; jobs[t].k = k; jobs[t].x = x; jobs[t].xp = xp;
+        jobs[t].lo = B * t / nthreads; jobs[t].hi = B * (t + 1) / nthreads;
+        pthread_create(&th[t], NULL, run_enc, &jobs[t]);
+    }
+    for (int t = 0; t < nthreads; t++) pthread_join(th[t], NULL);
+    return 0;
+}
+
 /* Whole coded path for B groups of k queries (exact encode, n = k + 1):
  *   H  = h(x)                         [B][k][d]
  *   m  = mean_i H                     [B][d]
@@ -345,15 +424,16 @@ void oracle_classify(const or_arch_t* a, const float* params, int head, long n, 
 int oracle_serve_group(const or_arch_t* a, const float* params, int k, long B, const float* x,
                        const int* drop, double* Hf, double* m, double* xp, double* P, double* R,
                        double* logits, int* labels, double* logits_n, int* labels_n,
-                       int nthreads) {
+                       int nthreads, int learned) {
     long din = (long)a->in_c * a->in_h * a->in_w, d = oracle_d(a);
     long n = B * k;
     double* xd = (double*)malloc(sizeof(double) * n * din);
     for (long i = 0; i < n * din; i++) xd[i] = (double)x[i];
     oracle_forward_h(a, params, n, xd, Hf, nthreads);
-    free(xd);
     oracle_mean(k, B, d, Hf, m);
-    oracle_inverse_h(a, params, B, m, xp, nthreads);
+    if (learned) oracle_encode_learned(a, params, k, B, xd, xp, nthreads);  /* Enc(x_1..x_k) */
+    else oracle_inverse_h(a, params, B, m, xp, nthreads);                   /* h^-1(mean h) */
+    free(xd);
     oracle_forward_h(a, params, B, xp, P, nthreads);
     oracle_decode(k, B, d, Hf, P, drop, R);
     long lo = 0, lab = 0;

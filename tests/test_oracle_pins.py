@@ -290,3 +290,58 @@ def test_group_assignment_and_drops():
     assert np.all(np.abs(counts - 10000) < 500)   # uniform one-of-k
     # counter-based: element b depends only on (seed, b)
     assert np.array_equal(fx.make_drops(50, 10, 103), drops[:50])
+
+
+# ---------------------------------------------------------------- learned encoder (a3', C4)
+def torch_encoder(arch, params, x):
+    """Independent f64 composition of Arch E from torch library ops."""
+    p = {k: torch.from_numpy(v.astype(np.float64)) for k, v in fx.split_params(arch, params).items()}
+    xt = torch.from_numpy(np.asarray(x, np.float64))           # [B, k, C, H, W]
+    B, k = xt.shape[:2]
+    e = torch.relu(Fnn.conv2d(xt.reshape(B * k, *xt.shape[2:]), p["E1.W"], p["E1.b"], padding=1))
+    m = e.reshape(B, k, *e.shape[1:]).mean(1)
+    z = Fnn.pixel_unshuffle(m, 2)
+    z = torch.relu(Fnn.conv2d(z, p["E2.W"], p["E2.b"], padding=1))
+    z = torch.relu(Fnn.conv2d(z, p["E3.W"], p["E3.b"], padding=1))
+    u = Fnn.pixel_shuffle(z, 2) + m
+    return Fnn.conv2d(u, p["E4.W"], p["E4.b"], padding=1).numpy()
+
+
+@pytest.mark.parametrize("name,k", [("TE", 3), ("CE", 2)])
+def test_learned_encoder_matches_torch_composition(name, k):
+    arch = fx.ARCHS[name]
+    params = fx.make_weights(arch, 14)
+    x = fx.make_inputs(arch, 2, k, 4)
+    assert rel(oracle.encode_learned(arch, params, x), torch_encoder(arch, params, x)) < 1e-12
+
+
+def test_learned_encoder_permutation_and_copy_invariance():
+    """P14 (PAPER.md:411 'permutation invariance ... average after the first layer'):
+    permuting the k inputs leaves x_p unchanged; k copies of one image encode like k = 1."""
+    arch = fx.ARCH_TE
+    params = fx.make_weights(arch, 14)
+    x = fx.make_inputs(arch, 3, 5, 4)
+    xp = oracle.encode_learned(arch, params, x)
+    perm = np.array([3, 0, 4, 1, 2])
+    assert rel(oracle.encode_learned(arch, params, x[:, perm]), xp) < 1e-14
+    one = x[:, :1]
+    assert rel(oracle.encode_learned(arch, params, np.repeat(one, 4, axis=1)),
+               oracle.encode_learned(arch, params, one)) < 1e-14
+
+
+def test_serve_group_learned_decode_algebra():
+    """With the learned encoder the parity is only approximate, but the decode algebra still
+    gives f^(x_j) = k P - sum_{i != j} H_i exactly."""
+    arch = fx.ARCH_TE
+    params = fx.make_weights(arch, 14)
+    x = fx.make_inputs(arch, 4, 3, 4)
+    drop = fx.make_drops(4, 3, 104)
+    out = oracle.serve_group(arch, params, x, drop, learned=True)
+    assert rel(out["xp"], oracle.encode_learned(arch, params, x)) < 1e-15
+    assert rel(out["P"], oracle.forward_h(arch, params, out["xp"])) < 1e-15
+    bi = np.arange(4)
+    H = out["H"]
+    mask = np.ones((4, 3), bool); mask[bi, drop] = False
+    ref = 3 * out["P"] - (H * mask[..., None]).sum(1)
+    assert rel(out["R"][bi, drop], ref) < 1e-13
+    assert len(out["logits"]) == 2 and out["logits"][1].shape == (4, 3, 2)
