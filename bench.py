@@ -96,7 +96,7 @@ class ClockSampler:
 def oracle_sample(cfg, params, x, drop, groups):
     import oracle
     t0 = time.perf_counter()
-    ref = oracle.serve_group(cfg.arch, params, x[groups], drop[groups])
+    ref = oracle.serve_group(cfg.arch, params, x[groups], drop[groups], learned=bool(cfg.arch.encoder))
     dt = time.perf_counter() - t0
     return ref, dt
 
@@ -112,12 +112,13 @@ def run_reference(args, rank, world):
     x = fx.make_inputs(cfg.arch, S, cfg.k, cfg.seed_x)
     drop = fx.make_drops(S, cfg.k, cfg.seed_drop)
     oracle.build()
+    learned = bool(cfg.arch.encoder)
     for _ in range(args.warmup):
-        oracle.serve_group(cfg.arch, params, x, drop)
+        oracle.serve_group(cfg.arch, params, x, drop, learned=learned)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        oracle.serve_group(cfg.arch, params, x, drop)
+        oracle.serve_group(cfg.arch, params, x, drop, learned=learned)
         times.append(time.perf_counter() - t0)
     total = sum(times)
     value = S * args.steps / total
@@ -147,7 +148,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32", "simt"])
-    ap.add_argument("--config", default="C3", choices=["C3", "C2", "C1"])
+    ap.add_argument("--config", default="C3", choices=["C3", "C4", "C2", "C1"])
     ap.add_argument("--ref-groups", type=int, default=8, help="oracle sample groups per step")
     ap.add_argument("--cpu-groups", type=int, default=8, help="oracle sample for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -172,6 +173,7 @@ def main():
     cfg = fx.CONFIGS[args.config]
     arch, k, B = cfg.arch, cfg.k, cfg.B
     d, din = arch.d, arch.in_c * arch.in_h * arch.in_w
+    learned = bool(arch.encoder)
     params = fx.make_weights(arch, cfg.seed_w)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
@@ -194,7 +196,7 @@ def main():
         ws = model.workspace(k, B)
         for i in range(warmup):
             j = i % NBUF
-            model.ci_serve_group(xs[j], drops[j], hs[j], ps[j], ws, logits=lg[j], labels=lb[j])
+            model.ci_serve_group(xs[j], drops[j], hs[j], ps[j], ws, logits=lg[j], labels=lb[j], learned=learned)
         torch.cuda.synchronize()
         ci.ci_test_prof_read()
         ci.ci_test_launch_count(reset=True)
@@ -210,7 +212,7 @@ def main():
         e0.record(stream)
         for i in range(steps):
             j = i % NBUF
-            model.ci_serve_group(xs[j], drops[j], hs[j], ps[j], ws, logits=lg[j], labels=lb[j])
+            model.ci_serve_group(xs[j], drops[j], hs[j], ps[j], ws, logits=lg[j], labels=lb[j], learned=learned)
         e1.record(stream)
         torch.cuda.synchronize()
         if dist:
@@ -308,14 +310,14 @@ def main():
         lbh = torch.empty(B * k * len(arch.heads), dtype=torch.int32).pin_memory()
         args_h = (xh.numpy(), dh.numpy(), hh.numpy(), ph.numpy(), lgh.numpy(), lbh.numpy())
         for _ in range(2):
-            model.ci_serve_group_host(*args_h, wsh)
+            model.ci_serve_group_host(*args_h, wsh, learned=learned)
         if dist:
             dist.barrier()
         e_steps = max(3, min(args.steps, 10))
         a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a_.record(stream)
         for _ in range(e_steps):
-            model.ci_serve_group_host(*args_h, wsh)
+            model.ci_serve_group_host(*args_h, wsh, learned=learned)
         b_.record(stream)
         torch.cuda.synchronize()
         ems = a_.elapsed_time(b_)
@@ -329,6 +331,31 @@ def main():
                "steps": e_steps, "note": "ci_serve_group_host: pinned H2D of x+drop, D2H of h_out, "
                                          "h_parity, logits, labels inside the device-timed region"}
         del wsh
+
+    # --- encoding overhead vs k (Figs. 6-7 analogue): encoder time / time of
+    #     h on the k main queries, batch of 1024 groups, learned encoder only
+    enc_over = None
+    if learned and rank == 0:
+        model = main_run["model"]
+        enc_over = {}
+        for kk in (2, 4, 10):
+            xk = torch.from_numpy(fx.make_inputs_slice(arch, 0, B, kk, cfg.seed_x)).to(dev)
+            wsk = model.workspace(kk, B)
+            hk = torch.empty(B * kk, d, device=dev)
+            xpk = torch.empty(B, arch.in_c, arch.in_h, arch.in_w, device=dev)
+            def timed(fn, reps=5):
+                fn(); torch.cuda.synchronize()
+                a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a_.record(stream)
+                for _ in range(reps):
+                    fn()
+                b_.record(stream)
+                torch.cuda.synchronize()
+                return a_.elapsed_time(b_) / reps
+            t_enc = timed(lambda: model.ci_encode(None, xpk, wsk, x=xk, learned=True))
+            t_h = timed(lambda: model.ci_forward_h(xk.reshape(B * kk, arch.in_c, arch.in_h, arch.in_w), hk, wsk))
+            enc_over[str(kk)] = {"encoder_ms": t_enc, "h_ms": t_h, "overhead": t_enc / t_h}
+            del xk, wsk, hk, xpk
 
     # --- other precision (throughput line item, same workload)
     alt = None
@@ -347,7 +374,7 @@ def main():
         dr0 = drops[0].cpu().numpy()
         model = main_run["model"]
         ws = main_run["ws"]
-        model.ci_serve_group(xs[0], drops[0], hs[0], ps[0], ws, logits=lg[0], labels=lb[0])
+        model.ci_serve_group(xs[0], drops[0], hs[0], ps[0], ws, logits=lg[0], labels=lb[0], learned=learned)
         torch.cuda.synchronize()
         rng = np.random.default_rng(2106)
         S = args.cpu_groups
@@ -359,7 +386,7 @@ def main():
                          f"oracle, pthreads over images), wall {dt:.1f} s"}
         R = hs[0].cpu().numpy()[groups]
         P = ps[0].cpu().numpy()[groups]
-        L = lg[0].cpu().numpy()[:B * k * 10].reshape(B, k, 10)[groups]
+        L = lg[0].cpu().numpy()[:B * k * arch.heads[0]].reshape(B, k, arch.heads[0])[groups]
         lab = lb[0].cpu().numpy()[:B * k].reshape(B, k)[groups]
         bi = np.arange(S)
         numerics = {"groups_checked": S, "precision": args.precision,
@@ -387,6 +414,9 @@ def main():
                 "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": main_run["launches"], "clocks": main_run["clocks"],
                 "numerics": numerics, "alt_precision": alt}
+        if enc_over is not None:
+            line["encoder_overhead"] = enc_over
+            line["config"]["encode"] = "learned encoder (Arch E), heads 10 + 2"
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()

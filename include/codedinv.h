@@ -71,7 +71,10 @@ typedef enum {
     CI_PREC_SIMT = 2
 } ci_precision_t;
 
-typedef enum { CI_ENC_EXACT = 0 } ci_encode_mode_t;
+typedef enum {
+    CI_ENC_EXACT = 0,   /* x_p = h^-1((1/k) sum_i h(x_i))  (ideal encoder)       */
+    CI_ENC_LEARNED = 1  /* x_p = Enc(x_1..x_k), the light learned encoder */
+} ci_encode_mode_t;
 
 typedef struct {
     int32_t squeeze_before; /* 1: psi (space-to-depth r=2) before this stage's blocks */
@@ -87,6 +90,10 @@ typedef struct {
     int32_t first_orientation;/* 0: block 0 of each stage does s_B += F(s_A); 1: s_A += F(s_B) */
     int32_t n_heads;          /* 0..4 linear heads g_t */
     int32_t head_classes[4];
+    /* light learned encoder (0 = none): e_i = ReLU(E1 x_i) (in_c -> enc_c1), mean over the k
+     * inputs, psi, ReLU(E2) (4 enc_c1 -> enc_mid), ReLU(E3) (enc_mid -> 4 enc_c1), psi^-1,
+     * + skip(mean), E4 (enc_c1 -> in_c); all conv3x3 with bias */
+    int32_t enc_c1, enc_mid;
 } ci_arch_t;
 
 /* Thread-local description of the last non-OK status (never NULL). */
@@ -103,7 +110,8 @@ CI_API void ci_model_destroy(ci_model_t* model);
 
 CI_API int64_t ci_feature_dim(const ci_model_t* model); /* d; -1 if model == NULL */
 
-/* Bytes of workspace needed by any call with up to B groups of k (or n = B * k images). */
+/* Bytes of workspace needed by any call with up to B groups of k (or n = B * k images; a plain
+ * ci_forward_h / ci_inverse_h on n images needs no more than ci_workspace_size(model, 1, n)). */
 CI_API ci_status_t ci_workspace_size(const ci_model_t* model, int32_t k, int64_t B, size_t* bytes);
 
 /* Synchronise `stream` and report device-side flags recorded in `ws` (drop index out of
@@ -121,12 +129,17 @@ CI_API ci_status_t ci_forward_h(const ci_model_t* model, const float* x, float* 
 CI_API ci_status_t ci_inverse_h(const ci_model_t* model, const float* h, float* x, int64_t n, void* ws,
                          size_t ws_bytes, ci_stream_t stream);
 
-/* Exact encode of B groups: m_b = (1/k) sum_{i<k} h[b][i] (fp32 sum in ascending i, then /k),
- * x_parity[b] = h^-1(m_b).  h [B][k][d]; x_parity [B][in_c][in_h][in_w]; mean_out [B][d] or
- * NULL.  (PAPER.md:125-127 Enc(x1,x2) = f^-1((f(x1)+f(x2))/2); :241 c_{1,j} = 1/k) */
+/* Encode B groups into their parity queries x_parity [B][in_c][in_h][in_w]:
+ *   CI_ENC_EXACT:   h [B][k][d] -> m_b = (1/k) sum_{i<k} h[b][i] (fp32 sum in ascending i, then
+ *                   /k), x_parity[b] = h^-1(m_b); mean_out [B][d] or NULL; x unused (may be NULL).
+ *                   (PAPER.md:125-127 Enc(x1,x2) = f^-1((f(x1)+f(x2))/2); :241 c_{1,j} = 1/k)
+ *   CI_ENC_LEARNED: x [B][k][in_c][in_h][in_w] -> x_parity = Enc(x_b1..x_bk) (model must have an
+ *                   encoder, else CI_ERR_UNSUPPORTED); h and mean_out unused (may be NULL).
+ *                   (PAPER.md:143-152 approximate encoder; weight-shared first layer + average,
+ *                   PAPER.md:411) */
 CI_API ci_status_t ci_encode(const ci_model_t* model, ci_encode_mode_t mode, int32_t k, int64_t B,
-                      const float* h, float* x_parity, float* mean_out, void* ws, size_t ws_bytes,
-                      ci_stream_t stream);
+                      const float* x, const float* h, float* x_parity, float* mean_out, void* ws,
+                      size_t ws_bytes, ci_stream_t stream);
 
 /* In-place decode of B groups: for each b with j = drop[b] in [0,k):
  *   h[b][j] = k * h_parity[b] - sum_{i != j, ascending} h[b][i]
@@ -141,7 +154,8 @@ CI_API ci_status_t ci_decode(int32_t k, int64_t B, int64_t d, float* h, const fl
 CI_API ci_status_t ci_classify(const ci_model_t* model, int32_t head, const float* z, int64_t n,
                         float* logits, int32_t* labels, ci_stream_t stream);
 
-/* The whole coded path for B groups (steps 1-5 above) on one GPU:
+/* The whole coded path for B groups (steps 1-5 above) on one GPU, with the parity query from
+ * `mode` (CI_ENC_LEARNED skips h^-1 and runs the learned encoder on x):
  *   x [B][k][in_c][in_h][in_w], drop [B]
  *   h_out [B][k][d]     : h(x), with slot drop[b] replaced by its decoded estimate
  *   h_parity [B][d]     : h(x_p)

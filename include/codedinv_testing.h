@@ -28,7 +28,8 @@ CI_API ci_status_t ci_test_umma_gemm(const uint16_t* A, int32_t RA, int32_t KA, 
 
 /* `nblocks` CTAs each issue `iters` back-to-back 128 x N x 16 bf16 MMAs from shared memory
  * (SS mode) and record the issue-to-completion SM cycles in cycles[nblocks] (int64).
- * N's upper bits select a variant: bits 16..23 = number of accumulators cycled (default 2),
+ * Plain N runs the reference tight issue loop (1 MMA per iteration, 2 accumulators).
+ * N's upper bits select a variant: bits 16..23 = number of accumulators cycled,
  * bits 24..31 = variant flags (1 packed accumulators, 2 LBO=16 A pairs, 4 spinning warps,
  * 8 moving B, 16 periodic commits). */
 CI_API ci_status_t ci_test_umma_rate(int32_t N, int32_t iters, int32_t nblocks, int64_t* cycles,

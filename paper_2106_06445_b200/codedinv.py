@@ -23,7 +23,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 CI_OK, CI_ERR_INVALID_ARG, CI_ERR_INVALID_SHAPE, CI_ERR_DIM_MISMATCH, CI_ERR_UNSUPPORTED, \
     CI_ERR_WORKSPACE, CI_ERR_CUDA = range(7)
 CI_PREC_FP32, CI_PREC_BF16, CI_PREC_SIMT = 0, 1, 2
-CI_ENC_EXACT = 0
+CI_ENC_EXACT, CI_ENC_LEARNED = 0, 1
 PRECISIONS = {"fp32": CI_PREC_FP32, "bf16": CI_PREC_BF16, "simt": CI_PREC_SIMT}
 
 EXPORTS = ["ci_last_error", "ci_model_create", "ci_model_destroy", "ci_feature_dim",
@@ -43,7 +43,7 @@ class CiArch(ctypes.Structure):
     _fields_ = [("in_c", ctypes.c_int32), ("in_h", ctypes.c_int32), ("in_w", ctypes.c_int32),
                 ("n_stages", ctypes.c_int32), ("stage", CiStage * 4), ("act", ctypes.c_int32),
                 ("first_orientation", ctypes.c_int32), ("n_heads", ctypes.c_int32),
-                ("head_classes", ctypes.c_int32 * 4)]
+                ("head_classes", ctypes.c_int32 * 4), ("enc_c1", ctypes.c_int32), ("enc_mid", ctypes.c_int32)]
 
 
 _P, _I32, _I64, _SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
@@ -56,7 +56,7 @@ _sig = {
     "ci_check": (_I32, [_P, _P, _SZ, _P]),
     "ci_forward_h": (_I32, [_P, _P, _P, _I64, _P, _SZ, _P]),
     "ci_inverse_h": (_I32, [_P, _P, _P, _I64, _P, _SZ, _P]),
-    "ci_encode": (_I32, [_P, _I32, _I32, _I64, _P, _P, _P, _P, _SZ, _P]),
+    "ci_encode": (_I32, [_P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
     "ci_decode": (_I32, [_I32, _I64, _I64, _P, _P, _P, _P, _SZ, _P]),
     "ci_classify": (_I32, [_P, _I32, _P, _I64, _P, _P, _P]),
     "ci_serve_group": (_I32, [_P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
@@ -113,6 +113,8 @@ def to_ci_arch(arch) -> CiArch:
     a.n_heads = len(arch.heads)
     for i, c in enumerate(arch.heads):
         a.head_classes[i] = c
+    if getattr(arch, "encoder", ()):
+        a.enc_c1, a.enc_mid = arch.encoder
     return a
 
 
@@ -162,25 +164,27 @@ class Model:
         _check(_lib.ci_inverse_h(self._h, _ptr(h), _ptr(x), h.shape[0], _ptr(ws), ws.numel(),
                                  _stream(stream)), "ci_inverse_h")
 
-    def ci_encode(self, h, x_parity, ws, mean_out=None, stream=None):
-        B, k = h.shape[0], h.shape[1]
-        _check(_lib.ci_encode(self._h, CI_ENC_EXACT, k, B, _ptr(h), _ptr(x_parity), _ptr(mean_out),
-                              _ptr(ws), ws.numel(), _stream(stream)), "ci_encode")
+    def ci_encode(self, h, x_parity, ws, mean_out=None, stream=None, x=None, learned=False):
+        """Exact mode: h [B, k, d].  Learned mode (learned=True): x [B, k, C, H, W]."""
+        src = x if learned else h
+        B, k = src.shape[0], src.shape[1]
+        _check(_lib.ci_encode(self._h, CI_ENC_LEARNED if learned else CI_ENC_EXACT, k, B, _ptr(x), _ptr(h),
+                              _ptr(x_parity), _ptr(mean_out), _ptr(ws), ws.numel(), _stream(stream)), "ci_encode")
 
     def ci_classify(self, head, z, logits, labels=None, stream=None):
         _check(_lib.ci_classify(self._h, head, _ptr(z), z.shape[0], _ptr(logits), _ptr(labels),
                                 _stream(stream)), "ci_classify")
 
     def ci_serve_group(self, x, drop, h_out, h_parity, ws, x_parity=None, logits=None, labels=None,
-                       stream=None):
+                       stream=None, learned=False):
         B, k = x.shape[0], x.shape[1]
-        _check(_lib.ci_serve_group(self._h, CI_ENC_EXACT, k, B, _ptr(x), _ptr(drop), _ptr(h_out),
+        _check(_lib.ci_serve_group(self._h, CI_ENC_LEARNED if learned else CI_ENC_EXACT, k, B, _ptr(x), _ptr(drop), _ptr(h_out),
                                    _ptr(h_parity), _ptr(x_parity), _ptr(logits), _ptr(labels),
                                    _ptr(ws), ws.numel(), _stream(stream)), "ci_serve_group")
 
-    def ci_serve_group_host(self, x, drop, h_out, h_parity, logits, labels, ws, stream=None):
+    def ci_serve_group_host(self, x, drop, h_out, h_parity, logits, labels, ws, stream=None, learned=False):
         B, k = x.shape[0], x.shape[1]
-        _check(_lib.ci_serve_group_host(self._h, CI_ENC_EXACT, k, B, _ptr(x), _ptr(drop), _ptr(h_out),
+        _check(_lib.ci_serve_group_host(self._h, CI_ENC_LEARNED if learned else CI_ENC_EXACT, k, B, _ptr(x), _ptr(drop), _ptr(h_out),
                                         _ptr(h_parity), _ptr(logits), _ptr(labels), _ptr(ws), ws.numel(),
                                         _stream(stream)), "ci_serve_group_host")
 

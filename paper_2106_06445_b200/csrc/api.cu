@@ -37,22 +37,30 @@ static constexpr size_t kAlign = 256;
 static size_t up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct WsLayout {
-    size_t flag = 0, scratch = 0, mean = 0, xp = 0, hidden = 0, total = 0;
+    size_t flag = 0, scratch = 0, mean = 0, xp = 0, hidden = 0, enc = 0, total = 0;
 };
 
 static constexpr int64_t kSimtChunk = 1024;
 
-static WsLayout ws_layout(const Model* m, int32_t k, int64_t B) {
+// groups = false: layout of a plain h / h^-1 call on n = B*k images (no per-group buffers)
+static WsLayout ws_layout(const Model* m, int32_t k, int64_t B, bool groups = true) {
     WsLayout L;
     int64_t n = B * (int64_t)k;
+    const int64_t Bg = groups ? std::max<int64_t>(B, 1) : 0;
     size_t off = 0;
     L.flag = off; off += up(256);
     L.scratch = off; off += up(sizeof(float) * (size_t)(std::max<int64_t>(n, 1) * m->d));
-    L.mean = off; off += up(sizeof(float) * (size_t)(std::max<int64_t>(B, 1) * m->d));
-    L.xp = off; off += up(sizeof(float) * (size_t)(std::max<int64_t>(B, 1) * m->din));
+    L.mean = off; off += up(sizeof(float) * (size_t)(Bg * m->d));
+    L.xp = off; off += up(sizeof(float) * (size_t)(Bg * m->din));
     L.hidden = off;
     if (m->prec == CI_PREC_SIMT)
         off += up(sizeof(float) * (size_t)(std::min<int64_t>(std::max<int64_t>(n, 1), kSimtChunk) * m->max_hidden));
+    L.enc = off;
+    if (m->enc_off >= 0 && groups) {   // m, z, z2, z3, u of the learned encoder
+        const int64_t HW = (int64_t)m->arch.in_h * m->arch.in_w;
+        const int64_t per = HW * (4 * m->arch.enc_c1) + HW / 4 * m->arch.enc_mid + 64;
+        off += up(sizeof(float) * (size_t)(std::max<int64_t>(B, 1) * per));
+    }
     L.total = off;
     return L;
 }
@@ -131,6 +139,34 @@ static ci_status_t inverse_impl(const Model* m, const float* h, float* x, int64_
     return CI_OK;
 }
 
+static ci_status_t encode_learned_impl(const Model* m, const float* x, float* xp, int32_t k, int64_t B,
+                                       void* ws, const WsLayout& L, cudaStream_t st) {
+    if (B == 0) return CI_OK;
+    const ci_arch_t& a = m->arch;
+    const int Ci = a.in_c, H = a.in_h, W = a.in_w, c1 = a.enc_c1, mid = a.enc_mid;
+    const int64_t HW = (int64_t)H * W, hw4 = HW / 4;
+    const float* E1W = m->d_params + m->enc_off;
+    const float* E1b = E1W + (int64_t)c1 * Ci * 9;
+    const float* E2W = E1b + c1;
+    const float* E2b = E2W + (int64_t)mid * 4 * c1 * 9;
+    const float* E3W = E2b + mid;
+    const float* E3b = E3W + (int64_t)4 * c1 * mid * 9;
+    const float* E4W = E3b + 4 * c1;
+    const float* E4b = E4W + (int64_t)Ci * c1 * 9;
+    float* Mb = at<float>(ws, L.enc);
+    float* Z = Mb + B * c1 * HW;
+    float* Z2 = Z + B * 4 * c1 * hw4;
+    float* Z3 = Z2 + B * mid * hw4;
+    float* U = Z3 + B * 4 * c1 * hw4;
+    CI_CUDA(launch_enc_e1_mean(x, k, B, Ci, H, W, E1W, E1b, c1, Mb, st));
+    CI_CUDA(launch_permute(Mb, Z, B, c1, H, W, 1, st));
+    CI_CUDA(launch_conv_simt(Z, 4 * c1 * hw4, 4 * c1, H / 2, W / 2, E2W, E2b, mid, Z2, mid * hw4, B, 0, 0, st));
+    CI_CUDA(launch_conv_simt(Z2, mid * hw4, mid, H / 2, W / 2, E3W, E3b, 4 * c1, Z3, 4 * c1 * hw4, B, 0, 0, st));
+    CI_CUDA(launch_unsqueeze_add(Z3, Mb, U, B, c1, H, W, st));
+    CI_CUDA(launch_conv_simt(U, c1 * HW, c1, H, W, E4W, E4b, Ci, xp, Ci * HW, B, 0, 2, st));
+    return CI_OK;
+}
+
 }  // namespace ci
 
 using namespace ci;
@@ -191,6 +227,14 @@ ci_status_t ci_model_create(const ci_arch_t* arch, const float* host_params, siz
         }
         m->head_off[t] = off;
         off += (int64_t)a.head_classes[t] * m->d + a.head_classes[t];
+    }
+    if (a.enc_c1 > 0 || a.enc_mid > 0) {
+        if (a.enc_c1 < 1 || a.enc_mid < 1 || a.in_h % 2 || a.in_w % 2) {
+            delete m; set_error("invalid learned encoder widths"); return CI_ERR_INVALID_SHAPE;
+        }
+        m->enc_off = off;
+        off += (int64_t)a.enc_c1 * a.in_c * 9 + a.enc_c1 + (int64_t)a.enc_mid * 4 * a.enc_c1 * 9 + a.enc_mid +
+               (int64_t)4 * a.enc_c1 * a.enc_mid * 9 + 4 * a.enc_c1 + (int64_t)a.in_c * a.enc_c1 * 9 + a.in_c;
     }
     m->n_params = off;
     if ((size_t)off != n_params) {
@@ -274,7 +318,7 @@ ci_status_t ci_forward_h(const ci_model_t* model, const float* x, float* h, int6
     if (n < 0 || (n > 0 && (!x || !h || !aligned16(x) || !aligned16(h)))) {
         set_error("invalid x/h/n"); return CI_ERR_INVALID_ARG;
     }
-    WsLayout L = ws_layout(m, 1, n);
+    WsLayout L = ws_layout(m, 1, n, false);
     ci_status_t r = check_ws(L, ws, ws_bytes);
     if (r != CI_OK) return r;
     return forward_impl(m, x, h, n, ws, L, (cudaStream_t)stream);
@@ -286,18 +330,20 @@ ci_status_t ci_inverse_h(const ci_model_t* model, const float* h, float* x, int6
     if (n < 0 || (n > 0 && (!x || !h || !aligned16(x) || !aligned16(h)))) {
         set_error("invalid x/h/n"); return CI_ERR_INVALID_ARG;
     }
-    WsLayout L = ws_layout(m, 1, n);
+    WsLayout L = ws_layout(m, 1, n, false);
     ci_status_t r = check_ws(L, ws, ws_bytes);
     if (r != CI_OK) return r;
     return inverse_impl(m, h, x, n, ws, L, (cudaStream_t)stream);
 }
 
 ci_status_t ci_encode(const ci_model_t* model, ci_encode_mode_t mode, int32_t k, int64_t B,
-                      const float* h, float* x_parity, float* mean_out, void* ws, size_t ws_bytes,
+                      const float* x, const float* h, float* x_parity, float* mean_out, void* ws, size_t ws_bytes,
                       ci_stream_t stream) {
     CI_MODEL_OR_FAIL(m, model);
-    if (mode != CI_ENC_EXACT) { set_error("only CI_ENC_EXACT is built"); return CI_ERR_UNSUPPORTED; }
-    if (k < 1 || B < 0 || (B > 0 && (!h || !x_parity || !aligned16(h) || !aligned16(x_parity))) ||
+    if (mode != CI_ENC_EXACT && mode != CI_ENC_LEARNED) { set_error("unknown encode mode"); return CI_ERR_INVALID_ARG; }
+    if (mode == CI_ENC_LEARNED && m->enc_off < 0) { set_error("model has no learned encoder"); return CI_ERR_UNSUPPORTED; }
+    const float* in = mode == CI_ENC_EXACT ? h : x;
+    if (k < 1 || B < 0 || (B > 0 && (!in || !x_parity || !aligned16(in) || !aligned16(x_parity))) ||
         (mean_out && !aligned16(mean_out))) {
         set_error("invalid argument"); return CI_ERR_INVALID_ARG;
     }
@@ -305,6 +351,7 @@ ci_status_t ci_encode(const ci_model_t* model, ci_encode_mode_t mode, int32_t k,
     ci_status_t r = check_ws(L, ws, ws_bytes);
     if (r != CI_OK) return r;
     cudaStream_t st = (cudaStream_t)stream;
+    if (mode == CI_ENC_LEARNED) return encode_learned_impl(m, x, x_parity, k, B, ws, L, st);
     float* mean = mean_out ? mean_out : at<float>(ws, L.mean);
     CI_CUDA(launch_mean(h, mean, k, B, m->d, st));
     return inverse_impl(m, mean, x_parity, B, ws, L, st);
@@ -333,7 +380,7 @@ ci_status_t ci_classify(const ci_model_t* model, int32_t head, const float* z, i
     return CI_OK;
 }
 
-static ci_status_t serve_impl(const Model* m, int32_t k, int64_t B, const float* x,
+static ci_status_t serve_impl(const Model* m, ci_encode_mode_t mode, int32_t k, int64_t B, const float* x,
                               const int32_t* drop, float* h_out, float* h_parity, float* x_parity,
                               float* logits, int32_t* labels, void* ws, const WsLayout& L,
                               cudaStream_t st) {
@@ -342,8 +389,12 @@ static ci_status_t serve_impl(const Model* m, int32_t k, int64_t B, const float*
     if (r != CI_OK) return r;
     float* mean = at<float>(ws, L.mean);
     float* xp = x_parity ? x_parity : at<float>(ws, L.xp);
-    CI_CUDA(launch_mean(h_out, mean, k, B, m->d, st));                   // (2) encode: mean ...
-    r = inverse_impl(m, mean, xp, B, ws, L, st);                          //     ... then h^-1
+    if (mode == CI_ENC_LEARNED) {
+        r = encode_learned_impl(m, x, xp, k, B, ws, L, st);              // (2) learned encoder
+    } else {
+        CI_CUDA(launch_mean(h_out, mean, k, B, m->d, st));               // (2) encode: mean ...
+        r = inverse_impl(m, mean, xp, B, ws, L, st);                      //     ... then h^-1
+    }
     if (r != CI_OK) return r;
     r = forward_impl(m, xp, h_parity, B, ws, L, st);                      // (3) h on parity query
     if (r != CI_OK) return r;
@@ -366,7 +417,8 @@ ci_status_t ci_serve_group(const ci_model_t* model, ci_encode_mode_t mode, int32
                            float* x_parity, float* logits, int32_t* labels, void* ws,
                            size_t ws_bytes, ci_stream_t stream) {
     CI_MODEL_OR_FAIL(m, model);
-    if (mode != CI_ENC_EXACT) { set_error("only CI_ENC_EXACT is built"); return CI_ERR_UNSUPPORTED; }
+    if (mode != CI_ENC_EXACT && mode != CI_ENC_LEARNED) { set_error("unknown encode mode"); return CI_ERR_INVALID_ARG; }
+    if (mode == CI_ENC_LEARNED && m->enc_off < 0) { set_error("model has no learned encoder"); return CI_ERR_UNSUPPORTED; }
     if (k < 1 || B < 0) { set_error("k must be >= 1 and B >= 0"); return CI_ERR_INVALID_ARG; }
     if (B > 0 && (!x || !drop || !h_out || !h_parity || !aligned16(x) || !aligned16(h_out) ||
                   !aligned16(h_parity) || (x_parity && !aligned16(x_parity)))) {
@@ -376,7 +428,7 @@ ci_status_t ci_serve_group(const ci_model_t* model, ci_encode_mode_t mode, int32
     ci_status_t r = check_ws(L, ws, ws_bytes);
     if (r != CI_OK) return r;
     if (B == 0) return CI_OK;
-    return serve_impl(m, k, B, x, drop, h_out, h_parity, x_parity, logits, labels, ws, L,
+    return serve_impl(m, mode, k, B, x, drop, h_out, h_parity, x_parity, logits, labels, ws, L,
                       (cudaStream_t)stream);
 }
 
@@ -416,7 +468,8 @@ ci_status_t ci_serve_group_host(const ci_model_t* model, ci_encode_mode_t mode, 
                                 int32_t* labels_host, void* ws, size_t ws_bytes,
                                 ci_stream_t stream) {
     CI_MODEL_OR_FAIL(m, model);
-    if (mode != CI_ENC_EXACT) { set_error("only CI_ENC_EXACT is built"); return CI_ERR_UNSUPPORTED; }
+    if (mode != CI_ENC_EXACT && mode != CI_ENC_LEARNED) { set_error("unknown encode mode"); return CI_ERR_INVALID_ARG; }
+    if (mode == CI_ENC_LEARNED && m->enc_off < 0) { set_error("model has no learned encoder"); return CI_ERR_UNSUPPORTED; }
     if (k < 1 || B < 0 || (B > 0 && (!x_host || !drop_host))) { set_error("invalid argument"); return CI_ERR_INVALID_ARG; }
     HostLayout H = host_layout(m, k, B);
     if (!ws || !aligned16(ws) || ws_bytes < H.total) {
@@ -435,7 +488,7 @@ ci_status_t ci_serve_group_host(const ci_model_t* model, ci_encode_mode_t mode, 
     int32_t* dlab = at<int32_t>(ws, H.labels);
     CI_CUDA(cudaMemcpyAsync(dx, x_host, sizeof(float) * n * m->din, cudaMemcpyHostToDevice, st));
     CI_CUDA(cudaMemcpyAsync(ddrop, drop_host, sizeof(int32_t) * B, cudaMemcpyHostToDevice, st));
-    ci_status_t r = serve_impl(m, k, B, dx, ddrop, dh, dp, nullptr, dl, dlab, ws, H.dev, st);
+    ci_status_t r = serve_impl(m, mode, k, B, dx, ddrop, dh, dp, nullptr, dl, dlab, ws, H.dev, st);
     if (r != CI_OK) return r;
     if (h_out_host) CI_CUDA(cudaMemcpyAsync(h_out_host, dh, sizeof(float) * n * m->d, cudaMemcpyDeviceToHost, st));
     if (h_parity_host) CI_CUDA(cudaMemcpyAsync(h_parity_host, dp, sizeof(float) * B * m->d, cudaMemcpyDeviceToHost, st));

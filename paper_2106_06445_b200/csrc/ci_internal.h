@@ -45,6 +45,7 @@ struct Model {
     int64_t head_off[4] = {0, 0, 0, 0};
     float* d_head[4] = {nullptr, nullptr, nullptr, nullptr};  // 16-B aligned copy: W [C][d], then b [C]
     int64_t max_hidden = 0;                  // max m*H*W over stages (SIMT scratch)
+    int64_t enc_off = -1;                    // learned encoder params (float offset), -1 = none
     // tcgen05 path
     uint16_t* d_wpack = nullptr;             // packed bf16 weights (hi [+ lo])
     float* d_bias = nullptr;                 // padded biases
@@ -72,6 +73,10 @@ cudaError_t launch_decode(float* h, const float* p, const int32_t* drop, int k, 
 cudaError_t launch_classify(const float* z, int64_t n, int64_t d, const float* W, const float* b,
                             int C, float* logits, int32_t* labels, cudaStream_t s);
 cudaError_t launch_make_drops(int k, int64_t B, uint64_t seed, int32_t* drop, cudaStream_t s);
+cudaError_t launch_enc_e1_mean(const float* x, int k, int64_t B, int Ci, int H, int W, const float* W1,
+                               const float* b1, int C1, float* m, cudaStream_t s);
+cudaError_t launch_unsqueeze_add(const float* z, const float* m, float* u, int64_t B, int C, int H, int W,
+                                 cudaStream_t s);
 
 // tcgen05 path (k_umma.cu)
 ci_status_t umma_prepare(Model* m, const float* host_params);

@@ -148,6 +148,40 @@ __global__ void __launch_bounds__(128) k_umma_rate(int N, int iters, int ntile, 
     if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
+// The reference tight issue loop (profiles/r01_umma_probe.md): one elected thread, one MMA per
+// iteration, A start moved by (j & 63) rows, accumulators alternating 0 / 256.
+__global__ void __launch_bounds__(128) k_umma_rate_v1(int N, int iters, long long* __restrict__ cycles) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tmem_base;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int i = tid; i < (2 * 192 + 2 * 256) * 4; i += 128) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+    fence_proxy_async();
+    if (warp == 0) tmem_alloc(&tmem_base, 512);
+    if (tid == 0) { mbar_init(&bar, 1); fence_mbar_init(); }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = tmem_base;
+    if (warp == 0 && elect_one()) {
+        const uint32_t idesc = idesc_bf16(128, N);
+        const uint32_t a0 = smem_u32(smem), b0 = a0 + 2 * 192 * 16;
+        long long t0 = clock64();
+        for (int j = 0; j < iters; j++) {
+            uint64_t ad = smem_desc(a0 + (uint32_t)(j & 63) * 16, 192 * 16, 128);
+            uint64_t bd = smem_desc(b0, 256 * 16, 128);
+            mma_bf16(tmem + (uint32_t)((j & 1) * 256), ad, bd, idesc, 1);
+        }
+        commit(&bar);
+        mbar_wait(&bar, 0);
+        cycles[blockIdx.x] = clock64() - t0;
+    }
+    __syncwarp();
+    fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
 }  // namespace ci
 
 using namespace ci;
@@ -172,6 +206,14 @@ ci_status_t ci_test_umma_rate(int32_t N, int32_t iters, int32_t nblocks, int64_t
                               ci_stream_t stream) {
     int32_t ntile = (N >> 16) & 0xFF, variant = N >> 24;
     N &= 0xFFFF;
+    if (variant == 0 && ntile == 0) {   // the reference tight loop
+        if (N < 16 || N > 256 || N % 16 || iters < 1 || nblocks < 1) { set_error("bad probe shape"); return CI_ERR_INVALID_ARG; }
+        size_t sm = (2 * 192 + 2 * 256) * 16;
+        CI_CUDA(cudaFuncSetAttribute(k_umma_rate_v1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        k_umma_rate_v1<<<nblocks, 128, sm, (cudaStream_t)stream>>>(N, iters, (long long*)cycles);
+        CI_CHECK_LAUNCH("k_umma_rate_v1");
+        return CI_OK;
+    }
     if (ntile < 1) ntile = 2;
     if (N < 16 || N > 256 || N % 16 || iters < 1 || nblocks < 1 || ntile * N > 512) {
         set_error("bad probe shape");

@@ -133,7 +133,7 @@ def test_classify_vs_oracle_and_ties(ci):
 
 
 # ------------------------------------------------------------------ h, h^-1, serve
-def run_serve(ci, m, arch, x, drop, B, k):
+def run_serve(ci, m, arch, x, drop, B, k, learned=False):
     xt, dt = dev(x), dev(drop)
     h = torch.empty(B, k, arch.d, device="cuda")
     p = torch.empty(B, arch.d, device="cuda")
@@ -143,7 +143,7 @@ def run_serve(ci, m, arch, x, drop, B, k):
     labels = torch.empty(max(nh * B * k, 1), dtype=torch.int32, device="cuda")
     ws = m.workspace(k, B)
     m.ci_serve_group(xt, dt, h, p, ws, x_parity=xp, logits=logits if nh else None,
-                     labels=labels if nh else None)
+                     labels=labels if nh else None, learned=learned)
     m.ci_check(ws)
     return dict(R=h.cpu().numpy(), P=p.cpu().numpy(), xp=xp.cpu().numpy(),
                 logits=logits.cpu().numpy(), labels=labels.cpu().numpy())
@@ -299,3 +299,51 @@ def test_host_entry_point_matches_device(ci):
     m.ci_serve_group_host(x, drop, hh, hp, lg, lb, ws)
     assert np.array_equal(hh, g["R"]) and np.array_equal(hp, g["P"])
     assert np.array_equal(lb, g["labels"][:B * c.k])
+
+
+# ------------------------------------------------------------------ learned encoder (a3', C4)
+@pytest.mark.parametrize("prec", PRECS)
+def test_serve_learned_small_arch(ci, prec):
+    arch = fx.ARCH_TE
+    B, k = 6, 3
+    params, x, drop = fx.make_weights(arch, 14), fx.make_inputs(arch, B, k, 4), fx.make_drops(B, k, 104)
+    ref = oracle.serve_group(arch, params, x, drop, learned=True)
+    g = run_serve(ci, model(ci, arch, params, prec), arch, x, drop, B, k, learned=True)
+    assert relerr(g["xp"].reshape(B, -1), ref["xp"].reshape(B, -1)) < 1e-5   # fp32 CUDA-core encoder
+    check_against_oracle(g, ref, arch, B, k, prec, "TE-learned")
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_serve_c4_sampled(ci, prec):
+    """C4: Arch C + learned encoder + heads 10/2, B=1024 groups at the bench launch size;
+    3 seeded groups checked against the oracle."""
+    c = fx.CONFIGS["C4"]
+    params, x, drop = fx.make_weights(c.arch, c.seed_w), fx.make_inputs(c.arch, c.B, c.k, c.seed_x), \
+        fx.make_drops(c.B, c.k, c.seed_drop)
+    g = run_serve(ci, model(ci, c.arch, params, prec), c.arch, x, drop, c.B, c.k, learned=True)
+    sample = np.array([0, 511, 1023])
+    ref = oracle.serve_group(c.arch, params, x[sample], drop[sample], learned=True)
+    n = c.B * c.k
+    lg = g["logits"]
+    gs = dict(R=g["R"][sample], P=g["P"][sample], xp=g["xp"][sample])
+    gs["logits"] = np.concatenate([lg[:n * 10].reshape(c.B, c.k, 10)[sample].reshape(-1),
+                                   lg[n * 10:n * 12].reshape(c.B, c.k, 2)[sample].reshape(-1)])
+    gs["labels"] = np.concatenate([g["labels"][:n].reshape(c.B, c.k)[sample].reshape(-1),
+                                   g["labels"][n:2 * n].reshape(c.B, c.k)[sample].reshape(-1)])
+    check_against_oracle(gs, ref, c.arch, len(sample), c.k, prec, "C4")
+
+
+def test_encoder_permutation_invariance_gpu(ci):
+    """P14 on the GPU: permuting the k inputs of each group leaves x_p unchanged (fp32 sums of
+    the first-layer mean are reordered, so equality is to rounding)."""
+    arch = fx.ARCH_CE
+    params = fx.make_weights(arch, 14)
+    x = fx.make_inputs(arch, 4, 10, 4)
+    m = model(ci, arch, params, "bf16")
+    ws = m.workspace(10, 4)
+    xp1 = torch.empty(4, 3, 32, 32, device="cuda")
+    xp2 = torch.empty_like(xp1)
+    m.ci_encode(None, xp1, ws, x=dev(x), learned=True)
+    m.ci_encode(None, xp2, ws, x=dev(np.ascontiguousarray(x[:, ::-1])), learned=True)
+    torch.cuda.synchronize()
+    assert relerr(xp1.cpu().numpy().reshape(4, -1), xp2.cpu().numpy().reshape(4, -1)) < 1e-6
