@@ -58,7 +58,7 @@ static WsLayout ws_layout(const Model* m, int32_t k, int64_t B, bool groups = tr
     L.enc = off;
     if (m->enc_off >= 0 && groups) {   // m, z, z2, z3, u of the learned encoder
         const int64_t HW = (int64_t)m->arch.in_h * m->arch.in_w;
-        const int64_t per = HW * (4 * m->arch.enc_c1) + HW / 4 * m->arch.enc_mid + 64;
+        const int64_t per = HW * (4 * m->arch.enc_c1) + HW / 4 * m->arch.enc_mid + 64;   // m, zbuf, z2, u
         off += up(sizeof(float) * (size_t)(std::max<int64_t>(B, 1) * per));
     }
     L.total = off;
@@ -153,16 +153,22 @@ static ci_status_t encode_learned_impl(const Model* m, const float* x, float* xp
     const float* E3b = E3W + (int64_t)4 * c1 * mid * 9;
     const float* E4W = E3b + 4 * c1;
     const float* E4b = E4W + (int64_t)Ci * c1 * 9;
+    // workspace: m [B][c1][H][W] | zbuf [B][8c1][H/2][W/2] (tail in | out) | z2 [B][mid][..] | u
     float* Mb = at<float>(ws, L.enc);
-    float* Z = Mb + B * c1 * HW;
-    float* Z2 = Z + B * 4 * c1 * hw4;
-    float* Z3 = Z2 + B * mid * hw4;
-    float* U = Z3 + B * 4 * c1 * hw4;
-    CI_CUDA(launch_enc_e1_mean(x, k, B, Ci, H, W, E1W, E1b, c1, Mb, st));
-    CI_CUDA(launch_permute(Mb, Z, B, c1, H, W, 1, st));
-    CI_CUDA(launch_conv_simt(Z, 4 * c1 * hw4, 4 * c1, H / 2, W / 2, E2W, E2b, mid, Z2, mid * hw4, B, 0, 0, st));
-    CI_CUDA(launch_conv_simt(Z2, mid * hw4, mid, H / 2, W / 2, E3W, E3b, 4 * c1, Z3, 4 * c1 * hw4, B, 0, 0, st));
-    CI_CUDA(launch_unsqueeze_add(Z3, Mb, U, B, c1, H, W, st));
+    float* Zb = Mb + B * c1 * HW;
+    const int64_t zstride = 8 * c1 * hw4;
+    float* Z2 = Zb + B * zstride;
+    float* U = Z2 + B * mid * hw4;
+    CI_CUDA(launch_enc_e1_mean(x, k, B, Ci, H, W, E1W, E1b, c1, Mb, Zb, zstride, st));
+    if (m->umma) {
+        ci_status_t r = umma_encoder_tail(m, Zb, B, st);   // tcgen05: ReLU(E3(ReLU(E2 z)))
+        if (r != CI_OK) return r;
+    } else {
+        CI_CUDA(launch_conv_simt(Zb, zstride, 4 * c1, H / 2, W / 2, E2W, E2b, mid, Z2, mid * hw4, B, 0, 0, st));
+        CI_CUDA(launch_conv_simt(Z2, mid * hw4, mid, H / 2, W / 2, E3W, E3b, 4 * c1, Zb + 4 * c1 * hw4, zstride, B,
+                                 0, 0, st));
+    }
+    CI_CUDA(launch_unsqueeze_add(Zb + 4 * c1 * hw4, zstride, Mb, U, B, c1, H, W, st));
     CI_CUDA(launch_conv_simt(U, c1 * HW, c1, H, W, E4W, E4b, Ci, xp, Ci * HW, B, 0, 2, st));
     return CI_OK;
 }

@@ -74,9 +74,9 @@ cudaError_t launch_classify(const float* z, int64_t n, int64_t d, const float* W
                             int C, float* logits, int32_t* labels, cudaStream_t s);
 cudaError_t launch_make_drops(int k, int64_t B, uint64_t seed, int32_t* drop, cudaStream_t s);
 cudaError_t launch_enc_e1_mean(const float* x, int k, int64_t B, int Ci, int H, int W, const float* W1,
-                               const float* b1, int C1, float* m, cudaStream_t s);
-cudaError_t launch_unsqueeze_add(const float* z, const float* m, float* u, int64_t B, int C, int H, int W,
-                                 cudaStream_t s);
+                               const float* b1, int C1, float* m, float* zpsi, int64_t zstride, cudaStream_t s);
+cudaError_t launch_unsqueeze_add(const float* z, int64_t zstride, const float* m, float* u, int64_t B, int C,
+                                 int H, int W, cudaStream_t s);
 
 // tcgen05 path (k_umma.cu)
 ci_status_t umma_prepare(Model* m, const float* host_params);
@@ -84,5 +84,8 @@ void umma_release(Model* m);
 // Runs one stage (all blocks) on the fp32 NCHW state `state` [n][C][H][W] in place.
 ci_status_t umma_stage(const Model* m, int stage, float* state, int64_t n, bool inverse,
                        cudaStream_t s);
+// Learned-encoder tail: zbuf [n][2*4c1][H/2][W/2]; channels [0,4c1) = psi(mean first layer) in,
+// channels [4c1, 8c1) = ReLU(E3(ReLU(E2 z))) out (tcgen05 stage kernel, fmode 1).
+ci_status_t umma_encoder_tail(const Model* m, float* zbuf, int64_t n, cudaStream_t s);
 
 }  // namespace ci

@@ -71,6 +71,7 @@ struct StageArgs {
     const uint8_t* wpack;  // stage stream: block t at t * blk_bytes
     const float* bias;     // block t: [Mp] b1 then [Nc2] b2
     int C, nb, first_orient, act, inverse;
+    int fmode;                // 0: s_out (+|-)= F(s_in) (coupling); 1: s_out = ReLU(F(s_in)) (encoder tail)
     unsigned long long* dbg;  // optional per-CTA cycle counters (CI_DEBUG_CYCLES), 16 per CTA
     StagePlan p;
 };
@@ -669,8 +670,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                     float nv = 0.f;
                                     if (o < ec) {
                                         const float f = (left[o] + za[8 + o] + right[o]) + __ldg(b2 + o);
-                                        const float old = dst[(int64_t)o * eHW];
-                                        nv = a.inverse ? old - f : old + f;
+                                        const float old = a.fmode ? 0.f : dst[(int64_t)o * eHW];
+                                        nv = a.fmode ? fmaxf(f, 0.f) : (a.inverse ? old - f : old + f);
                                         dst[(int64_t)o * eHW] = nv;
                                     }
                                     n8[o] = nv;
@@ -690,7 +691,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
 #pragma unroll
                     for (int e = 0; e < OLDN; e++) {
                         const int o = cb2 + e;
-                        oldv[e] = (valid && e < cw2 && o < ec) ? src[(int64_t)o * eHW] : 0.f;
+                        oldv[e] = (valid && !a.fmode && e < cw2 && o < ec) ? src[(int64_t)o * eHW] : 0.f;
                     }
                 };
                 load_old(0);
@@ -730,7 +731,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 float nv = 0.f;
                                 if (o < ec) {
                                     const float f = acc + __ldg(b2 + o);
-                                    nv = a.inverse ? oldv[q8 * 8 + e] - f : oldv[q8 * 8 + e] + f;
+                                    nv = a.fmode ? fmaxf(f, 0.f) : (a.inverse ? oldv[q8 * 8 + e] - f : oldv[q8 * 8 + e] + f);
                                     dst[(int64_t)o * eHW] = nv;
                                 }
                                 n8[e] = nv;
@@ -954,6 +955,10 @@ struct UmmaState {
     StagePlan plan[4];
     int64_t wpack_off[4];  // bytes into d_wpack per stage
     int64_t bias_off[4];   // floats into d_bias per stage
+    // learned-encoder tail (E2 -> ReLU -> E3 -> ReLU) run as one "block" in fmode 1
+    int has_enc = 0;
+    StagePlan enc_plan;
+    int64_t enc_wpack_off = 0, enc_bias_off = 0;
 };
 
 // ---- compile-time specialisations for the Arch-C stage plans (see make_plan) -----------------
@@ -968,6 +973,8 @@ static const SpecEntry kSpecs[] = {
     CI_SPEC(17, 8, 16, 32, 7, 1, 16384, 16, 6, 0),   // C stage 1, bf16x3 (hst)
     CI_SPEC(9, 32, 128, 32, 2, 1, 16384, 8, 24, 0),  // C stage 2, bf16x3
     CI_SPEC(5, 96, 64, 96, 2, 1, 16384, 4, 96, 0),   // C stage 3, bf16x3
+    CI_SPEC(17, 64, 32, 64, 5, 0, 16384, 16, 64, 0),  // learned-encoder tail (E2, E3), bf16
+    CI_SPEC(17, 64, 32, 64, 3, 1, 16384, 16, 64, 0),  // learned-encoder tail (E2, E3), bf16x3
 };
 
 static StageKernel pick_kernel(const StagePlan& p) {
@@ -1020,6 +1027,25 @@ ci_status_t umma_prepare(Model* m, const float* host_params) {
             for (int i = 0; i < p.Nc2; i++) bias.push_back(i < S.c ? b2[i] : 0.f);
         }
     }
+    if (m->enc_off >= 0) {   // encoder tail: c = 4*c1 channels at H/2 x W/2, hidden = enc_mid
+        const ci_arch_t& a = m->arch;
+        StageInfo S{};
+        S.H = a.in_h / 2; S.W = a.in_w / 2; S.c = 4 * a.enc_c1; S.C = 2 * S.c; S.m = a.enc_mid; S.nb = 1;
+        if (make_plan(S, prec3, U->enc_plan)) {
+            const StagePlan& p = U->enc_plan;
+            while ((pack.size() * 2) % 128) pack.push_back(0);
+            U->enc_wpack_off = (int64_t)pack.size() * 2;
+            U->enc_bias_off = (int64_t)bias.size();
+            const float* E2W = host_params + m->enc_off + (size_t)a.enc_c1 * a.in_c * 9 + a.enc_c1;
+            const float* E2b = E2W + (size_t)a.enc_mid * 4 * a.enc_c1 * 9;
+            const float* E3W = E2b + a.enc_mid;
+            const float* E3b = E3W + (size_t)4 * a.enc_c1 * a.enc_mid * 9;
+            pack_block(p, E2W, E3W, prec3, pack);
+            for (int i = 0; i < p.Mp; i++) bias.push_back(i < S.m ? E2b[i] : 0.f);
+            for (int i = 0; i < p.Nc2; i++) bias.push_back(i < S.c ? E3b[i] : 0.f);
+            U->has_enc = 1;
+        }
+    }
     cudaError_t e = cudaMalloc(&m->d_wpack, pack.size() * 2);
     if (e == cudaSuccess) e = cudaMemcpy(m->d_wpack, pack.data(), pack.size() * 2, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&m->d_bias, std::max<size_t>(bias.size(), 1) * 4);
@@ -1066,6 +1092,31 @@ static void prof_end(cudaStream_t st, int stage, double flops) {
     g_prof_open = nullptr;
 }
 
+ci_status_t umma_encoder_tail(const Model* m, float* zbuf, int64_t n, cudaStream_t st) {
+    const UmmaState* U = reinterpret_cast<const UmmaState*>(m->umma_state);
+    if (!U || !U->has_enc) { set_error("no tcgen05 encoder plan"); return CI_ERR_UNSUPPORTED; }
+    if (n == 0) return CI_OK;
+    StageArgs a;
+    a.p = U->enc_plan;
+    a.state = zbuf;
+    a.n = n;
+    a.wpack = reinterpret_cast<const uint8_t*>(m->d_wpack) + U->enc_wpack_off;
+    a.bias = m->d_bias + U->enc_bias_off;
+    a.C = 2 * a.p.c;
+    a.nb = 1;
+    a.first_orient = 0;
+    a.act = 0;
+    a.inverse = 0;
+    a.fmode = 1;
+    a.dbg = nullptr;
+    int64_t nbatch = (n + a.p.I - 1) / a.p.I;
+    int grid = (int)std::min<int64_t>(nbatch, 148);
+    pick_kernel(a.p)<<<grid, kThreads, a.p.smem, st>>>(a);
+    count_launch();
+    CI_CHECK_LAUNCH("k_stage (encoder tail)");
+    return CI_OK;
+}
+
 ci_status_t umma_stage(const Model* m, int s, float* state, int64_t n, bool inverse, cudaStream_t st) {
     if (n == 0) return CI_OK;
     const UmmaState* U = reinterpret_cast<const UmmaState*>(m->umma_state);
@@ -1080,6 +1131,7 @@ ci_status_t umma_stage(const Model* m, int s, float* state, int64_t n, bool inve
     a.first_orient = m->arch.first_orientation;
     a.act = m->arch.act;
     a.inverse = inverse ? 1 : 0;
+    a.fmode = 0;
     static unsigned long long* dbg = nullptr;
     const bool debug_cycles = getenv("CI_DEBUG_CYCLES") != nullptr;
     if (debug_cycles && !dbg) cudaMalloc(&dbg, 148 * 16 * sizeof(unsigned long long));

@@ -309,7 +309,8 @@ def test_serve_learned_small_arch(ci, prec):
     params, x, drop = fx.make_weights(arch, 14), fx.make_inputs(arch, B, k, 4), fx.make_drops(B, k, 104)
     ref = oracle.serve_group(arch, params, x, drop, learned=True)
     g = run_serve(ci, model(ci, arch, params, prec), arch, x, drop, B, k, learned=True)
-    assert relerr(g["xp"].reshape(B, -1), ref["xp"].reshape(B, -1)) < 1e-5   # fp32 CUDA-core encoder
+    # encoder tail on tcgen05 in the model's precision (fp32 CUDA cores for simt)
+    assert relerr(g["xp"].reshape(B, -1), ref["xp"].reshape(B, -1)) < (1e-5 if prec != "bf16" else 3e-2)
     check_against_oracle(g, ref, arch, B, k, prec, "TE-learned")
 
 
