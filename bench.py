@@ -134,6 +134,59 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- C5
+def run_c5(args, rank, world, local):
+    """Config C5: k = 7 main workers + 1 parity worker, one per GPU (8 ranks), 1024 groups per
+    step; encode exact (X2 reduce + h^-1 + h on the parity GPU) or learned (encoder on the parity
+    GPU); decode as a masked NCCL reduce-scatter (paper_2106_06445_b200/workers.py)."""
+    cfg = fx.CONFIGS["C5"]
+    k, B = cfg.k, cfg.B
+    if world != k + 1:
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "config": {"workload": "C5"},
+                              "unavailable": f"C5 needs {k + 1} ranks (one per worker), got {world}"}))
+        return
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2106_06445_b200 import codedinv as ci
+    from paper_2106_06445_b200.workers import GpuCompute, serve_workers
+    arch = cfg.arch
+    learned = args.encode == "learned"
+    model = ci.Model(arch, fx.make_weights(arch, cfg.seed_w), args.precision, device=local)
+    comp = GpuCompute(model, k, B)
+    dev = torch.device("cuda", local)
+    x = fx.make_inputs(arch, B, k, cfg.seed_x)
+    drop = torch.from_numpy(fx.make_drops(B, k, cfg.seed_drop)).to(dev)
+    x_slot = torch.from_numpy(np.ascontiguousarray(x[:, rank])).to(dev) if rank < k else None
+    x_all = torch.from_numpy(x).to(dev) if rank == k else None
+    step = lambda: serve_workers(comp, dist, rank, world, k, drop, x_slot=x_slot, x_all=x_all, learned=learned)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    t = torch.tensor([e0.elapsed_time(e1)], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": B * args.steps / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+                          "higher_is_better": True, "scaling": "none (fixed 8-worker partition)",
+                          "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
+                          "config": {"workload": "C5", "k": k, "groups_per_step": B, "encode": args.encode,
+                                     "parallelism": "worker-per-GPU (k=7 main + 1 parity), NCCL reduce / "
+                                                    "reduce-scatter decode"}}), flush=True)
+    dist.destroy_process_group()
+
+
 # ----------------------------------------------------------------------------- our path
 def relerr(a, ref):
     a = np.asarray(a, np.float64).reshape(-1, np.shape(ref)[-1])
@@ -148,7 +201,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32", "simt"])
-    ap.add_argument("--config", default="C3", choices=["C3", "C4", "C2", "C1"])
+    ap.add_argument("--config", default="C3", choices=["C3", "C4", "C5", "C2", "C1"])
+    ap.add_argument("--encode", default="exact", choices=["exact", "learned"], help="C5 parity encode mode")
     ap.add_argument("--ref-groups", type=int, default=8, help="oracle sample groups per step")
     ap.add_argument("--cpu-groups", type=int, default=8, help="oracle sample for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -162,6 +216,8 @@ def main():
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
+    if args.config == "C5":
+        return run_c5(args, rank, world, local)
     import torch
     torch.cuda.set_device(local)
     dist = None

@@ -269,4 +269,7 @@ CONFIGS = {
                  "k=10 CIFAR-shaped 3x32x32 full-depth h, exact h^-1 parity encode, 1024 groups"),
     "C4": Config("C4", ARCH_CE, 10, 1024, 14, 4, 104,
                  "k=10 CIFAR-shaped, light learned encoder replaces h^-1, multitask heads 10 + 2"),
+    "C5": Config("C5", ARCH_CE, 7, 1024, 15, 5, 105,
+                 "k=7 main + 1 parity worker, one per GPU (8 GPUs), exact or learned encode, "
+                 "decode as a masked reduction over workers"),
 }

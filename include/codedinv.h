@@ -178,6 +178,20 @@ CI_API ci_status_t ci_serve_group_host(const ci_model_t* model, ci_encode_mode_t
                                 int32_t* labels_host, void* ws, size_t ws_bytes,
                                 ci_stream_t stream);
 
+/* ---- Worker-partitioned serving (config C5: one worker per GPU) ----
+ * Decode is linear, so it rides a reduction over workers: worker w contributes coef_w[b] * f_w[b]
+ * and the sum over all n = k + 1 workers is the decoded feature of the lost worker of group b:
+ *   CI_COEF_DECODE: main worker w < k: -1 if w != drop[b], 0 if w == drop[b]; parity w = k: +k
+ *                   (sum = k f(x_p) - sum_{i != j} f(x_i))
+ *   CI_COEF_MEAN:   main worker w < k: 1/k; parity: 0      (sum = exact-encode mean)
+ * Groups with drop[b] = -1 get coefficient 0 for every worker in CI_COEF_DECODE. */
+typedef enum { CI_COEF_DECODE = 0, CI_COEF_MEAN = 1 } ci_coef_kind_t;
+CI_API ci_status_t ci_worker_coef(ci_coef_kind_t kind, int32_t k, int64_t B, int32_t worker,
+                                  const int32_t* drop, float* coef /*[B]*/, ci_stream_t stream);
+/* out[b][:] = coef[b] * f[b][:]   (f, out [B][d], coef [B]; out may alias f) */
+CI_API ci_status_t ci_combine(int64_t B, int64_t d, const float* f, const float* coef, float* out,
+                              ci_stream_t stream);
+
 /* Per-group drop indices generated on the device, bit-identical to the fixtures' host
  * generator: drop[b] = (uint32)(splitmix64_at(seed, b) >> 32) % k (counter-based splitmix64;
  * one uniformly random lost main worker per group). */

@@ -29,7 +29,7 @@ PRECISIONS = {"fp32": CI_PREC_FP32, "bf16": CI_PREC_BF16, "simt": CI_PREC_SIMT}
 EXPORTS = ["ci_last_error", "ci_model_create", "ci_model_destroy", "ci_feature_dim",
            "ci_workspace_size", "ci_check", "ci_forward_h", "ci_inverse_h", "ci_encode",
            "ci_decode", "ci_classify", "ci_serve_group", "ci_workspace_size_host",
-           "ci_serve_group_host", "ci_make_drops"]
+           "ci_serve_group_host", "ci_make_drops", "ci_worker_coef", "ci_combine"]
 TESTING_EXPORTS = ["ci_test_umma_gemm", "ci_test_umma_rate", "ci_test_prof_enable", "ci_test_prof_read",
                    "ci_test_launch_count", "ci_test_mean", "ci_test_plan"]  # include/codedinv_testing.h
 
@@ -63,6 +63,8 @@ _sig = {
     "ci_workspace_size_host": (_I32, [_P, _I32, _I64, _P]),
     "ci_serve_group_host": (_I32, [_P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "ci_make_drops": (_I32, [_I32, _I64, ctypes.c_uint64, _P, _P]),
+    "ci_worker_coef": (_I32, [_I32, _I32, _I64, _I32, _P, _P, _P]),
+    "ci_combine": (_I32, [_I64, _I64, _P, _P, _P, _P]),
     "ci_test_umma_gemm": (_I32, [_P, _I32, _I32, _P, _I32, _I32, _I32, _I32, _I32, _P, _P]),
     "ci_test_umma_rate": (_I32, [_I32, _I32, _I32, _P, _P]),
     "ci_test_prof_enable": (_I32, [_I32]),
@@ -196,6 +198,18 @@ def ci_decode(h, h_parity, drop, ws, stream=None):
     B, k, d = h.shape
     _check(_lib.ci_decode(k, B, d, _ptr(h), _ptr(h_parity), _ptr(drop), _ptr(ws), ws.numel(),
                           _stream(stream)), "ci_decode")
+
+
+CI_COEF_DECODE, CI_COEF_MEAN = 0, 1
+
+
+def ci_worker_coef(kind, k, B, worker, drop, coef, stream=None):
+    _check(_lib.ci_worker_coef(kind, k, B, worker, _ptr(drop), _ptr(coef), _stream(stream)), "ci_worker_coef")
+
+
+def ci_combine(f, coef, out, stream=None):
+    B, d = f.shape[0], f.numel() // max(f.shape[0], 1)
+    _check(_lib.ci_combine(B, d, _ptr(f), _ptr(coef), _ptr(out), _stream(stream)), "ci_combine")
 
 
 def ci_make_drops(k, B, seed, drop, stream=None):

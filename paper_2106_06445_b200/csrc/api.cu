@@ -516,6 +516,22 @@ int64_t ci_test_launch_count(int32_t reset) {
     return (int64_t)v;
 }
 
+ci_status_t ci_worker_coef(ci_coef_kind_t kind, int32_t k, int64_t B, int32_t worker, const int32_t* drop,
+                           float* coef, ci_stream_t stream) {
+    if ((kind != CI_COEF_DECODE && kind != CI_COEF_MEAN) || k < 1 || B < 0 || worker < 0 || worker > k ||
+        (B > 0 && (!coef || (kind == CI_COEF_DECODE && !drop)))) {
+        set_error("invalid argument"); return CI_ERR_INVALID_ARG;
+    }
+    CI_CUDA(launch_worker_coef((int)kind, k, B, worker, drop, coef, (cudaStream_t)stream));
+    return CI_OK;
+}
+
+ci_status_t ci_combine(int64_t B, int64_t d, const float* f, const float* coef, float* out, ci_stream_t stream) {
+    if (B < 0 || d < 0 || (B * d > 0 && (!f || !coef || !out))) { set_error("invalid argument"); return CI_ERR_INVALID_ARG; }
+    CI_CUDA(launch_combine(B, d, f, coef, out, (cudaStream_t)stream));
+    return CI_OK;
+}
+
 ci_status_t ci_make_drops(int32_t k, int64_t B, uint64_t seed, int32_t* drop, ci_stream_t stream) {
     if (k < 1 || B < 0 || (B > 0 && !drop)) { set_error("invalid argument"); return CI_ERR_INVALID_ARG; }
     CI_CUDA(launch_make_drops(k, B, seed, drop, (cudaStream_t)stream));

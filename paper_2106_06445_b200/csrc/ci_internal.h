@@ -73,6 +73,9 @@ cudaError_t launch_decode(float* h, const float* p, const int32_t* drop, int k, 
 cudaError_t launch_classify(const float* z, int64_t n, int64_t d, const float* W, const float* b,
                             int C, float* logits, int32_t* labels, cudaStream_t s);
 cudaError_t launch_make_drops(int k, int64_t B, uint64_t seed, int32_t* drop, cudaStream_t s);
+cudaError_t launch_worker_coef(int kind, int k, int64_t B, int worker, const int32_t* drop, float* coef,
+                               cudaStream_t s);
+cudaError_t launch_combine(int64_t B, int64_t d, const float* f, const float* coef, float* out, cudaStream_t s);
 cudaError_t launch_enc_e1_mean(const float* x, int k, int64_t B, int Ci, int H, int W, const float* W1,
                                const float* b1, int C1, float* m, float* zpsi, int64_t zstride, cudaStream_t s);
 cudaError_t launch_unsqueeze_add(const float* z, int64_t zstride, const float* m, float* u, int64_t B, int C,

@@ -291,4 +291,43 @@ cudaError_t launch_make_drops(int k, int64_t B, uint64_t seed, int32_t* drop, cu
     return cudaGetLastError();
 }
 
+// Worker coefficients of the masked-reduction decode / mean (codedinv.h CI_COEF_*)
+__global__ void k_worker_coef(int kind, int k, int64_t B, int worker, const int32_t* __restrict__ drop,
+                              float* __restrict__ coef) {
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < B; b += (int64_t)gridDim.x * blockDim.x) {
+        float c;
+        if (kind == 1) {
+            c = worker < k ? __fdiv_rn(1.f, (float)k) : 0.f;
+        } else {
+            const int j = drop[b];
+            if (j < 0 || j >= k) c = 0.f;
+            else if (worker == k) c = (float)k;
+            else c = worker == j ? 0.f : -1.f;
+        }
+        coef[b] = c;
+    }
+}
+
+__global__ void k_combine(int64_t B, int64_t d, const float* __restrict__ f, const float* __restrict__ coef,
+                          float* __restrict__ out) {
+    const int64_t total = B * d;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = __fmul_rn(coef[i / d], f[i]);
+}
+
+cudaError_t launch_worker_coef(int kind, int k, int64_t B, int worker, const int32_t* drop, float* coef,
+                               cudaStream_t s) {
+    if (B == 0) return cudaSuccess;
+    k_worker_coef<<<grid_for(B, 256), 256, 0, s>>>(kind, k, B, worker, drop, coef);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_combine(int64_t B, int64_t d, const float* f, const float* coef, float* out, cudaStream_t s) {
+    if (B * d == 0) return cudaSuccess;
+    k_combine<<<grid_for(B * d, 256), 256, 0, s>>>(B, d, f, coef, out);
+    count_launch();
+    return cudaGetLastError();
+}
+
 }  // namespace ci

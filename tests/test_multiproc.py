@@ -62,3 +62,94 @@ def test_group_sharded_gloo_world2(tmp_path):
     ref = oracle.serve_group(c.arch, fx.make_weights(c.arch, c.seed_w), x, drop, nthreads=1)
     assert np.array_equal(np.load(tmp_path / "R.npy"), ref["R"])
     assert float(np.load(tmp_path / "tmax.npy")[0]) == 11.0
+
+
+# ------------------------------------------------------------------ C5 worker partition
+class _OracleCompute:
+    """CPU stand-in for GpuCompute (test only): per-rank compute from the f64 oracle."""
+
+    def __init__(self, arch, params, k):
+        self.arch, self.params, self.k, self.d = arch, params, k, arch.d
+
+        class _M:
+            pass
+        self.model = _M()
+        self.model.arch = arch
+
+    def empty(self, *shape):
+        return torch.empty(*shape, dtype=torch.float64)
+
+    def zeros(self, *shape):
+        return torch.zeros(*shape, dtype=torch.float64)
+
+    def forward_h(self, x):
+        return torch.from_numpy(oracle.forward_h(self.arch, self.params, x.numpy(), nthreads=1))
+
+    def inverse_h(self, h):
+        return torch.from_numpy(oracle.inverse_h(self.arch, self.params, h.numpy(), nthreads=1))
+
+    def encode_learned(self, x_all):
+        return torch.from_numpy(oracle.encode_learned(self.arch, self.params, x_all.numpy(), nthreads=1))
+
+    def coef(self, kind, worker, drop):
+        d = torch.as_tensor(drop)
+        if kind == 1:
+            return torch.full((len(d),), (1.0 / self.k) if worker < self.k else 0.0, dtype=torch.float64)
+        c = torch.where(d == worker, 0.0, -1.0).double() if worker < self.k else torch.full((len(d),), float(self.k),
+                                                                                             dtype=torch.float64)
+        return torch.where(d < 0, torch.zeros_like(c), c)
+
+    def combine(self, f, coef):
+        return f * coef[:, None]
+
+    def classify(self, head, z):
+        lg, lb = oracle.classify(self.arch, self.params, head, z.numpy())
+        return torch.from_numpy(lg), torch.from_numpy(lb)
+
+
+def _worker_c5(rank, world, port, B, learned, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2106_06445_b200.workers import serve_workers
+    arch, k = fx.ARCH_TE, world - 1
+    params = fx.make_weights(arch, 15)
+    x = fx.make_inputs(arch, B, k, 5)
+    drop = fx.make_drops(B, k, 105)
+    drop[1] = -1                                  # one group without a loss
+    comp = _OracleCompute(arch, params, k)
+    xs = torch.from_numpy(x[:, rank].astype(np.float64)) if rank < k else None
+    xa = torch.from_numpy(x.astype(np.float64)) if rank == k else None
+    out = serve_workers(comp, dist, rank, world, k, torch.from_numpy(drop), x_slot=xs, x_all=xa, learned=learned)
+    parts = [torch.empty_like(out["decoded"]) for _ in range(world)]
+    dist.all_gather(parts, out["decoded"])
+    if rank == 0:
+        np.save(os.path.join(out_dir, "decoded.npy"), torch.cat(parts).numpy())
+        np.save(os.path.join(out_dir, "logits_dec.npy"), out["logits_decoded"][1].numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("learned", [False, True])
+def test_worker_partition_gloo(tmp_path, learned):
+    """C5 orchestration (k = 2 main workers + 1 parity worker, 3 ranks): the masked
+    reduce-scatter decode equals the single-process oracle decode of the lost slot."""
+    world, B = 3, 6
+    mp.spawn(_worker_c5, args=(world, _free_port(), B, learned, str(tmp_path)), nprocs=world, join=True)
+    arch, k = fx.ARCH_TE, world - 1
+    params = fx.make_weights(arch, 15)
+    x = fx.make_inputs(arch, B, k, 5)
+    drop = fx.make_drops(B, k, 105)
+    drop[1] = -1
+    ref = oracle.serve_group(arch, params, x, drop, learned=learned, nthreads=1)
+    dec = np.load(tmp_path / "decoded.npy")
+    for b in range(B):
+        if drop[b] < 0:
+            assert np.all(dec[b] == 0)
+        else:
+            r = ref["R"][b, drop[b]]
+            assert np.max(np.abs(dec[b] - r)) / np.max(np.abs(r)) < 1e-12
+    lg = np.load(tmp_path / "logits_dec.npy")          # rank 0's partition, coarse head
+    r0 = [b for b in range(B // world)]
+    for b in r0:
+        if drop[b] >= 0:
+            assert np.max(np.abs(lg[b] - ref["logits"][1][b, drop[b]])) < 1e-10
