@@ -208,6 +208,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-alt", action="store_true", help="skip the other-precision throughput line item")
+    ap.add_argument("--inflight", type=int, default=2, choices=[1, 2],
+                    help="request batches in flight (2: consecutive steps alternate between two CUDA streams)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -247,12 +249,25 @@ def main():
     lg = [torch.empty(B * k * ncls, device=dev) for _ in range(NBUF)]
     lb = [torch.empty(B * k * len(arch.heads), dtype=torch.int32, device=dev) for _ in range(NBUF)]
 
-    def run_mode(precision, steps, warmup, measure=True):
+    def run_mode(precision, steps, warmup, measure=True, nin=1, prof=None):
+        """measure: sample clocks; prof: per-launch CUDA events on the stage kernel (needs nin=1)."""
+        prof = (measure and nin == 1) if prof is None else prof
         model = ci.Model(arch, params, precision, device=local)
-        ws = model.workspace(k, B)
-        for i in range(warmup):
+        wss = [model.workspace(k, B) for _ in range(nin)]
+        ws = wss[0]
+        streams = [stream] + [torch.cuda.Stream(device=dev) for _ in range(nin - 1)]
+
+        def serve(i):
             j = i % NBUF
-            model.ci_serve_group(xs[j], drops[j], hs[j], ps[j], ws, logits=lg[j], labels=lb[j], learned=learned)
+            sidx = i % nin
+            st = streams[sidx]
+            model.ci_serve_group(xs[j], drops[j], hs[j], ps[j], wss[sidx], logits=lg[j], labels=lb[j],
+                                 learned=learned, stream=st)
+
+        for s_ in streams[1:]:
+            s_.wait_stream(stream)
+        for i in range(warmup):
+            serve(i)
         torch.cuda.synchronize()
         ci.ci_test_prof_read()
         ci.ci_test_launch_count(reset=True)
@@ -260,15 +275,18 @@ def main():
         if measure:
             sampler.start()
             time.sleep(0.2)
-        ci.ci_test_prof_enable(measure)
+        ci.ci_test_prof_enable(prof and nin == 1)
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
+        for s_ in streams[1:]:
+            s_.wait_stream(stream)
         for i in range(steps):
-            j = i % NBUF
-            model.ci_serve_group(xs[j], drops[j], hs[j], ps[j], ws, logits=lg[j], labels=lb[j], learned=learned)
+            serve(i)
+        for s_ in streams[1:]:
+            stream.wait_stream(s_)
         e1.record(stream)
         torch.cuda.synchronize()
         if dist:
@@ -278,7 +296,8 @@ def main():
         clocks = sampler.stop() if measure else None
         launches = ci.ci_test_launch_count(reset=True)
         kms, kl, kfl = ci.ci_test_prof_read()
-        model.ci_check(ws)
+        for w_ in wss:
+            model.ci_check(w_)
         if dist:
             t = torch.tensor([ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -287,12 +306,15 @@ def main():
                     kms=kms, klaunch=kl, kflops=kfl)
 
     peaks, peak_src = load_peaks()
-    main_run = run_mode(args.precision, args.steps, args.warmup)
+    main_run = run_mode(args.precision, args.steps, args.warmup, nin=args.inflight)
     ms_step = main_run["ms"] / args.steps
     value = world * B * args.steps / (main_run["ms"] / 1e3)
+    # per-launch kernel timing needs one stream: a separate single-stream pass when inflight > 1
+    prof_run = main_run if args.inflight == 1 else run_mode(args.precision, max(3, args.steps // 2), 3,
+                                                            measure=False, nin=1, prof=True)
 
     # --- roofline of the dominant kernel (fused tcgen05 stage kernel), live CUDA events
-    kms, kfl, kl = main_run["kms"], main_run["kflops"], main_run["klaunch"]
+    kms, kfl, kl = prof_run["kms"], prof_run["kflops"], prof_run["klaunch"]
     stage_ms, stage_fl = sum(kms), sum(kfl)
     roofline = None
     kernels = {}
@@ -312,7 +334,8 @@ def main():
                     "peak_source": f"{peak_src} bf16_tflops_sustained (dense bf16 cuBLAS, 4 s loop)",
                     "frac_of_burst": achieved / peaks["bf16_tflops"],
                     "issued_mma_multiplier": mult, "traffic": traffic,
-                    "share_of_step": stage_ms / main_run["ms"]}
+                    "share_of_step": stage_ms / prof_run["ms"],
+                    "measured_in": "single-stream pass" if args.inflight > 1 else "timed region"}
         for s in range(4):
             if kl[s]:
                 kernels[f"k_stage[s{s}]"] = {"launches": kl[s], "ms_per_launch": kms[s] / kl[s],
@@ -417,7 +440,7 @@ def main():
     alt = None
     if not args.no_alt:
         other = "fp32" if args.precision == "bf16" else "bf16"
-        r2 = run_mode(other, max(3, args.steps // 3), 2, measure=False)
+        r2 = run_mode(other, max(3, args.steps // 3), 3, measure=False, nin=args.inflight)
         alt = {"precision": other, "value": world * B * max(3, args.steps // 3) / (r2["ms"] / 1e3),
                "ms_per_step": r2["ms"] / max(3, args.steps // 3)}
         del r2
@@ -465,7 +488,8 @@ def main():
                            "arch": "C: 3 stages x 9 additive-coupling blocks (c=6/24/96, m=64/128/256)",
                            "encode": "exact h^-1(mean h)", "precision": args.precision,
                            "parallelism": f"group-sharded x{world}",
-                           "l2": f"inputs rotate over {NBUF} resident buffer sets (x+outputs ~1 GB > L2)"},
+                           "l2": f"inputs rotate over {NBUF} resident buffer sets (x+outputs ~1 GB > L2)",
+                           "inflight": args.inflight},
                 "roofline": roofline, "kernels": kernels, "hbm": hbm,
                 "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": main_run["launches"], "clocks": main_run["clocks"],

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <mutex>
 
 #include "ci_internal.h"
 #include "codedinv_testing.h"
@@ -38,7 +39,23 @@ static size_t up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct WsLayout {
     size_t flag = 0, scratch = 0, mean = 0, xp = 0, hidden = 0, enc = 0, total = 0;
+    mutable int ctr_next = 0;   // next batch-counter slot of this call (see next_ctr)
 };
+
+// The flag region (256 B) holds the drop-index error count (int 0) and, in ints
+// kCtrBase.., one zeroed batch counter per tcgen05 stage launch of an API call: the stage
+// kernel claims batches dynamically from it.  zero_ctrs runs once at the start of a call.
+static constexpr int kCtrBase = 16, kCtrSlots = 48;
+static cudaError_t zero_ctrs(void* ws, const WsLayout& L, cudaStream_t st) {
+    L.ctr_next = 0;
+    return cudaMemsetAsync(reinterpret_cast<int*>(reinterpret_cast<char*>(ws) + L.flag) + kCtrBase, 0,
+                           sizeof(int) * kCtrSlots, st);
+}
+static int* next_ctr(void* ws, const WsLayout& L) {
+    static const bool static_batches = getenv("CI_STATIC_BATCHES") != nullptr;   // A/B switch
+    if (static_batches || L.ctr_next >= kCtrSlots) return nullptr;   // static round-robin batches
+    return reinterpret_cast<int*>(reinterpret_cast<char*>(ws) + L.flag) + kCtrBase + L.ctr_next++;
+}
 
 static constexpr int64_t kSimtChunk = 1024;
 
@@ -72,9 +89,9 @@ static T* at(void* ws, size_t off) { return reinterpret_cast<T*>(reinterpret_cas
 // h / h^-1 orchestration (both precisions share the stage-boundary permutations)
 // ---------------------------------------------------------------------------
 static ci_status_t run_stage_blocks(const Model* m, int s, float* state, int64_t n, bool inverse,
-                                    float* hidden, cudaStream_t st) {
+                                    float* hidden, int* ctr, cudaStream_t st) {
     const StageInfo& S = m->st[s];
-    if (m->umma) return umma_stage(m, s, state, n, inverse, st);
+    if (m->umma) return umma_stage(m, s, state, n, inverse, ctr, st);
     const int64_t per = (int64_t)S.C * S.H * S.W, half = (int64_t)S.c * S.H * S.W;
     for (int tt = 0; tt < S.nb; tt++) {
         int t = inverse ? S.nb - 1 - tt : tt;
@@ -109,7 +126,7 @@ static ci_status_t forward_impl(const Model* m, const float* x, float* h, int64_
         float* dst = ((S - 1 - s) % 2 == 0) ? h : scratch;
         CI_CUDA(launch_permute(src, dst, n, C, H, W, m->st[s].squeeze ? 1 : 0, st));
         C = m->st[s].C; H = m->st[s].H; W = m->st[s].W;
-        ci_status_t r = run_stage_blocks(m, s, dst, n, false, hidden, st);
+        ci_status_t r = run_stage_blocks(m, s, dst, n, false, hidden, next_ctr(ws, L), st);
         if (r != CI_OK) return r;
         src = dst;
     }
@@ -129,7 +146,7 @@ static ci_status_t inverse_impl(const Model* m, const float* h, float* x, int64_
     const StageInfo& L3 = m->st[S - 1];
     CI_CUDA(launch_permute(h, cur, n, L3.C, L3.H, L3.W, 0, st));
     for (int s = S - 1; s >= 0; s--) {
-        ci_status_t r = run_stage_blocks(m, s, cur, n, true, hidden, st);
+        ci_status_t r = run_stage_blocks(m, s, cur, n, true, hidden, next_ctr(ws, L), st);
         if (r != CI_OK) return r;
         float* nxt = target(ci++);
         const StageInfo& Si = m->st[s];
@@ -161,7 +178,7 @@ static ci_status_t encode_learned_impl(const Model* m, const float* x, float* xp
     float* U = Z2 + B * mid * hw4;
     CI_CUDA(launch_enc_e1_mean(x, k, B, Ci, H, W, E1W, E1b, c1, Mb, Zb, zstride, st));
     if (m->umma) {
-        ci_status_t r = umma_encoder_tail(m, Zb, B, st);   // tcgen05: ReLU(E3(ReLU(E2 z)))
+        ci_status_t r = umma_encoder_tail(m, Zb, B, next_ctr(ws, L), st);   // tcgen05: ReLU(E3(ReLU(E2 z)))
         if (r != CI_OK) return r;
     } else {
         CI_CUDA(launch_conv_simt(Zb, zstride, 4 * c1, H / 2, W / 2, E2W, E2b, mid, Z2, mid * hw4, B, 0, 0, st));
@@ -274,6 +291,7 @@ void ci_model_destroy(ci_model_t* model) {
     Model* m = reinterpret_cast<Model*>(model);
     if (!m) return;
     umma_release(m);
+    release_host_pipe(m);
     cudaFree(m->d_params);
     for (int t = 0; t < 4; t++) cudaFree(m->d_head[t]);
     delete m;
@@ -327,6 +345,7 @@ ci_status_t ci_forward_h(const ci_model_t* model, const float* x, float* h, int6
     WsLayout L = ws_layout(m, 1, n, false);
     ci_status_t r = check_ws(L, ws, ws_bytes);
     if (r != CI_OK) return r;
+    CI_CUDA(zero_ctrs(ws, L, (cudaStream_t)stream));
     return forward_impl(m, x, h, n, ws, L, (cudaStream_t)stream);
 }
 
@@ -339,6 +358,7 @@ ci_status_t ci_inverse_h(const ci_model_t* model, const float* h, float* x, int6
     WsLayout L = ws_layout(m, 1, n, false);
     ci_status_t r = check_ws(L, ws, ws_bytes);
     if (r != CI_OK) return r;
+    CI_CUDA(zero_ctrs(ws, L, (cudaStream_t)stream));
     return inverse_impl(m, h, x, n, ws, L, (cudaStream_t)stream);
 }
 
@@ -357,6 +377,7 @@ ci_status_t ci_encode(const ci_model_t* model, ci_encode_mode_t mode, int32_t k,
     ci_status_t r = check_ws(L, ws, ws_bytes);
     if (r != CI_OK) return r;
     cudaStream_t st = (cudaStream_t)stream;
+    CI_CUDA(zero_ctrs(ws, L, st));
     if (mode == CI_ENC_LEARNED) return encode_learned_impl(m, x, x_parity, k, B, ws, L, st);
     float* mean = mean_out ? mean_out : at<float>(ws, L.mean);
     CI_CUDA(launch_mean(h, mean, k, B, m->d, st));
@@ -386,11 +407,13 @@ ci_status_t ci_classify(const ci_model_t* model, int32_t head, const float* z, i
     return CI_OK;
 }
 
+// logits[t] / labels[t]: head t's [n][C_t] logits and [n] labels (null = not wanted)
 static ci_status_t serve_impl(const Model* m, ci_encode_mode_t mode, int32_t k, int64_t B, const float* x,
                               const int32_t* drop, float* h_out, float* h_parity, float* x_parity,
-                              float* logits, int32_t* labels, void* ws, const WsLayout& L,
+                              float* const* logits, int32_t* const* labels, void* ws, const WsLayout& L,
                               cudaStream_t st) {
     const int64_t n = B * (int64_t)k;
+    CI_CUDA(zero_ctrs(ws, L, st));
     ci_status_t r = forward_impl(m, x, h_out, n, ws, L, st);             // (1) h on main queries
     if (r != CI_OK) return r;
     float* mean = at<float>(ws, L.mean);
@@ -405,17 +428,24 @@ static ci_status_t serve_impl(const Model* m, ci_encode_mode_t mode, int32_t k, 
     r = forward_impl(m, xp, h_parity, B, ws, L, st);                      // (3) h on parity query
     if (r != CI_OK) return r;
     CI_CUDA(launch_decode(h_out, h_parity, drop, k, B, m->d, at<int>(ws, L.flag), st));  // (4)
-    if (logits || labels) {                                               // (5) heads
-        int64_t lo = 0;
-        for (int t = 0; t < m->arch.n_heads; t++) {
-            const float* W = m->d_head[t];
-            const float* b = W + (int64_t)m->arch.head_classes[t] * m->d;
-            CI_CUDA(launch_classify(h_out, n, m->d, W, b, m->arch.head_classes[t],
-                                    logits ? logits + lo : nullptr, labels ? labels + t * n : nullptr, st));
-            lo += n * m->arch.head_classes[t];
-        }
+    for (int t = 0; t < m->arch.n_heads; t++) {                           // (5) heads
+        if (!logits[t] && !labels[t]) continue;
+        const float* W = m->d_head[t];
+        const float* b = W + (int64_t)m->arch.head_classes[t] * m->d;
+        CI_CUDA(launch_classify(h_out, n, m->d, W, b, m->arch.head_classes[t], logits[t], labels[t], st));
     }
     return CI_OK;
+}
+
+// head-major output layout of logits [t][n][C_t] and labels [t][n] -> per-head pointers
+static void head_ptrs(const Model* m, int64_t n, float* logits, int32_t* labels, float** lp, int32_t** bp) {
+    int64_t lo = 0;
+    for (int t = 0; t < 4; t++) { lp[t] = nullptr; bp[t] = nullptr; }
+    for (int t = 0; t < m->arch.n_heads; t++) {
+        lp[t] = logits ? logits + lo : nullptr;
+        bp[t] = labels ? labels + t * n : nullptr;
+        lo += n * m->arch.head_classes[t];
+    }
 }
 
 ci_status_t ci_serve_group(const ci_model_t* model, ci_encode_mode_t mode, int32_t k, int64_t B,
@@ -434,23 +464,44 @@ ci_status_t ci_serve_group(const ci_model_t* model, ci_encode_mode_t mode, int32
     ci_status_t r = check_ws(L, ws, ws_bytes);
     if (r != CI_OK) return r;
     if (B == 0) return CI_OK;
-    return serve_impl(m, mode, k, B, x, drop, h_out, h_parity, x_parity, logits, labels, ws, L,
-                      (cudaStream_t)stream);
+    float* lp[4];
+    int32_t* bp[4];
+    head_ptrs(m, B * (int64_t)k, logits, labels, lp, bp);
+    return serve_impl(m, mode, k, B, x, drop, h_out, h_parity, x_parity, lp, bp, ws, L, (cudaStream_t)stream);
 }
 
-// --- host-buffer variant: staging areas appended after the device workspace ---------------
+// --- host-buffer variant -----------------------------------------------------------------
+// The B groups are served in nc chunks so that PCIe traffic overlaps compute: chunk c's
+// inputs go up on a copy stream, its compute runs on the caller's stream (even c) or a
+// second compute stream (odd c, own device workspace), and its outputs come back on a
+// third stream while later chunks compute.  Layout: dev workspace 0 (first, so ci_check
+// sees its flag) | dev workspace 1 | x | drop | h | p | logits | labels (full size).
+static constexpr int kMaxChunks = 8;
+
+static int host_chunks(int64_t B) {
+    static const int env = getenv("CI_HOST_CHUNKS") ? atoi(getenv("CI_HOST_CHUNKS")) : 0;
+    int nc = env > 0 ? env : (B >= 512 ? 4 : B >= 64 ? 2 : 1);
+    nc = std::min(nc, kMaxChunks);
+    return (int)std::max<int64_t>(1, std::min<int64_t>(nc, B));
+}
+
 struct HostLayout {
-    WsLayout dev;
-    size_t x = 0, drop = 0, h = 0, p = 0, logits = 0, labels = 0, total = 0;
+    WsLayout dev;                 // per-chunk device workspace (chunk of Bc groups)
+    int nc = 1;
+    int64_t Bc = 0;
+    size_t dev1 = 0, x = 0, drop = 0, h = 0, p = 0, logits = 0, labels = 0, total = 0;
 };
 
 static HostLayout host_layout(const Model* m, int32_t k, int64_t B) {
     HostLayout H;
-    H.dev = ws_layout(m, k, B);
+    H.nc = host_chunks(B);
+    H.Bc = (B + H.nc - 1) / H.nc;
+    H.dev = ws_layout(m, k, H.Bc);
     int64_t n = B * (int64_t)k;
     int64_t ncls = 0;
     for (int t = 0; t < m->arch.n_heads; t++) ncls += m->arch.head_classes[t];
     size_t off = H.dev.total;
+    H.dev1 = off; off += H.nc > 1 ? H.dev.total : 0;
     H.x = off; off += up(sizeof(float) * (size_t)(n * m->din));
     H.drop = off; off += up(sizeof(int32_t) * (size_t)B);
     H.h = off; off += up(sizeof(float) * (size_t)(n * m->d));
@@ -460,6 +511,49 @@ static HostLayout host_layout(const Model* m, int32_t k, int64_t B) {
     H.total = off;
     return H;
 }
+
+}  // extern "C"
+
+namespace ci {
+struct HostPipe {
+    std::mutex mu;
+    cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+    cudaEvent_t start = nullptr, fin = nullptr, in[kMaxChunks] = {}, done[kMaxChunks] = {};
+};
+
+static ci_status_t host_pipe(Model* m, HostPipe** out) {
+    static std::mutex create_mu;
+    std::lock_guard<std::mutex> g(create_mu);
+    if (!m->host_pipe) {
+        HostPipe* P = new HostPipe();
+        const unsigned fl = cudaStreamNonBlocking;
+        CI_CUDA(cudaStreamCreateWithFlags(&P->h2d, fl));
+        CI_CUDA(cudaStreamCreateWithFlags(&P->comp, fl));
+        CI_CUDA(cudaStreamCreateWithFlags(&P->d2h, fl));
+        CI_CUDA(cudaEventCreateWithFlags(&P->start, cudaEventDisableTiming));
+        CI_CUDA(cudaEventCreateWithFlags(&P->fin, cudaEventDisableTiming));
+        for (int c = 0; c < kMaxChunks; c++) {
+            CI_CUDA(cudaEventCreateWithFlags(&P->in[c], cudaEventDisableTiming));
+            CI_CUDA(cudaEventCreateWithFlags(&P->done[c], cudaEventDisableTiming));
+        }
+        m->host_pipe = P;
+    }
+    *out = reinterpret_cast<HostPipe*>(m->host_pipe);
+    return CI_OK;
+}
+
+void release_host_pipe(Model* m) {
+    HostPipe* P = reinterpret_cast<HostPipe*>(m->host_pipe);
+    if (!P) return;
+    cudaStreamDestroy(P->h2d); cudaStreamDestroy(P->comp); cudaStreamDestroy(P->d2h);
+    cudaEventDestroy(P->start); cudaEventDestroy(P->fin);
+    for (int c = 0; c < kMaxChunks; c++) { cudaEventDestroy(P->in[c]); cudaEventDestroy(P->done[c]); }
+    delete P;
+    m->host_pipe = nullptr;
+}
+}  // namespace ci
+
+extern "C" {
 
 ci_status_t ci_workspace_size_host(const ci_model_t* model, int32_t k, int64_t B, size_t* bytes) {
     const Model* m = reinterpret_cast<const Model*>(model);
@@ -482,26 +576,73 @@ ci_status_t ci_serve_group_host(const ci_model_t* model, ci_encode_mode_t mode, 
         set_error("host workspace %zu bytes; need %zu", ws_bytes, H.total); return CI_ERR_WORKSPACE;
     }
     if (B == 0) return CI_OK;
+    HostPipe* P = nullptr;
+    ci_status_t r = host_pipe(const_cast<Model*>(m), &P);
+    if (r != CI_OK) return r;
+    std::lock_guard<std::mutex> g(P->mu);
     cudaStream_t st = (cudaStream_t)stream;
-    const int64_t n = B * (int64_t)k;
-    int64_t ncls = 0;
-    for (int t = 0; t < m->arch.n_heads; t++) ncls += m->arch.head_classes[t];
+    const int64_t n = B * (int64_t)k, d = m->d, din = m->din;
+    const int nh = m->arch.n_heads;
     float* dx = at<float>(ws, H.x);
     int32_t* ddrop = at<int32_t>(ws, H.drop);
     float* dh = at<float>(ws, H.h);
     float* dp = at<float>(ws, H.p);
     float* dl = at<float>(ws, H.logits);
     int32_t* dlab = at<int32_t>(ws, H.labels);
-    CI_CUDA(cudaMemcpyAsync(dx, x_host, sizeof(float) * n * m->din, cudaMemcpyHostToDevice, st));
-    CI_CUDA(cudaMemcpyAsync(ddrop, drop_host, sizeof(int32_t) * B, cudaMemcpyHostToDevice, st));
-    ci_status_t r = serve_impl(m, mode, k, B, dx, ddrop, dh, dp, nullptr, dl, dlab, ws, H.dev, st);
-    if (r != CI_OK) return r;
-    if (h_out_host) CI_CUDA(cudaMemcpyAsync(h_out_host, dh, sizeof(float) * n * m->d, cudaMemcpyDeviceToHost, st));
-    if (h_parity_host) CI_CUDA(cudaMemcpyAsync(h_parity_host, dp, sizeof(float) * B * m->d, cudaMemcpyDeviceToHost, st));
-    if (logits_host && ncls) CI_CUDA(cudaMemcpyAsync(logits_host, dl, sizeof(float) * n * ncls, cudaMemcpyDeviceToHost, st));
-    if (labels_host && m->arch.n_heads)
-        CI_CUDA(cudaMemcpyAsync(labels_host, dlab, sizeof(int32_t) * n * m->arch.n_heads, cudaMemcpyDeviceToHost, st));
+    float *dlp[4], *hlp[4];
+    int32_t *dbp[4], *hbp[4];
+    head_ptrs(m, n, dl, dlab, dlp, dbp);
+    head_ptrs(m, n, logits_host, labels_host, hlp, hbp);
+    CI_CUDA(cudaEventRecord(P->start, st));
+    CI_CUDA(cudaStreamWaitEvent(P->h2d, P->start, 0));
+    for (int c = 0; c < H.nc; c++) {
+        const int64_t b0 = c * H.Bc, nb = std::min<int64_t>(H.Bc, B - b0);
+        if (nb <= 0) break;
+        const int64_t q0 = b0 * k, nq = nb * k;
+        CI_CUDA(cudaMemcpyAsync(dx + q0 * din, x_host + q0 * din, sizeof(float) * nq * din, cudaMemcpyHostToDevice, P->h2d));
+        CI_CUDA(cudaMemcpyAsync(ddrop + b0, drop_host + b0, sizeof(int32_t) * nb, cudaMemcpyHostToDevice, P->h2d));
+        CI_CUDA(cudaEventRecord(P->in[c], P->h2d));
+        cudaStream_t cs = (c & 1) ? P->comp : st;
+        void* wsc = (c & 1) ? at<char>(ws, H.dev1) : ws;
+        CI_CUDA(cudaStreamWaitEvent(cs, P->in[c], 0));
+        float* clp[4];
+        int32_t* cbp[4];
+        for (int t = 0; t < 4; t++) {
+            const int64_t C = t < nh ? m->arch.head_classes[t] : 0;
+            clp[t] = dlp[t] ? dlp[t] + q0 * C : nullptr;
+            cbp[t] = dbp[t] ? dbp[t] + q0 : nullptr;
+        }
+        r = serve_impl(m, mode, k, nb, dx + q0 * din, ddrop + b0, dh + q0 * d, dp + b0 * d, nullptr, clp, cbp,
+                       wsc, H.dev, cs);
+        if (r != CI_OK) return r;
+        CI_CUDA(cudaEventRecord(P->done[c], cs));
+        CI_CUDA(cudaStreamWaitEvent(P->d2h, P->done[c], 0));
+        if (h_out_host)
+            CI_CUDA(cudaMemcpyAsync(h_out_host + q0 * d, dh + q0 * d, sizeof(float) * nq * d, cudaMemcpyDeviceToHost, P->d2h));
+        if (h_parity_host)
+            CI_CUDA(cudaMemcpyAsync(h_parity_host + b0 * d, dp + b0 * d, sizeof(float) * nb * d, cudaMemcpyDeviceToHost, P->d2h));
+        for (int t = 0; t < nh; t++) {
+            const int64_t C = m->arch.head_classes[t];
+            if (hlp[t] && C)
+                CI_CUDA(cudaMemcpyAsync(hlp[t] + q0 * C, clp[t], sizeof(float) * nq * C, cudaMemcpyDeviceToHost, P->d2h));
+            if (hbp[t])
+                CI_CUDA(cudaMemcpyAsync(hbp[t] + q0, cbp[t], sizeof(int32_t) * nq, cudaMemcpyDeviceToHost, P->d2h));
+        }
+    }
+    CI_CUDA(cudaEventRecord(P->fin, P->d2h));
+    CI_CUDA(cudaStreamWaitEvent(st, P->fin, 0));
     CI_CUDA(cudaStreamSynchronize(st));
+    if (H.nc > 1) {   // fold workspace 1's drop-error count into workspace 0's flag (ci_check)
+        int f[2] = {0, 0};
+        CI_CUDA(cudaMemcpy(&f[0], ws, sizeof(int), cudaMemcpyDeviceToHost));
+        CI_CUDA(cudaMemcpy(&f[1], at<char>(ws, H.dev1), sizeof(int), cudaMemcpyDeviceToHost));
+        if (f[1]) {
+            f[0] += f[1];
+            f[1] = 0;
+            CI_CUDA(cudaMemcpy(ws, &f[0], sizeof(int), cudaMemcpyHostToDevice));
+            CI_CUDA(cudaMemcpy(at<char>(ws, H.dev1), &f[1], sizeof(int), cudaMemcpyHostToDevice));
+        }
+    }
     return CI_OK;
 }
 

@@ -51,7 +51,10 @@ struct Model {
     float* d_bias = nullptr;                 // padded biases
     void* umma_state = nullptr;              // host-side stage plans (k_umma.cu)
     bool umma = false;
+    void* host_pipe = nullptr;               // streams/events of ci_serve_group_host (api.cu)
 };
+
+void release_host_pipe(Model* m);   // api.cu: streams/events of the host-buffer entry
 
 // ---- accounting (codedinv_testing.h)
 void count_launch(int n = 1);
@@ -85,10 +88,11 @@ cudaError_t launch_unsqueeze_add(const float* z, int64_t zstride, const float* m
 ci_status_t umma_prepare(Model* m, const float* host_params);
 void umma_release(Model* m);
 // Runs one stage (all blocks) on the fp32 NCHW state `state` [n][C][H][W] in place.
+// ctr: a zeroed int the launch claims batches from (null: static round-robin batches).
 ci_status_t umma_stage(const Model* m, int stage, float* state, int64_t n, bool inverse,
-                       cudaStream_t s);
+                       int* ctr, cudaStream_t s);
 // Learned-encoder tail: zbuf [n][2*4c1][H/2][W/2]; channels [0,4c1) = psi(mean first layer) in,
 // channels [4c1, 8c1) = ReLU(E3(ReLU(E2 z))) out (tcgen05 stage kernel, fmode 1).
-ci_status_t umma_encoder_tail(const Model* m, float* zbuf, int64_t n, cudaStream_t s);
+ci_status_t umma_encoder_tail(const Model* m, float* zbuf, int64_t n, int* ctr, cudaStream_t s);
 
 }  // namespace ci

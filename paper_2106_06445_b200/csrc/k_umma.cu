@@ -73,6 +73,7 @@ struct StageArgs {
     int C, nb, first_orient, act, inverse;
     int fmode;                // 0: s_out (+|-)= F(s_in) (coupling); 1: s_out = ReLU(F(s_in)) (encoder tail)
     unsigned long long* dbg;  // optional per-CTA cycle counters (CI_DEBUG_CYCLES), 16 per CTA
+    int* ctr;                 // zeroed batch counter of this launch (dynamic batch claiming), or null
     StagePlan p;
 };
 
@@ -227,8 +228,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
     uint64_t* hd_full = x_full + 3;    // [2]
     uint64_t* hd_empty = x_full + 5;   // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_full + 7);
+    // batch queue: the producer claims batch indices (one ahead) and publishes them here
+    uint64_t* bqf = x_full + 8;        // [4] entry published (1 arrival)
+    uint64_t* bqe = x_full + 12;       // [4] entry consumed (MMA thread + every epilogue thread)
+    volatile int64_t* bq = reinterpret_cast<volatile int64_t*>(x_full + 16);   // [4]
     // per-k-step A descriptors for tile 0 (hi planes): conv1 [k1], conv2 [k2]
-    uint64_t* adesc1 = x_full + 8;
+    uint64_t* adesc1 = x_full + 20;
     uint64_t* adesc2 = adesc1 + p.k1;
 
     // ---- zero the activation buffers (pads and guards must read as 0)
@@ -245,6 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
         mbar_init(acc1_full, 1);
         for (int i = 0; i < 2; i++) { mbar_init(&hd_full[i], kEpiThreads); mbar_init(&hd_empty[i], 1); }
         mbar_init(acc2_full, 1);
+        for (int i = 0; i < 4; i++) { mbar_init(&bqf[i], 1); mbar_init(&bqe[i], 1 + kEpiThreads); }
         fence_mbar_init();
         const uint32_t plane_b = (uint32_t)p.Rtot * 16;
         const uint32_t xb0 = smem_u32(xbuf), hb0 = smem_u32(hbuf);
@@ -277,6 +283,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
 
     const int64_t nbatch = (a.n + p.I - 1) / p.I;
     const int64_t HW = (int64_t)p.H * p.W;
+    // Batches are claimed dynamically (first one = blockIdx.x, then an atomic counter), so
+    // CTAs that start late -- e.g. while another stream's kernel still holds their SM --
+    // simply take fewer batches.  Entry i of the queue is batch i of this CTA; the entry
+    // after the last real batch is a terminator (>= nbatch).
+    auto bq_read = [&](int i) -> int64_t {
+        mbar_wait(&bqf[i & 3], (uint32_t)((i >> 2) & 1));
+        return bq[i & 3];
+    };
 
     if (warp == 0) {
         // ================= producer: stream packed weights through the ring ===============
@@ -284,7 +298,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
             int slot = 0;
             uint32_t phase = 0;
             unsigned long long w_empty = 0, t_start = clock64();
-            for (int64_t b = blockIdx.x; b < nbatch; b += gridDim.x) {
+            auto publish = [&](int i, int64_t v) {
+                mbar_wait(&bqe[i & 3], (uint32_t)(((i >> 2) & 1) ^ 1));
+                bq[i & 3] = v;
+                mbar_arrive(&bqf[i & 3]);
+            };
+            int64_t bcur = blockIdx.x;
+            publish(0, bcur);
+            for (int qi = 0; bcur < nbatch; qi++) {
+                const int64_t bnext = a.ctr ? (int64_t)gridDim.x + atomicAdd(a.ctr, 1) : bcur + gridDim.x;
+                publish(qi + 1, bnext);
+                bcur = bnext;
                 for (int tt = 0; tt < a.nb; tt++) {
                     int t = a.inverse ? a.nb - 1 - tt : tt;
                     const uint8_t* src = a.wpack + (int64_t)t * p.blk_bytes;
@@ -337,7 +361,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
             const int per1 = p.pair ? 2 : p.Cp / 16;   // k-steps per kernel row u (pair) / per tap
             const int per2 = p.MC / 16;
             unsigned long long w_x = 0, w_full = 0, w_hd = 0, t_start = clock64();
-            for (int64_t b = blockIdx.x; b < nbatch; b += gridDim.x) {
+            for (int qi = 0;; qi++) {
+                const int64_t b = bq_read(qi);
+                mbar_arrive(&bqe[qi & 3]);
+                if (b >= nbatch) break;
                 for (int tt = 0; tt < a.nb; tt++) {
                     TWAIT(w_x, mbar_wait(x_full, xph)); xph ^= 1;
                     fence_after();
@@ -523,11 +550,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
         };
         if (!esst && blockIdx.x < nbatch) prefetch_batch(blockIdx.x);
         float* sst = reinterpret_cast<float*>(smem + p.sstate_off);
-        for (int64_t b = blockIdx.x; b < nbatch; b += gridDim.x) {
+        for (int qi = 0;; qi++) {
+            const int64_t b = bq_read(qi);
+            if (b >= nbatch) break;
+            const int64_t bnext = bq_read(qi + 1);
+            mbar_arrive(&bqe[qi & 3]);
             long long tl0 = clock64();
             const int64_t img0 = b * p.I;
             const int nimg = (int)(a.n - img0 < (int64_t)p.I ? a.n - img0 : (int64_t)p.I);
-            if (!esst) prefetch_batch(b + gridDim.x);
+            if (!esst) prefetch_batch(bnext);
             // ---- (esst) copy the batch's fp32 state into shared memory
             if (esst) {
                 const int64_t nf = (int64_t)nimg * a.C * eHW;
@@ -1092,7 +1123,7 @@ static void prof_end(cudaStream_t st, int stage, double flops) {
     g_prof_open = nullptr;
 }
 
-ci_status_t umma_encoder_tail(const Model* m, float* zbuf, int64_t n, cudaStream_t st) {
+ci_status_t umma_encoder_tail(const Model* m, float* zbuf, int64_t n, int* ctr, cudaStream_t st) {
     const UmmaState* U = reinterpret_cast<const UmmaState*>(m->umma_state);
     if (!U || !U->has_enc) { set_error("no tcgen05 encoder plan"); return CI_ERR_UNSUPPORTED; }
     if (n == 0) return CI_OK;
@@ -1109,6 +1140,7 @@ ci_status_t umma_encoder_tail(const Model* m, float* zbuf, int64_t n, cudaStream
     a.inverse = 0;
     a.fmode = 1;
     a.dbg = nullptr;
+    a.ctr = ctr;
     int64_t nbatch = (n + a.p.I - 1) / a.p.I;
     int grid = (int)std::min<int64_t>(nbatch, 148);
     pick_kernel(a.p)<<<grid, kThreads, a.p.smem, st>>>(a);
@@ -1117,7 +1149,7 @@ ci_status_t umma_encoder_tail(const Model* m, float* zbuf, int64_t n, cudaStream
     return CI_OK;
 }
 
-ci_status_t umma_stage(const Model* m, int s, float* state, int64_t n, bool inverse, cudaStream_t st) {
+ci_status_t umma_stage(const Model* m, int s, float* state, int64_t n, bool inverse, int* ctr, cudaStream_t st) {
     if (n == 0) return CI_OK;
     const UmmaState* U = reinterpret_cast<const UmmaState*>(m->umma_state);
     StageArgs a;
@@ -1132,6 +1164,7 @@ ci_status_t umma_stage(const Model* m, int s, float* state, int64_t n, bool inve
     a.act = m->arch.act;
     a.inverse = inverse ? 1 : 0;
     a.fmode = 0;
+    a.ctr = ctr;
     static unsigned long long* dbg = nullptr;
     const bool debug_cycles = getenv("CI_DEBUG_CYCLES") != nullptr;
     if (debug_cycles && !dbg) cudaMalloc(&dbg, 148 * 16 * sizeof(unsigned long long));

@@ -301,6 +301,36 @@ def test_host_entry_point_matches_device(ci):
     assert np.array_equal(lb, g["labels"][:B * c.k])
 
 
+@pytest.mark.parametrize("B,learned", [(100, True), (515, False), (515, True)])
+def test_host_entry_point_chunked(ci, B, learned):
+    """The host-buffer entry pipelines PCIe copies with compute over 2 (B=100: 50+50) or 4
+    (B=515: 129+129+129+128) chunks on two compute streams; outputs are bit-identical to one
+    device-buffer call (per-image results do not depend on batch position), both heads."""
+    c = fx.CONFIGS["C4"]
+    k, arch = c.k, c.arch
+    params, x, drop = fx.make_weights(arch, c.seed_w), fx.make_inputs(arch, B, k, c.seed_x), \
+        fx.make_drops(B, k, c.seed_drop)
+    m = model(ci, arch, params, "bf16")
+    g = run_serve(ci, m, arch, x, drop, B, k, learned=learned)
+    ncls = sum(arch.heads)
+    hh = np.empty((B, k, arch.d), np.float32)
+    hp = np.empty((B, arch.d), np.float32)
+    lg = np.empty(B * k * ncls, np.float32)
+    lb = np.empty(B * k * len(arch.heads), np.int32)
+    ws = m.workspace(k, B, host=True)
+    m.ci_serve_group_host(x, drop, hh, hp, lg, lb, ws, learned=learned)
+    m.ci_check(ws)
+    assert np.array_equal(hh, g["R"]) and np.array_equal(hp, g["P"])
+    assert np.array_equal(lg, g["logits"]) and np.array_equal(lb, g["labels"])
+    # a bad drop index in the second chunk is counted (workspace 1) and reported by ci_check
+    bad = drop.copy()
+    bad[B - 1] = k + 3
+    m.ci_serve_group_host(x, bad, hh, hp, lg, lb, ws, learned=learned)
+    with pytest.raises(ci.CiError):
+        m.ci_check(ws)
+    m.ci_check(ws)   # cleared
+
+
 # ------------------------------------------------------------------ learned encoder (a3', C4)
 @pytest.mark.parametrize("prec", PRECS)
 def test_serve_learned_small_arch(ci, prec):
