@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcodedinv.so")
+# CI_LIB: load another build of the same ABI (same-box A/B timing of kernel variants)
+LIB_PATH = os.environ.get("CI_LIB") or os.path.join(_HERE, "libcodedinv.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`")

@@ -182,6 +182,39 @@ __global__ void __launch_bounds__(128) k_umma_rate_v1(int N, int iters, long lon
     if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
+// TMEM -> register read bandwidth: nw warps (warp w reads lane quarter w % 4), each loading
+// 32x32b.x16 (2 KB per warp-load) `iters` times; batch = loads in flight before tcgen05.wait::ld.
+__global__ void __launch_bounds__(512) k_tmem_ld_rate(int iters, int batch, long long* __restrict__ cycles,
+                                                      float* __restrict__ sink) {
+    __shared__ uint32_t tmem_base;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    if (warp == 0) tmem_alloc(&tmem_base, 512);
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = tmem_base + ((uint32_t)((warp & 3) * 32) << 16);
+    float acc = 0.f;
+    long long t0 = clock64();
+    for (int j = 0; j < iters; j += batch) {
+        float v[4][16];
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+            if (q < batch) tmem_ld16(tmem + (uint32_t)(((j + q) * 16 + warp * 64) & 511), v[q]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+            if (q < batch)
+#pragma unroll
+                for (int e = 0; e < 16; e++) acc += v[q][e];
+    }
+    __syncthreads();
+    if (tid == 0) cycles[blockIdx.x] = clock64() - t0;
+    if (acc == 12345.f) sink[tid] = acc;
+    fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem_base, 512);
+}
+
 }  // namespace ci
 
 using namespace ci;
@@ -206,6 +239,15 @@ ci_status_t ci_test_umma_rate(int32_t N, int32_t iters, int32_t nblocks, int64_t
                               ci_stream_t stream) {
     int32_t ntile = (N >> 16) & 0xFF, variant = N >> 24;
     N &= 0xFFFF;
+    if (variant == 15) {   // TMEM read bandwidth: N = warps (4..16), ntile = loads per wait (1..4)
+        const int nw = N, batch = ntile < 1 ? 1 : (ntile > 4 ? 4 : ntile);
+        if (nw < 1 || nw > 16 || iters < batch) { set_error("bad probe shape"); return CI_ERR_INVALID_ARG; }
+        static float* sink = nullptr;
+        if (!sink) CI_CUDA(cudaMalloc(&sink, 512 * sizeof(float)));
+        k_tmem_ld_rate<<<nblocks, nw * 32, 0, (cudaStream_t)stream>>>(iters, batch, (long long*)cycles, sink);
+        CI_CHECK_LAUNCH("k_tmem_ld_rate");
+        return CI_OK;
+    }
     if (variant == 0 && ntile == 0) {   // the reference tight loop
         if (N < 16 || N > 256 || N % 16 || iters < 1 || nblocks < 1) { set_error("bad probe shape"); return CI_ERR_INVALID_ARG; }
         size_t sm = (2 * 192 + 2 * 256) * 16;

@@ -196,11 +196,19 @@ struct SCfg {
 using SDyn = SCfg<0, 0, 0, 0, 0, 0, 0>;
 constexpr int kXchgBytes = 8 * 4 * 2 * 8 * 4;   // hst boundary exchange: [T<=8][quarter][2][8] fp32
 
+// Cycle instrumentation (CI_DEBUG_CYCLES; inactive unless requested).  -DCI_NO_CYCLES
+// compiles it out; same-box A/B showed no gain from that (s2 got slower), so it stays in.
+#ifdef CI_NO_CYCLES
+constexpr bool kCycles = false;
+#else
+constexpr bool kCycles = true;
+#endif
+#define CLK() (kCycles ? (long long)clock64() : 0ll)
 #define TWAIT(acc, call)                                      \
     do {                                                      \
-        long long t0_ = a.dbg ? clock64() : 0;                \
+        long long t0_ = (kCycles && a.dbg) ? CLK() : 0;       \
         call;                                                 \
-        if (a.dbg) acc += (unsigned long long)(clock64() - t0_); \
+        if (kCycles && a.dbg) acc += (unsigned long long)(CLK() - t0_); \
     } while (0)
 
 template <class CFG>
@@ -297,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
         if (lane == 0) {
             int slot = 0;
             uint32_t phase = 0;
-            unsigned long long w_empty = 0, t_start = clock64();
+            unsigned long long w_empty = 0, t_start = CLK();
             auto publish = [&](int i, int64_t v) {
                 mbar_wait(&bqe[i & 3], (uint32_t)(((i >> 2) & 1) ^ 1));
                 bq[i & 3] = v;
@@ -333,8 +341,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                     }
                 }
             }
-            if (a.dbg) {
-                a.dbg[blockIdx.x * 16 + 0] = clock64() - t_start;
+            if (kCycles && a.dbg) {
+                a.dbg[blockIdx.x * 16 + 0] = CLK() - t_start;
                 a.dbg[blockIdx.x * 16 + 1] = w_empty;
             }
         }
@@ -346,7 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
         // keeps them on the uniform datapath: no R2UR / waterfall in the inner loops.
         if (elect_one()) {
             int slot = 0;
-            uint32_t phase = 0, xph = 0, hph[2] = {0, 0};
+            uint32_t phase = 0, xph = 0, hph = 0;   // hph bit i: phase of hd_full[i]
             const uint32_t xb = smem_u32(xbuf) + (uint32_t)p.G * 16;
             const uint32_t hb = smem_u32(hbuf) + (uint32_t)p.G * 16;
             const uint32_t xlo_b = (uint32_t)(p.Cp / 8) * plane_bytes;   // lo planes (prec3)
@@ -360,7 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
             const uint32_t kb1 = (uint32_t)kstep_bytes(p.MC, p.prec3), kb2 = (uint32_t)kstep_bytes(p.Nc2, p.prec3);
             const int per1 = p.pair ? 2 : p.Cp / 16;   // k-steps per kernel row u (pair) / per tap
             const int per2 = p.MC / 16;
-            unsigned long long w_x = 0, w_full = 0, w_hd = 0, t_start = clock64();
+            unsigned long long w_x = 0, w_full = 0, w_hd = 0, t_start = CLK();
             for (int qi = 0;; qi++) {
                 const int64_t b = bq_read(qi);
                 mbar_arrive(&bqe[qi & 3]);
@@ -463,7 +471,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                     commit(acc1_full);
                     for (int j = 0; j < p.nch; j++) {
                         const int hbi = j & (p.nhd - 1);
-                        TWAIT(w_hd, mbar_wait(&hd_full[hbi], hph[hbi])); hph[hbi] ^= 1;
+                        TWAIT(w_hd, mbar_wait(&hd_full[hbi], (hph >> hbi) & 1u)); hph ^= 1u << hbi;
                         fence_after();
                         if (j + 1 < p.nch) {          // acc1 is free: epi1_j has read it
                             do_conv1(j + 1);
@@ -475,8 +483,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                     commit(acc2_full);
                 }
             }
-            if (a.dbg) {
-                a.dbg[blockIdx.x * 16 + 2] = clock64() - t_start;
+            if (kCycles && a.dbg) {
+                a.dbg[blockIdx.x * 16 + 2] = CLK() - t_start;
                 a.dbg[blockIdx.x * 16 + 3] = w_x;
                 a.dbg[blockIdx.x * 16 + 4] = w_full;
                 a.dbg[blockIdx.x * 16 + 5] = w_hd;
@@ -508,13 +516,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
         const int et = ew * 32 + lane;                 // 0..255
         const int row_in_tile = quarter * 32 + lane;
         const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
-        uint32_t a1ph = 0, a2ph = 0, heph[2] = {0, 0};
-        int hd_uses[2] = {0, 0};
+        uint32_t a1ph = 0, a2ph = 0, heph = 0;   // heph bit i: phase of hd_empty[i]
+        uint32_t hd_used = 0;                     // bit i: hidden buffer i has been filled before
         uint8_t* xlo_buf = xbuf + (size_t)(eCp / 8) * plane_bytes;
         const int cw1 = eMC / 2, cb1 = half * cw1;     // conv1 chunk columns of this half
         const int cw2 = eNC2 / 2, cb2 = half * cw2;    // conv2 columns of this half
         const bool any2 = cb2 < ec;                    // this half owns at least one real channel
-        unsigned long long w_a1 = 0, w_he = 0, w_a2 = 0, t_ld = 0, t_e1 = 0, t_e2 = 0, t_start = clock64();
+        unsigned long long w_a1 = 0, w_he = 0, w_a2 = 0, t_ld = 0, t_e1 = 0, t_e2 = 0, t_start = CLK();
         auto rowpix = [&](int r, int& ii, int& y, int& x) -> bool {
             const int band = r / eWp;
             x = r - band * eWp;
@@ -555,7 +563,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
             if (b >= nbatch) break;
             const int64_t bnext = bq_read(qi + 1);
             mbar_arrive(&bqe[qi & 3]);
-            long long tl0 = clock64();
+            long long tl0 = CLK();
             const int64_t img0 = b * p.I;
             const int nimg = (int)(a.n - img0 < (int64_t)p.I ? a.n - img0 : (int64_t)p.I);
             if (!esst) prefetch_batch(bnext);
@@ -586,7 +594,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                 fence_proxy_async();
                 mbar_arrive(x_full);
             }
-            t_ld += clock64() - tl0;
+            t_ld += CLK() - tl0;
             for (int tt = 0; tt < a.nb; tt++) {
                 const int t = a.inverse ? a.nb - 1 - tt : tt;
                 const int out_off = ((a.first_orient + t) & 1) == 0 ? ec : 0;
@@ -597,12 +605,58 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                     TWAIT(w_a1, mbar_wait(acc1_full, a1ph)); a1ph ^= 1;
                     fence_after();
                     const int hb_i = j & (p.nhd - 1);
-                    if (hd_uses[hb_i] > 0) { TWAIT(w_he, mbar_wait(&hd_empty[hb_i], heph[hb_i])); heph[hb_i] ^= 1; }
-                    hd_uses[hb_i]++;
+                    if ((hd_used >> hb_i) & 1u) {
+                        TWAIT(w_he, mbar_wait(&hd_empty[hb_i], (heph >> hb_i) & 1u));
+                        heph ^= 1u << hb_i;
+                    }
+                    hd_used |= 1u << hb_i;
                     uint8_t* hbuf_j = hbuf + (size_t)hb_i * hbuf_stride;
                     uint8_t* hlo_buf = hbuf_j + (size_t)(eMC / 8) * plane_bytes;
-                    long long te0 = clock64();
+                    long long te0 = CLK();
                     const float* bj = b1 + j * eMC + cb1;
+#ifndef CI_NO_EPI1_BATCH
+                    if constexpr (S && CFG::MC == 32) {
+                        // Batched TMEM reads: up to four LW-column loads in flight per wait::ld
+                        // (one load per wait is latency-bound at ~250 cycles), flattened over
+                        // (tile, column group); no registers stay live across batches.
+                        constexpr int CW1 = CFG::MC / 2;
+                        constexpr int LW = CW1 % 16 == 0 ? 16 : 8;
+                        constexpr int NG = CW1 / LW, NL = CFG::T * NG, LB = 2;
+#pragma unroll
+                        for (int q0 = 0; q0 < NL; q0 += LB) {
+                            float v[LB][LW];
+#pragma unroll
+                            for (int u = 0; u < LB; u++) {
+                                if (q0 + u >= NL) break;
+                                const int q = q0 + u, tile = q / NG, g = q % NG;
+                                const uint32_t ta = tmem + lane_addr + acc1_col0 + (uint32_t)(tile * CFG::MC + cb1 + g * LW);
+                                if constexpr (LW == 16) tmem_ld16(ta, v[u]); else tmem_ld8(ta, v[u]);
+                            }
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int u = 0; u < LB; u++) {
+                                if (q0 + u >= NL) break;
+                                const int q = q0 + u, tile = q / NG, g = q % NG;
+                                int r = tile * 128 + row_in_tile, ii, y, x;
+                                const bool valid = rowpix(r, ii, y, x) && ii < nimg;
+#pragma unroll
+                                for (int h = 0; h < LW / 8; h++) {
+                                    const float4 bA = __ldg(reinterpret_cast<const float4*>(bj + g * LW + h * 8));
+                                    const float4 bB = __ldg(reinterpret_cast<const float4*>(bj + g * LW + h * 8 + 4));
+                                    const float bb[8] = {bA.x, bA.y, bA.z, bA.w, bB.x, bB.y, bB.z, bB.w};
+                                    float h8[8];
+#pragma unroll
+                                    for (int e = 0; e < 8; e++) {
+                                        float hv = v[u][h * 8 + e] + bb[e];
+                                        if (a.act == 0) hv = fmaxf(hv, 0.f);
+                                        h8[e] = valid ? hv : 0.f;
+                                    }
+                                    store8(hbuf_j, hlo_buf, (cb1 + g * LW) / 8 + h, r, h8);
+                                }
+                            }
+                        }
+                    } else
+#endif
                     for (int tile = 0; tile < eT; tile++) {
                         int r = tile * 128 + row_in_tile, ii, y, x;
                         const bool valid = rowpix(r, ii, y, x) && ii < nimg;
@@ -639,7 +693,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                     fence_before();
                     fence_proxy_async();
                     mbar_arrive(&hd_full[hb_i]);
-                    t_e1 += clock64() - te0;
+                    t_e1 += CLK() - te0;
                 }
                 // ---- conv2 epilogue: s_out (+|-)= acc2 + b2 (fp32); bf16(s_out) -> X
                 const bool write_x = tt + 1 < a.nb;
@@ -650,7 +704,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                     // a small shared-memory exchange.  The two warp halves take alternate tiles.
                     TWAIT(w_a2, mbar_wait(acc2_full, a2ph)); a2ph ^= 1;
                     fence_after();
-                    long long te2h = clock64();
+                    long long te2h = CLK();
                     {
                         for (int tile = half; tile < eT; tile += 2) {
                             float za[16], zb[8];
@@ -712,7 +766,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                         }
                         asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
                     }
-                    t_e2 += clock64() - te2h;
+                    t_e2 += CLK() - te2h;
                 } else {
                 float oldv[OLDN];
                 auto load_old = [&](int tile) {
@@ -728,7 +782,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                 load_old(0);
                 TWAIT(w_a2, mbar_wait(acc2_full, a2ph)); a2ph ^= 1;
                 fence_after();
-                long long te2 = clock64();
+                long long te2 = CLK();
                 for (int tile = 0; tile < eT; tile++) {
                     int r = tile * 128 + row_in_tile, ii, y, x;
                     const bool valid = any2 && rowpix(r, ii, y, x) && ii < nimg;
@@ -772,7 +826,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                     }
                     if (tile + 1 < eT) load_old(tile + 1);
                 }
-                t_e2 += clock64() - te2;
+                t_e2 += CLK() - te2;
                 }
                 if (write_x) {
                     fence_before();
@@ -789,9 +843,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                 }
             }
         }
-        if (a.dbg && et == 0) {
+        if (kCycles && a.dbg && et == 0) {
             unsigned long long* o = a.dbg + blockIdx.x * 16;
-            o[6] = clock64() - t_start; o[7] = w_a1; o[8] = w_he; o[9] = w_a2;
+            o[6] = CLK() - t_start; o[7] = w_a1; o[8] = w_he; o[9] = w_a2;
             o[10] = t_ld; o[11] = t_e1; o[12] = t_e2;
         }
     }
@@ -1166,7 +1220,12 @@ ci_status_t umma_stage(const Model* m, int s, float* state, int64_t n, bool inve
     a.fmode = 0;
     a.ctr = ctr;
     static unsigned long long* dbg = nullptr;
-    const bool debug_cycles = getenv("CI_DEBUG_CYCLES") != nullptr;
+    const bool debug_cycles = getenv("CI_DEBUG_CYCLES") != nullptr && kCycles;
+    if (getenv("CI_DEBUG_CYCLES") && !kCycles) {
+        static bool warned = false;
+        if (!warned) fprintf(stderr, "[ci] CI_DEBUG_CYCLES: library built with CI_NO_CYCLES\n");
+        warned = true;
+    }
     if (debug_cycles && !dbg) cudaMalloc(&dbg, 148 * 16 * sizeof(unsigned long long));
     a.dbg = debug_cycles ? dbg : nullptr;
     if (a.dbg) cudaMemsetAsync(dbg, 0, 148 * 16 * sizeof(unsigned long long), st);
