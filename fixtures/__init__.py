@@ -81,20 +81,27 @@ class Arch:
     in_h: int
     in_w: int
     stages: tuple
-    act: str = "relu"            # "relu" | "identity"
+    act: str = "relu"            # "relu" | "elu" | "identity"
     first_orient: int = 0        # 0: block 0 does s_B += F(s_A); 1: s_A += F(s_B)
     heads: tuple = (10,)         # classes per linear head g_t
     gamma: float = 0.1           # gain on W2 (SURVEY §8a)
     encoder: tuple = ()          # learned encoder (Arch E): (c1, mid); () = none
+    # i-ResNet variant (SURVEY §8f f1): "residual" blocks y = x + G(x) on the whole state,
+    # each conv of G spectrally normalised to sqrt(lip) so Lip(G) <= lip < 1 (PAPER.md:169-170);
+    # h^-1 runs fp_iters fixed-point updates per block (the stated N)
+    block: str = "coupling"      # "coupling" | "residual"
+    lip: float = 0.9
+    fp_iters: int = 10
 
     def stage_shapes(self):
-        """[(C, H, W, c=C/2, m, n_blocks)] of each stage after its squeeze."""
+        """[(C, H, W, c, m, n_blocks)] of each stage after its squeeze; c = channels F acts on
+        (C/2 for coupling, C for residual)."""
         C, H, W = self.in_c, self.in_h, self.in_w
         out = []
         for st in self.stages:
             if st.squeeze_before:
                 C, H, W = C * 4, H // 2, W // 2
-            out.append((C, H, W, C // 2, st.mid, st.n_blocks))
+            out.append((C, H, W, C if self.block == "residual" else C // 2, st.mid, st.n_blocks))
         return out
 
     @property
@@ -104,7 +111,11 @@ class Arch:
 
     @property
     def act_id(self) -> int:
-        return {"relu": 0, "identity": 2}[self.act]
+        return {"relu": 0, "elu": 1, "identity": 2}[self.act]
+
+    @property
+    def block_id(self) -> int:
+        return {"coupling": 0, "residual": 1}[self.block]
 
 
 ARCH_T = Arch("T", 3, 8, 8, (Stage(1, 2, 16),))
@@ -117,14 +128,19 @@ ARCH_R = Arch("R", 2, 1, 1, (Stage(0, 3, 1),), act="identity", first_orient=1, h
 ARCH_CE = Arch("CE", 3, 32, 32, ARCH_C.stages, heads=(10, 2), encoder=(16, 64))
 # small encoder arch for fast oracle pins / GPU parity
 ARCH_TE = Arch("TE", 3, 8, 8, ARCH_T.stages, heads=(10, 2), encoder=(4, 8))
-ARCHS = {a.name: a for a in (ARCH_T, ARCH_M, ARCH_C, ARCH_R, ARCH_CE, ARCH_TE)}
+# i-ResNet variant of Arch C (f1): channel plan 12/48/192, m = 64/128/256, ELU, L = 0.9,
+# N = 10 fixed-point updates per block on the GPU (fp32-sufficient at L <= 0.9)
+ARCH_CR = Arch("CR", 3, 32, 32, ARCH_C.stages, act="elu", block="residual")
+ARCH_TR = Arch("TR", 3, 8, 8, (Stage(1, 2, 16),), act="elu", block="residual")
+ARCHS = {a.name: a for a in (ARCH_T, ARCH_M, ARCH_C, ARCH_R, ARCH_CE, ARCH_TE, ARCH_CR, ARCH_TR)}
 
 
 def linear_variant(arch: Arch) -> Arch:
     """Same shapes, identity activation (P1: h is linear when biases are 0)."""
     return Arch(arch.name + "lin", arch.in_c, arch.in_h, arch.in_w, arch.stages,
                 act="identity", first_orient=arch.first_orient, heads=arch.heads,
-                gamma=arch.gamma, encoder=arch.encoder)
+                gamma=arch.gamma, encoder=arch.encoder, block=arch.block, lip=arch.lip,
+                fp_iters=arch.fp_iters)
 
 
 # --------------------------------------------------------------------------
@@ -167,15 +183,60 @@ def n_params(arch: Arch) -> int:
 
 
 def make_weights(arch: Arch, seed: int, zero_bias: bool = False) -> np.ndarray:
-    """Flat fp32 parameter vector in canonical order (one splitmix64 stream per tensor)."""
+    """Flat fp32 parameter vector in canonical order (one splitmix64 stream per tensor).
+    Residual archs: each block conv is then scaled to spectral norm sqrt(arch.lip)."""
     parts = []
+    shapes = arch.stage_shapes()
     for tid, (name, shape, lo, hi) in enumerate(param_tensors(arch)):
         n = int(np.prod(shape))
         if zero_bias and (name.endswith(".b1") or name.endswith(".b2") or name.endswith(".b")):
             parts.append(np.zeros(n, np.float32))
-        else:
-            parts.append(uniform_f32(seed, tid + 1, n, lo, hi))
+            continue
+        w = uniform_f32(seed, tid + 1, n, lo, hi)
+        if arch.block == "residual" and name[0] == "s" and (name.endswith(".W1") or name.endswith(".W2")):
+            _, H, W = shapes[int(name[1:name.index("b")])][:3]
+            w4 = w.reshape(shape).astype(np.float64)
+            sigma = conv_spectral_norm(w4, H, W, seed=seed * 1000003 + tid)
+            w = (w4 * (math.sqrt(arch.lip) / sigma)).astype(np.float32).reshape(-1)
+        parts.append(w)
     return np.concatenate(parts) if parts else np.zeros(0, np.float32)
+
+
+# --------------------------------------------------------------------------
+# Spectral normalisation (weight preparation of the i-ResNet variant, PAPER.md:170 "bound
+# each layer's Lipschitz constant by normalizing the weight matrix by its spectral norm";
+# SURVEY §8c step 12: power iteration on conv / conv-transpose, 60 iterations).  This only
+# shapes the frozen random weights both sides receive; it is not on the hot path.
+# --------------------------------------------------------------------------
+def _conv_nobias(x, w):
+    """3x3 cross-correlation, zero padding 1: x [ci][H][W], w [co][ci][3][3] -> [co][H][W]."""
+    ci, H, W = x.shape
+    xp = np.zeros((ci, H + 2, W + 2))
+    xp[:, 1:-1, 1:-1] = x
+    out = np.zeros((w.shape[0], H, W))
+    for u in range(3):
+        for v in range(3):
+            out += np.tensordot(w[:, :, u, v], xp[:, u:u + H, v:v + W], axes=1)
+    return out
+
+
+def _conv_adjoint(y, w):
+    """Adjoint of _conv_nobias: y [co][H][W] -> [ci][H][W] (flipped, channel-swapped kernel)."""
+    return _conv_nobias(y, np.ascontiguousarray(w.transpose(1, 0, 2, 3)[:, :, ::-1, ::-1]))
+
+
+def conv_spectral_norm(w, H, W, iters=60, seed=0):
+    """Largest singular value of the zero-padded 3x3 conv operator on an H x W grid."""
+    v = uniform_f32(seed, 0, w.shape[1] * H * W, -1.0, 1.0).astype(np.float64).reshape(w.shape[1], H, W)
+    v /= np.linalg.norm(v)
+    sigma = 0.0
+    for _ in range(iters):
+        u = _conv_nobias(v, w)
+        sigma = np.linalg.norm(u)
+        u /= sigma
+        v = _conv_adjoint(u, w)
+        v /= np.linalg.norm(v)
+    return float(np.linalg.norm(_conv_nobias(v, w)))
 
 
 def split_params(arch: Arch, flat: np.ndarray) -> dict:

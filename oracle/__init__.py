@@ -33,7 +33,8 @@ class OrArch(ctypes.Structure):
                 ("n_blocks", ctypes.c_int * 4), ("mid", ctypes.c_int * 4),
                 ("act", ctypes.c_int), ("first_orient", ctypes.c_int),
                 ("n_heads", ctypes.c_int), ("head_classes", ctypes.c_int * 4),
-                ("enc_c1", ctypes.c_int), ("enc_mid", ctypes.c_int)]
+                ("enc_c1", ctypes.c_int), ("enc_mid", ctypes.c_int),
+                ("block_kind", ctypes.c_int), ("fp_iters", ctypes.c_int)]
 
 
 def to_orarch(arch) -> OrArch:
@@ -49,6 +50,8 @@ def to_orarch(arch) -> OrArch:
         a.head_classes[i] = c
     if arch.encoder:
         a.enc_c1, a.enc_mid = arch.encoder
+    a.block_kind = arch.block_id
+    a.fp_iters = 0            # residual inverse: iterate to the 1e-12 step tolerance
     return a
 
 
@@ -70,6 +73,8 @@ def lib():
         L.oracle_classify.argtypes = [P, P, ctypes.c_int, ctypes.c_long, P, P, P]
         L.oracle_serve_group.argtypes = [P, P, ctypes.c_int, ctypes.c_long, P, P] + [P] * 9 + [ctypes.c_int, ctypes.c_int]
         L.oracle_encode_learned.argtypes = [P, P, ctypes.c_int, ctypes.c_long, P, P, ctypes.c_int]
+        L.oracle_residual_inverse_block.restype = ctypes.c_int
+        L.oracle_residual_inverse_block.argtypes = [P, P] + [ctypes.c_int] * 4 + [P, P, ctypes.c_int, P, P]
         _lib = L
     return _lib
 
@@ -127,11 +132,13 @@ def forward_h(arch, params, x, nthreads=None):
     return out
 
 
-def inverse_h(arch, params, h, nthreads=None):
-    """h [n, d] -> x [n, C, H, W] (f64)."""
+def inverse_h(arch, params, h, nthreads=None, fp_iters=0):
+    """h [n, d] -> x [n, C, H, W] (f64).  Residual archs: fp_iters fixed-point updates per
+    block (0 = until the step is <= 1e-12, max 200)."""
     h = _f64(h)
     n = h.shape[0]
     a, p = to_orarch(arch), _f32(params)
+    a.fp_iters = fp_iters
     out = np.empty((n, arch.in_c, arch.in_h, arch.in_w))
     lib().oracle_inverse_h(ctypes.byref(a), _p(p), n, _p(h), _p(out), nthreads or default_threads())
     return out
@@ -167,6 +174,28 @@ def classify(arch, params, head, z):
     return logits, labels
 
 
+def residual_inverse_block(arch, params, stage, block, y, iters=0):
+    """Fixed-point inverse of one residual block (stage, block) on y [C, H, W]:
+    returns (x, number of updates)."""
+    y = _f64(y)
+    C, H, W = y.shape
+    m = arch.stages[stage].mid
+    a, p = to_orarch(arch), _f32(params)
+    off = 0
+    for s, (_, _, _, c, mm, nb) in enumerate(arch.stage_shapes()):
+        per = mm * c * 9 + mm + c * mm * 9 + c
+        if s == stage:
+            off += block * per
+            break
+        off += nb * per
+    x = np.empty_like(y)
+    tmp = np.empty_like(y)
+    hid = np.empty((m, H, W))
+    it = lib().oracle_residual_inverse_block(ctypes.byref(a), _p(p[off:]), C, m, H, W, _p(y), _p(x), iters,
+                                             _p(tmp), _p(hid))
+    return x, it
+
+
 def encode_learned(arch, params, x, nthreads=None):
     """Learned encoder (Arch E): x [B, k, C, H, W] -> x_p [B, C, H, W] (f64)."""
     x = _f64(x)
@@ -177,7 +206,7 @@ def encode_learned(arch, params, x, nthreads=None):
     return out
 
 
-def serve_group(arch, params, x, drop, nthreads=None, learned=False):
+def serve_group(arch, params, x, drop, nthreads=None, learned=False, fp_iters=0):
     """Whole coded path (exact encode, or the learned encoder when learned=True).
     x [B, k, C, H, W] fp32, drop [B] int32.
 
@@ -189,6 +218,7 @@ def serve_group(arch, params, x, drop, nthreads=None, learned=False):
     d = arch.d
     n = B * k
     a, p = to_orarch(arch), _f32(params)
+    a.fp_iters = fp_iters
     H = np.empty((B, k, d)); m = np.empty((B, d))
     xp = np.empty((B, arch.in_c, arch.in_h, arch.in_w)); P = np.empty((B, d)); R = np.empty((B, k, d))
     ncls = sum(arch.heads)

@@ -17,9 +17,17 @@
  *   conv3x3 ............... cross-correlation, zero padding 1, stride 1, bias
  *                           ("blocks of 3x3 convolutions",
  *                           BASELINE.json north_star)
- *   F = conv -> act -> conv (SURVEY Q3 reading; act = ReLU or identity)
+ *   F = conv -> act -> conv (SURVEY Q3 reading; act = ReLU, ELU or identity)
  *   additive coupling ..... s_B += F(s_A) / s_A += F(s_B), inverse by subtraction
  *                           in reverse order (i-RevNet)
+ *   i-ResNet residual ..... y = x + G(x), G = conv -> ELU -> conv on the whole state;
+ *                           inverse by the fixed-point iteration x <- y - G(x) from
+ *                           x_0 = y, which converges geometrically when Lip(G) < 1
+ *                           ("invert a residual block with an
+ *                           exponential convergence rate via fixed-point iteration",
+ *                           393, 408, 441 "solving fixed point equations"; stopping
+ *                           rule of SPEC.md:123, 147: step <= 1e-12 or 200 iterations,
+ *                           or a stated fixed count)
  *   h, h^-1 ............... stages of [psi, blocks]; no injective padding so h is
  *                           dimension preserving
  *   exact encode .......... m_b = (1/k) sum_i h(x_{b,i}); x_p = h^-1(m_b)
@@ -56,6 +64,9 @@ typedef struct {
     int n_heads;
     int head_classes[4];
     int enc_c1, enc_mid; /* learned encoder widths; 0 = no encoder */
+    int block_kind;      /* 0 = additive coupling on half the state, 1 = i-ResNet residual */
+    int fp_iters;        /* residual inverse: fixed-point iterations per block; 0 = until
+                            the step is <= 1e-12 (max 200) */
 } or_arch_t;
 
 /* ------------------------------------------------------------------------ */
@@ -80,7 +91,7 @@ static long block_offset(const or_arch_t* a, int s_target, int t_target) {
     for (int s = 0; s < a->n_stages; s++) {
         int C, H, W;
         stage_shape(a, s, &C, &H, &W);
-        long c = C / 2, m = a->mid[s];
+        long c = a->block_kind ? C : C / 2, m = a->mid[s];
         long per = m * c * 9 + m + c * m * 9 + c;
         for (int t = 0; t < a->n_blocks[s]; t++) {
             if (s == s_target && t == t_target) return off;
@@ -151,11 +162,38 @@ static void coupling_F(const or_arch_t* a, const float* blk, int c, int m, int H
     const float* W2 = b1 + m;
     const float* b2 = W2 + (long)c * m * 9;
     oracle_conv3x3(z, c, H, W, W1, b1, m, hid);
+    long n = (long)m * H * W;
     if (a->act == 0) {
-        long n = (long)m * H * W;
         for (long i = 0; i < n; i++) hid[i] = hid[i] > 0.0 ? hid[i] : 0.0;
+    } else if (a->act == 1) {   /* ELU(z) = z for z > 0, exp(z) - 1 otherwise (1-Lipschitz) */
+        for (long i = 0; i < n; i++) hid[i] = hid[i] > 0.0 ? hid[i] : expm1(hid[i]);
     }
     oracle_conv3x3(hid, m, H, W, W2, b2, c, out);
+}
+
+/* Inverse of one residual block y = x + G(x) by x <- y - G(x) from x_0 = y
+ * (PAPER.md:169).  iters > 0: exactly that many updates; iters == 0: until
+ * max|x_{i+1} - x_i| <= 1e-12 or 200 updates.  Returns the number of
+ * updates.  ybuf, tmp: [C][H][W]; hid: [m][H][W]. */
+int oracle_residual_inverse_block(const or_arch_t* a, const float* blk, int C, int m, int H, int W,
+                                  const double* y, double* x, int iters, double* tmp, double* hid) {
+    long n = (long)C * H * W;
+    memcpy(x, y, sizeof(double) * n);
+    int it = 0;
+    for (;;) {
+        if (iters > 0 && it == iters) break;
+        coupling_F(a, blk, C, m, H, W, x, hid, tmp);
+        double step = 0.0;
+        for (long i = 0; i < n; i++) {
+            double xn = y[i] - tmp[i];
+            double dlt = fabs(xn - x[i]);
+            if (dlt > step) step = dlt;
+            x[i] = xn;
+        }
+        it++;
+        if (iters == 0 && (step <= 1e-12 || it == 200)) break;
+    }
+    return it;
 }
 
 /* ------------------------------------------------------------------------ */
@@ -190,6 +228,14 @@ static void forward_one(const or_arch_t* a, const float* params, const double* x
         }
         int c = C / 2, m = a->mid[st];
         long half = (long)c * H * W;
+        if (a->block_kind == 1) {   /* i-ResNet: s <- s + G(s) */
+            long n = (long)C * H * W;
+            for (int t = 0; t < a->n_blocks[st]; t++) {
+                coupling_F(a, params + block_offset(a, st, t), C, m, H, W, s, hid, tmp);
+                for (long i = 0; i < n; i++) s[i] += tmp[i];
+            }
+            continue;
+        }
         for (int t = 0; t < a->n_blocks[st]; t++) {
             const float* blk = params + block_offset(a, st, t);
             int orient = (a->first_orient + t) & 1;
@@ -215,6 +261,14 @@ static void inverse_one(const or_arch_t* a, const float* params, const double* h
     for (int st = a->n_stages - 1; st >= 0; st--) {
         int c = C / 2, m = a->mid[st];
         long half = (long)c * H * W;
+        if (a->block_kind == 1) {   /* i-ResNet: blocks reversed, each by fixed point */
+            double* y = buf + 3 * mx;
+            for (int t = a->n_blocks[st] - 1; t >= 0; t--) {
+                memcpy(y, s, sizeof(double) * C * H * W);
+                oracle_residual_inverse_block(a, params + block_offset(a, st, t), C, m, H, W, y, s,
+                                              a->fp_iters, tmp, hid);
+            }
+        } else
         for (int t = a->n_blocks[st] - 1; t >= 0; t--) {
             const float* blk = params + block_offset(a, st, t);
             int orient = (a->first_orient + t) & 1;

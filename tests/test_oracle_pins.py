@@ -53,6 +53,11 @@ def torch_h(arch, params, x):
     for si, (C, H, W, c, m, nb) in enumerate(arch.stage_shapes()):
         if arch.stages[si].squeeze_before:
             s = Fnn.pixel_unshuffle(s, 2)
+        if arch.block == "residual":   # i-ResNet: s + G(s), G = conv -> ELU -> conv
+            for t in range(nb):
+                hid = Fnn.elu(Fnn.conv2d(s, p[f"s{si}b{t}.W1"], p[f"s{si}b{t}.b1"], padding=1))
+                s = s + Fnn.conv2d(hid, p[f"s{si}b{t}.W2"], p[f"s{si}b{t}.b2"], padding=1)
+            continue
         for t in range(nb):
             sa, sb = s[:, :c], s[:, c:]
             src, dst = (sa, sb) if ((arch.first_orient + t) & 1) == 0 else (sb, sa)
@@ -345,3 +350,106 @@ def test_serve_group_learned_decode_algebra():
     ref = 3 * out["P"] - (H * mask[..., None]).sum(1)
     assert rel(out["R"][bi, drop], ref) < 1e-13
     assert len(out["logits"]) == 2 and out["logits"][1].shape == (4, 3, 2)
+
+
+# ---------------------------------------------------------------- P7: i-ResNet variant (f1)
+ARCH_P7 = fx.Arch("P7", 1, 1, 1, (fx.Stage(0, 1, 1),), act="elu", block="residual", heads=())
+
+
+def p7_params():
+    """G(x) = 0.5 * ELU(x + 10) - 5 = 0.5 x for x > -10: on a 1x1 image only the
+    centre taps act; the off-centre taps are junk that zero padding must ignore."""
+    w1 = np.full((1, 1, 3, 3), 7.0, np.float32); w1[0, 0, 1, 1] = 1.0
+    w2 = np.full((1, 1, 3, 3), -3.0, np.float32); w2[0, 0, 1, 1] = 0.5
+    return np.concatenate([w1.ravel(), [10.0], w2.ravel(), [-5.0]]).astype(np.float32)
+
+
+def test_fixed_point_closed_form_rate_half():
+    """f(x) = 1.5 x: h(2) = 3; N updates of x <- 3 - 0.5 x from x_0 = 3 give exactly
+    2 + (-1/2)^N (dyadic, exact in f64); the converged inverse meets the 1e-12 step rule within
+    ceil(log(tol / |x_0 - x*|) / log L) + 2 updates."""
+    params = p7_params()
+    x = np.array([[[[2.0]]]])
+    assert oracle.forward_h(ARCH_P7, params, x)[0, 0] == 3.0
+    for N in (1, 2, 5, 10, 30):
+        xi, it = oracle.residual_inverse_block(ARCH_P7, params, 0, 0, np.array([[[3.0]]]), iters=N)
+        assert it == N and xi[0, 0, 0] == 2.0 + (-0.5) ** N
+        assert oracle.inverse_h(ARCH_P7, params, np.array([[3.0]]), fp_iters=N)[0, 0, 0, 0] == 2.0 + (-0.5) ** N
+    xi, it = oracle.residual_inverse_block(ARCH_P7, params, 0, 0, np.array([[[3.0]]]))
+    assert abs(xi[0, 0, 0] - 2.0) <= 1e-12 and it <= math.ceil(math.log(1e-12) / math.log(0.5)) + 2
+
+
+def test_spectral_norm_matches_svd_of_conv_operator():
+    """The fixtures' power iteration (weight prep) against the largest singular
+    value of the explicit zero-padded conv matrix (numpy SVD)."""
+    rng = np.random.default_rng(3)
+    for ci, co, H, W in ((12, 16, 4, 4), (5, 7, 3, 5)):
+        w = rng.standard_normal((co, ci, 3, 3))
+        A = np.zeros((co * H * W, ci * H * W))
+        for j in range(ci * H * W):
+            e = np.zeros(ci * H * W); e[j] = 1.0
+            A[:, j] = fx._conv_nobias(e.reshape(ci, H, W), w).ravel()
+        smax = np.linalg.svd(A, compute_uv=False)[0]
+        # power iteration approaches sigma_max from below (Rayleigh quotient of A^T A)
+        for iters, tol in ((200, 1e-6), (60, 2e-2)):
+            est = fx.conv_spectral_norm(w, H, W, iters=iters)
+            assert smax * (1 - tol) <= est <= smax * (1 + 1e-12), (iters, est, smax)
+        # the adjoint really is the transpose
+        y = rng.standard_normal((co, H, W))
+        assert np.allclose(fx._conv_adjoint(y, w).ravel(), A.T @ y.ravel(), atol=1e-12)
+
+
+def test_residual_h_matches_torch_composition():
+    arch = fx.ARCH_TR
+    params = fx.make_weights(arch, 5)
+    x = fx.make_inputs(arch, 3, 1, 9)[:, 0]
+    assert rel(oracle.forward_h(arch, params, x), torch_h(arch, params, x)) < 1e-12
+
+
+def test_residual_arch_c_one_image_matches_torch_composition():
+    arch = fx.ARCH_CR
+    params = fx.make_weights(arch, 13)
+    x = fx.make_inputs(arch, 1, 1, 3)[:, 0]
+    assert rel(oracle.forward_h(arch, params, x), torch_h(arch, params, x)) < 1e-12
+
+
+def test_residual_blocks_are_contractions():
+    """Lip(G) <= L = 0.9 for every block of Arch TR (spectral normalisation + 1-Lipschitz ELU):
+    random pairs, ||G(u) - G(v)||_2 <= L ||u - v||_2 (G from the oracle's own block: y - x)."""
+    arch = fx.ARCH_TR
+    params = fx.make_weights(arch, 5)
+    one = fx.Arch("TR1", 12, 4, 4, (fx.Stage(0, 1, 16),), act="elu", block="residual", heads=())
+    per = fx.n_params(one)
+    rng = np.random.default_rng(0)
+    for t in range(2):
+        blk = params[t * per:(t + 1) * per]
+        for _ in range(20):
+            u = rng.standard_normal((2, 12, 4, 4)) * rng.uniform(0.01, 3)
+            v = u + rng.standard_normal((2, 12, 4, 4)) * rng.uniform(1e-3, 1)
+            gu = oracle.forward_h(one, blk, u) - u.reshape(2, -1)
+            gv = oracle.forward_h(one, blk, v) - v.reshape(2, -1)
+            for i in range(2):
+                assert np.linalg.norm(gu[i] - gv[i]) <= arch.lip * np.linalg.norm((u - v)[i]) * (1 + 1e-9)
+
+
+def test_residual_round_trip_and_iteration_bound():
+    """h^-1(h(x)) = x for the converged fixed point; per-block update counts respect the
+    geometric bound ceil(log(tol / ||x_0 - x*||_inf) / log L) + 2."""
+    arch = fx.ARCH_TR
+    params = fx.make_weights(arch, 5)
+    x = fx.make_inputs(arch, 4, 1, 2)[:, 0]
+    h = oracle.forward_h(arch, params, x)
+    assert np.abs(oracle.inverse_h(arch, params, h) - x).max() < 1e-11
+    # block 1 of the only stage: y = h (as a state), x* = state before block 1
+    one = fx.Arch("TR1", 12, 4, 4, (fx.Stage(0, 1, 16),), act="elu", block="residual", heads=())
+    per = fx.n_params(one)
+    s0 = oracle.psi(x[0])                                   # state entering block 0
+    s1 = oracle.forward_h(one, params[:per], s0[None])[0].reshape(s0.shape)
+    y = oracle.forward_h(one, params[per:2 * per], s1[None])[0].reshape(s0.shape)
+    xs, it = oracle.residual_inverse_block(arch, params, 0, 1, y)
+    assert np.abs(xs - s1).max() < 1e-11
+    bound = math.ceil(math.log(1e-12 / np.abs(y - s1).max()) / math.log(arch.lip)) + 2
+    assert it <= bound, (it, bound)
+    # fixed N: error decays at least geometrically in N
+    errs = [np.abs(oracle.residual_inverse_block(arch, params, 0, 1, y, iters=N)[0] - s1).max() for N in (2, 4, 8)]
+    assert errs[0] > errs[1] > errs[2] and errs[2] <= arch.lip ** 8 * np.abs(y - s1).max()
