@@ -78,15 +78,16 @@ typedef enum {
 
 typedef struct {
     int32_t squeeze_before; /* 1: psi (space-to-depth r=2) before this stage's blocks */
-    int32_t n_blocks;       /* additive coupling blocks in the stage */
-    int32_t mid_channels;   /* m: F = conv3x3(c->m) -> act -> conv3x3(m->c), c = C/2 */
+    int32_t n_blocks;       /* blocks in the stage */
+    int32_t mid_channels;   /* m: F = conv3x3(c->m) -> act -> conv3x3(m->c); c = C/2 (coupling)
+                               or C (residual) */
 } ci_stage_t;
 
 typedef struct {
     int32_t in_c, in_h, in_w; /* input image shape */
     int32_t n_stages;         /* 1..4 */
     ci_stage_t stage[4];
-    int32_t act;              /* 0 = ReLU, 2 = identity */
+    int32_t act;              /* 0 = ReLU, 1 = ELU, 2 = identity */
     int32_t first_orientation;/* 0: block 0 of each stage does s_B += F(s_A); 1: s_A += F(s_B) */
     int32_t n_heads;          /* 0..4 linear heads g_t */
     int32_t head_classes[4];
@@ -94,6 +95,14 @@ typedef struct {
      * inputs, psi, ReLU(E2) (4 enc_c1 -> enc_mid), ReLU(E3) (enc_mid -> 4 enc_c1), psi^-1,
      * + skip(mean), E4 (enc_c1 -> in_c); all conv3x3 with bias */
     int32_t enc_c1, enc_mid;
+    /* block_kind 0: additive coupling on half the state (i-RevNet).
+     * block_kind 1: i-ResNet residual block y = x + F(x) on the whole state (PAPER.md:169-170,
+     *   393): the weights must make Lip(F) < 1 (spectral normalisation); h^-1
+     *   inverts each block by fp_iters >= 1 fixed-point updates x <- y - F(x) from x_0 = y
+     *   ("exponential convergence rate via fixed-point iteration", 408, 441).
+     *   first_orientation is ignored. */
+    int32_t block_kind;
+    int32_t fp_iters;
 } ci_arch_t;
 
 /* Thread-local description of the last non-OK status (never NULL). */

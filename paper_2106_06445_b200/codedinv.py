@@ -44,7 +44,8 @@ class CiArch(ctypes.Structure):
     _fields_ = [("in_c", ctypes.c_int32), ("in_h", ctypes.c_int32), ("in_w", ctypes.c_int32),
                 ("n_stages", ctypes.c_int32), ("stage", CiStage * 4), ("act", ctypes.c_int32),
                 ("first_orientation", ctypes.c_int32), ("n_heads", ctypes.c_int32),
-                ("head_classes", ctypes.c_int32 * 4), ("enc_c1", ctypes.c_int32), ("enc_mid", ctypes.c_int32)]
+                ("head_classes", ctypes.c_int32 * 4), ("enc_c1", ctypes.c_int32), ("enc_mid", ctypes.c_int32),
+                ("block_kind", ctypes.c_int32), ("fp_iters", ctypes.c_int32)]
 
 
 _P, _I32, _I64, _SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
@@ -118,6 +119,8 @@ def to_ci_arch(arch) -> CiArch:
         a.head_classes[i] = c
     if getattr(arch, "encoder", ()):
         a.enc_c1, a.enc_mid = arch.encoder
+    a.block_kind = {"coupling": 0, "residual": 1}[getattr(arch, "block", "coupling")]
+    a.fp_iters = getattr(arch, "fp_iters", 0) if a.block_kind else 0
     return a
 
 

@@ -70,8 +70,10 @@ static WsLayout ws_layout(const Model* m, int32_t k, int64_t B, bool groups = tr
     L.mean = off; off += up(sizeof(float) * (size_t)(Bg * m->d));
     L.xp = off; off += up(sizeof(float) * (size_t)(Bg * m->din));
     L.hidden = off;
-    if (m->prec == CI_PREC_SIMT)
-        off += up(sizeof(float) * (size_t)(std::min<int64_t>(std::max<int64_t>(n, 1), kSimtChunk) * m->max_hidden));
+    if (m->prec == CI_PREC_SIMT)   // hidden [chunk][max m*H*W] + (residual inverse) y copy [chunk][d]
+        off += m->arch.block_kind == 1
+                   ? sizeof(float) * (size_t)(kSimtChunk * m->max_hidden) + up(sizeof(float) * (size_t)(kSimtChunk * m->d))
+                   : up(sizeof(float) * (size_t)(std::min<int64_t>(std::max<int64_t>(n, 1), kSimtChunk) * m->max_hidden));
     L.enc = off;
     if (m->enc_off >= 0 && groups) {   // m, z, z2, z3, u of the learned encoder
         const int64_t HW = (int64_t)m->arch.in_h * m->arch.in_w;
@@ -93,6 +95,32 @@ static ci_status_t run_stage_blocks(const Model* m, int s, float* state, int64_t
     const StageInfo& S = m->st[s];
     if (m->umma) return umma_stage(m, s, state, n, inverse, ctr, st);
     const int64_t per = (int64_t)S.C * S.H * S.W, half = (int64_t)S.c * S.H * S.W;
+    if (m->arch.block_kind == 1) {   // i-ResNet: s += F(s); inverse: N x (x <- y - F(x))
+        const int64_t hstr = (int64_t)S.m * S.H * S.W;
+        float* ybuf = hidden + kSimtChunk * m->max_hidden;   // [chunk][C][H][W] copy of y
+        for (int tt = 0; tt < S.nb; tt++) {
+            int t = inverse ? S.nb - 1 - tt : tt;
+            const float* W1 = m->d_params + m->blk_off[m->blk_first[s] + t];
+            const float* b1 = W1 + (int64_t)S.m * S.c * 9;
+            const float* W2 = b1 + S.m;
+            const float* b2 = W2 + (int64_t)S.c * S.m * 9;
+            for (int64_t i0 = 0; i0 < n; i0 += kSimtChunk) {
+                int64_t nc = std::min<int64_t>(kSimtChunk, n - i0);
+                float* x = state + i0 * per;
+                if (!inverse) {
+                    CI_CUDA(launch_conv_simt(x, per, S.c, S.H, S.W, W1, b1, S.m, hidden, hstr, nc, 0, m->arch.act, st));
+                    CI_CUDA(launch_conv_simt(hidden, hstr, S.m, S.H, S.W, W2, b2, S.c, x, per, nc, 1, 0, st));
+                    continue;
+                }
+                CI_CUDA(cudaMemcpyAsync(ybuf, x, sizeof(float) * nc * per, cudaMemcpyDeviceToDevice, st));
+                for (int it = 0; it < m->arch.fp_iters; it++) {
+                    CI_CUDA(launch_conv_simt(x, per, S.c, S.H, S.W, W1, b1, S.m, hidden, hstr, nc, 0, m->arch.act, st));
+                    CI_CUDA(launch_conv_simt(hidden, hstr, S.m, S.H, S.W, W2, b2, S.c, x, per, nc, 3, 0, st, ybuf));
+                }
+            }
+        }
+        return CI_OK;
+    }
     for (int tt = 0; tt < S.nb; tt++) {
         int t = inverse ? S.nb - 1 - tt : tt;
         const float* blk = m->d_params + m->blk_off[m->blk_first[s] + t];
@@ -211,10 +239,12 @@ ci_status_t ci_model_create(const ci_arch_t* arch, const float* host_params, siz
     }
     const ci_arch_t& a = *arch;
     if (a.n_stages < 1 || a.n_stages > 4 || a.in_c < 1 || a.in_h < 1 || a.in_w < 1 ||
-        a.n_heads < 0 || a.n_heads > 4 || (a.act != 0 && a.act != 2)) {
+        a.n_heads < 0 || a.n_heads > 4 || a.act < 0 || a.act > 2 || a.block_kind < 0 || a.block_kind > 1 ||
+        (a.block_kind == 1 && (a.fp_iters < 1 || a.fp_iters > 1000))) {
         set_error("invalid arch descriptor");
         return CI_ERR_INVALID_SHAPE;
     }
+    const bool residual = a.block_kind == 1;
     Model* m = new Model();
     m->arch = a;
     m->prec = precision;
@@ -228,11 +258,11 @@ ci_status_t ci_model_create(const ci_arch_t* arch, const float* host_params, siz
             if (H % 2 || W % 2) { delete m; set_error("psi needs even H, W"); return CI_ERR_INVALID_SHAPE; }
             C *= 4; H /= 2; W /= 2;
         }
-        if (C % 2 || sg.n_blocks < 1 || sg.mid_channels < 1) {
+        if ((!residual && C % 2) || sg.n_blocks < 1 || sg.mid_channels < 1) {
             delete m; set_error("stage %d: odd channel count or empty stage", s); return CI_ERR_INVALID_SHAPE;
         }
         StageInfo& S = m->st[s];
-        S.C = C; S.H = H; S.W = W; S.c = C / 2; S.m = sg.mid_channels; S.nb = sg.n_blocks;
+        S.C = C; S.H = H; S.W = W; S.c = residual ? C : C / 2; S.m = sg.mid_channels; S.nb = sg.n_blocks;
         S.squeeze = sg.squeeze_before;
         m->blk_first.push_back((int)m->blk_off.size());
         for (int t = 0; t < S.nb; t++) {

@@ -64,12 +64,14 @@ void count_launch(int n = 1);
 // in: [n][C][H][W] of the SOURCE layout.  C,H,W are the source shape.
 cudaError_t launch_permute(const float* in, float* out, int64_t n, int C, int H, int W, int mode,
                            cudaStream_t s);
-// SIMT conv3x3 (NCHW, fp32): out = act(conv(in) + b)   (mode 0)
+// SIMT conv3x3 (NCHW, fp32): out = act(conv(in) + b)   (mode 0; act 0 ReLU, 1 ELU, 2 identity)
 //                            out += conv(in) + b       (mode 1)
 //                            out -= conv(in) + b       (mode 2)
+//                            out = base - conv(in) - b (mode 3, residual fixed-point update)
 cudaError_t launch_conv_simt(const float* in, int64_t in_stride, int Cin, int H, int W,
                              const float* Wt, const float* b, int Cout, float* out,
-                             int64_t out_stride, int64_t n, int mode, int act, cudaStream_t s);
+                             int64_t out_stride, int64_t n, int mode, int act, cudaStream_t s,
+                             const float* base = nullptr);
 cudaError_t launch_mean(const float* h, float* m, int k, int64_t B, int64_t d, cudaStream_t s);
 cudaError_t launch_decode(float* h, const float* p, const int32_t* drop, int k, int64_t B,
                           int64_t d, int* flag, cudaStream_t s);

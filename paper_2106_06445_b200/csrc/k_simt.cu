@@ -49,7 +49,7 @@ cudaError_t launch_permute(const float* in, float* out, int64_t n, int C, int H,
 __global__ void k_conv_simt(const float* __restrict__ in, int64_t in_stride, int Cin, int H, int W,
                             const float* __restrict__ Wt, const float* __restrict__ b, int Cout,
                             float* __restrict__ out, int64_t out_stride, int64_t n, int mode,
-                            int act) {
+                            int act, const float* __restrict__ base) {
     const int64_t per = (int64_t)Cout * H * W;
     const int64_t total = n * per;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -81,24 +81,28 @@ __global__ void k_conv_simt(const float* __restrict__ in, int64_t in_stride, int
         float* dst = out + img * out_stride + r;
         if (mode == 0) {
             if (act == 0) y = fmaxf(y, 0.f);
+            else if (act == 1) y = y > 0.f ? y : expm1f(y);   // ELU
             *dst = y;
         } else if (mode == 1) {
             *dst = *dst + y;
-        } else {
+        } else if (mode == 2) {
             *dst = *dst - y;
+        } else {   // 3: fixed-point update out = base - conv(in)   (base has out's layout)
+            *dst = base[img * out_stride + r] - y;
         }
     }
 }
 
 cudaError_t launch_conv_simt(const float* in, int64_t in_stride, int Cin, int H, int W,
                              const float* Wt, const float* b, int Cout, float* out,
-                             int64_t out_stride, int64_t n, int mode, int act, cudaStream_t s) {
+                             int64_t out_stride, int64_t n, int mode, int act, cudaStream_t s,
+                             const float* base) {
     int64_t total = n * (int64_t)Cout * H * W;
     if (total == 0) return cudaSuccess;
     int64_t blocks = (total + 255) / 256;
     if (blocks > 148 * 32) blocks = 148 * 32;
     k_conv_simt<<<(unsigned)blocks, 256, 0, s>>>(in, in_stride, Cin, H, W, Wt, b, Cout, out,
-                                                 out_stride, n, mode, act);
+                                                 out_stride, n, mode, act, base);
     count_launch();
     return cudaGetLastError();
 }

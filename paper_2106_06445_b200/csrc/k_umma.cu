@@ -74,6 +74,11 @@ struct StageArgs {
     int fmode;                // 0: s_out (+|-)= F(s_in) (coupling); 1: s_out = ReLU(F(s_in)) (encoder tail)
     unsigned long long* dbg;  // optional per-CTA cycle counters (CI_DEBUG_CYCLES), 16 per CTA
     int* ctr;                 // zeroed batch counter of this launch (dynamic batch claiming), or null
+    // i-ResNet residual blocks: F reads and updates the whole state (c = C).
+    // With inverse, each block is replayed fp_iters times as the fixed-point update
+    // x <- y - F(x) from x_0 = y: the state (= y) is only overwritten on the last replay, the
+    // intermediate iterates live in the bf16 X planes.
+    int residual, fp_iters;
     StagePlan p;
 };
 
@@ -291,6 +296,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
 
     const int64_t nbatch = (a.n + p.I - 1) / p.I;
     const int64_t HW = (int64_t)p.H * p.W;
+    // virtual blocks: R replays per block (R = fp_iters for the residual inverse, else 1)
+    const int R = (a.residual && a.inverse) ? a.fp_iters : 1;
+    const int nbv = a.nb * R;
     // Batches are claimed dynamically (first one = blockIdx.x, then an atomic counter), so
     // CTAs that start late -- e.g. while another stream's kernel still holds their SM --
     // simply take fewer batches.  Entry i of the queue is batch i of this CTA; the entry
@@ -317,8 +325,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                 const int64_t bnext = a.ctr ? (int64_t)gridDim.x + atomicAdd(a.ctr, 1) : bcur + gridDim.x;
                 publish(qi + 1, bnext);
                 bcur = bnext;
-                for (int tt = 0; tt < a.nb; tt++) {
-                    int t = a.inverse ? a.nb - 1 - tt : tt;
+                for (int tt = 0; tt < nbv; tt++) {
+                    int t = a.inverse ? a.nb - 1 - tt / R : tt / R;
                     const uint8_t* src = a.wpack + (int64_t)t * p.blk_bytes;
                     for (int q = 0; q < 2 * p.nch; q++) {
                         {
@@ -373,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                 const int64_t b = bq_read(qi);
                 mbar_arrive(&bqe[qi & 3]);
                 if (b >= nbatch) break;
-                for (int tt = 0; tt < a.nb; tt++) {
+                for (int tt = 0; tt < nbv; tt++) {
                     TWAIT(w_x, mbar_wait(x_full, xph)); xph ^= 1;
                     fence_after();
                     auto do_conv1 = [&](int j) {
@@ -579,7 +587,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
             // ---- load bf16(s_in) of the first processed block into the X planes (planes split by half)
             {
                 const int t0 = a.inverse ? a.nb - 1 : 0;
-                const int in_off = ((a.first_orient + t0) & 1) == 0 ? 0 : ec;
+                const int in_off = (a.residual || ((a.first_orient + t0) & 1) == 0) ? 0 : ec;
                 for (int tile = 0; tile < eT; tile++) {
                     int r = tile * 128 + row_in_tile, ii, y, x;
                     if (!rowpix(r, ii, y, x) || ii >= nimg) continue;
@@ -595,9 +603,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                 mbar_arrive(x_full);
             }
             t_ld += CLK() - tl0;
-            for (int tt = 0; tt < a.nb; tt++) {
-                const int t = a.inverse ? a.nb - 1 - tt : tt;
-                const int out_off = ((a.first_orient + t) & 1) == 0 ? ec : 0;
+            for (int tt = 0; tt < nbv; tt++) {
+                const int t = a.inverse ? a.nb - 1 - tt / R : tt / R;
+                const int out_off = a.residual ? 0 : (((a.first_orient + t) & 1) == 0 ? ec : 0);
+                // fixed-point replays before the last only refresh the X planes (the iterate)
+                const bool store_state = (tt % R) == R - 1;
                 const float* b1 = a.bias + (int64_t)t * (p.Mp + eNC2);
                 const float* b2 = b1 + p.Mp;
                 for (int j = 0; j < p.nch; j++) {
@@ -649,6 +659,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                     for (int e = 0; e < 8; e++) {
                                         float hv = v[u][h * 8 + e] + bb[e];
                                         if (a.act == 0) hv = fmaxf(hv, 0.f);
+                                        else if (a.act == 1) hv = hv > 0.f ? hv : expm1f(hv);
                                         h8[e] = valid ? hv : 0.f;
                                     }
                                     store8(hbuf_j, hlo_buf, (cb1 + g * LW) / 8 + h, r, h8);
@@ -684,6 +695,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 for (int e = 0; e < 8; e++) {
                                     float h = (q8 < 2 ? va[q8 * 8 + e] : vb[(q8 - 2) * 8 + e]) + bb[e];
                                     if (a.act == 0) h = fmaxf(h, 0.f);
+                                    else if (a.act == 1) h = h > 0.f ? h : expm1f(h);
                                     h8[e] = valid ? h : 0.f;
                                 }
                                 store8(hbuf_j, hlo_buf, (cb1 + g0) / 8 + q8, r, h8);
@@ -696,7 +708,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                     t_e1 += CLK() - te0;
                 }
                 // ---- conv2 epilogue: s_out (+|-)= acc2 + b2 (fp32); bf16(s_out) -> X
-                const bool write_x = tt + 1 < a.nb;
+                const bool write_x = tt + 1 < nbv;
                 if (ehst) {
                     // ---- horizontal tap stacking: acc2 row r holds Z_v[r][o] at column (v+1)*8+o;
                     // out[p][o] = Z_-1[p-1][o] + Z_0[p][o] + Z_+1[p+1][o]  (col2im over v).
@@ -757,7 +769,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                         const float f = (left[o] + za[8 + o] + right[o]) + __ldg(b2 + o);
                                         const float old = a.fmode ? 0.f : dst[(int64_t)o * eHW];
                                         nv = a.fmode ? fmaxf(f, 0.f) : (a.inverse ? old - f : old + f);
-                                        dst[(int64_t)o * eHW] = nv;
+                                        if (store_state) dst[(int64_t)o * eHW] = nv;
                                     }
                                     n8[o] = nv;
                                 }
@@ -767,6 +779,49 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                         asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
                     }
                     t_e2 += CLK() - te2h;
+                } else if (!S && (cw2 > 48 || (cw2 % 16 != 0 && cw2 != 8))) {
+                    // ---- generic widths (e.g. residual stages, c = 48 / 192): 16-column groups,
+                    // old state read in place
+                    TWAIT(w_a2, mbar_wait(acc2_full, a2ph)); a2ph ^= 1;
+                    fence_after();
+                    for (int tile = 0; tile < eT; tile++) {
+                        int r = tile * 128 + row_in_tile, ii, y, x;
+                        const bool valid = any2 && rowpix(r, ii, y, x) && ii < nimg;
+                        float* dst = stb + ((int64_t)(valid ? ii : 0) * a.C + out_off) * eHW + (valid ? y * eW + x : 0);
+                        for (int g = 0; g < cw2; g += 16) {
+                            const int n = cw2 - g < 16 ? cw2 - g : 16;
+                            float v[16];
+                            const uint32_t col = (uint32_t)(tile * eNC2 + cb2 + g);
+                            if (n == 16) {
+                                tmem_ld16(tmem + lane_addr + col, v);
+                            } else {
+                                float v8[8];
+                                tmem_ld8(tmem + lane_addr + col, v8);
+#pragma unroll
+                                for (int e = 0; e < 8; e++) v[e] = v8[e];
+                            }
+                            tmem_wait_ld();
+                            if (!valid) continue;
+                            for (int q8 = 0; q8 < n / 8; q8++) {
+                                const int o0 = cb2 + g + q8 * 8;
+                                if (o0 >= ec && !(write_x && o0 < eCp)) break;
+                                float n8[8];
+#pragma unroll
+                                for (int e = 0; e < 8; e++) {
+                                    const int o = o0 + e;
+                                    float nv = 0.f;
+                                    if (o < ec) {
+                                        const float f = v[q8 * 8 + e] + __ldg(b2 + o);
+                                        const float old = a.fmode ? 0.f : dst[(int64_t)o * eHW];
+                                        nv = a.fmode ? fmaxf(f, 0.f) : (a.inverse ? old - f : old + f);
+                                        if (store_state) dst[(int64_t)o * eHW] = nv;
+                                    }
+                                    n8[e] = nv;
+                                }
+                                if (write_x && o0 < eCp) store8(xbuf, xlo_buf, o0 / 8, r, n8);
+                            }
+                        }
+                    }
                 } else {
                 float oldv[OLDN];
                 auto load_old = [&](int tile) {
@@ -817,7 +872,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 if (o < ec) {
                                     const float f = acc + __ldg(b2 + o);
                                     nv = a.fmode ? fmaxf(f, 0.f) : (a.inverse ? oldv[q8 * 8 + e] - f : oldv[q8 * 8 + e] + f);
-                                    dst[(int64_t)o * eHW] = nv;
+                                    if (store_state) dst[(int64_t)o * eHW] = nv;
                                 }
                                 n8[e] = nv;
                             }
@@ -934,7 +989,7 @@ static bool make_plan(const StageInfo& S, bool prec3, StagePlan& best) {
                     const size_t smem0 = (size_t)nslot * slot_bytes + (size_t)P * ((p.Cp + nhd * MC) / 8) * Rtot * 16 +
                                          256 + kXchgBytes + 8 * (size_t)(9 * (p.Cp / 8 + 1) + 9 * (MC / 16));
                     if (smem0 > kSmemCap) continue;
-                    const size_t state_bytes = (size_t)I * 2 * p.c * p.H * p.W * 4;
+                    const size_t state_bytes = (size_t)I * S.C * p.H * p.W * 4;
                     const size_t soff = (smem0 + 127) / 128 * 128;
                     const int sst = soff + state_bytes <= kSmemCap ? 1 : 0;
                     // ---- cost per batch per block
@@ -1195,6 +1250,8 @@ ci_status_t umma_encoder_tail(const Model* m, float* zbuf, int64_t n, int* ctr, 
     a.fmode = 1;
     a.dbg = nullptr;
     a.ctr = ctr;
+    a.residual = 0;
+    a.fp_iters = 1;
     int64_t nbatch = (n + a.p.I - 1) / a.p.I;
     int grid = (int)std::min<int64_t>(nbatch, 148);
     pick_kernel(a.p)<<<grid, kThreads, a.p.smem, st>>>(a);
@@ -1219,6 +1276,8 @@ ci_status_t umma_stage(const Model* m, int s, float* state, int64_t n, bool inve
     a.inverse = inverse ? 1 : 0;
     a.fmode = 0;
     a.ctr = ctr;
+    a.residual = m->arch.block_kind == 1 ? 1 : 0;
+    a.fp_iters = a.residual ? m->arch.fp_iters : 1;
     static unsigned long long* dbg = nullptr;
     const bool debug_cycles = getenv("CI_DEBUG_CYCLES") != nullptr && kCycles;
     if (getenv("CI_DEBUG_CYCLES") && !kCycles) {
@@ -1233,7 +1292,7 @@ ci_status_t umma_stage(const Model* m, int s, float* state, int64_t n, bool inve
     int dev_sms = 148;
     int grid = (int)std::min<int64_t>(nbatch, dev_sms);
     const StageInfo& S = m->st[s];
-    double flops = (double)n * S.nb * 36.0 * S.H * S.W * S.c * S.m;
+    double flops = (double)n * S.nb * 36.0 * S.H * S.W * S.c * S.m * (a.residual && inverse ? a.fp_iters : 1);
     prof_begin(st);
     pick_kernel(a.p)<<<grid, kThreads, a.p.smem, st>>>(a);
     count_launch();
