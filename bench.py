@@ -96,7 +96,8 @@ class ClockSampler:
 def oracle_sample(cfg, params, x, drop, groups):
     import oracle
     t0 = time.perf_counter()
-    ref = oracle.serve_group(cfg.arch, params, x[groups], drop[groups], learned=bool(cfg.arch.encoder))
+    ref = oracle.serve_group(cfg.arch, params, x[groups], drop[groups], learned=bool(cfg.arch.encoder),
+                             fp_iters=cfg.arch.fp_iters)
     dt = time.perf_counter() - t0
     return ref, dt
 
@@ -114,11 +115,11 @@ def run_reference(args, rank, world):
     oracle.build()
     learned = bool(cfg.arch.encoder)
     for _ in range(args.warmup):
-        oracle.serve_group(cfg.arch, params, x, drop, learned=learned)
+        oracle.serve_group(cfg.arch, params, x, drop, learned=learned, fp_iters=cfg.arch.fp_iters)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        oracle.serve_group(cfg.arch, params, x, drop, learned=learned)
+        oracle.serve_group(cfg.arch, params, x, drop, learned=learned, fp_iters=cfg.arch.fp_iters)
         times.append(time.perf_counter() - t0)
     total = sum(times)
     value = S * args.steps / total
@@ -128,7 +129,7 @@ def run_reference(args, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": cfg.name, "k": cfg.k, "groups_per_step": S,
-                                            "arch": "C (3 stages x 9 coupling blocks)"},
+                                            "arch": fx.arch_summary(cfg.arch)},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -201,7 +202,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32", "simt"])
-    ap.add_argument("--config", default="C3", choices=["C3", "C4", "C5", "C2", "C1"])
+    ap.add_argument("--config", default="C3", choices=["C3", "C4", "C5", "C2", "C1", "C3R"])
     ap.add_argument("--encode", default="exact", choices=["exact", "learned"], help="C5 parity encode mode")
     ap.add_argument("--ref-groups", type=int, default=8, help="oracle sample groups per step")
     ap.add_argument("--cpu-groups", type=int, default=8, help="oracle sample for cpu_baseline")
@@ -485,7 +486,7 @@ def main():
                 "data": "synthetic",
                 "config": {"workload": cfg.name, "k": k, "groups_per_gpu": B, "global_groups": B * world,
                            "queries_per_group": k + 1, "image": "3x32x32",
-                           "arch": "C: 3 stages x 9 additive-coupling blocks (c=6/24/96, m=64/128/256)",
+                           "arch": fx.arch_summary(arch),
                            "encode": "exact h^-1(mean h)", "precision": args.precision,
                            "parallelism": f"group-sharded x{world}",
                            "l2": f"inputs rotate over {NBUF} resident buffer sets (x+outputs ~1 GB > L2)",

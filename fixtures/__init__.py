@@ -333,4 +333,21 @@ CONFIGS = {
     "C5": Config("C5", ARCH_CE, 7, 1024, 15, 5, 105,
                  "k=7 main + 1 parity worker, one per GPU (8 GPUs), exact or learned encode, "
                  "decode as a masked reduction over workers"),
+    # not a BASELINE config: the i-ResNet variant at C3's shape
+    "C3R": Config("C3R", ARCH_CR, 10, 1024, 16, 6, 106,
+                  "f1: C3 with i-ResNet residual blocks (12/48/192 channels, ELU, Lip 0.9); "
+                  "exact encode h^-1 by 10 fixed-point updates per block"),
 }
+
+
+def arch_summary(arch: Arch) -> str:
+    """One-line description of an arch for bench JSON lines."""
+    kind = "i-ResNet residual" if arch.block == "residual" else "additive-coupling"
+    sh = arch.stage_shapes()
+    s = (f"{arch.name}: {len(sh)} stages x {'/'.join(str(x[5]) for x in sh)} {kind} blocks "
+         f"(c={'/'.join(str(x[3]) for x in sh)}, m={'/'.join(str(x[4]) for x in sh)}, {arch.act})")
+    if arch.block == "residual":
+        s += f", h^-1 = {arch.fp_iters} fixed-point updates/block"
+    if arch.encoder:
+        s += f", learned encoder {arch.encoder}"
+    return s
