@@ -201,6 +201,34 @@ CI_API ci_status_t ci_worker_coef(ci_coef_kind_t kind, int32_t k, int64_t B, int
 CI_API ci_status_t ci_combine(int64_t B, int64_t d, const float* f, const float* coef, float* out,
                               ci_stream_t stream);
 
+/* ---- General (n, k) codes, n - k = r >= 1 parity tasks (Eq. 3, 563-597;
+ * SURVEY §8f f3) ----------------------------------------------------------------------------
+ * The generator is systematic: tasks 0..k-1 are the main queries (rows = I_k), task k+i is the
+ * parity query x_{k+i} = h^-1(sum_j c_{i,j} h(x_j)).  coef: DEVICE float
+ * [r][k] row-major c_{i,j}; any k rows of G must be full rank -- the caller
+ * guarantees it (decode flags a singular subset).  avail: DEVICE uint32 [B], bit s set when task
+ * s has a result (n <= 32).  Decode uses S = the k smallest available tasks and solves for the
+ * missing main tasks from the parity rows in S (fp64 p x p inverse per group, p = missing
+ * mains); available main results are left untouched.  Groups with fewer than k available tasks
+ * or a singular subset are left untouched and counted in the workspace flag (ci_check).
+ * Exact encode only (the learned encoder of a3' produces one parity query). */
+CI_API ci_status_t ci_workspace_size_general(const ci_model_t* model, int32_t k, int32_t r, int64_t B,
+                                             size_t* bytes);
+/* h [B][k][d] -> comb_out [B][r][d] (optional) and x_parity [B][r][C][H][W] */
+CI_API ci_status_t ci_encode_general(const ci_model_t* model, int32_t k, int32_t r, int64_t B,
+                                     const float* coef, const float* h, float* x_parity, float* comb_out,
+                                     void* ws, size_t ws_bytes, ci_stream_t stream);
+/* h [B][k][d] (in/out: missing main tasks overwritten), h_parity [B][r][d]; ws >= 256 B */
+CI_API ci_status_t ci_decode_general(int32_t k, int32_t r, int64_t B, int64_t d, const float* coef, float* h,
+                                     const float* h_parity, const uint32_t* avail, void* ws, size_t ws_bytes,
+                                     ci_stream_t stream);
+/* Whole path: h on B*k main queries -> encode r parity queries -> h on them -> decode ->
+ * heads on all B*k decoded features (logits/labels layout as ci_serve_group). */
+CI_API ci_status_t ci_serve_general(const ci_model_t* model, int32_t k, int32_t r, int64_t B, const float* coef,
+                                    const float* x, const uint32_t* avail, float* h_out, float* h_parity,
+                                    float* x_parity, float* logits, int32_t* labels, void* ws, size_t ws_bytes,
+                                    ci_stream_t stream);
+
 /* Per-group drop indices generated on the device, bit-identical to the fixtures' host
  * generator: drop[b] = (uint32)(splitmix64_at(seed, b) >> 32) % k (counter-based splitmix64;
  * one uniformly random lost main worker per group). */

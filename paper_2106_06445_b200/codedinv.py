@@ -30,7 +30,8 @@ PRECISIONS = {"fp32": CI_PREC_FP32, "bf16": CI_PREC_BF16, "simt": CI_PREC_SIMT}
 EXPORTS = ["ci_last_error", "ci_model_create", "ci_model_destroy", "ci_feature_dim",
            "ci_workspace_size", "ci_check", "ci_forward_h", "ci_inverse_h", "ci_encode",
            "ci_decode", "ci_classify", "ci_serve_group", "ci_workspace_size_host",
-           "ci_serve_group_host", "ci_make_drops", "ci_worker_coef", "ci_combine"]
+           "ci_serve_group_host", "ci_make_drops", "ci_worker_coef", "ci_combine",
+           "ci_workspace_size_general", "ci_encode_general", "ci_decode_general", "ci_serve_general"]
 TESTING_EXPORTS = ["ci_test_umma_gemm", "ci_test_umma_rate", "ci_test_prof_enable", "ci_test_prof_read",
                    "ci_test_launch_count", "ci_test_mean", "ci_test_plan"]  # include/codedinv_testing.h
 
@@ -67,6 +68,10 @@ _sig = {
     "ci_make_drops": (_I32, [_I32, _I64, ctypes.c_uint64, _P, _P]),
     "ci_worker_coef": (_I32, [_I32, _I32, _I64, _I32, _P, _P, _P]),
     "ci_combine": (_I32, [_I64, _I64, _P, _P, _P, _P]),
+    "ci_workspace_size_general": (_I32, [_P, _I32, _I32, _I64, _P]),
+    "ci_encode_general": (_I32, [_P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
+    "ci_decode_general": (_I32, [_I32, _I32, _I64, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
+    "ci_serve_general": (_I32, [_P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "ci_test_umma_gemm": (_I32, [_P, _I32, _I32, _P, _I32, _I32, _I32, _I32, _I32, _P, _P]),
     "ci_test_umma_rate": (_I32, [_I32, _I32, _I32, _P, _P]),
     "ci_test_prof_enable": (_I32, [_I32]),
@@ -161,6 +166,27 @@ class Model:
         n = self.workspace_size_host(k, B) if host else self.workspace_size(k, B)
         return torch.zeros(n, dtype=torch.uint8, device="cuda")
 
+    def workspace_general(self, k, r, B):
+        import torch
+        n = ctypes.c_size_t()
+        _check(_lib.ci_workspace_size_general(self._h, k, r, B, ctypes.byref(n)), "ci_workspace_size_general")
+        return torch.zeros(n.value, dtype=torch.uint8, device="cuda")
+
+    # ---- general (n, k) codes: coef [r][k] device fp32, avail [B] device uint32 (as int32)
+    def ci_encode_general(self, coef, h, x_parity, ws, comb_out=None, stream=None):
+        r, k = coef.shape
+        B = h.shape[0]
+        _check(_lib.ci_encode_general(self._h, k, r, B, _ptr(coef), _ptr(h), _ptr(x_parity), _ptr(comb_out),
+                                      _ptr(ws), ws.numel(), _stream(stream)), "ci_encode_general")
+
+    def ci_serve_general(self, coef, x, avail, h_out, h_parity, ws, x_parity=None, logits=None, labels=None,
+                         stream=None):
+        r, k = coef.shape
+        B = x.shape[0]
+        _check(_lib.ci_serve_general(self._h, k, r, B, _ptr(coef), _ptr(x), _ptr(avail), _ptr(h_out),
+                                     _ptr(h_parity), _ptr(x_parity), _ptr(logits), _ptr(labels), _ptr(ws),
+                                     ws.numel(), _stream(stream)), "ci_serve_general")
+
     # ---- ABI calls (same names as the C entry points)
     def ci_forward_h(self, x, h, ws, stream=None):
         _check(_lib.ci_forward_h(self._h, _ptr(x), _ptr(h), x.shape[0], _ptr(ws), ws.numel(),
@@ -202,6 +228,13 @@ def ci_decode(h, h_parity, drop, ws, stream=None):
     B, k, d = h.shape
     _check(_lib.ci_decode(k, B, d, _ptr(h), _ptr(h_parity), _ptr(drop), _ptr(ws), ws.numel(),
                           _stream(stream)), "ci_decode")
+
+
+def ci_decode_general(coef, h, h_parity, avail, ws, stream=None):
+    r, k = coef.shape
+    B, d = h.shape[0], h.shape[2]
+    _check(_lib.ci_decode_general(k, r, B, d, _ptr(coef), _ptr(h), _ptr(h_parity), _ptr(avail), _ptr(ws),
+                                  ws.numel(), _stream(stream)), "ci_decode_general")
 
 
 CI_COEF_DECODE, CI_COEF_MEAN = 0, 1

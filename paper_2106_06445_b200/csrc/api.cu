@@ -60,10 +60,11 @@ static int* next_ctr(void* ws, const WsLayout& L) {
 static constexpr int64_t kSimtChunk = 1024;
 
 // groups = false: layout of a plain h / h^-1 call on n = B*k images (no per-group buffers)
-static WsLayout ws_layout(const Model* m, int32_t k, int64_t B, bool groups = true) {
+// r: parity queries per group (1 for n = k + 1; general codes r = n - k)
+static WsLayout ws_layout(const Model* m, int32_t k, int64_t B, bool groups = true, int32_t r = 1) {
     WsLayout L;
-    int64_t n = B * (int64_t)k;
-    const int64_t Bg = groups ? std::max<int64_t>(B, 1) : 0;
+    int64_t n = B * (int64_t)std::max(k, r);
+    const int64_t Bg = groups ? std::max<int64_t>(B, 1) * r : 0;
     size_t off = 0;
     L.flag = off; off += up(256);
     L.scratch = off; off += up(sizeof(float) * (size_t)(std::max<int64_t>(n, 1) * m->d));
@@ -498,6 +499,88 @@ ci_status_t ci_serve_group(const ci_model_t* model, ci_encode_mode_t mode, int32
     int32_t* bp[4];
     head_ptrs(m, B * (int64_t)k, logits, labels, lp, bp);
     return serve_impl(m, mode, k, B, x, drop, h_out, h_parity, x_parity, lp, bp, ws, L, (cudaStream_t)stream);
+}
+
+// --- general (n, k) codes (f3) ------------------------------------------------------------
+static bool general_args_ok(int32_t k, int32_t r, int64_t B) {
+    return k >= 1 && r >= 1 && k + r <= 32 && B >= 0;
+}
+
+ci_status_t ci_workspace_size_general(const ci_model_t* model, int32_t k, int32_t r, int64_t B, size_t* bytes) {
+    const Model* m = reinterpret_cast<const Model*>(model);
+    if (!m || !bytes || !general_args_ok(k, r, B)) { set_error("invalid argument"); return CI_ERR_INVALID_ARG; }
+    *bytes = ws_layout(m, k, B, true, r).total;
+    return CI_OK;
+}
+
+ci_status_t ci_encode_general(const ci_model_t* model, int32_t k, int32_t r, int64_t B, const float* coef,
+                              const float* h, float* x_parity, float* comb_out, void* ws, size_t ws_bytes,
+                              ci_stream_t stream) {
+    CI_MODEL_OR_FAIL(m, model);
+    if (!general_args_ok(k, r, B) || (B > 0 && (!coef || !h || !x_parity || !aligned16(h) || !aligned16(x_parity) ||
+                                                 (comb_out && !aligned16(comb_out))))) {
+        set_error("invalid argument"); return CI_ERR_INVALID_ARG;
+    }
+    WsLayout L = ws_layout(m, k, B, true, r);
+    ci_status_t st_ = check_ws(L, ws, ws_bytes);
+    if (st_ != CI_OK) return st_;
+    if (B == 0) return CI_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    CI_CUDA(zero_ctrs(ws, L, st));
+    float* comb = comb_out ? comb_out : at<float>(ws, L.mean);
+    CI_CUDA(launch_combine_general(h, coef, comb, k, r, B, m->d, st));
+    return inverse_impl(m, comb, x_parity, B * r, ws, L, st);
+}
+
+ci_status_t ci_decode_general(int32_t k, int32_t r, int64_t B, int64_t d, const float* coef, float* h,
+                              const float* h_parity, const uint32_t* avail, void* ws, size_t ws_bytes,
+                              ci_stream_t stream) {
+    if (!general_args_ok(k, r, B) || d < 0 || (B > 0 && (!coef || !h || !h_parity || !avail))) {
+        set_error("invalid argument"); return CI_ERR_INVALID_ARG;
+    }
+    if (!ws || ws_bytes < 256 || !aligned16(ws)) { set_error("workspace too small"); return CI_ERR_WORKSPACE; }
+    CI_CUDA(launch_decode_general(h, h_parity, coef, avail, k, r, B, d, reinterpret_cast<int*>(ws),
+                                  (cudaStream_t)stream));
+    return CI_OK;
+}
+
+ci_status_t ci_serve_general(const ci_model_t* model, int32_t k, int32_t r, int64_t B, const float* coef,
+                             const float* x, const uint32_t* avail, float* h_out, float* h_parity,
+                             float* x_parity, float* logits, int32_t* labels, void* ws, size_t ws_bytes,
+                             ci_stream_t stream) {
+    CI_MODEL_OR_FAIL(m, model);
+    if (!general_args_ok(k, r, B) ||
+        (B > 0 && (!coef || !x || !avail || !h_out || !h_parity || !aligned16(x) || !aligned16(h_out) ||
+                   !aligned16(h_parity) || (x_parity && !aligned16(x_parity))))) {
+        set_error("invalid argument"); return CI_ERR_INVALID_ARG;
+    }
+    WsLayout L = ws_layout(m, k, B, true, r);
+    ci_status_t rc = check_ws(L, ws, ws_bytes);
+    if (rc != CI_OK) return rc;
+    if (B == 0) return CI_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    CI_CUDA(zero_ctrs(ws, L, st));
+    const int64_t n = B * (int64_t)k;
+    float* comb = at<float>(ws, L.mean);
+    float* xp = x_parity ? x_parity : at<float>(ws, L.xp);
+    rc = forward_impl(m, x, h_out, n, ws, L, st);                                // h on main queries
+    if (rc != CI_OK) return rc;
+    CI_CUDA(launch_combine_general(h_out, coef, comb, k, r, B, m->d, st));          // r weighted sums
+    rc = inverse_impl(m, comb, xp, B * r, ws, L, st);                             // ... through h^-1
+    if (rc != CI_OK) return rc;
+    rc = forward_impl(m, xp, h_parity, B * r, ws, L, st);                         // h on parity queries
+    if (rc != CI_OK) return rc;
+    CI_CUDA(launch_decode_general(h_out, h_parity, coef, avail, k, r, B, m->d, at<int>(ws, L.flag), st));
+    float* lp[4];
+    int32_t* bp[4];
+    head_ptrs(m, n, logits, labels, lp, bp);
+    for (int t = 0; t < m->arch.n_heads; t++) {
+        if (!lp[t] && !bp[t]) continue;
+        const float* W = m->d_head[t];
+        const float* b = W + (int64_t)m->arch.head_classes[t] * m->d;
+        CI_CUDA(launch_classify(h_out, n, m->d, W, b, m->arch.head_classes[t], lp[t], bp[t], st));
+    }
+    return CI_OK;
 }
 
 // --- host-buffer variant -----------------------------------------------------------------

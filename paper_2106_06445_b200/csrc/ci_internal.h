@@ -78,6 +78,11 @@ cudaError_t launch_decode(float* h, const float* p, const int32_t* drop, int k, 
 cudaError_t launch_classify(const float* z, int64_t n, int64_t d, const float* W, const float* b,
                             int C, float* logits, int32_t* labels, cudaStream_t s);
 cudaError_t launch_make_drops(int k, int64_t B, uint64_t seed, int32_t* drop, cudaStream_t s);
+// general (n, k) codes (k_codes.cu)
+cudaError_t launch_combine_general(const float* h, const float* coef, float* out, int k, int r, int64_t B,
+                                   int64_t d, cudaStream_t s);
+cudaError_t launch_decode_general(float* h, const float* hp, const float* coef, const uint32_t* avail, int k, int r,
+                                  int64_t B, int64_t d, int* flag, cudaStream_t s);
 cudaError_t launch_worker_coef(int kind, int k, int64_t B, int worker, const int32_t* drop, float* coef,
                                cudaStream_t s);
 cudaError_t launch_combine(int64_t B, int64_t d, const float* f, const float* coef, float* out, cudaStream_t s);
