@@ -412,6 +412,34 @@ def main():
                                          "h_parity, logits, labels inside the device-timed region"}
         del wsh
 
+    # --- bulk encoder-label generation (f4; "draw k random inputs and compute
+    #     labels f^-1(sum_j c_j f(x_j)) ... 50,000 times"): h on the k inputs + mean + h^-1 per
+    #     tuple, exact encode, 1024 tuples per call
+    label_gen = None
+    if not learned and rank == 0:
+        model = main_run["model"]
+        wsl = main_run["ws"]
+        hl = torch.empty(B, k, d, device=dev)
+        xl = torch.empty(B, arch.in_c, arch.in_h, arch.in_w, device=dev)
+        def gen(j):
+            model.ci_forward_h(xs[j].view(B * k, arch.in_c, arch.in_h, arch.in_w), hl.view(B * k, d), wsl)
+            model.ci_encode(hl, xl, wsl)
+        for j in range(3):
+            gen(j % NBUF)
+        torch.cuda.synchronize()
+        reps = 8
+        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_.record(stream)
+        for j in range(reps):
+            gen(j % NBUF)
+        b_.record(stream)
+        torch.cuda.synchronize()
+        lms = a_.elapsed_time(b_) / reps
+        label_gen = {"pairs_per_s": B / (lms / 1e3), "ms_per_1024": lms * 1024 / B,
+                     "seconds_for_50000": 50000 / (B / (lms / 1e3)),
+                     "note": "exact (x-tuple, h^-1(mean h)) training pairs for the learned encoder"}
+        del hl, xl
+
     # --- encoding overhead vs k (Figs. 6-7 analogue): encoder time / time of
     #     h on the k main queries, batch of 1024 groups, learned encoder only
     enc_over = None
@@ -498,6 +526,8 @@ def main():
         if enc_over is not None:
             line["encoder_overhead"] = enc_over
             line["config"]["encode"] = "learned encoder (Arch E), heads 10 + 2"
+        if label_gen:
+            line["label_generation"] = label_gen
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()

@@ -201,6 +201,15 @@ CI_API ci_status_t ci_worker_coef(ci_coef_kind_t kind, int32_t k, int64_t B, int
 CI_API ci_status_t ci_combine(int64_t B, int64_t d, const float* f, const float* coef, float* out,
                               ci_stream_t stream);
 
+/* Perturbed exact encode ("f(x_{k+1}) = sum_j c_j f(x_j) + eps",
+ * SPEC.md:192-200): x_parity = h^-1(mean_i h_i + eps) with a caller-supplied perturbation
+ * eps [B][d] (DEVICE fp32; e.g. i.i.d. N(0, sigma^2) drawn by the caller), modelling an
+ * approximate encoder.  Decoding such a parity amplifies eps by k (f^(x_a) = f(x_a) + k eps).
+ * eps = all zeros gives exactly ci_encode(CI_ENC_EXACT).  Same workspace as ci_encode. */
+CI_API ci_status_t ci_encode_perturbed(const ci_model_t* model, int32_t k, int64_t B, const float* h,
+                                       const float* eps, float* x_parity, float* mean_out, void* ws,
+                                       size_t ws_bytes, ci_stream_t stream);
+
 /* ---- General (n, k) codes, n - k = r >= 1 parity tasks (Eq. 3, 563-597;
  * SURVEY §8f f3) ----------------------------------------------------------------------------
  * The generator is systematic: tasks 0..k-1 are the main queries (rows = I_k), task k+i is the

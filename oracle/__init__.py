@@ -174,6 +174,13 @@ def classify(arch, params, head, z):
     return logits, labels
 
 
+def encode_perturbed(arch, params, H, eps, nthreads=None, fp_iters=0):
+    """Perturbed exact encode: m = mean_i H_i + eps,
+    x_p = h^-1(m).  H [B, k, d], eps [B, d] -> (m, x_p)."""
+    m = mean(H) + _f64(eps)
+    return m, inverse_h(arch, params, m, nthreads, fp_iters=fp_iters)
+
+
 def residual_inverse_block(arch, params, stage, block, y, iters=0):
     """Fixed-point inverse of one residual block (stage, block) on y [C, H, W]:
     returns (x, number of updates)."""

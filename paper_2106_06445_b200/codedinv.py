@@ -31,7 +31,8 @@ EXPORTS = ["ci_last_error", "ci_model_create", "ci_model_destroy", "ci_feature_d
            "ci_workspace_size", "ci_check", "ci_forward_h", "ci_inverse_h", "ci_encode",
            "ci_decode", "ci_classify", "ci_serve_group", "ci_workspace_size_host",
            "ci_serve_group_host", "ci_make_drops", "ci_worker_coef", "ci_combine",
-           "ci_workspace_size_general", "ci_encode_general", "ci_decode_general", "ci_serve_general"]
+           "ci_workspace_size_general", "ci_encode_general", "ci_decode_general", "ci_serve_general",
+           "ci_encode_perturbed"]
 TESTING_EXPORTS = ["ci_test_umma_gemm", "ci_test_umma_rate", "ci_test_prof_enable", "ci_test_prof_read",
                    "ci_test_launch_count", "ci_test_mean", "ci_test_plan"]  # include/codedinv_testing.h
 
@@ -69,6 +70,7 @@ _sig = {
     "ci_worker_coef": (_I32, [_I32, _I32, _I64, _I32, _P, _P, _P]),
     "ci_combine": (_I32, [_I64, _I64, _P, _P, _P, _P]),
     "ci_workspace_size_general": (_I32, [_P, _I32, _I32, _I64, _P]),
+    "ci_encode_perturbed": (_I32, [_P, _I32, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
     "ci_encode_general": (_I32, [_P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
     "ci_decode_general": (_I32, [_I32, _I32, _I64, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
     "ci_serve_general": (_I32, [_P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
@@ -171,6 +173,11 @@ class Model:
         n = ctypes.c_size_t()
         _check(_lib.ci_workspace_size_general(self._h, k, r, B, ctypes.byref(n)), "ci_workspace_size_general")
         return torch.zeros(n.value, dtype=torch.uint8, device="cuda")
+
+    def ci_encode_perturbed(self, h, eps, x_parity, ws, mean_out=None, stream=None):
+        B, k = h.shape[0], h.shape[1]
+        _check(_lib.ci_encode_perturbed(self._h, k, B, _ptr(h), _ptr(eps), _ptr(x_parity), _ptr(mean_out),
+                                        _ptr(ws), ws.numel(), _stream(stream)), "ci_encode_perturbed")
 
     # ---- general (n, k) codes: coef [r][k] device fp32, avail [B] device uint32 (as int32)
     def ci_encode_general(self, coef, h, x_parity, ws, comb_out=None, stream=None):

@@ -415,6 +415,23 @@ ci_status_t ci_encode(const ci_model_t* model, ci_encode_mode_t mode, int32_t k,
     return inverse_impl(m, mean, x_parity, B, ws, L, st);
 }
 
+ci_status_t ci_encode_perturbed(const ci_model_t* model, int32_t k, int64_t B, const float* h, const float* eps,
+                                float* x_parity, float* mean_out, void* ws, size_t ws_bytes, ci_stream_t stream) {
+    CI_MODEL_OR_FAIL(m, model);
+    if (k < 1 || B < 0 || (B > 0 && (!h || !eps || !x_parity || !aligned16(h) || !aligned16(eps) ||
+                                     !aligned16(x_parity) || (mean_out && !aligned16(mean_out))))) {
+        set_error("invalid argument"); return CI_ERR_INVALID_ARG;
+    }
+    WsLayout L = ws_layout(m, k, B);
+    ci_status_t r = check_ws(L, ws, ws_bytes);
+    if (r != CI_OK) return r;
+    cudaStream_t st = (cudaStream_t)stream;
+    CI_CUDA(zero_ctrs(ws, L, st));
+    float* mean = mean_out ? mean_out : at<float>(ws, L.mean);
+    CI_CUDA(launch_mean(h, mean, k, B, m->d, st, eps));
+    return inverse_impl(m, mean, x_parity, B, ws, L, st);
+}
+
 ci_status_t ci_decode(int32_t k, int64_t B, int64_t d, float* h, const float* h_parity,
                       const int32_t* drop, void* ws, size_t ws_bytes, ci_stream_t stream) {
     if (k < 1 || B < 0 || d < 0 ||

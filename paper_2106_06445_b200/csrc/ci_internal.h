@@ -72,7 +72,9 @@ cudaError_t launch_conv_simt(const float* in, int64_t in_stride, int Cin, int H,
                              const float* Wt, const float* b, int Cout, float* out,
                              int64_t out_stride, int64_t n, int mode, int act, cudaStream_t s,
                              const float* base = nullptr);
-cudaError_t launch_mean(const float* h, float* m, int k, int64_t B, int64_t d, cudaStream_t s);
+// m = (sum_i h_i) / k  (+ eps when given: perturbed encode, f4)
+cudaError_t launch_mean(const float* h, float* m, int k, int64_t B, int64_t d, cudaStream_t s,
+                        const float* eps = nullptr);
 cudaError_t launch_decode(float* h, const float* p, const int32_t* drop, int k, int64_t B,
                           int64_t d, int* flag, cudaStream_t s);
 cudaError_t launch_classify(const float* z, int64_t n, int64_t d, const float* W, const float* b,

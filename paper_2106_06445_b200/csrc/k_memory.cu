@@ -20,7 +20,7 @@ __device__ __forceinline__ float4 ld_stream(const float4* p) {
 // (SURVEY Q7 reading; c_{1,j} = 1/k).
 template <int KMAX>
 __global__ void __launch_bounds__(256) k_mean(const float4* __restrict__ h, float4* __restrict__ m,
-                                              int k, int64_t B, int64_t d4) {
+                                              int k, int64_t B, int64_t d4, const float4* __restrict__ eps) {
     const int64_t total = B * d4;
     const float fk = (float)k;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -46,8 +46,13 @@ __global__ void __launch_bounds__(256) k_mean(const float4* __restrict__ h, floa
                 acc.z = __fadd_rn(acc.z, t.z); acc.w = __fadd_rn(acc.w, t.w);
             }
         }
-        m[idx] = make_float4(__fdiv_rn(acc.x, fk), __fdiv_rn(acc.y, fk), __fdiv_rn(acc.z, fk),
-                             __fdiv_rn(acc.w, fk));
+        float4 r = make_float4(__fdiv_rn(acc.x, fk), __fdiv_rn(acc.y, fk), __fdiv_rn(acc.z, fk),
+                               __fdiv_rn(acc.w, fk));
+        if (eps) {   // perturbed encode (f4): mean + eps
+            const float4 e4 = ld_stream(eps + idx);
+            r.x = __fadd_rn(r.x, e4.x); r.y = __fadd_rn(r.y, e4.y); r.z = __fadd_rn(r.z, e4.z); r.w = __fadd_rn(r.w, e4.w);
+        }
+        m[idx] = r;
     }
 }
 
@@ -59,13 +64,15 @@ static int grid_for(int64_t total, int block) {
 }
 
 // scalar variants (d % 4 != 0, e.g. the 2-D rotation pin)
-__global__ void k_mean_scalar(const float* __restrict__ h, float* __restrict__ m, int k, int64_t B, int64_t d) {
+__global__ void k_mean_scalar(const float* __restrict__ h, float* __restrict__ m, int k, int64_t B, int64_t d,
+                              const float* __restrict__ eps) {
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < B * d;
          idx += (int64_t)gridDim.x * blockDim.x) {
         int64_t b = idx / d, e = idx - b * d;
         float acc = 0.f;
         for (int i = 0; i < k; i++) acc = __fadd_rn(acc, h[(b * k + i) * d + e]);
-        m[idx] = __fdiv_rn(acc, (float)k);
+        const float r = __fdiv_rn(acc, (float)k);
+        m[idx] = eps ? __fadd_rn(r, eps[idx]) : r;
     }
 }
 __global__ void k_decode_scalar(float* __restrict__ h, const float* __restrict__ p, const int32_t* __restrict__ drop,
@@ -83,10 +90,10 @@ __global__ void k_decode_scalar(float* __restrict__ h, const float* __restrict__
     }
 }
 
-cudaError_t launch_mean(const float* h, float* m, int k, int64_t B, int64_t d, cudaStream_t s) {
+cudaError_t launch_mean(const float* h, float* m, int k, int64_t B, int64_t d, cudaStream_t s, const float* eps) {
     if (d % 4) {
         if (B * d == 0) return cudaSuccess;
-        k_mean_scalar<<<grid_for(B * d, 256), 256, 0, s>>>(h, m, k, B, d);
+        k_mean_scalar<<<grid_for(B * d, 256), 256, 0, s>>>(h, m, k, B, d, eps);
         count_launch();
         return cudaGetLastError();
     }
@@ -95,10 +102,11 @@ cudaError_t launch_mean(const float* h, float* m, int k, int64_t B, int64_t d, c
     int g = grid_for(total, 256);
     auto H = reinterpret_cast<const float4*>(h);
     auto M = reinterpret_cast<float4*>(m);
-    if (k <= 4) k_mean<4><<<g, 256, 0, s>>>(H, M, k, B, d4);
-    else if (k <= 10) k_mean<10><<<g, 256, 0, s>>>(H, M, k, B, d4);
-    else if (k <= 16) k_mean<16><<<g, 256, 0, s>>>(H, M, k, B, d4);
-    else k_mean<0><<<g, 256, 0, s>>>(H, M, k, B, d4);
+    auto E = reinterpret_cast<const float4*>(eps);
+    if (k <= 4) k_mean<4><<<g, 256, 0, s>>>(H, M, k, B, d4, E);
+    else if (k <= 10) k_mean<10><<<g, 256, 0, s>>>(H, M, k, B, d4, E);
+    else if (k <= 16) k_mean<16><<<g, 256, 0, s>>>(H, M, k, B, d4, E);
+    else k_mean<0><<<g, 256, 0, s>>>(H, M, k, B, d4, E);
     count_launch();
     return cudaGetLastError();
 }

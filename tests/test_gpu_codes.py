@@ -177,3 +177,40 @@ def test_serve_general_arch_c_sampled(ci, prec):
     print(f"[serve_general C (12,10) {prec}] amp={amp:.3g} " + " ".join(f"{a}={b:.3g}" for a, b in e.items()))
     tol = TOL[prec]
     assert e["P"] < tol and e["R"] < tol * amp and e["logits"] < tol * amp
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_perturbed_encode_and_k_eps_law(ci, prec):
+    """f4: x_p = h^-1(mean + eps) on the GPU vs the oracle; eps = 0 reproduces ci_encode bit for
+    bit; decoding the perturbed parity returns f(x_a) + k eps."""
+    arch = fx.ARCH_M
+    k, B = 4, 64
+    params = fx.make_weights(arch, 2)
+    x = fx.make_inputs(arch, B, k, 6)
+    m = ci.Model(arch, params, prec)
+    ws = m.workspace(k, B)
+    h = torch.empty(B, k, arch.d, device="cuda")
+    m.ci_forward_h(dev(x.reshape(B * k, *x.shape[2:])), h.view(B * k, arch.d), ws)
+    xp0 = torch.empty(B, arch.in_c, arch.in_h, arch.in_w, device="cuda")
+    xpz = torch.empty_like(xp0)
+    m.ci_encode(h, xp0, ws)
+    m.ci_encode_perturbed(h, torch.zeros(B, arch.d, device="cuda"), xpz, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(xp0, xpz)
+    eps = (1e-2 * np.random.default_rng(3).standard_normal((B, arch.d))).astype(np.float32)
+    xp = torch.empty_like(xp0)
+    m.ci_encode_perturbed(h, dev(eps), xp, ws)
+    _, xref = oracle.encode_perturbed(arch, params, h.cpu().numpy().astype(np.float64), eps)
+    e_xp = relerr_rows(xp.cpu().numpy().reshape(B, -1), xref.reshape(B, -1))
+    P = torch.empty(B, arch.d, device="cuda")
+    m.ci_forward_h(xp, P, ws)
+    drop = (np.arange(B) % k).astype(np.int32)
+    R = h.clone()
+    ci.ci_decode(R, P, dev(drop), ws)
+    torch.cuda.synchronize()
+    Hn, Rn = h.cpu().numpy().astype(np.float64), R.cpu().numpy().astype(np.float64)
+    err = Rn[np.arange(B), drop] - Hn[np.arange(B), drop]
+    law = np.max(np.abs(err - k * eps)) / np.max(np.abs(k * eps))
+    print(f"[perturbed {prec}] xp={e_xp:.3g} k-eps-law residual={law:.3g}")
+    assert e_xp < TOL[prec]
+    assert law < (2e-2 if prec != "bf16" else 1.0)

@@ -453,3 +453,24 @@ def test_residual_round_trip_and_iteration_bound():
     # fixed N: error decays at least geometrically in N
     errs = [np.abs(oracle.residual_inverse_block(arch, params, 0, 1, y, iters=N)[0] - s1).max() for N in (2, 4, 8)]
     assert errs[0] > errs[1] > errs[2] and errs[2] <= arch.lip ** 8 * np.abs(y - s1).max()
+
+
+# ---------------------------------------------------------------- f4: perturbed encode
+def test_perturbed_encode_zero_noise_and_k_eps_law():
+    """sigma = 0 is the ideal encode bitwise; through an exactly invertible f,
+    h(x_p) = mean + eps, so decoding the lost slot returns f(x_a) + k eps."""
+    arch = fx.ARCH_T
+    params = fx.make_weights(arch, 3)
+    B, k = 6, 4
+    x = fx.make_inputs(arch, B, k, 2)
+    H = oracle.forward_h(arch, params, x.reshape(B * k, *x.shape[2:])).reshape(B, k, -1)
+    m0, xp0 = oracle.encode_perturbed(arch, params, H, np.zeros((B, arch.d)))
+    assert np.array_equal(xp0, oracle.inverse_h(arch, params, oracle.mean(H)))
+    eps = 1e-2 * np.random.default_rng(1).standard_normal((B, arch.d))
+    m, xp = oracle.encode_perturbed(arch, params, H, eps)
+    P = oracle.forward_h(arch, params, xp)
+    assert np.max(np.abs(P - (oracle.mean(H) + eps))) < 1e-12
+    drop = np.arange(B, dtype=np.int32) % k
+    R = oracle.decode(H, P, drop)
+    err = R[np.arange(B), drop] - H[np.arange(B), drop]
+    assert np.max(np.abs(err - k * eps)) < 1e-11
