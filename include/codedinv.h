@@ -210,6 +210,23 @@ CI_API ci_status_t ci_encode_perturbed(const ci_model_t* model, int32_t k, int64
                                        const float* eps, float* x_parity, float* mean_out, void* ws,
                                        size_t ws_bytes, ci_stream_t stream);
 
+/* Online decoding for n = k + 1 (App. C).  Results reach the
+ * decoder one task at a time; each call applies one "wave" of at most one completion event
+ * per group:
+ *   est   [B][k][d] DEVICE fp32 best-effort estimates f^(x_i) (zero before the first event);
+ *   state [B]       DEVICE uint64 (zero initially): bits 0..k = tasks received, bits 32..32+k-1
+ *                   = estimates finalised;
+ *   task  [B]       DEVICE int32: the task completing for group b in this wave (0..k-1 main,
+ *                   k = parity), or -1 for none;  value [B][d] DEVICE fp32: its result.
+ * Rule (App. C, with the third case read as "when the parity task completes", DESIGN.md R-f2a):
+ * a main task j sets f^(x_j) = value (final) and subtracts value from every unfinalised
+ * estimate; the parity adds k*value to every unfinalised estimate.  After k distinct tasks all
+ * estimates are final (= ci_decode's result); later events change nothing.  A repeated task
+ * is ignored and counted in the workspace flag (ci_check).  k <= 31; ws >= 256 B. */
+CI_API ci_status_t ci_online_update(int32_t k, int64_t B, int64_t d, float* est, uint64_t* state,
+                                    const int32_t* task, const float* value, void* ws, size_t ws_bytes,
+                                    ci_stream_t stream);
+
 /* ---- General (n, k) codes, n - k = r >= 1 parity tasks (Eq. 3, 563-597;
  * SURVEY §8f f3) ----------------------------------------------------------------------------
  * The generator is systematic: tasks 0..k-1 are the main queries (rows = I_k), task k+i is the

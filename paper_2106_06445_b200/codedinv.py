@@ -32,7 +32,7 @@ EXPORTS = ["ci_last_error", "ci_model_create", "ci_model_destroy", "ci_feature_d
            "ci_decode", "ci_classify", "ci_serve_group", "ci_workspace_size_host",
            "ci_serve_group_host", "ci_make_drops", "ci_worker_coef", "ci_combine",
            "ci_workspace_size_general", "ci_encode_general", "ci_decode_general", "ci_serve_general",
-           "ci_encode_perturbed"]
+           "ci_encode_perturbed", "ci_online_update"]
 TESTING_EXPORTS = ["ci_test_umma_gemm", "ci_test_umma_rate", "ci_test_prof_enable", "ci_test_prof_read",
                    "ci_test_launch_count", "ci_test_mean", "ci_test_plan"]  # include/codedinv_testing.h
 
@@ -71,6 +71,7 @@ _sig = {
     "ci_combine": (_I32, [_I64, _I64, _P, _P, _P, _P]),
     "ci_workspace_size_general": (_I32, [_P, _I32, _I32, _I64, _P]),
     "ci_encode_perturbed": (_I32, [_P, _I32, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
+    "ci_online_update": (_I32, [_I32, _I64, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
     "ci_encode_general": (_I32, [_P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
     "ci_decode_general": (_I32, [_I32, _I32, _I64, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
     "ci_serve_general": (_I32, [_P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
@@ -242,6 +243,13 @@ def ci_decode_general(coef, h, h_parity, avail, ws, stream=None):
     B, d = h.shape[0], h.shape[2]
     _check(_lib.ci_decode_general(k, r, B, d, _ptr(coef), _ptr(h), _ptr(h_parity), _ptr(avail), _ptr(ws),
                                   ws.numel(), _stream(stream)), "ci_decode_general")
+
+
+def ci_online_update(k, est, state, task, value, ws, stream=None):
+    """est [B][k][d] fp32, state [B] int64 (uint64 bits), task [B] int32, value [B][d] fp32."""
+    B, d = est.shape[0], est.shape[2]
+    _check(_lib.ci_online_update(k, B, d, _ptr(est), _ptr(state), _ptr(task), _ptr(value), _ptr(ws),
+                                 ws.numel(), _stream(stream)), "ci_online_update")
 
 
 CI_COEF_DECODE, CI_COEF_MEAN = 0, 1

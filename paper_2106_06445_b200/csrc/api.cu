@@ -432,6 +432,17 @@ ci_status_t ci_encode_perturbed(const ci_model_t* model, int32_t k, int64_t B, c
     return inverse_impl(m, mean, x_parity, B, ws, L, st);
 }
 
+ci_status_t ci_online_update(int32_t k, int64_t B, int64_t d, float* est, uint64_t* state, const int32_t* task,
+                             const float* value, void* ws, size_t ws_bytes, ci_stream_t stream) {
+    if (k < 1 || k > 31 || B < 0 || d < 0 || (B > 0 && (!est || !state || !task || !value || !aligned16(est) ||
+                                                      !aligned16(value)))) {
+        set_error("invalid argument"); return CI_ERR_INVALID_ARG;
+    }
+    if (!ws || ws_bytes < 256 || !aligned16(ws)) { set_error("workspace too small"); return CI_ERR_WORKSPACE; }
+    CI_CUDA(launch_online_update(k, B, d, est, state, task, value, reinterpret_cast<int*>(ws), (cudaStream_t)stream));
+    return CI_OK;
+}
+
 ci_status_t ci_decode(int32_t k, int64_t B, int64_t d, float* h, const float* h_parity,
                       const int32_t* drop, void* ws, size_t ws_bytes, ci_stream_t stream) {
     if (k < 1 || B < 0 || d < 0 ||

@@ -80,6 +80,9 @@ cudaError_t launch_decode(float* h, const float* p, const int32_t* drop, int k, 
 cudaError_t launch_classify(const float* z, int64_t n, int64_t d, const float* W, const float* b,
                             int C, float* logits, int32_t* labels, cudaStream_t s);
 cudaError_t launch_make_drops(int k, int64_t B, uint64_t seed, int32_t* drop, cudaStream_t s);
+// online decoding (k_online.cu)
+cudaError_t launch_online_update(int k, int64_t B, int64_t d, float* est, uint64_t* state, const int32_t* task,
+                                 const float* value, int* flag, cudaStream_t s);
 // general (n, k) codes (k_codes.cu)
 cudaError_t launch_combine_general(const float* h, const float* coef, float* out, int k, int r, int64_t B,
                                    int64_t d, cudaStream_t s);
