@@ -209,6 +209,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-alt", action="store_true", help="skip the other-precision throughput line item")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the standalone HBM / online-decode / label-generation line items")
     ap.add_argument("--inflight", type=int, default=2, choices=[1, 2],
                     help="request batches in flight (2: consecutive steps alternate between two CUDA streams)")
     args = ap.parse_args()
@@ -345,7 +347,7 @@ def main():
 
     # --- HBM roofline of encode-mean / decode: standalone, L2-cold, 1.1 GB working set
     hbm = {}
-    if rank == 0:
+    if rank == 0 and not args.no_extras:
         Bd = 8192
         Hb = torch.empty(Bd, k, d, device=dev).uniform_()
         Pb = torch.empty(Bd, d, device=dev).uniform_()
@@ -376,6 +378,46 @@ def main():
                          "frac": byts / (t / 1e3) / 1e9 / peaks["hbm_gbs"],
                          "note": "L2 flushed (256 MB write) before each launch"}
         del Hb, Pb, flush
+        # online decoding (f2): the wave that completes every group (the only
+        # decode work on the critical path) vs the batch decode, 1024 groups, L2 flushed
+        online = {}
+        flush = torch.empty(256 * 1024 * 1024 // 4, device=dev)
+
+        def t_of(fn, setup=None):
+            ts = []
+            for it in range(5):
+                flush.zero_()
+                if setup:
+                    setup()
+                torch.cuda.synchronize()
+                a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a_.record(stream)
+                fn()
+                b_.record(stream)
+                torch.cuda.synchronize()
+                if it >= 1:
+                    ts.append(a_.elapsed_time(b_))
+            return float(np.median(ts)) * 1e3
+
+        for kk in (2, 4, 10, 30):
+            Bo = 1024
+            est = torch.zeros(Bo, kk, d, device=dev)
+            val = torch.randn(Bo, d, device=dev)
+            Hk = torch.randn(Bo, kk, d, device=dev)
+            Dk = torch.zeros(Bo, dtype=torch.int32, device=dev)
+            rec = ((1 << kk) - 1) & ~1          # mains 1..k-1 in, main 0 missing, parity pending
+            state0 = torch.full((Bo,), (rec << 32) | rec, dtype=torch.int64, device=dev)
+            st_ = state0.clone()
+            task = torch.full((Bo,), kk, dtype=torch.int32, device=dev)
+            wso = torch.zeros(256, dtype=torch.uint8, device=dev)
+            online[f"k={kk}"] = {
+                "completing_event_us": t_of(lambda: ci.ci_online_update(kk, est, st_, task, val, wso),
+                                            setup=lambda: st_.copy_(state0)),
+                "batch_decode_us": t_of(lambda: ci.ci_decode(Hk, val, Dk, wso))}
+        hbm["online_decode"] = {"groups": 1024, "per_k": online,
+                                "note": "completing event = the parity arrives after k-1 mains: one fma "
+                                        "per element of the missing estimate; batch = k P - sum of k-1 mains"}
+        del flush
 
     # --- e2e through the host-buffer C-ABI call (pinned host memory, copies in the region)
     e2e = None
@@ -416,7 +458,7 @@ def main():
     #     labels f^-1(sum_j c_j f(x_j)) ... 50,000 times"): h on the k inputs + mean + h^-1 per
     #     tuple, exact encode, 1024 tuples per call
     label_gen = None
-    if not learned and rank == 0:
+    if not learned and rank == 0 and not args.no_extras:
         model = main_run["model"]
         wsl = main_run["ws"]
         hl = torch.empty(B, k, d, device=dev)

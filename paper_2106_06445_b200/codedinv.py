@@ -84,6 +84,8 @@ _sig = {
     "ci_test_plan": (_I32, [_I32, _I32, _I32, _I32, _I32, _P]),
 }
 for _name, (_res, _args) in _sig.items():
+    if os.environ.get("CI_LIB") and not hasattr(_lib, _name):
+        continue   # A/B build of an older revision (scripts/ab_build.py): newer entry points absent
     _f = getattr(_lib, _name)
     _f.restype, _f.argtypes = _res, _args
 

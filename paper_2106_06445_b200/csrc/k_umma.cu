@@ -296,8 +296,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
 
     const int64_t nbatch = (a.n + p.I - 1) / p.I;
     const int64_t HW = (int64_t)p.H * p.W;
-    // virtual blocks: R replays per block (R = fp_iters for the residual inverse, else 1)
-    const int R = (a.residual && a.inverse) ? a.fp_iters : 1;
+    // virtual blocks: R replays per block (R = fp_iters for the residual inverse, else 1).
+    // Residual / ELU code exists only in the generic kernel (pick_kernel routes them there).
+    constexpr bool kGen = !CFG::kStatic;
+    const bool residual = kGen && a.residual;
+    const int R = (residual && a.inverse) ? a.fp_iters : 1;
     const int nbv = a.nb * R;
     // Batches are claimed dynamically (first one = blockIdx.x, then an atomic counter), so
     // CTAs that start late -- e.g. while another stream's kernel still holds their SM --
@@ -587,7 +590,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
             // ---- load bf16(s_in) of the first processed block into the X planes (planes split by half)
             {
                 const int t0 = a.inverse ? a.nb - 1 : 0;
-                const int in_off = (a.residual || ((a.first_orient + t0) & 1) == 0) ? 0 : ec;
+                const int in_off = (residual || ((a.first_orient + t0) & 1) == 0) ? 0 : ec;
                 for (int tile = 0; tile < eT; tile++) {
                     int r = tile * 128 + row_in_tile, ii, y, x;
                     if (!rowpix(r, ii, y, x) || ii >= nimg) continue;
@@ -605,9 +608,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
             t_ld += CLK() - tl0;
             for (int tt = 0; tt < nbv; tt++) {
                 const int t = a.inverse ? a.nb - 1 - tt / R : tt / R;
-                const int out_off = a.residual ? 0 : (((a.first_orient + t) & 1) == 0 ? ec : 0);
+                const int out_off = residual ? 0 : (((a.first_orient + t) & 1) == 0 ? ec : 0);
                 // fixed-point replays before the last only refresh the X planes (the iterate)
-                const bool store_state = (tt % R) == R - 1;
+                const bool store_state = !kGen || (tt % R) == R - 1;
                 const float* b1 = a.bias + (int64_t)t * (p.Mp + eNC2);
                 const float* b2 = b1 + p.Mp;
                 for (int j = 0; j < p.nch; j++) {
@@ -659,7 +662,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                     for (int e = 0; e < 8; e++) {
                                         float hv = v[u][h * 8 + e] + bb[e];
                                         if (a.act == 0) hv = fmaxf(hv, 0.f);
-                                        else if (a.act == 1) hv = hv > 0.f ? hv : expm1f(hv);
+                                        else if (kGen && a.act == 1) hv = hv > 0.f ? hv : expm1f(hv);
                                         h8[e] = valid ? hv : 0.f;
                                     }
                                     store8(hbuf_j, hlo_buf, (cb1 + g * LW) / 8 + h, r, h8);
@@ -695,7 +698,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 for (int e = 0; e < 8; e++) {
                                     float h = (q8 < 2 ? va[q8 * 8 + e] : vb[(q8 - 2) * 8 + e]) + bb[e];
                                     if (a.act == 0) h = fmaxf(h, 0.f);
-                                    else if (a.act == 1) h = h > 0.f ? h : expm1f(h);
+                                    else if (kGen && a.act == 1) h = h > 0.f ? h : expm1f(h);
                                     h8[e] = valid ? h : 0.f;
                                 }
                                 store8(hbuf_j, hlo_buf, (cb1 + g0) / 8 + q8, r, h8);
@@ -1117,8 +1120,10 @@ static const SpecEntry kSpecs[] = {
     CI_SPEC(17, 64, 32, 64, 3, 1, 16384, 16, 64, 0),  // learned-encoder tail (E2, E3), bf16x3
 };
 
-static StageKernel pick_kernel(const StagePlan& p) {
-    if (!getenv("CI_NO_STATIC"))
+// Specialised kernels are built for the additive-coupling ReLU/identity shapes only; residual
+// blocks and ELU (f1) always take the generic kernel, which is the only one carrying that code.
+static StageKernel pick_kernel(const StagePlan& p, const StageArgs& a) {
+    if (!getenv("CI_NO_STATIC") && !a.residual && a.act != 1)
         for (const auto& e : kSpecs)
             if (e.Wp == p.Wp && e.Cp == p.Cp && e.MC == p.MC && e.Nc2 == p.Nc2 && e.T == p.T && e.p3 == p.prec3 &&
                 e.slot == p.slot_bytes && e.H == p.H && e.c == p.c && e.sst == p.sstate)
@@ -1254,7 +1259,7 @@ ci_status_t umma_encoder_tail(const Model* m, float* zbuf, int64_t n, int* ctr, 
     a.fp_iters = 1;
     int64_t nbatch = (n + a.p.I - 1) / a.p.I;
     int grid = (int)std::min<int64_t>(nbatch, 148);
-    pick_kernel(a.p)<<<grid, kThreads, a.p.smem, st>>>(a);
+    pick_kernel(a.p, a)<<<grid, kThreads, a.p.smem, st>>>(a);
     count_launch();
     CI_CHECK_LAUNCH("k_stage (encoder tail)");
     return CI_OK;
@@ -1294,7 +1299,7 @@ ci_status_t umma_stage(const Model* m, int s, float* state, int64_t n, bool inve
     const StageInfo& S = m->st[s];
     double flops = (double)n * S.nb * 36.0 * S.H * S.W * S.c * S.m * (a.residual && inverse ? a.fp_iters : 1);
     prof_begin(st);
-    pick_kernel(a.p)<<<grid, kThreads, a.p.smem, st>>>(a);
+    pick_kernel(a.p, a)<<<grid, kThreads, a.p.smem, st>>>(a);
     count_launch();
     CI_CHECK_LAUNCH("k_stage");
     prof_end(st, s, flops);
