@@ -58,6 +58,8 @@ struct StagePlan {
     size_t smem;
     int tmem_cols;
     double est_cycles;     // planner's cost estimate (cycles per image per block)
+    int fold;              // 1: conv1 bias folded into the MMA via a constant-1 input channel
+                           //    (channel c of the padded X planes, Cp > c); epilogue adds none
     int hst;               // conv2 "horizontal tap stacking": N = 3 taps x 8 outputs (c <= 8),
                            // 3 vertical k-steps per 16 hidden channels, col2im in the epilogue
     int nhd;               // hidden plane buffers (2: double-buffered, conv1/epilogue overlap conv2)
@@ -187,6 +189,7 @@ struct SCfg {
     static constexpr int RTOT = T * 128 + 2 * G;
     static constexpr int PLANE16 = RTOT;                 // plane bytes / 16
     static constexpr bool PAIR = CP == 8;
+    static constexpr bool FOLD = CP_ > C_;   // == StagePlan::fold
     static constexpr int PER1 = PAIR ? 2 : CP / 16;
     static constexpr int K1 = PAIR ? 6 : 9 * (CP / 16);
     static constexpr int PER2 = MC / 16;
@@ -519,6 +522,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
         const int eG = S ? CFG::G : p.G;
         const bool esst = S ? (CFG::SST != 0) : (p.sstate != 0);
         const bool ehst = S ? CFG::HST : (p.hst != 0);
+        const bool efold = S ? CFG::FOLD : (p.fold != 0);   // X channel ec = 1 on valid pixels
         const int64_t eHW = (int64_t)eH * eW;
         constexpr int OLDN = S ? (CFG::NC2 / 2 > 0 ? CFG::NC2 / 2 : 8) : 48;
         const int ew = warp - 2;                       // 0..7
@@ -598,7 +602,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                     for (int pl = half; pl < eCp / 8; pl += 2) {
                         float v8[8];
 #pragma unroll
-                        for (int e = 0; e < 8; e++) v8[e] = (pl * 8 + e < ec) ? src[(int64_t)(pl * 8 + e) * eHW] : 0.f;
+                        for (int e = 0; e < 8; e++)
+                            v8[e] = (pl * 8 + e < ec) ? src[(int64_t)(pl * 8 + e) * eHW]
+                                                      : ((efold && pl * 8 + e == ec) ? 1.f : 0.f);
                         store8(xbuf, xlo_buf, pl, r, v8);
                     }
                 }
@@ -652,6 +658,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 const int q = q0 + u, tile = q / NG, g = q % NG;
                                 int r = tile * 128 + row_in_tile, ii, y, x;
                                 const bool valid = rowpix(r, ii, y, x) && ii < nimg;
+                                if (CFG::FOLD) {
+                                    // bias already in the accumulator; pad / absent-image rows are
+                                    // never written (zero since kernel start, fenced by pad bands)
+                                    if (valid) {
+#pragma unroll
+                                        for (int h = 0; h < LW / 8; h++) {
+                                            float h8[8];
+#pragma unroll
+                                            for (int e = 0; e < 8; e++)
+                                                h8[e] = a.act == 0 ? fmaxf(v[u][h * 8 + e], 0.f) : v[u][h * 8 + e];
+                                            store8(hbuf_j, hlo_buf, (cb1 + g * LW) / 8 + h, r, h8);
+                                        }
+                                    }
+                                } else {
 #pragma unroll
                                 for (int h = 0; h < LW / 8; h++) {
                                     const float4 bA = __ldg(reinterpret_cast<const float4*>(bj + g * LW + h * 8));
@@ -666,6 +686,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                         h8[e] = valid ? hv : 0.f;
                                     }
                                     store8(hbuf_j, hlo_buf, (cb1 + g * LW) / 8 + h, r, h8);
+                                }
                                 }
                             }
                         }
@@ -690,8 +711,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
 #pragma unroll
                             for (int q8 = 0; q8 < 4; q8++) {
                                 if (q8 * 8 >= n) break;
-                                const float4 bA = __ldg(reinterpret_cast<const float4*>(bj + g0 + q8 * 8));
-                                const float4 bB = __ldg(reinterpret_cast<const float4*>(bj + g0 + q8 * 8 + 4));
+                                float4 bA = make_float4(0.f, 0.f, 0.f, 0.f), bB = bA;
+                                if (!efold) {
+                                    bA = __ldg(reinterpret_cast<const float4*>(bj + g0 + q8 * 8));
+                                    bB = __ldg(reinterpret_cast<const float4*>(bj + g0 + q8 * 8 + 4));
+                                }
                                 const float bb[8] = {bA.x, bA.y, bA.z, bA.w, bB.x, bB.y, bB.z, bB.w};
                                 float h8[8];
 #pragma unroll
@@ -774,7 +798,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                         nv = a.fmode ? fmaxf(f, 0.f) : (a.inverse ? old - f : old + f);
                                         if (store_state) dst[(int64_t)o * eHW] = nv;
                                     }
-                                    n8[o] = nv;
+                                    n8[o] = (efold && o == ec) ? 1.f : nv;
                                 }
                                 if (write_x) store8(xbuf, xlo_buf, 0, r, n8);
                             }
@@ -819,7 +843,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                         nv = a.fmode ? fmaxf(f, 0.f) : (a.inverse ? old - f : old + f);
                                         if (store_state) dst[(int64_t)o * eHW] = nv;
                                     }
-                                    n8[e] = nv;
+                                    n8[e] = (efold && o == ec) ? 1.f : nv;
                                 }
                                 if (write_x && o0 < eCp) store8(xbuf, xlo_buf, o0 / 8, r, n8);
                             }
@@ -877,7 +901,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                     nv = a.fmode ? fmaxf(f, 0.f) : (a.inverse ? oldv[q8 * 8 + e] - f : oldv[q8 * 8 + e] + f);
                                     if (store_state) dst[(int64_t)o * eHW] = nv;
                                 }
-                                n8[e] = nv;
+                                n8[e] = (efold && o == ec) ? 1.f : nv;
                             }
                             if (write_x && (cb2 + q8 * 8) < eCp) store8(xbuf, xlo_buf, (cb2 + q8 * 8) / 8, r, n8);
                         }
@@ -964,6 +988,7 @@ static bool make_plan(const StageInfo& S, bool prec3, StagePlan& best) {
     p.Cp = S.c <= 8 ? 8 : rup(S.c, 16);
     p.Mp = rup(S.m, 16);
     p.hst = S.c <= 8 ? 1 : 0;
+    p.fold = p.Cp > S.c ? 1 : 0;
     p.Nc2 = p.hst ? 32 : rup(S.c, 16);
     p.pair = p.Cp == 8;
     p.prec3 = prec3 ? 1 : 0;
@@ -1040,10 +1065,12 @@ static void put_tile(std::vector<uint16_t>& out, const std::vector<float>& w, in
                 }
 }
 
-static void pack_block(const StagePlan& p, const float* W1, const float* W2, bool prec3,
+static void pack_block(const StagePlan& p, const float* W1, const float* b1, const float* W2, bool prec3,
                        std::vector<uint16_t>& out) {
     const int c = p.c, m = p.m;
     auto w1 = [&](int h, int ci, int u, int v) -> float {  // u, v in -1..1
+        // folded bias: X channel c is 1 on every valid pixel, so its centre-tap weight is b1
+        if (p.fold && h < m && ci == c && u == 0 && v == 0) return b1[h];
         if (h >= m || ci >= c || v < -1 || v > 1) return 0.f;
         return W1[(((size_t)h * c + ci) * 3 + (u + 1)) * 3 + (v + 1)];
     };
@@ -1162,7 +1189,7 @@ ci_status_t umma_prepare(Model* m, const float* host_params) {
             const float* W2 = b1 + S.m;
             const float* b2 = W2 + (size_t)S.c * S.m * 9;
             size_t before = pack.size();
-            pack_block(p, W1, W2, prec3, pack);
+            pack_block(p, W1, b1, W2, prec3, pack);
             if ((int64_t)(pack.size() - before) * 2 != p.blk_bytes) {
                 delete U;
                 set_error("internal: packed block size mismatch");
@@ -1185,7 +1212,7 @@ ci_status_t umma_prepare(Model* m, const float* host_params) {
             const float* E2b = E2W + (size_t)a.enc_mid * 4 * a.enc_c1 * 9;
             const float* E3W = E2b + a.enc_mid;
             const float* E3b = E3W + (size_t)4 * a.enc_c1 * a.enc_mid * 9;
-            pack_block(p, E2W, E3W, prec3, pack);
+            pack_block(p, E2W, E2b, E3W, prec3, pack);
             for (int i = 0; i < p.Mp; i++) bias.push_back(i < S.m ? E2b[i] : 0.f);
             for (int i = 0; i < p.Nc2; i++) bias.push_back(i < S.c ? E3b[i] : 0.f);
             U->has_enc = 1;
