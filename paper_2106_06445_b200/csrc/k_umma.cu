@@ -58,6 +58,9 @@ struct StagePlan {
     size_t smem;
     int tmem_cols;
     double est_cycles;     // planner's cost estimate (cycles per image per block)
+    int split;             // 1: conv2 output columns are balanced over the two epilogue warp
+                           //    halves: half h holds channels [h c/2, (h+1) c/2) at columns
+                           //    [h Nc2/2, h Nc2/2 + c/2) (c = 24: 12 + 12 instead of 16 + 8)
     int fold;              // 1: conv1 bias folded into the MMA via a constant-1 input channel
                            //    (channel c of the padded X planes, Cp > c); epilogue adds none
     int hst;               // conv2 "horizontal tap stacking": N = 3 taps x 8 outputs (c <= 8),
@@ -190,6 +193,8 @@ struct SCfg {
     static constexpr int PLANE16 = RTOT;                 // plane bytes / 16
     static constexpr bool PAIR = CP == 8;
     static constexpr bool FOLD = CP_ > C_;   // == StagePlan::fold
+    static constexpr bool SPLIT = !HST && C_ % 8 == 0 && C_ / 2 < NC2_ / 2 &&
+                                  (NC2_ / 2 == 8 || NC2_ / 2 == 16 || NC2_ / 2 == 32 || NC2_ / 2 == 48);
     static constexpr int PER1 = PAIR ? 2 : CP / 16;
     static constexpr int K1 = PAIR ? 6 : 9 * (CP / 16);
     static constexpr int PER2 = MC / 16;
@@ -523,6 +528,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
         const bool esst = S ? (CFG::SST != 0) : (p.sstate != 0);
         const bool ehst = S ? CFG::HST : (p.hst != 0);
         const bool efold = S ? CFG::FOLD : (p.fold != 0);   // X channel ec = 1 on valid pixels
+        const bool esplit = S ? CFG::SPLIT : (p.split != 0);
         const int64_t eHW = (int64_t)eH * eW;
         constexpr int OLDN = S ? (CFG::NC2 / 2 > 0 ? CFG::NC2 / 2 : 8) : 48;
         const int ew = warp - 2;                       // 0..7
@@ -545,6 +551,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
             const int yy = band - ii * (eH + 1);
             y = yy - 1;
             return yy != 0 && x < eW;
+        };
+        // 4 channels (8 bytes) at channel offset sub*4 of a plane row (balanced conv2 split)
+        auto store4 = [&](uint8_t* base_hi, uint8_t* base_lo, int plane, int sub, int r, const float* v4) {
+            size_t off = (size_t)plane * plane_bytes + (size_t)(r + eG) * 16 + (size_t)sub * 8;
+            const uint32_t h0 = bf16x2_bits(v4[0], v4[1]), h1 = bf16x2_bits(v4[2], v4[3]);
+            *reinterpret_cast<uint2*>(base_hi + off) = make_uint2(h0, h1);
+            if (kP3) {
+                const uint32_t l0 = bf16x2_bits(v4[0] - __uint_as_float(h0 << 16), v4[1] - __uint_as_float(h0 & 0xFFFF0000u));
+                const uint32_t l1 = bf16x2_bits(v4[2] - __uint_as_float(h1 << 16), v4[3] - __uint_as_float(h1 & 0xFFFF0000u));
+                *reinterpret_cast<uint2*>(base_lo + off) = make_uint2(l0, l1);
+            }
         };
         auto store8 = [&](uint8_t* base_hi, uint8_t* base_lo, int plane, int r, const float* v8) {
             size_t off = (size_t)plane * plane_bytes + (size_t)(r + eG) * 16;
@@ -857,8 +874,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                     const float* src = stb + ((int64_t)(valid ? ii : 0) * a.C + out_off) * eHW + y * eW + x;
 #pragma unroll
                     for (int e = 0; e < OLDN; e++) {
-                        const int o = cb2 + e;
-                        oldv[e] = (valid && !a.fmode && e < cw2 && o < ec) ? src[(int64_t)o * eHW] : 0.f;
+                        const int o = esplit ? half * (ec / 2) + e : cb2 + e;
+                        const bool real = esplit ? e < ec / 2 : (e < cw2 && o < ec);
+                        oldv[e] = (valid && !a.fmode && real) ? src[(int64_t)o * eHW] : 0.f;
                     }
                 };
                 load_old(0);
@@ -884,7 +902,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             tmem_wait_ld();
                         }
                     }
-                    if (valid) {
+                    if (valid && esplit) {
+                        // balanced split: this half's channels [c0, c0 + ec/2) sit in its columns
+                        // 0 .. ec/2-1; bias is stored in column order
+                        float* dst = stb + ((int64_t)ii * a.C + out_off) * eHW + y * eW + x;
+                        const int c0 = half * (ec / 2);
+#pragma unroll
+                        for (int q4 = 0; q4 < OLDN / 4; q4++) {
+                            if (q4 * 4 >= ec / 2) break;
+                            float n4[4];
+#pragma unroll
+                            for (int e = 0; e < 4; e++) {
+                                const int el = q4 * 4 + e;
+                                const float acc = el < 16 ? v0[el] : (el < 32 ? v1[el - 16] : v2[el - 32]);
+                                const float f = acc + __ldg(b2 + cb2 + el);
+                                const float nv = a.fmode ? fmaxf(f, 0.f) : (a.inverse ? oldv[el] - f : oldv[el] + f);
+                                if (store_state) dst[(int64_t)(c0 + el) * eHW] = nv;
+                                n4[e] = nv;
+                            }
+                            if (write_x) store4(xbuf, xlo_buf, (c0 + q4 * 4) / 8, ((c0 + q4 * 4) % 8) / 4, r, n4);
+                        }
+                    } else if (valid) {
                         float* dst = stb + ((int64_t)ii * a.C + out_off) * eHW + y * eW + x;
 #pragma unroll
                         for (int q8 = 0; q8 < 6; q8++) {
@@ -990,6 +1028,8 @@ static bool make_plan(const StageInfo& S, bool prec3, StagePlan& best) {
     p.hst = S.c <= 8 ? 1 : 0;
     p.fold = p.Cp > S.c ? 1 : 0;
     p.Nc2 = p.hst ? 32 : rup(S.c, 16);
+    p.split = (!p.hst && S.c % 8 == 0 && S.c / 2 < p.Nc2 / 2 &&
+               (p.Nc2 / 2 == 8 || p.Nc2 / 2 == 16 || p.Nc2 / 2 == 32 || p.Nc2 / 2 == 48)) ? 1 : 0;
     p.pair = p.Cp == 8;
     p.prec3 = prec3 ? 1 : 0;
     if (p.Nc2 > 256) return false;
@@ -1052,6 +1092,14 @@ static bool make_plan(const StageInfo& S, bool prec3, StagePlan& best) {
     return true;
 }
 
+// conv2 output column n -> channel (-1 = padding column); see StagePlan::split
+static int conv2_col_channel(const StagePlan& p, int n) {
+    if (p.hst) return n < 24 ? n % 8 : -1;
+    if (!p.split) return n < p.c ? n : -1;
+    const int hn = p.Nc2 / 2, hc = p.c / 2, hh = n / hn, e = n % hn;
+    return e < hc ? hh * hc + e : -1;
+}
+
 // one k-step B tile: [khalf][n][8] bf16 (hi), then the lo tile when prec3
 static void put_tile(std::vector<uint16_t>& out, const std::vector<float>& w, int N, bool prec3) {
     // w is [N][16] (n, kk)
@@ -1075,7 +1123,7 @@ static void pack_block(const StagePlan& p, const float* W1, const float* b1, con
         return W1[(((size_t)h * c + ci) * 3 + (u + 1)) * 3 + (v + 1)];
     };
     auto w2 = [&](int o, int h, int u, int v) -> float {
-        if (o >= c || h >= m) return 0.f;
+        if (o < 0 || o >= c || h >= m) return 0.f;
         return W2[(((size_t)o * m + h) * 3 + (u + 1)) * 3 + (v + 1)];
     };
     std::vector<float> tile;
@@ -1114,7 +1162,7 @@ static void pack_block(const StagePlan& p, const float* W1, const float* b1, con
                     if (p.hst)   // column n = (v+1)*8 + o, k-step row u = tap-1
                         tile[(size_t)n * 16 + kk] = n < 24 ? w2(n % 8, h, tap - 1, n / 8 - 1) : 0.f;
                     else
-                        tile[(size_t)n * 16 + kk] = w2(n, h, tap / 3 - 1, tap % 3 - 1);
+                        tile[(size_t)n * 16 + kk] = w2(conv2_col_channel(p, n), h, tap / 3 - 1, tap % 3 - 1);
                 }
             put_tile(out, tile, p.Nc2, prec3);
         }
@@ -1133,9 +1181,12 @@ struct UmmaState {
 
 // ---- compile-time specialisations for the Arch-C stage plans (see make_plan) -----------------
 typedef void (*StageKernel)(StageArgs);
-struct SpecEntry { int Wp, Cp, MC, Nc2, T, p3, slot, H, c, sst; StageKernel fn; };
-#define CI_SPEC(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST) \
-    {WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, k_stage<SCfg<WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, ((C) <= 8)>>}
+struct SpecEntry { int Wp, Cp, MC, Nc2, T, p3, slot, H, c, sst, fold, split; StageKernel fn; };
+#define CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST) SCfg<WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, ((C) <= 8)>
+#define CI_SPEC(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST)                                       \
+    {WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST)::FOLD, \
+     CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST)::SPLIT,                               \
+     k_stage<CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST)>}
 static const SpecEntry kSpecs[] = {
     CI_SPEC(17, 8, 32, 32, 7, 0, 16384, 16, 6, 1),   // C stage 1, bf16 (hst)
     CI_SPEC(9, 32, 32, 32, 7, 0, 16384, 8, 24, 0),   // C stage 2, bf16
@@ -1153,7 +1204,8 @@ static StageKernel pick_kernel(const StagePlan& p, const StageArgs& a) {
     if (!getenv("CI_NO_STATIC") && !a.residual && a.act != 1)
         for (const auto& e : kSpecs)
             if (e.Wp == p.Wp && e.Cp == p.Cp && e.MC == p.MC && e.Nc2 == p.Nc2 && e.T == p.T && e.p3 == p.prec3 &&
-                e.slot == p.slot_bytes && e.H == p.H && e.c == p.c && e.sst == p.sstate)
+                e.slot == p.slot_bytes && e.H == p.H && e.c == p.c && e.sst == p.sstate &&
+                e.fold == p.fold && e.split == p.split)   // packing and epilogue must agree
                 return e.fn;
     return k_stage<SDyn>;
 }
@@ -1196,7 +1248,10 @@ ci_status_t umma_prepare(Model* m, const float* host_params) {
                 return CI_ERR_UNSUPPORTED;
             }
             for (int i = 0; i < p.Mp; i++) bias.push_back(i < S.m ? b1[i] : 0.f);
-            for (int i = 0; i < p.Nc2; i++) bias.push_back(i < S.c ? b2[i] : 0.f);
+            for (int i = 0; i < p.Nc2; i++) {   // conv2 bias: by channel (hst) or by column
+                const int o = p.hst ? (i < S.c ? i : -1) : conv2_col_channel(p, i);
+                bias.push_back(o >= 0 ? b2[o] : 0.f);
+            }
         }
     }
     if (m->enc_off >= 0) {   // encoder tail: c = 4*c1 channels at H/2 x W/2, hidden = enc_mid
@@ -1214,7 +1269,10 @@ ci_status_t umma_prepare(Model* m, const float* host_params) {
             const float* E3b = E3W + (size_t)4 * a.enc_c1 * a.enc_mid * 9;
             pack_block(p, E2W, E2b, E3W, prec3, pack);
             for (int i = 0; i < p.Mp; i++) bias.push_back(i < S.m ? E2b[i] : 0.f);
-            for (int i = 0; i < p.Nc2; i++) bias.push_back(i < S.c ? E3b[i] : 0.f);
+            for (int i = 0; i < p.Nc2; i++) {
+                const int o = p.hst ? (i < S.c ? i : -1) : conv2_col_channel(p, i);
+                bias.push_back(o >= 0 ? E3b[o] : 0.f);
+            }
             U->has_enc = 1;
         }
     }
