@@ -179,6 +179,55 @@ __device__ __forceinline__ void issue_static(uint32_t tmem, uint32_t alo0, uint3
     }
 }
 
+// Tile-outer variant for the FIRST conv1 chunk of a block: all of the chunk's weight slots
+// are resident (NS <= nslot), and tile t is issued as soon as the previous block's epilogue
+// has finished the X rows of tiles t-1..t+1 (x_tile[t+1]; arrivals are in tile order per
+// thread), so this chunk overlaps that epilogue instead of waiting for all of it.
+template <int K, int PER, bool PAIR, int WP, int PLANE16, int G, int KB16, int T, int N, bool P3,
+          int LOA16, int ACC0, int DSTRIDE>
+__device__ __forceinline__ void issue_static_tiles(uint32_t tmem, uint32_t alo0, uint32_t ringlo, uint32_t slot16,
+                                                   uint32_t idesc, int& slot, uint32_t& phase, int nslot,
+                                                   uint64_t* full, uint64_t* empty, uint64_t* x_tile, uint32_t xph) {
+    constexpr uint32_t HI = 0x4008u;
+    constexpr int NS = (K + G - 1) / G;
+    uint32_t bl[NS];
+    asm volatile("" : "+r"(alo0), "+r"(ringlo));
+    {
+        int sl = slot;
+        uint32_t ph = phase;
+#pragma unroll
+        for (int q = 0; q < NS; q++) {
+            mbar_wait(&full[sl], ph);
+            bl[q] = ringlo + (uint32_t)sl * slot16;
+            if (++sl == nslot) { sl = 0; ph ^= 1; }
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < T; t++) {
+        mbar_wait(&x_tile[t + 1 < T ? t + 1 : T - 1], xph);
+        fence_after();
+#pragma unroll
+        for (int s = 0; s < K; s++) {
+            const int shift = PAIR ? (s / 2 - 1) * WP + ((s & 1) ? 1 : -1)
+                                   : ((s / PER) / 3 - 1) * WP + ((s / PER) % 3 - 1);
+            const int poff16 = PAIR ? 0 : 2 * (s % PER) * PLANE16;
+            const uint64_t ad = ((uint64_t)HI << 32) | (alo0 + (uint32_t)(shift + poff16 + t * 128));
+            const uint64_t bd = ((uint64_t)HI << 32) | (bl[s / G] + (uint32_t)((s % G) * KB16));
+            const uint32_t d = tmem + (uint32_t)(ACC0 + t * DSTRIDE);
+            mma_bf16(d, ad, bd, idesc, s == 0 ? 0u : 1u);
+            if (P3) {
+                mma_bf16(d, ad, bd + (uint64_t)(N * 2), idesc, 1u);
+                mma_bf16(d, ad + (uint64_t)LOA16, bd, idesc, 1u);
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < NS; q++) {
+        commit(&empty[slot]);
+        if (++slot == nslot) { slot = 0; phase ^= 1; }
+    }
+}
+
 // Static stage configuration (0 = use the runtime plan)
 template <int WP_, int CP_, int MC_, int NC2_, int T_, int P3_, int SLOT_, int H_ = 0, int C_ = 0, int SST_ = 0,
           int HST_ = 0>
@@ -208,6 +257,8 @@ struct SCfg {
 };
 using SDyn = SCfg<0, 0, 0, 0, 0, 0, 0>;
 constexpr int kXchgBytes = 8 * 4 * 2 * 8 * 4;   // hst boundary exchange: [T<=8][quarter][2][8] fp32
+constexpr int kMaxTiles = 8;                     // T <= 8 (512 TMEM columns / >= 64 per tile)
+constexpr int kBarBytes = 384;                   // mbarriers, TMEM slot and batch queue
 
 // Cycle instrumentation (CI_DEBUG_CYCLES; inactive unless requested).  -DCI_NO_CYCLES
 // compiles it out; same-box A/B showed no gain from that (s2 got slower), so it stays in.
@@ -253,9 +304,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
     uint64_t* bqf = x_full + 8;        // [4] entry published (1 arrival)
     uint64_t* bqe = x_full + 12;       // [4] entry consumed (MMA thread + every epilogue thread)
     volatile int64_t* bq = reinterpret_cast<volatile int64_t*>(x_full + 16);   // [4]
-    // per-k-step A descriptors for tile 0 (hi planes): conv1 [k1], conv2 [k2]
-    uint64_t* adesc1 = x_full + 20;
-    uint64_t* adesc2 = adesc1 + p.k1;
+    // x_tile[t]: the bf16 X rows of M-tile t are final for the next conv1 (every epilogue
+    // thread arrives on every tile, in tile order; x_full itself is unused)
+    uint64_t* x_tile = x_full + 20;    // [kMaxTiles]
 
     // ---- zero the activation buffers (pads and guards must read as 0)
     {
@@ -267,34 +318,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
     if (warp == 1) tmem_alloc(tmem_slot, p.tmem_cols);
     if (tid == 0) {
         for (int i = 0; i < p.nslot; i++) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-        mbar_init(x_full, kEpiThreads);
+        for (int i = 0; i < kMaxTiles; i++) mbar_init(&x_tile[i], kEpiThreads);
         mbar_init(acc1_full, 1);
         for (int i = 0; i < 2; i++) { mbar_init(&hd_full[i], kEpiThreads); mbar_init(&hd_empty[i], 1); }
         mbar_init(acc2_full, 1);
         for (int i = 0; i < 4; i++) { mbar_init(&bqf[i], 1); mbar_init(&bqe[i], 1 + kEpiThreads); }
         fence_mbar_init();
-        const uint32_t plane_b = (uint32_t)p.Rtot * 16;
-        const uint32_t xb0 = smem_u32(xbuf), hb0 = smem_u32(hbuf);
-        for (int s = 0; s < p.k1; s++) {
-            int shift, plane;
-            uint32_t lbo;
-            if (p.pair) {
-                int u = s / 2 - 1, v0 = (s & 1) ? 1 : -1;
-                shift = u * p.Wp + v0; plane = 0; lbo = 16;
-            } else {
-                int per = p.Cp / 16;
-                int tap = s / per, kc = s - tap * per;
-                shift = (tap / 3 - 1) * p.Wp + (tap % 3 - 1);
-                plane = 2 * kc; lbo = plane_b;
-            }
-            adesc1[s] = smem_desc(xb0 + (uint32_t)(p.G + shift) * 16 + (uint32_t)plane * plane_b, lbo, 128);
-        }
-        const int per2 = p.MC / 16;
-        for (int s = 0; s < p.k2; s++) {
-            int tap = s / per2, kc = s - tap * per2;
-            int shift = (tap / 3 - 1) * p.Wp + (tap % 3 - 1);
-            adesc2[s] = smem_desc(hb0 + (uint32_t)(p.G + shift) * 16 + (uint32_t)(2 * kc) * plane_b, plane_b, 128);
-        }
     }
     fence_before();
     __syncthreads();
@@ -393,8 +422,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                 mbar_arrive(&bqe[qi & 3]);
                 if (b >= nbatch) break;
                 for (int tt = 0; tt < nbv; tt++) {
-                    TWAIT(w_x, mbar_wait(x_full, xph)); xph ^= 1;
-                    fence_after();
                     auto do_conv1 = [&](int j) {
                         if constexpr (CFG::kStatic) {
                             constexpr uint32_t LBO1 = CFG::PAIR ? 16u : (uint32_t)CFG::PLANE16 * 16u;
@@ -486,7 +513,30 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             }
                         }
                     };
-                    do_conv1(0);
+                    // first conv1 chunk: tile by tile behind the previous epilogue when its weight
+                    // slots fit the ring, else after all X rows are final
+                    bool tiles_first = false;
+                    if constexpr (CFG::kStatic && (CFG::K1 + CFG::G1 - 1) / CFG::G1 <= 3) {
+                        constexpr int NS1 = (CFG::K1 + CFG::G1 - 1) / CFG::G1;
+                        if (NS1 <= p.nslot) {
+                            tiles_first = true;
+                            constexpr uint32_t LBO1 = CFG::PAIR ? 16u : (uint32_t)CFG::PLANE16 * 16u;
+                            const uint32_t alo0 = ((xb >> 4) & 0x3FFFu) | ((LBO1 >> 4) << 16);
+                            const uint32_t ringlo = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::MC * 16 >> 4) << 16);
+                            long long tx0 = CLK();
+                            issue_static_tiles<CFG::K1, CFG::PER1, CFG::PAIR, CFG::WP, CFG::PLANE16, CFG::G1,
+                                               CFG::KB1 / 16, CFG::T, CFG::MC, CFG::P3, CFG::LOX16, CFG::ACC1, CFG::MC>(
+                                tmem, alo0, ringlo, (uint32_t)CFG::SLOT / 16u, id1, slot, phase, p.nslot, full, empty,
+                                x_tile, xph);
+                            if (kCycles && a.dbg) w_x += (unsigned long long)(CLK() - tx0);
+                        }
+                    }
+                    if (!tiles_first) {
+                        TWAIT(w_x, mbar_wait(&x_tile[p.T - 1], xph));
+                        fence_after();
+                        do_conv1(0);
+                    }
+                    xph ^= 1;
                     commit(acc1_full);
                     for (int j = 0; j < p.nch; j++) {
                         const int hbi = j & (p.nhd - 1);
@@ -626,7 +676,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                     }
                 }
                 fence_proxy_async();
-                mbar_arrive(x_full);
+                for (int t = 0; t < eT; t++) mbar_arrive(&x_tile[t]);
             }
             t_ld += CLK() - tl0;
             for (int tt = 0; tt < nbv; tt++) {
@@ -753,6 +803,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                 }
                 // ---- conv2 epilogue: s_out (+|-)= acc2 + b2 (fp32); bf16(s_out) -> X
                 const bool write_x = tt + 1 < nbv;
+                // tile t's X rows are final for the next block's conv1 (arrive in tile order)
+                auto x_ready = [&](int tile) {
+                    if (write_x) {
+                        fence_before();
+                        fence_proxy_async();
+                        mbar_arrive(&x_tile[tile]);
+                    }
+                };
                 if (ehst) {
                     // ---- horizontal tap stacking: acc2 row r holds Z_v[r][o] at column (v+1)*8+o;
                     // out[p][o] = Z_-1[p-1][o] + Z_0[p][o] + Z_+1[p+1][o]  (col2im over v).
@@ -779,7 +837,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             }
                         }
                         asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
-                        for (int tile = half; tile < eT; tile += 2) {
+                        for (int tile = 0; tile < eT; tile++) {
+                          if ((tile & 1) == half) {
                             int r = tile * 128 + row_in_tile, ii, y, x;
                             const bool valid = rowpix(r, ii, y, x) && ii < nimg;
                             float za[16], zb[8];
@@ -819,6 +878,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 }
                                 if (write_x) store8(xbuf, xlo_buf, 0, r, n8);
                             }
+                          }
+                          x_ready(tile);
                         }
                         asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
                     }
@@ -865,6 +926,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 if (write_x && o0 < eCp) store8(xbuf, xlo_buf, o0 / 8, r, n8);
                             }
                         }
+                        x_ready(tile);
                     }
                 } else {
                 float oldv[OLDN];
@@ -944,14 +1006,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             if (write_x && (cb2 + q8 * 8) < eCp) store8(xbuf, xlo_buf, (cb2 + q8 * 8) / 8, r, n8);
                         }
                     }
+                    x_ready(tile);
                     if (tile + 1 < eT) load_old(tile + 1);
                 }
                 t_e2 += CLK() - te2;
-                }
-                if (write_x) {
-                    fence_before();
-                    fence_proxy_async();
-                    mbar_arrive(x_full);
                 }
                 if (esst && !write_x) {   // last block of the stage: state back to global
                     asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads));
@@ -1055,7 +1113,7 @@ static bool make_plan(const StageInfo& S, bool prec3, StagePlan& best) {
                     const int slot_bytes = std::max(16384, std::max(kstep_bytes(MC, prec3), kstep_bytes(p.Nc2, prec3)));
                     const int Rtot = T * 128 + 2 * p.G;
                     const size_t smem0 = (size_t)nslot * slot_bytes + (size_t)P * ((p.Cp + nhd * MC) / 8) * Rtot * 16 +
-                                         256 + kXchgBytes + 8 * (size_t)(9 * (p.Cp / 8 + 1) + 9 * (MC / 16));
+                                         kBarBytes + kXchgBytes;
                     if (smem0 > kSmemCap) continue;
                     const size_t state_bytes = (size_t)I * S.C * p.H * p.W * 4;
                     const size_t soff = (smem0 + 127) / 128 * 128;
