@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             const uint32_t ringlo = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::NC2 * 16 >> 4) << 16);
                             issue_static<CFG::K2, CFG::PER2, false, CFG::WP, CFG::PLANE16, CFG::G2, CFG::KB2 / 16,
                                          CFG::T, CFG::NC2, CFG::P3, CFG::LOH16, 0, CFG::NC2, CFG::HST>(
-                                tmem, alo0, ringlo, (uint32_t)CFG::SLOT / 16u, id2, j > 0 ? 1u : 0u, slot, phase,
+                                tmem, alo0, ringlo, (uint32_t)CFG::SLOT / 16u, id2, 1u, slot, phase,
                                 p.nslot, full, empty);
                         } else
                         {
@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 const int shift = p.hst ? (tap - 1) * p.Wp : (tap / 3 - 1) * p.Wp + (tap % 3 - 1);
                                 const uint32_t aaddr = hbj + (uint32_t)shift * 16u + (uint32_t)(2 * kc) * plane_bytes;
                                 const uint32_t baddr = rb + (uint32_t)slot * (uint32_t)p.slot_bytes + (uint32_t)q * kb2;
-                                const uint32_t acc = (j > 0 || s > 0) ? 1u : 0u;
+                                const uint32_t acc = 1u;   // acc2 starts at the bias (epilogue-initialised)
                                 for (int tile = 0; tile < p.T; tile++) {
                                     const uint32_t d = tmem + (uint32_t)(tile * p.Nc2);
                                     const uint32_t at = aaddr + (uint32_t)tile * 2048u;
@@ -640,6 +640,39 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
         };
         if (!esst && blockIdx.x < nbatch) prefetch_batch(blockIdx.x);
         float* sst = reinterpret_cast<float*>(smem + p.sstate_off);
+        // conv2 bias lives in TMEM: after reading a tile's acc2 columns the epilogue writes the
+        // NEXT virtual block's bias there and the MMA accumulates on top (no per-element add)
+        auto bias2_of = [&](int vb) -> const float* {
+            const int tb = a.inverse ? a.nb - 1 - vb / R : vb / R;
+            return a.bias + (int64_t)tb * (p.Mp + eNC2) + p.Mp;
+        };
+        auto init_acc2 = [&](const float* b2src, int tile) {
+            const uint32_t base = tmem + lane_addr + (uint32_t)(tile * eNC2);
+            if (ehst) {   // centre-tap columns 8..15 carry b2[o], the other taps start at 0
+                float z16[16], z8[8];
+#pragma unroll
+                for (int e = 0; e < 8; e++) { z16[e] = 0.f; z16[8 + e] = e < ec ? __ldg(b2src + e) : 0.f; z8[e] = 0.f; }
+                tmem_st16(base, z16);
+                tmem_st8(base + 16, z8);
+            } else {
+                for (int g = 0; g < cw2; g += 16) {
+                    if (cw2 - g >= 16) {
+                        float v16[16];
+#pragma unroll
+                        for (int e = 0; e < 16; e++) v16[e] = __ldg(b2src + cb2 + g + e);
+                        tmem_st16(base + (uint32_t)(cb2 + g), v16);
+                    } else {
+                        float v8[8];
+#pragma unroll
+                        for (int e = 0; e < 8; e++) v8[e] = __ldg(b2src + cb2 + g + e);
+                        tmem_st8(base + (uint32_t)(cb2 + g), v8);
+                    }
+                }
+            }
+        };
+        for (int tile = 0; tile < eT; tile++)
+            if (!ehst || (tile & 1) == half) init_acc2(bias2_of(0), tile);
+        tmem_wait_st();
         for (int qi = 0;; qi++) {
             const int64_t b = bq_read(qi);
             if (b >= nbatch) break;
@@ -685,7 +718,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                 // fixed-point replays before the last only refresh the X planes (the iterate)
                 const bool store_state = !kGen || (tt % R) == R - 1;
                 const float* b1 = a.bias + (int64_t)t * (p.Mp + eNC2);
-                const float* b2 = b1 + p.Mp;
+                const float* b2n = bias2_of(tt + 1 < nbv ? tt + 1 : 0);   // next block's conv2 bias
                 for (int j = 0; j < p.nch; j++) {
                     // ---- conv1 epilogue: acc1 -> bias + act -> bf16 hidden planes
                     TWAIT(w_a1, mbar_wait(acc1_full, a1ph)); a1ph ^= 1;
@@ -846,6 +879,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             tmem_ld16(tmem + lane_addr + col, za);
                             tmem_ld8(tmem + lane_addr + col + 16, zb);
                             tmem_wait_ld();
+                            init_acc2(b2n, tile);
                             float left[8], right[8];
 #pragma unroll
                             for (int o = 0; o < 8; o++) {
@@ -869,7 +903,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 for (int o = 0; o < 8; o++) {
                                     float nv = 0.f;
                                     if (o < ec) {
-                                        const float f = (left[o] + za[8 + o] + right[o]) + __ldg(b2 + o);
+                                        const float f = left[o] + za[8 + o] + right[o];   // bias: in TMEM
                                         const float old = a.fmode ? 0.f : dst[(int64_t)o * eHW];
                                         nv = a.fmode ? fmaxf(f, 0.f) : (a.inverse ? old - f : old + f);
                                         if (store_state) dst[(int64_t)o * eHW] = nv;
@@ -881,6 +915,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                           }
                           x_ready(tile);
                         }
+                        tmem_wait_st();
                         asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
                     }
                     t_e2 += CLK() - te2h;
@@ -916,7 +951,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                     const int o = o0 + e;
                                     float nv = 0.f;
                                     if (o < ec) {
-                                        const float f = v[q8 * 8 + e] + __ldg(b2 + o);
+                                        const float f = v[q8 * 8 + e];   // bias: in TMEM
                                         const float old = a.fmode ? 0.f : dst[(int64_t)o * eHW];
                                         nv = a.fmode ? fmaxf(f, 0.f) : (a.inverse ? old - f : old + f);
                                         if (store_state) dst[(int64_t)o * eHW] = nv;
@@ -926,8 +961,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 if (write_x && o0 < eCp) store8(xbuf, xlo_buf, o0 / 8, r, n8);
                             }
                         }
+                        init_acc2(b2n, tile);
                         x_ready(tile);
                     }
+                    tmem_wait_st();
                 } else {
                 float oldv[OLDN];
                 auto load_old = [&](int tile) {
@@ -977,7 +1014,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             for (int e = 0; e < 4; e++) {
                                 const int el = q4 * 4 + e;
                                 const float acc = el < 16 ? v0[el] : (el < 32 ? v1[el - 16] : v2[el - 32]);
-                                const float f = acc + __ldg(b2 + cb2 + el);
+                                const float f = acc;   // bias: in TMEM
                                 const float nv = a.fmode ? fmaxf(f, 0.f) : (a.inverse ? oldv[el] - f : oldv[el] + f);
                                 if (store_state) dst[(int64_t)(c0 + el) * eHW] = nv;
                                 n4[e] = nv;
@@ -997,7 +1034,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 const float acc = q8 < 2 ? v0[q8 * 8 + e] : (q8 < 4 ? v1[(q8 - 2) * 8 + e] : v2[(q8 - 4) * 8 + e]);
                                 float nv = 0.f;
                                 if (o < ec) {
-                                    const float f = acc + __ldg(b2 + o);
+                                    const float f = acc;   // bias: in TMEM
                                     nv = a.fmode ? fmaxf(f, 0.f) : (a.inverse ? oldv[q8 * 8 + e] - f : oldv[q8 * 8 + e] + f);
                                     if (store_state) dst[(int64_t)o * eHW] = nv;
                                 }
@@ -1006,9 +1043,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             if (write_x && (cb2 + q8 * 8) < eCp) store8(xbuf, xlo_buf, (cb2 + q8 * 8) / 8, r, n8);
                         }
                     }
+                    init_acc2(b2n, tile);   // after the tile's values are consumed (register pressure)
                     x_ready(tile);
                     if (tile + 1 < eT) load_old(tile + 1);
                 }
+                tmem_wait_st();
                 t_e2 += CLK() - te2;
                 }
                 if (esst && !write_x) {   // last block of the stage: state back to global
