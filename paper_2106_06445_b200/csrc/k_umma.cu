@@ -186,8 +186,9 @@ __device__ __forceinline__ void issue_static(uint32_t tmem, uint32_t alo0, uint3
 template <int K, int PER, bool PAIR, int WP, int PLANE16, int G, int KB16, int T, int N, bool P3,
           int LOA16, int ACC0, int DSTRIDE>
 __device__ __forceinline__ void issue_static_tiles(uint32_t tmem, uint32_t alo0, uint32_t ringlo, uint32_t slot16,
-                                                   uint32_t idesc, int& slot, uint32_t& phase, int nslot,
-                                                   uint64_t* full, uint64_t* empty, uint64_t* x_tile, uint32_t xph) {
+                                                   uint32_t idesc, uint32_t acc_first, int& slot, uint32_t& phase,
+                                                   int nslot, uint64_t* full, uint64_t* empty, uint64_t* x_tile,
+                                                   uint32_t xph) {
     constexpr uint32_t HI = 0x4008u;
     constexpr int NS = (K + G - 1) / G;
     uint32_t bl[NS];
@@ -214,7 +215,7 @@ __device__ __forceinline__ void issue_static_tiles(uint32_t tmem, uint32_t alo0,
             const uint64_t ad = ((uint64_t)HI << 32) | (alo0 + (uint32_t)(shift + poff16 + t * 128));
             const uint64_t bd = ((uint64_t)HI << 32) | (bl[s / G] + (uint32_t)((s % G) * KB16));
             const uint32_t d = tmem + (uint32_t)(ACC0 + t * DSTRIDE);
-            mma_bf16(d, ad, bd, idesc, s == 0 ? 0u : 1u);
+            mma_bf16(d, ad, bd, idesc, s == 0 ? acc_first : 1u);
             if (P3) {
                 mma_bf16(d, ad, bd + (uint64_t)(N * 2), idesc, 1u);
                 mma_bf16(d, ad + (uint64_t)LOA16, bd, idesc, 1u);
@@ -429,8 +430,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             const uint32_t ringlo = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::MC * 16 >> 4) << 16);
                             issue_static<CFG::K1, CFG::PER1, CFG::PAIR, CFG::WP, CFG::PLANE16, CFG::G1, CFG::KB1 / 16,
                                          CFG::T, CFG::MC, CFG::P3, CFG::LOX16, CFG::ACC1, CFG::MC>(
-                                tmem, alo0, ringlo, (uint32_t)CFG::SLOT / 16u, id1, 0u, slot, phase, p.nslot,
-                                full, empty);
+                                tmem, alo0, ringlo, (uint32_t)CFG::SLOT / 16u, id1, CFG::FOLD ? 0u : 1u, slot, phase,
+                                p.nslot, full, empty);
                         } else
                                                 {
                             int tap = 0, kc = 0, q = 0;
@@ -450,7 +451,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 }
                                 const uint32_t aaddr = xb + (uint32_t)shift * 16u + poff;
                                 const uint32_t baddr = rb + (uint32_t)slot * (uint32_t)p.slot_bytes + (uint32_t)q * kb1;
-                                const uint32_t acc = s > 0 ? 1u : 0u;
+                                const uint32_t acc = (s > 0 || !p.fold) ? 1u : 0u;   // unfolded: acc1 = bias
                                 for (int tile = 0; tile < p.T; tile++) {
                                     const uint32_t d = tmem + acc1_col0 + (uint32_t)(tile * p.MC);
                                     const uint32_t at = aaddr + (uint32_t)tile * 2048u;
@@ -526,8 +527,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             long long tx0 = CLK();
                             issue_static_tiles<CFG::K1, CFG::PER1, CFG::PAIR, CFG::WP, CFG::PLANE16, CFG::G1,
                                                CFG::KB1 / 16, CFG::T, CFG::MC, CFG::P3, CFG::LOX16, CFG::ACC1, CFG::MC>(
-                                tmem, alo0, ringlo, (uint32_t)CFG::SLOT / 16u, id1, slot, phase, p.nslot, full, empty,
-                                x_tile, xph);
+                                tmem, alo0, ringlo, (uint32_t)CFG::SLOT / 16u, id1, CFG::FOLD ? 0u : 1u, slot, phase,
+                                p.nslot, full, empty, x_tile, xph);
                             if (kCycles && a.dbg) w_x += (unsigned long long)(CLK() - tx0);
                         }
                     }
@@ -670,8 +671,37 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                 }
             }
         };
-        for (int tile = 0; tile < eT; tile++)
+        // conv1 bias (plans without the constant-1 fold) likewise lives in acc1: after epi1 reads
+        // chunk j it writes the bias of the next conv1 chunk in issue order
+        auto bias1_of = [&](int vb) -> const float* {
+            const int tb = a.inverse ? a.nb - 1 - vb / R : vb / R;
+            return a.bias + (int64_t)tb * (p.Mp + eNC2);
+        };
+        auto init_acc1_cols = [&](const float* b1src, uint32_t col, int n) {   // n = 8, 16 or 32 columns
+            if (n >= 16) {
+                float v16[16];
+#pragma unroll
+                for (int e = 0; e < 16; e++) v16[e] = __ldg(b1src + e);
+                tmem_st16(tmem + lane_addr + col, v16);
+                if (n == 32) {
+#pragma unroll
+                    for (int e = 0; e < 16; e++) v16[e] = __ldg(b1src + 16 + e);
+                    tmem_st16(tmem + lane_addr + col + 16, v16);
+                }
+            } else {
+                float v8[8];
+#pragma unroll
+                for (int e = 0; e < 8; e++) v8[e] = __ldg(b1src + e);
+                tmem_st8(tmem + lane_addr + col, v8);
+            }
+        };
+        for (int tile = 0; tile < eT; tile++) {
             if (!ehst || (tile & 1) == half) init_acc2(bias2_of(0), tile);
+            if (!efold)
+                for (int g0 = 0; g0 < cw1; g0 += 32)
+                    init_acc1_cols(bias1_of(0) + cb1 + g0, acc1_col0 + (uint32_t)(tile * eMC + cb1 + g0),
+                                   cw1 - g0 < 32 ? cw1 - g0 : 32);
+        }
         tmem_wait_st();
         for (int qi = 0;; qi++) {
             const int64_t b = bq_read(qi);
@@ -732,7 +762,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                     uint8_t* hbuf_j = hbuf + (size_t)hb_i * hbuf_stride;
                     uint8_t* hlo_buf = hbuf_j + (size_t)(eMC / 8) * plane_bytes;
                     long long te0 = CLK();
-                    const float* bj = b1 + j * eMC + cb1;
+                    // bias of the next conv1 chunk in issue order, this half's columns
+                    const float* b1n = (j + 1 < p.nch ? b1 + (j + 1) * eMC : bias1_of(tt + 1 < nbv ? tt + 1 : 0)) + cb1;
 #ifndef CI_NO_EPI1_BATCH
                     if constexpr (S && CFG::MC == 32) {
                         // Batched TMEM reads: up to four LW-column loads in flight per wait::ld
@@ -774,19 +805,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 } else {
 #pragma unroll
                                 for (int h = 0; h < LW / 8; h++) {
-                                    const float4 bA = __ldg(reinterpret_cast<const float4*>(bj + g * LW + h * 8));
-                                    const float4 bB = __ldg(reinterpret_cast<const float4*>(bj + g * LW + h * 8 + 4));
-                                    const float bb[8] = {bA.x, bA.y, bA.z, bA.w, bB.x, bB.y, bB.z, bB.w};
                                     float h8[8];
 #pragma unroll
                                     for (int e = 0; e < 8; e++) {
-                                        float hv = v[u][h * 8 + e] + bb[e];
+                                        float hv = v[u][h * 8 + e];   // bias: in TMEM
                                         if (a.act == 0) hv = fmaxf(hv, 0.f);
                                         else if (kGen && a.act == 1) hv = hv > 0.f ? hv : expm1f(hv);
                                         h8[e] = valid ? hv : 0.f;
                                     }
                                     store8(hbuf_j, hlo_buf, (cb1 + g * LW) / 8 + h, r, h8);
                                 }
+                                init_acc1_cols(b1n + g * LW, acc1_col0 + (uint32_t)(tile * CFG::MC + cb1 + g * LW), LW);
                                 }
                             }
                         }
@@ -811,24 +840,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
 #pragma unroll
                             for (int q8 = 0; q8 < 4; q8++) {
                                 if (q8 * 8 >= n) break;
-                                float4 bA = make_float4(0.f, 0.f, 0.f, 0.f), bB = bA;
-                                if (!efold) {
-                                    bA = __ldg(reinterpret_cast<const float4*>(bj + g0 + q8 * 8));
-                                    bB = __ldg(reinterpret_cast<const float4*>(bj + g0 + q8 * 8 + 4));
-                                }
-                                const float bb[8] = {bA.x, bA.y, bA.z, bA.w, bB.x, bB.y, bB.z, bB.w};
                                 float h8[8];
 #pragma unroll
                                 for (int e = 0; e < 8; e++) {
-                                    float h = (q8 < 2 ? va[q8 * 8 + e] : vb[(q8 - 2) * 8 + e]) + bb[e];
+                                    float h = q8 < 2 ? va[q8 * 8 + e] : vb[(q8 - 2) * 8 + e];   // bias: folded or in TMEM
                                     if (a.act == 0) h = fmaxf(h, 0.f);
                                     else if (kGen && a.act == 1) h = h > 0.f ? h : expm1f(h);
                                     h8[e] = valid ? h : 0.f;
                                 }
                                 store8(hbuf_j, hlo_buf, (cb1 + g0) / 8 + q8, r, h8);
                             }
+                            if (!efold) init_acc1_cols(b1n + g0, col + (uint32_t)g0, n);
                         }
                     }
+                    tmem_wait_st();
                     fence_before();
                     fence_proxy_async();
                     mbar_arrive(&hd_full[hb_i]);
