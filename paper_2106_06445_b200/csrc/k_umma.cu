@@ -878,6 +878,37 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                     fence_after();
                     long long te2h = CLK();
                     {
+                      if constexpr (S) {
+                        // pass 1, batched: only the Z_-1 (cols 0-7) and Z_+1 (cols 16-23) columns the
+                        // exchange needs, all of this half's tiles in flight before one wait
+                        constexpr int NK = (CFG::T + 1) / 2;
+                        float zl[NK][8], zr[NK][8];
+#pragma unroll
+                        for (int k = 0; k < NK; k++) {
+                            const int tile = 2 * k + half;
+                            if (tile < eT) {
+                                const uint32_t col = (uint32_t)(tile * eNC2);
+                                tmem_ld8(tmem + lane_addr + col, zl[k]);
+                                tmem_ld8(tmem + lane_addr + col + 16, zr[k]);
+                            }
+                        }
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int k = 0; k < NK; k++) {
+                            const int tile = 2 * k + half;
+                            if (tile < eT) {
+                                float* xq = xchg + ((tile * 4 + quarter) * 2) * 8;
+                                if (lane == 31) {
+#pragma unroll
+                                    for (int o = 0; o < 8; o++) xq[o] = zl[k][o];
+                                }
+                                if (lane == 0) {
+#pragma unroll
+                                    for (int o = 0; o < 8; o++) xq[8 + o] = zr[k][o];
+                                }
+                            }
+                        }
+                      } else {
                         for (int tile = half; tile < eT; tile += 2) {
                             float za[16], zb[8];
                             const uint32_t col = (uint32_t)(tile * eNC2);
@@ -894,17 +925,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 for (int o = 0; o < 8; o++) xq[8 + o] = zb[o];    // Z_+1 of the first row
                             }
                         }
+                      }
                         asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
-                        for (int tile = 0; tile < eT; tile++) {
-                          if ((tile & 1) == half) {
+                        // pass 2 body for one of this half's tiles (za/zb = its 24 acc2 columns)
+                        auto hst_tile = [&](int tile, const float* za, const float* zb) {
                             int r = tile * 128 + row_in_tile, ii, y, x;
                             const bool valid = rowpix(r, ii, y, x) && ii < nimg;
-                            float za[16], zb[8];
-                            const uint32_t col = (uint32_t)(tile * eNC2);
-                            tmem_ld16(tmem + lane_addr + col, za);
-                            tmem_ld8(tmem + lane_addr + col + 16, zb);
-                            tmem_wait_ld();
-                            init_acc2(b2n, tile);
                             float left[8], right[8];
 #pragma unroll
                             for (int o = 0; o < 8; o++) {
@@ -937,8 +963,48 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 }
                                 if (write_x) store8(xbuf, xlo_buf, 0, r, n8);
                             }
-                          }
-                          x_ready(tile);
+                        };
+                        if constexpr (S) {
+                            // two of this half's tiles per wait::ld; X-ready arrivals stay in tile order
+                            constexpr int NK = (CFG::T + 1) / 2;
+                            int next_arr = 0;
+#pragma unroll
+                            for (int k0 = 0; k0 < NK; k0 += 2) {
+                                float za[2][16], zb[2][8];
+#pragma unroll
+                                for (int u = 0; u < 2; u++) {
+                                    const int tile = 2 * (k0 + u) + half;
+                                    if (k0 + u < NK && tile < eT) {
+                                        const uint32_t col = (uint32_t)(tile * eNC2);
+                                        tmem_ld16(tmem + lane_addr + col, za[u]);
+                                        tmem_ld8(tmem + lane_addr + col + 16, zb[u]);
+                                    }
+                                }
+                                tmem_wait_ld();
+#pragma unroll
+                                for (int u = 0; u < 2; u++) {
+                                    const int tile = 2 * (k0 + u) + half;
+                                    if (k0 + u < NK && tile < eT) {
+                                        init_acc2(b2n, tile);
+                                        hst_tile(tile, za[u], zb[u]);
+                                        for (; next_arr <= tile; next_arr++) x_ready(next_arr);
+                                    }
+                                }
+                            }
+                            for (; next_arr < eT; next_arr++) x_ready(next_arr);
+                        } else {
+                            for (int tile = 0; tile < eT; tile++) {
+                                if ((tile & 1) == half) {
+                                    float za[16], zb[8];
+                                    const uint32_t col = (uint32_t)(tile * eNC2);
+                                    tmem_ld16(tmem + lane_addr + col, za);
+                                    tmem_ld8(tmem + lane_addr + col + 16, zb);
+                                    tmem_wait_ld();
+                                    init_acc2(b2n, tile);
+                                    hst_tile(tile, za, zb);
+                                }
+                                x_ready(tile);
+                            }
                         }
                         tmem_wait_st();
                         asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
