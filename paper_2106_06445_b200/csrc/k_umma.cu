@@ -231,9 +231,10 @@ __device__ __forceinline__ void issue_static_tiles(uint32_t tmem, uint32_t alo0,
 
 // Static stage configuration (0 = use the runtime plan)
 template <int WP_, int CP_, int MC_, int NC2_, int T_, int P3_, int SLOT_, int H_ = 0, int C_ = 0, int SST_ = 0,
-          int HST_ = 0>
+          int HST_ = 0, int RES_ = 0>
 struct SCfg {
     static constexpr bool HST = HST_ != 0;
+    static constexpr bool RES = RES_ != 0;   // residual blocks / ELU / fixed-point replays compiled in
     static constexpr bool kStatic = WP_ > 0;
     static constexpr int WP = WP_, CP = CP_, MC = MC_, NC2 = NC2_, T = T_, SLOT = SLOT_;
     static constexpr int H = H_, W = WP_ - 1, C = C_, SST = SST_;
@@ -337,7 +338,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
     // virtual blocks: R replays per block (R = fp_iters for the residual inverse, else 1).
     // Residual / ELU code exists only in the generic kernel (pick_kernel routes them there).
     constexpr bool kGen = !CFG::kStatic;
-    const bool residual = kGen && a.residual;
+    constexpr bool kRes = kGen || CFG::RES;   // residual / ELU / fixed-point code present
+    const bool residual = kRes && a.residual;
     const int R = (residual && a.inverse) ? a.fp_iters : 1;
     const int nbv = a.nb * R;
     // Batches are claimed dynamically (first one = blockIdx.x, then an atomic counter), so
@@ -746,7 +748,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                 const int t = a.inverse ? a.nb - 1 - tt / R : tt / R;
                 const int out_off = residual ? 0 : (((a.first_orient + t) & 1) == 0 ? ec : 0);
                 // fixed-point replays before the last only refresh the X planes (the iterate)
-                const bool store_state = !kGen || (tt % R) == R - 1;
+                const bool store_state = !kRes || (tt % R) == R - 1;
                 const float* b1 = a.bias + (int64_t)t * (p.Mp + eNC2);
                 const float* b2n = bias2_of(tt + 1 < nbv ? tt + 1 : 0);   // next block's conv2 bias
                 for (int j = 0; j < p.nch; j++) {
@@ -797,8 +799,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                         for (int h = 0; h < LW / 8; h++) {
                                             float h8[8];
 #pragma unroll
-                                            for (int e = 0; e < 8; e++)
-                                                h8[e] = a.act == 0 ? fmaxf(v[u][h * 8 + e], 0.f) : v[u][h * 8 + e];
+                                            for (int e = 0; e < 8; e++) {
+                                                const float hv = v[u][h * 8 + e];
+                                                h8[e] = a.act == 0 ? fmaxf(hv, 0.f)
+                                                                   : ((kRes && a.act == 1 && hv <= 0.f) ? expm1f(hv) : hv);
+                                            }
                                             store8(hbuf_j, hlo_buf, (cb1 + g * LW) / 8 + h, r, h8);
                                         }
                                     }
@@ -810,7 +815,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                     for (int e = 0; e < 8; e++) {
                                         float hv = v[u][h * 8 + e];   // bias: in TMEM
                                         if (a.act == 0) hv = fmaxf(hv, 0.f);
-                                        else if (kGen && a.act == 1) hv = hv > 0.f ? hv : expm1f(hv);
+                                        else if (kRes && a.act == 1) hv = hv > 0.f ? hv : expm1f(hv);
                                         h8[e] = valid ? hv : 0.f;
                                     }
                                     store8(hbuf_j, hlo_buf, (cb1 + g * LW) / 8 + h, r, h8);
@@ -845,7 +850,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 for (int e = 0; e < 8; e++) {
                                     float h = q8 < 2 ? va[q8 * 8 + e] : vb[(q8 - 2) * 8 + e];   // bias: folded or in TMEM
                                     if (a.act == 0) h = fmaxf(h, 0.f);
-                                    else if (kGen && a.act == 1) h = h > 0.f ? h : expm1f(h);
+                                    else if (kRes && a.act == 1) h = h > 0.f ? h : expm1f(h);
                                     h8[e] = valid ? h : 0.f;
                                 }
                                 store8(hbuf_j, hlo_buf, (cb1 + g0) / 8 + q8, r, h8);
@@ -1010,7 +1015,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                         asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
                     }
                     t_e2 += CLK() - te2h;
-                } else if (!S && (cw2 > 48 || (cw2 % 16 != 0 && cw2 != 8))) {
+                } else if ((!S || CFG::RES) && (cw2 > 48 || (cw2 % 16 != 0 && cw2 != 8))) {
                     // ---- generic widths (e.g. residual stages, c = 48 / 192): 16-column groups,
                     // old state read in place
                     TWAIT(w_a2, mbar_wait(acc2_full, a2ph)); a2ph ^= 1;
@@ -1369,12 +1374,15 @@ struct UmmaState {
 
 // ---- compile-time specialisations for the Arch-C stage plans (see make_plan) -----------------
 typedef void (*StageKernel)(StageArgs);
-struct SpecEntry { int Wp, Cp, MC, Nc2, T, p3, slot, H, c, sst, fold, split; StageKernel fn; };
-#define CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST) SCfg<WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, ((C) <= 8)>
-#define CI_SPEC(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST)                                       \
-    {WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST)::FOLD, \
-     CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST)::SPLIT,                               \
-     k_stage<CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST)>}
+struct SpecEntry { int Wp, Cp, MC, Nc2, T, p3, slot, H, c, sst, fold, split, res; StageKernel fn; };
+#define CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, RES) \
+    SCfg<WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, ((C) <= 8), RES>
+#define CI_SPEC_X(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, RES)                                     \
+    {WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, RES)::FOLD, \
+     CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, RES)::SPLIT, RES,                          \
+     k_stage<CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, RES)>}
+#define CI_SPEC(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST) CI_SPEC_X(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, 0)
+#define CI_SPEC_R(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST) CI_SPEC_X(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, 1)
 static const SpecEntry kSpecs[] = {
     CI_SPEC(17, 8, 32, 32, 7, 0, 16384, 16, 6, 1),   // C stage 1, bf16 (hst)
     CI_SPEC(9, 32, 32, 32, 7, 0, 16384, 8, 24, 0),   // C stage 2, bf16
@@ -1384,16 +1392,24 @@ static const SpecEntry kSpecs[] = {
     CI_SPEC(5, 96, 64, 96, 2, 1, 16384, 4, 96, 0),   // C stage 3, bf16x3
     CI_SPEC(17, 64, 32, 64, 5, 0, 16384, 16, 64, 0),  // learned-encoder tail (E2, E3), bf16
     CI_SPEC(17, 64, 32, 64, 3, 1, 16384, 16, 64, 0),  // learned-encoder tail (E2, E3), bf16x3
+    // i-ResNet variant of Arch C (f1, config C3R): residual blocks on 12 / 48 / 192 channels
+    CI_SPEC_R(17, 16, 64, 16, 5, 0, 16384, 16, 12, 1),    // CR stage 1, bf16
+    CI_SPEC_R(9, 48, 128, 48, 2, 0, 16384, 8, 48, 1),     // CR stage 2, bf16
+    CI_SPEC_R(5, 192, 64, 192, 2, 0, 16384, 4, 192, 0),   // CR stage 3, bf16
+    CI_SPEC_R(17, 16, 32, 16, 7, 1, 16384, 16, 12, 0),    // CR stage 1, bf16x3
+    CI_SPEC_R(9, 48, 64, 48, 2, 1, 16384, 8, 48, 1),      // CR stage 2, bf16x3
+    CI_SPEC_R(5, 192, 64, 192, 1, 1, 16384, 4, 192, 0),   // CR stage 3, bf16x3
 };
 
-// Specialised kernels are built for the additive-coupling ReLU/identity shapes only; residual
-// blocks and ELU (f1) always take the generic kernel, which is the only one carrying that code.
+// Coupling specialisations carry no residual / ELU code (it would cost them registers); residual
+// blocks and ELU use an RES specialisation or the generic kernel.
 static StageKernel pick_kernel(const StagePlan& p, const StageArgs& a) {
-    if (!getenv("CI_NO_STATIC") && !a.residual && a.act != 1)
+    if (!getenv("CI_NO_STATIC"))
         for (const auto& e : kSpecs)
             if (e.Wp == p.Wp && e.Cp == p.Cp && e.MC == p.MC && e.Nc2 == p.Nc2 && e.T == p.T && e.p3 == p.prec3 &&
                 e.slot == p.slot_bytes && e.H == p.H && e.c == p.c && e.sst == p.sstate &&
-                e.fold == p.fold && e.split == p.split)   // packing and epilogue must agree
+                e.fold == p.fold && e.split == p.split &&   // packing and epilogue must agree
+                e.res == (a.residual ? 1 : 0) && (a.act != 1 || e.res))
                 return e.fn;
     return k_stage<SDyn>;
 }
@@ -1598,7 +1614,9 @@ ci_status_t umma_stage(const Model* m, int s, float* state, int64_t n, bool inve
 extern "C" {
 ci_status_t ci_test_plan(int32_t H, int32_t W, int32_t c, int32_t m, int32_t prec3, int64_t* out16) {
     ci::StageInfo S{};
-    S.H = H; S.W = W; S.c = c; S.m = m; S.C = 2 * c; S.nb = 1;
+    const bool residual = c < 0;   // c < 0: residual stage (F acts on all |c| state channels)
+    if (residual) c = -c;
+    S.H = H; S.W = W; S.c = c; S.m = m; S.C = residual ? c : 2 * c; S.nb = 1;
     ci::StagePlan p;
     if (!ci::make_plan(S, prec3 != 0, p)) { ci::set_error("no plan"); return CI_ERR_UNSUPPORTED; }
     int64_t v[20] = {p.Wp, p.G, p.Cp, p.Mp, p.MC, p.nch, p.Nc2, p.T, p.I, p.Rtot, p.k1, p.k2,
