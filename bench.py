@@ -211,7 +211,7 @@ def main():
     ap.add_argument("--no-alt", action="store_true", help="skip the other-precision throughput line item")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the standalone HBM / online-decode / label-generation line items")
-    ap.add_argument("--inflight", type=int, default=2, choices=[1, 2],
+    ap.add_argument("--inflight", type=int, default=2, choices=[1, 2, 3, 4],
                     help="request batches in flight (2: consecutive steps alternate between two CUDA streams)")
     args = ap.parse_args()
 

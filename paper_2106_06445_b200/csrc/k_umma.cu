@@ -63,8 +63,10 @@ struct StagePlan {
                            //    [h Nc2/2, h Nc2/2 + c/2) (c = 24: 12 + 12 instead of 16 + 8)
     int fold;              // 1: conv1 bias folded into the MMA via a constant-1 input channel
                            //    (channel c of the padded X planes, Cp > c); epilogue adds none
-    int hst;               // conv2 "horizontal tap stacking": N = 3 taps x 8 outputs (c <= 8),
+    int hst;               // conv2 "horizontal tap stacking": N = 3 taps x hc outputs (c <= 24),
                            // 3 vertical k-steps per 16 hidden channels, col2im in the epilogue
+    int hc;                // hst: outputs per tap group (c rounded up to 8: 8, 16 or 24)
+    int xchg_bytes;        // hst: warp-boundary exchange buffer [T][4 quarters][2][hc] fp32
     int nhd;               // hidden plane buffers (2: double-buffered, conv1/epilogue overlap conv2)
     int sstate;            // 1: the batch's fp32 state lives in shared memory for the whole stage
     uint32_t sstate_off;   // byte offset of the fp32 state region in dynamic smem
@@ -235,6 +237,7 @@ template <int WP_, int CP_, int MC_, int NC2_, int T_, int P3_, int SLOT_, int H
 struct SCfg {
     static constexpr bool HST = HST_ != 0;
     static constexpr bool RES = RES_ != 0;   // residual blocks / ELU / fixed-point replays compiled in
+    static constexpr int HC = HST_ ? (C_ + 7) / 8 * 8 : 0;   // == StagePlan::hc
     static constexpr bool kStatic = WP_ > 0;
     static constexpr int WP = WP_, CP = CP_, MC = MC_, NC2 = NC2_, T = T_, SLOT = SLOT_;
     static constexpr int H = H_, W = WP_ - 1, C = C_, SST = SST_;
@@ -258,7 +261,6 @@ struct SCfg {
     static constexpr int LOH16 = (MC / 8) * PLANE16;
 };
 using SDyn = SCfg<0, 0, 0, 0, 0, 0, 0>;
-constexpr int kXchgBytes = 8 * 4 * 2 * 8 * 4;   // hst boundary exchange: [T<=8][quarter][2][8] fp32
 constexpr int kMaxTiles = 8;                     // T <= 8 (512 TMEM columns / >= 64 per tile)
 constexpr int kBarBytes = 384;                   // mbarriers, TMEM slot and batch queue
 
@@ -293,7 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
     uint8_t* hbuf = xbuf + (size_t)P * (p.Cp / 8) * plane_bytes;    // nhd x (P * MC/8 planes)
     const size_t hbuf_stride = (size_t)P * (p.MC / 8) * plane_bytes;
     float* xchg = reinterpret_cast<float*>(hbuf + (size_t)p.nhd * hbuf_stride);     // hst exchange
-    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(xchg) + kXchgBytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(xchg) + p.xchg_bytes);
     uint64_t* full = bars;                  // [kMaxSlots]
     uint64_t* empty = bars + kMaxSlots;     // [kMaxSlots]
     uint64_t* x_full = bars + 2 * kMaxSlots;
@@ -582,6 +584,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
         const bool ehst = S ? CFG::HST : (p.hst != 0);
         const bool efold = S ? CFG::FOLD : (p.fold != 0);   // X channel ec = 1 on valid pixels
         const bool esplit = S ? CFG::SPLIT : (p.split != 0);
+        const int ehc = S ? CFG::HC : p.hc;           // hst: outputs per tap group
         const int64_t eHW = (int64_t)eH * eW;
         constexpr int OLDN = S ? (CFG::NC2 / 2 > 0 ? CFG::NC2 / 2 : 8) : 48;
         const int ew = warp - 2;                       // 0..7
@@ -651,7 +654,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
         };
         auto init_acc2 = [&](const float* b2src, int tile) {
             const uint32_t base = tmem + lane_addr + (uint32_t)(tile * eNC2);
-            if (ehst) {   // centre-tap columns 8..15 carry b2[o], the other taps start at 0
+            if (ehst && ehc != 8) {   // columns [hc, 2hc) carry b2, the side taps start at 0
+#pragma unroll
+                for (int g = 0; g < 9; g++) {
+                    if (g * 8 >= 3 * ehc) break;
+                    float v8[8];
+#pragma unroll
+                    for (int e = 0; e < 8; e++) {
+                        const int col = g * 8 + e;
+                        v8[e] = (col >= ehc && col < 2 * ehc && col - ehc < ec) ? __ldg(b2src + col - ehc) : 0.f;
+                    }
+                    tmem_st8(base + (uint32_t)(g * 8), v8);
+                }
+            } else if (ehst) {   // centre-tap columns 8..15 carry b2[o], the other taps start at 0
                 float z16[16], z8[8];
 #pragma unroll
                 for (int e = 0; e < 8; e++) { z16[e] = 0.f; z16[8 + e] = e < ec ? __ldg(b2src + e) : 0.f; z8[e] = 0.f; }
@@ -874,7 +889,138 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                         mbar_arrive(&x_tile[tile]);
                     }
                 };
-                if (ehst) {
+                if (ehst && ehc != 8) {
+                    // ---- wide horizontal tap stacking (hc = 16 / 24 outputs per tap group): acc2
+                    // row r holds Z_v[r][o] at column (v+1)*hc + o; out[p][o] = Z_-1[p-1][o] +
+                    // Z_0[p][o] + Z_+1[p+1][o].  Same scheme as the 8-channel path: shuffles inside
+                    // a warp's 32 rows, a shared-memory exchange for the warp-boundary rows (pass 1),
+                    // alternate tiles per warp half, 8-channel groups.
+                    constexpr int HCW = S ? (CFG::HC > 0 ? CFG::HC : 8) : 24;   // register arrays
+                    TWAIT(w_a2, mbar_wait(acc2_full, a2ph)); a2ph ^= 1;
+                    fence_after();
+                    long long te2w = CLK();
+                    for (int tile = half; tile < eT; tile += 2) {
+                        const uint32_t col = (uint32_t)(tile * eNC2);
+                        float* xq = xchg + ((tile * 4 + quarter) * 2) * ehc;
+                        if constexpr (S) {
+                            float zl[HCW], zr[HCW];
+#pragma unroll
+                            for (int g = 0; g < HCW / 8; g++) {
+                                float t8[8];
+                                tmem_ld8(tmem + lane_addr + col + (uint32_t)(g * 8), t8);
+#pragma unroll
+                                for (int e = 0; e < 8; e++) zl[g * 8 + e] = t8[e];
+                                tmem_ld8(tmem + lane_addr + col + (uint32_t)(2 * ehc + g * 8), t8);
+#pragma unroll
+                                for (int e = 0; e < 8; e++) zr[g * 8 + e] = t8[e];
+                            }
+                            tmem_wait_ld();
+                            if (lane == 31) {
+#pragma unroll
+                                for (int o = 0; o < HCW; o++) xq[o] = zl[o];          // Z_-1, last row
+                            }
+                            if (lane == 0) {
+#pragma unroll
+                                for (int o = 0; o < HCW; o++) xq[ehc + o] = zr[o];    // Z_+1, first row
+                            }
+                        } else {
+                            for (int g = 0; g < ehc / 8; g++) {
+                                float zl8[8], zr8[8];
+                                tmem_ld8(tmem + lane_addr + col + (uint32_t)(g * 8), zl8);
+                                tmem_ld8(tmem + lane_addr + col + (uint32_t)(2 * ehc + g * 8), zr8);
+                                tmem_wait_ld();
+                                if (lane == 31) {
+#pragma unroll
+                                    for (int o = 0; o < 8; o++) xq[g * 8 + o] = zl8[o];
+                                }
+                                if (lane == 0) {
+#pragma unroll
+                                    for (int o = 0; o < 8; o++) xq[ehc + g * 8 + o] = zr8[o];
+                                }
+                            }
+                        }
+                    }
+                    asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+                    for (int tile = 0; tile < eT; tile++) {
+                        if ((tile & 1) == half) {
+                            int r = tile * 128 + row_in_tile, ii, y, x;
+                            const bool valid = rowpix(r, ii, y, x) && ii < nimg;
+                            const uint32_t col = (uint32_t)(tile * eNC2);
+                            float* dst = stb + ((int64_t)(valid ? ii : 0) * a.C + out_off) * eHW + (valid ? y * eW + x : 0);
+                            const int tqL = quarter > 0 ? tile : tile - 1, qqL = quarter > 0 ? quarter - 1 : 3;
+                            const int tqR = quarter < 3 ? tile : tile + 1, qqR = quarter < 3 ? quarter + 1 : 0;
+                            // one 8-channel group: Z_-1 / Z_0 / Z_+1 columns of this row
+                            auto group = [&](int g, const float* zl, const float* zc, const float* zr) {
+                                float left[8], right[8];
+#pragma unroll
+                                for (int o = 0; o < 8; o++) {
+                                    left[o] = __shfl_up_sync(0xffffffffu, zl[o], 1);
+                                    right[o] = __shfl_down_sync(0xffffffffu, zr[o], 1);
+                                }
+                                if (lane == 0) {
+#pragma unroll
+                                    for (int o = 0; o < 8; o++)
+                                        left[o] = tqL >= 0 ? xchg[((tqL * 4 + qqL) * 2) * ehc + g * 8 + o] : 0.f;
+                                }
+                                if (lane == 31) {
+#pragma unroll
+                                    for (int o = 0; o < 8; o++)
+                                        right[o] = tqR < eT ? xchg[((tqR * 4 + qqR) * 2 + 1) * ehc + g * 8 + o] : 0.f;
+                                }
+                                if (valid) {
+                                    float n8[8];
+#pragma unroll
+                                    for (int o = 0; o < 8; o++) {
+                                        const int oc = g * 8 + o;
+                                        float nv = 0.f;
+                                        if (oc < ec) {
+                                            const float f = left[o] + zc[o] + right[o];   // bias: in TMEM
+                                            const float old = a.fmode ? 0.f : dst[(int64_t)oc * eHW];
+                                            nv = a.fmode ? fmaxf(f, 0.f) : (a.inverse ? old - f : old + f);
+                                            if (store_state) dst[(int64_t)oc * eHW] = nv;
+                                        }
+                                        n8[o] = (efold && oc == ec) ? 1.f : nv;
+                                    }
+                                    if (write_x) store8(xbuf, xlo_buf, g, r, n8);
+                                }
+                            };
+                            if constexpr (S) {   // all groups' loads in flight, one wait
+                                float zl[HCW], zc[HCW], zr[HCW];
+#pragma unroll
+                                for (int g = 0; g < HCW / 8; g++) {
+                                    float t8[8];
+                                    tmem_ld8(tmem + lane_addr + col + (uint32_t)(g * 8), t8);
+#pragma unroll
+                                    for (int e = 0; e < 8; e++) zl[g * 8 + e] = t8[e];
+                                    tmem_ld8(tmem + lane_addr + col + (uint32_t)(ehc + g * 8), t8);
+#pragma unroll
+                                    for (int e = 0; e < 8; e++) zc[g * 8 + e] = t8[e];
+                                    tmem_ld8(tmem + lane_addr + col + (uint32_t)(2 * ehc + g * 8), t8);
+#pragma unroll
+                                    for (int e = 0; e < 8; e++) zr[g * 8 + e] = t8[e];
+                                }
+                                tmem_wait_ld();
+                                init_acc2(b2n, tile);
+#pragma unroll
+                                for (int g = 0; g < HCW / 8; g++) group(g, zl + g * 8, zc + g * 8, zr + g * 8);
+                            } else {             // generic kernel: one group at a time (registers)
+                                for (int g = 0; g < ehc / 8; g++) {
+                                    float zl[8], zc[8], zr[8];
+                                    tmem_ld8(tmem + lane_addr + col + (uint32_t)(g * 8), zl);
+                                    tmem_ld8(tmem + lane_addr + col + (uint32_t)(ehc + g * 8), zc);
+                                    tmem_ld8(tmem + lane_addr + col + (uint32_t)(2 * ehc + g * 8), zr);
+                                    tmem_wait_ld();
+                                    group(g, zl, zc, zr);
+                                }
+                                init_acc2(b2n, tile);   // after all groups were read
+                            }
+                        }
+                        x_ready(tile);
+                    }
+                    tmem_wait_st();
+                    asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+                    t_e2 += CLK() - te2w;
+                } else if (ehst) {
                     // ---- horizontal tap stacking: acc2 row r holds Z_v[r][o] at column (v+1)*8+o;
                     // out[p][o] = Z_-1[p-1][o] + Z_0[p][o] + Z_+1[p+1][o]  (col2im over v).
                     // Rows are lanes: neighbours come from warp shuffles, warp-boundary rows from
@@ -1199,38 +1345,50 @@ static double mma_cyc(int N) { return std::max(N / 2.0, 32.0 + N / 4.0); }
 //   a 2-slot ring cannot hide the L2 latency of the weight stream (x1.3)
 // Tuned plans for the Arch-C stage shapes (chosen from CI_DEBUG_CYCLES measurements);
 // other shapes use the cost model.
-struct TunedPlan { int H, W, c, m, prec3, MC, T, nhd, nslot; };
+struct TunedPlan { int H, W, c, m, prec3, MC, T, nhd, nslot, hst; };
 static const TunedPlan kTuned[] = {
-    {16, 16, 6, 64, 0, 32, 7, 2, 3},    // stage 1 bf16: SMEM-resident state fits
-    {8, 8, 24, 128, 0, 32, 7, 2, 3},    // stage 2 bf16
-    {4, 4, 96, 256, 0, 128, 2, 1, 4},   // stage 3 bf16
-    {16, 16, 6, 64, 1, 16, 7, 2, 4},    // stage 1 bf16x3
-    {8, 8, 24, 128, 1, 128, 2, 1, 3},   // stage 2 bf16x3
-    {4, 4, 96, 256, 1, 64, 2, 1, 3},    // stage 3 bf16x3
+    {16, 16, 6, 64, 0, 32, 7, 2, 3, 1},    // stage 1 bf16: SMEM-resident state fits
+    {8, 8, 24, 128, 0, 32, 4, 2, 3, 1},    // stage 2 bf16: wide hst (N = 3 x 24 -> 80)
+    {8, 8, 24, 128, 0, 32, 7, 2, 3, 0},    // stage 2 bf16, plain conv2 (CI_NO_WIDE_HST)
+    {4, 4, 96, 256, 0, 128, 2, 1, 4, 0},   // stage 3 bf16
+    {16, 16, 6, 64, 1, 16, 7, 2, 4, 1},    // stage 1 bf16x3
+    {8, 8, 24, 128, 1, 128, 2, 1, 3, 0},   // stage 2 bf16x3
+    {4, 4, 96, 256, 1, 64, 2, 1, 3, 0},    // stage 3 bf16x3
+    {16, 16, 12, 64, 0, 64, 5, 1, 4, 0},   // CR (residual, f1) stage 1 bf16
+    {16, 16, 12, 64, 1, 32, 7, 1, 3, 0},   // CR stage 1 bf16x3
 };
 
 static bool make_plan(const StageInfo& S, bool prec3, StagePlan& best) {
     StagePlan p{};
+    static const bool no_wide_hst = getenv("CI_NO_WIDE_HST") != nullptr;   // A/B switch
     const TunedPlan* tuned = nullptr;
-    for (const auto& tp : kTuned)
-        if (tp.H == S.H && tp.W == S.W && tp.c == S.c && tp.m == S.m && tp.prec3 == (prec3 ? 1 : 0)) tuned = &tp;
+    for (const auto& tp : kTuned)   // first match wins
+        if (!tuned && tp.H == S.H && tp.W == S.W && tp.c == S.c && tp.m == S.m && tp.prec3 == (prec3 ? 1 : 0) &&
+            !(no_wide_hst && tp.hst && tp.c > 8))
+            tuned = &tp;
     p.H = S.H; p.W = S.W; p.Wp = S.W + 1; p.G = p.Wp + 2;
     p.c = S.c; p.m = S.m;
     p.Cp = S.c <= 8 ? 8 : rup(S.c, 16);
     p.Mp = rup(S.m, 16);
-    p.hst = S.c <= 8 ? 1 : 0;
     p.fold = p.Cp > S.c ? 1 : 0;
-    p.Nc2 = p.hst ? 32 : rup(S.c, 16);
-    p.split = (!p.hst && S.c % 8 == 0 && S.c / 2 < p.Nc2 / 2 &&
-               (p.Nc2 / 2 == 8 || p.Nc2 / 2 == 16 || p.Nc2 / 2 == 32 || p.Nc2 / 2 == 48)) ? 1 : 0;
     p.pair = p.Cp == 8;
     p.prec3 = prec3 ? 1 : 0;
-    if (p.Nc2 > 256) return false;
     const int P = prec3 ? 2 : 1;
     const double P3f = prec3 ? 3.0 : 1.0;
     const int img_rows = (p.H + 1) * p.Wp;
     const int k1 = p.pair ? 6 : 9 * (p.Cp / 16);
     double best_cost = 1e300;
+    // conv2 with horizontal tap stacking (mandatory for c <= 8, optional up to c = 24) or plain
+    for (int hopt = 1; hopt >= 0; hopt--) {
+    if (hopt == 1 && (S.c > 24 || (S.c > 8 && no_wide_hst))) continue;
+    if (hopt == 0 && S.c <= 8) continue;
+    if (tuned && hopt != tuned->hst) continue;
+    p.hst = hopt;
+    p.hc = hopt ? rup(S.c, 8) : 0;
+    p.Nc2 = hopt ? rup(3 * p.hc, 16) : rup(S.c, 16);
+    p.split = (!p.hst && S.c % 8 == 0 && S.c / 2 < p.Nc2 / 2 &&
+               (p.Nc2 / 2 == 8 || p.Nc2 / 2 == 16 || p.Nc2 / 2 == 32 || p.Nc2 / 2 == 48)) ? 1 : 0;
+    if (p.Nc2 > 256) continue;
     for (int MC = p.Mp; MC >= 16; MC -= 16) {
         if (p.Mp % MC || MC > 256) continue;
         if (tuned && MC != tuned->MC) continue;
@@ -1247,8 +1405,9 @@ static bool make_plan(const StageInfo& S, bool prec3, StagePlan& best) {
                     if (tuned && nslot != tuned->nslot) continue;
                     const int slot_bytes = std::max(16384, std::max(kstep_bytes(MC, prec3), kstep_bytes(p.Nc2, prec3)));
                     const int Rtot = T * 128 + 2 * p.G;
+                    const int xchg = p.hst ? T * 4 * 2 * p.hc * 4 : 0;
                     const size_t smem0 = (size_t)nslot * slot_bytes + (size_t)P * ((p.Cp + nhd * MC) / 8) * Rtot * 16 +
-                                         kBarBytes + kXchgBytes;
+                                         kBarBytes + (size_t)rup(xchg, 16);
                     if (smem0 > kSmemCap) continue;
                     const size_t state_bytes = (size_t)I * S.C * p.H * p.W * 4;
                     const size_t soff = (smem0 + 127) / 128 * 128;
@@ -1273,11 +1432,13 @@ static bool make_plan(const StageInfo& S, bool prec3, StagePlan& best) {
                         best.k1 = k1; best.k2 = k2;
                         best.blk_bytes = (int64_t)wbytes;
                         best.est_cycles = cost;
+                        best.xchg_bytes = rup(xchg, 16);
                     }
                 }
             }
         }
     }
+    }   // hopt
     if (best_cost >= 1e300) return false;
     int cols = best.T * (best.MC + best.Nc2);
     best.tmem_cols = 32;
@@ -1287,7 +1448,7 @@ static bool make_plan(const StageInfo& S, bool prec3, StagePlan& best) {
 
 // conv2 output column n -> channel (-1 = padding column); see StagePlan::split
 static int conv2_col_channel(const StagePlan& p, int n) {
-    if (p.hst) return n < 24 ? n % 8 : -1;
+    if (p.hst) return n < 3 * p.hc ? n % p.hc : -1;
     if (!p.split) return n < p.c ? n : -1;
     const int hn = p.Nc2 / 2, hc = p.c / 2, hh = n / hn, e = n % hn;
     return e < hc ? hh * hc + e : -1;
@@ -1352,8 +1513,8 @@ static void pack_block(const StagePlan& p, const float* W1, const float* b1, con
             for (int n = 0; n < p.Nc2; n++)
                 for (int kk = 0; kk < 16; kk++) {
                     const int h = j * p.MC + kc * 16 + kk;
-                    if (p.hst)   // column n = (v+1)*8 + o, k-step row u = tap-1
-                        tile[(size_t)n * 16 + kk] = n < 24 ? w2(n % 8, h, tap - 1, n / 8 - 1) : 0.f;
+                    if (p.hst)   // column n = (v+1)*hc + o, k-step row u = tap-1
+                        tile[(size_t)n * 16 + kk] = n < 3 * p.hc ? w2(n % p.hc, h, tap - 1, n / p.hc - 1) : 0.f;
                     else
                         tile[(size_t)n * 16 + kk] = w2(conv2_col_channel(p, n), h, tap / 3 - 1, tap % 3 - 1);
                 }
@@ -1374,18 +1535,22 @@ struct UmmaState {
 
 // ---- compile-time specialisations for the Arch-C stage plans (see make_plan) -----------------
 typedef void (*StageKernel)(StageArgs);
-struct SpecEntry { int Wp, Cp, MC, Nc2, T, p3, slot, H, c, sst, fold, split, res; StageKernel fn; };
-#define CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, RES) \
-    SCfg<WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, ((C) <= 8), RES>
-#define CI_SPEC_X(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, RES)                                     \
-    {WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, RES)::FOLD, \
-     CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, RES)::SPLIT, RES,                          \
-     k_stage<CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, RES)>}
-#define CI_SPEC(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST) CI_SPEC_X(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, 0)
-#define CI_SPEC_R(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST) CI_SPEC_X(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, 1)
+struct SpecEntry { int Wp, Cp, MC, Nc2, T, p3, slot, H, c, sst, hst, fold, split, res; StageKernel fn; };
+#define CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES) \
+    SCfg<WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES>
+#define CI_SPEC_X(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES)                                          \
+    {WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST,                                                         \
+     CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES)::FOLD,                                  \
+     CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES)::SPLIT, RES,                            \
+     k_stage<CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES)>}
+#define CI_SPEC(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST) \
+    CI_SPEC_X(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, ((C) <= 8), 0)
+#define CI_SPEC_R(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST) \
+    CI_SPEC_X(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, ((C) <= 8), 1)
 static const SpecEntry kSpecs[] = {
     CI_SPEC(17, 8, 32, 32, 7, 0, 16384, 16, 6, 1),   // C stage 1, bf16 (hst)
-    CI_SPEC(9, 32, 32, 32, 7, 0, 16384, 8, 24, 0),   // C stage 2, bf16
+    CI_SPEC(9, 32, 32, 32, 7, 0, 16384, 8, 24, 0),   // C stage 2, bf16 (plain conv2)
+    CI_SPEC_X(9, 32, 32, 80, 4, 0, 16384, 8, 24, 1, 1, 0),   // C stage 2, bf16, wide hst, SMEM state
     CI_SPEC(5, 96, 128, 96, 2, 0, 16384, 4, 96, 0),  // C stage 3, bf16
     CI_SPEC(17, 8, 16, 32, 7, 1, 16384, 16, 6, 0),   // C stage 1, bf16x3 (hst)
     CI_SPEC(9, 32, 128, 32, 2, 1, 16384, 8, 24, 0),  // C stage 2, bf16x3
@@ -1407,7 +1572,7 @@ static StageKernel pick_kernel(const StagePlan& p, const StageArgs& a) {
     if (!getenv("CI_NO_STATIC"))
         for (const auto& e : kSpecs)
             if (e.Wp == p.Wp && e.Cp == p.Cp && e.MC == p.MC && e.Nc2 == p.Nc2 && e.T == p.T && e.p3 == p.prec3 &&
-                e.slot == p.slot_bytes && e.H == p.H && e.c == p.c && e.sst == p.sstate &&
+                e.slot == p.slot_bytes && e.H == p.H && e.c == p.c && e.sst == p.sstate && e.hst == p.hst &&
                 e.fold == p.fold && e.split == p.split &&   // packing and epilogue must agree
                 e.res == (a.residual ? 1 : 0) && (a.act != 1 || e.res))
                 return e.fn;
