@@ -68,7 +68,7 @@ the fused stage kernel.
 | C3 (Arch C, k=10, 1024 groups) | bf16 | {b['value']:,.0f} | {b['ms_per_step']:.2f} | {b['e2e']['value']:,.0f} | {b['roofline']['achieved']:.0f} ({b['roofline']['frac']:.3f}) |
 | C3 | fp32 parity (bf16x3) | {f['value']:,.0f} | {f['ms_per_step']:.2f} | {f['e2e']['value']:,.0f} | {f['roofline']['achieved']:.0f}, 3 MMAs issued per product ({f['roofline']['frac']:.3f}) |
 | C4 (learned encoder, heads 10+2) | bf16 | {c4['value']:,.0f} | {c4['ms_per_step']:.2f} | {c4['e2e']['value']:,.0f} | {c4['roofline']['achieved']:.0f} ({c4['roofline']['frac']:.3f}) |
-| C3R (f1: i-ResNet residual, N=10 fixed-point h^-1; generic kernel) | bf16 | {cr['value']:,.0f} | {cr['ms_per_step']:.2f} | {cr['e2e']['value']:,.0f} | {cr['roofline']['achieved']:.0f} ({cr['roofline']['frac']:.3f}) |
+| C3R (f1: i-ResNet residual, N=10 fixed-point h^-1) | bf16 | {cr['value']:,.0f} | {cr['ms_per_step']:.2f} | {cr['e2e']['value']:,.0f} | {cr['roofline']['achieved']:.0f} ({cr['roofline']['frac']:.3f}) |
 | reference arm = f64 CPU oracle, {ref['cpu_baseline']['cores']} cores | f64 | {ref['value']:.2f} | {ref['ms_per_step']:.0f} | — | — |
 
 Per-stage fused kernel (C3 bf16, single-stream profiled pass, avg over the 3 launch sizes):
