@@ -1354,7 +1354,8 @@ static const TunedPlan kTuned[] = {
     {16, 16, 6, 64, 1, 16, 7, 2, 4, 1},    // stage 1 bf16x3
     {8, 8, 24, 128, 1, 128, 2, 1, 3, 0},   // stage 2 bf16x3
     {4, 4, 96, 256, 1, 64, 2, 1, 3, 0},    // stage 3 bf16x3
-    {16, 16, 12, 64, 0, 64, 5, 1, 4, 0},   // CR (residual, f1) stage 1 bf16
+    {16, 16, 12, 64, 0, 32, 5, 2, 4, 1},   // CR (residual, f1) stage 1 bf16: wide hst (N = 48)
+    {16, 16, 12, 64, 0, 64, 5, 1, 4, 0},   // CR stage 1 bf16, plain conv2 (CI_NO_WIDE_HST)
     {16, 16, 12, 64, 1, 32, 7, 1, 3, 0},   // CR stage 1 bf16x3
 };
 
@@ -1558,7 +1559,8 @@ static const SpecEntry kSpecs[] = {
     CI_SPEC(17, 64, 32, 64, 5, 0, 16384, 16, 64, 0),  // learned-encoder tail (E2, E3), bf16
     CI_SPEC(17, 64, 32, 64, 3, 1, 16384, 16, 64, 0),  // learned-encoder tail (E2, E3), bf16x3
     // i-ResNet variant of Arch C (f1, config C3R): residual blocks on 12 / 48 / 192 channels
-    CI_SPEC_R(17, 16, 64, 16, 5, 0, 16384, 16, 12, 1),    // CR stage 1, bf16
+    CI_SPEC_R(17, 16, 64, 16, 5, 0, 16384, 16, 12, 1),    // CR stage 1, bf16 (plain conv2)
+    CI_SPEC_X(17, 16, 32, 48, 5, 0, 16384, 16, 12, 1, 1, 1),   // CR stage 1, bf16, wide hst
     CI_SPEC_R(9, 48, 128, 48, 2, 0, 16384, 8, 48, 1),     // CR stage 2, bf16
     CI_SPEC_R(5, 192, 64, 192, 2, 0, 16384, 4, 192, 0),   // CR stage 3, bf16
     CI_SPEC_R(17, 16, 32, 16, 7, 1, 16384, 16, 12, 0),    // CR stage 1, bf16x3
