@@ -187,6 +187,17 @@ CI_API ci_status_t ci_serve_group_host(const ci_model_t* model, ci_encode_mode_t
                                 int32_t* labels_host, void* ws, size_t ws_bytes,
                                 ci_stream_t stream);
 
+/* Same as ci_serve_group_host without the final synchronisation: the whole chunked
+ * H2D -> compute -> D2H pipeline is enqueued and the call returns; `stream` completes when the
+ * outputs are in the host buffers.  Until then the host buffers must stay alive and unmodified
+ * and the workspace must not be reused.  Calls with distinct workspaces (and streams) may be in
+ * flight together: their copies and compute overlap. */
+CI_API ci_status_t ci_serve_group_host_async(const ci_model_t* model, ci_encode_mode_t mode, int32_t k,
+                                             int64_t B, const float* x_host, const int32_t* drop_host,
+                                             float* h_out_host, float* h_parity_host, float* logits_host,
+                                             int32_t* labels_host, void* ws, size_t ws_bytes,
+                                             ci_stream_t stream);
+
 /* ---- Worker-partitioned serving (config C5: one worker per GPU) ----
  * Decode is linear, so it rides a reduction over workers: worker w contributes coef_w[b] * f_w[b]
  * and the sum over all n = k + 1 workers is the decoded feature of the lost worker of group b:

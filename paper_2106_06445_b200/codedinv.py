@@ -32,7 +32,7 @@ EXPORTS = ["ci_last_error", "ci_model_create", "ci_model_destroy", "ci_feature_d
            "ci_decode", "ci_classify", "ci_serve_group", "ci_workspace_size_host",
            "ci_serve_group_host", "ci_make_drops", "ci_worker_coef", "ci_combine",
            "ci_workspace_size_general", "ci_encode_general", "ci_decode_general", "ci_serve_general",
-           "ci_encode_perturbed", "ci_online_update"]
+           "ci_encode_perturbed", "ci_online_update", "ci_serve_group_host_async"]
 TESTING_EXPORTS = ["ci_test_umma_gemm", "ci_test_umma_rate", "ci_test_prof_enable", "ci_test_prof_read",
                    "ci_test_launch_count", "ci_test_mean", "ci_test_plan"]  # include/codedinv_testing.h
 
@@ -66,6 +66,7 @@ _sig = {
     "ci_serve_group": (_I32, [_P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "ci_workspace_size_host": (_I32, [_P, _I32, _I64, _P]),
     "ci_serve_group_host": (_I32, [_P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "ci_serve_group_host_async": (_I32, [_P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "ci_make_drops": (_I32, [_I32, _I64, ctypes.c_uint64, _P, _P]),
     "ci_worker_coef": (_I32, [_I32, _I32, _I64, _I32, _P, _P, _P]),
     "ci_combine": (_I32, [_I64, _I64, _P, _P, _P, _P]),
@@ -224,11 +225,14 @@ class Model:
                                    _ptr(h_parity), _ptr(x_parity), _ptr(logits), _ptr(labels),
                                    _ptr(ws), ws.numel(), _stream(stream)), "ci_serve_group")
 
-    def ci_serve_group_host(self, x, drop, h_out, h_parity, logits, labels, ws, stream=None, learned=False):
+    def ci_serve_group_host(self, x, drop, h_out, h_parity, logits, labels, ws, stream=None, learned=False,
+                            sync=True):
+        """sync=False: ci_serve_group_host_async (returns after enqueueing; sync the stream)."""
         B, k = x.shape[0], x.shape[1]
-        _check(_lib.ci_serve_group_host(self._h, CI_ENC_LEARNED if learned else CI_ENC_EXACT, k, B, _ptr(x), _ptr(drop), _ptr(h_out),
-                                        _ptr(h_parity), _ptr(logits), _ptr(labels), _ptr(ws), ws.numel(),
-                                        _stream(stream)), "ci_serve_group_host")
+        fn = _lib.ci_serve_group_host if sync else _lib.ci_serve_group_host_async
+        _check(fn(self._h, CI_ENC_LEARNED if learned else CI_ENC_EXACT, k, B, _ptr(x), _ptr(drop), _ptr(h_out),
+                  _ptr(h_parity), _ptr(logits), _ptr(labels), _ptr(ws), ws.numel(), _stream(stream)),
+               "ci_serve_group_host")
 
     def ci_check(self, ws, stream=None):
         _check(_lib.ci_check(self._h, _ptr(ws), ws.numel(), _stream(stream)), "ci_check")

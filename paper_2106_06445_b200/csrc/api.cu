@@ -703,11 +703,22 @@ ci_status_t ci_workspace_size_host(const ci_model_t* model, int32_t k, int64_t B
     return CI_OK;
 }
 
-ci_status_t ci_serve_group_host(const ci_model_t* model, ci_encode_mode_t mode, int32_t k,
-                                int64_t B, const float* x_host, const int32_t* drop_host,
-                                float* h_out_host, float* h_parity_host, float* logits_host,
-                                int32_t* labels_host, void* ws, size_t ws_bytes,
-                                ci_stream_t stream) {
+}  // extern "C"
+
+namespace ci {
+// fold workspace 1's drop-error count into workspace 0's flag (read by ci_check)
+__global__ void k_fold_flag(int* f0, int* f1) {
+    if (threadIdx.x == 0 && *f1) { *f0 += *f1; *f1 = 0; }
+}
+}  // namespace ci
+
+extern "C" {
+
+static ci_status_t serve_host_impl(const ci_model_t* model, ci_encode_mode_t mode, int32_t k,
+                                   int64_t B, const float* x_host, const int32_t* drop_host,
+                                   float* h_out_host, float* h_parity_host, float* logits_host,
+                                   int32_t* labels_host, void* ws, size_t ws_bytes,
+                                   ci_stream_t stream, bool sync) {
     CI_MODEL_OR_FAIL(m, model);
     if (mode != CI_ENC_EXACT && mode != CI_ENC_LEARNED) { set_error("unknown encode mode"); return CI_ERR_INVALID_ARG; }
     if (mode == CI_ENC_LEARNED && m->enc_off < 0) { set_error("model has no learned encoder"); return CI_ERR_UNSUPPORTED; }
@@ -772,19 +783,31 @@ ci_status_t ci_serve_group_host(const ci_model_t* model, ci_encode_mode_t mode, 
     }
     CI_CUDA(cudaEventRecord(P->fin, P->d2h));
     CI_CUDA(cudaStreamWaitEvent(st, P->fin, 0));
-    CI_CUDA(cudaStreamSynchronize(st));
-    if (H.nc > 1) {   // fold workspace 1's drop-error count into workspace 0's flag (ci_check)
-        int f[2] = {0, 0};
-        CI_CUDA(cudaMemcpy(&f[0], ws, sizeof(int), cudaMemcpyDeviceToHost));
-        CI_CUDA(cudaMemcpy(&f[1], at<char>(ws, H.dev1), sizeof(int), cudaMemcpyDeviceToHost));
-        if (f[1]) {
-            f[0] += f[1];
-            f[1] = 0;
-            CI_CUDA(cudaMemcpy(ws, &f[0], sizeof(int), cudaMemcpyHostToDevice));
-            CI_CUDA(cudaMemcpy(at<char>(ws, H.dev1), &f[1], sizeof(int), cudaMemcpyHostToDevice));
-        }
+    if (H.nc > 1) {   // workspace 1's drop-error count -> workspace 0's flag (ci_check)
+        ci::k_fold_flag<<<1, 32, 0, st>>>(reinterpret_cast<int*>(ws), at<int>(ws, H.dev1));
+        count_launch();
+        CI_CUDA(cudaGetLastError());
     }
+    if (sync) CI_CUDA(cudaStreamSynchronize(st));
     return CI_OK;
+}
+
+ci_status_t ci_serve_group_host(const ci_model_t* model, ci_encode_mode_t mode, int32_t k,
+                                int64_t B, const float* x_host, const int32_t* drop_host,
+                                float* h_out_host, float* h_parity_host, float* logits_host,
+                                int32_t* labels_host, void* ws, size_t ws_bytes,
+                                ci_stream_t stream) {
+    return serve_host_impl(model, mode, k, B, x_host, drop_host, h_out_host, h_parity_host, logits_host,
+                           labels_host, ws, ws_bytes, stream, true);
+}
+
+ci_status_t ci_serve_group_host_async(const ci_model_t* model, ci_encode_mode_t mode, int32_t k,
+                                      int64_t B, const float* x_host, const int32_t* drop_host,
+                                      float* h_out_host, float* h_parity_host, float* logits_host,
+                                      int32_t* labels_host, void* ws, size_t ws_bytes,
+                                      ci_stream_t stream) {
+    return serve_host_impl(model, mode, k, B, x_host, drop_host, h_out_host, h_parity_host, logits_host,
+                           labels_host, ws, ws_bytes, stream, false);
 }
 
 ci_status_t ci_test_mean(int32_t k, int64_t B, int64_t d, const float* h, float* m, ci_stream_t stream) {

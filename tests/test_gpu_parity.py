@@ -331,6 +331,35 @@ def test_host_entry_point_chunked(ci, B, learned):
     m.ci_check(ws)   # cleared
 
 
+def test_host_entry_async_two_in_flight(ci):
+    """ci_serve_group_host_async: two calls with their own workspaces / outputs on two streams,
+    in flight together, give exactly the synchronous results."""
+    c = fx.CONFIGS["C3"]
+    B, k, arch = 300, c.k, c.arch
+    params = fx.make_weights(arch, c.seed_w)
+    m = model(ci, arch, params, "bf16")
+    xs = [fx.make_inputs(arch, B, k, s) for s in (1, 2)]
+    drops = [fx.make_drops(B, k, s) for s in (3, 4)]
+    def bufs():
+        return [np.empty((B, k, arch.d), np.float32), np.empty((B, arch.d), np.float32),
+                np.empty(B * k * 10, np.float32), np.empty(B * k, np.int32)]
+    ref = []
+    for i in range(2):
+        o = bufs()
+        m.ci_serve_group_host(xs[i], drops[i], *o, m.workspace(k, B, host=True))
+        ref.append(o)
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [bufs(), bufs()]
+    wss = [m.workspace(k, B, host=True) for _ in range(2)]
+    for i in range(2):
+        m.ci_serve_group_host(xs[i], drops[i], *outs[i], wss[i], stream=streams[i], sync=False)
+    torch.cuda.synchronize()
+    for i in range(2):
+        m.ci_check(wss[i])
+        for a_, b_ in zip(outs[i], ref[i]):
+            assert np.array_equal(a_, b_)
+
+
 # ------------------------------------------------------------------ learned encoder (a3', C4)
 @pytest.mark.parametrize("prec", PRECS)
 def test_serve_learned_small_arch(ci, prec):
