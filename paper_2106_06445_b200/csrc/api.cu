@@ -619,9 +619,11 @@ ci_status_t ci_serve_general(const ci_model_t* model, int32_t k, int32_t r, int6
 // sees its flag) | dev workspace 1 | x | drop | h | p | logits | labels (full size).
 static constexpr int kMaxChunks = 8;
 
-static int host_chunks(int64_t B) {
+// chunks per call: a lone synchronous call overlaps its own copies with compute (4 chunks); async
+// calls overlap with each other, so fewer, more efficient chunks (2) win (measured, bench e2e)
+static int host_chunks(int64_t B, bool async_call) {
     static const int env = getenv("CI_HOST_CHUNKS") ? atoi(getenv("CI_HOST_CHUNKS")) : 0;
-    int nc = env > 0 ? env : (B >= 512 ? 4 : B >= 64 ? 2 : 1);
+    int nc = env > 0 ? env : (B >= 512 ? (async_call ? 2 : 4) : B >= 64 ? 2 : 1);
     nc = std::min(nc, kMaxChunks);
     return (int)std::max<int64_t>(1, std::min<int64_t>(nc, B));
 }
@@ -633,9 +635,9 @@ struct HostLayout {
     size_t dev1 = 0, x = 0, drop = 0, h = 0, p = 0, logits = 0, labels = 0, total = 0;
 };
 
-static HostLayout host_layout(const Model* m, int32_t k, int64_t B) {
+static HostLayout host_layout(const Model* m, int32_t k, int64_t B, bool async_call) {
     HostLayout H;
-    H.nc = host_chunks(B);
+    H.nc = host_chunks(B, async_call);
     H.Bc = (B + H.nc - 1) / H.nc;
     H.dev = ws_layout(m, k, H.Bc);
     int64_t n = B * (int64_t)k;
@@ -699,7 +701,7 @@ extern "C" {
 ci_status_t ci_workspace_size_host(const ci_model_t* model, int32_t k, int64_t B, size_t* bytes) {
     const Model* m = reinterpret_cast<const Model*>(model);
     if (!m || !bytes || k < 1 || B < 0) { set_error("invalid argument"); return CI_ERR_INVALID_ARG; }
-    *bytes = host_layout(m, k, B).total;
+    *bytes = std::max(host_layout(m, k, B, false).total, host_layout(m, k, B, true).total);
     return CI_OK;
 }
 
@@ -723,7 +725,7 @@ static ci_status_t serve_host_impl(const ci_model_t* model, ci_encode_mode_t mod
     if (mode != CI_ENC_EXACT && mode != CI_ENC_LEARNED) { set_error("unknown encode mode"); return CI_ERR_INVALID_ARG; }
     if (mode == CI_ENC_LEARNED && m->enc_off < 0) { set_error("model has no learned encoder"); return CI_ERR_UNSUPPORTED; }
     if (k < 1 || B < 0 || (B > 0 && (!x_host || !drop_host))) { set_error("invalid argument"); return CI_ERR_INVALID_ARG; }
-    HostLayout H = host_layout(m, k, B);
+    HostLayout H = host_layout(m, k, B, !sync);
     if (!ws || !aligned16(ws) || ws_bytes < H.total) {
         set_error("host workspace %zu bytes; need %zu", ws_bytes, H.total); return CI_ERR_WORKSPACE;
     }
