@@ -50,7 +50,7 @@ CI_API int64_t ci_test_launch_count(int32_t reset);
  * (H x W state, c = half channels, m = hidden width; c < 0: a residual stage whose F acts on
  * all |c| state channels).  out16 = {Wp, G, Cp, Mp, MC, nch, Nc2,
  * T, I, Rtot, k1, k2, nslot, slot_bytes, smem_bytes, packed_bytes_per_block, nhd, sstate,
- * est_cycles_per_image_per_block, tmem_cols}  (20 entries). */
+ * est_cycles_per_image_per_block, tmem_cols, hst, hc, has_specialised_kernel}  (23 entries). */
 CI_API ci_status_t ci_test_plan(int32_t H, int32_t W, int32_t c, int32_t m, int32_t prec3, int64_t* out16);
 
 /* The encode-mean kernel alone: m [B][d] = (sum_{i<k} h[b][i]) / k  (as inside ci_encode). */

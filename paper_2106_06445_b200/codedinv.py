@@ -311,10 +311,10 @@ def ci_test_mean(h, m, stream=None):
 
 
 PLAN_FIELDS = ["Wp", "G", "Cp", "Mp", "MC", "nch", "Nc2", "T", "I", "Rtot", "k1", "k2", "nslot",
-               "slot_bytes", "smem", "blk_bytes", "nhd", "sstate", "est", "tmem_cols"]
+               "slot_bytes", "smem", "blk_bytes", "nhd", "sstate", "est", "tmem_cols", "hst", "hc", "static"]
 
 
 def ci_test_plan(H, W, c, m, prec3):
-    out = (ctypes.c_int64 * 20)()
+    out = (ctypes.c_int64 * len(PLAN_FIELDS))()
     _check(_lib.ci_test_plan(H, W, c, m, 1 if prec3 else 0, out), "ci_test_plan")
     return dict(zip(PLAN_FIELDS, list(out)))

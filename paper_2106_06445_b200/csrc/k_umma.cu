@@ -1565,7 +1565,7 @@ static const SpecEntry kSpecs[] = {
     CI_SPEC_R(5, 192, 64, 192, 2, 0, 16384, 4, 192, 0),   // CR stage 3, bf16
     CI_SPEC_R(17, 16, 32, 16, 7, 1, 16384, 16, 12, 0),    // CR stage 1, bf16x3
     CI_SPEC_R(9, 48, 64, 48, 2, 1, 16384, 8, 48, 1),      // CR stage 2, bf16x3
-    CI_SPEC_R(5, 192, 64, 192, 1, 1, 16384, 4, 192, 0),   // CR stage 3, bf16x3
+    CI_SPEC_R(5, 192, 128, 192, 1, 1, 16384, 4, 192, 0),  // CR stage 3, bf16x3
 };
 
 // Coupling specialisations carry no residual / ELU code (it would cost them registers); residual
@@ -1786,10 +1786,14 @@ ci_status_t ci_test_plan(int32_t H, int32_t W, int32_t c, int32_t m, int32_t pre
     S.H = H; S.W = W; S.c = c; S.m = m; S.C = residual ? c : 2 * c; S.nb = 1;
     ci::StagePlan p;
     if (!ci::make_plan(S, prec3 != 0, p)) { ci::set_error("no plan"); return CI_ERR_UNSUPPORTED; }
-    int64_t v[20] = {p.Wp, p.G, p.Cp, p.Mp, p.MC, p.nch, p.Nc2, p.T, p.I, p.Rtot, p.k1, p.k2,
+    ci::StageArgs sa{};
+    sa.residual = residual ? 1 : 0;
+    sa.act = residual ? 1 : 0;   // the residual archs use ELU, the coupling archs ReLU
+    const bool has_static = ci::pick_kernel(p, sa) != ci::k_stage<ci::SDyn>;
+    int64_t v[23] = {p.Wp, p.G, p.Cp, p.Mp, p.MC, p.nch, p.Nc2, p.T, p.I, p.Rtot, p.k1, p.k2,
                      p.nslot, p.slot_bytes, (int64_t)p.smem, p.blk_bytes, p.nhd, p.sstate,
-                     (int64_t)p.est_cycles, p.tmem_cols};
-    for (int i = 0; i < 20; i++) out16[i] = v[i];
+                     (int64_t)p.est_cycles, p.tmem_cols, p.hst, p.hc, has_static ? 1 : 0};
+    for (int i = 0; i < 23; i++) out16[i] = v[i];
     return CI_OK;
 }
 ci_status_t ci_test_prof_enable(int32_t enable) {

@@ -86,3 +86,23 @@ def test_binding_has_no_cpu_fallback():
             if f.endswith((".py", ".cu", ".h", ".cpp")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in src.replace("no CPU fallback", ""), f
+
+
+def test_hot_path_plans_have_specialised_kernels():
+    """Every stage of the benchmarked archs (C3/C4: Arch C; C3R: the residual arch) in both
+    tensor-core precisions must dispatch to a compile-time specialised stage kernel: a plan/spec
+    mismatch (e.g. the SMEM-state flag) would silently fall back to the ~3x slower generic
+    kernel.  Host-only planner query, no GPU needed."""
+    from paper_2106_06445_b200 import codedinv as ci
+    import fixtures as fx
+    for arch in (fx.ARCH_C, fx.ARCH_CR):
+        for (C, H, W, c, m, nb) in arch.stage_shapes():
+            for prec3 in (0, 1):
+                q = -c if arch.block == "residual" else c
+                plan = ci.ci_test_plan(H, W, q, m, prec3)
+                assert plan["static"] == 1, (arch.name, H, c, m, prec3, plan)
+                assert plan["tmem_cols"] <= 512 and plan["smem"] <= 227 * 1024
+    # the tuned Arch-C bf16 plans use horizontal tap stacking on stages 1-2
+    assert ci.ci_test_plan(16, 16, 6, 64, 0)["hst"] == 1
+    p2 = ci.ci_test_plan(8, 8, 24, 128, 0)
+    assert p2["hst"] == 1 and p2["hc"] == 24 and p2["Nc2"] == 80
