@@ -1352,7 +1352,8 @@ static const TunedPlan kTuned[] = {
     {8, 8, 24, 128, 0, 32, 7, 2, 3, 0},    // stage 2 bf16, plain conv2 (CI_NO_WIDE_HST)
     {4, 4, 96, 256, 0, 128, 2, 1, 4, 0},   // stage 3 bf16
     {16, 16, 6, 64, 1, 16, 7, 2, 4, 1},    // stage 1 bf16x3
-    {8, 8, 24, 128, 1, 128, 2, 1, 3, 0},   // stage 2 bf16x3
+    {8, 8, 24, 128, 1, 64, 3, 1, 3, 1},    // stage 2 bf16x3: wide hst
+    {8, 8, 24, 128, 1, 128, 2, 1, 3, 0},   // stage 2 bf16x3, plain conv2 (CI_NO_WIDE_HST)
     {4, 4, 96, 256, 1, 64, 2, 1, 3, 0},    // stage 3 bf16x3
     {16, 16, 12, 64, 0, 32, 5, 2, 4, 1},   // CR (residual, f1) stage 1 bf16: wide hst (N = 48)
     {16, 16, 12, 64, 0, 64, 5, 1, 4, 0},   // CR stage 1 bf16, plain conv2 (CI_NO_WIDE_HST)
@@ -1554,7 +1555,8 @@ static const SpecEntry kSpecs[] = {
     CI_SPEC_X(9, 32, 32, 80, 4, 0, 16384, 8, 24, 1, 1, 0),   // C stage 2, bf16, wide hst, SMEM state
     CI_SPEC(5, 96, 128, 96, 2, 0, 16384, 4, 96, 0),  // C stage 3, bf16
     CI_SPEC(17, 8, 16, 32, 7, 1, 16384, 16, 6, 0),   // C stage 1, bf16x3 (hst)
-    CI_SPEC(9, 32, 128, 32, 2, 1, 16384, 8, 24, 0),  // C stage 2, bf16x3
+    CI_SPEC(9, 32, 128, 32, 2, 1, 16384, 8, 24, 0),  // C stage 2, bf16x3 (plain conv2)
+    CI_SPEC_X(9, 32, 64, 80, 3, 1, 16384, 8, 24, 0, 1, 0),   // C stage 2, bf16x3, wide hst
     CI_SPEC(5, 96, 64, 96, 2, 1, 16384, 4, 96, 0),   // C stage 3, bf16x3
     CI_SPEC(17, 64, 32, 64, 5, 0, 16384, 16, 64, 0),  // learned-encoder tail (E2, E3), bf16
     CI_SPEC(17, 64, 32, 64, 3, 1, 16384, 16, 64, 0),  // learned-encoder tail (E2, E3), bf16x3
