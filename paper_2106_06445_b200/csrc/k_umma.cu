@@ -231,6 +231,57 @@ __device__ __forceinline__ void issue_static_tiles(uint32_t tmem, uint32_t alo0,
     }
 }
 
+// Tile-streamed segment (STREAM configurations): all of the segment's weight slots are resident,
+// tile t is issued once dep[min(t + AHEAD, T-1)] completes (the epilogue has produced what
+// tile t reads: X / hidden rows of tiles <= t+1, or acc1 tile t read), and -- when `done` is
+// given -- a per-tile commit lets the epilogue consume tile t while later tiles still run.
+template <int K, int PER, bool PAIR, bool HSTK, int WP, int PLANE16, int G, int KB16, int T, int N, bool P3,
+          int LOA16, int ACC0, int DSTRIDE, int AHEAD>
+__device__ __forceinline__ void issue_stream(uint32_t tmem, uint32_t alo0, uint32_t ringlo, uint32_t slot16,
+                                             uint32_t idesc, uint32_t acc_first, int& slot, uint32_t& phase,
+                                             int nslot, uint64_t* full, uint64_t* empty, uint64_t* dep,
+                                             uint32_t dph, uint64_t* done) {
+    constexpr uint32_t HI = 0x4008u;
+    constexpr int NS = (K + G - 1) / G;
+    uint32_t bl[NS];
+    asm volatile("" : "+r"(alo0), "+r"(ringlo));
+    {
+        int sl = slot;
+        uint32_t ph = phase;
+#pragma unroll
+        for (int q = 0; q < NS; q++) {
+            mbar_wait(&full[sl], ph);
+            bl[q] = ringlo + (uint32_t)sl * slot16;
+            if (++sl == nslot) { sl = 0; ph ^= 1; }
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < T; t++) {
+        mbar_wait(&dep[t + AHEAD < T ? t + AHEAD : T - 1], dph);
+        fence_after();
+#pragma unroll
+        for (int s = 0; s < K; s++) {
+            const int shift = PAIR ? (s / 2 - 1) * WP + ((s & 1) ? 1 : -1)
+                                   : (HSTK ? (s / PER - 1) * WP : ((s / PER) / 3 - 1) * WP + ((s / PER) % 3 - 1));
+            const int poff16 = PAIR ? 0 : 2 * (s % PER) * PLANE16;
+            const uint64_t ad = ((uint64_t)HI << 32) | (alo0 + (uint32_t)(shift + poff16 + t * 128));
+            const uint64_t bd = ((uint64_t)HI << 32) | (bl[s / G] + (uint32_t)((s % G) * KB16));
+            const uint32_t d = tmem + (uint32_t)(ACC0 + t * DSTRIDE);
+            mma_bf16(d, ad, bd, idesc, s == 0 ? acc_first : 1u);
+            if (P3) {
+                mma_bf16(d, ad, bd + (uint64_t)(N * 2), idesc, 1u);
+                mma_bf16(d, ad + (uint64_t)LOA16, bd, idesc, 1u);
+            }
+        }
+        if (done) commit(&done[t]);
+    }
+#pragma unroll
+    for (int q = 0; q < NS; q++) {
+        commit(&empty[slot]);
+        if (++slot == nslot) { slot = 0; phase ^= 1; }
+    }
+}
+
 // Static stage configuration (0 = use the runtime plan)
 template <int WP_, int CP_, int MC_, int NC2_, int T_, int P3_, int SLOT_, int H_ = 0, int C_ = 0, int SST_ = 0,
           int HST_ = 0, int RES_ = 0>
@@ -259,10 +310,25 @@ struct SCfg {
     static constexpr int ACC1 = T * NC2;
     static constexpr int LOX16 = (CP / 8) * PLANE16;
     static constexpr int LOH16 = (MC / 8) * PLANE16;
+    // Tile-streamed block schedule: every segment's weights fit one ring slot,
+    // 8-channel hst conv2, folded conv1 bias, 2-tile batched conv1 epilogue.  Hand-offs between
+    // the MMA thread and the epilogue are per M-tile instead of per segment, so conv1 of chunk
+    // j+1 runs behind the conv1 epilogue of chunk j and the conv2 epilogue runs behind the last
+    // conv2 chunk.  -DCI_NO_STREAM keeps the per-segment schedule (same-box A/B).
+#if defined(CI_NO_STREAM) || defined(CI_NO_EPI1_BATCH)
+    static constexpr bool STREAM = false;
+#else
+    static constexpr bool STREAM = kStatic && HST && HC == 8 && FOLD && !RES && MC == 32 && K1 <= G1 && K2 <= G2;
+#endif
+#ifdef CI_NO_EPI1_PIPE
+    static constexpr bool EPI1_PIPE = false;
+#else
+    static constexpr bool EPI1_PIPE = true;   // STREAM conv1 epilogue: relu only (act 0)
+#endif
 };
 using SDyn = SCfg<0, 0, 0, 0, 0, 0, 0>;
 constexpr int kMaxTiles = 8;                     // T <= 8 (512 TMEM columns / >= 64 per tile)
-constexpr int kBarBytes = 384;                   // mbarriers, TMEM slot and batch queue
+constexpr int kBarBytes = 640;                   // mbarriers, TMEM slot and batch queue
 
 // Cycle instrumentation (CI_DEBUG_CYCLES; inactive unless requested).  -DCI_NO_CYCLES
 // compiles it out; same-box A/B showed no gain from that (s2 got slower), so it stays in.
@@ -311,6 +377,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
     // x_tile[t]: the bf16 X rows of M-tile t are final for the next conv1 (every epilogue
     // thread arrives on every tile, in tile order; x_full itself is unused)
     uint64_t* x_tile = x_full + 20;    // [kMaxTiles]
+    // STREAM schedule: per-tile hand-offs (see SCfg::STREAM)
+    uint64_t* a1t = x_full + 28;       // [kMaxTiles] conv1 of tile t done (tcgen05.commit)
+    uint64_t* a1f = x_full + 36;       // [kMaxTiles] acc1 tile t read by the conv1 epilogue (all threads)
+    uint64_t* hdt = x_full + 44;       // [2][kMaxTiles] hidden rows of tile t written (all threads)
+    uint64_t* a2t = x_full + 60;       // [kMaxTiles] last conv2 chunk of tile t done (tcgen05.commit)
 
     // ---- zero the activation buffers (pads and guards must read as 0)
     {
@@ -327,6 +398,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
         for (int i = 0; i < 2; i++) { mbar_init(&hd_full[i], kEpiThreads); mbar_init(&hd_empty[i], 1); }
         mbar_init(acc2_full, 1);
         for (int i = 0; i < 4; i++) { mbar_init(&bqf[i], 1); mbar_init(&bqe[i], 1 + kEpiThreads); }
+        for (int i = 0; i < kMaxTiles; i++) {
+            mbar_init(&a1t[i], 1); mbar_init(&a1f[i], kEpiThreads); mbar_init(&a2t[i], 1);
+            mbar_init(&hdt[i], kEpiThreads); mbar_init(&hdt[kMaxTiles + i], kEpiThreads);
+        }
         fence_mbar_init();
     }
     fence_before();
@@ -407,7 +482,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
         // keeps them on the uniform datapath: no R2UR / waterfall in the inner loops.
         if (elect_one()) {
             int slot = 0;
-            uint32_t phase = 0, xph = 0, hph = 0;   // hph bit i: phase of hd_full[i]
+            uint32_t phase = 0, xph = 0, hph = 0;   // hph bit i: phase of hd_full[i] (STREAM: hdt[i][*])
+            uint32_t a1fph = 0;                      // STREAM: phase of a1f[*]
             const uint32_t xb = smem_u32(xbuf) + (uint32_t)p.G * 16;
             const uint32_t hb = smem_u32(hbuf) + (uint32_t)p.G * 16;
             const uint32_t xlo_b = (uint32_t)(p.Cp / 8) * plane_bytes;   // lo planes (prec3)
@@ -518,6 +594,44 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             }
                         }
                     };
+                    if constexpr (CFG::STREAM) {
+                        // per-tile hand-offs: conv1_0 behind the X rows (previous conv2 epilogue),
+                        // conv1_{j+1} behind epi1_j's acc1 reads, conv2_j behind epi1_j's hidden
+                        // rows; every conv1 tile and the last conv2 chunk's tiles commit per tile
+                        constexpr uint32_t LBO1 = CFG::PAIR ? 16u : (uint32_t)CFG::PLANE16 * 16u;
+                        constexpr uint32_t LBO2 = (uint32_t)CFG::PLANE16 * 16u;
+                        const uint32_t alo1 = ((xb >> 4) & 0x3FFFu) | ((LBO1 >> 4) << 16);
+                        const uint32_t ring1 = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::MC * 16 >> 4) << 16);
+                        const uint32_t ring2 = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::NC2 * 16 >> 4) << 16);
+                        long long tx0 = CLK();
+                        issue_stream<CFG::K1, CFG::PER1, CFG::PAIR, false, CFG::WP, CFG::PLANE16, CFG::G1, CFG::KB1 / 16,
+                                     CFG::T, CFG::MC, CFG::P3, CFG::LOX16, CFG::ACC1, CFG::MC, 1>(
+                            tmem, alo1, ring1, (uint32_t)CFG::SLOT / 16u, id1, 0u, slot, phase, p.nslot, full, empty,
+                            x_tile, xph, a1t);
+                        if (kCycles && a.dbg) w_x += (unsigned long long)(CLK() - tx0);
+                        xph ^= 1;
+                        for (int j = 0; j < p.nch; j++) {
+                            const int hbi = j & (p.nhd - 1);
+                            if (j + 1 < p.nch) {
+                                issue_stream<CFG::K1, CFG::PER1, CFG::PAIR, false, CFG::WP, CFG::PLANE16, CFG::G1,
+                                             CFG::KB1 / 16, CFG::T, CFG::MC, CFG::P3, CFG::LOX16, CFG::ACC1, CFG::MC, 0>(
+                                    tmem, alo1, ring1, (uint32_t)CFG::SLOT / 16u, id1, 0u, slot, phase, p.nslot, full,
+                                    empty, a1f, a1fph, a1t);
+                                a1fph ^= 1;
+                            }
+                            const uint32_t hbj = hb + (uint32_t)(hbi * hbuf_stride);
+                            const uint32_t alo2 = ((hbj >> 4) & 0x3FFFu) | ((LBO2 >> 4) << 16);
+                            long long th0 = CLK();
+                            issue_stream<CFG::K2, CFG::PER2, false, CFG::HST, CFG::WP, CFG::PLANE16, CFG::G2, CFG::KB2 / 16,
+                                         CFG::T, CFG::NC2, CFG::P3, CFG::LOH16, 0, CFG::NC2, 1>(
+                                tmem, alo2, ring2, (uint32_t)CFG::SLOT / 16u, id2, 1u, slot, phase, p.nslot, full,
+                                empty, hdt + hbi * kMaxTiles, (hph >> hbi) & 1u, j + 1 == p.nch ? a2t : nullptr);
+                            if (kCycles && a.dbg) w_hd += (unsigned long long)(CLK() - th0);
+                            hph ^= 1u << hbi;
+                            commit(&hd_empty[hbi]);
+                        }
+                        continue;
+                    }
                     // first conv1 chunk: tile by tile behind the previous epilogue when its weight
                     // slots fit the ring, else after all X rows are final
                     bool tiles_first = false;
@@ -768,8 +882,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                 const float* b2n = bias2_of(tt + 1 < nbv ? tt + 1 : 0);   // next block's conv2 bias
                 for (int j = 0; j < p.nch; j++) {
                     // ---- conv1 epilogue: acc1 -> bias + act -> bf16 hidden planes
-                    TWAIT(w_a1, mbar_wait(acc1_full, a1ph)); a1ph ^= 1;
-                    fence_after();
+                    if constexpr (!CFG::STREAM) {   // STREAM: per-tile waits below
+                        TWAIT(w_a1, mbar_wait(acc1_full, a1ph)); a1ph ^= 1;
+                        fence_after();
+                    }
                     const int hb_i = j & (p.nhd - 1);
                     if ((hd_used >> hb_i) & 1u) {
                         TWAIT(w_he, mbar_wait(&hd_empty[hb_i], (heph >> hb_i) & 1u));
@@ -782,7 +898,49 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                     // bias of the next conv1 chunk in issue order, this half's columns
                     const float* b1n = (j + 1 < p.nch ? b1 + (j + 1) * eMC : bias1_of(tt + 1 < nbv ? tt + 1 : 0)) + cb1;
 #ifndef CI_NO_EPI1_BATCH
-                    if constexpr (S && CFG::MC == 32) {
+                    if constexpr (CFG::STREAM && CFG::EPI1_PIPE) {
+                        // tile pairs, software pipelined: the TMEM loads of pair k+1 are in flight
+                        // while pair k is converted and stored (one wait::ld per pair)
+                        constexpr int T = CFG::T, NP = (CFG::T + 1) / 2;
+                        float v[2][2][16];
+                        auto issue = [&](int q0, float (&vv)[2][16]) {
+                            TWAIT(w_a1, mbar_wait(&a1t[q0 + 1 < T ? q0 + 1 : T - 1], a1ph));
+                            fence_after();
+#pragma unroll
+                            for (int u = 0; u < 2; u++)
+                                if (q0 + u < T)
+                                    tmem_ld16(tmem + lane_addr + acc1_col0 + (uint32_t)((q0 + u) * CFG::MC + cb1), vv[u]);
+                        };
+                        issue(0, v[0]);
+#pragma unroll
+                        for (int k = 0; k < NP; k++) {
+                            const int q0 = 2 * k;
+                            tmem_wait_ld();
+                            if (j + 1 < p.nch) {   // acc1 tiles free for the next conv1 chunk
+                                fence_before();
+                                for (int u = 0; u < 2 && q0 + u < T; u++) mbar_arrive(&a1f[q0 + u]);
+                            }
+                            if (k + 1 < NP) issue(q0 + 2, v[(k + 1) & 1]);
+#pragma unroll
+                            for (int u = 0; u < 2; u++) {
+                                if (q0 + u >= T) break;
+                                const int tile = q0 + u;
+                                int r = tile * 128 + row_in_tile, ii, y, x;
+                                if (rowpix(r, ii, y, x) && ii < nimg) {   // folded bias; pad rows never written
+#pragma unroll
+                                    for (int h = 0; h < 2; h++) {
+                                        float h8[8];
+#pragma unroll
+                                        for (int e = 0; e < 8; e++) h8[e] = fmaxf(v[k & 1][u][h * 8 + e], 0.f);
+                                        store8(hbuf_j, hlo_buf, cb1 / 8 + h, r, h8);
+                                    }
+                                }
+                            }
+                            fence_proxy_async();   // hidden rows of these tiles -> conv2_j
+                            for (int u = 0; u < 2 && q0 + u < T; u++) mbar_arrive(&hdt[hb_i * kMaxTiles + q0 + u]);
+                        }
+                        a1ph ^= 1;
+                    } else if constexpr (S && CFG::MC == 32) {
                         // Batched TMEM reads: up to four LW-column loads in flight per wait::ld
                         // (one load per wait is latency-bound at ~250 cycles), flattened over
                         // (tile, column group); no registers stay live across batches.
@@ -792,6 +950,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
 #pragma unroll
                         for (int q0 = 0; q0 < NL; q0 += LB) {
                             float v[LB][LW];
+                            if constexpr (CFG::STREAM) {   // NG == 1: q = tile
+                                TWAIT(w_a1, mbar_wait(&a1t[q0 + LB - 1 < NL ? q0 + LB - 1 : NL - 1], a1ph));
+                                fence_after();
+                            }
 #pragma unroll
                             for (int u = 0; u < LB; u++) {
                                 if (q0 + u >= NL) break;
@@ -800,6 +962,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 if constexpr (LW == 16) tmem_ld16(ta, v[u]); else tmem_ld8(ta, v[u]);
                             }
                             tmem_wait_ld();
+                            if constexpr (CFG::STREAM) {   // acc1 tiles free for the next conv1 chunk
+                                if (j + 1 < p.nch) {
+                                    fence_before();
+                                    for (int u = 0; u < LB && q0 + u < NL; u++) mbar_arrive(&a1f[q0 + u]);
+                                }
+                            }
 #pragma unroll
                             for (int u = 0; u < LB; u++) {
                                 if (q0 + u >= NL) break;
@@ -838,7 +1006,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 init_acc1_cols(b1n + g * LW, acc1_col0 + (uint32_t)(tile * CFG::MC + cb1 + g * LW), LW);
                                 }
                             }
+                            if constexpr (CFG::STREAM) {   // hidden rows of these tiles -> conv2_j
+                                fence_proxy_async();
+                                for (int u = 0; u < LB && q0 + u < NL; u++) mbar_arrive(&hdt[hb_i * kMaxTiles + q0 + u]);
+                            }
                         }
+                        if constexpr (CFG::STREAM) a1ph ^= 1;
                     } else
 #endif
                     for (int tile = 0; tile < eT; tile++) {
@@ -873,10 +1046,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             if (!efold) init_acc1_cols(b1n + g0, col + (uint32_t)g0, n);
                         }
                     }
-                    tmem_wait_st();
-                    fence_before();
-                    fence_proxy_async();
-                    mbar_arrive(&hd_full[hb_i]);
+                    if constexpr (!CFG::STREAM) {
+                        tmem_wait_st();
+                        fence_before();
+                        fence_proxy_async();
+                        mbar_arrive(&hd_full[hb_i]);
+                    }
                     t_e1 += CLK() - te0;
                 }
                 // ---- conv2 epilogue: s_out (+|-)= acc2 + b2 (fp32); bf16(s_out) -> X
@@ -1025,11 +1200,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                     // out[p][o] = Z_-1[p-1][o] + Z_0[p][o] + Z_+1[p+1][o]  (col2im over v).
                     // Rows are lanes: neighbours come from warp shuffles, warp-boundary rows from
                     // a small shared-memory exchange.  The two warp halves take alternate tiles.
-                    TWAIT(w_a2, mbar_wait(acc2_full, a2ph)); a2ph ^= 1;
-                    fence_after();
+                    if constexpr (!CFG::STREAM) {   // STREAM: per-tile waits below
+                        TWAIT(w_a2, mbar_wait(acc2_full, a2ph)); a2ph ^= 1;
+                        fence_after();
+                    }
                     long long te2h = CLK();
                     {
-                      if constexpr (S) {
+                      if constexpr (CFG::STREAM) {
+                      } else if constexpr (S) {
                         // pass 1, batched: only the Z_-1 (cols 0-7) and Z_+1 (cols 16-23) columns the
                         // exchange needs, all of this half's tiles in flight before one wait
                         constexpr int NK = (CFG::T + 1) / 2;
@@ -1077,7 +1255,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             }
                         }
                       }
-                        asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+                        if constexpr (!CFG::STREAM) asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
                         // pass 2 body for one of this half's tiles (za/zb = its 24 acc2 columns)
                         auto hst_tile = [&](int tile, const float* za, const float* zb) {
                             int r = tile * 128 + row_in_tile, ii, y, x;
@@ -1115,7 +1293,47 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 if (write_x) store8(xbuf, xlo_buf, 0, r, n8);
                             }
                         };
-                        if constexpr (S) {
+                        if constexpr (CFG::STREAM) {
+                            // streamed behind the last conv2 chunk, one tile pair per step: step k
+                            // reads pair k's acc2 (kept in registers) and publishes its boundary rows
+                            // (pass 1); after the barrier it finishes pair k-1 (pass 2), whose
+                            // neighbours' boundary rows are now all published
+                            constexpr int NK = (CFG::T + 1) / 2;
+                            float za[2][16], zb[2][8];
+                            int next_arr = 0;
+#pragma unroll
+                            for (int k = 0; k <= NK; k++) {
+                                if (k < NK) {
+                                    const int tile = 2 * k + half;
+                                    TWAIT(w_a2, mbar_wait(&a2t[2 * k + 1 < CFG::T ? 2 * k + 1 : CFG::T - 1], a2ph));
+                                    fence_after();
+                                    if (tile < CFG::T) {
+                                        const uint32_t col = (uint32_t)(tile * CFG::NC2);
+                                        tmem_ld16(tmem + lane_addr + col, za[k & 1]);
+                                        tmem_ld8(tmem + lane_addr + col + 16, zb[k & 1]);
+                                        tmem_wait_ld();
+                                        init_acc2(b2n, tile);
+                                        float* xq = xchg + ((tile * 4 + quarter) * 2) * 8;
+                                        if (lane == 31) {
+#pragma unroll
+                                            for (int o = 0; o < 8; o++) xq[o] = za[k & 1][o];   // Z_-1, last row
+                                        }
+                                        if (lane == 0) {
+#pragma unroll
+                                            for (int o = 0; o < 8; o++) xq[8 + o] = zb[k & 1][o];   // Z_+1, first row
+                                        }
+                                    }
+                                }
+                                asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+                                if (k >= 1) {
+                                    const int tile = 2 * (k - 1) + half;
+                                    if (tile < CFG::T) hst_tile(tile, za[(k - 1) & 1], zb[(k - 1) & 1]);
+                                    const int last = 2 * k - 1 < CFG::T ? 2 * k - 1 : CFG::T - 1;
+                                    for (; next_arr <= last; next_arr++) x_ready(next_arr);
+                                }
+                            }
+                            a2ph ^= 1;
+                        } else if constexpr (S) {
                             // two of this half's tiles per wait::ld; X-ready arrivals stay in tile order
                             constexpr int NK = (CFG::T + 1) / 2;
                             int next_arr = 0;
