@@ -282,6 +282,39 @@ __device__ __forceinline__ void issue_stream(uint32_t tmem, uint32_t alo0, uint3
     }
 }
 
+// Building blocks of the interleaved STREAM issue: wait a segment's resident weight slots
+// (advancing the ring cursor), and issue every k-step of one M-tile of that segment.
+template <int NS>
+__device__ __forceinline__ void acquire_slots(uint32_t (&bl)[NS], uint32_t ringlo, uint32_t slot16, int& slot,
+                                              uint32_t& phase, int nslot, uint64_t* full) {
+#pragma unroll
+    for (int q = 0; q < NS; q++) {
+        mbar_wait(&full[slot], phase);
+        bl[q] = ringlo + (uint32_t)slot * slot16;
+        if (++slot == nslot) { slot = 0; phase ^= 1; }
+    }
+}
+template <int K, int PER, bool PAIR, bool HSTK, int WP, int PLANE16, int G, int KB16, int N, bool P3, int LOA16,
+          int ACC0, int DSTRIDE, int NS>
+__device__ __forceinline__ void issue_tile(int t, uint32_t tmem, uint32_t alo0, const uint32_t (&bl)[NS],
+                                           uint32_t idesc, uint32_t acc_first) {
+    constexpr uint32_t HI = 0x4008u;
+#pragma unroll
+    for (int s = 0; s < K; s++) {
+        const int shift = PAIR ? (s / 2 - 1) * WP + ((s & 1) ? 1 : -1)
+                               : (HSTK ? (s / PER - 1) * WP : ((s / PER) / 3 - 1) * WP + ((s / PER) % 3 - 1));
+        const int poff16 = PAIR ? 0 : 2 * (s % PER) * PLANE16;
+        const uint64_t ad = ((uint64_t)HI << 32) | (alo0 + (uint32_t)(shift + poff16 + t * 128));
+        const uint64_t bd = ((uint64_t)HI << 32) | (bl[s / G] + (uint32_t)((s % G) * KB16));
+        const uint32_t d = tmem + (uint32_t)(ACC0 + t * DSTRIDE);
+        mma_bf16(d, ad, bd, idesc, s == 0 ? acc_first : 1u);
+        if (P3) {
+            mma_bf16(d, ad, bd + (uint64_t)(N * 2), idesc, 1u);
+            mma_bf16(d, ad + (uint64_t)LOA16, bd, idesc, 1u);
+        }
+    }
+}
+
 // Static stage configuration (0 = use the runtime plan)
 template <int WP_, int CP_, int MC_, int NC2_, int T_, int P3_, int SLOT_, int H_ = 0, int C_ = 0, int SST_ = 0,
           int HST_ = 0, int RES_ = 0>
@@ -319,6 +352,11 @@ struct SCfg {
     static constexpr bool STREAM = false;
 #else
     static constexpr bool STREAM = kStatic && HST && HC == 8 && FOLD && !RES && MC == 32 && K1 <= G1 && K2 <= G2;
+#endif
+#ifdef CI_NO_INTERLEAVE
+    static constexpr bool INTERLEAVE = false;
+#else
+    static constexpr bool INTERLEAVE = true;   // STREAM: conv1_{j+1} / conv2_j issued tile-interleaved
 #endif
 #ifdef CI_NO_EPI1_PIPE
     static constexpr bool EPI1_PIPE = false;
@@ -600,7 +638,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                         // rows; every conv1 tile and the last conv2 chunk's tiles commit per tile
                         constexpr uint32_t LBO1 = CFG::PAIR ? 16u : (uint32_t)CFG::PLANE16 * 16u;
                         constexpr uint32_t LBO2 = (uint32_t)CFG::PLANE16 * 16u;
-                        const uint32_t alo1 = ((xb >> 4) & 0x3FFFu) | ((LBO1 >> 4) << 16);
+                        uint32_t alo1 = ((xb >> 4) & 0x3FFFu) | ((LBO1 >> 4) << 16);
                         const uint32_t ring1 = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::MC * 16 >> 4) << 16);
                         const uint32_t ring2 = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::NC2 * 16 >> 4) << 16);
                         long long tx0 = CLK();
@@ -612,6 +650,49 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                         xph ^= 1;
                         for (int j = 0; j < p.nch; j++) {
                             const int hbi = j & (p.nhd - 1);
+                            if (CFG::INTERLEAVE && j + 1 < p.nch) {
+                                // conv1_{j+1} tile t and conv2_j tile t-1 alternate: both trail epi1_j
+                                // (acc1 reads / hidden rows), so the tensor pipe holds little of
+                                // conv2_j when epi1_j finishes and the conv2 epilogue starts early
+                                constexpr int NS1 = (CFG::K1 + CFG::G1 - 1) / CFG::G1;
+                                constexpr int NS2 = (CFG::K2 + CFG::G2 - 1) / CFG::G2;
+                                const uint32_t hbj = hb + (uint32_t)(hbi * hbuf_stride);
+                                const uint32_t alo2 = ((hbj >> 4) & 0x3FFFu) | ((LBO2 >> 4) << 16);
+                                uint32_t bl1[NS1], bl2[NS2];
+                                int rslot = slot;
+                                asm volatile("" : "+r"(alo1), "+r"(alo2));
+                                acquire_slots<NS1>(bl1, ring1, (uint32_t)CFG::SLOT / 16u, slot, phase, p.nslot, full);
+                                acquire_slots<NS2>(bl2, ring2, (uint32_t)CFG::SLOT / 16u, slot, phase, p.nslot, full);
+                                uint64_t* hdt_j = hdt + hbi * kMaxTiles;
+                                const uint32_t hdph = (hph >> hbi) & 1u;
+#pragma unroll
+                                for (int t = 0; t <= CFG::T; t++) {
+                                    if (t < CFG::T) {
+                                        TWAIT(w_hd, mbar_wait(&a1f[t], a1fph));
+                                        fence_after();
+                                        issue_tile<CFG::K1, CFG::PER1, CFG::PAIR, false, CFG::WP, CFG::PLANE16, CFG::G1,
+                                                   CFG::KB1 / 16, CFG::MC, CFG::P3, CFG::LOX16, CFG::ACC1, CFG::MC, NS1>(
+                                            t, tmem, alo1, bl1, id1, 0u);
+                                        commit(&a1t[t]);
+                                    }
+                                    if (t >= 1) {
+                                        TWAIT(w_hd, mbar_wait(&hdt_j[t < CFG::T ? t : CFG::T - 1], hdph));
+                                        fence_after();
+                                        issue_tile<CFG::K2, CFG::PER2, false, CFG::HST, CFG::WP, CFG::PLANE16, CFG::G2,
+                                                   CFG::KB2 / 16, CFG::NC2, CFG::P3, CFG::LOH16, 0, CFG::NC2, NS2>(
+                                            t - 1, tmem, alo2, bl2, id2, 1u);
+                                    }
+                                }
+#pragma unroll
+                                for (int q = 0; q < NS1 + NS2; q++) {
+                                    commit(&empty[rslot]);
+                                    if (++rslot == p.nslot) rslot = 0;
+                                }
+                                a1fph ^= 1;
+                                hph ^= 1u << hbi;
+                                commit(&hd_empty[hbi]);
+                                continue;
+                            }
                             if (j + 1 < p.nch) {
                                 issue_stream<CFG::K1, CFG::PER1, CFG::PAIR, false, CFG::WP, CFG::PLANE16, CFG::G1,
                                              CFG::KB1 / 16, CFG::T, CFG::MC, CFG::P3, CFG::LOX16, CFG::ACC1, CFG::MC, 0>(
