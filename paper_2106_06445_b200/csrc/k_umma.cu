@@ -344,24 +344,25 @@ struct SCfg {
     static constexpr int LOX16 = (CP / 8) * PLANE16;
     static constexpr int LOH16 = (MC / 8) * PLANE16;
     // Tile-streamed block schedule: every segment's weights fit one ring slot,
-    // 8-channel hst conv2, folded conv1 bias, 2-tile batched conv1 epilogue.  Hand-offs between
+    // 8-channel hst conv2, folded conv1 bias, tile-pair conv1 epilogue.  Hand-offs between
     // the MMA thread and the epilogue are per M-tile instead of per segment, so conv1 of chunk
     // j+1 runs behind the conv1 epilogue of chunk j and the conv2 epilogue runs behind the last
     // conv2 chunk.  -DCI_NO_STREAM keeps the per-segment schedule (same-box A/B).
+#ifdef CI_NO_EPI1_PIPE
+    static constexpr bool EPI1_PIPE = false;
+#else
+    static constexpr bool EPI1_PIPE = true;   // STREAM conv1 epilogue: relu only (act 0)
+#endif
 #if defined(CI_NO_STREAM) || defined(CI_NO_EPI1_BATCH)
     static constexpr bool STREAM = false;
 #else
-    static constexpr bool STREAM = kStatic && HST && HC == 8 && FOLD && !RES && MC == 32 && K1 <= G1 && K2 <= G2;
+    static constexpr bool STREAM = kStatic && HST && HC == 8 && FOLD && !RES &&
+                                  (MC == 32 || (MC == 16 && EPI1_PIPE)) && K1 <= G1 && K2 <= G2;
 #endif
 #ifdef CI_NO_INTERLEAVE
     static constexpr bool INTERLEAVE = false;
 #else
     static constexpr bool INTERLEAVE = true;   // STREAM: conv1_{j+1} / conv2_j issued tile-interleaved
-#endif
-#ifdef CI_NO_EPI1_PIPE
-    static constexpr bool EPI1_PIPE = false;
-#else
-    static constexpr bool EPI1_PIPE = true;   // STREAM conv1 epilogue: relu only (act 0)
 #endif
 };
 using SDyn = SCfg<0, 0, 0, 0, 0, 0, 0>;
@@ -982,15 +983,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                     if constexpr (CFG::STREAM && CFG::EPI1_PIPE) {
                         // tile pairs, software pipelined: the TMEM loads of pair k+1 are in flight
                         // while pair k is converted and stored (one wait::ld per pair)
-                        constexpr int T = CFG::T, NP = (CFG::T + 1) / 2;
-                        float v[2][2][16];
-                        auto issue = [&](int q0, float (&vv)[2][16]) {
+                        constexpr int T = CFG::T, NP = (CFG::T + 1) / 2, CW1 = CFG::MC / 2;   // 16 or 8 columns
+                        float v[2][2][CW1];
+                        auto issue = [&](int q0, float (&vv)[2][CW1]) {
                             TWAIT(w_a1, mbar_wait(&a1t[q0 + 1 < T ? q0 + 1 : T - 1], a1ph));
                             fence_after();
 #pragma unroll
                             for (int u = 0; u < 2; u++)
-                                if (q0 + u < T)
-                                    tmem_ld16(tmem + lane_addr + acc1_col0 + (uint32_t)((q0 + u) * CFG::MC + cb1), vv[u]);
+                                if (q0 + u < T) {
+                                    const uint32_t ta = tmem + lane_addr + acc1_col0 + (uint32_t)((q0 + u) * CFG::MC + cb1);
+                                    if constexpr (CW1 == 16) tmem_ld16(ta, vv[u]); else tmem_ld8(ta, vv[u]);
+                                }
                         };
                         issue(0, v[0]);
 #pragma unroll
@@ -1009,7 +1012,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 int r = tile * 128 + row_in_tile, ii, y, x;
                                 if (rowpix(r, ii, y, x) && ii < nimg) {   // folded bias; pad rows never written
 #pragma unroll
-                                    for (int h = 0; h < 2; h++) {
+                                    for (int h = 0; h < CW1 / 8; h++) {
                                         float h8[8];
 #pragma unroll
                                         for (int e = 0; e < 8; e++) h8[e] = fmaxf(v[k & 1][u][h * 8 + e], 0.f);
