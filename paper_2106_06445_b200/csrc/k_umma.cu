@@ -830,6 +830,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                 *reinterpret_cast<uint4*>(base_lo + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
             }
         };
+        // hst warp-boundary exchange: 8 floats as two 16-B shared accesses (the buffer is 16-B
+        // aligned per entry); reads are warp-uniform broadcasts, the boundary lane then selects
+        auto xst8 = [&](float* dst, const float* v) {
+            reinterpret_cast<float4*>(dst)[0] = make_float4(v[0], v[1], v[2], v[3]);
+            reinterpret_cast<float4*>(dst)[1] = make_float4(v[4], v[5], v[6], v[7]);
+        };
+        auto xsel8 = [&](float* out, bool take, bool have, const float* src) {
+            float4 a4 = make_float4(0.f, 0.f, 0.f, 0.f), b4 = a4;
+            if (have) { a4 = reinterpret_cast<const float4*>(src)[0]; b4 = reinterpret_cast<const float4*>(src)[1]; }
+            const float w[8] = {a4.x, a4.y, a4.z, a4.w, b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+            for (int o = 0; o < 8; o++) out[o] = take ? w[o] : out[o];
+        };
         // L2 prefetch of a batch's fp32 state (contiguous images) when it stays in global memory
         auto prefetch_batch = [&](int64_t bb) {
             if (bb >= nbatch) return;
@@ -1176,11 +1189,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             tmem_wait_ld();
                             if (lane == 31) {
 #pragma unroll
-                                for (int o = 0; o < HCW; o++) xq[o] = zl[o];          // Z_-1, last row
+                                for (int g = 0; g < HCW / 8; g++) xst8(xq + g * 8, zl + g * 8);   // Z_-1, last row
                             }
                             if (lane == 0) {
 #pragma unroll
-                                for (int o = 0; o < HCW; o++) xq[ehc + o] = zr[o];    // Z_+1, first row
+                                for (int g = 0; g < HCW / 8; g++) xst8(xq + ehc + g * 8, zr + g * 8);   // Z_+1, first row
                             }
                         } else {
                             for (int g = 0; g < ehc / 8; g++) {
@@ -1216,6 +1229,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                     left[o] = __shfl_up_sync(0xffffffffu, zl[o], 1);
                                     right[o] = __shfl_down_sync(0xffffffffu, zr[o], 1);
                                 }
+                                if constexpr (S) {
+                                    xsel8(left, lane == 0, tqL >= 0, xchg + ((tqL * 4 + qqL) * 2) * ehc + g * 8);
+                                    xsel8(right, lane == 31, tqR < eT, xchg + ((tqR * 4 + qqR) * 2 + 1) * ehc + g * 8);
+                                } else {
                                 if (lane == 0) {
 #pragma unroll
                                     for (int o = 0; o < 8; o++)
@@ -1225,6 +1242,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
 #pragma unroll
                                     for (int o = 0; o < 8; o++)
                                         right[o] = tqR < eT ? xchg[((tqR * 4 + qqR) * 2 + 1) * ehc + g * 8 + o] : 0.f;
+                                }
                                 }
                                 if (valid) {
                                     float n8[8];
@@ -1312,12 +1330,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             if (tile < eT) {
                                 float* xq = xchg + ((tile * 4 + quarter) * 2) * 8;
                                 if (lane == 31) {
-#pragma unroll
-                                    for (int o = 0; o < 8; o++) xq[o] = zl[k][o];
+                                    xst8(xq, zl[k]);
                                 }
                                 if (lane == 0) {
-#pragma unroll
-                                    for (int o = 0; o < 8; o++) xq[8 + o] = zr[k][o];
+                                    xst8(xq + 8, zr[k]);
                                 }
                             }
                         }
@@ -1350,6 +1366,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 left[o] = __shfl_up_sync(0xffffffffu, za[o], 1);
                                 right[o] = __shfl_down_sync(0xffffffffu, zb[o], 1);
                             }
+                            if constexpr (S) {
+                                const int tqL = quarter > 0 ? tile : tile - 1, qqL = quarter > 0 ? quarter - 1 : 3;
+                                const int tqR = quarter < 3 ? tile : tile + 1, qqR = quarter < 3 ? quarter + 1 : 0;
+                                xsel8(left, lane == 0, tqL >= 0, xchg + ((tqL * 4 + qqL) * 2) * 8);
+                                xsel8(right, lane == 31, tqR < eT, xchg + ((tqR * 4 + qqR) * 2 + 1) * 8);
+                            } else {
                             if (lane == 0) {
                                 const int tq = quarter > 0 ? tile : tile - 1, qq = quarter > 0 ? quarter - 1 : 3;
 #pragma unroll
@@ -1359,6 +1381,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 const int tq = quarter < 3 ? tile : tile + 1, qq = quarter < 3 ? quarter + 1 : 0;
 #pragma unroll
                                 for (int o = 0; o < 8; o++) right[o] = tq < eT ? xchg[((tq * 4 + qq) * 2 + 1) * 8 + o] : 0.f;
+                            }
                             }
                             if (valid) {
                                 float* dst = stb + ((int64_t)ii * a.C + out_off) * eHW + y * eW + x;
@@ -1399,12 +1422,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                         init_acc2(b2n, tile);
                                         float* xq = xchg + ((tile * 4 + quarter) * 2) * 8;
                                         if (lane == 31) {
-#pragma unroll
-                                            for (int o = 0; o < 8; o++) xq[o] = za[k & 1][o];   // Z_-1, last row
+                                            xst8(xq, za[k & 1]);   // Z_-1, last row
                                         }
                                         if (lane == 0) {
-#pragma unroll
-                                            for (int o = 0; o < 8; o++) xq[8 + o] = zb[k & 1][o];   // Z_+1, first row
+                                            xst8(xq + 8, zb[k & 1]);   // Z_+1, first row
                                         }
                                     }
                                 }
