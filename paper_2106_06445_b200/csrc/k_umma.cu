@@ -367,7 +367,7 @@ struct SCfg {
 };
 using SDyn = SCfg<0, 0, 0, 0, 0, 0, 0>;
 constexpr int kMaxTiles = 8;                     // T <= 8 (512 TMEM columns / >= 64 per tile)
-constexpr int kBarBytes = 640;                   // mbarriers, TMEM slot and batch queue
+constexpr int kBarBytes = 1024;                  // mbarriers, TMEM slot, batch queue, staged conv2 bias
 
 // Cycle instrumentation (CI_DEBUG_CYCLES; inactive unless requested).  -DCI_NO_CYCLES
 // compiles it out; same-box A/B showed no gain from that (s2 got slower), so it stays in.
@@ -421,6 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
     uint64_t* a1f = x_full + 36;       // [kMaxTiles] acc1 tile t read by the conv1 epilogue (all threads)
     uint64_t* hdt = x_full + 44;       // [2][kMaxTiles] hidden rows of tile t written (all threads)
     uint64_t* a2t = x_full + 60;       // [kMaxTiles] last conv2 chunk of tile t done (tcgen05.commit)
+    float* sbias2 = reinterpret_cast<float*>(x_full + 68);   // [96] next block's conv2 bias (wide hst)
 
     // ---- zero the activation buffers (pads and guards must read as 0)
     {
@@ -1168,6 +1169,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                     // a warp's 32 rows, a shared-memory exchange for the warp-boundary rows (pass 1),
                     // alternate tiles per warp half, 8-channel groups.
                     constexpr int HCW = S ? (CFG::HC > 0 ? CFG::HC : 8) : 24;   // register arrays
+                    // stage the next block's conv2 bias in shared memory (read after the barrier
+                    // below; the previous block's readers finished before its closing barrier)
+                    if (S && et < ec) sbias2[et] = __ldg(b2n + et);
                     TWAIT(w_a2, mbar_wait(acc2_full, a2ph)); a2ph ^= 1;
                     fence_after();
                     long long te2w = CLK();
@@ -1277,7 +1281,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                     for (int e = 0; e < 8; e++) zr[g * 8 + e] = t8[e];
                                 }
                                 tmem_wait_ld();
-                                init_acc2(b2n, tile);
+                                {   // acc2 <- next block's bias (columns [hc, 2hc)), from shared memory
+                                    const uint32_t base = tmem + lane_addr + col;
+#pragma unroll
+                                    for (int g = 0; g < 3 * HCW / 8; g++) {
+                                        float v8[8];
+#pragma unroll
+                                        for (int e = 0; e < 8; e++) {
+                                            const int c8 = g * 8 + e;
+                                            v8[e] = (c8 >= HCW && c8 < 2 * HCW && c8 - HCW < CFG::C) ? sbias2[c8 - HCW] : 0.f;
+                                        }
+                                        tmem_st8(base + (uint32_t)(g * 8), v8);
+                                    }
+                                }
 #pragma unroll
                                 for (int g = 0; g < HCW / 8; g++) group(g, zl + g * 8, zc + g * 8, zr + g * 8);
                             } else {             // generic kernel: one group at a time (registers)
@@ -1408,6 +1424,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             constexpr int NK = (CFG::T + 1) / 2;
                             float za[2][16], zb[2][8];
                             int next_arr = 0;
+                            // next block's conv2 bias: centre-tap columns 8..15, loaded once per block
+                            float zb16[16], z8[8];
+#pragma unroll
+                            for (int e = 0; e < 8; e++) {
+                                zb16[e] = 0.f;
+                                zb16[8 + e] = e < CFG::C ? __ldg(b2n + e) : 0.f;
+                                z8[e] = 0.f;
+                            }
 #pragma unroll
                             for (int k = 0; k <= NK; k++) {
                                 if (k < NK) {
@@ -1419,7 +1443,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                         tmem_ld16(tmem + lane_addr + col, za[k & 1]);
                                         tmem_ld8(tmem + lane_addr + col + 16, zb[k & 1]);
                                         tmem_wait_ld();
-                                        init_acc2(b2n, tile);
+                                        tmem_st16(tmem + lane_addr + col, zb16);
+                                        tmem_st8(tmem + lane_addr + col + 16, z8);
                                         float* xq = xchg + ((tile * 4 + quarter) * 2) * 8;
                                         if (lane == 31) {
                                             xst8(xq, za[k & 1]);   // Z_-1, last row
