@@ -938,6 +938,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
             long long tl0 = CLK();
             const int64_t img0 = b * p.I;
             const int nimg = (int)(a.n - img0 < (int64_t)p.I ? a.n - img0 : (int64_t)p.I);
+            // bit t: this thread's pixel row of tile t is a real pixel of a present image
+            uint32_t vmask = 0;
+            for (int tile = 0; tile < eT; tile++) {
+                int ii, y, x;
+                if (rowpix(tile * 128 + row_in_tile, ii, y, x) && ii < nimg) vmask |= 1u << tile;
+            }
             if (!esst) prefetch_batch(bnext);
             // ---- (esst) copy the batch's fp32 state into shared memory
             if (esst) {
@@ -1023,14 +1029,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             for (int u = 0; u < 2; u++) {
                                 if (q0 + u >= T) break;
                                 const int tile = q0 + u;
-                                int r = tile * 128 + row_in_tile, ii, y, x;
-                                if (rowpix(r, ii, y, x) && ii < nimg) {   // folded bias; pad rows never written
+                                const int r = tile * 128 + row_in_tile;
+                                if ((vmask >> tile) & 1u) {   // folded bias; pad rows never written
 #pragma unroll
                                     for (int h = 0; h < CW1 / 8; h++) {
-                                        float h8[8];
+                                        const float* hv = &v[k & 1][u][h * 8];
+                                        if constexpr (!CFG::P3) {   // ReLU fused into the bf16 rounding
+                                            uint32_t w[4];
 #pragma unroll
-                                        for (int e = 0; e < 8; e++) h8[e] = fmaxf(v[k & 1][u][h * 8 + e], 0.f);
-                                        store8(hbuf_j, hlo_buf, cb1 / 8 + h, r, h8);
+                                            for (int e = 0; e < 4; e++)
+                                                asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(w[e]) : "f"(hv[2 * e + 1]), "f"(hv[2 * e]));
+                                            *reinterpret_cast<uint4*>(hbuf_j + (size_t)(cb1 / 8 + h) * plane_bytes + (size_t)(r + eG) * 16) =
+                                                make_uint4(w[0], w[1], w[2], w[3]);
+                                        } else {
+                                            float h8[8];
+#pragma unroll
+                                            for (int e = 0; e < 8; e++) h8[e] = fmaxf(hv[e], 0.f);
+                                            store8(hbuf_j, hlo_buf, cb1 / 8 + h, r, h8);
+                                        }
                                     }
                                 }
                             }
