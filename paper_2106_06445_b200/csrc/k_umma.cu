@@ -939,10 +939,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
             const int64_t img0 = b * p.I;
             const int nimg = (int)(a.n - img0 < (int64_t)p.I ? a.n - img0 : (int64_t)p.I);
             // bit t: this thread's pixel row of tile t is a real pixel of a present image
+            // (static configurations) pown[k]: state offset ii*C*HW + y*W + x of this thread's row in
+            // tile 2k + half (the tiles its warp half owns in the alternating conv2 epilogues)
             uint32_t vmask = 0;
-            for (int tile = 0; tile < eT; tile++) {
+            constexpr bool kPown = S && CFG::HST && CFG::HC == 8;
+            int pown[kPown ? (CFG::T + 1) / 2 : 1];
+#pragma unroll
+            for (int tile = 0; tile < (S ? CFG::T : eT); tile++) {
                 int ii, y, x;
-                if (rowpix(tile * 128 + row_in_tile, ii, y, x) && ii < nimg) vmask |= 1u << tile;
+                const bool v = rowpix(tile * 128 + row_in_tile, ii, y, x) && ii < nimg;
+                if (v) vmask |= 1u << tile;
+                if constexpr (kPown) {
+                    const int off = v ? ii * a.C * (int)eHW + y * eW + x : 0;
+                    if ((tile & 1) == 0) pown[tile / 2] = half ? pown[tile / 2] : off;
+                    else pown[tile / 2] = half ? off : pown[tile / 2];
+                }
             }
             if (!esst) prefetch_batch(bnext);
             // ---- (esst) copy the batch's fp32 state into shared memory
@@ -1389,9 +1400,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                       }
                         if constexpr (!CFG::STREAM) asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
                         // pass 2 body for one of this half's tiles (za/zb = its 24 acc2 columns)
-                        auto hst_tile = [&](int tile, const float* za, const float* zb) {
-                            int r = tile * 128 + row_in_tile, ii, y, x;
-                            const bool valid = rowpix(r, ii, y, x) && ii < nimg;
+                        auto hst_tile = [&](int tile, const float* za, const float* zb, int pk) {
+                            int r = tile * 128 + row_in_tile, ii = 0, y = 0, x = 0;
+                            bool valid;
+                            if constexpr (kPown) valid = (vmask >> tile) & 1u;
+                            else valid = rowpix(r, ii, y, x) && ii < nimg;
                             float left[8], right[8];
 #pragma unroll
                             for (int o = 0; o < 8; o++) {
@@ -1416,7 +1429,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             }
                             }
                             if (valid) {
-                                float* dst = stb + ((int64_t)ii * a.C + out_off) * eHW + y * eW + x;
+                                float* dst;
+                                if constexpr (kPown) dst = stb + pk + out_off * (int)eHW;
+                                else dst = stb + ((int64_t)ii * a.C + out_off) * eHW + y * eW + x;
                                 float n8[8];
 #pragma unroll
                                 for (int o = 0; o < 8; o++) {
@@ -1473,9 +1488,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
                                 if (k >= 1) {
                                     const int tile = 2 * (k - 1) + half;
-                                    if (tile < CFG::T) hst_tile(tile, za[(k - 1) & 1], zb[(k - 1) & 1]);
+                                    if (tile < CFG::T) hst_tile(tile, za[(k - 1) & 1], zb[(k - 1) & 1], pown[kPown ? k - 1 : 0]);
                                     const int last = 2 * k - 1 < CFG::T ? 2 * k - 1 : CFG::T - 1;
-                                    for (; next_arr <= last; next_arr++) x_ready(next_arr);
+                                    if (write_x && next_arr <= last) {   // one fence pair for the step's tiles
+                                        fence_before();
+                                        fence_proxy_async();
+                                        for (; next_arr <= last; next_arr++) mbar_arrive(&x_tile[next_arr]);
+                                    }
                                 }
                             }
                             a2ph ^= 1;
@@ -1501,7 +1520,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                     const int tile = 2 * (k0 + u) + half;
                                     if (k0 + u < NK && tile < eT) {
                                         init_acc2(b2n, tile);
-                                        hst_tile(tile, za[u], zb[u]);
+                                        hst_tile(tile, za[u], zb[u], pown[kPown ? k0 + u : 0]);
                                         for (; next_arr <= tile; next_arr++) x_ready(next_arr);
                                     }
                                 }
@@ -1516,7 +1535,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                     tmem_ld8(tmem + lane_addr + col + 16, zb);
                                     tmem_wait_ld();
                                     init_acc2(b2n, tile);
-                                    hst_tile(tile, za, zb);
+                                    hst_tile(tile, za, zb, 0);
                                 }
                                 x_ready(tile);
                             }
