@@ -1041,18 +1041,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 if (q0 + u >= T) break;
                                 const int tile = q0 + u;
                                 const int r = tile * 128 + row_in_tile;
-                                if ((vmask >> tile) & 1u) {   // folded bias; pad rows never written
+                                const bool rv = (vmask >> tile) & 1u;
+                                if constexpr (!CFG::P3) {
+                                    // ReLU fused into the bf16 rounding; pad rows are written as zeros
+                                    // (branch-free: every lane stores its row)
 #pragma unroll
                                     for (int h = 0; h < CW1 / 8; h++) {
                                         const float* hv = &v[k & 1][u][h * 8];
-                                        if constexpr (!CFG::P3) {   // ReLU fused into the bf16 rounding
-                                            uint32_t w[4];
+                                        uint32_t w[4];
 #pragma unroll
-                                            for (int e = 0; e < 4; e++)
-                                                asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(w[e]) : "f"(hv[2 * e + 1]), "f"(hv[2 * e]));
-                                            *reinterpret_cast<uint4*>(hbuf_j + (size_t)(cb1 / 8 + h) * plane_bytes + (size_t)(r + eG) * 16) =
-                                                make_uint4(w[0], w[1], w[2], w[3]);
-                                        } else {
+                                        for (int e = 0; e < 4; e++) {
+                                            asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(w[e]) : "f"(hv[2 * e + 1]), "f"(hv[2 * e]));
+                                            w[e] = rv ? w[e] : 0u;
+                                        }
+                                        *reinterpret_cast<uint4*>(hbuf_j + (size_t)(cb1 / 8 + h) * plane_bytes + (size_t)(r + eG) * 16) =
+                                            make_uint4(w[0], w[1], w[2], w[3]);
+                                    }
+                                } else if (rv) {   // folded bias; pad rows never written
+#pragma unroll
+                                    for (int h = 0; h < CW1 / 8; h++) {
+                                        const float* hv = &v[k & 1][u][h * 8];
+                                        {
                                             float h8[8];
 #pragma unroll
                                             for (int e = 0; e < 8; e++) h8[e] = fmaxf(hv[e], 0.f);
@@ -1097,9 +1106,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             for (int u = 0; u < LB; u++) {
                                 if (q0 + u >= NL) break;
                                 const int q = q0 + u, tile = q / NG, g = q % NG;
-                                int r = tile * 128 + row_in_tile, ii, y, x;
-                                const bool valid = rowpix(r, ii, y, x) && ii < nimg;
-                                if (CFG::FOLD) {
+                                int r = tile * 128 + row_in_tile;
+                                const bool valid = (vmask >> tile) & 1u;
+                                if (CFG::FOLD && !CFG::P3 && !kRes) {
+                                    // ReLU (the only coupling-spec activation) fused into the bf16
+                                    // rounding; pad rows written as zeros, branch-free
+#pragma unroll
+                                    for (int h = 0; h < LW / 8; h++) {
+                                        uint32_t w[4];
+#pragma unroll
+                                        for (int e = 0; e < 4; e++) {
+                                            asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;"
+                                                : "=r"(w[e]) : "f"(v[u][h * 8 + 2 * e + 1]), "f"(v[u][h * 8 + 2 * e]));
+                                            w[e] = valid ? w[e] : 0u;
+                                        }
+                                        *reinterpret_cast<uint4*>(hbuf_j + (size_t)((cb1 + g * LW) / 8 + h) * plane_bytes +
+                                                                  (size_t)(r + eG) * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+                                    }
+                                } else if (CFG::FOLD) {
                                     // bias already in the accumulator; pad / absent-image rows are
                                     // never written (zero since kernel start, fenced by pad bands)
                                     if (valid) {
@@ -1964,7 +1988,7 @@ static StageKernel pick_kernel(const StagePlan& p, const StageArgs& a) {
             if (e.Wp == p.Wp && e.Cp == p.Cp && e.MC == p.MC && e.Nc2 == p.Nc2 && e.T == p.T && e.p3 == p.prec3 &&
                 e.slot == p.slot_bytes && e.H == p.H && e.c == p.c && e.sst == p.sstate && e.hst == p.hst &&
                 e.fold == p.fold && e.split == p.split &&   // packing and epilogue must agree
-                e.res == (a.residual ? 1 : 0) && (a.act != 1 || e.res))
+                e.res == (a.residual ? 1 : 0) && (e.res || a.act == 0))   // coupling specs: ReLU only
                 return e.fn;
     return k_stage<SDyn>;
 }
