@@ -133,6 +133,23 @@ __device__ __forceinline__ bool row_pixel(int r, const StagePlan& p, int& ii, in
 }
 
 // ----------------------------------------------------------------------------------------
+// conv1 pair mode (<= 8 input channels, one 16-B row per pixel): 9 taps x 8 channels = 72 K
+// in 5 K=16 k-steps.  A k-step's two 8-channel K halves are two core matrices LBO bytes apart:
+//   s = 0, 1, 2 : kernel row u = s-1, taps (u, -1) | (u, 0)           LBO = 16 B (next pixel)
+//   s = 3       : kernel column v = +1, taps (-1, +1) | (0, +1)       LBO = Wp * 16 B (next row)
+//   s = 4       : tap (+1, +1) | (+1, +2) (zero weights; reads finite in-buffer rows)  LBO = 16 B
+// pair_shift = start row offset; pair_lbo_add = what moves the descriptor's LBO field
+// (bits 16-29, in 16-B units) from 1 to Wp.  pack_block packs B in the same order.
+// ----------------------------------------------------------------------------------------
+__host__ __device__ constexpr int pair_shift(int s, int wp) {
+    return s < 3 ? (s - 1) * wp - 1 : (s == 3 ? -wp + 1 : wp + 1);
+}
+__host__ __device__ constexpr uint32_t pair_lbo_add(int s, int wp) {
+    return s == 3 ? (uint32_t)(wp - 1) << 16 : 0u;
+}
+constexpr int kPairK1 = 5;
+
+// ----------------------------------------------------------------------------------------
 // Compile-time specialised MMA issue for one conv segment (conv1 chunk or conv2 chunk).
 // Every k-step's A/B descriptor offsets, accumulate flags and ring-slot boundaries are
 // constants, so each MMA costs one uniform add + UTCHMMA in the issuing thread.
@@ -158,10 +175,10 @@ __device__ __forceinline__ void issue_static(uint32_t tmem, uint32_t alo0, uint3
         }
         constexpr int dummy = 0;
         (void)dummy;
-        const int shift = PAIR ? (s / 2 - 1) * WP + ((s & 1) ? 1 : -1)
+        const int shift = PAIR ? pair_shift(s, WP)
                                : (HSTK ? (s / PER - 1) * WP : ((s / PER) / 3 - 1) * WP + ((s / PER) % 3 - 1));
         const int poff16 = PAIR ? 0 : 2 * (s % PER) * PLANE16;
-        const uint32_t al = alo0 + (uint32_t)(shift + poff16);
+        const uint32_t al = alo0 + (uint32_t)(shift + poff16) + (PAIR ? pair_lbo_add(s, WP) : 0u);
         const uint32_t b = bl + (uint32_t)((s % G) * KB16);
 #pragma unroll
         for (int t = 0; t < T; t++) {
@@ -211,10 +228,10 @@ __device__ __forceinline__ void issue_static_tiles(uint32_t tmem, uint32_t alo0,
         fence_after();
 #pragma unroll
         for (int s = 0; s < K; s++) {
-            const int shift = PAIR ? (s / 2 - 1) * WP + ((s & 1) ? 1 : -1)
+            const int shift = PAIR ? pair_shift(s, WP)
                                    : ((s / PER) / 3 - 1) * WP + ((s / PER) % 3 - 1);
             const int poff16 = PAIR ? 0 : 2 * (s % PER) * PLANE16;
-            const uint64_t ad = ((uint64_t)HI << 32) | (alo0 + (uint32_t)(shift + poff16 + t * 128));
+            const uint64_t ad = ((uint64_t)HI << 32) | (alo0 + (uint32_t)(shift + poff16 + t * 128) + (PAIR ? pair_lbo_add(s, WP) : 0u));
             const uint64_t bd = ((uint64_t)HI << 32) | (bl[s / G] + (uint32_t)((s % G) * KB16));
             const uint32_t d = tmem + (uint32_t)(ACC0 + t * DSTRIDE);
             mma_bf16(d, ad, bd, idesc, s == 0 ? acc_first : 1u);
@@ -261,10 +278,10 @@ __device__ __forceinline__ void issue_stream(uint32_t tmem, uint32_t alo0, uint3
         fence_after();
 #pragma unroll
         for (int s = 0; s < K; s++) {
-            const int shift = PAIR ? (s / 2 - 1) * WP + ((s & 1) ? 1 : -1)
+            const int shift = PAIR ? pair_shift(s, WP)
                                    : (HSTK ? (s / PER - 1) * WP : ((s / PER) / 3 - 1) * WP + ((s / PER) % 3 - 1));
             const int poff16 = PAIR ? 0 : 2 * (s % PER) * PLANE16;
-            const uint64_t ad = ((uint64_t)HI << 32) | (alo0 + (uint32_t)(shift + poff16 + t * 128));
+            const uint64_t ad = ((uint64_t)HI << 32) | (alo0 + (uint32_t)(shift + poff16 + t * 128) + (PAIR ? pair_lbo_add(s, WP) : 0u));
             const uint64_t bd = ((uint64_t)HI << 32) | (bl[s / G] + (uint32_t)((s % G) * KB16));
             const uint32_t d = tmem + (uint32_t)(ACC0 + t * DSTRIDE);
             mma_bf16(d, ad, bd, idesc, s == 0 ? acc_first : 1u);
@@ -301,10 +318,10 @@ __device__ __forceinline__ void issue_tile(int t, uint32_t tmem, uint32_t alo0, 
     constexpr uint32_t HI = 0x4008u;
 #pragma unroll
     for (int s = 0; s < K; s++) {
-        const int shift = PAIR ? (s / 2 - 1) * WP + ((s & 1) ? 1 : -1)
+        const int shift = PAIR ? pair_shift(s, WP)
                                : (HSTK ? (s / PER - 1) * WP : ((s / PER) / 3 - 1) * WP + ((s / PER) % 3 - 1));
         const int poff16 = PAIR ? 0 : 2 * (s % PER) * PLANE16;
-        const uint64_t ad = ((uint64_t)HI << 32) | (alo0 + (uint32_t)(shift + poff16 + t * 128));
+        const uint64_t ad = ((uint64_t)HI << 32) | (alo0 + (uint32_t)(shift + poff16 + t * 128) + (PAIR ? pair_lbo_add(s, WP) : 0u));
         const uint64_t bd = ((uint64_t)HI << 32) | (bl[s / G] + (uint32_t)((s % G) * KB16));
         const uint32_t d = tmem + (uint32_t)(ACC0 + t * DSTRIDE);
         mma_bf16(d, ad, bd, idesc, s == 0 ? acc_first : 1u);
@@ -334,7 +351,7 @@ struct SCfg {
     static constexpr bool SPLIT = !HST && C_ % 8 == 0 && C_ / 2 < NC2_ / 2 &&
                                   (NC2_ / 2 == 8 || NC2_ / 2 == 16 || NC2_ / 2 == 32 || NC2_ / 2 == 48);
     static constexpr int PER1 = PAIR ? 2 : CP / 16;
-    static constexpr int K1 = PAIR ? 6 : 9 * (CP / 16);
+    static constexpr int K1 = PAIR ? kPairK1 : 9 * (CP / 16);
     static constexpr int PER2 = MC / 16;
     static constexpr int K2 = (HST ? 3 : 9) * (MC / 16);
     static constexpr int KB1 = MC * 32 * (P3 ? 2 : 1), KB2 = NC2 * 32 * (P3 ? 2 : 1);
@@ -561,10 +578,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                     fence_after();
                                 }
                                 int shift;
-                                uint32_t poff;
-                                if (p.pair) {           // tap = kernel row u+1; kc = 0: v0=-1, 1: v0=+1
-                                    shift = (tap - 1) * p.Wp + (kc ? 1 : -1);
+                                uint32_t poff, lbo = lbo1;
+                                if (p.pair) {           // see pair_shift
+                                    shift = pair_shift(s, p.Wp);
                                     poff = 0;
+                                    if (s == 3) lbo = (uint32_t)p.Wp * 16u;
                                 } else {
                                     shift = (tap / 3 - 1) * p.Wp + (tap % 3 - 1);
                                     poff = (uint32_t)(2 * kc) * plane_bytes;
@@ -575,11 +593,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 for (int tile = 0; tile < p.T; tile++) {
                                     const uint32_t d = tmem + acc1_col0 + (uint32_t)(tile * p.MC);
                                     const uint32_t at = aaddr + (uint32_t)tile * 2048u;
-                                    mma_bf16(d, smem_desc(at, lbo1, 128), smem_desc(baddr, (uint32_t)p.MC * 16u, 128), id1, acc);
+                                    mma_bf16(d, smem_desc(at, lbo, 128), smem_desc(baddr, (uint32_t)p.MC * 16u, 128), id1, acc);
                                     if (p.prec3) {
-                                        mma_bf16(d, smem_desc(at, lbo1, 128),
+                                        mma_bf16(d, smem_desc(at, lbo, 128),
                                                  smem_desc(baddr + (uint32_t)p.MC * 32u, (uint32_t)p.MC * 16u, 128), id1, 1);
-                                        mma_bf16(d, smem_desc(at + xlo_b, lbo1, 128),
+                                        mma_bf16(d, smem_desc(at + xlo_b, lbo, 128),
                                                  smem_desc(baddr, (uint32_t)p.MC * 16u, 128), id1, 1);
                                     }
                                 }
@@ -1787,7 +1805,7 @@ static bool make_plan(const StageInfo& S, bool prec3, StagePlan& best) {
     const int P = prec3 ? 2 : 1;
     const double P3f = prec3 ? 3.0 : 1.0;
     const int img_rows = (p.H + 1) * p.Wp;
-    const int k1 = p.pair ? 6 : 9 * (p.Cp / 16);
+    const int k1 = p.pair ? kPairK1 : 9 * (p.Cp / 16);
     double best_cost = 1e300;
     // conv2 with horizontal tap stacking (mandatory for c <= 8, optional up to c = 24) or plain
     for (int hopt = 1; hopt >= 0; hopt--) {
@@ -1903,9 +1921,12 @@ static void pack_block(const StagePlan& p, const float* W1, const float* b1, con
                 int h = j * p.MC + n;
                 for (int kk = 0; kk < 16; kk++) {
                     float v;
-                    if (p.pair) {
-                        int u = s / 2 - 1, v0 = (s & 1) ? 1 : -1;
-                        int vv = v0 + kk / 8, ci = kk % 8;
+                    if (p.pair) {   // k-step order of pair_shift / pair_lbo_add
+                        const int ci = kk % 8, half = kk / 8;
+                        int u, vv;
+                        if (s < 3) { u = s - 1; vv = half - 1; }
+                        else if (s == 3) { u = half - 1; vv = 1; }
+                        else { u = 1; vv = 1 + half; }
                         v = w1(h, ci, u, vv);
                     } else {
                         int per = p.Cp / 16, tap = s / per, kc = s % per;
