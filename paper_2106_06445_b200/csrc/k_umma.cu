@@ -51,6 +51,7 @@ struct StagePlan {
     int T, I;              // M-tiles per CTA batch, images per batch
     int Rtot;              // rows per plane incl. guards
     int pair;              // conv1 pair mode (Cp == 8)
+    int tri;               // conv1 tri mode (Cp == 32, c == 24; a_off)
     int k1, k2;            // k-steps per chunk: conv1, conv2
     int prec3;             // bf16x3
     int nslot, slot_bytes;
@@ -149,6 +150,32 @@ __host__ __device__ constexpr uint32_t pair_lbo_add(int s, int wp) {
 }
 constexpr int kPairK1 = 5;
 
+// conv1 "tri" mode (Cp = 32 planes holding c = 24 channels + the constant-1 channel 24): the
+// K of a tap is 3 useful 8-channel planes, so instead of 2 k-steps per tap (18, the 4th plane
+// almost all padding) conv1 runs 14:
+//   s = 0..8    : tap s, planes 0 | 1                                LBO = plane
+//   s = 9,10,11 : kernel row u = s-10, plane 2 of taps (u,-1) | (u,0)  LBO = 16 B
+//   s = 12      : plane 2 of taps (-1,+1) | (0,+1)                   LBO = Wp * 16 B
+//   s = 13      : plane 2 of tap (+1,+1) | plane 3 of the centre tap (the folded bias)
+//                                                                    LBO = plane - (Wp+1) * 16 B
+constexpr int kTriK1 = 14;
+struct AOff {
+    int shift, poff16;   // A start: row shift, plane offset (16-B units)
+    uint32_t lbo_add;    // added to the descriptor low word: LBO field delta (bits 16-29)
+};
+__host__ __device__ constexpr AOff a_off(int s, int am, bool hstk, int per, int wp, int plane16) {
+    if (am == 1) return AOff{pair_shift(s, wp), 0, pair_lbo_add(s, wp)};
+    if (am == 2) {
+        if (s < 9) return AOff{(s / 3 - 1) * wp + (s % 3 - 1), 0, 0u};
+        const int q = s - 9;
+        if (q < 3) return AOff{(q - 1) * wp - 1, 2 * plane16, (uint32_t)(1 - plane16) << 16};
+        if (q == 3) return AOff{-wp + 1, 2 * plane16, (uint32_t)(wp - plane16) << 16};
+        return AOff{wp + 1, 2 * plane16, (uint32_t)(-(wp + 1)) << 16};
+    }
+    return AOff{hstk ? (s / per - 1) * wp : ((s / per) / 3 - 1) * wp + ((s / per) % 3 - 1), 2 * (s % per) * plane16,
+                0u};
+}
+
 // ----------------------------------------------------------------------------------------
 // Compile-time specialised MMA issue for one conv segment (conv1 chunk or conv2 chunk).
 // Every k-step's A/B descriptor offsets, accumulate flags and ring-slot boundaries are
@@ -156,7 +183,7 @@ constexpr int kPairK1 = 5;
 //   alo0  : low descriptor word (start>>4 | LBO>>4 << 16) of the A buffer at row G, plane 0
 //   ringlo: low descriptor word of ring slot 0 with this segment's B LBO field
 // ----------------------------------------------------------------------------------------
-template <int K, int PER, bool PAIR, int WP, int PLANE16, int G, int KB16, int T, int N, bool P3,
+template <int K, int PER, int AM, int WP, int PLANE16, int G, int KB16, int T, int N, bool P3,
           int LOA16, int ACC0, int DSTRIDE, bool HSTK = false>
 __device__ __forceinline__ void issue_static(uint32_t tmem, uint32_t alo0, uint32_t ringlo, uint32_t slot16,
                                              uint32_t idesc, uint32_t acc_first, int& slot, uint32_t& phase,
@@ -175,10 +202,9 @@ __device__ __forceinline__ void issue_static(uint32_t tmem, uint32_t alo0, uint3
         }
         constexpr int dummy = 0;
         (void)dummy;
-        const int shift = PAIR ? pair_shift(s, WP)
-                               : (HSTK ? (s / PER - 1) * WP : ((s / PER) / 3 - 1) * WP + ((s / PER) % 3 - 1));
-        const int poff16 = PAIR ? 0 : 2 * (s % PER) * PLANE16;
-        const uint32_t al = alo0 + (uint32_t)(shift + poff16) + (PAIR ? pair_lbo_add(s, WP) : 0u);
+        const AOff o = a_off(s, AM, HSTK, PER, WP, PLANE16);
+        const int shift = o.shift, poff16 = o.poff16;
+        const uint32_t al = alo0 + (uint32_t)(shift + poff16) + o.lbo_add;
         const uint32_t b = bl + (uint32_t)((s % G) * KB16);
 #pragma unroll
         for (int t = 0; t < T; t++) {
@@ -202,7 +228,7 @@ __device__ __forceinline__ void issue_static(uint32_t tmem, uint32_t alo0, uint3
 // are resident (NS <= nslot), and tile t is issued as soon as the previous block's epilogue
 // has finished the X rows of tiles t-1..t+1 (x_tile[t+1]; arrivals are in tile order per
 // thread), so this chunk overlaps that epilogue instead of waiting for all of it.
-template <int K, int PER, bool PAIR, int WP, int PLANE16, int G, int KB16, int T, int N, bool P3,
+template <int K, int PER, int AM, int WP, int PLANE16, int G, int KB16, int T, int N, bool P3,
           int LOA16, int ACC0, int DSTRIDE>
 __device__ __forceinline__ void issue_static_tiles(uint32_t tmem, uint32_t alo0, uint32_t ringlo, uint32_t slot16,
                                                    uint32_t idesc, uint32_t acc_first, int& slot, uint32_t& phase,
@@ -228,10 +254,9 @@ __device__ __forceinline__ void issue_static_tiles(uint32_t tmem, uint32_t alo0,
         fence_after();
 #pragma unroll
         for (int s = 0; s < K; s++) {
-            const int shift = PAIR ? pair_shift(s, WP)
-                                   : ((s / PER) / 3 - 1) * WP + ((s / PER) % 3 - 1);
-            const int poff16 = PAIR ? 0 : 2 * (s % PER) * PLANE16;
-            const uint64_t ad = ((uint64_t)HI << 32) | (alo0 + (uint32_t)(shift + poff16 + t * 128) + (PAIR ? pair_lbo_add(s, WP) : 0u));
+            const AOff o = a_off(s, AM, false, PER, WP, PLANE16);
+            const int shift = o.shift, poff16 = o.poff16;
+            const uint64_t ad = ((uint64_t)HI << 32) | (alo0 + (uint32_t)(shift + poff16 + t * 128) + o.lbo_add);
             const uint64_t bd = ((uint64_t)HI << 32) | (bl[s / G] + (uint32_t)((s % G) * KB16));
             const uint32_t d = tmem + (uint32_t)(ACC0 + t * DSTRIDE);
             mma_bf16(d, ad, bd, idesc, s == 0 ? acc_first : 1u);
@@ -252,7 +277,7 @@ __device__ __forceinline__ void issue_static_tiles(uint32_t tmem, uint32_t alo0,
 // tile t is issued once dep[min(t + AHEAD, T-1)] completes (the epilogue has produced what
 // tile t reads: X / hidden rows of tiles <= t+1, or acc1 tile t read), and -- when `done` is
 // given -- a per-tile commit lets the epilogue consume tile t while later tiles still run.
-template <int K, int PER, bool PAIR, bool HSTK, int WP, int PLANE16, int G, int KB16, int T, int N, bool P3,
+template <int K, int PER, int AM, bool HSTK, int WP, int PLANE16, int G, int KB16, int T, int N, bool P3,
           int LOA16, int ACC0, int DSTRIDE, int AHEAD>
 __device__ __forceinline__ void issue_stream(uint32_t tmem, uint32_t alo0, uint32_t ringlo, uint32_t slot16,
                                              uint32_t idesc, uint32_t acc_first, int& slot, uint32_t& phase,
@@ -278,10 +303,9 @@ __device__ __forceinline__ void issue_stream(uint32_t tmem, uint32_t alo0, uint3
         fence_after();
 #pragma unroll
         for (int s = 0; s < K; s++) {
-            const int shift = PAIR ? pair_shift(s, WP)
-                                   : (HSTK ? (s / PER - 1) * WP : ((s / PER) / 3 - 1) * WP + ((s / PER) % 3 - 1));
-            const int poff16 = PAIR ? 0 : 2 * (s % PER) * PLANE16;
-            const uint64_t ad = ((uint64_t)HI << 32) | (alo0 + (uint32_t)(shift + poff16 + t * 128) + (PAIR ? pair_lbo_add(s, WP) : 0u));
+            const AOff o = a_off(s, AM, HSTK, PER, WP, PLANE16);
+            const int shift = o.shift, poff16 = o.poff16;
+            const uint64_t ad = ((uint64_t)HI << 32) | (alo0 + (uint32_t)(shift + poff16 + t * 128) + o.lbo_add);
             const uint64_t bd = ((uint64_t)HI << 32) | (bl[s / G] + (uint32_t)((s % G) * KB16));
             const uint32_t d = tmem + (uint32_t)(ACC0 + t * DSTRIDE);
             mma_bf16(d, ad, bd, idesc, s == 0 ? acc_first : 1u);
@@ -311,17 +335,16 @@ __device__ __forceinline__ void acquire_slots(uint32_t (&bl)[NS], uint32_t ringl
         if (++slot == nslot) { slot = 0; phase ^= 1; }
     }
 }
-template <int K, int PER, bool PAIR, bool HSTK, int WP, int PLANE16, int G, int KB16, int N, bool P3, int LOA16,
+template <int K, int PER, int AM, bool HSTK, int WP, int PLANE16, int G, int KB16, int N, bool P3, int LOA16,
           int ACC0, int DSTRIDE, int NS>
 __device__ __forceinline__ void issue_tile(int t, uint32_t tmem, uint32_t alo0, const uint32_t (&bl)[NS],
                                            uint32_t idesc, uint32_t acc_first) {
     constexpr uint32_t HI = 0x4008u;
 #pragma unroll
     for (int s = 0; s < K; s++) {
-        const int shift = PAIR ? pair_shift(s, WP)
-                               : (HSTK ? (s / PER - 1) * WP : ((s / PER) / 3 - 1) * WP + ((s / PER) % 3 - 1));
-        const int poff16 = PAIR ? 0 : 2 * (s % PER) * PLANE16;
-        const uint64_t ad = ((uint64_t)HI << 32) | (alo0 + (uint32_t)(shift + poff16 + t * 128) + (PAIR ? pair_lbo_add(s, WP) : 0u));
+        const AOff o = a_off(s, AM, HSTK, PER, WP, PLANE16);
+        const int shift = o.shift, poff16 = o.poff16;
+        const uint64_t ad = ((uint64_t)HI << 32) | (alo0 + (uint32_t)(shift + poff16 + t * 128) + o.lbo_add);
         const uint64_t bd = ((uint64_t)HI << 32) | (bl[s / G] + (uint32_t)((s % G) * KB16));
         const uint32_t d = tmem + (uint32_t)(ACC0 + t * DSTRIDE);
         mma_bf16(d, ad, bd, idesc, s == 0 ? acc_first : 1u);
@@ -350,8 +373,10 @@ struct SCfg {
     static constexpr bool FOLD = CP_ > C_;   // == StagePlan::fold
     static constexpr bool SPLIT = !HST && C_ % 8 == 0 && C_ / 2 < NC2_ / 2 &&
                                   (NC2_ / 2 == 8 || NC2_ / 2 == 16 || NC2_ / 2 == 32 || NC2_ / 2 == 48);
+    static constexpr bool TRI = CP_ == 32 && C_ == 24;   // == StagePlan::tri
+    static constexpr int AM1 = PAIR ? 1 : (TRI ? 2 : 0);  // conv1 A-operand mode (a_off)
     static constexpr int PER1 = PAIR ? 2 : CP / 16;
-    static constexpr int K1 = PAIR ? kPairK1 : 9 * (CP / 16);
+    static constexpr int K1 = PAIR ? kPairK1 : (TRI ? kTriK1 : 9 * (CP / 16));
     static constexpr int PER2 = MC / 16;
     static constexpr int K2 = (HST ? 3 : 9) * (MC / 16);
     static constexpr int KB1 = MC * 32 * (P3 ? 2 : 1), KB2 = NC2 * 32 * (P3 ? 2 : 1);
@@ -565,7 +590,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             constexpr uint32_t LBO1 = CFG::PAIR ? 16u : (uint32_t)CFG::PLANE16 * 16u;
                             const uint32_t alo0 = ((xb >> 4) & 0x3FFFu) | ((LBO1 >> 4) << 16);
                             const uint32_t ringlo = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::MC * 16 >> 4) << 16);
-                            issue_static<CFG::K1, CFG::PER1, CFG::PAIR, CFG::WP, CFG::PLANE16, CFG::G1, CFG::KB1 / 16,
+                            issue_static<CFG::K1, CFG::PER1, CFG::AM1, CFG::WP, CFG::PLANE16, CFG::G1, CFG::KB1 / 16,
                                          CFG::T, CFG::MC, CFG::P3, CFG::LOX16, CFG::ACC1, CFG::MC>(
                                 tmem, alo0, ringlo, (uint32_t)CFG::SLOT / 16u, id1, CFG::FOLD ? 0u : 1u, slot, phase,
                                 p.nslot, full, empty);
@@ -583,6 +608,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                     shift = pair_shift(s, p.Wp);
                                     poff = 0;
                                     if (s == 3) lbo = (uint32_t)p.Wp * 16u;
+                                } else if (p.tri) {
+                                    const AOff o = a_off(s, 2, false, 2, p.Wp, p.Rtot);
+                                    shift = o.shift;
+                                    poff = (uint32_t)o.poff16 * 16u;
+                                    lbo = (uint32_t)(p.Rtot + ((int32_t)o.lbo_add >> 16)) * 16u;
                                 } else {
                                     shift = (tap / 3 - 1) * p.Wp + (tap % 3 - 1);
                                     poff = (uint32_t)(2 * kc) * plane_bytes;
@@ -662,7 +692,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                         const uint32_t ring1 = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::MC * 16 >> 4) << 16);
                         const uint32_t ring2 = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::NC2 * 16 >> 4) << 16);
                         long long tx0 = CLK();
-                        issue_stream<CFG::K1, CFG::PER1, CFG::PAIR, false, CFG::WP, CFG::PLANE16, CFG::G1, CFG::KB1 / 16,
+                        issue_stream<CFG::K1, CFG::PER1, CFG::AM1, false, CFG::WP, CFG::PLANE16, CFG::G1, CFG::KB1 / 16,
                                      CFG::T, CFG::MC, CFG::P3, CFG::LOX16, CFG::ACC1, CFG::MC, 1>(
                             tmem, alo1, ring1, (uint32_t)CFG::SLOT / 16u, id1, 0u, slot, phase, p.nslot, full, empty,
                             x_tile, xph, a1t);
@@ -690,7 +720,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                     if (t < CFG::T) {
                                         TWAIT(w_hd, mbar_wait(&a1f[t], a1fph));
                                         fence_after();
-                                        issue_tile<CFG::K1, CFG::PER1, CFG::PAIR, false, CFG::WP, CFG::PLANE16, CFG::G1,
+                                        issue_tile<CFG::K1, CFG::PER1, CFG::AM1, false, CFG::WP, CFG::PLANE16, CFG::G1,
                                                    CFG::KB1 / 16, CFG::MC, CFG::P3, CFG::LOX16, CFG::ACC1, CFG::MC, NS1>(
                                             t, tmem, alo1, bl1, id1, 0u);
                                         commit(&a1t[t]);
@@ -714,7 +744,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 continue;
                             }
                             if (j + 1 < p.nch) {
-                                issue_stream<CFG::K1, CFG::PER1, CFG::PAIR, false, CFG::WP, CFG::PLANE16, CFG::G1,
+                                issue_stream<CFG::K1, CFG::PER1, CFG::AM1, false, CFG::WP, CFG::PLANE16, CFG::G1,
                                              CFG::KB1 / 16, CFG::T, CFG::MC, CFG::P3, CFG::LOX16, CFG::ACC1, CFG::MC, 0>(
                                     tmem, alo1, ring1, (uint32_t)CFG::SLOT / 16u, id1, 0u, slot, phase, p.nslot, full,
                                     empty, a1f, a1fph, a1t);
@@ -744,7 +774,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             const uint32_t alo0 = ((xb >> 4) & 0x3FFFu) | ((LBO1 >> 4) << 16);
                             const uint32_t ringlo = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::MC * 16 >> 4) << 16);
                             long long tx0 = CLK();
-                            issue_static_tiles<CFG::K1, CFG::PER1, CFG::PAIR, CFG::WP, CFG::PLANE16, CFG::G1,
+                            issue_static_tiles<CFG::K1, CFG::PER1, CFG::AM1, CFG::WP, CFG::PLANE16, CFG::G1,
                                                CFG::KB1 / 16, CFG::T, CFG::MC, CFG::P3, CFG::LOX16, CFG::ACC1, CFG::MC>(
                                 tmem, alo0, ringlo, (uint32_t)CFG::SLOT / 16u, id1, CFG::FOLD ? 0u : 1u, slot, phase,
                                 p.nslot, full, empty, x_tile, xph);
@@ -1801,11 +1831,12 @@ static bool make_plan(const StageInfo& S, bool prec3, StagePlan& best) {
     p.Mp = rup(S.m, 16);
     p.fold = p.Cp > S.c ? 1 : 0;
     p.pair = p.Cp == 8;
+    p.tri = p.Cp == 32 && S.c == 24;
     p.prec3 = prec3 ? 1 : 0;
     const int P = prec3 ? 2 : 1;
     const double P3f = prec3 ? 3.0 : 1.0;
     const int img_rows = (p.H + 1) * p.Wp;
-    const int k1 = p.pair ? kPairK1 : 9 * (p.Cp / 16);
+    const int k1 = p.pair ? kPairK1 : (p.tri ? kTriK1 : 9 * (p.Cp / 16));
     double best_cost = 1e300;
     // conv2 with horizontal tap stacking (mandatory for c <= 8, optional up to c = 24) or plain
     for (int hopt = 1; hopt >= 0; hopt--) {
@@ -1928,6 +1959,12 @@ static void pack_block(const StagePlan& p, const float* W1, const float* b1, con
                         else if (s == 3) { u = half - 1; vv = 1; }
                         else { u = 1; vv = 1 + half; }
                         v = w1(h, ci, u, vv);
+                    } else if (p.tri) {   // k-step order of a_off mode 2
+                        const int e = kk % 8, half = kk / 8;
+                        if (s < 9) v = w1(h, half * 8 + e, s / 3 - 1, s % 3 - 1);
+                        else if (s < 12) v = w1(h, 16 + e, s - 10, half - 1);
+                        else if (s == 12) v = w1(h, 16 + e, half - 1, 1);
+                        else v = half ? w1(h, 24 + e, 0, 0) : w1(h, 16 + e, 1, 1);
                     } else {
                         int per = p.Cp / 16, tap = s / per, kc = s % per;
                         v = w1(h, kc * 16 + kk, tap / 3 - 1, tap % 3 - 1);
