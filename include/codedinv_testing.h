@@ -21,7 +21,12 @@ extern "C" {
  *           [16j, 16j+16)   (row-shifted start address, K-planes at LBO = RA*16 B);
  *   mode 1: KA = 8; step j uses A channels 0..7 of rows shift+2j+i (K-half 0) and
  *           shift+2j+1+i (K-half 1) against B columns [16j, 16j+16) (LBO = 16 B).
- * Requires 16 <= N <= 256, N % 16 == 0, KA % 8 == 0, KB % 16 == 0, shift + 127 + 2nk < RA. */
+ *   mode 2 | (L << 8): the A planes concatenated as one column of 16-B rows (plane p row r =
+ *           row p*RA + r); step j's K-half 0 = rows shift+j+i, K-half 1 = rows shift+j+L+i
+ *           against B columns [16j, 16j+16) (LBO = L*16 B: the conv kernel's vertical tap
+ *           pairs, L = Wp, and cross-plane pairs, L = plane rows - Wp - 1).
+ * Requires 16 <= N <= 256, N % 16 == 0, KA % 8 == 0, KB % 16 == 0, shift + 127 + 2nk < RA
+ * (mode 2: 1 <= L < 16384, shift + nk + L + 127 < RA * KA/8). */
 CI_API ci_status_t ci_test_umma_gemm(const uint16_t* A, int32_t RA, int32_t KA, const uint16_t* B,
                                      int32_t N, int32_t KB, int32_t shift, int32_t mode, int32_t nk,
                                      float* D, ci_stream_t stream);

@@ -1,6 +1,7 @@
 // Test-only probes of the tcgen05 building blocks (include/codedinv_testing.h):
 //  * ci_test_umma_gemm: one 128 x N x (16*nk) UMMA with the descriptor tricks the conv
-//    kernel relies on (row-shifted start address; LBO = 16 B pairing adjacent rows),
+//    kernel relies on (row-shifted start address; LBO = 16 B pairing adjacent rows; any
+//    LBO, e.g. Wp rows for vertical tap pairs or across planes for the tri mode),
 //    checked against a host reference by tests/test_gpu_umma.py;
 //  * ci_test_umma_rate: back-to-back MMA issue rate per SM for a given N.
 #include <stdio.h>
@@ -48,8 +49,10 @@ __global__ void __launch_bounds__(128) k_umma_gemm(const uint16_t* __restrict__ 
             uint64_t ad, bd;
             if (mode == 0) {  // K-halves = planes 2j, 2j+1
                 ad = smem_desc(smem_u32(sA) + (uint32_t)(2 * j * RA + shift) * 16, RA * 16, 128);
-            } else {          // K-halves = rows r and r+1 of plane 0 (LBO = 16 B); step j moves 2 rows
+            } else if ((mode & 0xFF) == 1) {   // K-halves = rows r and r+1 of plane 0 (LBO = 16 B); step j moves 2 rows
                 ad = smem_desc(smem_u32(sA) + (uint32_t)(shift + 2 * j) * 16, 16, 128);
+            } else {   // mode 2: K-half 1 = LBO (mode >> 8) 16-B rows after K-half 0 (across planes); step j moves 1 row
+                ad = smem_desc(smem_u32(sA) + (uint32_t)(shift + j) * 16, (uint32_t)(mode >> 8) * 16u, 128);
             }
             bd = smem_desc(smem_u32(sB) + (uint32_t)(2 * j * N) * 16, N * 16, 128);
             mma_bf16(tmem, ad, bd, idesc, j > 0);
@@ -224,7 +227,9 @@ extern "C" {
 ci_status_t ci_test_umma_gemm(const uint16_t* A, int32_t RA, int32_t KA, const uint16_t* B, int32_t N,
                               int32_t KB, int32_t shift, int32_t mode, int32_t nk, float* D,
                               ci_stream_t stream) {
-    if (N < 16 || N > 256 || N % 16 || KA % 8 || KB % 16 || nk < 1 || shift < 0) {
+    const int lbo_rows = mode >> 8;
+    if (N < 16 || N > 256 || N % 16 || KA % 8 || KB % 16 || nk < 1 || shift < 0 || (mode & 0xFF) > 2 ||
+        ((mode & 0xFF) == 2 && (lbo_rows < 1 || lbo_rows >= 16384 || shift + nk + lbo_rows + 127 >= RA * (KA / 8)))) {
         set_error("bad probe shape");
         return CI_ERR_INVALID_ARG;
     }

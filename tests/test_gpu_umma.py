@@ -57,6 +57,28 @@ def test_umma_gemm_lbo16_pairs_adjacent_rows(ci, shift):
     assert np.array_equal(D.cpu().numpy(), ref)
 
 
+@pytest.mark.parametrize("lbo_rows,shift", [(17, 0), (9, 4), (5, 2), (1187, 3), (300, 130)])
+def test_umma_gemm_any_lbo(ci, lbo_rows, shift):
+    """Any LBO is legal for K-major no-swizzle: the pair-mode vertical taps (LBO = Wp rows:
+    17 / 9 / 5) and the tri mode's cross-plane pair (LBO = plane - (Wp+1) rows, here into the
+    next plane: K-half 1 reads plane 1)."""
+    rng = np.random.default_rng(lbo_rows * 7 + shift)
+    N, nk, KA = 48, 3, 16
+    RA = 1200 if lbo_rows > 200 else 160 + shift + lbo_rows
+    A = bf16_small_ints(rng, (RA, KA))
+    B = bf16_small_ints(rng, (N, 16 * nk))
+    D = torch.empty(128, N, device="cuda")
+    ci.ci_test_umma_gemm(to_bf16_bits(A), to_bf16_bits(B), N, shift, 2 | (lbo_rows << 8), nk, D)
+    torch.cuda.synchronize()
+    lin = np.concatenate([A[:, 0:8], A[:, 8:16]], axis=0)   # plane p row r -> row p*RA + r
+    ref = np.zeros((128, N), np.float32)
+    for j in range(nk):
+        r0 = shift + j
+        ref += lin[r0:r0 + 128] @ B[:, 16 * j:16 * j + 8].T
+        ref += lin[r0 + lbo_rows:r0 + lbo_rows + 128] @ B[:, 16 * j + 8:16 * j + 16].T
+    assert np.array_equal(D.cpu().numpy(), ref)
+
+
 def test_umma_issue_rate_report(ci):
     """Reports the SS-mode tcgen05 rate (cycles per 128xNx16 MMA, 148 CTAs, tight issue loop;
     profiles/r01_umma_probe.md); sanity only."""
