@@ -1803,7 +1803,8 @@ static double mma_cyc(int N) { return std::max(N / 2.0, 32.0 + N / 4.0); }
 struct TunedPlan { int H, W, c, m, prec3, MC, T, nhd, nslot, hst; };
 static const TunedPlan kTuned[] = {
     {16, 16, 6, 64, 0, 32, 7, 2, 3, 1},    // stage 1 bf16: SMEM-resident state fits
-    {8, 8, 24, 128, 0, 64, 3, 2, 3, 1},    // stage 2 bf16: wide hst (N = 3 x 24 -> 80), N = 64 conv1 (T = 3)
+    {8, 8, 24, 128, 0, 128, 2, 1, 3, 1},   // stage 2 bf16: wide hst (N = 3 x 24 -> 80), one N = 128 conv1 chunk, T = 2
+    {8, 8, 24, 128, 0, 64, 3, 2, 3, 1},    // stage 2 bf16: wide hst, N = 64 conv1, T = 3 (CI_S1_MC64)
     {8, 8, 24, 128, 0, 32, 4, 2, 3, 1},    // stage 2 bf16: wide hst, N = 32 conv1, T = 4 (CI_S1_MC32)
     {8, 8, 24, 128, 0, 32, 7, 2, 3, 0},    // stage 2 bf16, plain conv2 (CI_NO_WIDE_HST)
     {4, 4, 96, 256, 0, 128, 2, 1, 4, 0},   // stage 3 bf16
@@ -1820,10 +1821,12 @@ static bool make_plan(const StageInfo& S, bool prec3, StagePlan& best) {
     StagePlan p{};
     static const bool no_wide_hst = getenv("CI_NO_WIDE_HST") != nullptr;   // A/B switch
     static const bool s1_mc32 = getenv("CI_S1_MC32") != nullptr;           // A/B switch
+    static const bool s1_mc64 = getenv("CI_S1_MC64") != nullptr;           // A/B switch
     const TunedPlan* tuned = nullptr;
     for (const auto& tp : kTuned)   // first match wins
         if (!tuned && tp.H == S.H && tp.W == S.W && tp.c == S.c && tp.m == S.m && tp.prec3 == (prec3 ? 1 : 0) &&
-            !(no_wide_hst && tp.hst && tp.c > 8) && !(tp.c == 24 && !tp.prec3 && tp.MC == 64 && tp.hst && s1_mc32))
+            !(no_wide_hst && tp.hst && tp.c > 8) && !(tp.c == 24 && !tp.prec3 && tp.MC == 64 && tp.hst && s1_mc32) &&
+            !(tp.c == 24 && !tp.prec3 && tp.MC == 128 && tp.hst && (s1_mc64 || s1_mc32)))
             tuned = &tp;
     p.H = S.H; p.W = S.W; p.Wp = S.W + 1; p.G = p.Wp + 2;
     p.c = S.c; p.m = S.m;
@@ -2021,6 +2024,7 @@ static const SpecEntry kSpecs[] = {
     CI_SPEC(9, 32, 32, 32, 7, 0, 16384, 8, 24, 0),   // C stage 2, bf16 (plain conv2)
     CI_SPEC_X(9, 32, 32, 80, 4, 0, 16384, 8, 24, 1, 1, 0),   // C stage 2, bf16, wide hst, SMEM state
     CI_SPEC_X(9, 32, 64, 80, 3, 0, 16384, 8, 24, 1, 1, 0),   // C stage 2, bf16, wide hst, N = 64 conv1
+    CI_SPEC_X(9, 32, 128, 80, 2, 0, 16384, 8, 24, 1, 1, 0),  // C stage 2, bf16, wide hst, N = 128 conv1
     CI_SPEC(5, 96, 128, 96, 2, 0, 16384, 4, 96, 0),  // C stage 3, bf16
     CI_SPEC(17, 8, 16, 32, 7, 1, 16384, 16, 6, 0),   // C stage 1, bf16x3 (hst)
     CI_SPEC(9, 32, 128, 32, 2, 1, 16384, 8, 24, 0),  // C stage 2, bf16x3 (plain conv2)
