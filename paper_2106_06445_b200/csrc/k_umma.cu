@@ -1122,7 +1122,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             for (int u = 0; u < 2 && q0 + u < T; u++) mbar_arrive(&hdt[hb_i * kMaxTiles + q0 + u]);
                         }
                         a1ph ^= 1;
-                    } else if constexpr (S && (CFG::MC == 32 || (CFG::MC == 64 && !CFG::P3 && !CFG::RES))) {
+                    } else if constexpr (S && (CFG::MC == 32 || ((CFG::MC == 64 || (CFG::MC == 128 && CFG::FOLD)) && !CFG::P3 && !CFG::RES))) {
                         // Batched TMEM reads: up to four LW-column loads in flight per wait::ld
                         // (one load per wait is latency-bound at ~250 cycles), flattened over
                         // (tile, column group); no registers stay live across batches.
