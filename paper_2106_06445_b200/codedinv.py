@@ -13,8 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# CI_LIB: load another build of the same ABI (same-box A/B timing of kernel variants)
-LIB_PATH = os.environ.get("CI_LIB") or os.path.join(_HERE, "libcodedinv.so")
+LIB_PATH = os.path.join(_HERE, "libcodedinv.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
@@ -23,9 +22,9 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 CI_OK, CI_ERR_INVALID_ARG, CI_ERR_INVALID_SHAPE, CI_ERR_DIM_MISMATCH, CI_ERR_UNSUPPORTED, \
     CI_ERR_WORKSPACE, CI_ERR_CUDA = range(7)
-CI_PREC_FP32, CI_PREC_BF16, CI_PREC_SIMT = 0, 1, 2
+CI_PREC_FP32, CI_PREC_BF16, CI_PREC_F16X2 = 0, 1, 2
 CI_ENC_EXACT, CI_ENC_LEARNED = 0, 1
-PRECISIONS = {"fp32": CI_PREC_FP32, "bf16": CI_PREC_BF16, "simt": CI_PREC_SIMT}
+PRECISIONS = {"fp32": CI_PREC_FP32, "bf16": CI_PREC_BF16, "f16x2": CI_PREC_F16X2}
 
 EXPORTS = ["ci_last_error", "ci_model_create", "ci_model_destroy", "ci_feature_dim",
            "ci_workspace_size", "ci_check", "ci_forward_h", "ci_inverse_h", "ci_encode",
@@ -33,8 +32,8 @@ EXPORTS = ["ci_last_error", "ci_model_create", "ci_model_destroy", "ci_feature_d
            "ci_serve_group_host", "ci_make_drops", "ci_worker_coef", "ci_combine",
            "ci_workspace_size_general", "ci_encode_general", "ci_decode_general", "ci_serve_general",
            "ci_encode_perturbed", "ci_online_update", "ci_serve_group_host_async"]
-TESTING_EXPORTS = ["ci_test_umma_gemm", "ci_test_umma_rate", "ci_test_prof_enable", "ci_test_prof_read",
-                   "ci_test_launch_count", "ci_test_mean", "ci_test_plan"]  # include/codedinv_testing.h
+TESTING_EXPORTS = ["ci_test_prof_enable", "ci_test_prof_read", "ci_test_launch_count", "ci_test_mean",
+                   "ci_test_plan"]  # include/codedinv_testing.h
 
 
 class CiStage(ctypes.Structure):
@@ -76,8 +75,6 @@ _sig = {
     "ci_encode_general": (_I32, [_P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
     "ci_decode_general": (_I32, [_I32, _I32, _I64, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
     "ci_serve_general": (_I32, [_P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
-    "ci_test_umma_gemm": (_I32, [_P, _I32, _I32, _P, _I32, _I32, _I32, _I32, _I32, _P, _P]),
-    "ci_test_umma_rate": (_I32, [_I32, _I32, _I32, _P, _P]),
     "ci_test_prof_enable": (_I32, [_I32]),
     "ci_test_prof_read": (_I32, [_P, _P, _P]),
     "ci_test_launch_count": (_I64, [_I32]),
@@ -85,8 +82,6 @@ _sig = {
     "ci_test_plan": (_I32, [_I32, _I32, _I32, _I32, _I32, _P]),
 }
 for _name, (_res, _args) in _sig.items():
-    if os.environ.get("CI_LIB") and not hasattr(_lib, _name):
-        continue   # A/B build of an older revision (scripts/ab_build.py): newer entry points absent
     _f = getattr(_lib, _name)
     _f.restype, _f.argtypes = _res, _args
 
@@ -278,16 +273,7 @@ def ci_last_error() -> str:
     return _lib.ci_last_error().decode()
 
 
-# ---- test-only entry points (include/codedinv_testing.h)
-def ci_test_umma_gemm(A, B, N, shift, mode, nk, D, stream=None):
-    _check(_lib.ci_test_umma_gemm(_ptr(A), A.shape[0], A.shape[1], _ptr(B), N, B.shape[1], shift, mode,
-                                  nk, _ptr(D), _stream(stream)), "ci_test_umma_gemm")
-
-
-def ci_test_umma_rate(N, iters, nblocks, cycles, stream=None):
-    _check(_lib.ci_test_umma_rate(N, iters, nblocks, _ptr(cycles), _stream(stream)), "ci_test_umma_rate")
-
-
+# ---- instrumentation entry points (include/codedinv_testing.h)
 def ci_test_prof_enable(enable=True):
     _check(_lib.ci_test_prof_enable(1 if enable else 0), "ci_test_prof_enable")
 
@@ -314,7 +300,8 @@ PLAN_FIELDS = ["Wp", "G", "Cp", "Mp", "MC", "nch", "Nc2", "T", "I", "Rtot", "k1"
                "slot_bytes", "smem", "blk_bytes", "nhd", "sstate", "est", "tmem_cols", "hst", "hc", "static"]
 
 
-def ci_test_plan(H, W, c, m, prec3):
+def ci_test_plan(H, W, c, m, pm):
+    """pm: 0 bf16, 1 f16x2, 2 f16x3 (CI_PREC_FP32)."""
     out = (ctypes.c_int64 * len(PLAN_FIELDS))()
-    _check(_lib.ci_test_plan(H, W, c, m, 1 if prec3 else 0, out), "ci_test_plan")
+    _check(_lib.ci_test_plan(H, W, c, m, int(pm), out), "ci_test_plan")
     return dict(zip(PLAN_FIELDS, list(out)))

@@ -57,8 +57,6 @@ static int* next_ctr(void* ws, const WsLayout& L) {
     return reinterpret_cast<int*>(reinterpret_cast<char*>(ws) + L.flag) + kCtrBase + L.ctr_next++;
 }
 
-static constexpr int64_t kSimtChunk = 1024;
-
 // groups = false: layout of a plain h / h^-1 call on n = B*k images (no per-group buffers)
 // r: parity queries per group (1 for n = k + 1; general codes r = n - k)
 static WsLayout ws_layout(const Model* m, int32_t k, int64_t B, bool groups = true, int32_t r = 1) {
@@ -70,11 +68,6 @@ static WsLayout ws_layout(const Model* m, int32_t k, int64_t B, bool groups = tr
     L.scratch = off; off += up(sizeof(float) * (size_t)(std::max<int64_t>(n, 1) * m->d));
     L.mean = off; off += up(sizeof(float) * (size_t)(Bg * m->d));
     L.xp = off; off += up(sizeof(float) * (size_t)(Bg * m->din));
-    L.hidden = off;
-    if (m->prec == CI_PREC_SIMT)   // hidden [chunk][max m*H*W] + (residual inverse) y copy [chunk][d]
-        off += m->arch.block_kind == 1
-                   ? sizeof(float) * (size_t)(kSimtChunk * m->max_hidden) + up(sizeof(float) * (size_t)(kSimtChunk * m->d))
-                   : up(sizeof(float) * (size_t)(std::min<int64_t>(std::max<int64_t>(n, 1), kSimtChunk) * m->max_hidden));
     L.enc = off;
     if (m->enc_off >= 0 && groups) {   // m, z, z2, z3, u of the learned encoder
         const int64_t HW = (int64_t)m->arch.in_h * m->arch.in_w;
@@ -91,62 +84,10 @@ static T* at(void* ws, size_t off) { return reinterpret_cast<T*>(reinterpret_cas
 // ---------------------------------------------------------------------------
 // h / h^-1 orchestration (both precisions share the stage-boundary permutations)
 // ---------------------------------------------------------------------------
-static ci_status_t run_stage_blocks(const Model* m, int s, float* state, int64_t n, bool inverse,
-                                    float* hidden, int* ctr, cudaStream_t st) {
-    const StageInfo& S = m->st[s];
-    if (m->umma) return umma_stage(m, s, state, n, inverse, ctr, st);
-    const int64_t per = (int64_t)S.C * S.H * S.W, half = (int64_t)S.c * S.H * S.W;
-    if (m->arch.block_kind == 1) {   // i-ResNet: s += F(s); inverse: N x (x <- y - F(x))
-        const int64_t hstr = (int64_t)S.m * S.H * S.W;
-        float* ybuf = hidden + kSimtChunk * m->max_hidden;   // [chunk][C][H][W] copy of y
-        for (int tt = 0; tt < S.nb; tt++) {
-            int t = inverse ? S.nb - 1 - tt : tt;
-            const float* W1 = m->d_params + m->blk_off[m->blk_first[s] + t];
-            const float* b1 = W1 + (int64_t)S.m * S.c * 9;
-            const float* W2 = b1 + S.m;
-            const float* b2 = W2 + (int64_t)S.c * S.m * 9;
-            for (int64_t i0 = 0; i0 < n; i0 += kSimtChunk) {
-                int64_t nc = std::min<int64_t>(kSimtChunk, n - i0);
-                float* x = state + i0 * per;
-                if (!inverse) {
-                    CI_CUDA(launch_conv_simt(x, per, S.c, S.H, S.W, W1, b1, S.m, hidden, hstr, nc, 0, m->arch.act, st));
-                    CI_CUDA(launch_conv_simt(hidden, hstr, S.m, S.H, S.W, W2, b2, S.c, x, per, nc, 1, 0, st));
-                    continue;
-                }
-                CI_CUDA(cudaMemcpyAsync(ybuf, x, sizeof(float) * nc * per, cudaMemcpyDeviceToDevice, st));
-                for (int it = 0; it < m->arch.fp_iters; it++) {
-                    CI_CUDA(launch_conv_simt(x, per, S.c, S.H, S.W, W1, b1, S.m, hidden, hstr, nc, 0, m->arch.act, st));
-                    CI_CUDA(launch_conv_simt(hidden, hstr, S.m, S.H, S.W, W2, b2, S.c, x, per, nc, 3, 0, st, ybuf));
-                }
-            }
-        }
-        return CI_OK;
-    }
-    for (int tt = 0; tt < S.nb; tt++) {
-        int t = inverse ? S.nb - 1 - tt : tt;
-        const float* blk = m->d_params + m->blk_off[m->blk_first[s] + t];
-        const float* W1 = blk;
-        const float* b1 = W1 + (int64_t)S.m * S.c * 9;
-        const float* W2 = b1 + S.m;
-        const float* b2 = W2 + (int64_t)S.c * S.m * 9;
-        int orient = (m->arch.first_orientation + t) & 1;
-        int64_t src_off = orient == 0 ? 0 : half, dst_off = orient == 0 ? half : 0;
-        for (int64_t i0 = 0; i0 < n; i0 += kSimtChunk) {
-            int64_t nc = std::min<int64_t>(kSimtChunk, n - i0);
-            CI_CUDA(launch_conv_simt(state + i0 * per + src_off, per, S.c, S.H, S.W, W1, b1, S.m,
-                                     hidden, (int64_t)S.m * S.H * S.W, nc, 0, m->arch.act, st));
-            CI_CUDA(launch_conv_simt(hidden, (int64_t)S.m * S.H * S.W, S.m, S.H, S.W, W2, b2, S.c,
-                                     state + i0 * per + dst_off, per, nc, inverse ? 2 : 1, 0, st));
-        }
-    }
-    return CI_OK;
-}
-
 static ci_status_t forward_impl(const Model* m, const float* x, float* h, int64_t n, void* ws,
                                 const WsLayout& L, cudaStream_t st) {
     if (n == 0) return CI_OK;
     float* scratch = at<float>(ws, L.scratch);
-    float* hidden = at<float>(ws, L.hidden);
     // stage s starts with a copy (psi or identity) into buffer buf[s]; last buffer = h
     const int S = m->n_stages;
     const float* src = x;
@@ -155,7 +96,7 @@ static ci_status_t forward_impl(const Model* m, const float* x, float* h, int64_
         float* dst = ((S - 1 - s) % 2 == 0) ? h : scratch;
         CI_CUDA(launch_permute(src, dst, n, C, H, W, m->st[s].squeeze ? 1 : 0, st));
         C = m->st[s].C; H = m->st[s].H; W = m->st[s].W;
-        ci_status_t r = run_stage_blocks(m, s, dst, n, false, hidden, next_ctr(ws, L), st);
+        ci_status_t r = umma_stage(m, s, dst, n, false, next_ctr(ws, L), st);
         if (r != CI_OK) return r;
         src = dst;
     }
@@ -166,7 +107,6 @@ static ci_status_t inverse_impl(const Model* m, const float* h, float* x, int64_
                                 const WsLayout& L, cudaStream_t st) {
     if (n == 0) return CI_OK;
     float* scratch = at<float>(ws, L.scratch);
-    float* hidden = at<float>(ws, L.hidden);
     const int S = m->n_stages;
     // copies: 1 initial + 1 after each stage -> S + 1 copies, the last one lands in x
     int ncopy = S + 1, ci = 0;
@@ -175,7 +115,7 @@ static ci_status_t inverse_impl(const Model* m, const float* h, float* x, int64_
     const StageInfo& L3 = m->st[S - 1];
     CI_CUDA(launch_permute(h, cur, n, L3.C, L3.H, L3.W, 0, st));
     for (int s = S - 1; s >= 0; s--) {
-        ci_status_t r = run_stage_blocks(m, s, cur, n, true, hidden, next_ctr(ws, L), st);
+        ci_status_t r = umma_stage(m, s, cur, n, true, next_ctr(ws, L), st);
         if (r != CI_OK) return r;
         float* nxt = target(ci++);
         const StageInfo& Si = m->st[s];
@@ -193,11 +133,8 @@ static ci_status_t encode_learned_impl(const Model* m, const float* x, float* xp
     const int64_t HW = (int64_t)H * W, hw4 = HW / 4;
     const float* E1W = m->d_params + m->enc_off;
     const float* E1b = E1W + (int64_t)c1 * Ci * 9;
-    const float* E2W = E1b + c1;
-    const float* E2b = E2W + (int64_t)mid * 4 * c1 * 9;
-    const float* E3W = E2b + mid;
-    const float* E3b = E3W + (int64_t)4 * c1 * mid * 9;
-    const float* E4W = E3b + 4 * c1;
+    // E2 / E3 are packed into the model's tcgen05 weight stream (umma_prepare)
+    const float* E4W = E1b + c1 + (int64_t)mid * 4 * c1 * 9 + mid + (int64_t)4 * c1 * mid * 9 + 4 * c1;
     const float* E4b = E4W + (int64_t)Ci * c1 * 9;
     // workspace: m [B][c1][H][W] | zbuf [B][8c1][H/2][W/2] (tail in | out) | z2 [B][mid][..] | u
     float* Mb = at<float>(ws, L.enc);
@@ -206,14 +143,8 @@ static ci_status_t encode_learned_impl(const Model* m, const float* x, float* xp
     float* Z2 = Zb + B * zstride;
     float* U = Z2 + B * mid * hw4;
     CI_CUDA(launch_enc_e1_mean(x, k, B, Ci, H, W, E1W, E1b, c1, Mb, Zb, zstride, st));
-    if (m->umma) {
-        ci_status_t r = umma_encoder_tail(m, Zb, B, next_ctr(ws, L), st);   // tcgen05: ReLU(E3(ReLU(E2 z)))
-        if (r != CI_OK) return r;
-    } else {
-        CI_CUDA(launch_conv_simt(Zb, zstride, 4 * c1, H / 2, W / 2, E2W, E2b, mid, Z2, mid * hw4, B, 0, 0, st));
-        CI_CUDA(launch_conv_simt(Z2, mid * hw4, mid, H / 2, W / 2, E3W, E3b, 4 * c1, Zb + 4 * c1 * hw4, zstride, B,
-                                 0, 0, st));
-    }
+    ci_status_t r = umma_encoder_tail(m, Zb, B, next_ctr(ws, L), st);   // tcgen05: ReLU(E3(ReLU(E2 z)))
+    if (r != CI_OK) return r;
     CI_CUDA(launch_unsqueeze_add(Zb + 4 * c1 * hw4, zstride, Mb, U, B, c1, H, W, st));
     CI_CUDA(launch_conv_simt(U, c1 * HW, c1, H, W, E4W, E4b, Ci, xp, Ci * HW, B, 0, 2, st));
     return CI_OK;
@@ -234,7 +165,7 @@ ci_status_t ci_model_create(const ci_arch_t* arch, const float* host_params, siz
                             ci_precision_t precision, int device, ci_model_t** out) {
     if (!arch || !host_params || !out) { set_error("NULL argument"); return CI_ERR_INVALID_ARG; }
     *out = nullptr;
-    if (precision != CI_PREC_FP32 && precision != CI_PREC_BF16 && precision != CI_PREC_SIMT) {
+    if (precision != CI_PREC_FP32 && precision != CI_PREC_BF16 && precision != CI_PREC_F16X2) {
         set_error("unknown precision %d", (int)precision);
         return CI_ERR_INVALID_ARG;
     }
@@ -270,7 +201,6 @@ ci_status_t ci_model_create(const ci_arch_t* arch, const float* host_params, siz
             m->blk_off.push_back(off);
             off += (int64_t)S.m * S.c * 9 + S.m + (int64_t)S.c * S.m * 9 + S.c;
         }
-        m->max_hidden = std::max<int64_t>(m->max_hidden, (int64_t)S.m * H * W);
     }
     m->d = (int64_t)C * H * W;
     m->din = (int64_t)a.in_c * a.in_h * a.in_w;
@@ -309,10 +239,12 @@ ci_status_t ci_model_create(const ci_arch_t* arch, const float* host_params, siz
             e = cudaMemcpy(m->d_head[t], host_params + m->head_off[t], sizeof(float) * nh, cudaMemcpyHostToDevice);
         if (e != cudaSuccess) { ci_model_destroy(reinterpret_cast<ci_model_t*>(m)); return cuda_status(e, "head weights"); }
     }
-    if (precision != CI_PREC_SIMT) {
-        ci_status_t r = umma_prepare(m, host_params);
-        if (r != CI_OK) { ci_model_destroy(reinterpret_cast<ci_model_t*>(m)); return r; }
-        m->umma = true;
+    ci_status_t r = umma_prepare(m, host_params);
+    if (r != CI_OK) { ci_model_destroy(reinterpret_cast<ci_model_t*>(m)); return r; }
+    if (m->enc_off >= 0 && !umma_has_encoder(m)) {   // every later learned-mode call needs the tail plan
+        ci_model_destroy(reinterpret_cast<ci_model_t*>(m));
+        set_error("learned encoder widths (c1=%d, mid=%d) do not fit the tcgen05 stage kernel", a.enc_c1, a.enc_mid);
+        return CI_ERR_UNSUPPORTED;
     }
     *out = reinterpret_cast<ci_model_t*>(m);
     return CI_OK;

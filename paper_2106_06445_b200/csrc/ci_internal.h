@@ -44,13 +44,11 @@ struct Model {
     std::vector<int> blk_first;              // first block index of each stage
     int64_t head_off[4] = {0, 0, 0, 0};
     float* d_head[4] = {nullptr, nullptr, nullptr, nullptr};  // 16-B aligned copy: W [C][d], then b [C]
-    int64_t max_hidden = 0;                  // max m*H*W over stages (SIMT scratch)
     int64_t enc_off = -1;                    // learned encoder params (float offset), -1 = none
     // tcgen05 path
-    uint16_t* d_wpack = nullptr;             // packed bf16 weights (hi [+ lo])
+    uint16_t* d_wpack = nullptr;             // packed bf16 / fp16 weights (k_umma.cu pack_block)
     float* d_bias = nullptr;                 // padded biases
     void* umma_state = nullptr;              // host-side stage plans (k_umma.cu)
-    bool umma = false;
     void* host_pipe = nullptr;               // streams/events of ci_serve_group_host (api.cu)
 };
 
@@ -106,5 +104,6 @@ ci_status_t umma_stage(const Model* m, int stage, float* state, int64_t n, bool 
 // Learned-encoder tail: zbuf [n][2*4c1][H/2][W/2]; channels [0,4c1) = psi(mean first layer) in,
 // channels [4c1, 8c1) = ReLU(E3(ReLU(E2 z))) out (tcgen05 stage kernel, fmode 1).
 ci_status_t umma_encoder_tail(const Model* m, float* zbuf, int64_t n, int* ctr, cudaStream_t s);
+bool umma_has_encoder(const Model* m);   // the encoder tail has a tcgen05 plan
 
 }  // namespace ci

@@ -21,8 +21,12 @@
 //    T M-tiles of the CTA.
 //  * Warp roles: warp 0 = producer, warp 1 = MMA issuer (one thread), warps 2..9 = epilogue
 //    (thread <-> TMEM lane <-> pixel row; two warps per lane quarter split the columns).
-//  * CI_PREC_FP32 ("bf16x3"): operands split x = hi + lo (bf16 each); 3 MMAs per k-step
-//    (hi*hi + hi*lo + lo*hi) into the same fp32 accumulator.
+//  * Precisions (StagePlan::pm): bf16 (CI_PREC_BF16: 1 MMA per k-step); f16x3 (CI_PREC_FP32:
+//    activations and weights split x = hi + lo in fp16, 22 significant bits each; 3 MMAs
+//    hi(x)W_hi + lo(x)W_hi + hi(x)W_lo into the same fp32 accumulator); f16x2 (CI_PREC_F16X2:
+//    weights rounded once to fp16, 2 MMAs).  Weight rounding is one fixed perturbation of h that
+//    every query sees (the coupling inverse and the decode stay exact for it); activation
+//    rounding is per-query noise that the decode amplifies k-fold.
 //  * Determinism: the k-step order per accumulator is fixed and independent of the tile or
 //    batch position, so forward and inverse compute bit-identical F for identical inputs.
 #include <stdio.h>
@@ -30,10 +34,12 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
 #include <vector>
 
 #include "ci_internal.h"
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include "codedinv_testing.h"
 #include "umma.cuh"
@@ -53,7 +59,7 @@ struct StagePlan {
     int pair;              // conv1 pair mode (Cp == 8)
     int tri;               // conv1 tri mode (Cp == 32, c == 24; a_off)
     int k1, k2;            // k-steps per chunk: conv1, conv2
-    int prec3;             // bf16x3
+    int pm;                // precision: 0 bf16, 1 f16x2 (fp32-parity), 2 f16x3 (fp32-parity, residual)
     int nslot, slot_bytes;
     int64_t blk_bytes;     // packed weight stream bytes per block
     size_t smem;
@@ -93,9 +99,10 @@ struct StageArgs {
 // ----------------------------------------------------------------------------------------
 // schedule helpers shared by producer / MMA (device) and packer (host)
 // ----------------------------------------------------------------------------------------
-__host__ __device__ inline int kstep_bytes(int N, int prec3) { return N * 32 * (prec3 ? 2 : 1); }
-__host__ __device__ inline int steps_per_slot(int N, int prec3, int slot_bytes) {
-    int g = slot_bytes / kstep_bytes(N, prec3);
+// one k-step of B: N x 16 operands of 2 bytes (bf16, or fp16), plus the fp16 lo tile in f16x3
+__host__ __device__ inline int kstep_bytes(int N, int pm) { return N * 32 * (pm == 2 ? 2 : 1); }
+__host__ __device__ inline int steps_per_slot(int N, int pm, int slot_bytes) {
+    int g = slot_bytes / kstep_bytes(N, pm);
     return g < 1 ? 1 : g;
 }
 
@@ -118,6 +125,14 @@ __device__ __forceinline__ uint32_t bf16x2_bits(float a, float b) {
     uint32_t r;
     asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
     return r;
+}
+// f16x2 precision: (a, b) -> packed fp16 hi = rn(a, b) and lo = rn(a - hi_a, b - hi_b), a in the
+// low halves; hi + lo carries 22 significant bits of each fp32 value
+__device__ __forceinline__ void f16x2_split(float a, float b, uint32_t& hi, uint32_t& lo) {
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(b), "f"(a));
+    const __half2 h = *reinterpret_cast<const __half2*>(&hi);
+    const float2 f = __half22float2(h);
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(b - f.y), "f"(a - f.x));
 }
 __device__ __forceinline__ float bf16_val(uint32_t b) {
     return __bfloat162float(__ushort_as_bfloat16((unsigned short)b));
@@ -183,7 +198,7 @@ __host__ __device__ constexpr AOff a_off(int s, int am, bool hstk, int per, int 
 //   alo0  : low descriptor word (start>>4 | LBO>>4 << 16) of the A buffer at row G, plane 0
 //   ringlo: low descriptor word of ring slot 0 with this segment's B LBO field
 // ----------------------------------------------------------------------------------------
-template <int K, int PER, int AM, int WP, int PLANE16, int G, int KB16, int T, int N, bool P3,
+template <int K, int PER, int AM, int WP, int PLANE16, int G, int KB16, int T, int N, int PM,
           int LOA16, int ACC0, int DSTRIDE, bool HSTK = false>
 __device__ __forceinline__ void issue_static(uint32_t tmem, uint32_t alo0, uint32_t ringlo, uint32_t slot16,
                                              uint32_t idesc, uint32_t acc_first, int& slot, uint32_t& phase,
@@ -212,10 +227,8 @@ __device__ __forceinline__ void issue_static(uint32_t tmem, uint32_t alo0, uint3
             const uint64_t bd = ((uint64_t)HI << 32) | b;
             const uint32_t d = tmem + (uint32_t)(ACC0 + t * DSTRIDE);
             mma_bf16(d, ad, bd, idesc, s == 0 ? acc_first : 1u);
-            if (P3) {
-                mma_bf16(d, ad, bd + (uint64_t)(N * 2), idesc, 1u);
-                mma_bf16(d, ad + (uint64_t)LOA16, bd, idesc, 1u);
-            }
+            if (PM >= 1) mma_bf16(d, ad + (uint64_t)LOA16, bd, idesc, 1u);          // lo(A) * B
+            if (PM == 2) mma_bf16(d, ad, bd + (uint64_t)(N * 2), idesc, 1u);          // hi(A) * lo(B)
         }
         if (s % G == G - 1 || s == K - 1) {
             commit(&empty[slot]);
@@ -228,7 +241,7 @@ __device__ __forceinline__ void issue_static(uint32_t tmem, uint32_t alo0, uint3
 // are resident (NS <= nslot), and tile t is issued as soon as the previous block's epilogue
 // has finished the X rows of tiles t-1..t+1 (x_tile[t+1]; arrivals are in tile order per
 // thread), so this chunk overlaps that epilogue instead of waiting for all of it.
-template <int K, int PER, int AM, int WP, int PLANE16, int G, int KB16, int T, int N, bool P3,
+template <int K, int PER, int AM, int WP, int PLANE16, int G, int KB16, int T, int N, int PM,
           int LOA16, int ACC0, int DSTRIDE>
 __device__ __forceinline__ void issue_static_tiles(uint32_t tmem, uint32_t alo0, uint32_t ringlo, uint32_t slot16,
                                                    uint32_t idesc, uint32_t acc_first, int& slot, uint32_t& phase,
@@ -260,10 +273,8 @@ __device__ __forceinline__ void issue_static_tiles(uint32_t tmem, uint32_t alo0,
             const uint64_t bd = ((uint64_t)HI << 32) | (bl[s / G] + (uint32_t)((s % G) * KB16));
             const uint32_t d = tmem + (uint32_t)(ACC0 + t * DSTRIDE);
             mma_bf16(d, ad, bd, idesc, s == 0 ? acc_first : 1u);
-            if (P3) {
-                mma_bf16(d, ad, bd + (uint64_t)(N * 2), idesc, 1u);
-                mma_bf16(d, ad + (uint64_t)LOA16, bd, idesc, 1u);
-            }
+            if (PM >= 1) mma_bf16(d, ad + (uint64_t)LOA16, bd, idesc, 1u);          // lo(A) * B
+            if (PM == 2) mma_bf16(d, ad, bd + (uint64_t)(N * 2), idesc, 1u);          // hi(A) * lo(B)
         }
     }
 #pragma unroll
@@ -277,7 +288,7 @@ __device__ __forceinline__ void issue_static_tiles(uint32_t tmem, uint32_t alo0,
 // tile t is issued once dep[min(t + AHEAD, T-1)] completes (the epilogue has produced what
 // tile t reads: X / hidden rows of tiles <= t+1, or acc1 tile t read), and -- when `done` is
 // given -- a per-tile commit lets the epilogue consume tile t while later tiles still run.
-template <int K, int PER, int AM, bool HSTK, int WP, int PLANE16, int G, int KB16, int T, int N, bool P3,
+template <int K, int PER, int AM, bool HSTK, int WP, int PLANE16, int G, int KB16, int T, int N, int PM,
           int LOA16, int ACC0, int DSTRIDE, int AHEAD>
 __device__ __forceinline__ void issue_stream(uint32_t tmem, uint32_t alo0, uint32_t ringlo, uint32_t slot16,
                                              uint32_t idesc, uint32_t acc_first, int& slot, uint32_t& phase,
@@ -309,10 +320,8 @@ __device__ __forceinline__ void issue_stream(uint32_t tmem, uint32_t alo0, uint3
             const uint64_t bd = ((uint64_t)HI << 32) | (bl[s / G] + (uint32_t)((s % G) * KB16));
             const uint32_t d = tmem + (uint32_t)(ACC0 + t * DSTRIDE);
             mma_bf16(d, ad, bd, idesc, s == 0 ? acc_first : 1u);
-            if (P3) {
-                mma_bf16(d, ad, bd + (uint64_t)(N * 2), idesc, 1u);
-                mma_bf16(d, ad + (uint64_t)LOA16, bd, idesc, 1u);
-            }
+            if (PM >= 1) mma_bf16(d, ad + (uint64_t)LOA16, bd, idesc, 1u);          // lo(A) * B
+            if (PM == 2) mma_bf16(d, ad, bd + (uint64_t)(N * 2), idesc, 1u);          // hi(A) * lo(B)
         }
         if (done) commit(&done[t]);
     }
@@ -335,7 +344,7 @@ __device__ __forceinline__ void acquire_slots(uint32_t (&bl)[NS], uint32_t ringl
         if (++slot == nslot) { slot = 0; phase ^= 1; }
     }
 }
-template <int K, int PER, int AM, bool HSTK, int WP, int PLANE16, int G, int KB16, int N, bool P3, int LOA16,
+template <int K, int PER, int AM, bool HSTK, int WP, int PLANE16, int G, int KB16, int N, int PM, int LOA16,
           int ACC0, int DSTRIDE, int NS>
 __device__ __forceinline__ void issue_tile(int t, uint32_t tmem, uint32_t alo0, const uint32_t (&bl)[NS],
                                            uint32_t idesc, uint32_t acc_first) {
@@ -348,15 +357,13 @@ __device__ __forceinline__ void issue_tile(int t, uint32_t tmem, uint32_t alo0, 
         const uint64_t bd = ((uint64_t)HI << 32) | (bl[s / G] + (uint32_t)((s % G) * KB16));
         const uint32_t d = tmem + (uint32_t)(ACC0 + t * DSTRIDE);
         mma_bf16(d, ad, bd, idesc, s == 0 ? acc_first : 1u);
-        if (P3) {
-            mma_bf16(d, ad, bd + (uint64_t)(N * 2), idesc, 1u);
-            mma_bf16(d, ad + (uint64_t)LOA16, bd, idesc, 1u);
-        }
+        if (PM >= 1) mma_bf16(d, ad + (uint64_t)LOA16, bd, idesc, 1u);          // lo(A) * B
+        if (PM == 2) mma_bf16(d, ad, bd + (uint64_t)(N * 2), idesc, 1u);          // hi(A) * lo(B)
     }
 }
 
 // Static stage configuration (0 = use the runtime plan)
-template <int WP_, int CP_, int MC_, int NC2_, int T_, int P3_, int SLOT_, int H_ = 0, int C_ = 0, int SST_ = 0,
+template <int WP_, int CP_, int MC_, int NC2_, int T_, int PM_, int SLOT_, int H_ = 0, int C_ = 0, int SST_ = 0,
           int HST_ = 0, int RES_ = 0>
 struct SCfg {
     static constexpr bool HST = HST_ != 0;
@@ -365,7 +372,8 @@ struct SCfg {
     static constexpr bool kStatic = WP_ > 0;
     static constexpr int WP = WP_, CP = CP_, MC = MC_, NC2 = NC2_, T = T_, SLOT = SLOT_;
     static constexpr int H = H_, W = WP_ - 1, C = C_, SST = SST_;
-    static constexpr bool P3 = P3_ != 0;
+    static constexpr int PM = PM_;            // StagePlan::pm
+    static constexpr bool P3 = PM_ != 0;      // activations split into fp16 hi + lo planes
     static constexpr int G = WP + 2;
     static constexpr int RTOT = T * 128 + 2 * G;
     static constexpr int PLANE16 = RTOT;                 // plane bytes / 16
@@ -379,7 +387,7 @@ struct SCfg {
     static constexpr int K1 = PAIR ? kPairK1 : (TRI ? kTriK1 : 9 * (CP / 16));
     static constexpr int PER2 = MC / 16;
     static constexpr int K2 = (HST ? 3 : 9) * (MC / 16);
-    static constexpr int KB1 = MC * 32 * (P3 ? 2 : 1), KB2 = NC2 * 32 * (P3 ? 2 : 1);
+    static constexpr int KB1 = MC * 32 * (PM == 2 ? 2 : 1), KB2 = NC2 * 32 * (PM == 2 ? 2 : 1);
     static constexpr int G1 = (SLOT / (KB1 > 0 ? KB1 : 1)) < 1 ? 1 : SLOT / (KB1 > 0 ? KB1 : 1);
     static constexpr int G2 = (SLOT / (KB2 > 0 ? KB2 : 1)) < 1 ? 1 : SLOT / (KB2 > 0 ? KB2 : 1);
     static constexpr int ACC1 = T * NC2;
@@ -431,9 +439,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
     const StagePlan& p = a.p;
     extern __shared__ __align__(1024) uint8_t smem[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int P = p.prec3 ? 2 : 1;
+    const int P = p.pm ? 2 : 1;
     // precision known at compile time for the static configurations
-    const bool kP3 = CFG::kStatic ? CFG::P3 : (p.prec3 != 0);
+    const bool kP3 = CFG::kStatic ? CFG::P3 : (p.pm != 0);
 
     // ---- shared memory carve-up
     uint8_t* ring = smem;                                           // nslot * slot_bytes
@@ -536,8 +544,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             seg_of(q, p.nch, seg, jj);
                             int N = seg == 0 ? p.MC : p.Nc2;
                             int K = seg == 0 ? p.k1 : p.k2;
-                            int g = steps_per_slot(N, p.prec3, p.slot_bytes);
-                            int kb = kstep_bytes(N, p.prec3);
+                            int g = steps_per_slot(N, p.pm, p.slot_bytes);
+                            int kb = kstep_bytes(N, p.pm);
                             for (int s0 = 0; s0 < K; s0 += g) {
                                 int cnt = min(g, K - s0);
                                 uint32_t bytes = (uint32_t)(cnt * kb);
@@ -568,15 +576,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
             uint32_t a1fph = 0;                      // STREAM: phase of a1f[*]
             const uint32_t xb = smem_u32(xbuf) + (uint32_t)p.G * 16;
             const uint32_t hb = smem_u32(hbuf) + (uint32_t)p.G * 16;
-            const uint32_t xlo_b = (uint32_t)(p.Cp / 8) * plane_bytes;   // lo planes (prec3)
+            const uint32_t xlo_b = (uint32_t)(p.Cp / 8) * plane_bytes;   // lo planes (f16x2 / f16x3)
             const uint32_t hlo_b = (uint32_t)(p.MC / 8) * plane_bytes;
             (void)hlo_b;
-            const uint32_t id1 = idesc_bf16(128, p.MC), id2 = idesc_bf16(128, p.Nc2);
+            const uint32_t id1 = idesc_of(128, p.MC, kP3), id2 = idesc_of(128, p.Nc2, kP3);
             const uint32_t rb = smem_u32(ring);
             const uint32_t lbo1 = p.pair ? 16u : plane_bytes;
-            const int g1 = steps_per_slot(p.MC, p.prec3, p.slot_bytes);
-            const int g2 = steps_per_slot(p.Nc2, p.prec3, p.slot_bytes);
-            const uint32_t kb1 = (uint32_t)kstep_bytes(p.MC, p.prec3), kb2 = (uint32_t)kstep_bytes(p.Nc2, p.prec3);
+            const int g1 = steps_per_slot(p.MC, p.pm, p.slot_bytes);
+            const int g2 = steps_per_slot(p.Nc2, p.pm, p.slot_bytes);
+            const uint32_t kb1 = (uint32_t)kstep_bytes(p.MC, p.pm), kb2 = (uint32_t)kstep_bytes(p.Nc2, p.pm);
             const int per1 = p.pair ? 2 : p.Cp / 16;   // k-steps per kernel row u (pair) / per tap
             const int per2 = p.MC / 16;
             unsigned long long w_x = 0, w_full = 0, w_hd = 0, t_start = CLK();
@@ -591,7 +599,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             const uint32_t alo0 = ((xb >> 4) & 0x3FFFu) | ((LBO1 >> 4) << 16);
                             const uint32_t ringlo = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::MC * 16 >> 4) << 16);
                             issue_static<CFG::K1, CFG::PER1, CFG::AM1, CFG::WP, CFG::PLANE16, CFG::G1, CFG::KB1 / 16,
-                                         CFG::T, CFG::MC, CFG::P3, CFG::LOX16, CFG::ACC1, CFG::MC>(
+                                         CFG::T, CFG::MC, CFG::PM, CFG::LOX16, CFG::ACC1, CFG::MC>(
                                 tmem, alo0, ringlo, (uint32_t)CFG::SLOT / 16u, id1, CFG::FOLD ? 0u : 1u, slot, phase,
                                 p.nslot, full, empty);
                         } else
@@ -624,12 +632,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                     const uint32_t d = tmem + acc1_col0 + (uint32_t)(tile * p.MC);
                                     const uint32_t at = aaddr + (uint32_t)tile * 2048u;
                                     mma_bf16(d, smem_desc(at, lbo, 128), smem_desc(baddr, (uint32_t)p.MC * 16u, 128), id1, acc);
-                                    if (p.prec3) {
-                                        mma_bf16(d, smem_desc(at, lbo, 128),
-                                                 smem_desc(baddr + (uint32_t)p.MC * 32u, (uint32_t)p.MC * 16u, 128), id1, 1);
+                                    if (p.pm)        // lo(A) * B
                                         mma_bf16(d, smem_desc(at + xlo_b, lbo, 128),
                                                  smem_desc(baddr, (uint32_t)p.MC * 16u, 128), id1, 1);
-                                    }
+                                    if (p.pm == 2)   // hi(A) * lo(B)
+                                        mma_bf16(d, smem_desc(at, lbo, 128),
+                                                 smem_desc(baddr + (uint32_t)p.MC * 32u, (uint32_t)p.MC * 16u, 128), id1, 1);
                                 }
                                 if (++kc == per1) { kc = 0; ++tap; }
                                 if (++q == g1 || s + 1 == p.k1) {
@@ -647,7 +655,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             const uint32_t alo0 = ((hbj >> 4) & 0x3FFFu) | ((LBO2 >> 4) << 16);
                             const uint32_t ringlo = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::NC2 * 16 >> 4) << 16);
                             issue_static<CFG::K2, CFG::PER2, false, CFG::WP, CFG::PLANE16, CFG::G2, CFG::KB2 / 16,
-                                         CFG::T, CFG::NC2, CFG::P3, CFG::LOH16, 0, CFG::NC2, CFG::HST>(
+                                         CFG::T, CFG::NC2, CFG::PM, CFG::LOH16, 0, CFG::NC2, CFG::HST>(
                                 tmem, alo0, ringlo, (uint32_t)CFG::SLOT / 16u, id2, 1u, slot, phase,
                                 p.nslot, full, empty);
                         } else
@@ -666,12 +674,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                     const uint32_t d = tmem + (uint32_t)(tile * p.Nc2);
                                     const uint32_t at = aaddr + (uint32_t)tile * 2048u;
                                     mma_bf16(d, smem_desc(at, plane_bytes, 128), smem_desc(baddr, (uint32_t)p.Nc2 * 16u, 128), id2, acc);
-                                    if (p.prec3) {
-                                        mma_bf16(d, smem_desc(at, plane_bytes, 128),
-                                                 smem_desc(baddr + (uint32_t)p.Nc2 * 32u, (uint32_t)p.Nc2 * 16u, 128), id2, 1);
+                                    if (p.pm)        // lo(A) * B
                                         mma_bf16(d, smem_desc(at + hlo_b, plane_bytes, 128),
                                                  smem_desc(baddr, (uint32_t)p.Nc2 * 16u, 128), id2, 1);
-                                    }
+                                    if (p.pm == 2)   // hi(A) * lo(B)
+                                        mma_bf16(d, smem_desc(at, plane_bytes, 128),
+                                                 smem_desc(baddr + (uint32_t)p.Nc2 * 32u, (uint32_t)p.Nc2 * 16u, 128), id2, 1);
                                 }
                                 if (++kc == per2) { kc = 0; ++tap; }
                                 if (++q == g2 || s + 1 == p.k2) {
@@ -693,7 +701,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                         const uint32_t ring2 = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::NC2 * 16 >> 4) << 16);
                         long long tx0 = CLK();
                         issue_stream<CFG::K1, CFG::PER1, CFG::AM1, false, CFG::WP, CFG::PLANE16, CFG::G1, CFG::KB1 / 16,
-                                     CFG::T, CFG::MC, CFG::P3, CFG::LOX16, CFG::ACC1, CFG::MC, 1>(
+                                     CFG::T, CFG::MC, CFG::PM, CFG::LOX16, CFG::ACC1, CFG::MC, 1>(
                             tmem, alo1, ring1, (uint32_t)CFG::SLOT / 16u, id1, 0u, slot, phase, p.nslot, full, empty,
                             x_tile, xph, a1t);
                         if (kCycles && a.dbg) w_x += (unsigned long long)(CLK() - tx0);
@@ -721,7 +729,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                         TWAIT(w_hd, mbar_wait(&a1f[t], a1fph));
                                         fence_after();
                                         issue_tile<CFG::K1, CFG::PER1, CFG::AM1, false, CFG::WP, CFG::PLANE16, CFG::G1,
-                                                   CFG::KB1 / 16, CFG::MC, CFG::P3, CFG::LOX16, CFG::ACC1, CFG::MC, NS1>(
+                                                   CFG::KB1 / 16, CFG::MC, CFG::PM, CFG::LOX16, CFG::ACC1, CFG::MC, NS1>(
                                             t, tmem, alo1, bl1, id1, 0u);
                                         commit(&a1t[t]);
                                     }
@@ -729,7 +737,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                         TWAIT(w_hd, mbar_wait(&hdt_j[t < CFG::T ? t : CFG::T - 1], hdph));
                                         fence_after();
                                         issue_tile<CFG::K2, CFG::PER2, false, CFG::HST, CFG::WP, CFG::PLANE16, CFG::G2,
-                                                   CFG::KB2 / 16, CFG::NC2, CFG::P3, CFG::LOH16, 0, CFG::NC2, NS2>(
+                                                   CFG::KB2 / 16, CFG::NC2, CFG::PM, CFG::LOH16, 0, CFG::NC2, NS2>(
                                             t - 1, tmem, alo2, bl2, id2, 1u);
                                     }
                                 }
@@ -745,7 +753,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             }
                             if (j + 1 < p.nch) {
                                 issue_stream<CFG::K1, CFG::PER1, CFG::AM1, false, CFG::WP, CFG::PLANE16, CFG::G1,
-                                             CFG::KB1 / 16, CFG::T, CFG::MC, CFG::P3, CFG::LOX16, CFG::ACC1, CFG::MC, 0>(
+                                             CFG::KB1 / 16, CFG::T, CFG::MC, CFG::PM, CFG::LOX16, CFG::ACC1, CFG::MC, 0>(
                                     tmem, alo1, ring1, (uint32_t)CFG::SLOT / 16u, id1, 0u, slot, phase, p.nslot, full,
                                     empty, a1f, a1fph, a1t);
                                 a1fph ^= 1;
@@ -754,7 +762,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             const uint32_t alo2 = ((hbj >> 4) & 0x3FFFu) | ((LBO2 >> 4) << 16);
                             long long th0 = CLK();
                             issue_stream<CFG::K2, CFG::PER2, false, CFG::HST, CFG::WP, CFG::PLANE16, CFG::G2, CFG::KB2 / 16,
-                                         CFG::T, CFG::NC2, CFG::P3, CFG::LOH16, 0, CFG::NC2, 1>(
+                                         CFG::T, CFG::NC2, CFG::PM, CFG::LOH16, 0, CFG::NC2, 1>(
                                 tmem, alo2, ring2, (uint32_t)CFG::SLOT / 16u, id2, 1u, slot, phase, p.nslot, full,
                                 empty, hdt + hbi * kMaxTiles, (hph >> hbi) & 1u, j + 1 == p.nch ? a2t : nullptr);
                             if (kCycles && a.dbg) w_hd += (unsigned long long)(CLK() - th0);
@@ -775,7 +783,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             const uint32_t ringlo = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::MC * 16 >> 4) << 16);
                             long long tx0 = CLK();
                             issue_static_tiles<CFG::K1, CFG::PER1, CFG::AM1, CFG::WP, CFG::PLANE16, CFG::G1,
-                                               CFG::KB1 / 16, CFG::T, CFG::MC, CFG::P3, CFG::LOX16, CFG::ACC1, CFG::MC>(
+                                               CFG::KB1 / 16, CFG::T, CFG::MC, CFG::PM, CFG::LOX16, CFG::ACC1, CFG::MC>(
                                 tmem, alo0, ringlo, (uint32_t)CFG::SLOT / 16u, id1, CFG::FOLD ? 0u : 1u, slot, phase,
                                 p.nslot, full, empty, x_tile, xph);
                             if (kCycles && a.dbg) w_x += (unsigned long long)(CLK() - tx0);
@@ -854,29 +862,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
             return yy != 0 && x < eW;
         };
         // 4 channels (8 bytes) at channel offset sub*4 of a plane row (balanced conv2 split)
+        // bf16 precision: one bf16 plane.  f16x2 (kP3): fp16 hi plane + fp16 lo plane, x = hi + lo
         auto store4 = [&](uint8_t* base_hi, uint8_t* base_lo, int plane, int sub, int r, const float* v4) {
             size_t off = (size_t)plane * plane_bytes + (size_t)(r + eG) * 16 + (size_t)sub * 8;
-            const uint32_t h0 = bf16x2_bits(v4[0], v4[1]), h1 = bf16x2_bits(v4[2], v4[3]);
-            *reinterpret_cast<uint2*>(base_hi + off) = make_uint2(h0, h1);
             if (kP3) {
-                const uint32_t l0 = bf16x2_bits(v4[0] - __uint_as_float(h0 << 16), v4[1] - __uint_as_float(h0 & 0xFFFF0000u));
-                const uint32_t l1 = bf16x2_bits(v4[2] - __uint_as_float(h1 << 16), v4[3] - __uint_as_float(h1 & 0xFFFF0000u));
-                *reinterpret_cast<uint2*>(base_lo + off) = make_uint2(l0, l1);
+                uint32_t h[2], l[2];
+                f16x2_split(v4[0], v4[1], h[0], l[0]);
+                f16x2_split(v4[2], v4[3], h[1], l[1]);
+                *reinterpret_cast<uint2*>(base_hi + off) = make_uint2(h[0], h[1]);
+                *reinterpret_cast<uint2*>(base_lo + off) = make_uint2(l[0], l[1]);
+            } else {
+                *reinterpret_cast<uint2*>(base_hi + off) = make_uint2(bf16x2_bits(v4[0], v4[1]), bf16x2_bits(v4[2], v4[3]));
             }
         };
         auto store8 = [&](uint8_t* base_hi, uint8_t* base_lo, int plane, int r, const float* v8) {
             size_t off = (size_t)plane * plane_bytes + (size_t)(r + eG) * 16;
-            uint32_t hi[4];
-#pragma unroll
-            for (int e = 0; e < 4; e++) hi[e] = bf16x2_bits(v8[2 * e], v8[2 * e + 1]);
-            *reinterpret_cast<uint4*>(base_hi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
             if (kP3) {
-                uint32_t lo[4];
+                uint32_t hi[4], lo[4];
 #pragma unroll
-                for (int e = 0; e < 4; e++)
-                    lo[e] = bf16x2_bits(v8[2 * e] - __uint_as_float(hi[e] << 16),
-                                        v8[2 * e + 1] - __uint_as_float(hi[e] & 0xFFFF0000u));
+                for (int e = 0; e < 4; e++) f16x2_split(v8[2 * e], v8[2 * e + 1], hi[e], lo[e]);
+                *reinterpret_cast<uint4*>(base_hi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
                 *reinterpret_cast<uint4*>(base_lo + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+            } else {
+                uint32_t hi[4];
+#pragma unroll
+                for (int e = 0; e < 4; e++) hi[e] = bf16x2_bits(v8[2 * e], v8[2 * e + 1]);
+                *reinterpret_cast<uint4*>(base_hi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
             }
         };
         // hst warp-boundary exchange: 8 floats as two 16-B shared accesses (the buffer is 16-B
@@ -1779,6 +1790,31 @@ static uint16_t f2bf(float f) {  // round-to-nearest-even, no NaN inputs
     u += 0x7FFFu + ((u >> 16) & 1u);
     return (uint16_t)(u >> 16);
 }
+// fp32 -> fp16 bits, round-to-nearest-even incl. subnormals (finite inputs; |f| >= 65520 -> inf)
+static uint16_t f2h(float f) {
+    uint32_t x;
+    memcpy(&x, &f, 4);
+    const uint32_t sign = (x >> 16) & 0x8000u, ax = x & 0x7FFFFFFFu;
+    if (ax >= 0x477FF000u) return (uint16_t)(sign | 0x7C00u);
+    if (ax < 0x38800000u) {   // below 2^-14: fp16 subnormal (or zero), units of 2^-24
+        float v;
+        memcpy(&v, &ax, 4);
+        return (uint16_t)(sign | (uint32_t)nearbyintf(v * 16777216.0f));
+    }
+    const uint32_t r = ax - 0x38000000u;   // exponent rebias 127 -> 15
+    return (uint16_t)(sign | ((r + 0xFFFu + ((r >> 13) & 1u)) >> 13));
+}
+static float h2f(uint16_t h) {
+    const uint32_t sign = (uint32_t)(h & 0x8000u) << 16, e = (h >> 10) & 0x1Fu, mant = h & 0x3FFu;
+    float v;
+    if (e == 0) v = (float)mant * (1.0f / 16777216.0f);                  // subnormal: mant * 2^-24
+    else { const uint32_t u = ((e + 112u) << 23) | (mant << 13); memcpy(&v, &u, 4); }
+    uint32_t u;
+    memcpy(&u, &v, 4);
+    u |= sign;
+    memcpy(&v, &u, 4);
+    return v;
+}
 static float bf2f(uint16_t b) {
     uint32_t u = (uint32_t)b << 16;
     float f;
@@ -1792,7 +1828,7 @@ static const size_t kSmemCap = 227 * 1024;
 static double mma_cyc(int N) { return std::max(N / 2.0, 32.0 + N / 4.0); }
 
 // Cost model (cycles per image per block), calibrated on B200 with CI_DEBUG_CYCLES:
-//   MMA: k-steps x tiles x mma_cyc(N) (x3 for bf16x3)
+//   MMA: k-steps x tiles x mma_cyc(N) (x2 for f16x2)
 //   epilogue-1 per tile per chunk ~ 100 + 15 * (MC/2) columns per thread
 //   epilogue-2 per tile ~ 300 + 60 * (Nc2/2) (global fp32 state) / 200 + 40 * (Nc2/2) (smem state)
 //   nhd = 2 overlaps epilogue-1 of chunk j+1 with conv2 of chunk j
@@ -1800,7 +1836,7 @@ static double mma_cyc(int N) { return std::max(N / 2.0, 32.0 + N / 4.0); }
 //   a 2-slot ring cannot hide the L2 latency of the weight stream (x1.3)
 // Tuned plans for the Arch-C stage shapes (chosen from CI_DEBUG_CYCLES measurements);
 // other shapes use the cost model.
-struct TunedPlan { int H, W, c, m, prec3, MC, T, nhd, nslot, hst; };
+struct TunedPlan { int H, W, c, m, pm, MC, T, nhd, nslot, hst; };
 static const TunedPlan kTuned[] = {
     {16, 16, 6, 64, 0, 32, 7, 2, 3, 1},    // stage 1 bf16: SMEM-resident state fits
     {8, 8, 24, 128, 0, 128, 2, 1, 3, 1},   // stage 2 bf16: wide hst (N = 3 x 24 -> 80), one N = 128 conv1 chunk, T = 2
@@ -1808,25 +1844,32 @@ static const TunedPlan kTuned[] = {
     {8, 8, 24, 128, 0, 32, 4, 2, 3, 1},    // stage 2 bf16: wide hst, N = 32 conv1, T = 4 (CI_S1_MC32)
     {8, 8, 24, 128, 0, 32, 7, 2, 3, 0},    // stage 2 bf16, plain conv2 (CI_NO_WIDE_HST)
     {4, 4, 96, 256, 0, 128, 2, 1, 4, 0},   // stage 3 bf16
-    {16, 16, 6, 64, 1, 16, 7, 2, 4, 1},    // stage 1 bf16x3
-    {8, 8, 24, 128, 1, 64, 3, 1, 3, 1},    // stage 2 bf16x3: wide hst
-    {8, 8, 24, 128, 1, 128, 2, 1, 3, 0},   // stage 2 bf16x3, plain conv2 (CI_NO_WIDE_HST)
-    {4, 4, 96, 256, 1, 64, 2, 1, 3, 0},    // stage 3 bf16x3
+    // split-activation precisions (f16x2, f16x3: two SMEM planes per 8 channels): the cost
+    // model's picks, measured 18-22% per stage faster than the round-1 bf16x3 plans (MC = 16 /
+    // 64 / 64) -- MMA count, not SMEM, bounds these stages
+    {16, 16, 6, 64, 1, 32, 5, 1, 4, 1},    // stage 1 f16x2: MC = 32, T = 5, SMEM state
+    {8, 8, 24, 128, 1, 128, 2, 1, 3, 1},   // stage 2 f16x2: wide hst, one N = 128 conv1 chunk
+    {4, 4, 96, 256, 1, 128, 1, 1, 4, 0},   // stage 3 f16x2: N = 128 conv1 chunks, T = 1
+    {16, 16, 6, 64, 2, 32, 5, 1, 4, 1},    // stage 1 f16x3
+    {8, 8, 24, 128, 2, 128, 2, 1, 3, 1},   // stage 2 f16x3
+    {4, 4, 96, 256, 2, 128, 1, 1, 4, 0},   // stage 3 f16x3
     {16, 16, 12, 64, 0, 32, 5, 2, 4, 1},   // CR (residual, f1) stage 1 bf16: wide hst (N = 48)
     {16, 16, 12, 64, 0, 64, 5, 1, 4, 0},   // CR stage 1 bf16, plain conv2 (CI_NO_WIDE_HST)
-    {16, 16, 12, 64, 1, 32, 7, 1, 3, 0},   // CR stage 1 bf16x3
+    {16, 16, 12, 64, 2, 32, 7, 1, 3, 0},   // CR stage 1 f16x3
 };
 
-static bool make_plan(const StageInfo& S, bool prec3, StagePlan& best) {
+static bool make_plan(const StageInfo& S, int pm, StagePlan& best) {
     StagePlan p{};
     static const bool no_wide_hst = getenv("CI_NO_WIDE_HST") != nullptr;   // A/B switch
     static const bool s1_mc32 = getenv("CI_S1_MC32") != nullptr;           // A/B switch
     static const bool s1_mc64 = getenv("CI_S1_MC64") != nullptr;           // A/B switch
+    static const bool no_tuned = getenv("CI_NO_TUNED") != nullptr;         // A/B switch: cost model only
     const TunedPlan* tuned = nullptr;
+    if (!no_tuned)
     for (const auto& tp : kTuned)   // first match wins
-        if (!tuned && tp.H == S.H && tp.W == S.W && tp.c == S.c && tp.m == S.m && tp.prec3 == (prec3 ? 1 : 0) &&
-            !(no_wide_hst && tp.hst && tp.c > 8) && !(tp.c == 24 && !tp.prec3 && tp.MC == 64 && tp.hst && s1_mc32) &&
-            !(tp.c == 24 && !tp.prec3 && tp.MC == 128 && tp.hst && (s1_mc64 || s1_mc32)))
+        if (!tuned && tp.H == S.H && tp.W == S.W && tp.c == S.c && tp.m == S.m && tp.pm == pm &&
+            !(no_wide_hst && tp.hst && tp.c > 8) && !(tp.c == 24 && !tp.pm && tp.MC == 64 && tp.hst && s1_mc32) &&
+            !(tp.c == 24 && !tp.pm && tp.MC == 128 && tp.hst && (s1_mc64 || s1_mc32)))
             tuned = &tp;
     p.H = S.H; p.W = S.W; p.Wp = S.W + 1; p.G = p.Wp + 2;
     p.c = S.c; p.m = S.m;
@@ -1835,9 +1878,9 @@ static bool make_plan(const StageInfo& S, bool prec3, StagePlan& best) {
     p.fold = p.Cp > S.c ? 1 : 0;
     p.pair = p.Cp == 8;
     p.tri = p.Cp == 32 && S.c == 24;
-    p.prec3 = prec3 ? 1 : 0;
-    const int P = prec3 ? 2 : 1;
-    const double P3f = prec3 ? 3.0 : 1.0;
+    p.pm = pm;
+    const int P = pm ? 2 : 1;
+    const double P3f = 1.0 + pm;   // MMAs per k-step: f16x2 hi(A)*B + lo(A)*B, f16x3 + hi(A)*lo(B)
     const int img_rows = (p.H + 1) * p.Wp;
     const int k1 = p.pair ? kPairK1 : (p.tri ? kTriK1 : 9 * (p.Cp / 16));
     double best_cost = 1e300;
@@ -1866,7 +1909,7 @@ static bool make_plan(const StageInfo& S, bool prec3, StagePlan& best) {
                 if (tuned && nhd != tuned->nhd) continue;
                 for (int nslot = 4; nslot >= 2; nslot--) {
                     if (tuned && nslot != tuned->nslot) continue;
-                    const int slot_bytes = std::max(16384, std::max(kstep_bytes(MC, prec3), kstep_bytes(p.Nc2, prec3)));
+                    const int slot_bytes = std::max(16384, std::max(kstep_bytes(MC, pm), kstep_bytes(p.Nc2, pm)));
                     const int Rtot = T * 128 + 2 * p.G;
                     const int xchg = p.hst ? T * 4 * 2 * p.hc * 4 : 0;
                     const size_t smem0 = (size_t)nslot * slot_bytes + (size_t)P * ((p.Cp + nhd * MC) / 8) * Rtot * 16 +
@@ -1878,10 +1921,10 @@ static bool make_plan(const StageInfo& S, bool prec3, StagePlan& best) {
                     // ---- cost per batch per block
                     const double mma1 = (double)nch * k1 * T * mma_cyc(MC) * P3f;
                     const double mma2 = (double)nch * k2 * T * mma_cyc(p.Nc2) * P3f;
-                    const double e1c = T * (100.0 + 15.0 * (MC / 2)) * (prec3 ? 1.3 : 1.0);   // per chunk
+                    const double e1c = T * (100.0 + 15.0 * (MC / 2)) * (pm ? 1.3 : 1.0);   // per chunk
                     const double e2 = T * (sst ? 200.0 + 40.0 * (p.Nc2 / 2) : 300.0 + 60.0 * (p.Nc2 / 2));
                     double t = nhd == 2 ? std::max(mma1 + mma2, nch * e1c) + e1c + e2 : mma1 + mma2 + nch * e1c + e2;
-                    const double wbytes = (double)nch * (k1 * kstep_bytes(MC, prec3) + k2 * kstep_bytes(p.Nc2, prec3));
+                    const double wbytes = (double)nch * (k1 * kstep_bytes(MC, pm) + k2 * kstep_bytes(p.Nc2, pm));
                     t = std::max(t, wbytes / 40.0);
                     if (nslot < 3) t *= 1.3;
                     const double cost = t / I;
@@ -1917,20 +1960,23 @@ static int conv2_col_channel(const StagePlan& p, int n) {
     return e < hc ? hh * hc + e : -1;
 }
 
-// one k-step B tile: [khalf][n][8] bf16 (hi), then the lo tile when prec3
-static void put_tile(std::vector<uint16_t>& out, const std::vector<float>& w, int N, bool prec3) {
+// one k-step B tile: [khalf][n][8], bf16 (CI_PREC_BF16) or fp16 (f16x2: the weights are rounded
+// once to fp16, a fixed perturbation of h that every query sees alike -- DESIGN.md 5)
+// f16x3 (residual archs) appends the fp16 lo tile w - hi)
+static void put_tile(std::vector<uint16_t>& out, const std::vector<float>& w, int N, int pm) {
     // w is [N][16] (n, kk)
-    for (int part = 0; part < (prec3 ? 2 : 1); part++)
+    for (int part = 0; part < (pm == 2 ? 2 : 1); part++)
         for (int kh = 0; kh < 2; kh++)
             for (int n = 0; n < N; n++)
                 for (int e = 0; e < 8; e++) {
-                    float v = w[(size_t)n * 16 + kh * 8 + e];
-                    uint16_t hi = f2bf(v);
-                    out.push_back(part == 0 ? hi : f2bf(v - bf2f(hi)));
+                    const float v = w[(size_t)n * 16 + kh * 8 + e];
+                    if (pm == 0) { out.push_back(f2bf(v)); continue; }
+                    const uint16_t hi = f2h(v);
+                    out.push_back(part == 0 ? hi : f2h(v - h2f(hi)));
                 }
 }
 
-static void pack_block(const StagePlan& p, const float* W1, const float* b1, const float* W2, bool prec3,
+static void pack_block(const StagePlan& p, const float* W1, const float* b1, const float* W2, int pm,
                        std::vector<uint16_t>& out) {
     const int c = p.c, m = p.m;
     auto w1 = [&](int h, int ci, int u, int v) -> float {  // u, v in -1..1
@@ -1975,7 +2021,7 @@ static void pack_block(const StagePlan& p, const float* W1, const float* b1, con
                     tile[(size_t)n * 16 + kk] = v;
                 }
             }
-            put_tile(out, tile, p.MC, prec3);
+            put_tile(out, tile, p.MC, pm);
         }
         // conv2 chunk j: N = Nc2 outputs, K = this chunk's hidden channels
         if (is2)
@@ -1990,7 +2036,7 @@ static void pack_block(const StagePlan& p, const float* W1, const float* b1, con
                     else
                         tile[(size_t)n * 16 + kk] = w2(conv2_col_channel(p, n), h, tap / 3 - 1, tap % 3 - 1);
                 }
-            put_tile(out, tile, p.Nc2, prec3);
+            put_tile(out, tile, p.Nc2, pm);
         }
     }
 }
@@ -2008,8 +2054,8 @@ struct UmmaState {
 // ---- compile-time specialisations for the Arch-C stage plans (see make_plan) -----------------
 typedef void (*StageKernel)(StageArgs);
 struct SpecEntry { int Wp, Cp, MC, Nc2, T, p3, slot, H, c, sst, hst, fold, split, res; StageKernel fn; };
-#define CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES) \
-    SCfg<WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES>
+#define CI_SPEC_CFG(WP, CP, MC, NC2, T, PM, SLOT, H, C, SST, HST, RES) \
+    SCfg<WP, CP, MC, NC2, T, PM, SLOT, H, C, SST, HST, RES>
 #define CI_SPEC_X(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES)                                          \
     {WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST,                                                         \
      CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES)::FOLD,                                  \
@@ -2026,20 +2072,22 @@ static const SpecEntry kSpecs[] = {
     CI_SPEC_X(9, 32, 64, 80, 3, 0, 16384, 8, 24, 1, 1, 0),   // C stage 2, bf16, wide hst, N = 64 conv1
     CI_SPEC_X(9, 32, 128, 80, 2, 0, 16384, 8, 24, 1, 1, 0),  // C stage 2, bf16, wide hst, N = 128 conv1
     CI_SPEC(5, 96, 128, 96, 2, 0, 16384, 4, 96, 0),  // C stage 3, bf16
-    CI_SPEC(17, 8, 16, 32, 7, 1, 16384, 16, 6, 0),   // C stage 1, bf16x3 (hst)
-    CI_SPEC(9, 32, 128, 32, 2, 1, 16384, 8, 24, 0),  // C stage 2, bf16x3 (plain conv2)
-    CI_SPEC_X(9, 32, 64, 80, 3, 1, 16384, 8, 24, 0, 1, 0),   // C stage 2, bf16x3, wide hst
-    CI_SPEC(5, 96, 64, 96, 2, 1, 16384, 4, 96, 0),   // C stage 3, bf16x3
+    CI_SPEC(17, 8, 32, 32, 5, 1, 16384, 16, 6, 1),   // C stage 1, f16x2, MC = 32, T = 5, SMEM state
+    CI_SPEC_X(9, 32, 128, 80, 2, 1, 16384, 8, 24, 0, 1, 0),  // C stage 2, f16x2, wide hst, N = 128 conv1
+    CI_SPEC(5, 96, 128, 96, 1, 1, 16384, 4, 96, 0),  // C stage 3, f16x2, N = 128 conv1, T = 1
+    CI_SPEC(17, 8, 32, 32, 5, 2, 16384, 16, 6, 1),   // C stage 1, f16x3 (CI_PREC_FP32)
+    CI_SPEC_X(9, 32, 128, 80, 2, 2, 16384, 8, 24, 0, 1, 0),  // C stage 2, f16x3
+    CI_SPEC(5, 96, 128, 96, 1, 2, 16384, 4, 96, 0),  // C stage 3, f16x3
     CI_SPEC(17, 64, 32, 64, 5, 0, 16384, 16, 64, 0),  // learned-encoder tail (E2, E3), bf16
-    CI_SPEC(17, 64, 32, 64, 3, 1, 16384, 16, 64, 0),  // learned-encoder tail (E2, E3), bf16x3
+    CI_SPEC(17, 64, 32, 64, 3, 2, 16384, 16, 64, 0),  // learned-encoder tail (E2, E3), f16x3
     // i-ResNet variant of Arch C (f1, config C3R): residual blocks on 12 / 48 / 192 channels
     CI_SPEC_R(17, 16, 64, 16, 5, 0, 16384, 16, 12, 1),    // CR stage 1, bf16 (plain conv2)
     CI_SPEC_X(17, 16, 32, 48, 5, 0, 16384, 16, 12, 1, 1, 1),   // CR stage 1, bf16, wide hst
     CI_SPEC_R(9, 48, 128, 48, 2, 0, 16384, 8, 48, 1),     // CR stage 2, bf16
     CI_SPEC_R(5, 192, 64, 192, 2, 0, 16384, 4, 192, 0),   // CR stage 3, bf16
-    CI_SPEC_R(17, 16, 32, 16, 7, 1, 16384, 16, 12, 0),    // CR stage 1, bf16x3
-    CI_SPEC_R(9, 48, 64, 48, 2, 1, 16384, 8, 48, 1),      // CR stage 2, bf16x3
-    CI_SPEC_R(5, 192, 128, 192, 1, 1, 16384, 4, 192, 0),  // CR stage 3, bf16x3
+    CI_SPEC_R(17, 16, 32, 16, 7, 2, 16384, 16, 12, 0),    // CR stage 1, f16x3
+    CI_SPEC_R(9, 48, 64, 48, 2, 2, 16384, 8, 48, 1),      // CR stage 2, f16x3
+    CI_SPEC_R(5, 192, 128, 192, 1, 2, 16384, 4, 192, 0),  // CR stage 3, f16x3
 };
 
 // Coupling specialisations carry no residual / ELU code (it would cost them registers); residual
@@ -2047,7 +2095,7 @@ static const SpecEntry kSpecs[] = {
 static StageKernel pick_kernel(const StagePlan& p, const StageArgs& a) {
     if (!getenv("CI_NO_STATIC"))
         for (const auto& e : kSpecs)
-            if (e.Wp == p.Wp && e.Cp == p.Cp && e.MC == p.MC && e.Nc2 == p.Nc2 && e.T == p.T && e.p3 == p.prec3 &&
+            if (e.Wp == p.Wp && e.Cp == p.Cp && e.MC == p.MC && e.Nc2 == p.Nc2 && e.T == p.T && e.p3 == p.pm &&
                 e.slot == p.slot_bytes && e.H == p.H && e.c == p.c && e.sst == p.sstate && e.hst == p.hst &&
                 e.fold == p.fold && e.split == p.split &&   // packing and epilogue must agree
                 e.res == (a.residual ? 1 : 0) && (e.res || a.act == 0))   // coupling specs: ReLU only
@@ -2056,13 +2104,15 @@ static StageKernel pick_kernel(const StagePlan& p, const StageArgs& a) {
 }
 
 ci_status_t umma_prepare(Model* m, const float* host_params) {
-    const bool prec3 = m->prec == CI_PREC_FP32;
+    // product precision: CI_PREC_FP32 -> f16x3 (hi(x)W_hi + lo(x)W_hi + hi(x)W_lo, fp16 splits of
+    // both operands), CI_PREC_F16X2 -> f16x2 (weights rounded to fp16), CI_PREC_BF16 -> bf16
+    const int pm = m->prec == CI_PREC_FP32 ? 2 : (m->prec == CI_PREC_F16X2 ? 1 : 0);
     UmmaState* U = new UmmaState();
     std::vector<uint16_t> pack;
     std::vector<float> bias;
     for (int s = 0; s < m->n_stages; s++) {
         const StageInfo& S = m->st[s];
-        if (!make_plan(S, prec3, U->plan[s])) {
+        if (!make_plan(S, pm, U->plan[s])) {
             delete U;
             set_error("stage %d (%dx%d, c=%d, m=%d) does not fit the tcgen05 kernel", s, S.H, S.W, S.c, S.m);
             return CI_ERR_UNSUPPORTED;
@@ -2070,9 +2120,9 @@ ci_status_t umma_prepare(Model* m, const float* host_params) {
         const StagePlan& p = U->plan[s];
         if (getenv("CI_DEBUG_PLAN"))
             fprintf(stderr,
-                    "[ci plan] stage %d %dx%d c=%d m=%d prec3=%d: Cp=%d Mp=%d MC=%d nch=%d Nc2=%d T=%d I=%d "
+                    "[ci plan] stage %d %dx%d c=%d m=%d pm=%d: Cp=%d Mp=%d MC=%d nch=%d Nc2=%d T=%d I=%d "
                     "k1=%d k2=%d slots=%dx%d smem=%zu tmem=%d blk_bytes=%lld M-eff=%.3f nhd=%d sst=%d est=%.0f cyc/img/blk\n",
-                    s, p.H, p.W, p.c, p.m, p.prec3, p.Cp, p.Mp, p.MC, p.nch, p.Nc2, p.T, p.I, p.k1, p.k2,
+                    s, p.H, p.W, p.c, p.m, p.pm, p.Cp, p.Mp, p.MC, p.nch, p.Nc2, p.T, p.I, p.k1, p.k2,
                     p.nslot, p.slot_bytes, p.smem, p.tmem_cols, (long long)p.blk_bytes,
                     (double)p.I * p.H * p.W / (p.T * 128.0), p.nhd, p.sstate, p.est_cycles);
         // align each stage stream to 128 B
@@ -2086,7 +2136,7 @@ ci_status_t umma_prepare(Model* m, const float* host_params) {
             const float* W2 = b1 + S.m;
             const float* b2 = W2 + (size_t)S.c * S.m * 9;
             size_t before = pack.size();
-            pack_block(p, W1, b1, W2, prec3, pack);
+            pack_block(p, W1, b1, W2, pm, pack);
             if ((int64_t)(pack.size() - before) * 2 != p.blk_bytes) {
                 delete U;
                 set_error("internal: packed block size mismatch");
@@ -2103,7 +2153,10 @@ ci_status_t umma_prepare(Model* m, const float* host_params) {
         const ci_arch_t& a = m->arch;
         StageInfo S{};
         S.H = a.in_h / 2; S.W = a.in_w / 2; S.c = 4 * a.enc_c1; S.C = 2 * S.c; S.m = a.enc_mid; S.nb = 1;
-        if (make_plan(S, prec3, U->enc_plan)) {
+        // split precisions: the encoder has no exact inverse to absorb a weight perturbation (x_p
+        // itself is compared), so its two convolutions keep the weights exact (f16x3; ~2% of the FLOPs)
+        const int pm_enc = pm ? 2 : 0;
+        if (make_plan(S, pm_enc, U->enc_plan)) {
             const StagePlan& p = U->enc_plan;
             while ((pack.size() * 2) % 128) pack.push_back(0);
             U->enc_wpack_off = (int64_t)pack.size() * 2;
@@ -2112,7 +2165,7 @@ ci_status_t umma_prepare(Model* m, const float* host_params) {
             const float* E2b = E2W + (size_t)a.enc_mid * 4 * a.enc_c1 * 9;
             const float* E3W = E2b + a.enc_mid;
             const float* E3b = E3W + (size_t)4 * a.enc_c1 * a.enc_mid * 9;
-            pack_block(p, E2W, E2b, E3W, prec3, pack);
+            pack_block(p, E2W, E2b, E3W, pm_enc, pack);
             for (int i = 0; i < p.Mp; i++) bias.push_back(i < S.m ? E2b[i] : 0.f);
             for (int i = 0; i < p.Nc2; i++) {
                 const int o = p.hst ? (i < S.c ? i : -1) : conv2_col_channel(p, i);
@@ -2165,6 +2218,11 @@ static void prof_end(cudaStream_t st, int stage, double flops) {
     cudaEventRecord(b, st);
     g_prof.push_back({g_prof_open, b, stage, flops});
     g_prof_open = nullptr;
+}
+
+bool umma_has_encoder(const Model* m) {
+    const UmmaState* U = reinterpret_cast<const UmmaState*>(m->umma_state);
+    return U && U->has_enc;
 }
 
 ci_status_t umma_encoder_tail(const Model* m, float* zbuf, int64_t n, int* ctr, cudaStream_t st) {
@@ -2253,13 +2311,13 @@ ci_status_t umma_stage(const Model* m, int s, float* state, int64_t n, bool inve
 }  // namespace ci
 
 extern "C" {
-ci_status_t ci_test_plan(int32_t H, int32_t W, int32_t c, int32_t m, int32_t prec3, int64_t* out16) {
+ci_status_t ci_test_plan(int32_t H, int32_t W, int32_t c, int32_t m, int32_t pm, int64_t* out16) {
     ci::StageInfo S{};
     const bool residual = c < 0;   // c < 0: residual stage (F acts on all |c| state channels)
     if (residual) c = -c;
     S.H = H; S.W = W; S.c = c; S.m = m; S.C = residual ? c : 2 * c; S.nb = 1;
     ci::StagePlan p;
-    if (!ci::make_plan(S, prec3 != 0, p)) { ci::set_error("no plan"); return CI_ERR_UNSUPPORTED; }
+    if (!ci::make_plan(S, pm, p)) { ci::set_error("no plan"); return CI_ERR_UNSUPPORTED; }
     ci::StageArgs sa{};
     sa.residual = residual ? 1 : 0;
     sa.act = residual ? 1 : 0;   // the residual archs use ELU, the coupling archs ReLU

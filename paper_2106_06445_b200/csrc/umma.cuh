@@ -30,11 +30,18 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo_bytes
     return d;
 }
 
-// Instruction descriptor, kind::f16: A = B = bf16, D = f32, both K-major.
-//   [4,6) c_format = 1 (F32) | [7,10) a_format = 1 (BF16) | [10,13) b_format = 1 (BF16)
+// Instruction descriptor, kind::f16: A = B = bf16 (or fp16), D = f32, both K-major.
+//   [4,6) c_format = 1 (F32) | [7,10) a_format (0 = F16, 1 = BF16) | [10,13) b_format
 //   [15] a_major = 0 (K) | [16] b_major = 0 (K) | [17,23) N >> 3 | [24,29) M >> 4
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
     return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+    return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+// the stage kernel's two operand types: bf16 (CI_PREC_BF16) or fp16 (CI_PREC_FP32, f16x2)
+__host__ __device__ constexpr uint32_t idesc_of(int M, int N, bool f16) {
+    return f16 ? idesc_f16(M, N) : idesc_bf16(M, N);
 }
 
 // D[tmem] (+)= A[smem] * B[smem]^T   (M x N x 16), issued by ONE thread.

@@ -1,23 +1,48 @@
-// Test-only probes of the tcgen05 building blocks (include/codedinv_testing.h):
+// Test-only probes of the tcgen05 building blocks (include/codedinv_probe.h), built as their own
+// library (libcodedinv_probe.so) so that none of this code ships in libcodedinv.so:
 //  * ci_test_umma_gemm: one 128 x N x (16*nk) UMMA with the descriptor tricks the conv
 //    kernel relies on (row-shifted start address; LBO = 16 B pairing adjacent rows; any
 //    LBO, e.g. Wp rows for vertical tap pairs or across planes for the tri mode),
 //    checked against a host reference by tests/test_gpu_umma.py;
 //  * ci_test_umma_rate: back-to-back MMA issue rate per SM for a given N.
+#include <stdarg.h>
 #include <stdio.h>
 
-#include "ci_internal.h"
-#include "codedinv_testing.h"
+#include "codedinv_probe.h"
 #include "umma.cuh"
 
 namespace ci {
 using namespace umma;
+
+static thread_local char g_probe_err[256] = "no error";
+static void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_probe_err, sizeof(g_probe_err), fmt, ap);
+    va_end(ap);
+}
+static ci_status_t cuda_status(cudaError_t e, const char* what) {
+    set_error("CUDA error %d (%s) in %s", (int)e, cudaGetErrorString(e), what);
+    return CI_ERR_CUDA;
+}
+#define CI_CUDA(call)                                              \
+    do {                                                           \
+        cudaError_t e_ = (call);                                   \
+        if (e_ != cudaSuccess) return ::ci::cuda_status(e_, #call); \
+    } while (0)
+#define CI_CHECK_LAUNCH(what)                                      \
+    do {                                                           \
+        cudaError_t e_ = cudaGetLastError();                       \
+        if (e_ != cudaSuccess) return ::ci::cuda_status(e_, what); \
+    } while (0)
 
 // A: [RA][KA] bf16 row-major in global; B: [N][KB] bf16 row-major.  SMEM planes of 8 channels:
 // plane p holds rows 0..R-1 at 16-B stride (uniform, SBO = 128).
 __global__ void __launch_bounds__(128) k_umma_gemm(const uint16_t* __restrict__ A, int RA, int KA,
                                                    const uint16_t* __restrict__ B, int N, int KB,
                                                    int shift, int mode, int nk, float* __restrict__ D) {
+    const bool f16 = (mode >> 30) & 1;   // operands are fp16 (the f16x2 precision's instruction descriptor)
+    mode &= ~(1 << 30);
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t bar;
     __shared__ uint32_t tmem_base;
@@ -44,7 +69,7 @@ __global__ void __launch_bounds__(128) k_umma_gemm(const uint16_t* __restrict__ 
     fence_after();
     const uint32_t tmem = tmem_base;
     if (warp == 0 && elect_one()) {
-        const uint32_t idesc = idesc_bf16(128, N);
+        const uint32_t idesc = idesc_of(128, N, f16);
         for (int j = 0; j < nk; j++) {
             uint64_t ad, bd;
             if (mode == 0) {  // K-halves = planes 2j, 2j+1
@@ -224,10 +249,12 @@ using namespace ci;
 
 extern "C" {
 
+const char* ci_probe_last_error(void) { return ci::g_probe_err; }
+
 ci_status_t ci_test_umma_gemm(const uint16_t* A, int32_t RA, int32_t KA, const uint16_t* B, int32_t N,
                               int32_t KB, int32_t shift, int32_t mode, int32_t nk, float* D,
                               ci_stream_t stream) {
-    const int lbo_rows = mode >> 8;
+    const int lbo_rows = (mode & ~(1 << 30)) >> 8;
     if (N < 16 || N > 256 || N % 16 || KA % 8 || KB % 16 || nk < 1 || shift < 0 || (mode & 0xFF) > 2 ||
         ((mode & 0xFF) == 2 && (lbo_rows < 1 || lbo_rows >= 16384 || shift + nk + lbo_rows + 127 >= RA * (KA / 8)))) {
         set_error("bad probe shape");

@@ -20,12 +20,14 @@ def ci():
     return codedinv
 
 
-def declared_symbols(header="*"):
-    import glob
+def declared_symbols(*headers):
     syms = set()
-    for h in glob.glob(os.path.join(ROOT, "include", header + ".h")):
-        syms |= set(re.findall(r"CI_API[^;(]*?\b(ci_\w+)\s*\(", open(h).read()))
+    for h in headers:
+        syms |= set(re.findall(r"CI_API[^;(]*?\b(ci_\w+)\s*\(", open(os.path.join(ROOT, "include", h + ".h")).read()))
     return sorted(syms)
+
+
+PRODUCT_HEADERS = ("codedinv", "codedinv_testing")
 
 
 def test_header_declares_the_north_star_entry_points():
@@ -37,9 +39,24 @@ def test_header_declares_the_north_star_entry_points():
 
 def test_library_exports_every_declared_symbol(ci):
     lib = ctypes.CDLL(ci.LIB_PATH)
-    for name in declared_symbols():
+    for name in declared_symbols(*PRODUCT_HEADERS):
         assert hasattr(lib, name), name
-    assert sorted(ci.EXPORTS + ci.TESTING_EXPORTS) == declared_symbols()
+    assert sorted(ci.EXPORTS + ci.TESTING_EXPORTS) == declared_symbols(*PRODUCT_HEADERS)
+
+
+def test_probe_library_is_separate(ci):
+    """The tcgen05 probes (include/codedinv_probe.h) live in libcodedinv_probe.so only."""
+    import subprocess
+    from paper_2106_06445_b200 import build
+    probe = ctypes.CDLL(build.PROBE_LIB)
+    for name in declared_symbols("codedinv_probe"):
+        assert hasattr(probe, name), name
+    dyn = subprocess.run(["nm", "-D", "--defined-only", ci.LIB_PATH], capture_output=True, text=True).stdout
+    for name in declared_symbols("codedinv_probe"):
+        assert name not in dyn, name
+    elf = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-text", ci.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "k_umma_gemm" not in elf and "k_umma_rate" not in elf
 
 
 def test_library_is_sm100a(ci):
@@ -95,12 +112,12 @@ def test_hot_path_plans_have_specialised_kernels():
     kernel.  Host-only planner query, no GPU needed."""
     from paper_2106_06445_b200 import codedinv as ci
     import fixtures as fx
-    for arch in (fx.ARCH_C, fx.ARCH_CR):
+    for arch, pms in ((fx.ARCH_C, (0, 1, 2)), (fx.ARCH_CR, (0, 2))):   # pm: bf16, f16x2, f16x3 (CI_PREC_FP32)
         for (C, H, W, c, m, nb) in arch.stage_shapes():
-            for prec3 in (0, 1):
+            for pm in pms:
                 q = -c if arch.block == "residual" else c
-                plan = ci.ci_test_plan(H, W, q, m, prec3)
-                assert plan["static"] == 1, (arch.name, H, c, m, prec3, plan)
+                plan = ci.ci_test_plan(H, W, q, m, pm)
+                assert plan["static"] == 1, (arch.name, H, c, m, pm, plan)
                 assert plan["tmem_cols"] <= 512 and plan["smem"] <= 227 * 1024
     # the tuned Arch-C bf16 plans use horizontal tap stacking on stages 1-2
     assert ci.ci_test_plan(16, 16, 6, 64, 0)["hst"] == 1

@@ -14,8 +14,8 @@ from oracle import codes
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-PRECS = ["simt", "fp32", "bf16"]
-TOL = {"simt": 1e-3, "fp32": 1e-3, "bf16": 3e-2}
+PRECS = ["fp32", "f16x2", "bf16"]
+TOL = {"fp32": 1e-3, "f16x2": 5e-3, "bf16": 3e-2}
 
 
 @pytest.fixture(scope="module")

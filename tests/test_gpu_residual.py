@@ -5,7 +5,7 @@ spectrally normalised to Lip(G) <= 0.9 (fixtures); h^-1 runs arch.fp_iters = 10 
 updates x <- y - G(x) per block.  The GPU is compared with the oracle run for the SAME number
 of updates (isolates arithmetic precision) and with the oracle's converged inverse (adds the
 truncation of the fixed point, ~3e-7 at L = 0.9, N = 10).  Tolerances as in
-test_gpu_parity.py: 1e-3 (simt, fp32 = bf16x3), 3e-2 (bf16, reported).
+test_gpu_parity.py: 1e-3 (fp32: f16x3 products for residual archs), 3e-2 (bf16, reported).
 """
 import numpy as np
 import pytest
@@ -16,8 +16,8 @@ import oracle
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-PRECS = ["simt", "fp32", "bf16"]
-TOL = {"simt": 1e-3, "fp32": 1e-3, "bf16": 3e-2}
+PRECS = ["fp32", "f16x2", "bf16"]
+TOL = {"fp32": 1e-3, "f16x2": 5e-3, "bf16": 3e-2}
 
 
 @pytest.fixture(scope="module")

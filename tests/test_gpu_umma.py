@@ -1,18 +1,51 @@
 """Pins of the tcgen05 descriptor encodings the implicit convolution relies on
-(row-shifted start addresses, LBO = 16 B pairing), against an exact host reference."""
+(row-shifted start addresses, LBO = 16 B pairing, fp16 operand type), against an exact host
+reference, through the test-only probe library (include/codedinv_probe.h)."""
+import ctypes
+import os
+
 import numpy as np
 import pytest
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
+PROBE_LIB = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2106_06445_b200",
+                         "libcodedinv_probe.so")
+
+
+class _Probe:
+    """ctypes marshalling of libcodedinv_probe.so (test-only library)."""
+
+    def __init__(self):
+        self.lib = ctypes.CDLL(PROBE_LIB)
+        P, I32 = ctypes.c_void_p, ctypes.c_int32
+        self.lib.ci_probe_last_error.restype = ctypes.c_char_p
+        self.lib.ci_test_umma_gemm.restype = I32
+        self.lib.ci_test_umma_gemm.argtypes = [P, I32, I32, P, I32, I32, I32, I32, I32, P, P]
+        self.lib.ci_test_umma_rate.restype = I32
+        self.lib.ci_test_umma_rate.argtypes = [I32, I32, I32, P, P]
+
+    def _check(self, st, where):
+        if st != 0:
+            raise RuntimeError(f"{where}: status {st}: {self.lib.ci_probe_last_error().decode()}")
+
+    @staticmethod
+    def _s():
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def ci_test_umma_gemm(self, A, B, N, shift, mode, nk, D):
+        self._check(self.lib.ci_test_umma_gemm(A.data_ptr(), A.shape[0], A.shape[1], B.data_ptr(), N, B.shape[1],
+                                               shift, mode, nk, D.data_ptr(), self._s()), "ci_test_umma_gemm")
+
+    def ci_test_umma_rate(self, N, iters, nblocks, cycles):
+        self._check(self.lib.ci_test_umma_rate(N, iters, nblocks, cycles.data_ptr(), self._s()), "ci_test_umma_rate")
 
 
 @pytest.fixture(scope="module")
 def ci():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    from paper_2106_06445_b200 import codedinv
-    return codedinv
+    return _Probe()
 
 
 def bf16_small_ints(rng, shape):
@@ -77,6 +110,22 @@ def test_umma_gemm_any_lbo(ci, lbo_rows, shift):
         ref += lin[r0:r0 + 128] @ B[:, 16 * j:16 * j + 8].T
         ref += lin[r0 + lbo_rows:r0 + lbo_rows + 128] @ B[:, 16 * j + 8:16 * j + 16].T
     assert np.array_equal(D.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("N", [32, 128, 256])
+def test_umma_gemm_fp16_operands(ci, N):
+    """The f16x2 precision's instruction descriptor (a/b_format = F16): values j/512 with
+    |j| < 1024 are exact in fp16 but not in bf16, and one K=16 step sums exactly in fp32."""
+    rng = np.random.default_rng(N)
+    RA, KA, nk, shift = 160, 16, 1, 7
+    A = (rng.integers(-1023, 1024, size=(RA, KA)) / 512.0).astype(np.float32)
+    B = (rng.integers(-1023, 1024, size=(N, KA)) / 512.0).astype(np.float32)
+    D = torch.empty(128, N, device="cuda")
+    to16 = lambda a: torch.from_numpy(a).to(torch.float16).view(torch.int16).cuda()
+    ci.ci_test_umma_gemm(to16(A), to16(B), N, shift, 0 | (1 << 30), nk, D)
+    torch.cuda.synchronize()
+    ref = A[shift:shift + 128].astype(np.float64) @ B.T.astype(np.float64)
+    assert np.array_equal(D.cpu().numpy().astype(np.float64), ref)
 
 
 def test_umma_issue_rate_report(ci):

@@ -11,6 +11,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+import bench
 import fixtures as fx
 import oracle
 
@@ -21,6 +22,24 @@ def _free_port():
     port = s.getsockname()[1]
     s.close()
     return port
+
+
+def test_bench_spawns_n_ranks_itself():
+    """`bench.py --gpus 2` outside torchrun re-launches itself with 2 ranks (spawn_cmd); the
+    reference arm runs on CPU, so the whole launcher path executes here: rank 0 prints one JSON
+    line with n_gpus = 2, rank 1 exits 0."""
+    import json
+    import subprocess
+    import sys
+    env = {k_: v for k_, v in os.environ.items() if k_ not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, bench.__file__, "--impl", "reference", "--gpus", "2", "--config", "C1",
+                          "--steps", "1", "--warmup", "1", "--ref-groups", "1"], capture_output=True, text=True,
+                         env=env, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(ln) for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1 and lines[0]["n_gpus"] == 2 and lines[0]["impl"] == "reference"
+    cmd = bench.spawn_cmd(["--gpus", "4"], 4, 29500)
+    assert cmd[1:3] == ["-m", "torch.distributed.run"] and "--nproc-per-node=4" in cmd and "127.0.0.1" in cmd
 
 
 def test_input_slices_match_monolithic():
@@ -43,12 +62,13 @@ def _worker(rank, world, port, B, out_dir):
     R = torch.from_numpy(out["R"])
     gathered = [torch.empty_like(R) for _ in range(world)]
     dist.all_gather(gathered, R)
-    # max-over-ranks timing as bench.py does it
-    t = torch.tensor([10.0 + rank])
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    # bench.py's own rank discovery and max-over-ranks timing
+    os.environ.update(RANK=str(rank), WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    assert bench.dist_env() == (rank, world, rank)
+    t = np.array([bench.max_over_ranks(10.0 + rank, dist)])
     if rank == 0:
         np.save(os.path.join(out_dir, "R.npy"), torch.cat(gathered).numpy())
-        np.save(os.path.join(out_dir, "tmax.npy"), t.numpy())
+        np.save(os.path.join(out_dir, "tmax.npy"), t)
     dist.barrier()
     dist.destroy_process_group()
 
