@@ -226,8 +226,11 @@ def run_reference(args, rank, world):
 # ----------------------------------------------------------------------------- C5
 def run_c5(args, rank, world, local):
     """Config C5: k = 7 main workers + 1 parity worker, one per GPU (8 ranks), 1024 groups per
-    step; encode exact (X2 reduce + h^-1 + h on the parity GPU) or learned (encoder on the parity
-    GPU); decode as a masked NCCL reduce-scatter (paper_2106_06445_b200/workers.py)."""
+    step, through ci_serve_group with a CI_SHARD_WORKERS communicator: encode exact (X2: the
+    parity GPU reads the mains' features over NVLink and forms the mean, then h^-1 and h) or
+    learned (encoder on the parity GPU); decode = K11, every GPU reading its share of the groups
+    from all peers' windows.  Drops are masked, not waited on (PAPER.md:669's straggler delay is
+    the first_k harness)."""
     cfg = fx.CONFIGS["C5"]
     k, B = cfg.k, cfg.B
     if world != k + 1:
@@ -238,19 +241,22 @@ def run_c5(args, rank, world, local):
     import torch
     import torch.distributed as dist
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist.init_process_group("gloo")
     from paper_2106_06445_b200 import codedinv as ci
-    from paper_2106_06445_b200.workers import GpuCompute, serve_workers
+    from paper_2106_06445_b200.workers import WorkerBuffers, make_comm, serve_worker
     arch = cfg.arch
     learned = args.encode == "learned"
     model = ci.Model(arch, fx.make_weights(arch, cfg.seed_w), args.precision, device=local)
-    comp = GpuCompute(model, k, B)
+    comm = make_comm(dist, ci.CI_SHARD_WORKERS, B, model.d, device=local)
+    bufs = WorkerBuffers(model, k, B, torch.device("cuda", local))
     dev = torch.device("cuda", local)
     x = fx.make_inputs(arch, B, k, cfg.seed_x)
     drop = torch.from_numpy(fx.make_drops(B, k, cfg.seed_drop)).to(dev)
-    x_slot = torch.from_numpy(np.ascontiguousarray(x[:, rank])).to(dev) if rank < k else None
-    x_all = torch.from_numpy(x).to(dev) if rank == k else None
-    step = lambda: serve_workers(comp, dist, rank, world, k, drop, x_slot=x_slot, x_all=x_all, learned=learned)
+    if rank < k:
+        xin = torch.from_numpy(np.ascontiguousarray(x[:, rank])).to(dev)
+    else:
+        xin = torch.from_numpy(x).to(dev) if learned else None
+    step = lambda: serve_worker(model, comm, xin, drop, bufs, learned=learned)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -262,15 +268,18 @@ def run_c5(args, rank, world, local):
     e1.record()
     torch.cuda.synchronize()
     dist.barrier()
-    ms = max_over_ranks(e0.elapsed_time(e1), dist, dev)
+    ms = max_over_ranks(e0.elapsed_time(e1), dist)
+    model.ci_check(bufs.ws)
     if rank == 0:
         print(json.dumps({"metric": METRIC, "value": B * args.steps / (ms / 1e3), "unit": UNIT, "n_gpus": world,
                           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
                           "higher_is_better": True, "scaling": "none (fixed 8-worker partition)",
                           "vs_baseline": None, "dtype": DTYPE[args.precision], "data": "synthetic",
                           "config": {"workload": "C5", "k": k, "groups_per_step": B, "encode": args.encode,
-                                     "parallelism": "worker-per-GPU (k=7 main + 1 parity), NCCL reduce / "
-                                                    "reduce-scatter decode"}}), flush=True)
+                                     "parallelism": "worker-per-GPU (k=7 main + 1 parity); mean and decode "
+                                                    "fused over peer memory (NVLink)"}}), flush=True)
+    dist.barrier()
+    comm.close()
     dist.destroy_process_group()
 
 

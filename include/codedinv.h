@@ -58,7 +58,11 @@ typedef enum {
     CI_ERR_DIM_MISMATCH = 3,  /* SPEC.md:115 DimensionMismatch */
     CI_ERR_UNSUPPORTED = 4,   /* arch/precision combination not built */
     CI_ERR_WORKSPACE = 5,     /* workspace NULL or smaller than ci_workspace_size() */
-    CI_ERR_CUDA = 6
+    CI_ERR_CUDA = 6,
+    CI_ERR_UNDECODABLE = 7,   /* SPEC.md:283 Undecodable: a group had fewer than k results or a
+                                 singular k-subset (general codes); reported by ci_check */
+    CI_ERR_COMM = 8           /* communicator bootstrap / peer mapping failed (SURVEY's CI_ERR_NCCL:
+                                 the exchange is this library's own peer-memory kernels) */
 } ci_status_t;
 
 typedef enum {
@@ -131,8 +135,9 @@ CI_API int64_t ci_feature_dim(const ci_model_t* model); /* d; -1 if model == NUL
  * ci_forward_h / ci_inverse_h on n images needs no more than ci_workspace_size(model, 1, n)). */
 CI_API ci_status_t ci_workspace_size(const ci_model_t* model, int32_t k, int64_t B, size_t* bytes);
 
-/* Synchronise `stream` and report device-side flags recorded in `ws` (drop index out of
- * range), then clear them. */
+/* Synchronise `stream` and report device-side flags recorded in `ws`, then clear them:
+ * CI_ERR_UNDECODABLE if a general-code group could not be decoded, else CI_ERR_INVALID_ARG if a
+ * drop index was out of range. */
 CI_API ci_status_t ci_check(const ci_model_t* model, void* ws, size_t ws_bytes, ci_stream_t stream);
 
 /* h on n images: x [n][in_c][in_h][in_w] -> h [n][d].  x and h must not overlap.
@@ -171,17 +176,64 @@ CI_API ci_status_t ci_decode(int32_t k, int64_t B, int64_t d, float* h, const fl
 CI_API ci_status_t ci_classify(const ci_model_t* model, int32_t head, const float* z, int64_t n,
                         float* logits, int32_t* labels, ci_stream_t stream);
 
-/* The whole coded path for B groups (steps 1-5 above) on one GPU, with the parity query from
- * `mode` (CI_ENC_LEARNED skips h^-1 and runs the learned encoder on x):
+/* ---- Communicator: the paper's worker partition across processes (config C5) -------------
+ * One process per worker (Fig. 2, 665-668: one worker per instance): ranks
+ * 0..k-1 are the main workers (slot r of every group), rank k is the parity worker, which also
+ * hosts the encoder.  Every rank owns a symmetric window of device
+ * memory (its published features + two epoch counters) that all ranks map (CUDA IPC; NVLink
+ * peer loads between GPUs, plain loads when several ranks share a GPU).  The exchange steps run
+ * as fused compute + collective kernels over that peer memory:
+ *   X2 exact encode: the parity rank reads the k mains' h(x_i) and forms their mean
+ *   X4 decode      : rank p reads every rank's features for its 1/(k+1) share of the groups
+ *                    and forms k h(x_p) - sum_{i != j} h(x_i)
+ * Bootstrap: rank 0 calls ci_comm_unique_id and the caller broadcasts the bytes (e.g. with
+ * torch.distributed); every rank then calls ci_comm_create with the same id, nranks, max_B and
+ * d (a host rendezvous through POSIX shared memory on this node; returns CI_ERR_COMM if a rank
+ * does not arrive within 120 s).  Serve calls on a communicator are collective: every rank
+ * issues the same sequence of ci_serve_group calls (same k, B), one stream per communicator.
+ * ci_comm_destroy is collective too (call it after all ranks finished serving). */
+#define CI_COMM_ID_BYTES 128
+typedef struct ci_comm ci_comm_t;
+typedef enum {
+    CI_SHARD_GROUPS = 0, /* data parallel: each rank serves its own groups; no exchange */
+    CI_SHARD_WORKERS = 1 /* the paper's partition: one worker (slot) per rank, nranks = k + 1 */
+} ci_layout_t;
+CI_API ci_status_t ci_comm_unique_id(uint8_t out[CI_COMM_ID_BYTES]);
+/* max_B: most groups per serve call; d: feature dim (multiple of 4).  Window = 256 B + max_B*d*4. */
+CI_API ci_status_t ci_comm_create(const uint8_t id[CI_COMM_ID_BYTES], int32_t nranks, int32_t rank,
+                                  ci_layout_t layout, int64_t max_B, int64_t d, int device, ci_comm_t** out);
+CI_API void ci_comm_destroy(ci_comm_t* comm);
+
+/* The whole coded path for B groups (steps 1-5 above), with the parity query from `mode`
+ * (CI_ENC_LEARNED skips h^-1 and runs the learned encoder on x).
+ *
+ * comm == NULL, or a CI_SHARD_GROUPS communicator (nothing is exchanged: groups are independent
+ * units), serves this process's B groups on one GPU:
  *   x [B][k][in_c][in_h][in_w], drop [B]
  *   h_out [B][k][d]     : h(x), with slot drop[b] replaced by its decoded estimate
  *   h_parity [B][d]     : h(x_p)
  *   x_parity [B][in_c][in_h][in_w] or NULL : the encoded query x_p
  *   logits [n_heads][B][k][C_t] (heads packed one after another), labels [n_heads][B][k]
- *   (either may be NULL to skip the heads) */
+ *   (either may be NULL to skip the heads)
+ *
+ * A CI_SHARD_WORKERS communicator (nranks == k + 1, B <= max_B, d == the model's d) runs this
+ * rank's worker of the partition; with Bp = ceil(B / (k+1)) and this rank's groups
+ * G = [rank*Bp, min(B, (rank+1)*Bp)):
+ *   x        main rank r: [B][in_c][in_h][in_w] = slot r of every group;  parity rank: the k
+ *            slots [B][k][in_c][in_h][in_w] in CI_ENC_LEARNED (X3: the front end hands the
+ *            encoder its inputs), unused (may be NULL) in CI_ENC_EXACT;
+ *   drop     [B], identical on every rank;
+ *   h_out    [B][d]: this worker's result (main: h(x_r); parity: h(x_p));
+ *   h_parity [Bp][d]: the decoded features of the lost slot of groups G (rows of groups with
+ *            drop = -1 are zero);
+ *   x_parity [B][in_c][in_h][in_w] or NULL: x_p (parity rank only; ignored elsewhere);
+ *   logits   [n_heads][B + Bp][C_t], labels [n_heads][B + Bp]: rows 0..B-1 = the heads on h_out
+ *            (main ranks; the parity rank leaves them unwritten), rows B.. = on the decoded rows.
+ * Drops are simulated by masking: the dropped worker still computes (PAPER.md:669 injects a
+ * delay instead; see ci_serve_first_k for latency). */
 CI_API ci_status_t ci_serve_group(const ci_model_t* model, ci_encode_mode_t mode, int32_t k, int64_t B,
                            const float* x, const int32_t* drop, float* h_out, float* h_parity,
-                           float* x_parity, float* logits, int32_t* labels, void* ws,
+                           float* x_parity, float* logits, int32_t* labels, ci_comm_t* comm, void* ws,
                            size_t ws_bytes, ci_stream_t stream);
 
 /* Same as ci_serve_group with HOST buffers (x, drop in; h_out, h_parity, logits, labels out;
@@ -205,20 +257,6 @@ CI_API ci_status_t ci_serve_group_host_async(const ci_model_t* model, ci_encode_
                                              float* h_out_host, float* h_parity_host, float* logits_host,
                                              int32_t* labels_host, void* ws, size_t ws_bytes,
                                              ci_stream_t stream);
-
-/* ---- Worker-partitioned serving (config C5: one worker per GPU) ----
- * Decode is linear, so it rides a reduction over workers: worker w contributes coef_w[b] * f_w[b]
- * and the sum over all n = k + 1 workers is the decoded feature of the lost worker of group b:
- *   CI_COEF_DECODE: main worker w < k: -1 if w != drop[b], 0 if w == drop[b]; parity w = k: +k
- *                   (sum = k f(x_p) - sum_{i != j} f(x_i))
- *   CI_COEF_MEAN:   main worker w < k: 1/k; parity: 0      (sum = exact-encode mean)
- * Groups with drop[b] = -1 get coefficient 0 for every worker in CI_COEF_DECODE. */
-typedef enum { CI_COEF_DECODE = 0, CI_COEF_MEAN = 1 } ci_coef_kind_t;
-CI_API ci_status_t ci_worker_coef(ci_coef_kind_t kind, int32_t k, int64_t B, int32_t worker,
-                                  const int32_t* drop, float* coef /*[B]*/, ci_stream_t stream);
-/* out[b][:] = coef[b] * f[b][:]   (f, out [B][d], coef [B]; out may alias f) */
-CI_API ci_status_t ci_combine(int64_t B, int64_t d, const float* f, const float* coef, float* out,
-                              ci_stream_t stream);
 
 /* Perturbed exact encode ("f(x_{k+1}) = sum_j c_j f(x_j) + eps",
  * SPEC.md:192-200): x_parity = h^-1(mean_i h_i + eps) with a caller-supplied perturbation
@@ -255,7 +293,8 @@ CI_API ci_status_t ci_online_update(int32_t k, int64_t B, int64_t d, float* est,
  * s has a result (n <= 32).  Decode uses S = the k smallest available tasks and solves for the
  * missing main tasks from the parity rows in S (fp64 p x p inverse per group, p = missing
  * mains); available main results are left untouched.  Groups with fewer than k available tasks
- * or a singular subset are left untouched and counted in the workspace flag (ci_check).
+ * or a singular subset (scaled |det G_S| <= 1e-9, rows of G_S normalised: SPEC.md:24) are left
+ * untouched and counted in the workspace's undecodable flag (ci_check: CI_ERR_UNDECODABLE).
  * Exact encode only (the learned encoder of a3' produces one parity query). */
 CI_API ci_status_t ci_workspace_size_general(const ci_model_t* model, int32_t k, int32_t r, int64_t B,
                                              size_t* bytes);

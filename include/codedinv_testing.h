@@ -36,6 +36,12 @@ CI_API ci_status_t ci_test_plan(int32_t H, int32_t W, int32_t c, int32_t m, int3
 CI_API ci_status_t ci_test_mean(int32_t k, int64_t B, int64_t d, const float* h, float* m,
                                 ci_stream_t stream);
 
+/* Host-only: the node-local rendezvous ci_comm_create uses (POSIX shared memory named by `id`):
+ * rank `rank` of `nranks` publishes `bytes` (<= 64) of `payload` and receives every rank's,
+ * out = nranks x 64 bytes (slot q at q * 64).  CI_ERR_COMM after 60 s without all ranks. */
+CI_API ci_status_t ci_test_rendezvous(const uint8_t id[CI_COMM_ID_BYTES], int32_t nranks, int32_t rank,
+                                      const uint8_t* payload, int32_t bytes, uint8_t* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,7 +21,9 @@ if not os.path.exists(LIB_PATH):
 _lib = ctypes.CDLL(LIB_PATH)
 
 CI_OK, CI_ERR_INVALID_ARG, CI_ERR_INVALID_SHAPE, CI_ERR_DIM_MISMATCH, CI_ERR_UNSUPPORTED, \
-    CI_ERR_WORKSPACE, CI_ERR_CUDA = range(7)
+    CI_ERR_WORKSPACE, CI_ERR_CUDA, CI_ERR_UNDECODABLE, CI_ERR_COMM = range(9)
+CI_SHARD_GROUPS, CI_SHARD_WORKERS = 0, 1
+CI_COMM_ID_BYTES = 128
 CI_PREC_FP32, CI_PREC_BF16, CI_PREC_F16X2 = 0, 1, 2
 CI_ENC_EXACT, CI_ENC_LEARNED = 0, 1
 PRECISIONS = {"fp32": CI_PREC_FP32, "bf16": CI_PREC_BF16, "f16x2": CI_PREC_F16X2}
@@ -29,11 +31,11 @@ PRECISIONS = {"fp32": CI_PREC_FP32, "bf16": CI_PREC_BF16, "f16x2": CI_PREC_F16X2
 EXPORTS = ["ci_last_error", "ci_model_create", "ci_model_destroy", "ci_feature_dim",
            "ci_workspace_size", "ci_check", "ci_forward_h", "ci_inverse_h", "ci_encode",
            "ci_decode", "ci_classify", "ci_serve_group", "ci_workspace_size_host",
-           "ci_serve_group_host", "ci_make_drops", "ci_worker_coef", "ci_combine",
+           "ci_serve_group_host", "ci_make_drops", "ci_comm_unique_id", "ci_comm_create", "ci_comm_destroy",
            "ci_workspace_size_general", "ci_encode_general", "ci_decode_general", "ci_serve_general",
            "ci_encode_perturbed", "ci_online_update", "ci_serve_group_host_async"]
 TESTING_EXPORTS = ["ci_test_prof_enable", "ci_test_prof_read", "ci_test_launch_count", "ci_test_mean",
-                   "ci_test_plan"]  # include/codedinv_testing.h
+                   "ci_test_plan", "ci_test_rendezvous"]  # include/codedinv_testing.h
 
 
 class CiStage(ctypes.Structure):
@@ -62,13 +64,15 @@ _sig = {
     "ci_encode": (_I32, [_P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
     "ci_decode": (_I32, [_I32, _I64, _I64, _P, _P, _P, _P, _SZ, _P]),
     "ci_classify": (_I32, [_P, _I32, _P, _I64, _P, _P, _P]),
-    "ci_serve_group": (_I32, [_P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "ci_serve_group": (_I32, [_P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "ci_workspace_size_host": (_I32, [_P, _I32, _I64, _P]),
     "ci_serve_group_host": (_I32, [_P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "ci_serve_group_host_async": (_I32, [_P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "ci_make_drops": (_I32, [_I32, _I64, ctypes.c_uint64, _P, _P]),
-    "ci_worker_coef": (_I32, [_I32, _I32, _I64, _I32, _P, _P, _P]),
-    "ci_combine": (_I32, [_I64, _I64, _P, _P, _P, _P]),
+    "ci_comm_unique_id": (_I32, [_P]),
+    "ci_comm_create": (_I32, [_P, _I32, _I32, _I32, _I64, _I64, ctypes.c_int, _P]),
+    "ci_comm_destroy": (None, [_P]),
+    "ci_test_rendezvous": (_I32, [_P, _I32, _I32, _P, _I32, _P]),
     "ci_workspace_size_general": (_I32, [_P, _I32, _I32, _I64, _P]),
     "ci_encode_perturbed": (_I32, [_P, _I32, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
     "ci_online_update": (_I32, [_I32, _I64, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
@@ -214,11 +218,17 @@ class Model:
                                 _stream(stream)), "ci_classify")
 
     def ci_serve_group(self, x, drop, h_out, h_parity, ws, x_parity=None, logits=None, labels=None,
-                       stream=None, learned=False):
-        B, k = x.shape[0], x.shape[1]
-        _check(_lib.ci_serve_group(self._h, CI_ENC_LEARNED if learned else CI_ENC_EXACT, k, B, _ptr(x), _ptr(drop), _ptr(h_out),
-                                   _ptr(h_parity), _ptr(x_parity), _ptr(logits), _ptr(labels),
-                                   _ptr(ws), ws.numel(), _stream(stream)), "ci_serve_group")
+                       stream=None, learned=False, comm=None, k=None):
+        """comm: a Comm (CI_SHARD_WORKERS: this rank's worker; x is its slot [B, C, H, W], or the
+        parity rank's [B, k, C, H, W] / None, so k must be given)."""
+        if comm is not None and comm.layout == CI_SHARD_WORKERS:
+            B, k = drop.shape[0], comm.nranks - 1
+        else:
+            B, k = x.shape[0], x.shape[1]
+        _check(_lib.ci_serve_group(self._h, CI_ENC_LEARNED if learned else CI_ENC_EXACT, k, B, _ptr(x), _ptr(drop),
+                                   _ptr(h_out), _ptr(h_parity), _ptr(x_parity), _ptr(logits), _ptr(labels),
+                                   comm._h if comm is not None else None, _ptr(ws), ws.numel(), _stream(stream)),
+               "ci_serve_group")
 
     def ci_serve_group_host(self, x, drop, h_out, h_parity, logits, labels, ws, stream=None, learned=False,
                             sync=True):
@@ -253,20 +263,33 @@ def ci_online_update(k, est, state, task, value, ws, stream=None):
                                  ws.numel(), _stream(stream)), "ci_online_update")
 
 
-CI_COEF_DECODE, CI_COEF_MEAN = 0, 1
-
-
-def ci_worker_coef(kind, k, B, worker, drop, coef, stream=None):
-    _check(_lib.ci_worker_coef(kind, k, B, worker, _ptr(drop), _ptr(coef), _stream(stream)), "ci_worker_coef")
-
-
-def ci_combine(f, coef, out, stream=None):
-    B, d = f.shape[0], f.numel() // max(f.shape[0], 1)
-    _check(_lib.ci_combine(B, d, _ptr(f), _ptr(coef), _ptr(out), _stream(stream)), "ci_combine")
-
-
 def ci_make_drops(k, B, seed, drop, stream=None):
     _check(_lib.ci_make_drops(k, B, seed, _ptr(drop), _stream(stream)), "ci_make_drops")
+
+
+def ci_comm_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * CI_COMM_ID_BYTES)()
+    _check(_lib.ci_comm_unique_id(buf), "ci_comm_unique_id")
+    return bytes(buf)
+
+
+class Comm:
+    """Owns a ci_comm_t (include/codedinv.h "Communicator"): collective create / destroy."""
+
+    def __init__(self, uid: bytes, nranks, rank, layout, max_B, d, device=0):
+        assert len(uid) == CI_COMM_ID_BYTES
+        self.nranks, self.rank, self.layout = nranks, rank, layout
+        h = ctypes.c_void_p()
+        buf = (ctypes.c_uint8 * CI_COMM_ID_BYTES).from_buffer_copy(uid)
+        _check(_lib.ci_comm_create(buf, nranks, rank, layout, max_B, d, device, ctypes.byref(h)), "ci_comm_create")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.ci_comm_destroy(self._h)
+            self._h = None
+
+    __del__ = close
 
 
 def ci_last_error() -> str:
@@ -289,6 +312,16 @@ def ci_test_prof_read():
 
 def ci_test_launch_count(reset=False):
     return int(_lib.ci_test_launch_count(1 if reset else 0))
+
+
+def ci_test_rendezvous(uid: bytes, nranks, rank, payload: bytes):
+    """-> list of every rank's payload (host-only shared-memory rendezvous of ci_comm_create)."""
+    out = (ctypes.c_uint8 * (64 * nranks))()
+    buf = (ctypes.c_uint8 * CI_COMM_ID_BYTES).from_buffer_copy(uid)
+    pay = (ctypes.c_uint8 * max(len(payload), 1)).from_buffer_copy(payload or b"\0")
+    _check(_lib.ci_test_rendezvous(buf, nranks, rank, pay, len(payload), out), "ci_test_rendezvous")
+    raw = bytes(out)
+    return [raw[64 * q:64 * q + len(payload)] for q in range(nranks)]
 
 
 def ci_test_mean(h, m, stream=None):

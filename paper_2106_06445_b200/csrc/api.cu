@@ -287,13 +287,17 @@ static ci_status_t check_ws(const WsLayout& L, void* ws, size_t ws_bytes) {
 ci_status_t ci_check(const ci_model_t* model, void* ws, size_t ws_bytes, ci_stream_t stream) {
     (void)model;
     if (!ws || ws_bytes < 256) { set_error("workspace too small"); return CI_ERR_WORKSPACE; }
-    int flag = 0;
-    CI_CUDA(cudaMemcpyAsync(&flag, ws, sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    int flag[2] = {0, 0};   // [0] drop index out of range, [1] undecodable groups
+    CI_CUDA(cudaMemcpyAsync(flag, ws, sizeof(flag), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
     CI_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
-    if (flag) {
-        CI_CUDA(cudaMemsetAsync(ws, 0, sizeof(int), (cudaStream_t)stream));
+    if (flag[0] || flag[1]) {
+        CI_CUDA(cudaMemsetAsync(ws, 0, sizeof(flag), (cudaStream_t)stream));
         CI_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
-        set_error("%d group(s) had a drop index outside [-1, k)", flag);
+        if (flag[1]) {
+            set_error("%d group(s) could not be decoded (fewer than k results or a singular subset)", flag[1]);
+            return CI_ERR_UNDECODABLE;
+        }
+        set_error("%d group(s) had a drop index outside [-1, k)", flag[0]);
         return CI_ERR_INVALID_ARG;
     }
     return CI_OK;
@@ -439,14 +443,79 @@ static void head_ptrs(const Model* m, int64_t n, float* logits, int32_t* labels,
     }
 }
 
+// One worker of the paper's partition (CI_SHARD_WORKERS): see ci_serve_group in codedinv.h.
+static ci_status_t serve_worker_impl(const Model* m, ci_encode_mode_t mode, int32_t k, int64_t B, const float* x,
+                                     const int32_t* drop, float* h_out, float* h_dec, float* x_parity,
+                                     float* const* logits, int32_t* const* labels, Comm* c, void* ws,
+                                     const WsLayout& L, cudaStream_t st) {
+    c->epoch++;
+    const int r = c->rank;
+    const int64_t Bp = (B + c->nranks - 1) / c->nranks;
+    const int64_t b0 = std::min<int64_t>(B, (int64_t)r * Bp), nb = std::min<int64_t>(B, b0 + Bp) - b0;
+    CI_CUDA(zero_ctrs(ws, L, st));
+    ci_status_t rc;
+    if (r < k) {
+        rc = forward_impl(m, x, h_out, B, ws, L, st);                      // (1) h on slot r's queries
+    } else {
+        float* xp = x_parity ? x_parity : at<float>(ws, L.xp);
+        if (mode == CI_ENC_LEARNED) {
+            rc = encode_learned_impl(m, x, xp, k, B, ws, L, st);            // (2) X3 + learned encoder
+        } else {
+            float* mean = at<float>(ws, L.mean);
+            rc = comm_peer_mean(c, k, B, mean, st);                         // (2) X2: mean over peers ...
+            if (rc == CI_OK) rc = inverse_impl(m, mean, xp, B, ws, L, st); //     ... then h^-1
+        }
+        if (rc == CI_OK) rc = forward_impl(m, xp, h_out, B, ws, L, st);   // (3) h(x_p)
+    }
+    if (rc != CI_OK) return rc;
+    rc = comm_publish(c, h_out, B, st);                                    // my result -> my window
+    if (rc != CI_OK) return rc;
+    rc = comm_peer_decode(c, k, B, drop, h_dec, at<int>(ws, L.flag), st);  // (4) X4 / K11 on my groups
+    if (rc != CI_OK) return rc;
+    for (int t = 0; t < m->arch.n_heads; t++) {                            // (5) heads
+        const int64_t C = m->arch.head_classes[t];
+        const float* W = m->d_head[t];
+        const float* bias = W + C * m->d;
+        if (r < k && (logits[t] || labels[t]))
+            CI_CUDA(launch_classify(h_out, B, m->d, W, bias, (int)C, logits[t], labels[t], st));
+        if (nb > 0 && (logits[t] || labels[t]))
+            CI_CUDA(launch_classify(h_dec, nb, m->d, W, bias, (int)C, logits[t] ? logits[t] + B * C : nullptr,
+                                    labels[t] ? labels[t] + B : nullptr, st));
+    }
+    return CI_OK;
+}
+
 ci_status_t ci_serve_group(const ci_model_t* model, ci_encode_mode_t mode, int32_t k, int64_t B,
                            const float* x, const int32_t* drop, float* h_out, float* h_parity,
-                           float* x_parity, float* logits, int32_t* labels, void* ws,
+                           float* x_parity, float* logits, int32_t* labels, ci_comm_t* comm, void* ws,
                            size_t ws_bytes, ci_stream_t stream) {
     CI_MODEL_OR_FAIL(m, model);
     if (mode != CI_ENC_EXACT && mode != CI_ENC_LEARNED) { set_error("unknown encode mode"); return CI_ERR_INVALID_ARG; }
     if (mode == CI_ENC_LEARNED && m->enc_off < 0) { set_error("model has no learned encoder"); return CI_ERR_UNSUPPORTED; }
     if (k < 1 || B < 0) { set_error("k must be >= 1 and B >= 0"); return CI_ERR_INVALID_ARG; }
+    Comm* c = reinterpret_cast<Comm*>(comm);
+    if (c && c->layout == CI_SHARD_WORKERS) {
+        const bool parity = c->rank == k;
+        const bool need_x = !parity || mode == CI_ENC_LEARNED;
+        if (c->nranks != k + 1 || B > c->cap_B || c->d != m->d) {
+            set_error("worker communicator: nranks %d (need k+1 = %d), B %lld (max %lld), d %lld (model %lld)",
+                      c->nranks, k + 1, (long long)B, (long long)c->cap_B, (long long)c->d, (long long)m->d);
+            return CI_ERR_INVALID_ARG;
+        }
+        if (B > 0 && ((need_x && (!x || !aligned16(x))) || !drop || !h_out || !h_parity || !aligned16(h_out) ||
+                      !aligned16(h_parity) || (x_parity && !aligned16(x_parity)))) {
+            set_error("invalid pointer argument"); return CI_ERR_INVALID_ARG;
+        }
+        WsLayout L = ws_layout(m, k, B);
+        ci_status_t r = check_ws(L, ws, ws_bytes);
+        if (r != CI_OK) return r;
+        if (B == 0) return CI_OK;
+        float* lp[4];
+        int32_t* bp[4];
+        head_ptrs(m, B + (B + k) / (k + 1), logits, labels, lp, bp);
+        return serve_worker_impl(m, mode, k, B, x, drop, h_out, h_parity, x_parity, lp, bp, c, ws, L,
+                                 (cudaStream_t)stream);
+    }
     if (B > 0 && (!x || !drop || !h_out || !h_parity || !aligned16(x) || !aligned16(h_out) ||
                   !aligned16(h_parity) || (x_parity && !aligned16(x_parity)))) {
         set_error("invalid pointer argument"); return CI_ERR_INVALID_ARG;
@@ -642,7 +711,7 @@ ci_status_t ci_workspace_size_host(const ci_model_t* model, int32_t k, int64_t B
 namespace ci {
 // fold workspace 1's drop-error count into workspace 0's flag (read by ci_check)
 __global__ void k_fold_flag(int* f0, int* f1) {
-    if (threadIdx.x == 0 && *f1) { *f0 += *f1; *f1 = 0; }
+    if (threadIdx.x < 2 && f1[threadIdx.x]) { f0[threadIdx.x] += f1[threadIdx.x]; f1[threadIdx.x] = 0; }
 }
 }  // namespace ci
 
@@ -753,22 +822,6 @@ ci_status_t ci_test_mean(int32_t k, int64_t B, int64_t d, const float* h, float*
 int64_t ci_test_launch_count(int32_t reset) {
     long long v = reset ? g_launches.exchange(0) : g_launches.load();
     return (int64_t)v;
-}
-
-ci_status_t ci_worker_coef(ci_coef_kind_t kind, int32_t k, int64_t B, int32_t worker, const int32_t* drop,
-                           float* coef, ci_stream_t stream) {
-    if ((kind != CI_COEF_DECODE && kind != CI_COEF_MEAN) || k < 1 || B < 0 || worker < 0 || worker > k ||
-        (B > 0 && (!coef || (kind == CI_COEF_DECODE && !drop)))) {
-        set_error("invalid argument"); return CI_ERR_INVALID_ARG;
-    }
-    CI_CUDA(launch_worker_coef((int)kind, k, B, worker, drop, coef, (cudaStream_t)stream));
-    return CI_OK;
-}
-
-ci_status_t ci_combine(int64_t B, int64_t d, const float* f, const float* coef, float* out, ci_stream_t stream) {
-    if (B < 0 || d < 0 || (B * d > 0 && (!f || !coef || !out))) { set_error("invalid argument"); return CI_ERR_INVALID_ARG; }
-    CI_CUDA(launch_combine(B, d, f, coef, out, (cudaStream_t)stream));
-    return CI_OK;
 }
 
 ci_status_t ci_make_drops(int32_t k, int64_t B, uint64_t seed, int32_t* drop, ci_stream_t stream) {

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -54,6 +55,24 @@ struct Model {
 
 void release_host_pipe(Model* m);   // api.cu: streams/events of the host-buffer entry
 
+// ---- worker-partition communicator (comm.cu)
+constexpr int kCommMaxRanks = 32;
+constexpr size_t kCommHeader = 256;          // window: [pub, done] epoch counters, then feat [cap_B][d]
+constexpr int kCommPub = 0, kCommDone = 1;   // uint64 index of the counters in the window
+struct Comm {
+    int nranks = 0, rank = 0, layout = 0, device = 0;
+    int64_t cap_B = 0, d = 0;
+    void* win = nullptr;                     // own window (cudaMalloc, exported by CUDA IPC)
+    void* peers[kCommMaxRanks] = {};         // every rank's window base in this process
+    bool opened[kCommMaxRanks] = {};         // peers[q] came from cudaIpcOpenMemHandle
+    void** d_peers = nullptr;                // device copy of peers[]
+    uint64_t epoch = 0;                      // serve calls issued on this communicator
+};
+ci_status_t comm_publish(Comm* c, const float* src, int64_t B, cudaStream_t st);
+ci_status_t comm_peer_mean(Comm* c, int k, int64_t B, float* mean, cudaStream_t st);
+ci_status_t comm_peer_decode(Comm* c, int k, int64_t B, const int32_t* drop, float* out, int* flag,
+                             cudaStream_t st);
+
 // ---- accounting (codedinv_testing.h)
 void count_launch(int n = 1);
 
@@ -86,9 +105,6 @@ cudaError_t launch_combine_general(const float* h, const float* coef, float* out
                                    int64_t d, cudaStream_t s);
 cudaError_t launch_decode_general(float* h, const float* hp, const float* coef, const uint32_t* avail, int k, int r,
                                   int64_t B, int64_t d, int* flag, cudaStream_t s);
-cudaError_t launch_worker_coef(int kind, int k, int64_t B, int worker, const int32_t* drop, float* coef,
-                               cudaStream_t s);
-cudaError_t launch_combine(int64_t B, int64_t d, const float* f, const float* coef, float* out, cudaStream_t s);
 cudaError_t launch_enc_e1_mean(const float* x, int k, int64_t B, int Ci, int H, int W, const float* W1,
                                const float* b1, int C1, float* m, float* zpsi, int64_t zstride, cudaStream_t s);
 cudaError_t launch_unsqueeze_add(const float* z, int64_t zstride, const float* m, float* u, int64_t B, int C,

@@ -19,6 +19,8 @@ namespace ci {
 namespace {
 constexpr int kMaxN = 32;
 
+constexpr double kSingTol = 1e-9;   // SPEC.md:24 singular-subset threshold (scaled determinant)
+
 __global__ void __launch_bounds__(256) k_combine_general(const float* __restrict__ h, const float* __restrict__ coef,
                                                          float* __restrict__ out, int k, int r, int64_t B,
                                                          int64_t d) {
@@ -67,7 +69,7 @@ __global__ void __launch_bounds__(256) k_decode_general(float* __restrict__ h, c
                 if ((av >> t) & 1u) S[ns++] = t;
             int p = 0, nsrc = 0;
             if (ns < k) {
-                atomicAdd(flag, 1);   // fewer than k results: cannot decode
+                atomicAdd(flag + 1, 1);   // fewer than k results: undecodable (ci_check)
             } else {
                 int par[kMaxN], np = 0;
                 // missing mains = main tasks not in S (mains have the smallest indices, so every
@@ -87,12 +89,25 @@ __global__ void __launch_bounds__(256) k_decode_general(float* __restrict__ h, c
                     for (int c2 = 0; c2 < 2 * p; c2++)
                         s_a[a][c2] = c2 < p ? (double)__ldg(coef + par[a] * k + s_miss[c2])
                                             : (c2 - p == a ? 1.0 : 0.0);
+                // singular test of SPEC.md:24: |det G_S| with every row of G_S scaled to unit 2-norm.  G_S's main rows are unit vectors, so this
+                // is |det A| / prod_a ||c[par[a]]||_2 (full k-length parity rows), det A = the
+                // product of the Gauss-Jordan pivots: scale invariant, unlike an absolute pivot floor.
+                double sdet = 1.0;
+                for (int a = 0; a < p; a++) {
+                    double nrm = 0.0;
+                    for (int j = 0; j < k; j++) {
+                        const double c = (double)__ldg(coef + par[a] * k + j);
+                        nrm += c * c;
+                    }
+                    sdet /= sqrt(nrm);
+                }
                 bool singular = false;
                 for (int col = 0; col < p && !singular; col++) {
                     int piv = col;
                     for (int a = col + 1; a < p; a++)
                         if (fabs(s_a[a][col]) > fabs(s_a[piv][col])) piv = a;
-                    if (fabs(s_a[piv][col]) < 1e-12) { singular = true; break; }
+                    sdet *= fabs(s_a[piv][col]);
+                    if (s_a[piv][col] == 0.0 || !(sdet > kSingTol)) { singular = true; break; }
                     if (piv != col)
                         for (int c2 = 0; c2 < 2 * p; c2++) {
                             double t = s_a[col][c2]; s_a[col][c2] = s_a[piv][c2]; s_a[piv][c2] = t;
@@ -107,7 +122,7 @@ __global__ void __launch_bounds__(256) k_decode_general(float* __restrict__ h, c
                     }
                 }
                 if (singular) {
-                    atomicAdd(flag, 1);
+                    atomicAdd(flag + 1, 1);   // singular subset: undecodable (ci_check)
                     p = 0;
                 } else {
                     // f_M = Ainv P_S - Ainv C[P_S][avail mains] f_avail

@@ -81,8 +81,8 @@ __global__ void k_decode_scalar(float* __restrict__ h, const float* __restrict__
          idx += (int64_t)gridDim.x * blockDim.x) {
         int64_t b = idx / d, e = idx - b * d;
         int j = drop[b];
-        if (j < 0) continue;
-        if (j >= k) { if (e == 0) atomicAdd(flag, 1); continue; }
+        if (j == -1) continue;                                    // no loss in this group
+        if (j < 0 || j >= k) { if (e == 0) atomicAdd(flag, 1); continue; }
         float acc = 0.f;
         for (int i = 0; i < k; i++)
             if (i != j) acc = __fadd_rn(acc, h[(b * k + i) * d + e]);
@@ -117,14 +117,19 @@ template <int KMAX>
 __global__ void __launch_bounds__(256) k_decode(float4* __restrict__ h, const float4* __restrict__ p,
                                                 const int32_t* __restrict__ drop, int k, int64_t B,
                                                 int64_t d4, int* __restrict__ flag) {
-    const int64_t total = B * d4;
+    const int64_t total = B * d4, stride = (int64_t)gridDim.x * blockDim.x;
     const float fk = (float)k;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
+    int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    // the next iteration's drop index is loaded one iteration ahead: the k-1 row loads depend on
+    // it (slot j is skipped), so a just-in-time load would serialise an L2 round trip before
+    // every batch of DRAM loads (measured 69% vs 82% DRAM throughput of k_mean under ncu)
+    int jn = idx < total ? __ldg(drop + idx / d4) : -1;
+    for (; idx < total; idx += stride) {
         int64_t b = idx / d4, e = idx - b * d4;
-        int j = __ldg(drop + b);
-        if (j < 0) continue;
-        if (j >= k) {
+        const int j = jn;
+        if (idx + stride < total) jn = __ldg(drop + (idx + stride) / d4);
+        if (j == -1) continue;                                    // no loss in this group
+        if (j < 0 || j >= k) {
             if (e == 0) atomicAdd(flag, 1);
             continue;
         }
@@ -315,42 +320,5 @@ cudaError_t launch_make_drops(int k, int64_t B, uint64_t seed, int32_t* drop, cu
 }
 
 // Worker coefficients of the masked-reduction decode / mean (codedinv.h CI_COEF_*)
-__global__ void k_worker_coef(int kind, int k, int64_t B, int worker, const int32_t* __restrict__ drop,
-                              float* __restrict__ coef) {
-    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < B; b += (int64_t)gridDim.x * blockDim.x) {
-        float c;
-        if (kind == 1) {
-            c = worker < k ? __fdiv_rn(1.f, (float)k) : 0.f;
-        } else {
-            const int j = drop[b];
-            if (j < 0 || j >= k) c = 0.f;
-            else if (worker == k) c = (float)k;
-            else c = worker == j ? 0.f : -1.f;
-        }
-        coef[b] = c;
-    }
-}
-
-__global__ void k_combine(int64_t B, int64_t d, const float* __restrict__ f, const float* __restrict__ coef,
-                          float* __restrict__ out) {
-    const int64_t total = B * d;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x)
-        out[i] = __fmul_rn(coef[i / d], f[i]);
-}
-
-cudaError_t launch_worker_coef(int kind, int k, int64_t B, int worker, const int32_t* drop, float* coef,
-                               cudaStream_t s) {
-    if (B == 0) return cudaSuccess;
-    k_worker_coef<<<grid_for(B, 256), 256, 0, s>>>(kind, k, B, worker, drop, coef);
-    count_launch();
-    return cudaGetLastError();
-}
-
-cudaError_t launch_combine(int64_t B, int64_t d, const float* f, const float* coef, float* out, cudaStream_t s) {
-    if (B * d == 0) return cudaSuccess;
-    k_combine<<<grid_for(B * d, 256), 256, 0, s>>>(B, d, f, coef, out);
-    count_launch();
-    return cudaGetLastError();
-}
 
 }  // namespace ci

@@ -112,8 +112,39 @@ def test_decode_general_flags_undecodable(ci):
     ws = torch.zeros(256, dtype=torch.uint8, device="cuda")
     ci.ci_decode_general(dev(c32), Ht, dev(Pp), dev(avail.view(np.int32)), ws)
     torch.cuda.synchronize()
-    assert int(ws[:4].view(torch.int32).item()) == 2
+    assert int(ws[4:8].view(torch.int32).item()) == 2          # the undecodable count (flag int 1)
     assert np.array_equal(Ht.cpu().numpy(), H)
+    with pytest.raises(ci.CiError) as e:
+        ci._check(ci._lib.ci_check(None, ci._ptr(ws), ws.numel(), ci._stream(None)), "ci_check")
+    assert e.value.status == ci.CI_ERR_UNDECODABLE
+
+
+@pytest.mark.parametrize("scale", [1.0, 1e-14])
+def test_decode_general_singular_subset_is_scale_invariant(ci, scale):
+    """A non-MDS code (SPEC.md:59 SingularSubset): parity rows [a, 2a] and [a, 2a(1 + 1e-12)]
+    (= [a, 2a] in fp32) with both mains lost leave a singular subset: left untouched and flagged,
+    whatever the scale a.  An invertible pair of rows [a, 2a], [2a, a] decodes at any scale (at
+    a = 1e-14 an absolute pivot floor of 1e-12 would have called it singular; the row-normalised
+    determinant is 3/5)."""
+    k, d = 2, 8
+    a = scale
+    coef = np.array([[a, 2 * a], [a, 2 * a + 1e-12 * a]], np.float32)
+    coef_ok = np.array([[a, 2 * a], [2 * a, a]], np.float32)
+    F = np.array([[1.0, -2.0], [0.5, 3.0]])                          # true f(x_1), f(x_2) of 2 groups
+    Fd = np.repeat(F[:, :, None], d, axis=2).astype(np.float32)       # [B=2][k][d]
+    for c, singular in ((coef, True), (coef_ok, False)):
+        P = np.einsum("rk,bkd->brd", c.astype(np.float64), Fd.astype(np.float64)).astype(np.float32)
+        Ht = dev(np.zeros_like(Fd))
+        avail = np.array([0b1100, 0b1100], np.uint32)                 # only the two parities arrived
+        ws = torch.zeros(256, dtype=torch.uint8, device="cuda")
+        ci.ci_decode_general(dev(c), Ht, dev(P), dev(avail.view(np.int32)), ws)
+        torch.cuda.synchronize()
+        got = Ht.cpu().numpy()
+        if singular:
+            assert int(ws[4:8].view(torch.int32).item()) == 2 and np.all(got == 0)
+        else:
+            assert int(ws[4:8].view(torch.int32).item()) == 0
+            assert np.max(np.abs(got - Fd)) < 1e-5
 
 
 def run_serve_general(ci, m, arch, c32, x, avail):

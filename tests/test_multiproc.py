@@ -1,7 +1,10 @@
-"""World-size-2 CPU tests (gloo) of the multi-GPU host logic bench.py uses for N > 1:
-group sharding (rank r serves global groups [r*B, (r+1)*B), no data-path collective),
-counter-based input slices, and max-over-ranks timing.  Groups are independent units
-(PAPER.md:211-214), so the sharded result must equal the single-process result bit-exactly."""
+"""Multi-process CPU tests of the host logic of the multi-GPU paths.
+
+Group-sharded data parallelism (bench.py for N > 1; gloo, world size 2): rank r serves global
+groups [r*B, (r+1)*B) with no data-path collective, counter-based input slices, bench.py's own
+rank discovery / max-over-ranks timing / self-spawn.  Groups are independent units
+(PAPER.md:211-214), so the sharded result equals the single-process result bit-exactly.
+Worker partition (C5): the node-local rendezvous that bootstraps ci_comm_create."""
 import os
 import socket
 
@@ -84,92 +87,24 @@ def test_group_sharded_gloo_world2(tmp_path):
     assert float(np.load(tmp_path / "tmax.npy")[0]) == 11.0
 
 
-# ------------------------------------------------------------------ C5 worker partition
-class _OracleCompute:
-    """CPU stand-in for GpuCompute (test only): per-rank compute from the f64 oracle."""
-
-    def __init__(self, arch, params, k):
-        self.arch, self.params, self.k, self.d = arch, params, k, arch.d
-
-        class _M:
-            pass
-        self.model = _M()
-        self.model.arch = arch
-
-    def empty(self, *shape):
-        return torch.empty(*shape, dtype=torch.float64)
-
-    def zeros(self, *shape):
-        return torch.zeros(*shape, dtype=torch.float64)
-
-    def forward_h(self, x):
-        return torch.from_numpy(oracle.forward_h(self.arch, self.params, x.numpy(), nthreads=1))
-
-    def inverse_h(self, h):
-        return torch.from_numpy(oracle.inverse_h(self.arch, self.params, h.numpy(), nthreads=1))
-
-    def encode_learned(self, x_all):
-        return torch.from_numpy(oracle.encode_learned(self.arch, self.params, x_all.numpy(), nthreads=1))
-
-    def coef(self, kind, worker, drop):
-        d = torch.as_tensor(drop)
-        if kind == 1:
-            return torch.full((len(d),), (1.0 / self.k) if worker < self.k else 0.0, dtype=torch.float64)
-        c = torch.where(d == worker, 0.0, -1.0).double() if worker < self.k else torch.full((len(d),), float(self.k),
-                                                                                             dtype=torch.float64)
-        return torch.where(d < 0, torch.zeros_like(c), c)
-
-    def combine(self, f, coef):
-        return f * coef[:, None]
-
-    def classify(self, head, z):
-        lg, lb = oracle.classify(self.arch, self.params, head, z.numpy())
-        return torch.from_numpy(lg), torch.from_numpy(lb)
+# ------------------------------------------------------------------ C5 communicator bootstrap
+def _rendezvous_worker(rank, world, uid, out_dir):
+    from paper_2106_06445_b200 import codedinv as ci
+    got = ci.ci_test_rendezvous(uid, world, rank, bytes([rank + 1]) * 40)
+    np.save(os.path.join(out_dir, f"rv{rank}.npy"), np.frombuffer(b"".join(got), np.uint8))
 
 
-def _worker_c5(rank, world, port, B, learned, out_dir):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    from paper_2106_06445_b200.workers import serve_workers
-    arch, k = fx.ARCH_TE, world - 1
-    params = fx.make_weights(arch, 15)
-    x = fx.make_inputs(arch, B, k, 5)
-    drop = fx.make_drops(B, k, 105)
-    drop[1] = -1                                  # one group without a loss
-    comp = _OracleCompute(arch, params, k)
-    xs = torch.from_numpy(x[:, rank].astype(np.float64)) if rank < k else None
-    xa = torch.from_numpy(x.astype(np.float64)) if rank == k else None
-    out = serve_workers(comp, dist, rank, world, k, torch.from_numpy(drop), x_slot=xs, x_all=xa, learned=learned)
-    parts = [torch.empty_like(out["decoded"]) for _ in range(world)]
-    dist.all_gather(parts, out["decoded"])
-    if rank == 0:
-        np.save(os.path.join(out_dir, "decoded.npy"), torch.cat(parts).numpy())
-        np.save(os.path.join(out_dir, "logits_dec.npy"), out["logits_decoded"][1].numpy())
-    dist.barrier()
-    dist.destroy_process_group()
-
-
-@pytest.mark.parametrize("learned", [False, True])
-def test_worker_partition_gloo(tmp_path, learned):
-    """C5 orchestration (k = 2 main workers + 1 parity worker, 3 ranks): the masked
-    reduce-scatter decode equals the single-process oracle decode of the lost slot."""
-    world, B = 3, 6
-    mp.spawn(_worker_c5, args=(world, _free_port(), B, learned, str(tmp_path)), nprocs=world, join=True)
-    arch, k = fx.ARCH_TE, world - 1
-    params = fx.make_weights(arch, 15)
-    x = fx.make_inputs(arch, B, k, 5)
-    drop = fx.make_drops(B, k, 105)
-    drop[1] = -1
-    ref = oracle.serve_group(arch, params, x, drop, learned=learned, nthreads=1)
-    dec = np.load(tmp_path / "decoded.npy")
-    for b in range(B):
-        if drop[b] < 0:
-            assert np.all(dec[b] == 0)
-        else:
-            r = ref["R"][b, drop[b]]
-            assert np.max(np.abs(dec[b] - r)) / np.max(np.abs(r)) < 1e-12
-    lg = np.load(tmp_path / "logits_dec.npy")          # rank 0's partition, coarse head
-    r0 = [b for b in range(B // world)]
-    for b in r0:
-        if drop[b] >= 0:
-            assert np.max(np.abs(lg[b] - ref["logits"][1][b, drop[b]])) < 1e-10
+def test_comm_rendezvous_world4(tmp_path):
+    """The host rendezvous of ci_comm_create (POSIX shared memory named by ci_comm_unique_id):
+    4 processes each publish 40 bytes and all receive every rank's payload in rank order."""
+    from paper_2106_06445_b200 import build
+    build.build()
+    from paper_2106_06445_b200 import codedinv as ci
+    uid = ci.ci_comm_unique_id()
+    assert len(uid) == ci.CI_COMM_ID_BYTES and any(uid[:16]) and ci.ci_comm_unique_id() != uid
+    world = 4
+    mp.spawn(_rendezvous_worker, args=(world, uid, str(tmp_path)), nprocs=world, join=True)
+    want = np.frombuffer(b"".join(bytes([q + 1]) * 40 for q in range(world)), np.uint8)
+    for r in range(world):
+        assert np.array_equal(np.load(tmp_path / f"rv{r}.npy"), want)
+    assert not os.path.exists("/dev/shm/codedinv_" + uid[:16].hex())   # the name is unlinked after use
