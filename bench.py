@@ -33,6 +33,9 @@ import time
 
 import numpy as np
 
+# one hardware queue per CUDA stream (first-k harness: k + 2 + in-flight streams; must be set
+# before the CUDA context exists)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -522,6 +525,65 @@ def hbm_extras(ci, dev, stream, peaks, k, d):
     return hbm
 
 
+def nearest_rank(v, p):
+    """Nearest-rank percentile (SPEC.md LatencyStats): sorted[ceil(p/100 * N) - 1]."""
+    v = np.sort(np.asarray(v))
+    return float(v[max(0, int(np.ceil(p / 100.0 * len(v))) - 1)])
+
+
+def first_k_extras(ci, dev, precision, queries=1000, delay_ns=100_000_000, inflight=16):
+    """f2: first-k gated serving with online decoding (ci_serve_first_k) on the learned-encoder
+    arch (the parity worker encodes from the raw queries), one group of k = 10
+    CIFAR-shaped queries per query, 0.1 s injected on one random main worker per query
+    (PAPER.md:669).  Three arms (SPEC.md latency_comparison): coded with the straggler, uncoded
+    (waits for all k) with the straggler, coded without stragglers; plus the completing event's
+    online-update cost vs k (App. C: independent of k)."""
+    import torch
+    cfg = fx.CONFIGS["C4"]
+    arch = cfg.arch
+    model = ci.Model(arch, fx.make_weights(arch, cfg.seed_w), precision)
+
+    def arm(k, Q, strag, uncoded, inflight=inflight):
+        x = torch.from_numpy(fx.make_inputs(arch, Q, k, cfg.seed_x + k)).to(dev)
+        feats = torch.empty(Q, k, arch.d, device=dev)
+        lg = torch.empty(Q * k * sum(arch.heads), device=dev)
+        lb = torch.empty(Q * k * len(arch.heads), dtype=torch.int32, device=dev)
+        rec = torch.zeros(Q, 4, dtype=torch.int64, device=dev)
+        ws = model.workspace_first_k(k, inflight)
+        model.ci_serve_first_k(x, strag[:8], delay_ns, feats[:8], lg, lb, rec, ws, max_inflight=inflight,
+                               uncoded=uncoded)   # warm-up (8 queries)
+        t0 = time.perf_counter()
+        model.ci_serve_first_k(x, strag, delay_ns, feats, lg, lb, rec, ws, max_inflight=inflight, uncoded=uncoded)
+        wall = time.perf_counter() - t0
+        r = rec.cpu().numpy()
+        lat = r[:, 0] / 1e6
+        return {"queries": Q, "p50_ms": nearest_rank(lat, 50), "p99_ms": nearest_rank(lat, 99),
+                "p999_ms": nearest_rank(lat, 99.9), "mean_ms": float(lat.mean()),
+                "update_us_median": float(np.median(r[:, 1]) / 1e3), "heads_us_median": float(np.median(r[:, 2]) / 1e3),
+                "degraded_frac": float(np.mean(r[:, 3] >> 32)), "wall_s": wall}
+
+    k = cfg.k
+    rng = np.random.default_rng(669)
+    strag = rng.integers(0, k, queries).astype(np.int32)
+    none = np.full(queries, -1, np.int32)
+    out = {"k": k, "delay_ms": delay_ns / 1e6, "inflight": inflight, "precision": precision,
+           "coded_straggler": arm(k, queries, strag, False),
+           "uncoded_straggler": arm(k, max(queries // 3, 64), strag, True),
+           "coded_no_straggler": arm(k, queries, none, False, inflight=1)}
+    per_k = {}
+    for kk in (2, 4, 10):
+        a = arm(kk, 200, np.full(200, -1, np.int32), False, inflight=1)
+        per_k[f"k={kk}"] = {"update_us_median": a["update_us_median"], "heads_us_median": a["heads_us_median"],
+                            "p50_ms": a["p50_ms"]}
+    out["completing_event_vs_k"] = per_k
+    out["note"] = ("latency = device globaltimer from query submission to the heads' output on the k recovered "
+                   "features; workers = CUDA streams of one GPU; update = the completing event's online "
+                   "update (App. C), heads = the linear heads on the k features; straggler arms keep up to "
+                   "`inflight` queries in flight (a slot frees when its straggler reports), the no-straggler "
+                   "and per-k arms run one query at a time (no queueing)")
+    return out
+
+
 def e2e_measure(ci, wl, model, args, dist, nin):
     """Same metric through the host-buffer C-ABI call: pinned H2D of x + drop and D2H of every
     output inside the device-timed region."""
@@ -680,6 +742,7 @@ def main():
     extras = rank == 0 and world == 1 and not args.no_extras
 
     hbm = hbm_extras(ci, dev, stream, peaks, k, arch.d) if extras else {}
+    first_k = first_k_extras(ci, dev, args.precision) if extras else None
     e2e = None if args.no_e2e else e2e_measure(ci, wl, main_res["model"], args, dist, args.inflight)
 
     # --- bulk encoder-label generation (f4): h on the k inputs + mean + h^-1
@@ -779,6 +842,8 @@ def main():
             line["encoder_overhead"] = enc_over
         if label_gen:
             line["label_generation"] = label_gen
+        if first_k:
+            line["first_k"] = first_k
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()

@@ -284,6 +284,38 @@ CI_API ci_status_t ci_online_update(int32_t k, int64_t B, int64_t d, float* est,
                                     const int32_t* task, const float* value, void* ws, size_t ws_bytes,
                                     ci_stream_t stream);
 
+/* ---- First-k gated serving with an injected straggler (App. C
+ * PAPER.md:938-952; SPEC.md:279-287 run_query_*, 317 first-k gating, 388 per-event cost) -------
+ * A latency harness of Q independent queries of one group each (k CIFAR-shaped inputs):
+ * k main workers and, in CI_FIRSTK_CODED, the parity worker (learned encoder + f on the encoded
+ * query) run concurrently, each on its own CUDA stream; straggler[q] >= 0 delays
+ * main worker straggler[q]'s result of query q by delay_ns (0.1 s on one random
+ * worker).  Each result is applied on arrival by the online decoder (ci_online_update's rule,
+ * reading R-f2a); the query completes when any k results are in (coded: first-k gating) or when
+ * all k mains are in (CI_FIRSTK_UNCODED: no parity worker), and the heads run on the k
+ * recovered features right there.  Up to max_inflight queries overlap (a slot is reused once
+ * all of its workers, including a straggler, have reported).
+ *   x        [Q][k][in_c][in_h][in_w] DEVICE;  straggler [Q] HOST int32 (-1: none)
+ *   features [Q][k][d] DEVICE: the recovered f(x_i) (the straggler's slot decoded when the
+ *            parity beat it)
+ *   logits   [n_heads][Q][k][C_t], labels [n_heads][Q][k] DEVICE (may be NULL without heads)
+ *   records  [Q][4] DEVICE int64: {latency_ns (submit -> predictions, device globaltimer),
+ *            update_ns (the completing event's online update), heads_ns, decode-set mask
+ *            (bit j = task j used, bit k = parity) | degraded << 32}
+ * Synchronous: blocks while more than max_inflight queries are outstanding and returns when all
+ * Q queries have finished (it creates and destroys its own k + 1 + max_inflight streams).
+ * CI_FIRSTK_CODED needs a model with the learned encoder (CI_ERR_UNSUPPORTED otherwise).  Every
+ * stream needs its own hardware queue: the process must have been started with
+ * CUDA_DEVICE_MAX_CONNECTIONS >= k + 2 + max_inflight (<= 32), else CI_ERR_UNSUPPORTED (with
+ * shared queues a delayed worker would falsely stall other queries' workers). */
+typedef enum { CI_FIRSTK_CODED = 0, CI_FIRSTK_UNCODED = 1 } ci_firstk_mode_t;
+CI_API ci_status_t ci_workspace_size_first_k(const ci_model_t* model, int32_t k, int32_t max_inflight,
+                                             size_t* bytes);
+CI_API ci_status_t ci_serve_first_k(const ci_model_t* model, ci_firstk_mode_t mode, int32_t k, int64_t Q,
+                                    const float* x, const int32_t* straggler, int64_t delay_ns,
+                                    int32_t max_inflight, float* features, float* logits, int32_t* labels,
+                                    int64_t* records, void* ws, size_t ws_bytes, ci_stream_t stream);
+
 /* ---- General (n, k) codes, n - k = r >= 1 parity tasks (Eq. 3, 563-597;
  * SURVEY §8f f3) ----------------------------------------------------------------------------
  * The generator is systematic: tasks 0..k-1 are the main queries (rows = I_k), task k+i is the

@@ -24,6 +24,7 @@ CI_OK, CI_ERR_INVALID_ARG, CI_ERR_INVALID_SHAPE, CI_ERR_DIM_MISMATCH, CI_ERR_UNS
     CI_ERR_WORKSPACE, CI_ERR_CUDA, CI_ERR_UNDECODABLE, CI_ERR_COMM = range(9)
 CI_SHARD_GROUPS, CI_SHARD_WORKERS = 0, 1
 CI_COMM_ID_BYTES = 128
+CI_FIRSTK_CODED, CI_FIRSTK_UNCODED = 0, 1
 CI_PREC_FP32, CI_PREC_BF16, CI_PREC_F16X2 = 0, 1, 2
 CI_ENC_EXACT, CI_ENC_LEARNED = 0, 1
 PRECISIONS = {"fp32": CI_PREC_FP32, "bf16": CI_PREC_BF16, "f16x2": CI_PREC_F16X2}
@@ -33,7 +34,8 @@ EXPORTS = ["ci_last_error", "ci_model_create", "ci_model_destroy", "ci_feature_d
            "ci_decode", "ci_classify", "ci_serve_group", "ci_workspace_size_host",
            "ci_serve_group_host", "ci_make_drops", "ci_comm_unique_id", "ci_comm_create", "ci_comm_destroy",
            "ci_workspace_size_general", "ci_encode_general", "ci_decode_general", "ci_serve_general",
-           "ci_encode_perturbed", "ci_online_update", "ci_serve_group_host_async"]
+           "ci_encode_perturbed", "ci_online_update", "ci_serve_group_host_async", "ci_workspace_size_first_k",
+           "ci_serve_first_k"]
 TESTING_EXPORTS = ["ci_test_prof_enable", "ci_test_prof_read", "ci_test_launch_count", "ci_test_mean",
                    "ci_test_plan", "ci_test_rendezvous"]  # include/codedinv_testing.h
 
@@ -69,6 +71,8 @@ _sig = {
     "ci_serve_group_host": (_I32, [_P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "ci_serve_group_host_async": (_I32, [_P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "ci_make_drops": (_I32, [_I32, _I64, ctypes.c_uint64, _P, _P]),
+    "ci_workspace_size_first_k": (_I32, [_P, _I32, _I32, _P]),
+    "ci_serve_first_k": (_I32, [_P, _I32, _I32, _I64, _P, _P, _I64, _I32, _P, _P, _P, _P, _P, _SZ, _P]),
     "ci_comm_unique_id": (_I32, [_P]),
     "ci_comm_create": (_I32, [_P, _I32, _I32, _I32, _I64, _I64, ctypes.c_int, _P]),
     "ci_comm_destroy": (None, [_P]),
@@ -149,7 +153,7 @@ class Model:
         self.d = int(_lib.ci_feature_dim(h))
 
     def close(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:   # (module globals may be gone at exit)
             _lib.ci_model_destroy(self._h)
             self._h = None
 
@@ -239,6 +243,22 @@ class Model:
                   _ptr(h_parity), _ptr(logits), _ptr(labels), _ptr(ws), ws.numel(), _stream(stream)),
                "ci_serve_group_host")
 
+    def workspace_first_k(self, k, max_inflight):
+        import torch
+        n = ctypes.c_size_t()
+        _check(_lib.ci_workspace_size_first_k(self._h, k, max_inflight, ctypes.byref(n)), "ci_workspace_size_first_k")
+        return torch.zeros(n.value, dtype=torch.uint8, device="cuda")
+
+    def ci_serve_first_k(self, x, straggler, delay_ns, features, logits, labels, records, ws, max_inflight=32,
+                         uncoded=False, stream=None):
+        """x [Q, k, C, H, W] device; straggler: numpy int32 [Q] (host); records int64 [Q, 4] device."""
+        Q, k = x.shape[0], x.shape[1]
+        st = np.ascontiguousarray(straggler, dtype=np.int32)
+        _check(_lib.ci_serve_first_k(self._h, CI_FIRSTK_UNCODED if uncoded else CI_FIRSTK_CODED, k, Q, _ptr(x),
+                                     _ptr(st), int(delay_ns), max_inflight, _ptr(features), _ptr(logits),
+                                     _ptr(labels), _ptr(records), _ptr(ws), ws.numel(), _stream(stream)),
+               "ci_serve_first_k")
+
     def ci_check(self, ws, stream=None):
         _check(_lib.ci_check(self._h, _ptr(ws), ws.numel(), _stream(stream)), "ci_check")
 
@@ -285,7 +305,7 @@ class Comm:
         self._h = h
 
     def close(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:
             _lib.ci_comm_destroy(self._h)
             self._h = None
 

@@ -2,6 +2,7 @@
 // orchestration of the coded path (see include/codedinv.h for the contract).
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -822,6 +823,152 @@ ci_status_t ci_test_mean(int32_t k, int64_t B, int64_t d, const float* h, float*
 int64_t ci_test_launch_count(int32_t reset) {
     long long v = reset ? g_launches.exchange(0) : g_launches.load();
     return (int64_t)v;
+}
+
+// --- first-k gated serving harness (f2) --------------------------------------------------
+// Workspace: (k+1) per-worker device workspaces for one-group calls | per in-flight slot: FkSlot,
+// worker results [k+1][d], estimates [k][d], x_p [din] | head pointer / class tables.
+struct FkLayout {
+    WsLayout w;          // one worker's workspace (B = 1 group)
+    size_t wstride = 0, slots = 0, sstride = 0, tables = 0, total = 0;
+};
+static FkLayout fk_layout(const Model* m, int32_t k, int32_t S) {
+    FkLayout F;
+    F.w = ws_layout(m, k, 1);
+    F.wstride = up(F.w.total);
+    F.slots = F.wstride * (size_t)(k + 1);
+    F.sstride = up(sizeof(FkSlot)) + up(sizeof(float) * (size_t)((2 * k + 1) * m->d)) + up(sizeof(float) * (size_t)m->din);
+    F.tables = F.slots + F.sstride * (size_t)S;
+    F.total = F.tables + up(4 * sizeof(void*) + 4 * sizeof(int));
+    return F;
+}
+
+ci_status_t ci_workspace_size_first_k(const ci_model_t* model, int32_t k, int32_t max_inflight, size_t* bytes) {
+    const Model* m = reinterpret_cast<const Model*>(model);
+    if (!m || !bytes || k < 1 || k > 30 || max_inflight < 1 || max_inflight > 256) {
+        set_error("invalid argument"); return CI_ERR_INVALID_ARG;
+    }
+    *bytes = fk_layout(m, k, max_inflight).total;
+    return CI_OK;
+}
+
+ci_status_t ci_serve_first_k(const ci_model_t* model, ci_firstk_mode_t mode, int32_t k, int64_t Q, const float* x,
+                             const int32_t* straggler, int64_t delay_ns, int32_t max_inflight, float* features,
+                             float* logits, int32_t* labels, int64_t* records, void* ws, size_t ws_bytes,
+                             ci_stream_t stream) {
+    CI_MODEL_OR_FAIL(m, model);
+    if ((mode != CI_FIRSTK_CODED && mode != CI_FIRSTK_UNCODED) || k < 1 || k > 30 || Q < 0 || delay_ns < 0 ||
+        max_inflight < 1 || max_inflight > 256 || m->d % 4 ||
+        (Q > 0 && (!x || !straggler || !features || !records || !aligned16(x) || !aligned16(features) ||
+                   (m->arch.n_heads > 0 && (!logits || !labels))))) {
+        set_error("invalid argument"); return CI_ERR_INVALID_ARG;
+    }
+    if (mode == CI_FIRSTK_CODED && m->enc_off < 0) {
+        set_error("coded first-k serving needs the learned encoder (the parity worker encodes from the raw "
+                  "queries, PAPER.md:667)");
+        return CI_ERR_UNSUPPORTED;
+    }
+    for (int64_t q = 0; q < Q; q++)
+        if (straggler[q] < -1 || straggler[q] >= k) { set_error("straggler[%lld] out of range", (long long)q); return CI_ERR_INVALID_ARG; }
+    {   // every worker / delay stream needs its own hardware queue: with shared queues a delayed
+        // worker's wait falsely blocks unrelated streams (measured: 30 ms stalls in other queries)
+        const char* env = getenv("CUDA_DEVICE_MAX_CONNECTIONS");
+        const int need = k + 2 + max_inflight, have = env ? atoi(env) : 8;
+        if (need > 32 || have < need) {
+            set_error("first-k serving needs CUDA_DEVICE_MAX_CONNECTIONS >= k + 2 + max_inflight = %d (<= 32) set "
+                      "before the CUDA context is created (have %d)", need, have);
+            return CI_ERR_UNSUPPORTED;
+        }
+    }
+    const int S = max_inflight;
+    FkLayout F = fk_layout(m, k, S);
+    if (!ws || !aligned16(ws) || ws_bytes < F.total) {
+        set_error("workspace %zu bytes; need %zu", ws_bytes, F.total); return CI_ERR_WORKSPACE;
+    }
+    if (Q == 0) return CI_OK;
+    cudaStream_t front = (cudaStream_t)stream;
+    const int nw = mode == CI_FIRSTK_CODED ? k + 1 : k;   // the uncoded arm has no parity worker
+    const int64_t d = m->d, din = m->din;
+    // head tables (device): weight pointers and class counts
+    const float** hw = at<const float*>(ws, F.tables);
+    int* hc = reinterpret_cast<int*>(hw + 4);
+    {
+        const float* hp[4] = {m->d_head[0], m->d_head[1], m->d_head[2], m->d_head[3]};
+        int cc[4] = {0, 0, 0, 0};
+        for (int t = 0; t < m->arch.n_heads; t++) cc[t] = m->arch.head_classes[t];
+        CI_CUDA(cudaMemcpyAsync(hw, hp, sizeof(hp), cudaMemcpyHostToDevice, front));
+        CI_CUDA(cudaMemcpyAsync(hc, cc, sizeof(cc), cudaMemcpyHostToDevice, front));
+        CI_CUDA(cudaStreamSynchronize(front));
+    }
+    std::vector<cudaStream_t> wst(nw), dst(S);
+    std::vector<cudaEvent_t> esub(S), eall(S), ework((size_t)S * nw);
+    ci_status_t rc = CI_OK;
+    auto cleanup = [&]() {
+        for (auto sv : wst) if (sv) cudaStreamDestroy(sv);
+        for (auto sv : dst) if (sv) cudaStreamDestroy(sv);
+        for (auto ev : esub) if (ev) cudaEventDestroy(ev);
+        for (auto ev : eall) if (ev) cudaEventDestroy(ev);
+        for (auto ev : ework) if (ev) cudaEventDestroy(ev);
+    };
+#define FK_CUDA(call)                                                   \
+    do {                                                                \
+        cudaError_t e_ = (call);                                        \
+        if (e_ != cudaSuccess) { rc = cuda_status(e_, #call); cleanup(); return rc; } \
+    } while (0)
+#define FK_OK(call)                                                     \
+    do {                                                                \
+        rc = (call);                                                    \
+        if (rc != CI_OK) { cleanup(); return rc; }                      \
+    } while (0)
+    for (auto& sv : wst) FK_CUDA(cudaStreamCreateWithFlags(&sv, cudaStreamNonBlocking));
+    for (auto& sv : dst) FK_CUDA(cudaStreamCreateWithFlags(&sv, cudaStreamNonBlocking));
+    for (auto& ev : esub) FK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    for (auto& ev : eall) FK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    for (auto& ev : ework) FK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    FK_CUDA(cudaEventRecord(esub[0], front));   // workers start after the caller's prior work
+    for (int w = 0; w < nw; w++) FK_CUDA(cudaStreamWaitEvent(wst[w], esub[0], 0));
+    for (int64_t q = 0; q < Q; q++) {
+        const int s_ = (int)(q % S);
+        if (q >= S) FK_CUDA(cudaEventSynchronize(eall[s_]));   // slot s_ free: its last query fully done
+        char* sb = at<char>(ws, F.slots + F.sstride * (size_t)s_);
+        FkSlot* slot = reinterpret_cast<FkSlot*>(sb);
+        float* hres = reinterpret_cast<float*>(sb + up(sizeof(FkSlot)));   // [k+1][d] worker results
+        float* est = hres + (size_t)(k + 1) * d;                              // [k][d]
+        float* xp = reinterpret_cast<float*>(sb + up(sizeof(FkSlot)) + up(sizeof(float) * (size_t)((2 * k + 1) * d)));
+        FK_CUDA(launch_fk_submit(slot, est, (int64_t)k * d, q, front));
+        FK_CUDA(cudaEventRecord(esub[s_], front));
+        for (int w = 0; w < nw; w++) {
+            cudaStream_t st = wst[w];
+            void* wsw = at<char>(ws, F.wstride * (size_t)w);
+            FK_CUDA(cudaStreamWaitEvent(st, esub[s_], 0));
+            FK_CUDA(zero_ctrs(wsw, F.w, st));
+            float* res = hres + (size_t)w * d;
+            if (w < k) {
+                FK_OK(forward_impl(m, x + (q * k + w) * din, res, 1, wsw, F.w, st));     // main worker w
+            } else {
+                FK_OK(encode_learned_impl(m, x + q * k * din, xp, k, 1, wsw, F.w, st));  // parity worker:
+                FK_OK(forward_impl(m, xp, res, 1, wsw, F.w, st));                        // Enc, then f
+            }
+            cudaStream_t ast = st;
+            if (w == straggler[q]) {   // its result reaches the decoder delay_ns late
+                FK_CUDA(cudaEventRecord(ework[(size_t)s_ * nw + w], st));
+                ast = dst[s_];
+                FK_CUDA(cudaStreamWaitEvent(ast, ework[(size_t)s_ * nw + w], 0));
+                FK_CUDA(launch_fk_delay(delay_ns, ast));
+            }
+            FK_CUDA(launch_fk_arrive(slot, est, res, w, k, d, mode == CI_FIRSTK_UNCODED, hw, hc, m->arch.n_heads,
+                                     features, logits, labels, Q, records, ast));
+            FK_CUDA(cudaEventRecord(ework[(size_t)s_ * nw + w], ast));
+        }
+        for (int w = 0; w < nw; w++) FK_CUDA(cudaStreamWaitEvent(dst[s_], ework[(size_t)s_ * nw + w], 0));
+        FK_CUDA(cudaEventRecord(eall[s_], dst[s_]));
+    }
+    for (int s2 = 0; s2 < S; s2++) FK_CUDA(cudaStreamWaitEvent(front, eall[s2], 0));
+    FK_CUDA(cudaStreamSynchronize(front));   // the harness owns its streams: finish before destroying them
+    cleanup();
+#undef FK_CUDA
+#undef FK_OK
+    return CI_OK;
 }
 
 ci_status_t ci_make_drops(int32_t k, int64_t B, uint64_t seed, int32_t* drop, ci_stream_t stream) {

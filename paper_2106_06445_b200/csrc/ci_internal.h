@@ -68,6 +68,19 @@ struct Comm {
     void** d_peers = nullptr;                // device copy of peers[]
     uint64_t epoch = 0;                      // serve calls issued on this communicator
 };
+// ---- first-k gated serving harness (firstk.cu; orchestration in api.cu)
+struct FkSlot {              // one in-flight query
+    uint64_t t_submit;       // device globaltimer at submission
+    int64_t q;               // query index using the slot
+    uint32_t recv, fin;      // tasks received (bit k = parity) / estimates finalised
+    int lock, complete;
+    int pad[2];
+};
+cudaError_t launch_fk_submit(FkSlot* slot, float* est, int64_t nest, int64_t q, cudaStream_t s);
+cudaError_t launch_fk_delay(int64_t delay_ns, cudaStream_t s);
+cudaError_t launch_fk_arrive(FkSlot* slot, float* est, const float* v, int j, int k, int64_t d, int need_mains,
+                             const float* const* heads_w, const int* head_c, int n_heads, float* feat_out,
+                             float* logits, int32_t* labels, int64_t Q, int64_t* rec, cudaStream_t s);
 ci_status_t comm_publish(Comm* c, const float* src, int64_t B, cudaStream_t st);
 ci_status_t comm_peer_mean(Comm* c, int k, int64_t B, float* mean, cudaStream_t st);
 ci_status_t comm_peer_decode(Comm* c, int k, int64_t B, const int32_t* drop, float* out, int* flag,
