@@ -72,7 +72,7 @@ static WsLayout ws_layout(const Model* m, int32_t k, int64_t B, bool groups = tr
     L.enc = off;
     if (m->enc_off >= 0 && groups) {   // m, z, z2, z3, u of the learned encoder
         const int64_t HW = (int64_t)m->arch.in_h * m->arch.in_w;
-        const int64_t per = HW * (4 * m->arch.enc_c1) + HW / 4 * m->arch.enc_mid + 64;   // m, zbuf, z2, u
+        const int64_t per = HW * (3 * m->arch.enc_c1) + 64;   // m [c1][H][W], zbuf [8 c1][H/2][W/2]
         off += up(sizeof(float) * (size_t)(std::max<int64_t>(B, 1) * per));
     }
     L.total = off;
@@ -132,22 +132,18 @@ static ci_status_t encode_learned_impl(const Model* m, const float* x, float* xp
     const ci_arch_t& a = m->arch;
     const int Ci = a.in_c, H = a.in_h, W = a.in_w, c1 = a.enc_c1, mid = a.enc_mid;
     const int64_t HW = (int64_t)H * W, hw4 = HW / 4;
-    const float* E1W = m->d_params + m->enc_off;
+    const float* E1W = m->enc_host.data();                         // host copies: kernel parameters
     const float* E1b = E1W + (int64_t)c1 * Ci * 9;
-    // E2 / E3 are packed into the model's tcgen05 weight stream (umma_prepare)
-    const float* E4W = E1b + c1 + (int64_t)mid * 4 * c1 * 9 + mid + (int64_t)4 * c1 * mid * 9 + 4 * c1;
+    const float* E4W = E1b + c1;
     const float* E4b = E4W + (int64_t)Ci * c1 * 9;
-    // workspace: m [B][c1][H][W] | zbuf [B][8c1][H/2][W/2] (tail in | out) | z2 [B][mid][..] | u
+    // workspace: m [B][c1][H][W] | zbuf [B][8c1][H/2][W/2] (tail in | out, in place)
     float* Mb = at<float>(ws, L.enc);
     float* Zb = Mb + B * c1 * HW;
     const int64_t zstride = 8 * c1 * hw4;
-    float* Z2 = Zb + B * zstride;
-    float* U = Z2 + B * mid * hw4;
-    CI_CUDA(launch_enc_e1_mean(x, k, B, Ci, H, W, E1W, E1b, c1, Mb, Zb, zstride, st));
-    ci_status_t r = umma_encoder_tail(m, Zb, B, next_ctr(ws, L), st);   // tcgen05: ReLU(E3(ReLU(E2 z)))
+    CI_CUDA(launch_enc_e1_mean(x, k, B, Ci, H, W, E1W, E1b, c1, Mb, Zb, zstride, st));   // E1, mean, psi
+    ci_status_t r = umma_encoder_tail(m, Zb, B, next_ctr(ws, L), st);              // ReLU(E3(ReLU(E2 z)))
     if (r != CI_OK) return r;
-    CI_CUDA(launch_unsqueeze_add(Zb + 4 * c1 * hw4, zstride, Mb, U, B, c1, H, W, st));
-    CI_CUDA(launch_conv_simt(U, c1 * HW, c1, H, W, E4W, E4b, Ci, xp, Ci * HW, B, 0, 2, st));
+    CI_CUDA(launch_enc_out(Zb + 4 * c1 * hw4, zstride, Mb, B, Ci, c1, H, W, E4W, E4b, xp, st));   // psi^-1 + skip, E4
     return CI_OK;
 }
 
@@ -217,11 +213,27 @@ ci_status_t ci_model_create(const ci_arch_t* arch, const float* host_params, siz
         if (a.enc_c1 < 1 || a.enc_mid < 1 || a.in_h % 2 || a.in_w % 2) {
             delete m; set_error("invalid learned encoder widths"); return CI_ERR_INVALID_SHAPE;
         }
+        if (!enc_supported(a.in_c, a.enc_c1, a.in_h, a.in_w)) {
+            delete m;
+            set_error("learned encoder: in_c must be 3, enc_c1 4, 8 or 16, in_w a multiple of 4");
+            return CI_ERR_UNSUPPORTED;
+        }
         m->enc_off = off;
         off += (int64_t)a.enc_c1 * a.in_c * 9 + a.enc_c1 + (int64_t)a.enc_mid * 4 * a.enc_c1 * 9 + a.enc_mid +
                (int64_t)4 * a.enc_c1 * a.enc_mid * 9 + 4 * a.enc_c1 + (int64_t)a.in_c * a.enc_c1 * 9 + a.in_c;
     }
     m->n_params = off;
+    if (m->enc_off >= 0) {   // E1 (W, b) and E4 (W, b) travel as kernel parameters
+        const ci_arch_t& e = a;
+        const float* p0 = host_params + m->enc_off;
+        const int64_t n1 = (int64_t)e.enc_c1 * e.in_c * 9 + e.enc_c1;
+        const int64_t mid = (int64_t)e.enc_mid * 4 * e.enc_c1 * 9 + e.enc_mid + (int64_t)4 * e.enc_c1 * e.enc_mid * 9 + 4 * e.enc_c1;
+        const int64_t n4 = (int64_t)e.in_c * e.enc_c1 * 9 + e.in_c;
+        if ((size_t)off == n_params) {
+            m->enc_host.assign(p0, p0 + n1);
+            m->enc_host.insert(m->enc_host.end(), p0 + n1 + mid, p0 + n1 + mid + n4);
+        }
+    }
     if ((size_t)off != n_params) {
         delete m;
         set_error("n_params %zu != %lld implied by arch", n_params, (long long)off);

@@ -46,6 +46,7 @@ struct Model {
     int64_t head_off[4] = {0, 0, 0, 0};
     float* d_head[4] = {nullptr, nullptr, nullptr, nullptr};  // 16-B aligned copy: W [C][d], then b [C]
     int64_t enc_off = -1;                    // learned encoder params (float offset), -1 = none
+    std::vector<float> enc_host;             // host copy of E1 W, b and E4 W, b (kernel parameters)
     // tcgen05 path
     uint16_t* d_wpack = nullptr;             // packed bf16 / fp16 weights (k_umma.cu pack_block)
     float* d_bias = nullptr;                 // padded biases
@@ -98,10 +99,6 @@ cudaError_t launch_permute(const float* in, float* out, int64_t n, int C, int H,
 //                            out += conv(in) + b       (mode 1)
 //                            out -= conv(in) + b       (mode 2)
 //                            out = base - conv(in) - b (mode 3, residual fixed-point update)
-cudaError_t launch_conv_simt(const float* in, int64_t in_stride, int Cin, int H, int W,
-                             const float* Wt, const float* b, int Cout, float* out,
-                             int64_t out_stride, int64_t n, int mode, int act, cudaStream_t s,
-                             const float* base = nullptr);
 // m = (sum_i h_i) / k  (+ eps when given: perturbed encode, f4)
 cudaError_t launch_mean(const float* h, float* m, int k, int64_t B, int64_t d, cudaStream_t s,
                         const float* eps = nullptr);
@@ -118,10 +115,12 @@ cudaError_t launch_combine_general(const float* h, const float* coef, float* out
                                    int64_t d, cudaStream_t s);
 cudaError_t launch_decode_general(float* h, const float* hp, const float* coef, const uint32_t* avail, int k, int r,
                                   int64_t B, int64_t d, int* flag, cudaStream_t s);
-cudaError_t launch_enc_e1_mean(const float* x, int k, int64_t B, int Ci, int H, int W, const float* W1,
-                               const float* b1, int C1, float* m, float* zpsi, int64_t zstride, cudaStream_t s);
-cudaError_t launch_unsqueeze_add(const float* z, int64_t zstride, const float* m, float* u, int64_t B, int C,
-                                 int H, int W, cudaStream_t s);
+// learned encoder (k_encoder.cu): weights are HOST pointers (passed as kernel parameters)
+bool enc_supported(int Ci, int C1, int H, int W);
+cudaError_t launch_enc_e1_mean(const float* x, int k, int64_t B, int Ci, int H, int W, const float* hw1,
+                               const float* hb1, int C1, float* m, float* zpsi, int64_t zstride, cudaStream_t s);
+cudaError_t launch_enc_out(const float* z, int64_t zstride, const float* m, int64_t B, int Ci, int C1, int H, int W,
+                           const float* hw4, const float* hb4, float* xp, cudaStream_t s);
 
 // tcgen05 path (k_umma.cu)
 ci_status_t umma_prepare(Model* m, const float* host_params);

@@ -1,111 +1,146 @@
-// Light learned encoder (Arch E, CI_ENC_LEARNED): the parts that are not the conv->ReLU->conv
-// tail (which runs on tcgen05 through the fused stage kernel, umma_encoder_tail):
-//   k_enc_e1_mean  : m[b] = (1/k) sum_i ReLU(conv3x3(E1, x_{b,i}))  -- weight-shared first layer
-//                    on every input, averaged after it; fp32, ascending i.  One
-//                    thread per output pixel computes all C1 channels (inputs read once per
-//                    image, register-tiled).  Also writes psi(m) into the encoder-tail buffer.
-//   k_unsqueeze_add: u = psi^-1(z) + m  (U-Net-style skip, SURVEY Arch E)
-// E4 (c1 -> in_c, ~1% of the encoder FLOPs) uses the fp32 direct-convolution kernel.
+// Light learned encoder (Arch E, CI_ENC_LEARNED): the CUDA-core parts around
+// the conv->ReLU->conv tail (which runs on tcgen05 through the fused stage kernel,
+// umma_encoder_tail):
+//   k_enc_e1_mean : m[b] = (1/k) sum_i ReLU(conv3x3(E1, x_{b,i}))  -- weight-shared first layer on
+//                   every input, averaged after it; also writes psi(m), the tail's
+//                   input.  fp32, summation over i ascending.
+//   k_enc_out     : x_p = conv3x3(E4, psi^-1(z) + m)  -- the U-Net-style skip fused into E4: the
+//                   CTA of group b builds u = psi^-1(z) + m in shared memory, then every thread
+//                   computes the in_c outputs of four pixels (no u round trip through HBM).
+// Both hold their (small) weights in the kernel parameter space -- the constant bank, so every
+// FFMA reads its weight as an immediate constant-bank operand: no load instruction per MAC.
 #include "ci_internal.h"
 
 namespace ci {
 
 template <int CI, int C1>
-__global__ void __launch_bounds__(128) k_enc_e1_mean(const float* __restrict__ x, int k, int64_t B, int H, int W,
-                                                     const float* __restrict__ W1, const float* __restrict__ b1,
+struct E1Params {
+    float w[C1 * CI * 9];   // [C1][CI][3][3]
+    float b[C1];
+};
+template <int CI, int C1>
+struct E4Params {
+    float w[CI * C1 * 9];   // [CI][C1][3][3]
+    float b[CI];
+};
+
+// thread -> 4 horizontally adjacent pixels of group b's image plane, all C1 channels
+template <int CI, int C1>
+__global__ void __launch_bounds__(256) k_enc_e1_mean(const float* __restrict__ x, int k, int64_t B, int H, int W,
+                                                     const __grid_constant__ E1Params<CI, C1> p,
                                                      float* __restrict__ m, float* __restrict__ zpsi,
                                                      int64_t zstride) {
-    __shared__ float sw[C1 * CI * 9 + C1];
-    for (int i = threadIdx.x; i < C1 * CI * 9 + C1; i += blockDim.x)
-        sw[i] = i < C1 * CI * 9 ? W1[i] : b1[i - C1 * CI * 9];
-    __syncthreads();
+    constexpr int PX = 4;
     const int64_t HW = (int64_t)H * W;
-    const int Ho = H / 2, Wo = W / 2;
+    const int Ho = H / 2, Wo = W / 2, wq = W / PX;
     const float fk = (float)k;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < B * HW;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t b = idx / HW;
-        const int rem = (int)(idx - b * HW);
-        const int y = rem / W, xx = rem - (rem / W) * W;
-        float sum[C1];
+    const int64_t units = B * (int64_t)H * wq;
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < units; u += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = u / ((int64_t)H * wq);
+        const int r = (int)(u - b * H * wq);
+        const int y = r / wq, x0 = (r - y * wq) * PX;
+        float sum[C1][PX];
 #pragma unroll
-        for (int o = 0; o < C1; o++) sum[o] = 0.f;
-        for (int q = 0; q < k; q++) {
-            const float* xq = x + (b * k + q) * CI * HW;
-            float in[CI * 9];
+        for (int o = 0; o < C1; o++)
+#pragma unroll
+            for (int q = 0; q < PX; q++) sum[o][q] = 0.f;
+        for (int i = 0; i < k; i++) {
+            const float* xi = x + (b * k + i) * CI * HW;
+            float in[CI][3][PX + 2];   // rows y-1..y+1, columns x0-1 .. x0+PX (zero outside)
 #pragma unroll
             for (int c = 0; c < CI; c++)
 #pragma unroll
-                for (int u = 0; u < 3; u++)
+                for (int uu = 0; uu < 3; uu++) {
+                    const int yy = y + uu - 1;
+                    const bool rowok = yy >= 0 && yy < H;
 #pragma unroll
-                    for (int v = 0; v < 3; v++) {
-                        const int ii = y + u - 1, jj = xx + v - 1;
-                        in[(c * 3 + u) * 3 + v] =
-                            (ii >= 0 && ii < H && jj >= 0 && jj < W) ? __ldg(xq + c * HW + ii * W + jj) : 0.f;
+                    for (int j = 0; j < PX + 2; j++) {
+                        const int xx = x0 + j - 1;
+                        in[c][uu][j] = (rowok && xx >= 0 && xx < W) ? __ldg(xi + c * HW + yy * W + xx) : 0.f;
                     }
+                }
 #pragma unroll
             for (int o = 0; o < C1; o++) {
-                float acc = 0.f;
 #pragma unroll
-                for (int t = 0; t < CI * 9; t++) acc = fmaf(sw[o * CI * 9 + t], in[t], acc);
-                sum[o] = __fadd_rn(sum[o], fmaxf(acc + sw[C1 * CI * 9 + o], 0.f));
+                for (int q = 0; q < PX; q++) {
+                    float acc = 0.f;   // taps in (c, u, v) order, then the bias
+#pragma unroll
+                    for (int c = 0; c < CI; c++)
+#pragma unroll
+                        for (int uu = 0; uu < 3; uu++)
+#pragma unroll
+                            for (int v = 0; v < 3; v++) acc = fmaf(p.w[((o * CI + c) * 3 + uu) * 3 + v], in[c][uu][q + v], acc);
+                    sum[o][q] = __fadd_rn(sum[o][q], fmaxf(acc + p.b[o], 0.f));
+                }
             }
         }
         float* zb = zpsi + b * zstride;
 #pragma unroll
         for (int o = 0; o < C1; o++) {
-            const float mv = __fdiv_rn(sum[o], fk);
-            m[(b * C1 + o) * HW + rem] = mv;
-            zb[((int64_t)(o * 4 + 2 * (y & 1) + (xx & 1)) * Ho + (y >> 1)) * Wo + (xx >> 1)] = mv;
+            float mv[PX];
+#pragma unroll
+            for (int q = 0; q < PX; q++) mv[q] = __fdiv_rn(sum[o][q], fk);
+            *reinterpret_cast<float4*>(m + (b * C1 + o) * HW + y * W + x0) = make_float4(mv[0], mv[1], mv[2], mv[3]);
+            // psi: pixel (y, x) -> channel 4o + 2(y&1) + (x&1) at (y/2, x/2); x0 is even
+            float* z0 = zb + ((int64_t)(o * 4 + 2 * (y & 1)) * Ho + (y >> 1)) * Wo + (x0 >> 1);
+            *reinterpret_cast<float2*>(z0) = make_float2(mv[0], mv[2]);
+            *reinterpret_cast<float2*>(z0 + (int64_t)Ho * Wo) = make_float2(mv[1], mv[3]);
         }
     }
 }
 
-// generic fallback (any CI <= 4, C1 <= 32)
-__global__ void k_enc_e1_mean_generic(const float* __restrict__ x, int k, int64_t B, int CI, int H, int W,
-                                      const float* __restrict__ W1, const float* __restrict__ b1, int C1,
-                                      float* __restrict__ m, float* __restrict__ zpsi, int64_t zstride) {
+// one CTA per group (grid-stride): u = psi^-1(z) + m in shared memory [C1][H+2][W+2] (zero
+// border), then x_p[o] = b[o] + sum_{c,u,v} E4[o][c][u][v] u[c][y+u-1][x+v-1]
+template <int CI, int C1>
+__global__ void __launch_bounds__(256) k_enc_out(const float* __restrict__ z, int64_t zstride,
+                                                 const float* __restrict__ m, int64_t B, int H, int W,
+                                                 const __grid_constant__ E4Params<CI, C1> p, float* __restrict__ xp) {
+    constexpr int PX = 4;
+    extern __shared__ float us[];
+    const int Hp = H + 2, Wp = W + 2;
     const int64_t HW = (int64_t)H * W;
     const int Ho = H / 2, Wo = W / 2;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < B * C1 * HW;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t b = idx / (C1 * HW);
-        const int r = (int)(idx - b * C1 * HW);
-        const int o = r / (int)HW, rem = r - o * (int)HW;
-        const int y = rem / W, xx = rem - (rem / W) * W;
-        float sum = 0.f;
-        for (int q = 0; q < k; q++) {
-            const float* xq = x + (b * k + q) * CI * HW;
-            float acc = 0.f;
-            for (int c = 0; c < CI; c++)
-                for (int u = -1; u <= 1; u++)
-                    for (int v = -1; v <= 1; v++) {
-                        const int ii = y + u, jj = xx + v;
-                        if (ii < 0 || ii >= H || jj < 0 || jj >= W) continue;
-                        acc = fmaf(W1[((o * CI + c) * 3 + u + 1) * 3 + v + 1], xq[c * HW + ii * W + jj], acc);
-                    }
-            sum = __fadd_rn(sum, fmaxf(acc + b1[o], 0.f));
+    for (int i = threadIdx.x; i < C1 * Hp * Wp; i += blockDim.x) us[i] = 0.f;
+    for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
+        __syncthreads();   // the previous group's reads are done
+        const float* zb = z + b * zstride;
+        const float* mb = m + b * C1 * HW;
+        for (int i = threadIdx.x; i < C1 * (int)HW; i += blockDim.x) {   // m-order: coalesced m reads
+            const int c = i / (int)HW, rem = i - c * (int)HW, y = rem / W, xx = rem - y * W;
+            const float zv = zb[((int64_t)(c * 4 + 2 * (y & 1) + (xx & 1)) * Ho + (y >> 1)) * Wo + (xx >> 1)];
+            us[(c * Hp + y + 1) * Wp + xx + 1] = zv + mb[i];
         }
-        const float mv = __fdiv_rn(sum, (float)k);
-        m[idx] = mv;
-        zpsi[b * zstride + ((int64_t)(o * 4 + 2 * (y & 1) + (xx & 1)) * Ho + (y >> 1)) * Wo + (xx >> 1)] = mv;
-    }
-}
-
-// u[b][c][y][x] = z[b][4c + 2(y&1) + (x&1)][y/2][x/2] + m[b][c][y][x]   (z rows at zstride)
-__global__ void k_unsqueeze_add(const float* __restrict__ z, int64_t zstride, const float* __restrict__ m,
-                                float* __restrict__ u, int64_t B, int C, int H, int W) {
-    const int64_t HW = (int64_t)H * W, total = B * C * HW;
-    const int Ho = H / 2, Wo = W / 2;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t b = idx / (C * HW);
-        const int r = (int)(idx - b * C * HW);
-        const int c = r / (int)HW;
-        const int rem = r - c * (int)HW;
-        const int y = rem / W, xx = rem - (rem / W) * W;
-        const int zc = c * 4 + 2 * (y & 1) + (xx & 1);
-        u[idx] = z[b * zstride + ((int64_t)zc * Ho + (y >> 1)) * Wo + (xx >> 1)] + m[idx];
+        __syncthreads();
+        const int wq = W / PX;
+        for (int t = threadIdx.x; t < H * wq; t += blockDim.x) {
+            const int y = t / wq, x0 = (t - y * wq) * PX;
+            float acc[CI][PX];
+#pragma unroll
+            for (int o = 0; o < CI; o++)
+#pragma unroll
+                for (int q = 0; q < PX; q++) acc[o][q] = 0.f;
+#pragma unroll 4
+            for (int c = 0; c < C1; c++) {
+                float win[3][PX + 2];
+#pragma unroll
+                for (int uu = 0; uu < 3; uu++)
+#pragma unroll
+                    for (int j = 0; j < PX + 2; j++) win[uu][j] = us[(c * Hp + y + uu) * Wp + x0 + j];
+#pragma unroll
+                for (int o = 0; o < CI; o++)
+#pragma unroll
+                    for (int q = 0; q < PX; q++)
+#pragma unroll
+                        for (int uu = 0; uu < 3; uu++)
+#pragma unroll
+                            for (int v = 0; v < 3; v++) acc[o][q] = fmaf(p.w[((o * C1 + c) * 3 + uu) * 3 + v], win[uu][q + v], acc[o][q]);
+            }
+            float* ob = xp + b * CI * HW + y * W + x0;
+#pragma unroll
+            for (int o = 0; o < CI; o++)   // identity activation on the encoder output
+                *reinterpret_cast<float4*>(ob + o * HW) =
+                    make_float4(acc[o][0] + p.b[o], acc[o][1] + p.b[o], acc[o][2] + p.b[o], acc[o][3] + p.b[o]);
+        }
     }
 }
 
@@ -115,28 +150,59 @@ static int grid_of(int64_t total, int block) {
     return (int)(g < 1 ? 1 : g);
 }
 
-cudaError_t launch_enc_e1_mean(const float* x, int k, int64_t B, int Ci, int H, int W, const float* W1,
-                               const float* b1, int C1, float* m, float* zpsi, int64_t zstride, cudaStream_t s) {
-    const int64_t npix = B * (int64_t)H * W;
-    if (npix == 0) return cudaSuccess;
-    if (Ci == 3 && C1 == 16)
-        k_enc_e1_mean<3, 16><<<grid_of(npix, 128), 128, 0, s>>>(x, k, B, H, W, W1, b1, m, zpsi, zstride);
-    else if (Ci == 3 && C1 == 4)
-        k_enc_e1_mean<3, 4><<<grid_of(npix, 128), 128, 0, s>>>(x, k, B, H, W, W1, b1, m, zpsi, zstride);
-    else
-        k_enc_e1_mean_generic<<<grid_of(npix * C1, 256), 256, 0, s>>>(x, k, B, Ci, H, W, W1, b1, C1, m, zpsi,
-                                                                      zstride);
-    count_launch();
+bool enc_supported(int Ci, int C1, int H, int W) {
+    return Ci == 3 && (C1 == 4 || C1 == 8 || C1 == 16) && W % 4 == 0 && H % 2 == 0 &&
+           (size_t)C1 * (H + 2) * (W + 2) * sizeof(float) <= 200 * 1024;
+}
+
+template <int CI, int C1>
+static cudaError_t e1_t(const float* x, int k, int64_t B, int H, int W, const float* hw1, const float* hb1, float* m,
+                        float* zpsi, int64_t zstride, cudaStream_t s) {
+    E1Params<CI, C1> p;
+    memcpy(p.w, hw1, sizeof(p.w));
+    memcpy(p.b, hb1, sizeof(p.b));
+    k_enc_e1_mean<CI, C1><<<grid_of(B * (int64_t)H * (W / 4), 256), 256, 0, s>>>(x, k, B, H, W, p, m, zpsi, zstride);
     return cudaGetLastError();
 }
 
-cudaError_t launch_unsqueeze_add(const float* z, int64_t zstride, const float* m, float* u, int64_t B, int C,
-                                 int H, int W, cudaStream_t s) {
-    const int64_t total = B * C * (int64_t)H * W;
-    if (total == 0) return cudaSuccess;
-    k_unsqueeze_add<<<grid_of(total, 256), 256, 0, s>>>(z, zstride, m, u, B, C, H, W);
+cudaError_t launch_enc_e1_mean(const float* x, int k, int64_t B, int Ci, int H, int W, const float* hw1,
+                               const float* hb1, int C1, float* m, float* zpsi, int64_t zstride, cudaStream_t s) {
+    if (B == 0) return cudaSuccess;
+    cudaError_t e = cudaErrorInvalidValue;
+    if (Ci == 3 && C1 == 16) e = e1_t<3, 16>(x, k, B, H, W, hw1, hb1, m, zpsi, zstride, s);
+    else if (Ci == 3 && C1 == 8) e = e1_t<3, 8>(x, k, B, H, W, hw1, hb1, m, zpsi, zstride, s);
+    else if (Ci == 3 && C1 == 4) e = e1_t<3, 4>(x, k, B, H, W, hw1, hb1, m, zpsi, zstride, s);
     count_launch();
+    return e;
+}
+
+template <int CI, int C1>
+static cudaError_t out_t(const float* z, int64_t zstride, const float* m, int64_t B, int H, int W, const float* hw4,
+                         const float* hb4, float* xp, cudaStream_t s) {
+    E4Params<CI, C1> p;
+    memcpy(p.w, hw4, sizeof(p.w));
+    memcpy(p.b, hb4, sizeof(p.b));
+    const size_t smem = (size_t)C1 * (H + 2) * (W + 2) * sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_enc_out<CI, C1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const int grid = (int)std::min<int64_t>(B, 148 * 3);
+    k_enc_out<CI, C1><<<grid, 256, smem, s>>>(z, zstride, m, B, H, W, p, xp);
     return cudaGetLastError();
+}
+
+cudaError_t launch_enc_out(const float* z, int64_t zstride, const float* m, int64_t B, int Ci, int C1, int H, int W,
+                           const float* hw4, const float* hb4, float* xp, cudaStream_t s) {
+    if (B == 0) return cudaSuccess;
+    cudaError_t e = cudaErrorInvalidValue;
+    if (Ci == 3 && C1 == 16) e = out_t<3, 16>(z, zstride, m, B, H, W, hw4, hb4, xp, s);
+    else if (Ci == 3 && C1 == 8) e = out_t<3, 8>(z, zstride, m, B, H, W, hw4, hb4, xp, s);
+    else if (Ci == 3 && C1 == 4) e = out_t<3, 4>(z, zstride, m, B, H, W, hw4, hb4, xp, s);
+    count_launch();
+    return e;
 }
 
 }  // namespace ci

@@ -1,5 +1,5 @@
-// CUDA-core kernels: stage-layout permutations (psi / psi^-1) and the fp32 direct
-// convolution used by the CI_PREC_SIMT cross-check mode.
+// Stage-boundary permutations of the fp32 state: psi (space-to-depth r = 2, torch
+// pixel_unshuffle order), psi^-1 and the identity copy (i-RevNet's squeeze).
 #include "ci_internal.h"
 
 namespace ci {
@@ -95,69 +95,6 @@ cudaError_t launch_permute(const float* in, float* out, int64_t n, int C, int H,
     int64_t blocks = (total + 255) / 256;
     if (blocks > 148 * 64) blocks = 148 * 64;
     k_permute<<<(unsigned)blocks, 256, 0, s>>>(in, out, total, C, H, W, mode);
-    count_launch();
-    return cudaGetLastError();
-}
-
-// y[o][i][j] = b[o] + sum_c sum_{u,v} W[o][c][u+1][v+1] x[c][i+u][j+v]   (zero padding)
-// Accumulation order (c ascending, u, v ascending) is fixed -> deterministic.
-__global__ void k_conv_simt(const float* __restrict__ in, int64_t in_stride, int Cin, int H, int W,
-                            const float* __restrict__ Wt, const float* __restrict__ b, int Cout,
-                            float* __restrict__ out, int64_t out_stride, int64_t n, int mode,
-                            int act, const float* __restrict__ base) {
-    const int64_t per = (int64_t)Cout * H * W;
-    const int64_t total = n * per;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        int64_t img = idx / per;
-        int r = (int)(idx - img * per);
-        int o = r / (H * W);
-        int rem = r - o * H * W;
-        int i = rem / W, j = rem - (rem / W) * W;
-        const float* x = in + img * in_stride;
-        const float* w = Wt + (int64_t)o * Cin * 9;
-        float acc = 0.f;
-        for (int c = 0; c < Cin; c++) {
-            const float* xc = x + (int64_t)c * H * W;
-            const float* wc = w + c * 9;
-#pragma unroll
-            for (int u = -1; u <= 1; u++) {
-                int ii = i + u;
-                if (ii < 0 || ii >= H) continue;
-#pragma unroll
-                for (int v = -1; v <= 1; v++) {
-                    int jj = j + v;
-                    if (jj < 0 || jj >= W) continue;
-                    acc = fmaf(__ldg(wc + (u + 1) * 3 + (v + 1)), xc[ii * W + jj], acc);
-                }
-            }
-        }
-        float y = acc + __ldg(b + o);
-        float* dst = out + img * out_stride + r;
-        if (mode == 0) {
-            if (act == 0) y = fmaxf(y, 0.f);
-            else if (act == 1) y = y > 0.f ? y : expm1f(y);   // ELU
-            *dst = y;
-        } else if (mode == 1) {
-            *dst = *dst + y;
-        } else if (mode == 2) {
-            *dst = *dst - y;
-        } else {   // 3: fixed-point update out = base - conv(in)   (base has out's layout)
-            *dst = base[img * out_stride + r] - y;
-        }
-    }
-}
-
-cudaError_t launch_conv_simt(const float* in, int64_t in_stride, int Cin, int H, int W,
-                             const float* Wt, const float* b, int Cout, float* out,
-                             int64_t out_stride, int64_t n, int mode, int act, cudaStream_t s,
-                             const float* base) {
-    int64_t total = n * (int64_t)Cout * H * W;
-    if (total == 0) return cudaSuccess;
-    int64_t blocks = (total + 255) / 256;
-    if (blocks > 148 * 32) blocks = 148 * 32;
-    k_conv_simt<<<(unsigned)blocks, 256, 0, s>>>(in, in_stride, Cin, H, W, Wt, b, Cout, out,
-                                                 out_stride, n, mode, act, base);
     count_launch();
     return cudaGetLastError();
 }
