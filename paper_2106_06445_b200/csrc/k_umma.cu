@@ -416,6 +416,11 @@ struct SCfg {
 #endif
 };
 using SDyn = SCfg<0, 0, 0, 0, 0, 0, 0>;
+#ifdef CI_NO_XPREF
+constexpr bool kXPrefetch = false;   // A/B switch
+#else
+constexpr bool kXPrefetch = true;    // cross-batch X prefetch (epilogue, see x_pref)
+#endif
 constexpr int kMaxTiles = 8;                     // T <= 8 (512 TMEM columns / >= 64 per tile)
 constexpr int kBarBytes = 1024;                  // mbarriers, TMEM slot, batch queue, staged conv2 bias
 
@@ -989,6 +994,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                    cw1 - g0 < 32 ? cw1 - g0 : 32);
         }
         tmem_wait_st();
+        // X planes <- the first processed block's input half of the batch state at stb (nimg images)
+        auto load_x = [&](const float* stb, int nimg) {
+            const int t0 = a.inverse ? a.nb - 1 : 0;
+            const int in_off = (residual || ((a.first_orient + t0) & 1) == 0) ? 0 : ec;
+            for (int tile = 0; tile < eT; tile++) {
+                int r = tile * 128 + row_in_tile, ii, y, x;
+                if (!rowpix(r, ii, y, x) || ii >= nimg) continue;
+                const float* src = stb + ((int64_t)ii * a.C + in_off) * eHW + y * eW + x;
+                for (int pl = half; pl < eCp / 8; pl += 2) {
+                    float v8[8];
+#pragma unroll
+                    for (int e = 0; e < 8; e++)
+                        v8[e] = (pl * 8 + e < ec) ? src[(int64_t)(pl * 8 + e) * eHW]
+                                                  : ((efold && pl * 8 + e == ec) ? 1.f : 0.f);
+                    store8(xbuf, xlo_buf, pl, r, v8);
+                }
+            }
+            fence_proxy_async();
+            for (int t = 0; t < eT; t++) mbar_arrive(&x_tile[t]);
+        };
+        // Cross-batch X prefetch: once the last block's last conv1 chunk has completed (its epilogue
+        // has waited for it) nothing reads the X planes of this batch any more, so the next batch's
+        // input is loaded there right away -- its first conv1 chunk then runs on the tensor core
+        // while this batch's last conv2 and its epilogue are still in flight.  acc1 is free (read),
+        // acc2 / the hidden buffers are only touched after this batch's conv2 epilogue.
+        bool x_pref = false;
         for (int qi = 0;; qi++) {
             const int64_t b = bq_read(qi);
             if (b >= nbatch) break;
@@ -1024,26 +1055,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                 asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads));
             }
             float* stb = esst ? sst : a.state + img0 * a.C * eHW;
-            // ---- load bf16(s_in) of the first processed block into the X planes (planes split by half)
-            {
-                const int t0 = a.inverse ? a.nb - 1 : 0;
-                const int in_off = (residual || ((a.first_orient + t0) & 1) == 0) ? 0 : ec;
-                for (int tile = 0; tile < eT; tile++) {
-                    int r = tile * 128 + row_in_tile, ii, y, x;
-                    if (!rowpix(r, ii, y, x) || ii >= nimg) continue;
-                    const float* src = stb + ((int64_t)ii * a.C + in_off) * eHW + y * eW + x;
-                    for (int pl = half; pl < eCp / 8; pl += 2) {
-                        float v8[8];
-#pragma unroll
-                        for (int e = 0; e < 8; e++)
-                            v8[e] = (pl * 8 + e < ec) ? src[(int64_t)(pl * 8 + e) * eHW]
-                                                      : ((efold && pl * 8 + e == ec) ? 1.f : 0.f);
-                        store8(xbuf, xlo_buf, pl, r, v8);
-                    }
-                }
-                fence_proxy_async();
-                for (int t = 0; t < eT; t++) mbar_arrive(&x_tile[t]);
-            }
+            // ---- bf16 / fp16 (s_in) of the first processed block into the X planes (planes split by
+            // half) -- unless the previous batch already prefetched them (see x_pref below)
+            if (!x_pref) load_x(stb, nimg);
+            x_pref = false;
             t_ld += CLK() - tl0;
             for (int tt = 0; tt < nbv; tt++) {
                 const int t = a.inverse ? a.nb - 1 - tt / R : tt / R;
@@ -1261,6 +1276,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                         mbar_arrive(&hd_full[hb_i]);
                     }
                     t_e1 += CLK() - te0;
+                    if (kXPrefetch && tt == nbv - 1 && j == p.nch - 1 && bnext < nbatch) {
+                        const int64_t img1 = bnext * p.I;
+                        load_x(a.state + img1 * a.C * eHW, (int)(a.n - img1 < (int64_t)p.I ? a.n - img1 : (int64_t)p.I));
+                        x_pref = true;
+                    }
                 }
                 // ---- conv2 epilogue: s_out (+|-)= acc2 + b2 (fp32); bf16(s_out) -> X
                 const bool write_x = tt + 1 < nbv;
@@ -1864,7 +1884,23 @@ static bool make_plan(const StageInfo& S, int pm, StagePlan& best) {
     static const bool s1_mc32 = getenv("CI_S1_MC32") != nullptr;           // A/B switch
     static const bool s1_mc64 = getenv("CI_S1_MC64") != nullptr;           // A/B switch
     static const bool no_tuned = getenv("CI_NO_TUNED") != nullptr;         // A/B switch: cost model only
+    // CI_TUNE="H,W,c,m,pm,MC,T,nhd,nslot,hst;..." overrides the table (same-box plan A/B)
+    static const std::vector<TunedPlan> env_tuned = [] {
+        std::vector<TunedPlan> v;
+        const char* e = getenv("CI_TUNE");
+        while (e && *e) {
+            TunedPlan t{};
+            if (sscanf(e, "%d,%d,%d,%d,%d,%d,%d,%d,%d,%d", &t.H, &t.W, &t.c, &t.m, &t.pm, &t.MC, &t.T, &t.nhd, &t.nslot,
+                       &t.hst) == 10)
+                v.push_back(t);
+            e = strchr(e, ';');
+            if (e) e++;
+        }
+        return v;
+    }();
     const TunedPlan* tuned = nullptr;
+    for (const auto& tp : env_tuned)
+        if (!tuned && tp.H == S.H && tp.W == S.W && tp.c == S.c && tp.m == S.m && tp.pm == pm) tuned = &tp;
     if (!no_tuned)
     for (const auto& tp : kTuned)   // first match wins
         if (!tuned && tp.H == S.H && tp.W == S.W && tp.c == S.c && tp.m == S.m && tp.pm == pm &&
@@ -2078,6 +2114,8 @@ static const SpecEntry kSpecs[] = {
     CI_SPEC(17, 8, 32, 32, 5, 2, 16384, 16, 6, 1),   // C stage 1, f16x3 (CI_PREC_FP32)
     CI_SPEC_X(9, 32, 128, 80, 2, 2, 16384, 8, 24, 0, 1, 0),  // C stage 2, f16x3
     CI_SPEC(5, 96, 128, 96, 1, 2, 16384, 4, 96, 0),  // C stage 3, f16x3
+    CI_SPEC(17, 8, 16, 32, 5, 2, 16384, 16, 6, 1),   // C stage 1, f16x3, MC = 16, nhd = 2 (A/B)
+    CI_SPEC(17, 8, 32, 32, 3, 2, 16384, 16, 6, 1),   // C stage 1, f16x3, T = 3, I = 1, nhd = 2 (A/B)
     CI_SPEC(17, 64, 32, 64, 5, 0, 16384, 16, 64, 0),  // learned-encoder tail (E2, E3), bf16
     CI_SPEC(17, 64, 32, 64, 3, 2, 16384, 16, 64, 0),  // learned-encoder tail (E2, E3), f16x3
     // i-ResNet variant of Arch C (f1, config C3R): residual blocks on 12 / 48 / 192 channels
@@ -2172,6 +2210,12 @@ ci_status_t umma_prepare(Model* m, const float* host_params) {
                 bias.push_back(o >= 0 ? E3b[o] : 0.f);
             }
             U->has_enc = 1;
+            if (getenv("CI_DEBUG_PLAN"))
+                fprintf(stderr,
+                        "[ci plan] encoder tail %dx%d c=%d m=%d pm=%d: MC=%d nch=%d Nc2=%d T=%d I=%d k1=%d k2=%d "
+                        "slots=%dx%d smem=%zu tmem=%d nhd=%d sst=%d est=%.0f\n",
+                        p.H, p.W, p.c, p.m, p.pm, p.MC, p.nch, p.Nc2, p.T, p.I, p.k1, p.k2, p.nslot, p.slot_bytes,
+                        p.smem, p.tmem_cols, p.nhd, p.sstate, p.est_cycles);
         }
     }
     cudaError_t e = cudaMalloc(&m->d_wpack, pack.size() * 2);
@@ -2220,6 +2264,38 @@ static void prof_end(cudaStream_t st, int stage, double flops) {
     g_prof_open = nullptr;
 }
 
+// per-role cycle counters of one launch (CI_DEBUG_CYCLES; scripts/cycles.sh): a zeroed
+// per-CTA buffer, and the CTA-averaged report after the launch (synchronises the stream)
+static unsigned long long* cycles_buffer(cudaStream_t st) {
+    static unsigned long long* dbg = nullptr;
+    if (!getenv("CI_DEBUG_CYCLES")) return nullptr;
+    if (!kCycles) {
+        static bool warned = false;
+        if (!warned) fprintf(stderr, "[ci] CI_DEBUG_CYCLES: library built with CI_NO_CYCLES\n");
+        warned = true;
+        return nullptr;
+    }
+    if (!dbg) cudaMalloc(&dbg, 148 * 16 * sizeof(unsigned long long));
+    cudaMemsetAsync(dbg, 0, 148 * 16 * sizeof(unsigned long long), st);
+    return dbg;
+}
+static void cycles_report(const unsigned long long* dbg, int grid, const char* label, int64_t n, int inverse,
+                          cudaStream_t st) {
+    if (!dbg) return;
+    unsigned long long h[148 * 16];
+    cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    double acc[16] = {0};
+    for (int b = 0; b < grid; b++)
+        for (int i = 0; i < 16; i++) acc[i] += (double)h[b * 16 + i] / grid;
+    fprintf(stderr,
+            "[ci cycles] stage %s n=%lld inv=%d | prod total %.0f wait_empty %.0f | mma total %.0f wait_x %.0f "
+            "wait_full %.0f wait_hd %.0f | epi total %.0f wait_acc1 %.0f wait_hd_empty %.0f wait_acc2 %.0f "
+            "load %.0f epi1 %.0f epi2 %.0f\n",
+            label, (long long)n, inverse, acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6], acc[7], acc[8],
+            acc[9], acc[10], acc[11], acc[12]);
+}
+
 bool umma_has_encoder(const Model* m) {
     const UmmaState* U = reinterpret_cast<const UmmaState*>(m->umma_state);
     return U && U->has_enc;
@@ -2241,7 +2317,7 @@ ci_status_t umma_encoder_tail(const Model* m, float* zbuf, int64_t n, int* ctr, 
     a.act = 0;
     a.inverse = 0;
     a.fmode = 1;
-    a.dbg = nullptr;
+    a.dbg = cycles_buffer(st);
     a.ctr = ctr;
     a.residual = 0;
     a.fp_iters = 1;
@@ -2250,6 +2326,7 @@ ci_status_t umma_encoder_tail(const Model* m, float* zbuf, int64_t n, int* ctr, 
     pick_kernel(a.p, a)<<<grid, kThreads, a.p.smem, st>>>(a);
     count_launch();
     CI_CHECK_LAUNCH("k_stage (encoder tail)");
+    cycles_report(a.dbg, grid, "enc", n, 0, st);
     return CI_OK;
 }
 
@@ -2271,16 +2348,7 @@ ci_status_t umma_stage(const Model* m, int s, float* state, int64_t n, bool inve
     a.ctr = ctr;
     a.residual = m->arch.block_kind == 1 ? 1 : 0;
     a.fp_iters = a.residual ? m->arch.fp_iters : 1;
-    static unsigned long long* dbg = nullptr;
-    const bool debug_cycles = getenv("CI_DEBUG_CYCLES") != nullptr && kCycles;
-    if (getenv("CI_DEBUG_CYCLES") && !kCycles) {
-        static bool warned = false;
-        if (!warned) fprintf(stderr, "[ci] CI_DEBUG_CYCLES: library built with CI_NO_CYCLES\n");
-        warned = true;
-    }
-    if (debug_cycles && !dbg) cudaMalloc(&dbg, 148 * 16 * sizeof(unsigned long long));
-    a.dbg = debug_cycles ? dbg : nullptr;
-    if (a.dbg) cudaMemsetAsync(dbg, 0, 148 * 16 * sizeof(unsigned long long), st);
+    a.dbg = cycles_buffer(st);
     int64_t nbatch = (n + a.p.I - 1) / a.p.I;
     int dev_sms = 148;
     int grid = (int)std::min<int64_t>(nbatch, dev_sms);
@@ -2291,20 +2359,9 @@ ci_status_t umma_stage(const Model* m, int s, float* state, int64_t n, bool inve
     count_launch();
     CI_CHECK_LAUNCH("k_stage");
     prof_end(st, s, flops);
-    if (a.dbg) {
-        unsigned long long h[148 * 16];
-        cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, st);
-        cudaStreamSynchronize(st);
-        double acc[16] = {0};
-        for (int b = 0; b < grid; b++)
-            for (int i = 0; i < 16; i++) acc[i] += (double)h[b * 16 + i] / grid;
-        fprintf(stderr,
-                "[ci cycles] stage %d n=%lld inv=%d | prod total %.0f wait_empty %.0f | mma total %.0f wait_x %.0f "
-                "wait_full %.0f wait_hd %.0f | epi total %.0f wait_acc1 %.0f wait_hd_empty %.0f wait_acc2 %.0f "
-                "load %.0f epi1 %.0f epi2 %.0f\n",
-                s, (long long)n, (int)inverse, acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6], acc[7],
-                acc[8], acc[9], acc[10], acc[11], acc[12]);
-    }
+    char label[16];
+    snprintf(label, sizeof(label), "%d", s);
+    cycles_report(a.dbg, grid, label, n, inverse ? 1 : 0, st);
     return CI_OK;
 }
 
