@@ -4,11 +4,13 @@
 //   k_enc_e1_mean : m[b] = (1/k) sum_i ReLU(conv3x3(E1, x_{b,i}))  -- weight-shared first layer on
 //                   every input, averaged after it; also writes psi(m), the tail's
 //                   input.  fp32, summation over i ascending.
-//   k_enc_out     : x_p = conv3x3(E4, psi^-1(z) + m)  -- the U-Net-style skip fused into E4: the
-//                   CTA of group b builds u = psi^-1(z) + m in shared memory, then every thread
-//                   computes the in_c outputs of four pixels (no u round trip through HBM).
-// Both hold their (small) weights in the kernel parameter space -- the constant bank, so every
-// FFMA reads its weight as an immediate constant-bank operand: no load instruction per MAC.
+//   k_enc_out     : x_p = conv3x3(E4, psi^-1(z) + m)  -- the U-Net-style skip fused into E4.
+// Both are band-tiled: a CTA of 256 threads owns one band of BR = 256 / W image rows of one group
+// (one output pixel per thread).  The band's input window (BR + 2 rows incl. the 3x3 halo, zero
+// padded) is staged in shared memory -- E1 double-buffers the k inputs with cp.async so input
+// i+1 streams in while input i is convolved; E4 builds u = psi^-1(z) + m there.  The weights
+// live in the kernel parameter space (the constant bank): every FFMA reads its weight as an
+// immediate constant-bank operand, so the inner loops are FFMA + LDS only.
 #include "ci_internal.h"
 
 namespace ci {
@@ -24,136 +26,175 @@ struct E4Params {
     float b[CI];
 };
 
-// thread -> 4 horizontally adjacent pixels of group b's image plane, all C1 channels
+constexpr int kEncThreads = 256;
+
+__device__ __forceinline__ void cp_async4(float* dst, const float* src, bool ok) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(ok ? 4 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// rows per band: one pixel per thread
+__host__ __device__ inline int enc_band_rows(int H, int W) { return min(kEncThreads / W, H); }
+
 template <int CI, int C1>
-__global__ void __launch_bounds__(256) k_enc_e1_mean(const float* __restrict__ x, int k, int64_t B, int H, int W,
-                                                     const __grid_constant__ E1Params<CI, C1> p,
-                                                     float* __restrict__ m, float* __restrict__ zpsi,
-                                                     int64_t zstride) {
-    constexpr int PX = 4;
+__global__ void __launch_bounds__(kEncThreads, 4) k_enc_e1_mean(const float* __restrict__ x, int k, int64_t B, int H,
+                                                            int W, const __grid_constant__ E1Params<CI, C1> p,
+                                                            float* __restrict__ m, float* __restrict__ zpsi,
+                                                            int64_t zstride) {
+    extern __shared__ float xs[];   // [2][CI][BR + 2][W + 2]
+    const int BR = enc_band_rows(H, W), nb = (H + BR - 1) / BR;
+    const int Wp = W + 2, plane = (BR + 2) * Wp, tileN = CI * plane;
     const int64_t HW = (int64_t)H * W;
-    const int Ho = H / 2, Wo = W / 2, wq = W / PX;
+    const int Ho = H / 2, Wo = W / 2;
+    const int r = threadIdx.x / W, xx = threadIdx.x - r * W;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const float fk = (float)k;
-    const int64_t units = B * (int64_t)H * wq;
-    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < units; u += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t b = u / ((int64_t)H * wq);
-        const int r = (int)(u - b * H * wq);
-        const int y = r / wq, x0 = (r - y * wq) * PX;
-        float sum[C1][PX];
-#pragma unroll
-        for (int o = 0; o < C1; o++)
-#pragma unroll
-            for (int q = 0; q < PX; q++) sum[o][q] = 0.f;
-        for (int i = 0; i < k; i++) {
+    for (int64_t unit = blockIdx.x; unit < B * nb; unit += gridDim.x) {
+        const int64_t b = unit / nb;
+        const int y0 = (int)(unit - b * nb) * BR, y = y0 + r;
+        const bool act = r < BR && y < H;
+        auto load = [&](int i, int buf) {   // input i's band window, zero outside the image
             const float* xi = x + (b * k + i) * CI * HW;
-            float in[CI][3][PX + 2];   // rows y-1..y+1, columns x0-1 .. x0+PX (zero outside)
-#pragma unroll
-            for (int c = 0; c < CI; c++)
-#pragma unroll
-                for (int uu = 0; uu < 3; uu++) {
-                    const int yy = y + uu - 1;
-                    const bool rowok = yy >= 0 && yy < H;
-#pragma unroll
-                    for (int j = 0; j < PX + 2; j++) {
-                        const int xx = x0 + j - 1;
-                        in[c][uu][j] = (rowok && xx >= 0 && xx < W) ? __ldg(xi + c * HW + yy * W + xx) : 0.f;
-                    }
+            float* dst = xs + buf * tileN;
+            // warp w fills window rows w, w + 8, ...; lanes walk the columns
+            for (int row = warp; row < CI * (BR + 2); row += kEncThreads / 32) {
+                const int c = row / (BR + 2), yy = y0 + row - c * (BR + 2) - 1;
+                const bool rok = yy >= 0 && yy < H;
+                const float* src = xi + c * HW + (int64_t)yy * W - 1;
+                for (int cc = lane; cc < Wp; cc += 32) {
+                    const bool ok = rok && cc >= 1 && cc <= W;
+                    cp_async4(dst + row * Wp + cc, ok ? src + cc : xi, ok);
                 }
+            }
+            cp_async_commit();
+        };
+        __syncthreads();   // the previous unit's readers are done with both buffers
+        load(0, 0);
+        float sum[C1];
 #pragma unroll
-            for (int o = 0; o < C1; o++) {
+        for (int o = 0; o < C1; o++) sum[o] = 0.f;
+        for (int i = 0; i < k; i++) {
+            if (i + 1 < k) {
+                load(i + 1, (i + 1) & 1);
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
+            }
+            __syncthreads();
+            if (act) {
+                const float* t = xs + (i & 1) * tileN + r * Wp + xx;
+                float in[CI][3][3];
 #pragma unroll
-                for (int q = 0; q < PX; q++) {
+                for (int c = 0; c < CI; c++)
+#pragma unroll
+                    for (int u = 0; u < 3; u++)
+#pragma unroll
+                        for (int v = 0; v < 3; v++) in[c][u][v] = t[c * plane + u * Wp + v];
+#pragma unroll
+                for (int o = 0; o < C1; o++) {
                     float acc = 0.f;   // taps in (c, u, v) order, then the bias
 #pragma unroll
                     for (int c = 0; c < CI; c++)
 #pragma unroll
-                        for (int uu = 0; uu < 3; uu++)
+                        for (int u = 0; u < 3; u++)
 #pragma unroll
-                            for (int v = 0; v < 3; v++) acc = fmaf(p.w[((o * CI + c) * 3 + uu) * 3 + v], in[c][uu][q + v], acc);
-                    sum[o][q] = __fadd_rn(sum[o][q], fmaxf(acc + p.b[o], 0.f));
+                            for (int v = 0; v < 3; v++) acc = fmaf(p.w[((o * CI + c) * 3 + u) * 3 + v], in[c][u][v], acc);
+                    sum[o] = __fadd_rn(sum[o], fmaxf(acc + p.b[o], 0.f));
                 }
             }
+            __syncthreads();   // buffer i & 1 is refilled by the next iteration's prefetch
         }
-        float* zb = zpsi + b * zstride;
+        if (act) {
+            float* zb = zpsi + b * zstride;
+            // psi: pixel (y, x) -> channel 4o + 2(y&1) + (x&1) at (y/2, x/2)
+            const int64_t zoff = ((int64_t)(2 * (y & 1) + (xx & 1)) * Ho + (y >> 1)) * Wo + (xx >> 1);
 #pragma unroll
-        for (int o = 0; o < C1; o++) {
-            float mv[PX];
-#pragma unroll
-            for (int q = 0; q < PX; q++) mv[q] = __fdiv_rn(sum[o][q], fk);
-            *reinterpret_cast<float4*>(m + (b * C1 + o) * HW + y * W + x0) = make_float4(mv[0], mv[1], mv[2], mv[3]);
-            // psi: pixel (y, x) -> channel 4o + 2(y&1) + (x&1) at (y/2, x/2); x0 is even
-            float* z0 = zb + ((int64_t)(o * 4 + 2 * (y & 1)) * Ho + (y >> 1)) * Wo + (x0 >> 1);
-            *reinterpret_cast<float2*>(z0) = make_float2(mv[0], mv[2]);
-            *reinterpret_cast<float2*>(z0 + (int64_t)Ho * Wo) = make_float2(mv[1], mv[3]);
+            for (int o = 0; o < C1; o++) {
+                const float mv = __fdiv_rn(sum[o], fk);
+                m[(b * C1 + o) * HW + y * W + xx] = mv;
+                zb[(int64_t)o * 4 * Ho * Wo + zoff] = mv;
+            }
         }
     }
 }
 
-// one CTA per group (grid-stride): u = psi^-1(z) + m in shared memory [C1][H+2][W+2] (zero
-// border), then x_p[o] = b[o] + sum_{c,u,v} E4[o][c][u][v] u[c][y+u-1][x+v-1]
+// u = psi^-1(z) + m in shared memory [C1][BR+2][W+2] (zero border), then
+// x_p[o] = b[o] + sum_{c,u,v} E4[o][c][u][v] u[c][y+u-1][x+v-1].  The z gather and the m rows
+// stream in with cp.async (all of a thread's copies in flight at once: the fill is latency-,
+// not bandwidth-bound), then one pass adds them in place.
 template <int CI, int C1>
-__global__ void __launch_bounds__(256) k_enc_out(const float* __restrict__ z, int64_t zstride,
-                                                 const float* __restrict__ m, int64_t B, int H, int W,
-                                                 const __grid_constant__ E4Params<CI, C1> p, float* __restrict__ xp) {
-    constexpr int PX = 4;
-    extern __shared__ float us[];
-    const int Hp = H + 2, Wp = W + 2;
+__global__ void __launch_bounds__(kEncThreads, 4) k_enc_out(const float* __restrict__ z, int64_t zstride,
+                                                           const float* __restrict__ m, int64_t B, int H, int W,
+                                                           const __grid_constant__ E4Params<CI, C1> p,
+                                                           float* __restrict__ xp) {
+    extern __shared__ float us[];   // [2][C1][BR + 2][W + 2]: psi^-1(z) window, m window
+    const int BR = enc_band_rows(H, W), nb = (H + BR - 1) / BR;
+    const int Wp = W + 2, plane = (BR + 2) * Wp, tileN = C1 * plane;
+    float* ms = us + tileN;
     const int64_t HW = (int64_t)H * W;
     const int Ho = H / 2, Wo = W / 2;
-    for (int i = threadIdx.x; i < C1 * Hp * Wp; i += blockDim.x) us[i] = 0.f;
-    for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
-        __syncthreads();   // the previous group's reads are done
+    const int r = threadIdx.x / W, xx = threadIdx.x - r * W;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t unit = blockIdx.x; unit < B * nb; unit += gridDim.x) {
+        const int64_t b = unit / nb;
+        const int y0 = (int)(unit - b * nb) * BR, y = y0 + r;
         const float* zb = z + b * zstride;
         const float* mb = m + b * C1 * HW;
-        for (int i = threadIdx.x; i < C1 * (int)HW; i += blockDim.x) {   // m-order: coalesced m reads
-            const int c = i / (int)HW, rem = i - c * (int)HW, y = rem / W, xx = rem - y * W;
-            const float zv = zb[((int64_t)(c * 4 + 2 * (y & 1) + (xx & 1)) * Ho + (y >> 1)) * Wo + (xx >> 1)];
-            us[(c * Hp + y + 1) * Wp + xx + 1] = zv + mb[i];
+        __syncthreads();   // the previous unit's readers are done
+        // warp w fills window rows w, w + 8, ...; lanes walk the columns (zero outside the image)
+        for (int row = warp; row < C1 * (BR + 2); row += kEncThreads / 32) {
+            const int c = row / (BR + 2), yy = y0 + row - c * (BR + 2) - 1;
+            const bool rok = yy >= 0 && yy < H;
+            const float* zr = zb + ((int64_t)(c * 4 + 2 * (yy & 1)) * Ho + (yy >> 1)) * Wo;   // + (x&1) plane
+            const float* mr = mb + c * HW + (int64_t)yy * W;
+            for (int cc = lane; cc < Wp; cc += 32) {
+                const int xc = cc - 1;
+                const bool ok = rok && xc >= 0 && xc < W;
+                cp_async4(us + row * Wp + cc, ok ? zr + (int64_t)(xc & 1) * Ho * Wo + (xc >> 1) : zb, ok);
+                cp_async4(ms + row * Wp + cc, ok ? mr + xc : mb, ok);
+            }
         }
+        cp_async_commit();
+        cp_async_wait<0>();
         __syncthreads();
-        const int wq = W / PX;
-        for (int t = threadIdx.x; t < H * wq; t += blockDim.x) {
-            const int y = t / wq, x0 = (t - y * wq) * PX;
-            float acc[CI][PX];
+        for (int e = threadIdx.x; e < tileN; e += kEncThreads) us[e] += ms[e];
+        __syncthreads();
+        if (r < BR && y < H) {
+            float acc[CI];
 #pragma unroll
-            for (int o = 0; o < CI; o++)
+            for (int o = 0; o < CI; o++) acc[o] = 0.f;
+            const float* t = us + r * Wp + xx;
 #pragma unroll
-                for (int q = 0; q < PX; q++) acc[o][q] = 0.f;
-#pragma unroll 4
             for (int c = 0; c < C1; c++) {
-                float win[3][PX + 2];
+                float win[3][3];
 #pragma unroll
-                for (int uu = 0; uu < 3; uu++)
+                for (int u = 0; u < 3; u++)
 #pragma unroll
-                    for (int j = 0; j < PX + 2; j++) win[uu][j] = us[(c * Hp + y + uu) * Wp + x0 + j];
+                    for (int v = 0; v < 3; v++) win[u][v] = t[c * plane + u * Wp + v];
 #pragma unroll
                 for (int o = 0; o < CI; o++)
 #pragma unroll
-                    for (int q = 0; q < PX; q++)
+                    for (int u = 0; u < 3; u++)
 #pragma unroll
-                        for (int uu = 0; uu < 3; uu++)
-#pragma unroll
-                            for (int v = 0; v < 3; v++) acc[o][q] = fmaf(p.w[((o * C1 + c) * 3 + uu) * 3 + v], win[uu][q + v], acc[o][q]);
+                        for (int v = 0; v < 3; v++) acc[o] = fmaf(p.w[((o * C1 + c) * 3 + u) * 3 + v], win[u][v], acc[o]);
             }
-            float* ob = xp + b * CI * HW + y * W + x0;
 #pragma unroll
             for (int o = 0; o < CI; o++)   // identity activation on the encoder output
-                *reinterpret_cast<float4*>(ob + o * HW) =
-                    make_float4(acc[o][0] + p.b[o], acc[o][1] + p.b[o], acc[o][2] + p.b[o], acc[o][3] + p.b[o]);
+                xp[(b * CI + o) * HW + y * W + xx] = acc[o] + p.b[o];
         }
     }
 }
 
-static int grid_of(int64_t total, int block) {
-    int64_t g = (total + block - 1) / block;
-    if (g > 148 * 32) g = 148 * 32;
-    return (int)(g < 1 ? 1 : g);
+bool enc_supported(int Ci, int C1, int H, int W) {
+    return Ci == 3 && (C1 == 4 || C1 == 8 || C1 == 16) && W >= 2 && W <= kEncThreads && kEncThreads % W == 0 &&
+           H % 2 == 0 && W % 2 == 0;
 }
 
-bool enc_supported(int Ci, int C1, int H, int W) {
-    return Ci == 3 && (C1 == 4 || C1 == 8 || C1 == 16) && W % 4 == 0 && H % 2 == 0 &&
-           (size_t)C1 * (H + 2) * (W + 2) * sizeof(float) <= 200 * 1024;
-}
+// resident units: a few waves of 148 SMs, grid-stride beyond
+static int enc_grid(int64_t units) { return (int)std::max<int64_t>(1, std::min<int64_t>(units, 148 * 16)); }
 
 template <int CI, int C1>
 static cudaError_t e1_t(const float* x, int k, int64_t B, int H, int W, const float* hw1, const float* hb1, float* m,
@@ -161,7 +202,9 @@ static cudaError_t e1_t(const float* x, int k, int64_t B, int H, int W, const fl
     E1Params<CI, C1> p;
     memcpy(p.w, hw1, sizeof(p.w));
     memcpy(p.b, hb1, sizeof(p.b));
-    k_enc_e1_mean<CI, C1><<<grid_of(B * (int64_t)H * (W / 4), 256), 256, 0, s>>>(x, k, B, H, W, p, m, zpsi, zstride);
+    const int BR = enc_band_rows(H, W), nb = (H + BR - 1) / BR;
+    const size_t smem = sizeof(float) * 2 * CI * (BR + 2) * (W + 2);
+    k_enc_e1_mean<CI, C1><<<enc_grid(B * nb), kEncThreads, smem, s>>>(x, k, B, H, W, p, m, zpsi, zstride);
     return cudaGetLastError();
 }
 
@@ -182,15 +225,13 @@ static cudaError_t out_t(const float* z, int64_t zstride, const float* m, int64_
     E4Params<CI, C1> p;
     memcpy(p.w, hw4, sizeof(p.w));
     memcpy(p.b, hb4, sizeof(p.b));
-    const size_t smem = (size_t)C1 * (H + 2) * (W + 2) * sizeof(float);
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_enc_out<CI, C1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    const int BR = enc_band_rows(H, W), nb = (H + BR - 1) / BR;
+    const size_t smem = sizeof(float) * 2 * C1 * (BR + 2) * (W + 2);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k_enc_out<CI, C1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        attr = true;
     }
-    const int grid = (int)std::min<int64_t>(B, 148 * 3);
-    k_enc_out<CI, C1><<<grid, 256, smem, s>>>(z, zstride, m, B, H, W, p, xp);
+    k_enc_out<CI, C1><<<enc_grid(B * nb), kEncThreads, smem, s>>>(z, zstride, m, B, H, W, p, xp);
     return cudaGetLastError();
 }
 

@@ -77,6 +77,8 @@ struct StagePlan {
     int nhd;               // hidden plane buffers (2: double-buffered, conv1/epilogue overlap conv2)
     int sstate;            // 1: the batch's fp32 state lives in shared memory for the whole stage
     uint32_t sstate_off;   // byte offset of the fp32 state region in dynamic smem
+    int stk1, stk2;        // stacked f16x3 for conv1 / conv2 (mma_prec): B tiles of 2N rows, 2N
+                           // accumulator columns per tile (specialised kernels only)
 };
 
 struct StageArgs {
@@ -191,6 +193,24 @@ __host__ __device__ constexpr AOff a_off(int s, int am, bool hstk, int per, int 
                 0u};
 }
 
+// The MMAs of one k-step in the plan's precision.  Stacked f16x3 (STK): the packed
+// B tile holds W_hi and W_lo as 2N rows per K half, so hi(A) x [W_hi | W_lo] is ONE MMA of width 2N
+// (the A tile is read once for both) into accumulator columns [0, 2N), then lo(A) x W_hi adds into
+// [0, N); the epilogue folds column n + N into n.  Unstacked f16x3 issues hi(A)W_hi + lo(A)W_hi +
+// hi(A)W_lo into [0, N).
+template <int PM, int N, int LOA16, int STK>
+__device__ __forceinline__ void mma_prec(uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t idescw,
+                                         uint32_t acc) {
+    if constexpr (STK != 0) {
+        mma_bf16(d, ad, bd, idescw, acc);
+        mma_bf16(d, ad + (uint64_t)LOA16, bd, idesc, 1u);
+    } else {
+        mma_bf16(d, ad, bd, idesc, acc);
+        if (PM >= 1) mma_bf16(d, ad + (uint64_t)LOA16, bd, idesc, 1u);          // lo(A) * B
+        if (PM == 2) mma_bf16(d, ad, bd + (uint64_t)(N * 2), idesc, 1u);          // hi(A) * lo(B)
+    }
+}
+
 // ----------------------------------------------------------------------------------------
 // Compile-time specialised MMA issue for one conv segment (conv1 chunk or conv2 chunk).
 // Every k-step's A/B descriptor offsets, accumulate flags and ring-slot boundaries are
@@ -199,10 +219,10 @@ __host__ __device__ constexpr AOff a_off(int s, int am, bool hstk, int per, int 
 //   ringlo: low descriptor word of ring slot 0 with this segment's B LBO field
 // ----------------------------------------------------------------------------------------
 template <int K, int PER, int AM, int WP, int PLANE16, int G, int KB16, int T, int N, int PM,
-          int LOA16, int ACC0, int DSTRIDE, bool HSTK = false>
+          int LOA16, int ACC0, int DSTRIDE, bool HSTK = false, int STK = 0>
 __device__ __forceinline__ void issue_static(uint32_t tmem, uint32_t alo0, uint32_t ringlo, uint32_t slot16,
                                              uint32_t idesc, uint32_t acc_first, int& slot, uint32_t& phase,
-                                             int nslot, uint64_t* full, uint64_t* empty) {
+                                             int nslot, uint64_t* full, uint64_t* empty, uint32_t idescw = 0) {
     constexpr uint32_t HI = 0x4008u;   // SBO = 128 B, descriptor version 1
     uint32_t bl = 0;
     // opaque to the optimiser: keeps ptxas from hoisting every k-step's descriptor constant out
@@ -226,9 +246,7 @@ __device__ __forceinline__ void issue_static(uint32_t tmem, uint32_t alo0, uint3
             const uint64_t ad = ((uint64_t)HI << 32) | (al + (uint32_t)(t * 128));
             const uint64_t bd = ((uint64_t)HI << 32) | b;
             const uint32_t d = tmem + (uint32_t)(ACC0 + t * DSTRIDE);
-            mma_bf16(d, ad, bd, idesc, s == 0 ? acc_first : 1u);
-            if (PM >= 1) mma_bf16(d, ad + (uint64_t)LOA16, bd, idesc, 1u);          // lo(A) * B
-            if (PM == 2) mma_bf16(d, ad, bd + (uint64_t)(N * 2), idesc, 1u);          // hi(A) * lo(B)
+            mma_prec<PM, N, LOA16, STK>(d, ad, bd, idesc, idescw, s == 0 ? acc_first : 1u);
         }
         if (s % G == G - 1 || s == K - 1) {
             commit(&empty[slot]);
@@ -242,11 +260,11 @@ __device__ __forceinline__ void issue_static(uint32_t tmem, uint32_t alo0, uint3
 // has finished the X rows of tiles t-1..t+1 (x_tile[t+1]; arrivals are in tile order per
 // thread), so this chunk overlaps that epilogue instead of waiting for all of it.
 template <int K, int PER, int AM, int WP, int PLANE16, int G, int KB16, int T, int N, int PM,
-          int LOA16, int ACC0, int DSTRIDE>
+          int LOA16, int ACC0, int DSTRIDE, int STK = 0>
 __device__ __forceinline__ void issue_static_tiles(uint32_t tmem, uint32_t alo0, uint32_t ringlo, uint32_t slot16,
                                                    uint32_t idesc, uint32_t acc_first, int& slot, uint32_t& phase,
                                                    int nslot, uint64_t* full, uint64_t* empty, uint64_t* x_tile,
-                                                   uint32_t xph) {
+                                                   uint32_t xph, uint32_t idescw = 0) {
     constexpr uint32_t HI = 0x4008u;
     constexpr int NS = (K + G - 1) / G;
     uint32_t bl[NS];
@@ -272,9 +290,7 @@ __device__ __forceinline__ void issue_static_tiles(uint32_t tmem, uint32_t alo0,
             const uint64_t ad = ((uint64_t)HI << 32) | (alo0 + (uint32_t)(shift + poff16 + t * 128) + o.lbo_add);
             const uint64_t bd = ((uint64_t)HI << 32) | (bl[s / G] + (uint32_t)((s % G) * KB16));
             const uint32_t d = tmem + (uint32_t)(ACC0 + t * DSTRIDE);
-            mma_bf16(d, ad, bd, idesc, s == 0 ? acc_first : 1u);
-            if (PM >= 1) mma_bf16(d, ad + (uint64_t)LOA16, bd, idesc, 1u);          // lo(A) * B
-            if (PM == 2) mma_bf16(d, ad, bd + (uint64_t)(N * 2), idesc, 1u);          // hi(A) * lo(B)
+            mma_prec<PM, N, LOA16, STK>(d, ad, bd, idesc, idescw, s == 0 ? acc_first : 1u);
         }
     }
 #pragma unroll
@@ -289,11 +305,11 @@ __device__ __forceinline__ void issue_static_tiles(uint32_t tmem, uint32_t alo0,
 // tile t reads: X / hidden rows of tiles <= t+1, or acc1 tile t read), and -- when `done` is
 // given -- a per-tile commit lets the epilogue consume tile t while later tiles still run.
 template <int K, int PER, int AM, bool HSTK, int WP, int PLANE16, int G, int KB16, int T, int N, int PM,
-          int LOA16, int ACC0, int DSTRIDE, int AHEAD>
+          int LOA16, int ACC0, int DSTRIDE, int AHEAD, int STK = 0>
 __device__ __forceinline__ void issue_stream(uint32_t tmem, uint32_t alo0, uint32_t ringlo, uint32_t slot16,
                                              uint32_t idesc, uint32_t acc_first, int& slot, uint32_t& phase,
                                              int nslot, uint64_t* full, uint64_t* empty, uint64_t* dep,
-                                             uint32_t dph, uint64_t* done) {
+                                             uint32_t dph, uint64_t* done, uint32_t idescw = 0) {
     constexpr uint32_t HI = 0x4008u;
     constexpr int NS = (K + G - 1) / G;
     uint32_t bl[NS];
@@ -319,9 +335,7 @@ __device__ __forceinline__ void issue_stream(uint32_t tmem, uint32_t alo0, uint3
             const uint64_t ad = ((uint64_t)HI << 32) | (alo0 + (uint32_t)(shift + poff16 + t * 128) + o.lbo_add);
             const uint64_t bd = ((uint64_t)HI << 32) | (bl[s / G] + (uint32_t)((s % G) * KB16));
             const uint32_t d = tmem + (uint32_t)(ACC0 + t * DSTRIDE);
-            mma_bf16(d, ad, bd, idesc, s == 0 ? acc_first : 1u);
-            if (PM >= 1) mma_bf16(d, ad + (uint64_t)LOA16, bd, idesc, 1u);          // lo(A) * B
-            if (PM == 2) mma_bf16(d, ad, bd + (uint64_t)(N * 2), idesc, 1u);          // hi(A) * lo(B)
+            mma_prec<PM, N, LOA16, STK>(d, ad, bd, idesc, idescw, s == 0 ? acc_first : 1u);
         }
         if (done) commit(&done[t]);
     }
@@ -345,9 +359,9 @@ __device__ __forceinline__ void acquire_slots(uint32_t (&bl)[NS], uint32_t ringl
     }
 }
 template <int K, int PER, int AM, bool HSTK, int WP, int PLANE16, int G, int KB16, int N, int PM, int LOA16,
-          int ACC0, int DSTRIDE, int NS>
+          int ACC0, int DSTRIDE, int NS, int STK = 0>
 __device__ __forceinline__ void issue_tile(int t, uint32_t tmem, uint32_t alo0, const uint32_t (&bl)[NS],
-                                           uint32_t idesc, uint32_t acc_first) {
+                                           uint32_t idesc, uint32_t acc_first, uint32_t idescw = 0) {
     constexpr uint32_t HI = 0x4008u;
 #pragma unroll
     for (int s = 0; s < K; s++) {
@@ -356,16 +370,19 @@ __device__ __forceinline__ void issue_tile(int t, uint32_t tmem, uint32_t alo0, 
         const uint64_t ad = ((uint64_t)HI << 32) | (alo0 + (uint32_t)(shift + poff16 + t * 128) + o.lbo_add);
         const uint64_t bd = ((uint64_t)HI << 32) | (bl[s / G] + (uint32_t)((s % G) * KB16));
         const uint32_t d = tmem + (uint32_t)(ACC0 + t * DSTRIDE);
-        mma_bf16(d, ad, bd, idesc, s == 0 ? acc_first : 1u);
-        if (PM >= 1) mma_bf16(d, ad + (uint64_t)LOA16, bd, idesc, 1u);          // lo(A) * B
-        if (PM == 2) mma_bf16(d, ad, bd + (uint64_t)(N * 2), idesc, 1u);          // hi(A) * lo(B)
+        mma_prec<PM, N, LOA16, STK>(d, ad, bd, idesc, idescw, s == 0 ? acc_first : 1u);
     }
 }
 
 // Static stage configuration (0 = use the runtime plan)
 template <int WP_, int CP_, int MC_, int NC2_, int T_, int PM_, int SLOT_, int H_ = 0, int C_ = 0, int SST_ = 0,
-          int HST_ = 0, int RES_ = 0>
+          int HST_ = 0, int RES_ = 0, int STK1_ = 0, int STK2_ = 0>
 struct SCfg {
+    // stacked f16x3 (mma_prec): conv1 / conv2 B tiles of 2N rows, accumulators 2N columns per tile
+    static constexpr int STK1 = STK1_, STK2 = STK2_;
+    static constexpr int NB1 = MC_ * (STK1_ ? 2 : 1), NB2 = NC2_ * (STK2_ ? 2 : 1);
+    static_assert(!(STK1_ || STK2_) || PM_ == 2, "stacking is an f16x3 layout");
+    static_assert(!STK2_ || (!HST_ && !RES_), "stacked conv2: plain-width coupling epilogue only");
     static constexpr bool HST = HST_ != 0;
     static constexpr bool RES = RES_ != 0;   // residual blocks / ELU / fixed-point replays compiled in
     static constexpr int HC = HST_ ? (C_ + 7) / 8 * 8 : 0;   // == StagePlan::hc
@@ -390,7 +407,7 @@ struct SCfg {
     static constexpr int KB1 = MC * 32 * (PM == 2 ? 2 : 1), KB2 = NC2 * 32 * (PM == 2 ? 2 : 1);
     static constexpr int G1 = (SLOT / (KB1 > 0 ? KB1 : 1)) < 1 ? 1 : SLOT / (KB1 > 0 ? KB1 : 1);
     static constexpr int G2 = (SLOT / (KB2 > 0 ? KB2 : 1)) < 1 ? 1 : SLOT / (KB2 > 0 ? KB2 : 1);
-    static constexpr int ACC1 = T * NC2;
+    static constexpr int ACC1 = T * NB2;   // acc2[tile] at tile * NB2, acc1[tile] at ACC1 + tile * NB1
     static constexpr int LOX16 = (CP / 8) * PLANE16;
     static constexpr int LOH16 = (MC / 8) * PLANE16;
     // Tile-streamed block schedule: every segment's weights fit one ring slot,
@@ -503,7 +520,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
     __syncthreads();
     fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t acc1_col0 = (uint32_t)(p.T * p.Nc2);  // acc2[tile] at tile*Nc2, acc1[tile] after
+    // acc2[tile] at tile * NB2, acc1[tile] at acc1_col0 + tile * NB1 (NB = N, or 2N when stacked)
+    const uint32_t acc1_col0 = CFG::kStatic ? (uint32_t)CFG::ACC1 : (uint32_t)(p.T * p.Nc2);
 
     const int64_t nbatch = (a.n + p.I - 1) / p.I;
     const int64_t HW = (int64_t)p.H * p.W;
@@ -585,6 +603,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
             const uint32_t hlo_b = (uint32_t)(p.MC / 8) * plane_bytes;
             (void)hlo_b;
             const uint32_t id1 = idesc_of(128, p.MC, kP3), id2 = idesc_of(128, p.Nc2, kP3);
+            // stacked f16x3: the hi(A) MMA is 2N wide (static configurations only)
+            const uint32_t id1w = idesc_of(128, CFG::kStatic ? CFG::NB1 : p.MC, kP3);
+            const uint32_t id2w = idesc_of(128, CFG::kStatic ? CFG::NB2 : p.Nc2, kP3);
             const uint32_t rb = smem_u32(ring);
             const uint32_t lbo1 = p.pair ? 16u : plane_bytes;
             const int g1 = steps_per_slot(p.MC, p.pm, p.slot_bytes);
@@ -602,11 +623,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                         if constexpr (CFG::kStatic) {
                             constexpr uint32_t LBO1 = CFG::PAIR ? 16u : (uint32_t)CFG::PLANE16 * 16u;
                             const uint32_t alo0 = ((xb >> 4) & 0x3FFFu) | ((LBO1 >> 4) << 16);
-                            const uint32_t ringlo = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::MC * 16 >> 4) << 16);
+                            const uint32_t ringlo = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::NB1 * 16 >> 4) << 16);
                             issue_static<CFG::K1, CFG::PER1, CFG::AM1, CFG::WP, CFG::PLANE16, CFG::G1, CFG::KB1 / 16,
-                                         CFG::T, CFG::MC, CFG::PM, CFG::LOX16, CFG::ACC1, CFG::MC>(
+                                         CFG::T, CFG::MC, CFG::PM, CFG::LOX16, CFG::ACC1, CFG::NB1, false, CFG::STK1>(
                                 tmem, alo0, ringlo, (uint32_t)CFG::SLOT / 16u, id1, CFG::FOLD ? 0u : 1u, slot, phase,
-                                p.nslot, full, empty);
+                                p.nslot, full, empty, id1w);
                         } else
                                                 {
                             int tap = 0, kc = 0, q = 0;
@@ -658,11 +679,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                         if constexpr (CFG::kStatic) {
                             constexpr uint32_t LBO2 = (uint32_t)CFG::PLANE16 * 16u;
                             const uint32_t alo0 = ((hbj >> 4) & 0x3FFFu) | ((LBO2 >> 4) << 16);
-                            const uint32_t ringlo = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::NC2 * 16 >> 4) << 16);
+                            const uint32_t ringlo = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::NB2 * 16 >> 4) << 16);
                             issue_static<CFG::K2, CFG::PER2, false, CFG::WP, CFG::PLANE16, CFG::G2, CFG::KB2 / 16,
-                                         CFG::T, CFG::NC2, CFG::PM, CFG::LOH16, 0, CFG::NC2, CFG::HST>(
+                                         CFG::T, CFG::NC2, CFG::PM, CFG::LOH16, 0, CFG::NB2, CFG::HST, CFG::STK2>(
                                 tmem, alo0, ringlo, (uint32_t)CFG::SLOT / 16u, id2, 1u, slot, phase,
-                                p.nslot, full, empty);
+                                p.nslot, full, empty, id2w);
                         } else
                         {
                             int tap = 0, kc = 0, q = 0;
@@ -702,13 +723,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                         constexpr uint32_t LBO1 = CFG::PAIR ? 16u : (uint32_t)CFG::PLANE16 * 16u;
                         constexpr uint32_t LBO2 = (uint32_t)CFG::PLANE16 * 16u;
                         uint32_t alo1 = ((xb >> 4) & 0x3FFFu) | ((LBO1 >> 4) << 16);
-                        const uint32_t ring1 = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::MC * 16 >> 4) << 16);
-                        const uint32_t ring2 = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::NC2 * 16 >> 4) << 16);
+                        const uint32_t ring1 = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::NB1 * 16 >> 4) << 16);
+                        const uint32_t ring2 = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::NB2 * 16 >> 4) << 16);
                         long long tx0 = CLK();
                         issue_stream<CFG::K1, CFG::PER1, CFG::AM1, false, CFG::WP, CFG::PLANE16, CFG::G1, CFG::KB1 / 16,
-                                     CFG::T, CFG::MC, CFG::PM, CFG::LOX16, CFG::ACC1, CFG::MC, 1>(
+                                     CFG::T, CFG::MC, CFG::PM, CFG::LOX16, CFG::ACC1, CFG::NB1, 1, CFG::STK1>(
                             tmem, alo1, ring1, (uint32_t)CFG::SLOT / 16u, id1, 0u, slot, phase, p.nslot, full, empty,
-                            x_tile, xph, a1t);
+                            x_tile, xph, a1t, id1w);
                         if (kCycles && a.dbg) w_x += (unsigned long long)(CLK() - tx0);
                         xph ^= 1;
                         for (int j = 0; j < p.nch; j++) {
@@ -734,16 +755,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                         TWAIT(w_hd, mbar_wait(&a1f[t], a1fph));
                                         fence_after();
                                         issue_tile<CFG::K1, CFG::PER1, CFG::AM1, false, CFG::WP, CFG::PLANE16, CFG::G1,
-                                                   CFG::KB1 / 16, CFG::MC, CFG::PM, CFG::LOX16, CFG::ACC1, CFG::MC, NS1>(
-                                            t, tmem, alo1, bl1, id1, 0u);
+                                                   CFG::KB1 / 16, CFG::MC, CFG::PM, CFG::LOX16, CFG::ACC1, CFG::NB1, NS1,
+                                                   CFG::STK1>(t, tmem, alo1, bl1, id1, 0u, id1w);
                                         commit(&a1t[t]);
                                     }
                                     if (t >= 1) {
                                         TWAIT(w_hd, mbar_wait(&hdt_j[t < CFG::T ? t : CFG::T - 1], hdph));
                                         fence_after();
                                         issue_tile<CFG::K2, CFG::PER2, false, CFG::HST, CFG::WP, CFG::PLANE16, CFG::G2,
-                                                   CFG::KB2 / 16, CFG::NC2, CFG::PM, CFG::LOH16, 0, CFG::NC2, NS2>(
-                                            t - 1, tmem, alo2, bl2, id2, 1u);
+                                                   CFG::KB2 / 16, CFG::NC2, CFG::PM, CFG::LOH16, 0, CFG::NB2, NS2,
+                                                   CFG::STK2>(t - 1, tmem, alo2, bl2, id2, 1u, id2w);
                                     }
                                 }
 #pragma unroll
@@ -758,18 +779,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             }
                             if (j + 1 < p.nch) {
                                 issue_stream<CFG::K1, CFG::PER1, CFG::AM1, false, CFG::WP, CFG::PLANE16, CFG::G1,
-                                             CFG::KB1 / 16, CFG::T, CFG::MC, CFG::PM, CFG::LOX16, CFG::ACC1, CFG::MC, 0>(
+                                             CFG::KB1 / 16, CFG::T, CFG::MC, CFG::PM, CFG::LOX16, CFG::ACC1, CFG::NB1, 0,
+                                             CFG::STK1>(
                                     tmem, alo1, ring1, (uint32_t)CFG::SLOT / 16u, id1, 0u, slot, phase, p.nslot, full,
-                                    empty, a1f, a1fph, a1t);
+                                    empty, a1f, a1fph, a1t, id1w);
                                 a1fph ^= 1;
                             }
                             const uint32_t hbj = hb + (uint32_t)(hbi * hbuf_stride);
                             const uint32_t alo2 = ((hbj >> 4) & 0x3FFFu) | ((LBO2 >> 4) << 16);
                             long long th0 = CLK();
                             issue_stream<CFG::K2, CFG::PER2, false, CFG::HST, CFG::WP, CFG::PLANE16, CFG::G2, CFG::KB2 / 16,
-                                         CFG::T, CFG::NC2, CFG::PM, CFG::LOH16, 0, CFG::NC2, 1>(
+                                         CFG::T, CFG::NC2, CFG::PM, CFG::LOH16, 0, CFG::NB2, 1, CFG::STK2>(
                                 tmem, alo2, ring2, (uint32_t)CFG::SLOT / 16u, id2, 1u, slot, phase, p.nslot, full,
-                                empty, hdt + hbi * kMaxTiles, (hph >> hbi) & 1u, j + 1 == p.nch ? a2t : nullptr);
+                                empty, hdt + hbi * kMaxTiles, (hph >> hbi) & 1u, j + 1 == p.nch ? a2t : nullptr, id2w);
                             if (kCycles && a.dbg) w_hd += (unsigned long long)(CLK() - th0);
                             hph ^= 1u << hbi;
                             commit(&hd_empty[hbi]);
@@ -785,12 +807,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             tiles_first = true;
                             constexpr uint32_t LBO1 = CFG::PAIR ? 16u : (uint32_t)CFG::PLANE16 * 16u;
                             const uint32_t alo0 = ((xb >> 4) & 0x3FFFu) | ((LBO1 >> 4) << 16);
-                            const uint32_t ringlo = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::MC * 16 >> 4) << 16);
+                            const uint32_t ringlo = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::NB1 * 16 >> 4) << 16);
                             long long tx0 = CLK();
                             issue_static_tiles<CFG::K1, CFG::PER1, CFG::AM1, CFG::WP, CFG::PLANE16, CFG::G1,
-                                               CFG::KB1 / 16, CFG::T, CFG::MC, CFG::PM, CFG::LOX16, CFG::ACC1, CFG::MC>(
+                                               CFG::KB1 / 16, CFG::T, CFG::MC, CFG::PM, CFG::LOX16, CFG::ACC1, CFG::NB1,
+                                               CFG::STK1>(
                                 tmem, alo0, ringlo, (uint32_t)CFG::SLOT / 16u, id1, CFG::FOLD ? 0u : 1u, slot, phase,
-                                p.nslot, full, empty, x_tile, xph);
+                                p.nslot, full, empty, x_tile, xph, id1w);
                             if (kCycles && a.dbg) w_x += (unsigned long long)(CLK() - tx0);
                         }
                     }
@@ -832,6 +855,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
         const int eT = S ? CFG::T : p.T;
         const int eMC = S ? CFG::MC : p.MC;
         const int eNC2 = S ? CFG::NC2 : p.Nc2;
+        // stacked f16x3 (mma_prec): column n + N of a tile's accumulator holds hi(x) W_lo of column n
+        constexpr bool kSTK1 = S && CFG::STK1 != 0, kSTK2 = S && CFG::STK2 != 0;
+        const int eA1S = S ? CFG::NB1 : p.MC;    // acc1 columns per tile
+        const int eA2S = S ? CFG::NB2 : p.Nc2;   // acc2 columns per tile
         const int eCp = S ? CFG::CP : p.Cp;
         const int ec = S ? CFG::C : p.c;
         const int eH = S ? CFG::H : p.H;
@@ -927,7 +954,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
             return a.bias + (int64_t)tb * (p.Mp + eNC2) + p.Mp;
         };
         auto init_acc2 = [&](const float* b2src, int tile) {
-            const uint32_t base = tmem + lane_addr + (uint32_t)(tile * eNC2);
+            const uint32_t base = tmem + lane_addr + (uint32_t)(tile * eA2S);
             if (ehst && ehc != 8) {   // columns [hc, 2hc) carry b2, the side taps start at 0
 #pragma unroll
                 for (int g = 0; g < 9; g++) {
@@ -953,11 +980,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
 #pragma unroll
                         for (int e = 0; e < 16; e++) v16[e] = __ldg(b2src + cb2 + g + e);
                         tmem_st16(base + (uint32_t)(cb2 + g), v16);
+                        if constexpr (kSTK2) {
+#pragma unroll
+                            for (int e = 0; e < 16; e++) v16[e] = 0.f;
+                            tmem_st16(base + (uint32_t)(eNC2 + cb2 + g), v16);
+                        }
                     } else {
                         float v8[8];
 #pragma unroll
                         for (int e = 0; e < 8; e++) v8[e] = __ldg(b2src + cb2 + g + e);
                         tmem_st8(base + (uint32_t)(cb2 + g), v8);
+                        if constexpr (kSTK2) {
+#pragma unroll
+                            for (int e = 0; e < 8; e++) v8[e] = 0.f;
+                            tmem_st8(base + (uint32_t)(eNC2 + cb2 + g), v8);
+                        }
                     }
                 }
             }
@@ -979,18 +1016,29 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                     for (int e = 0; e < 16; e++) v16[e] = __ldg(b1src + 16 + e);
                     tmem_st16(tmem + lane_addr + col + 16, v16);
                 }
+                if constexpr (kSTK1) {   // stacked: the hi(x) W_lo columns start at zero
+#pragma unroll
+                    for (int e = 0; e < 16; e++) v16[e] = 0.f;
+                    tmem_st16(tmem + lane_addr + col + eMC, v16);
+                    if (n == 32) tmem_st16(tmem + lane_addr + col + eMC + 16, v16);
+                }
             } else {
                 float v8[8];
 #pragma unroll
                 for (int e = 0; e < 8; e++) v8[e] = __ldg(b1src + e);
                 tmem_st8(tmem + lane_addr + col, v8);
+                if constexpr (kSTK1) {
+#pragma unroll
+                    for (int e = 0; e < 8; e++) v8[e] = 0.f;
+                    tmem_st8(tmem + lane_addr + col + eMC, v8);
+                }
             }
         };
         for (int tile = 0; tile < eT; tile++) {
             if (!ehst || (tile & 1) == half) init_acc2(bias2_of(0), tile);
             if (!efold)
                 for (int g0 = 0; g0 < cw1; g0 += 32)
-                    init_acc1_cols(bias1_of(0) + cb1 + g0, acc1_col0 + (uint32_t)(tile * eMC + cb1 + g0),
+                    init_acc1_cols(bias1_of(0) + cb1 + g0, acc1_col0 + (uint32_t)(tile * eA1S + cb1 + g0),
                                    cw1 - g0 < 32 ? cw1 - g0 : 32);
         }
         tmem_wait_st();
@@ -1090,26 +1138,37 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                         // while pair k is converted and stored (one wait::ld per pair)
                         constexpr int T = CFG::T, NP = (CFG::T + 1) / 2, CW1 = CFG::MC / 2;   // 16 or 8 columns
                         float v[2][2][CW1];
-                        auto issue = [&](int q0, float (&vv)[2][CW1]) {
+                        float vs[kSTK1 ? 2 : 1][2][kSTK1 ? CW1 : 1];   // stacked: the hi(x) W_lo columns
+                        auto issue = [&](int q0, int bi) {
                             TWAIT(w_a1, mbar_wait(&a1t[q0 + 1 < T ? q0 + 1 : T - 1], a1ph));
                             fence_after();
 #pragma unroll
                             for (int u = 0; u < 2; u++)
                                 if (q0 + u < T) {
-                                    const uint32_t ta = tmem + lane_addr + acc1_col0 + (uint32_t)((q0 + u) * CFG::MC + cb1);
-                                    if constexpr (CW1 == 16) tmem_ld16(ta, vv[u]); else tmem_ld8(ta, vv[u]);
+                                    const uint32_t ta = tmem + lane_addr + acc1_col0 + (uint32_t)((q0 + u) * CFG::NB1 + cb1);
+                                    if constexpr (CW1 == 16) tmem_ld16(ta, v[bi][u]); else tmem_ld8(ta, v[bi][u]);
+                                    if constexpr (kSTK1) {
+                                        if constexpr (CW1 == 16) tmem_ld16(ta + CFG::MC, vs[bi][u]);
+                                        else tmem_ld8(ta + CFG::MC, vs[bi][u]);
+                                    }
                                 }
                         };
-                        issue(0, v[0]);
+                        issue(0, 0);
 #pragma unroll
                         for (int k = 0; k < NP; k++) {
                             const int q0 = 2 * k;
                             tmem_wait_ld();
+                            if constexpr (kSTK1) {
+#pragma unroll
+                                for (int u = 0; u < 2; u++)
+#pragma unroll
+                                    for (int e = 0; e < CW1; e++) v[k & 1][u][e] += vs[k & 1][u][e];
+                            }
                             if (j + 1 < p.nch) {   // acc1 tiles free for the next conv1 chunk
                                 fence_before();
                                 for (int u = 0; u < 2 && q0 + u < T; u++) mbar_arrive(&a1f[q0 + u]);
                             }
-                            if (k + 1 < NP) issue(q0 + 2, v[(k + 1) & 1]);
+                            if (k + 1 < NP) issue(q0 + 2, (k + 1) & 1);
 #pragma unroll
                             for (int u = 0; u < 2; u++) {
                                 if (q0 + u >= T) break;
@@ -1158,6 +1217,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
 #pragma unroll
                         for (int q0 = 0; q0 < NL; q0 += LB) {
                             float v[LB][LW];
+                            float vs[kSTK1 ? LB : 1][kSTK1 ? LW : 1];   // stacked: the hi(x) W_lo columns
                             if constexpr (CFG::STREAM) {   // NG == 1: q = tile
                                 TWAIT(w_a1, mbar_wait(&a1t[q0 + LB - 1 < NL ? q0 + LB - 1 : NL - 1], a1ph));
                                 fence_after();
@@ -1166,10 +1226,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             for (int u = 0; u < LB; u++) {
                                 if (q0 + u >= NL) break;
                                 const int q = q0 + u, tile = q / NG, g = q % NG;
-                                const uint32_t ta = tmem + lane_addr + acc1_col0 + (uint32_t)(tile * CFG::MC + cb1 + g * LW);
+                                const uint32_t ta = tmem + lane_addr + acc1_col0 + (uint32_t)(tile * CFG::NB1 + cb1 + g * LW);
                                 if constexpr (LW == 16) tmem_ld16(ta, v[u]); else tmem_ld8(ta, v[u]);
+                                if constexpr (kSTK1) {
+                                    if constexpr (LW == 16) tmem_ld16(ta + CFG::MC, vs[u]); else tmem_ld8(ta + CFG::MC, vs[u]);
+                                }
                             }
                             tmem_wait_ld();
+                            if constexpr (kSTK1) {
+#pragma unroll
+                                for (int u = 0; u < LB; u++)
+#pragma unroll
+                                    for (int e = 0; e < LW; e++) v[u][e] += vs[u][e];
+                            }
                             if constexpr (CFG::STREAM) {   // acc1 tiles free for the next conv1 chunk
                                 if (j + 1 < p.nch) {
                                     fence_before();
@@ -1226,7 +1295,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                     }
                                     store8(hbuf_j, hlo_buf, (cb1 + g * LW) / 8 + h, r, h8);
                                 }
-                                init_acc1_cols(b1n + g * LW, acc1_col0 + (uint32_t)(tile * CFG::MC + cb1 + g * LW), LW);
+                                init_acc1_cols(b1n + g * LW, acc1_col0 + (uint32_t)(tile * CFG::NB1 + cb1 + g * LW), LW);
                                 }
                             }
                             if constexpr (CFG::STREAM) {   // hidden rows of these tiles -> conv2_j
@@ -1240,7 +1309,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                     for (int tile = 0; tile < eT; tile++) {
                         int r = tile * 128 + row_in_tile, ii, y, x;
                         const bool valid = rowpix(r, ii, y, x) && ii < nimg;
-                        const uint32_t col = acc1_col0 + (uint32_t)(tile * eMC + cb1);
+                        const uint32_t col = acc1_col0 + (uint32_t)(tile * eA1S + cb1);
                         for (int g0 = 0; g0 < cw1; g0 += 32) {
                             const int n = cw1 - g0 < 32 ? cw1 - g0 : 32;   // 8, 16 or 32
                             float va[16], vb[16];
@@ -1251,6 +1320,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 tmem_ld8(tmem + lane_addr + col + g0, v8);
 #pragma unroll
                                 for (int e = 0; e < 8; e++) va[e] = v8[e];
+                            }
+                            if constexpr (kSTK1) {   // fold the hi(x) W_lo columns (n = 16 or 32 here)
+                                float sa[16], sb[16];
+                                if (n >= 16) tmem_ld16(tmem + lane_addr + col + eMC + g0, sa);
+                                if (n == 32) tmem_ld16(tmem + lane_addr + col + eMC + g0 + 16, sb);
+                                if (n == 8) {
+                                    float s8[8];
+                                    tmem_ld8(tmem + lane_addr + col + eMC + g0, s8);
+#pragma unroll
+                                    for (int e = 0; e < 8; e++) sa[e] = s8[e];
+                                }
+                                tmem_wait_ld();
+#pragma unroll
+                                for (int e = 0; e < 16; e++) {
+                                    va[e] += (n >= 16 || e < 8) ? sa[e] : 0.f;
+                                    vb[e] += n == 32 ? sb[e] : 0.f;
+                                }
                             }
                             tmem_wait_ld();
 #pragma unroll
@@ -1715,18 +1801,43 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                     const bool valid = any2 && rowpix(r, ii, y, x) && ii < nimg;
                     float v0[16], v1[16], v2[16];
                     {
-                        const uint32_t col = (uint32_t)(tile * eNC2 + cb2);
+                        const uint32_t col = (uint32_t)(tile * eA2S + cb2);
                         if (cw2 == 8) {
                             float v8[8];
                             tmem_ld8(tmem + lane_addr + col, v8);
                             tmem_wait_ld();
 #pragma unroll
                             for (int e = 0; e < 8; e++) v0[e] = v8[e];
+                            if constexpr (kSTK2) {   // fold the hi(x) W_lo columns
+                                tmem_ld8(tmem + lane_addr + col + eNC2, v8);
+                                tmem_wait_ld();
+#pragma unroll
+                                for (int e = 0; e < 8; e++) v0[e] += v8[e];
+                            }
                         } else {
                             tmem_ld16(tmem + lane_addr + col, v0);
                             if (cw2 >= 32) tmem_ld16(tmem + lane_addr + col + 16, v1);
                             if (cw2 >= 48) tmem_ld16(tmem + lane_addr + col + 32, v2);
                             tmem_wait_ld();
+                            if constexpr (kSTK2) {   // fold the hi(x) W_lo columns, one 16-column group at a time
+                                float t16[16];
+                                tmem_ld16(tmem + lane_addr + col + eNC2, t16);
+                                tmem_wait_ld();
+#pragma unroll
+                                for (int e = 0; e < 16; e++) v0[e] += t16[e];
+                                if (cw2 >= 32) {
+                                    tmem_ld16(tmem + lane_addr + col + eNC2 + 16, t16);
+                                    tmem_wait_ld();
+#pragma unroll
+                                    for (int e = 0; e < 16; e++) v1[e] += t16[e];
+                                }
+                                if (cw2 >= 48) {
+                                    tmem_ld16(tmem + lane_addr + col + eNC2 + 32, t16);
+                                    tmem_wait_ld();
+#pragma unroll
+                                    for (int e = 0; e < 16; e++) v2[e] += t16[e];
+                                }
+                            }
                         }
                     }
                     if (valid && esplit) {
@@ -1856,7 +1967,7 @@ static double mma_cyc(int N) { return std::max(N / 2.0, 32.0 + N / 4.0); }
 //   a 2-slot ring cannot hide the L2 latency of the weight stream (x1.3)
 // Tuned plans for the Arch-C stage shapes (chosen from CI_DEBUG_CYCLES measurements);
 // other shapes use the cost model.
-struct TunedPlan { int H, W, c, m, pm, MC, T, nhd, nslot, hst; };
+struct TunedPlan { int H, W, c, m, pm, MC, T, nhd, nslot, hst, stk1, stk2; };
 static const TunedPlan kTuned[] = {
     {16, 16, 6, 64, 0, 32, 7, 2, 3, 1},    // stage 1 bf16: SMEM-resident state fits
     {8, 8, 24, 128, 0, 128, 2, 1, 3, 1},   // stage 2 bf16: wide hst (N = 3 x 24 -> 80), one N = 128 conv1 chunk, T = 2
@@ -1870,28 +1981,32 @@ static const TunedPlan kTuned[] = {
     {16, 16, 6, 64, 1, 32, 5, 1, 4, 1},    // stage 1 f16x2: MC = 32, T = 5, SMEM state
     {8, 8, 24, 128, 1, 128, 2, 1, 3, 1},   // stage 2 f16x2: wide hst, one N = 128 conv1 chunk
     {4, 4, 96, 256, 1, 128, 1, 1, 4, 0},   // stage 3 f16x2: N = 128 conv1 chunks, T = 1
-    {16, 16, 6, 64, 2, 32, 5, 1, 4, 1},    // stage 1 f16x3
     {8, 8, 24, 128, 2, 128, 2, 1, 3, 1},   // stage 2 f16x3
+    {16, 16, 6, 64, 2, 32, 5, 1, 4, 1, 1, 0},    // stage 1 f16x3, stacked conv1 (CI_NO_STK: unstacked)
+    {16, 16, 6, 64, 2, 32, 5, 1, 4, 1},    // stage 1 f16x3
+    {4, 4, 96, 256, 2, 128, 1, 1, 4, 0, 1, 1},   // stage 3 f16x3, stacked conv1 + conv2
+    {16, 16, 64, 64, 2, 32, 3, 1, 4, 0, 1, 0},   // learned-encoder tail f16x3, stacked conv1
     {4, 4, 96, 256, 2, 128, 1, 1, 4, 0},   // stage 3 f16x3
     {16, 16, 12, 64, 0, 32, 5, 2, 4, 1},   // CR (residual, f1) stage 1 bf16: wide hst (N = 48)
     {16, 16, 12, 64, 0, 64, 5, 1, 4, 0},   // CR stage 1 bf16, plain conv2 (CI_NO_WIDE_HST)
     {16, 16, 12, 64, 2, 32, 7, 1, 3, 0},   // CR stage 1 f16x3
 };
 
-static bool make_plan(const StageInfo& S, int pm, StagePlan& best) {
+static bool make_plan(const StageInfo& S, int pm, StagePlan& best, bool allow_stk = true) {
     StagePlan p{};
     static const bool no_wide_hst = getenv("CI_NO_WIDE_HST") != nullptr;   // A/B switch
     static const bool s1_mc32 = getenv("CI_S1_MC32") != nullptr;           // A/B switch
     static const bool s1_mc64 = getenv("CI_S1_MC64") != nullptr;           // A/B switch
     static const bool no_tuned = getenv("CI_NO_TUNED") != nullptr;         // A/B switch: cost model only
+    static const bool no_stk = getenv("CI_NO_STK") != nullptr;             // A/B switch: unstacked f16x3
     // CI_TUNE="H,W,c,m,pm,MC,T,nhd,nslot,hst;..." overrides the table (same-box plan A/B)
     static const std::vector<TunedPlan> env_tuned = [] {
         std::vector<TunedPlan> v;
         const char* e = getenv("CI_TUNE");
         while (e && *e) {
             TunedPlan t{};
-            if (sscanf(e, "%d,%d,%d,%d,%d,%d,%d,%d,%d,%d", &t.H, &t.W, &t.c, &t.m, &t.pm, &t.MC, &t.T, &t.nhd, &t.nslot,
-                       &t.hst) == 10)
+            if (sscanf(e, "%d,%d,%d,%d,%d,%d,%d,%d,%d,%d,%d,%d", &t.H, &t.W, &t.c, &t.m, &t.pm, &t.MC, &t.T, &t.nhd,
+                       &t.nslot, &t.hst, &t.stk1, &t.stk2) >= 10)
                 v.push_back(t);
             e = strchr(e, ';');
             if (e) e++;
@@ -1904,7 +2019,7 @@ static bool make_plan(const StageInfo& S, int pm, StagePlan& best) {
     if (!no_tuned)
     for (const auto& tp : kTuned)   // first match wins
         if (!tuned && tp.H == S.H && tp.W == S.W && tp.c == S.c && tp.m == S.m && tp.pm == pm &&
-            !(no_wide_hst && tp.hst && tp.c > 8) && !(tp.c == 24 && !tp.pm && tp.MC == 64 && tp.hst && s1_mc32) &&
+            !((no_stk || !allow_stk) && (tp.stk1 || tp.stk2)) && !(no_wide_hst && tp.hst && tp.c > 8) && !(tp.c == 24 && !tp.pm && tp.MC == 64 && tp.hst && s1_mc32) &&
             !(tp.c == 24 && !tp.pm && tp.MC == 128 && tp.hst && (s1_mc64 || s1_mc32)))
             tuned = &tp;
     p.H = S.H; p.W = S.W; p.Wp = S.W + 1; p.G = p.Wp + 2;
@@ -1919,6 +2034,8 @@ static bool make_plan(const StageInfo& S, int pm, StagePlan& best) {
     const double P3f = 1.0 + pm;   // MMAs per k-step: f16x2 hi(A)*B + lo(A)*B, f16x3 + hi(A)*lo(B)
     const int img_rows = (p.H + 1) * p.Wp;
     const int k1 = p.pair ? kPairK1 : (p.tri ? kTriK1 : 9 * (p.Cp / 16));
+    p.stk1 = (tuned && pm == 2 && allow_stk) ? tuned->stk1 : 0;
+    p.stk2 = (tuned && pm == 2 && allow_stk) ? tuned->stk2 : 0;
     double best_cost = 1e300;
     // conv2 with horizontal tap stacking (mandatory for c <= 8, optional up to c = 24) or plain
     for (int hopt = 1; hopt >= 0; hopt--) {
@@ -1937,7 +2054,7 @@ static bool make_plan(const StageInfo& S, int pm, StagePlan& best) {
         const int nch = p.Mp / MC;
         const int k2 = (p.hst ? 3 : 9) * (MC / 16);
         for (int T = 1; T <= 8; T++) {
-            if (T * (MC + p.Nc2) > 512) break;
+            if (T * (MC * (1 + p.stk1) + p.Nc2 * (1 + p.stk2)) > 512) break;
             if (tuned && T != tuned->T) continue;
             const int I = (T * 128) / img_rows;
             if (I < 1) continue;
@@ -1982,7 +2099,7 @@ static bool make_plan(const StageInfo& S, int pm, StagePlan& best) {
     }
     }   // hopt
     if (best_cost >= 1e300) return false;
-    int cols = best.T * (best.MC + best.Nc2);
+    int cols = best.T * (best.MC * (1 + best.stk1) + best.Nc2 * (1 + best.stk2));
     best.tmem_cols = 32;
     while (best.tmem_cols < cols) best.tmem_cols *= 2;
     return true;
@@ -1999,17 +2116,27 @@ static int conv2_col_channel(const StagePlan& p, int n) {
 // one k-step B tile: [khalf][n][8], bf16 (CI_PREC_BF16) or fp16 (f16x2: the weights are rounded
 // once to fp16, a fixed perturbation of h that every query sees alike -- DESIGN.md 5)
 // f16x3 (residual archs) appends the fp16 lo tile w - hi)
-static void put_tile(std::vector<uint16_t>& out, const std::vector<float>& w, int N, int pm) {
+// stacked (f16x3 only): [khalf][part][n][8] -- per K half the hi rows then the lo rows, one
+// 2N-row B operand (LBO = 2N * 16 B); the lo(A) x W_hi MMA reads its first N rows
+static void put_tile(std::vector<uint16_t>& out, const std::vector<float>& w, int N, int pm, int stacked = 0) {
     // w is [N][16] (n, kk)
+    auto val = [&](int part, int kh, int n, int e) -> uint16_t {
+        const float v = w[(size_t)n * 16 + kh * 8 + e];
+        if (pm == 0) return f2bf(v);
+        const uint16_t hi = f2h(v);
+        return part == 0 ? hi : f2h(v - h2f(hi));
+    };
+    if (stacked) {
+        for (int kh = 0; kh < 2; kh++)
+            for (int part = 0; part < 2; part++)
+                for (int n = 0; n < N; n++)
+                    for (int e = 0; e < 8; e++) out.push_back(val(part, kh, n, e));
+        return;
+    }
     for (int part = 0; part < (pm == 2 ? 2 : 1); part++)
         for (int kh = 0; kh < 2; kh++)
             for (int n = 0; n < N; n++)
-                for (int e = 0; e < 8; e++) {
-                    const float v = w[(size_t)n * 16 + kh * 8 + e];
-                    if (pm == 0) { out.push_back(f2bf(v)); continue; }
-                    const uint16_t hi = f2h(v);
-                    out.push_back(part == 0 ? hi : f2h(v - h2f(hi)));
-                }
+                for (int e = 0; e < 8; e++) out.push_back(val(part, kh, n, e));
 }
 
 static void pack_block(const StagePlan& p, const float* W1, const float* b1, const float* W2, int pm,
@@ -2057,7 +2184,7 @@ static void pack_block(const StagePlan& p, const float* W1, const float* b1, con
                     tile[(size_t)n * 16 + kk] = v;
                 }
             }
-            put_tile(out, tile, p.MC, pm);
+            put_tile(out, tile, p.MC, pm, p.stk1);
         }
         // conv2 chunk j: N = Nc2 outputs, K = this chunk's hidden channels
         if (is2)
@@ -2072,7 +2199,7 @@ static void pack_block(const StagePlan& p, const float* W1, const float* b1, con
                     else
                         tile[(size_t)n * 16 + kk] = w2(conv2_col_channel(p, n), h, tap / 3 - 1, tap % 3 - 1);
                 }
-            put_tile(out, tile, p.Nc2, pm);
+            put_tile(out, tile, p.Nc2, pm, p.stk2);
         }
     }
 }
@@ -2089,14 +2216,16 @@ struct UmmaState {
 
 // ---- compile-time specialisations for the Arch-C stage plans (see make_plan) -----------------
 typedef void (*StageKernel)(StageArgs);
-struct SpecEntry { int Wp, Cp, MC, Nc2, T, p3, slot, H, c, sst, hst, fold, split, res; StageKernel fn; };
-#define CI_SPEC_CFG(WP, CP, MC, NC2, T, PM, SLOT, H, C, SST, HST, RES) \
-    SCfg<WP, CP, MC, NC2, T, PM, SLOT, H, C, SST, HST, RES>
-#define CI_SPEC_X(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES)                                          \
+struct SpecEntry { int Wp, Cp, MC, Nc2, T, p3, slot, H, c, sst, hst, fold, split, res, stk1, stk2; StageKernel fn; };
+#define CI_SPEC_CFG(WP, CP, MC, NC2, T, PM, SLOT, H, C, SST, HST, RES, S1, S2) \
+    SCfg<WP, CP, MC, NC2, T, PM, SLOT, H, C, SST, HST, RES, S1, S2>
+#define CI_SPEC_XS(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES, S1, S2)                                  \
     {WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST,                                                         \
-     CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES)::FOLD,                                  \
-     CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES)::SPLIT, RES,                            \
-     k_stage<CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES)>}
+     CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES, S1, S2)::FOLD,                          \
+     CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES, S1, S2)::SPLIT, RES, S1, S2,            \
+     k_stage<CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES, S1, S2)>}
+#define CI_SPEC_X(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES) \
+    CI_SPEC_XS(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES, 0, 0)
 #define CI_SPEC(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST) \
     CI_SPEC_X(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, ((C) <= 8), 0)
 #define CI_SPEC_R(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST) \
@@ -2114,6 +2243,9 @@ static const SpecEntry kSpecs[] = {
     CI_SPEC(17, 8, 32, 32, 5, 2, 16384, 16, 6, 1),   // C stage 1, f16x3 (CI_PREC_FP32)
     CI_SPEC_X(9, 32, 128, 80, 2, 2, 16384, 8, 24, 0, 1, 0),  // C stage 2, f16x3
     CI_SPEC(5, 96, 128, 96, 1, 2, 16384, 4, 96, 0),  // C stage 3, f16x3
+    CI_SPEC_XS(17, 8, 32, 32, 5, 2, 16384, 16, 6, 1, 1, 0, 1, 0),   // C stage 1, f16x3, stacked conv1
+    CI_SPEC_XS(5, 96, 128, 96, 1, 2, 16384, 4, 96, 0, 0, 0, 1, 1),  // C stage 3, f16x3, stacked conv1 + conv2
+    CI_SPEC_XS(17, 64, 32, 64, 3, 2, 16384, 16, 64, 0, 0, 0, 1, 0), // encoder tail, f16x3, stacked conv1
     CI_SPEC(17, 8, 16, 32, 5, 2, 16384, 16, 6, 1),   // C stage 1, f16x3, MC = 16, nhd = 2 (A/B)
     CI_SPEC(17, 8, 32, 32, 3, 2, 16384, 16, 6, 1),   // C stage 1, f16x3, T = 3, I = 1, nhd = 2 (A/B)
     CI_SPEC(17, 64, 32, 64, 5, 0, 16384, 16, 64, 0),  // learned-encoder tail (E2, E3), bf16
@@ -2130,15 +2262,28 @@ static const SpecEntry kSpecs[] = {
 
 // Coupling specialisations carry no residual / ELU code (it would cost them registers); residual
 // blocks and ELU use an RES specialisation or the generic kernel.
+static StageKernel find_spec(const StagePlan& p, int residual, int act) {
+    for (const auto& e : kSpecs)
+        if (e.Wp == p.Wp && e.Cp == p.Cp && e.MC == p.MC && e.Nc2 == p.Nc2 && e.T == p.T && e.p3 == p.pm &&
+            e.slot == p.slot_bytes && e.H == p.H && e.c == p.c && e.sst == p.sstate && e.hst == p.hst &&
+            e.fold == p.fold && e.split == p.split && e.stk1 == p.stk1 && e.stk2 == p.stk2 &&   // packing and epilogue must agree
+            e.res == (residual ? 1 : 0) && (e.res || act == 0))   // coupling specs: ReLU only
+            return e.fn;
+    return nullptr;
+}
+// stacked plans exist only as specialisations (umma_prepare re-plans unstacked otherwise)
 static StageKernel pick_kernel(const StagePlan& p, const StageArgs& a) {
-    if (!getenv("CI_NO_STATIC"))
-        for (const auto& e : kSpecs)
-            if (e.Wp == p.Wp && e.Cp == p.Cp && e.MC == p.MC && e.Nc2 == p.Nc2 && e.T == p.T && e.p3 == p.pm &&
-                e.slot == p.slot_bytes && e.H == p.H && e.c == p.c && e.sst == p.sstate && e.hst == p.hst &&
-                e.fold == p.fold && e.split == p.split &&   // packing and epilogue must agree
-                e.res == (a.residual ? 1 : 0) && (e.res || a.act == 0))   // coupling specs: ReLU only
-                return e.fn;
+    if (!getenv("CI_NO_STATIC") || p.stk1 || p.stk2) {
+        StageKernel f = find_spec(p, a.residual, a.act);
+        if (f) return f;
+    }
     return k_stage<SDyn>;
+}
+// plan a stage; a stacked plan without a specialised kernel falls back to the unstacked plan
+static bool make_plan_spec(const StageInfo& S, int pm, StagePlan& p, int residual, int act) {
+    if (!make_plan(S, pm, p)) return false;
+    if ((p.stk1 || p.stk2) && !find_spec(p, residual, act)) return make_plan(S, pm, p, false);
+    return true;
 }
 
 ci_status_t umma_prepare(Model* m, const float* host_params) {
@@ -2150,7 +2295,7 @@ ci_status_t umma_prepare(Model* m, const float* host_params) {
     std::vector<float> bias;
     for (int s = 0; s < m->n_stages; s++) {
         const StageInfo& S = m->st[s];
-        if (!make_plan(S, pm, U->plan[s])) {
+        if (!make_plan_spec(S, pm, U->plan[s], m->arch.block_kind == 1, m->arch.act)) {
             delete U;
             set_error("stage %d (%dx%d, c=%d, m=%d) does not fit the tcgen05 kernel", s, S.H, S.W, S.c, S.m);
             return CI_ERR_UNSUPPORTED;
@@ -2159,10 +2304,10 @@ ci_status_t umma_prepare(Model* m, const float* host_params) {
         if (getenv("CI_DEBUG_PLAN"))
             fprintf(stderr,
                     "[ci plan] stage %d %dx%d c=%d m=%d pm=%d: Cp=%d Mp=%d MC=%d nch=%d Nc2=%d T=%d I=%d "
-                    "k1=%d k2=%d slots=%dx%d smem=%zu tmem=%d blk_bytes=%lld M-eff=%.3f nhd=%d sst=%d est=%.0f cyc/img/blk\n",
+                    "k1=%d k2=%d slots=%dx%d smem=%zu tmem=%d blk_bytes=%lld M-eff=%.3f nhd=%d sst=%d stk=%d%d est=%.0f cyc/img/blk\n",
                     s, p.H, p.W, p.c, p.m, p.pm, p.Cp, p.Mp, p.MC, p.nch, p.Nc2, p.T, p.I, p.k1, p.k2,
                     p.nslot, p.slot_bytes, p.smem, p.tmem_cols, (long long)p.blk_bytes,
-                    (double)p.I * p.H * p.W / (p.T * 128.0), p.nhd, p.sstate, p.est_cycles);
+                    (double)p.I * p.H * p.W / (p.T * 128.0), p.nhd, p.sstate, p.stk1, p.stk2, p.est_cycles);
         // align each stage stream to 128 B
         while ((pack.size() * 2) % 128) pack.push_back(0);
         U->wpack_off[s] = (int64_t)pack.size() * 2;
@@ -2194,7 +2339,7 @@ ci_status_t umma_prepare(Model* m, const float* host_params) {
         // split precisions: the encoder has no exact inverse to absorb a weight perturbation (x_p
         // itself is compared), so its two convolutions keep the weights exact (f16x3; ~2% of the FLOPs)
         const int pm_enc = pm ? 2 : 0;
-        if (make_plan(S, pm_enc, U->enc_plan)) {
+        if (make_plan_spec(S, pm_enc, U->enc_plan, 0, 0)) {
             const StagePlan& p = U->enc_plan;
             while ((pack.size() * 2) % 128) pack.push_back(0);
             U->enc_wpack_off = (int64_t)pack.size() * 2;
@@ -2213,9 +2358,9 @@ ci_status_t umma_prepare(Model* m, const float* host_params) {
             if (getenv("CI_DEBUG_PLAN"))
                 fprintf(stderr,
                         "[ci plan] encoder tail %dx%d c=%d m=%d pm=%d: MC=%d nch=%d Nc2=%d T=%d I=%d k1=%d k2=%d "
-                        "slots=%dx%d smem=%zu tmem=%d nhd=%d sst=%d est=%.0f\n",
+                        "slots=%dx%d smem=%zu tmem=%d nhd=%d sst=%d stk=%d%d est=%.0f\n",
                         p.H, p.W, p.c, p.m, p.pm, p.MC, p.nch, p.Nc2, p.T, p.I, p.k1, p.k2, p.nslot, p.slot_bytes,
-                        p.smem, p.tmem_cols, p.nhd, p.sstate, p.est_cycles);
+                        p.smem, p.tmem_cols, p.nhd, p.sstate, p.stk1, p.stk2, p.est_cycles);
         }
     }
     cudaError_t e = cudaMalloc(&m->d_wpack, pack.size() * 2);
@@ -2374,7 +2519,7 @@ ci_status_t ci_test_plan(int32_t H, int32_t W, int32_t c, int32_t m, int32_t pm,
     if (residual) c = -c;
     S.H = H; S.W = W; S.c = c; S.m = m; S.C = residual ? c : 2 * c; S.nb = 1;
     ci::StagePlan p;
-    if (!ci::make_plan(S, pm, p)) { ci::set_error("no plan"); return CI_ERR_UNSUPPORTED; }
+    if (!ci::make_plan_spec(S, pm, p, residual ? 1 : 0, residual ? 1 : 0)) { ci::set_error("no plan"); return CI_ERR_UNSUPPORTED; }
     ci::StageArgs sa{};
     sa.residual = residual ? 1 : 0;
     sa.act = residual ? 1 : 0;   // the residual archs use ELU, the coupling archs ReLU
