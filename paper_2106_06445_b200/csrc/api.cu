@@ -215,7 +215,7 @@ ci_status_t ci_model_create(const ci_arch_t* arch, const float* host_params, siz
         }
         if (!enc_supported(a.in_c, a.enc_c1, a.in_h, a.in_w)) {
             delete m;
-            set_error("learned encoder: in_c must be 3, enc_c1 4, 8 or 16, in_w even and dividing 256, in_h even");
+            set_error("learned encoder: in_c must be 3, enc_c1 4, 8 or 16, in_w 8, 16 or 32, in_h even, in_h * in_w <= 1024");
             return CI_ERR_UNSUPPORTED;
         }
         m->enc_off = off;
