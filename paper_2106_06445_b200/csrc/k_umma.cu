@@ -439,7 +439,7 @@ constexpr bool kXPrefetch = false;   // A/B switch
 constexpr bool kXPrefetch = true;    // cross-batch X prefetch (epilogue, see x_pref)
 #endif
 constexpr int kMaxTiles = 8;                     // T <= 8 (512 TMEM columns / >= 64 per tile)
-constexpr int kBarBytes = 1024;                  // mbarriers, TMEM slot, batch queue, staged conv2 bias
+constexpr int kBarBytes = 1088;                  // mbarriers, TMEM slot, batch queue, staged conv2 bias
 
 // Cycle instrumentation (CI_DEBUG_CYCLES; inactive unless requested).  -DCI_NO_CYCLES
 // compiles it out; same-box A/B showed no gain from that (s2 got slower), so it stays in.
@@ -494,6 +494,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
     uint64_t* hdt = x_full + 44;       // [2][kMaxTiles] hidden rows of tile t written (all threads)
     uint64_t* a2t = x_full + 60;       // [kMaxTiles] last conv2 chunk of tile t done (tcgen05.commit)
     float* sbias2 = reinterpret_cast<float*>(x_full + 68);   // [96] next block's conv2 bias (wide hst)
+    // STREAM with one hidden buffer: h2t[t] = conv2 of a non-last chunk has finished M-tile t (one
+    // tcgen05.commit per tile), so the next chunk's conv1 epilogue may overwrite the hidden rows of
+    // tile t-1 once tile t is done, instead of waiting for the whole chunk (hd_empty)
+    uint64_t* h2t = x_full + 116;      // [kMaxTiles]
 
     // ---- zero the activation buffers (pads and guards must read as 0)
     {
@@ -511,7 +515,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
         mbar_init(acc2_full, 1);
         for (int i = 0; i < 4; i++) { mbar_init(&bqf[i], 1); mbar_init(&bqe[i], 1 + kEpiThreads); }
         for (int i = 0; i < kMaxTiles; i++) {
-            mbar_init(&a1t[i], 1); mbar_init(&a1f[i], kEpiThreads); mbar_init(&a2t[i], 1);
+            mbar_init(&a1t[i], 1); mbar_init(&a1f[i], kEpiThreads); mbar_init(&a2t[i], 1); mbar_init(&h2t[i], 1);
             mbar_init(&hdt[i], kEpiThreads); mbar_init(&hdt[kMaxTiles + i], kEpiThreads);
         }
         fence_mbar_init();
@@ -765,6 +769,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                         issue_tile<CFG::K2, CFG::PER2, false, CFG::HST, CFG::WP, CFG::PLANE16, CFG::G2,
                                                    CFG::KB2 / 16, CFG::NC2, CFG::PM, CFG::LOH16, 0, CFG::NB2, NS2,
                                                    CFG::STK2>(t - 1, tmem, alo2, bl2, id2, 1u, id2w);
+                                        if (p.nhd == 1) commit(&h2t[t - 1]);   // hidden tile t-2 reusable
                                     }
                                 }
 #pragma unroll
@@ -879,6 +884,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
         const int row_in_tile = quarter * 32 + lane;
         const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
         uint32_t a1ph = 0, a2ph = 0, heph = 0;   // heph bit i: phase of hd_empty[i]
+        uint32_t h2ph = 0;                        // phase of h2t[*]
+#if defined(CI_NO_TILE_RELEASE) || defined(CI_NO_EPI1_BATCH)
+        const bool trel = false;
+#else
+        const bool trel = CFG::STREAM && CFG::INTERLEAVE && CFG::EPI1_PIPE && p.nhd == 1;
+#endif
         uint32_t hd_used = 0;                     // bit i: hidden buffer i has been filled before
         uint8_t* xlo_buf = xbuf + (size_t)(eCp / 8) * plane_bytes;
         const int cw1 = eMC / 2, cb1 = half * cw1;     // conv1 chunk columns of this half
@@ -1122,7 +1133,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                         fence_after();
                     }
                     const int hb_i = j & (p.nhd - 1);
-                    if ((hd_used >> hb_i) & 1u) {
+                    // tile release (STREAM, one hidden buffer): chunk j > 0 waits per tile pair on h2t
+                    // below; chunk 0 follows the previous block's conv2 epilogue, which has waited for
+                    // every tile of the last conv2 chunk (a2t), so it needs no wait at all
+                    if (!trel && ((hd_used >> hb_i) & 1u)) {
                         TWAIT(w_he, mbar_wait(&hd_empty[hb_i], (heph >> hb_i) & 1u));
                         heph ^= 1u << hb_i;
                     }
@@ -1169,6 +1183,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 for (int u = 0; u < 2 && q0 + u < T; u++) mbar_arrive(&a1f[q0 + u]);
                             }
                             if (k + 1 < NP) issue(q0 + 2, (k + 1) & 1);
+                            if (trel && j > 0)   // conv2_{j-1} no longer reads hidden rows of tiles q0, q0+1
+                                TWAIT(w_he, mbar_wait(&h2t[q0 + 2 < T ? q0 + 2 : T - 1], h2ph));
 #pragma unroll
                             for (int u = 0; u < 2; u++) {
                                 if (q0 + u >= T) break;
@@ -1207,6 +1223,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             for (int u = 0; u < 2 && q0 + u < T; u++) mbar_arrive(&hdt[hb_i * kMaxTiles + q0 + u]);
                         }
                         a1ph ^= 1;
+                        if (trel && j > 0) h2ph ^= 1;
                     } else if constexpr (S && (CFG::MC == 32 || ((CFG::MC == 64 || (CFG::MC == 128 && CFG::FOLD)) && !CFG::P3 && !CFG::RES))) {
                         // Batched TMEM reads: up to four LW-column loads in flight per wait::ld
                         // (one load per wait is latency-bound at ~250 cycles), flattened over
