@@ -433,6 +433,11 @@ struct SCfg {
 #endif
 };
 using SDyn = SCfg<0, 0, 0, 0, 0, 0, 0>;
+#ifndef CI_NO_EPI1_BATCH_P3
+constexpr bool kEpi1BatchP3 = true;    // A/B: batched conv1 epilogue also for the split precisions
+#else
+constexpr bool kEpi1BatchP3 = false;
+#endif
 #ifdef CI_NO_XPREF
 constexpr bool kXPrefetch = false;   // A/B switch
 #else
@@ -1224,7 +1229,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                         }
                         a1ph ^= 1;
                         if (trel && j > 0) h2ph ^= 1;
-                    } else if constexpr (S && (CFG::MC == 32 || ((CFG::MC == 64 || (CFG::MC == 128 && CFG::FOLD)) && !CFG::P3 && !CFG::RES))) {
+                    } else if constexpr (S && (CFG::MC == 32 || ((CFG::MC == 64 || (CFG::MC == 128 && CFG::FOLD)) && !CFG::RES &&
+                                                   (!CFG::P3 || kEpi1BatchP3)))) {
                         // Batched TMEM reads: up to four LW-column loads in flight per wait::ld
                         // (one load per wait is latency-bound at ~250 cycles), flattened over
                         // (tile, column group); no registers stay live across batches.
