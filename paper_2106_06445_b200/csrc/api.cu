@@ -104,17 +104,24 @@ static ci_status_t forward_impl(const Model* m, const float* x, float* h, int64_
     return CI_OK;
 }
 
+// consume_h: h is library scratch (the encode mean inside ci_serve_group) that the inverse may
+// overwrite, so the last stage runs on it in place and the initial identity copy is skipped
 static ci_status_t inverse_impl(const Model* m, const float* h, float* x, int64_t n, void* ws,
-                                const WsLayout& L, cudaStream_t st) {
+                                const WsLayout& L, cudaStream_t st, bool consume_h = false) {
     if (n == 0) return CI_OK;
     float* scratch = at<float>(ws, L.scratch);
     const int S = m->n_stages;
-    // copies: 1 initial + 1 after each stage -> S + 1 copies, the last one lands in x
-    int ncopy = S + 1, ci = 0;
+    // copies: [1 initial] + 1 after each stage, the last one lands in x
+    int ncopy = consume_h ? S : S + 1, ci = 0;
     auto target = [&](int i) { return ((ncopy - 1 - i) % 2 == 0) ? x : scratch; };
-    float* cur = target(ci++);
-    const StageInfo& L3 = m->st[S - 1];
-    CI_CUDA(launch_permute(h, cur, n, L3.C, L3.H, L3.W, 0, st));
+    float* cur;
+    if (consume_h) {
+        cur = const_cast<float*>(h);
+    } else {
+        cur = target(ci++);
+        const StageInfo& L3 = m->st[S - 1];
+        CI_CUDA(launch_permute(h, cur, n, L3.C, L3.H, L3.W, 0, st));
+    }
     for (int s = S - 1; s >= 0; s--) {
         ci_status_t r = umma_stage(m, s, cur, n, true, next_ctr(ws, L), st);
         if (r != CI_OK) return r;
@@ -430,7 +437,7 @@ static ci_status_t serve_impl(const Model* m, ci_encode_mode_t mode, int32_t k, 
         r = encode_learned_impl(m, x, xp, k, B, ws, L, st);              // (2) learned encoder
     } else {
         CI_CUDA(launch_mean(h_out, mean, k, B, m->d, st));               // (2) encode: mean ...
-        r = inverse_impl(m, mean, xp, B, ws, L, st);                      //     ... then h^-1
+        r = inverse_impl(m, mean, xp, B, ws, L, st, true);                //     ... then h^-1 (in place)
     }
     if (r != CI_OK) return r;
     r = forward_impl(m, xp, h_parity, B, ws, L, st);                      // (3) h on parity query

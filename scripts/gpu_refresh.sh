@@ -19,6 +19,9 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_st
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,dram__throughput.avg.pct_of_peak_sustained_elapsed \
   --clock-control none -k regex:"k_mean|k_decode" --csv --log-file gpurun_out/hbm_dram.csv \
   python bench.py --steps 1 --warmup 1 --inflight 1 --no-e2e --no-alt --no-cpu-baseline --reps 0 > /dev/null 2>&1
+# learned-encoder launch list at k = 2, 4, 10 (E1, tail, E4)
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/enc_launches.csv \
+  python scripts/enc_launches.py > /dev/null 2>&1
 python - <<'PY'
 import json
 for f in ("bench", "bench_c3r", "bench_ref"):

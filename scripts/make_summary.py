@@ -162,5 +162,25 @@ for n = 10240); f16x3 issues 3 MMAs per product.  DRAM traffic per launch is the
 and out (126 MB) plus weights from L2: the kernel is bound by tensor issue (SS-mode A reads) and
 epilogue/MMA serialisation, not DRAM.
 """
+# ---- learned encoder (C4 arch): launch list of ci_encode(CI_ENC_LEARNED) at k = 2, 4, 10
+ep = os.path.join(G, "enc_launches.csv")
+if os.path.exists(ep):
+    h, rows = ncu_csv(ep)
+    ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    names = [(r[ki], float(r[vi].replace(",", "")) / 1000.0) for r in rows if len(r) > vi and "ci::" in r[ki]]
+    eo = b.get("workloads", {}).get("C4", {}) and b.get("encoder_overhead") or b.get("encoder_overhead")
+    txt += """
+## Learned encoder (a3', Arch E, 1024 groups; ncu launch list of `scripts/enc_launches.py`, second call per k)
+| k | E1 + mean + psi (us) | tail E2/E3 on tcgen05 (us) | psi^-1 + skip + E4 (us) | live encoder / h (bench `encoder_overhead`) |
+|---|---|---|---|---|
+"""
+    per = len(names) // 6 if names else 0   # 3 k values x 2 calls, 3 kernels each
+    for i, kk in enumerate((2, 4, 10)):
+        blk = names[(2 * i + 1) * 3:(2 * i + 2) * 3]
+        if len(blk) == 3:
+            ov = (eo or {}).get(str(kk), {})
+            txt += (f"| {kk} | {blk[0][1]:.1f} | {blk[1][1]:.1f} | {blk[2][1]:.1f} | "
+                    f"{ov.get('encoder_ms', float('nan')):.3f} / {ov.get('h_ms', float('nan')):.3f} ms = "
+                    f"{ov.get('overhead', float('nan')) * 100:.1f}% |\n")
 open(os.path.join(P, f"{tag}_summary.md"), "w").write(txt)
 print(txt[:3000])
