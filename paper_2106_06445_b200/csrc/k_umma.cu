@@ -79,6 +79,9 @@ struct StagePlan {
     uint32_t sstate_off;   // byte offset of the fp32 state region in dynamic smem
     int stk1, stk2;        // stacked f16x3 for conv1 / conv2 (mma_prec): B tiles of 2N rows, 2N
                            // accumulator columns per tile (specialised kernels only)
+    int nopad;             // raster without pad column (Wp = W): conv1's horizontal taps stacked in
+                           // N as well (3 MC columns, masked col2im in the epilogue), conv2 hst
+    int n1;                // conv1 segment width: MC, or 3 MC with nopad
 };
 
 struct StageArgs {
@@ -201,7 +204,18 @@ __host__ __device__ constexpr AOff a_off(int s, int am, bool hstk, int per, int 
 template <int PM, int N, int LOA16, int STK>
 __device__ __forceinline__ void mma_prec(uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t idescw,
                                          uint32_t acc) {
-    if constexpr (STK != 0) {
+    if constexpr (N > 256) {   // two MMAs of N/2 columns (idesc is the N/2 one): B rows / D columns split
+        static_assert(STK == 0 && N % 32 == 0, "split segments are unstacked");
+        constexpr int HN = N / 2;
+#pragma unroll
+        for (int hh = 0; hh < 2; hh++) {
+            const uint32_t dh = d + (uint32_t)(hh * HN);
+            const uint64_t bh = bd + (uint64_t)(hh * HN);   // HN rows of 16 B (descriptor units)
+            mma_bf16(dh, ad, bh, idesc, acc);
+            if (PM >= 1) mma_bf16(dh, ad + (uint64_t)LOA16, bh, idesc, 1u);
+            if (PM == 2) mma_bf16(dh, ad, bh + (uint64_t)(N * 2), idesc, 1u);
+        }
+    } else if constexpr (STK != 0) {
         mma_bf16(d, ad, bd, idescw, acc);
         mma_bf16(d, ad + (uint64_t)LOA16, bd, idesc, 1u);
     } else {
@@ -376,11 +390,16 @@ __device__ __forceinline__ void issue_tile(int t, uint32_t tmem, uint32_t alo0, 
 
 // Static stage configuration (0 = use the runtime plan)
 template <int WP_, int CP_, int MC_, int NC2_, int T_, int PM_, int SLOT_, int H_ = 0, int C_ = 0, int SST_ = 0,
-          int HST_ = 0, int RES_ = 0, int STK1_ = 0, int STK2_ = 0>
+          int HST_ = 0, int RES_ = 0, int STK1_ = 0, int STK2_ = 0, int NOPAD_ = 0>
 struct SCfg {
+    // no-pad raster (StagePlan::nopad): Wp = W, both convolutions take their horizontal taps as
+    // N-stacked column groups and the epilogues do a masked col2im
+    static constexpr bool NOPAD = NOPAD_ != 0;
+    static_assert(!NOPAD_ || (HST_ && !RES_), "no-pad raster: horizontal taps stacked in both convolutions");
     // stacked f16x3 (mma_prec): conv1 / conv2 B tiles of 2N rows, accumulators 2N columns per tile
     static constexpr int STK1 = STK1_, STK2 = STK2_;
-    static constexpr int NB1 = MC_ * (STK1_ ? 2 : 1), NB2 = NC2_ * (STK2_ ? 2 : 1);
+    static constexpr int NB1 = MC_ * (NOPAD_ ? 3 : 1) * (STK1_ ? 2 : 1), NB2 = NC2_ * (STK2_ ? 2 : 1);
+    static_assert(!(NOPAD_ && STK1_), "no-pad conv1 is 3 MC wide already");
     static_assert(!(STK1_ || STK2_) || PM_ == 2, "stacking is an f16x3 layout");
     static_assert(!STK2_ || (!HST_ && !RES_), "stacked conv2: plain-width coupling epilogue only");
     static constexpr bool HST = HST_ != 0;
@@ -388,7 +407,7 @@ struct SCfg {
     static constexpr int HC = HST_ ? (C_ + 7) / 8 * 8 : 0;   // == StagePlan::hc
     static constexpr bool kStatic = WP_ > 0;
     static constexpr int WP = WP_, CP = CP_, MC = MC_, NC2 = NC2_, T = T_, SLOT = SLOT_;
-    static constexpr int H = H_, W = WP_ - 1, C = C_, SST = SST_;
+    static constexpr int H = H_, W = NOPAD_ ? WP_ : WP_ - 1, C = C_, SST = SST_;
     static constexpr int PM = PM_;            // StagePlan::pm
     static constexpr bool P3 = PM_ != 0;      // activations split into fp16 hi + lo planes
     static constexpr int G = WP + 2;
@@ -401,10 +420,11 @@ struct SCfg {
     static constexpr bool TRI = CP_ == 32 && C_ == 24;   // == StagePlan::tri
     static constexpr int AM1 = PAIR ? 1 : (TRI ? 2 : 0);  // conv1 A-operand mode (a_off)
     static constexpr int PER1 = PAIR ? 2 : CP / 16;
-    static constexpr int K1 = PAIR ? kPairK1 : (TRI ? kTriK1 : 9 * (CP / 16));
+    static constexpr int K1 = NOPAD ? 3 * (CP / 16) : (PAIR ? kPairK1 : (TRI ? kTriK1 : 9 * (CP / 16)));
+    static constexpr int N1 = NOPAD ? 3 * MC : MC;   // conv1 columns per tile: 3 tap groups when no-pad
     static constexpr int PER2 = MC / 16;
     static constexpr int K2 = (HST ? 3 : 9) * (MC / 16);
-    static constexpr int KB1 = MC * 32 * (PM == 2 ? 2 : 1), KB2 = NC2 * 32 * (PM == 2 ? 2 : 1);
+    static constexpr int KB1 = N1 * 32 * (PM == 2 ? 2 : 1), KB2 = NC2 * 32 * (PM == 2 ? 2 : 1);
     static constexpr int G1 = (SLOT / (KB1 > 0 ? KB1 : 1)) < 1 ? 1 : SLOT / (KB1 > 0 ? KB1 : 1);
     static constexpr int G2 = (SLOT / (KB2 > 0 ? KB2 : 1)) < 1 ? 1 : SLOT / (KB2 > 0 ? KB2 : 1);
     static constexpr int ACC1 = T * NB2;   // acc2[tile] at tile * NB2, acc1[tile] at ACC1 + tile * NB1
@@ -574,7 +594,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                         {
                             int seg, jj;
                             seg_of(q, p.nch, seg, jj);
-                            int N = seg == 0 ? p.MC : p.Nc2;
+                            int N = seg == 0 ? p.n1 : p.Nc2;
                             int K = seg == 0 ? p.k1 : p.k2;
                             int g = steps_per_slot(N, p.pm, p.slot_bytes);
                             int kb = kstep_bytes(N, p.pm);
@@ -611,15 +631,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
             const uint32_t xlo_b = (uint32_t)(p.Cp / 8) * plane_bytes;   // lo planes (f16x2 / f16x3)
             const uint32_t hlo_b = (uint32_t)(p.MC / 8) * plane_bytes;
             (void)hlo_b;
-            const uint32_t id1 = idesc_of(128, p.MC, kP3), id2 = idesc_of(128, p.Nc2, kP3);
+            // segments wider than 256 columns are issued as two halves (mma_prec)
+            const uint32_t id1 = idesc_of(128, p.n1 > 256 ? p.n1 / 2 : p.n1, kP3);
+            const uint32_t id2 = idesc_of(128, p.Nc2 > 256 ? p.Nc2 / 2 : p.Nc2, kP3);
             // stacked f16x3: the hi(A) MMA is 2N wide (static configurations only)
             const uint32_t id1w = idesc_of(128, CFG::kStatic ? CFG::NB1 : p.MC, kP3);
             const uint32_t id2w = idesc_of(128, CFG::kStatic ? CFG::NB2 : p.Nc2, kP3);
             const uint32_t rb = smem_u32(ring);
             const uint32_t lbo1 = p.pair ? 16u : plane_bytes;
-            const int g1 = steps_per_slot(p.MC, p.pm, p.slot_bytes);
+            const int g1 = steps_per_slot(p.n1, p.pm, p.slot_bytes);
             const int g2 = steps_per_slot(p.Nc2, p.pm, p.slot_bytes);
-            const uint32_t kb1 = (uint32_t)kstep_bytes(p.MC, p.pm), kb2 = (uint32_t)kstep_bytes(p.Nc2, p.pm);
+            const uint32_t kb1 = (uint32_t)kstep_bytes(p.n1, p.pm), kb2 = (uint32_t)kstep_bytes(p.Nc2, p.pm);
             const int per1 = p.pair ? 2 : p.Cp / 16;   // k-steps per kernel row u (pair) / per tap
             const int per2 = p.MC / 16;
             unsigned long long w_x = 0, w_full = 0, w_hd = 0, t_start = CLK();
@@ -634,7 +656,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             const uint32_t alo0 = ((xb >> 4) & 0x3FFFu) | ((LBO1 >> 4) << 16);
                             const uint32_t ringlo = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::NB1 * 16 >> 4) << 16);
                             issue_static<CFG::K1, CFG::PER1, CFG::AM1, CFG::WP, CFG::PLANE16, CFG::G1, CFG::KB1 / 16,
-                                         CFG::T, CFG::MC, CFG::PM, CFG::LOX16, CFG::ACC1, CFG::NB1, false, CFG::STK1>(
+                                         CFG::T, CFG::N1, CFG::PM, CFG::LOX16, CFG::ACC1, CFG::NB1, CFG::NOPAD, CFG::STK1>(
                                 tmem, alo0, ringlo, (uint32_t)CFG::SLOT / 16u, id1, CFG::FOLD ? 0u : 1u, slot, phase,
                                 p.nslot, full, empty, id1w);
                         } else
@@ -736,7 +758,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                         const uint32_t ring2 = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::NB2 * 16 >> 4) << 16);
                         long long tx0 = CLK();
                         issue_stream<CFG::K1, CFG::PER1, CFG::AM1, false, CFG::WP, CFG::PLANE16, CFG::G1, CFG::KB1 / 16,
-                                     CFG::T, CFG::MC, CFG::PM, CFG::LOX16, CFG::ACC1, CFG::NB1, 1, CFG::STK1>(
+                                     CFG::T, CFG::N1, CFG::PM, CFG::LOX16, CFG::ACC1, CFG::NB1, 1, CFG::STK1>(
                             tmem, alo1, ring1, (uint32_t)CFG::SLOT / 16u, id1, 0u, slot, phase, p.nslot, full, empty,
                             x_tile, xph, a1t, id1w);
                         if (kCycles && a.dbg) w_x += (unsigned long long)(CLK() - tx0);
@@ -764,7 +786,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                         TWAIT(w_hd, mbar_wait(&a1f[t], a1fph));
                                         fence_after();
                                         issue_tile<CFG::K1, CFG::PER1, CFG::AM1, false, CFG::WP, CFG::PLANE16, CFG::G1,
-                                                   CFG::KB1 / 16, CFG::MC, CFG::PM, CFG::LOX16, CFG::ACC1, CFG::NB1, NS1,
+                                                   CFG::KB1 / 16, CFG::N1, CFG::PM, CFG::LOX16, CFG::ACC1, CFG::NB1, NS1,
                                                    CFG::STK1>(t, tmem, alo1, bl1, id1, 0u, id1w);
                                         commit(&a1t[t]);
                                     }
@@ -789,7 +811,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             }
                             if (j + 1 < p.nch) {
                                 issue_stream<CFG::K1, CFG::PER1, CFG::AM1, false, CFG::WP, CFG::PLANE16, CFG::G1,
-                                             CFG::KB1 / 16, CFG::T, CFG::MC, CFG::PM, CFG::LOX16, CFG::ACC1, CFG::NB1, 0,
+                                             CFG::KB1 / 16, CFG::T, CFG::N1, CFG::PM, CFG::LOX16, CFG::ACC1, CFG::NB1, 0,
                                              CFG::STK1>(
                                     tmem, alo1, ring1, (uint32_t)CFG::SLOT / 16u, id1, 0u, slot, phase, p.nslot, full,
                                     empty, a1f, a1fph, a1t, id1w);
@@ -811,7 +833,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                     // first conv1 chunk: tile by tile behind the previous epilogue when its weight
                     // slots fit the ring, else after all X rows are final
                     bool tiles_first = false;
-                    if constexpr (CFG::kStatic && (CFG::K1 + CFG::G1 - 1) / CFG::G1 <= 3) {
+                    if constexpr (CFG::kStatic && !CFG::NOPAD && (CFG::K1 + CFG::G1 - 1) / CFG::G1 <= 3) {
                         constexpr int NS1 = (CFG::K1 + CFG::G1 - 1) / CFG::G1;
                         if (NS1 <= p.nslot) {
                             tiles_first = true;
@@ -820,7 +842,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             const uint32_t ringlo = ((rb >> 4) & 0x3FFFu) | ((uint32_t)(CFG::NB1 * 16 >> 4) << 16);
                             long long tx0 = CLK();
                             issue_static_tiles<CFG::K1, CFG::PER1, CFG::AM1, CFG::WP, CFG::PLANE16, CFG::G1,
-                                               CFG::KB1 / 16, CFG::T, CFG::MC, CFG::PM, CFG::LOX16, CFG::ACC1, CFG::NB1,
+                                               CFG::KB1 / 16, CFG::T, CFG::N1, CFG::PM, CFG::LOX16, CFG::ACC1, CFG::NB1,
                                                CFG::STK1>(
                                 tmem, alo0, ringlo, (uint32_t)CFG::SLOT / 16u, id1, CFG::FOLD ? 0u : 1u, slot, phase,
                                 p.nslot, full, empty, x_tile, xph, id1w);
@@ -973,7 +995,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
             const uint32_t base = tmem + lane_addr + (uint32_t)(tile * eA2S);
             if (ehst && ehc != 8) {   // columns [hc, 2hc) carry b2, the side taps start at 0
 #pragma unroll
-                for (int g = 0; g < 9; g++) {
+                for (int g = 0; g < 36; g++) {   // 3 tap groups of up to 96 channels
                     if (g * 8 >= 3 * ehc) break;
                     float v8[8];
 #pragma unroll
@@ -1050,9 +1072,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                 }
             }
         };
+        // no-pad conv1 (3 tap groups of MC columns): the bias rides in the centre group, the side
+        // groups start at zero; this half's cw1 channels of each group
+        auto init_acc1_nopad = [&](const float* b1src, uint32_t col) {
+            if constexpr (S && CFG::NOPAD) {
+#pragma unroll
+                for (int v = 0; v < 3; v++)
+#pragma unroll
+                    for (int g = 0; g < CFG::MC / 2; g += 16) {
+                        float v16[16];
+#pragma unroll
+                        for (int e = 0; e < 16; e++) v16[e] = v == 1 ? __ldg(b1src + g + e) : 0.f;
+                        tmem_st16(tmem + lane_addr + col + (uint32_t)(v * CFG::MC + g), v16);
+                    }
+            }
+        };
         for (int tile = 0; tile < eT; tile++) {
             if (!ehst || (tile & 1) == half) init_acc2(bias2_of(0), tile);
-            if (!efold)
+            if constexpr (S && CFG::NOPAD)
+                init_acc1_nopad(bias1_of(0) + cb1, acc1_col0 + (uint32_t)(tile * eA1S + cb1));
+            else if (!efold)
                 for (int g0 = 0; g0 < cw1; g0 += 32)
                     init_acc1_cols(bias1_of(0) + cb1 + g0, acc1_col0 + (uint32_t)(tile * eA1S + cb1 + g0),
                                    cw1 - g0 < 32 ? cw1 - g0 : 32);
@@ -1151,6 +1190,45 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                     long long te0 = CLK();
                     // bias of the next conv1 chunk in issue order, this half's columns
                     const float* b1n = (j + 1 < p.nch ? b1 + (j + 1) * eMC : bias1_of(tt + 1 < nbv ? tt + 1 : 0)) + cb1;
+                    if constexpr (S && CFG::NOPAD) {
+                        // no-pad raster: acc1 row r holds Z_v[r][h] at column (v+1) MC + h; hidden[p] =
+                        // act(Z_-1[p-1] + Z_0[p] + Z_+1[p+1]) with the x = 0 / x = W-1 neighbours masked
+                        // (zero padding).  Image rows are W-aligned inside a warp (W | 32), so the row
+                        // neighbours are lanes +-1 of the same warp: shuffles only.
+                        constexpr int CW = CFG::MC / 2;   // this half's channels of the chunk
+#pragma unroll
+                        for (int tile = 0; tile < CFG::T; tile++) {
+                            const int r = tile * 128 + row_in_tile;
+                            int ii, y, x;
+                            const bool valid = rowpix(r, ii, y, x) && ii < nimg;
+                            const bool hl = x > 0, hr = x < CFG::W - 1;
+                            const uint32_t col = acc1_col0 + (uint32_t)(tile * CFG::NB1 + cb1);
+#pragma unroll
+                            for (int g = 0; g < CW / 8; g += 2) {
+                                float zl[2][8], zc[2][8], zr[2][8];
+#pragma unroll
+                                for (int u = 0; u < 2; u++) {
+                                    tmem_ld8(tmem + lane_addr + col + (uint32_t)((g + u) * 8), zl[u]);
+                                    tmem_ld8(tmem + lane_addr + col + (uint32_t)(CFG::MC + (g + u) * 8), zc[u]);
+                                    tmem_ld8(tmem + lane_addr + col + (uint32_t)(2 * CFG::MC + (g + u) * 8), zr[u]);
+                                }
+                                tmem_wait_ld();
+#pragma unroll
+                                for (int u = 0; u < 2; u++) {
+                                    float h8[8];
+#pragma unroll
+                                    for (int o = 0; o < 8; o++) {
+                                        const float left = __shfl_up_sync(0xffffffffu, zl[u][o], 1);
+                                        const float right = __shfl_down_sync(0xffffffffu, zr[u][o], 1);
+                                        const float hv = zc[u][o] + (hl ? left : 0.f) + (hr ? right : 0.f);   // bias: in TMEM
+                                        h8[o] = valid ? fmaxf(hv, 0.f) : 0.f;
+                                    }
+                                    store8(hbuf_j, hlo_buf, (cb1 + (g + u) * 8) / 8, r, h8);
+                                }
+                            }
+                            init_acc1_nopad(b1n, col);   // the next conv1 chunk's bias (after all reads)
+                        }
+                    } else {
 #ifndef CI_NO_EPI1_BATCH
                     if constexpr (CFG::STREAM && CFG::EPI1_PIPE) {
                         // tile pairs, software pipelined: the TMEM loads of pair k+1 are in flight
@@ -1378,6 +1456,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             if (!efold) init_acc1_cols(b1n + g0, col + (uint32_t)g0, n);
                         }
                     }
+                    }   // not no-pad
                     if constexpr (!CFG::STREAM) {
                         tmem_wait_st();
                         fence_before();
@@ -1401,7 +1480,77 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                         mbar_arrive(&x_tile[tile]);
                     }
                 };
-                if (ehst && ehc != 8) {
+                if constexpr (S && CFG::NOPAD) {
+                    // no-pad raster, conv2 with horizontal tap stacking over hc = c outputs: acc2 row r
+                    // holds Z_v[r][o] at column (v+1) hc + o; out[p] = Z_-1[p-1] + Z_0[p] + Z_+1[p+1]
+                    // with the x = 0 / x = W-1 neighbours masked; each warp half owns c/2 channels
+                    constexpr int HCW = CFG::HC, OH = HCW / 2;
+                    // this thread's old state values of tile t (its row, this half's channels), loaded
+                    // before the accumulator is waited for (global-memory latency off the critical path)
+                    float oldv[OH];
+                    auto load_old_np = [&](int tile) {
+                        const int r = tile * 128 + row_in_tile;
+                        int ii, y, x;
+                        const bool valid = rowpix(r, ii, y, x) && ii < nimg && !a.fmode;
+                        const float* src = stb + ((int64_t)(valid ? ii : 0) * a.C + out_off + half * OH) * eHW +
+                                           (valid ? y * eW + x : 0);
+#pragma unroll
+                        for (int o = 0; o < OH; o++) oldv[o] = valid ? src[(int64_t)o * eHW] : 0.f;
+                    };
+                    load_old_np(0);
+                    TWAIT(w_a2, mbar_wait(acc2_full, a2ph)); a2ph ^= 1;
+                    fence_after();
+                    long long te2n = CLK();
+#pragma unroll
+                    for (int tile = 0; tile < CFG::T; tile++) {
+                        if (tile > 0) load_old_np(tile);
+                        const int r = tile * 128 + row_in_tile;
+                        int ii, y, x;
+                        const bool valid = rowpix(r, ii, y, x) && ii < nimg;
+                        const bool hl = x > 0, hr = x < CFG::W - 1;
+                        const uint32_t col = (uint32_t)(tile * CFG::NB2 + half * OH);
+                        float* dst = stb + ((int64_t)(valid ? ii : 0) * a.C + out_off) * eHW + (valid ? y * eW + x : 0);
+#pragma unroll
+                        for (int g = 0; g < OH / 8; g += 2) {
+                            float zl[2][8], zc[2][8], zr[2][8];
+#pragma unroll
+                            for (int u = 0; u < 2; u++) {
+                                tmem_ld8(tmem + lane_addr + col + (uint32_t)((g + u) * 8), zl[u]);
+                                tmem_ld8(tmem + lane_addr + col + (uint32_t)(HCW + (g + u) * 8), zc[u]);
+                                tmem_ld8(tmem + lane_addr + col + (uint32_t)(2 * HCW + (g + u) * 8), zr[u]);
+                            }
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int u = 0; u < 2; u++) {
+                                const int oc0 = half * OH + (g + u) * 8;
+                                float n8[8], bz[8], bc[8];
+#pragma unroll
+                                for (int o = 0; o < 8; o++) {
+                                    const float left = __shfl_up_sync(0xffffffffu, zl[u][o], 1);
+                                    const float right = __shfl_down_sync(0xffffffffu, zr[u][o], 1);
+                                    const float f = zc[u][o] + (hl ? left : 0.f) + (hr ? right : 0.f);   // bias: in TMEM
+                                    float nv = 0.f;
+                                    if (valid) {
+                                        const float old = oldv[(g + u) * 8 + o];
+                                        nv = a.fmode ? fmaxf(f, 0.f) : (a.inverse ? old - f : old + f);
+                                        if (store_state) dst[(int64_t)(oc0 + o) * eHW] = nv;
+                                    }
+                                    n8[o] = nv;
+                                    bz[o] = 0.f;
+                                    bc[o] = __ldg(b2n + oc0 + o);
+                                }
+                                if (valid && write_x) store8(xbuf, xlo_buf, oc0 / 8, r, n8);
+                                // the next block's conv2 bias rides in the centre group
+                                tmem_st8(tmem + lane_addr + col + (uint32_t)((g + u) * 8), bz);
+                                tmem_st8(tmem + lane_addr + col + (uint32_t)(HCW + (g + u) * 8), bc);
+                                tmem_st8(tmem + lane_addr + col + (uint32_t)(2 * HCW + (g + u) * 8), bz);
+                            }
+                        }
+                        x_ready(tile);
+                    }
+                    tmem_wait_st();
+                    t_e2 += CLK() - te2n;
+                } else if (ehst && ehc != 8) {
                     // ---- wide horizontal tap stacking (hc = 16 / 24 outputs per tap group): acc2
                     // row r holds Z_v[r][o] at column (v+1)*hc + o; out[p][o] = Z_-1[p-1][o] +
                     // Z_0[p][o] + Z_+1[p+1][o].  Same scheme as the 8-channel path: shuffles inside
@@ -1990,7 +2139,7 @@ static double mma_cyc(int N) { return std::max(N / 2.0, 32.0 + N / 4.0); }
 //   a 2-slot ring cannot hide the L2 latency of the weight stream (x1.3)
 // Tuned plans for the Arch-C stage shapes (chosen from CI_DEBUG_CYCLES measurements);
 // other shapes use the cost model.
-struct TunedPlan { int H, W, c, m, pm, MC, T, nhd, nslot, hst, stk1, stk2; };
+struct TunedPlan { int H, W, c, m, pm, MC, T, nhd, nslot, hst, stk1, stk2, nopad; };
 static const TunedPlan kTuned[] = {
     {16, 16, 6, 64, 0, 32, 7, 2, 3, 1},    // stage 1 bf16: SMEM-resident state fits
     {8, 8, 24, 128, 0, 128, 2, 1, 3, 1},   // stage 2 bf16: wide hst (N = 3 x 24 -> 80), one N = 128 conv1 chunk, T = 2
@@ -2007,6 +2156,7 @@ static const TunedPlan kTuned[] = {
     {8, 8, 24, 128, 2, 128, 2, 1, 3, 1},   // stage 2 f16x3
     {16, 16, 6, 64, 2, 32, 5, 1, 4, 1, 1, 0},    // stage 1 f16x3, stacked conv1 (CI_NO_STK: unstacked)
     {16, 16, 6, 64, 2, 32, 5, 1, 4, 1},    // stage 1 f16x3
+    {4, 4, 96, 256, 2, 64, 1, 2, 4, 1, 0, 0, 1},  // stage 3 f16x3, no-pad raster (CI_NO_NOPAD: padded)
     {4, 4, 96, 256, 2, 128, 1, 1, 4, 0, 1, 1},   // stage 3 f16x3, stacked conv1 + conv2
     {16, 16, 64, 64, 2, 32, 3, 1, 4, 0, 1, 0},   // learned-encoder tail f16x3, stacked conv1
     {4, 4, 96, 256, 2, 128, 1, 1, 4, 0},   // stage 3 f16x3
@@ -2022,14 +2172,15 @@ static bool make_plan(const StageInfo& S, int pm, StagePlan& best, bool allow_st
     static const bool s1_mc64 = getenv("CI_S1_MC64") != nullptr;           // A/B switch
     static const bool no_tuned = getenv("CI_NO_TUNED") != nullptr;         // A/B switch: cost model only
     static const bool no_stk = getenv("CI_NO_STK") != nullptr;             // A/B switch: unstacked f16x3
+    static const bool no_nopad = getenv("CI_NO_NOPAD") != nullptr;         // A/B switch: padded raster
     // CI_TUNE="H,W,c,m,pm,MC,T,nhd,nslot,hst;..." overrides the table (same-box plan A/B)
     static const std::vector<TunedPlan> env_tuned = [] {
         std::vector<TunedPlan> v;
         const char* e = getenv("CI_TUNE");
         while (e && *e) {
             TunedPlan t{};
-            if (sscanf(e, "%d,%d,%d,%d,%d,%d,%d,%d,%d,%d,%d,%d", &t.H, &t.W, &t.c, &t.m, &t.pm, &t.MC, &t.T, &t.nhd,
-                       &t.nslot, &t.hst, &t.stk1, &t.stk2) >= 10)
+            if (sscanf(e, "%d,%d,%d,%d,%d,%d,%d,%d,%d,%d,%d,%d,%d", &t.H, &t.W, &t.c, &t.m, &t.pm, &t.MC, &t.T, &t.nhd,
+                       &t.nslot, &t.hst, &t.stk1, &t.stk2, &t.nopad) >= 10)
                 v.push_back(t);
             e = strchr(e, ';');
             if (e) e++;
@@ -2042,10 +2193,11 @@ static bool make_plan(const StageInfo& S, int pm, StagePlan& best, bool allow_st
     if (!no_tuned)
     for (const auto& tp : kTuned)   // first match wins
         if (!tuned && tp.H == S.H && tp.W == S.W && tp.c == S.c && tp.m == S.m && tp.pm == pm &&
-            !((no_stk || !allow_stk) && (tp.stk1 || tp.stk2)) && !(no_wide_hst && tp.hst && tp.c > 8) && !(tp.c == 24 && !tp.pm && tp.MC == 64 && tp.hst && s1_mc32) &&
+            !((no_stk || !allow_stk) && (tp.stk1 || tp.stk2)) && !((no_nopad || !allow_stk) && tp.nopad) && !(no_wide_hst && tp.hst && tp.c > 8) && !(tp.c == 24 && !tp.pm && tp.MC == 64 && tp.hst && s1_mc32) &&
             !(tp.c == 24 && !tp.pm && tp.MC == 128 && tp.hst && (s1_mc64 || s1_mc32)))
             tuned = &tp;
-    p.H = S.H; p.W = S.W; p.Wp = S.W + 1; p.G = p.Wp + 2;
+    p.nopad = (tuned && allow_stk) ? tuned->nopad : 0;
+    p.H = S.H; p.W = S.W; p.Wp = p.nopad ? S.W : S.W + 1; p.G = p.Wp + 2;
     p.c = S.c; p.m = S.m;
     p.Cp = S.c <= 8 ? 8 : rup(S.c, 16);
     p.Mp = rup(S.m, 16);
@@ -2056,13 +2208,15 @@ static bool make_plan(const StageInfo& S, int pm, StagePlan& best, bool allow_st
     const int P = pm ? 2 : 1;
     const double P3f = 1.0 + pm;   // MMAs per k-step: f16x2 hi(A)*B + lo(A)*B, f16x3 + hi(A)*lo(B)
     const int img_rows = (p.H + 1) * p.Wp;
-    const int k1 = p.pair ? kPairK1 : (p.tri ? kTriK1 : 9 * (p.Cp / 16));
+    if (p.nopad) p.pair = p.tri = 0;
+    const int k1 = p.nopad ? 3 * (p.Cp / 16) : (p.pair ? kPairK1 : (p.tri ? kTriK1 : 9 * (p.Cp / 16)));
     p.stk1 = (tuned && pm == 2 && allow_stk) ? tuned->stk1 : 0;
     p.stk2 = (tuned && pm == 2 && allow_stk) ? tuned->stk2 : 0;
     double best_cost = 1e300;
     // conv2 with horizontal tap stacking (mandatory for c <= 8, optional up to c = 24) or plain
     for (int hopt = 1; hopt >= 0; hopt--) {
-    if (hopt == 1 && (S.c > 24 || (S.c > 8 && no_wide_hst))) continue;
+    if (hopt == 1 && !p.nopad && (S.c > 24 || (S.c > 8 && no_wide_hst))) continue;
+    if (hopt == 0 && p.nopad) continue;
     if (hopt == 0 && S.c <= 8) continue;
     if (tuned && hopt != tuned->hst) continue;
     p.hst = hopt;
@@ -2070,14 +2224,15 @@ static bool make_plan(const StageInfo& S, int pm, StagePlan& best, bool allow_st
     p.Nc2 = hopt ? rup(3 * p.hc, 16) : rup(S.c, 16);
     p.split = (!p.hst && S.c % 8 == 0 && S.c / 2 < p.Nc2 / 2 &&
                (p.Nc2 / 2 == 8 || p.Nc2 / 2 == 16 || p.Nc2 / 2 == 32 || p.Nc2 / 2 == 48)) ? 1 : 0;
-    if (p.Nc2 > 256) continue;
+    if (p.Nc2 > (p.nopad ? 512 : 256)) continue;   // no-pad conv2 segments > 256 columns are split
     for (int MC = p.Mp; MC >= 16; MC -= 16) {
         if (p.Mp % MC || MC > 256) continue;
         if (tuned && MC != tuned->MC) continue;
         const int nch = p.Mp / MC;
+        const int n1 = p.nopad ? 3 * MC : MC;
         const int k2 = (p.hst ? 3 : 9) * (MC / 16);
         for (int T = 1; T <= 8; T++) {
-            if (T * (MC * (1 + p.stk1) + p.Nc2 * (1 + p.stk2)) > 512) break;
+            if (T * (n1 * (1 + p.stk1) + p.Nc2 * (1 + p.stk2)) > 512) break;
             if (tuned && T != tuned->T) continue;
             const int I = (T * 128) / img_rows;
             if (I < 1) continue;
@@ -2085,9 +2240,9 @@ static bool make_plan(const StageInfo& S, int pm, StagePlan& best, bool allow_st
                 if (tuned && nhd != tuned->nhd) continue;
                 for (int nslot = 4; nslot >= 2; nslot--) {
                     if (tuned && nslot != tuned->nslot) continue;
-                    const int slot_bytes = std::max(16384, std::max(kstep_bytes(MC, pm), kstep_bytes(p.Nc2, pm)));
+                    const int slot_bytes = std::max(16384, std::max(kstep_bytes(n1, pm), kstep_bytes(p.Nc2, pm)));
                     const int Rtot = T * 128 + 2 * p.G;
-                    const int xchg = p.hst ? T * 4 * 2 * p.hc * 4 : 0;
+                    const int xchg = (p.hst && !p.nopad) ? T * 4 * 2 * p.hc * 4 : 0;   // no-pad: rows 4-aligned, no exchange
                     const size_t smem0 = (size_t)nslot * slot_bytes + (size_t)P * ((p.Cp + nhd * MC) / 8) * Rtot * 16 +
                                          kBarBytes + (size_t)rup(xchg, 16);
                     if (smem0 > kSmemCap) continue;
@@ -2100,14 +2255,14 @@ static bool make_plan(const StageInfo& S, int pm, StagePlan& best, bool allow_st
                     const double e1c = T * (100.0 + 15.0 * (MC / 2)) * (pm ? 1.3 : 1.0);   // per chunk
                     const double e2 = T * (sst ? 200.0 + 40.0 * (p.Nc2 / 2) : 300.0 + 60.0 * (p.Nc2 / 2));
                     double t = nhd == 2 ? std::max(mma1 + mma2, nch * e1c) + e1c + e2 : mma1 + mma2 + nch * e1c + e2;
-                    const double wbytes = (double)nch * (k1 * kstep_bytes(MC, pm) + k2 * kstep_bytes(p.Nc2, pm));
+                    const double wbytes = (double)nch * (k1 * kstep_bytes(n1, pm) + k2 * kstep_bytes(p.Nc2, pm));
                     t = std::max(t, wbytes / 40.0);
                     if (nslot < 3) t *= 1.3;
                     const double cost = t / I;
                     if (cost < best_cost) {
                         best_cost = cost;
                         best = p;
-                        best.MC = MC; best.nch = nch; best.T = T; best.I = I; best.Rtot = Rtot;
+                        best.MC = MC; best.n1 = n1; best.nch = nch; best.T = T; best.I = I; best.Rtot = Rtot;
                         best.nslot = nslot; best.slot_bytes = slot_bytes; best.nhd = nhd;
                         best.sstate = sst; best.sstate_off = (uint32_t)soff;
                         best.smem = sst ? soff + state_bytes : smem0;
@@ -2122,7 +2277,7 @@ static bool make_plan(const StageInfo& S, int pm, StagePlan& best, bool allow_st
     }
     }   // hopt
     if (best_cost >= 1e300) return false;
-    int cols = best.T * (best.MC * (1 + best.stk1) + best.Nc2 * (1 + best.stk2));
+    int cols = best.T * (best.n1 * (1 + best.stk1) + best.Nc2 * (1 + best.stk2));
     best.tmem_cols = 32;
     while (best.tmem_cols < cols) best.tmem_cols *= 2;
     return true;
@@ -2180,14 +2335,18 @@ static void pack_block(const StagePlan& p, const float* W1, const float* b1, con
         int is2, j;
         seg_of(qseg, p.nch, is2, j);
         if (!is2)
-        // conv1 chunk j: N = MC hidden channels
+        // conv1 chunk j: N = MC hidden channels (no-pad: 3 tap groups of MC, column (v+1) MC + h,
+        // k-step = vertical tap u x 16 input channels)
         for (int s = 0; s < p.k1; s++) {
-            tile.assign((size_t)p.MC * 16, 0.f);
-            for (int n = 0; n < p.MC; n++) {
-                int h = j * p.MC + n;
+            tile.assign((size_t)p.n1 * 16, 0.f);
+            for (int n = 0; n < p.n1; n++) {
+                int h = j * p.MC + n % p.MC;
                 for (int kk = 0; kk < 16; kk++) {
                     float v;
-                    if (p.pair) {   // k-step order of pair_shift / pair_lbo_add
+                    if (p.nopad) {
+                        const int per = p.Cp / 16;
+                        v = w1(h, (s % per) * 16 + kk, s / per - 1, n / p.MC - 1);
+                    } else if (p.pair) {   // k-step order of pair_shift / pair_lbo_add
                         const int ci = kk % 8, half = kk / 8;
                         int u, vv;
                         if (s < 3) { u = s - 1; vv = half - 1; }
@@ -2207,7 +2366,7 @@ static void pack_block(const StagePlan& p, const float* W1, const float* b1, con
                     tile[(size_t)n * 16 + kk] = v;
                 }
             }
-            put_tile(out, tile, p.MC, pm, p.stk1);
+            put_tile(out, tile, p.n1, pm, p.stk1);
         }
         // conv2 chunk j: N = Nc2 outputs, K = this chunk's hidden channels
         if (is2)
@@ -2239,14 +2398,16 @@ struct UmmaState {
 
 // ---- compile-time specialisations for the Arch-C stage plans (see make_plan) -----------------
 typedef void (*StageKernel)(StageArgs);
-struct SpecEntry { int Wp, Cp, MC, Nc2, T, p3, slot, H, c, sst, hst, fold, split, res, stk1, stk2; StageKernel fn; };
-#define CI_SPEC_CFG(WP, CP, MC, NC2, T, PM, SLOT, H, C, SST, HST, RES, S1, S2) \
-    SCfg<WP, CP, MC, NC2, T, PM, SLOT, H, C, SST, HST, RES, S1, S2>
-#define CI_SPEC_XS(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES, S1, S2)                                  \
+struct SpecEntry { int Wp, Cp, MC, Nc2, T, p3, slot, H, c, sst, hst, fold, split, res, stk1, stk2, nopad; StageKernel fn; };
+#define CI_SPEC_CFG(WP, CP, MC, NC2, T, PM, SLOT, H, C, SST, HST, RES, S1, S2, NP) \
+    SCfg<WP, CP, MC, NC2, T, PM, SLOT, H, C, SST, HST, RES, S1, S2, NP>
+#define CI_SPEC_XN(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES, S1, S2, NP)                              \
     {WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST,                                                         \
-     CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES, S1, S2)::FOLD,                          \
-     CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES, S1, S2)::SPLIT, RES, S1, S2,            \
-     k_stage<CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES, S1, S2)>}
+     CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES, S1, S2, NP)::FOLD,                      \
+     CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES, S1, S2, NP)::SPLIT, RES, S1, S2, NP,    \
+     k_stage<CI_SPEC_CFG(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES, S1, S2, NP)>}
+#define CI_SPEC_XS(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES, S1, S2) \
+    CI_SPEC_XN(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES, S1, S2, 0)
 #define CI_SPEC_X(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES) \
     CI_SPEC_XS(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST, HST, RES, 0, 0)
 #define CI_SPEC(WP, CP, MC, NC2, T, P3, SLOT, H, C, SST) \
@@ -2268,6 +2429,7 @@ static const SpecEntry kSpecs[] = {
     CI_SPEC(5, 96, 128, 96, 1, 2, 16384, 4, 96, 0),  // C stage 3, f16x3
     CI_SPEC_XS(17, 8, 32, 32, 5, 2, 16384, 16, 6, 1, 1, 0, 1, 0),   // C stage 1, f16x3, stacked conv1
     CI_SPEC_XS(5, 96, 128, 96, 1, 2, 16384, 4, 96, 0, 0, 0, 1, 1),  // C stage 3, f16x3, stacked conv1 + conv2
+    CI_SPEC_XN(4, 96, 64, 288, 1, 2, 18432, 4, 96, 0, 1, 0, 0, 0, 1),   // C stage 3, f16x3, no-pad raster
     CI_SPEC_XS(17, 64, 32, 64, 3, 2, 16384, 16, 64, 0, 0, 0, 1, 0), // encoder tail, f16x3, stacked conv1
     CI_SPEC(17, 8, 16, 32, 5, 2, 16384, 16, 6, 1),   // C stage 1, f16x3, MC = 16, nhd = 2 (A/B)
     CI_SPEC(17, 8, 32, 32, 3, 2, 16384, 16, 6, 1),   // C stage 1, f16x3, T = 3, I = 1, nhd = 2 (A/B)
@@ -2289,7 +2451,7 @@ static StageKernel find_spec(const StagePlan& p, int residual, int act) {
     for (const auto& e : kSpecs)
         if (e.Wp == p.Wp && e.Cp == p.Cp && e.MC == p.MC && e.Nc2 == p.Nc2 && e.T == p.T && e.p3 == p.pm &&
             e.slot == p.slot_bytes && e.H == p.H && e.c == p.c && e.sst == p.sstate && e.hst == p.hst &&
-            e.fold == p.fold && e.split == p.split && e.stk1 == p.stk1 && e.stk2 == p.stk2 &&   // packing and epilogue must agree
+            e.fold == p.fold && e.split == p.split && e.stk1 == p.stk1 && e.stk2 == p.stk2 && e.nopad == p.nopad &&
             e.res == (residual ? 1 : 0) && (e.res || act == 0))   // coupling specs: ReLU only
             return e.fn;
     return nullptr;
@@ -2305,7 +2467,7 @@ static StageKernel pick_kernel(const StagePlan& p, const StageArgs& a) {
 // plan a stage; a stacked plan without a specialised kernel falls back to the unstacked plan
 static bool make_plan_spec(const StageInfo& S, int pm, StagePlan& p, int residual, int act) {
     if (!make_plan(S, pm, p)) return false;
-    if ((p.stk1 || p.stk2) && !find_spec(p, residual, act)) return make_plan(S, pm, p, false);
+    if ((p.stk1 || p.stk2 || p.nopad) && !find_spec(p, residual, act)) return make_plan(S, pm, p, false);
     return true;
 }
 
