@@ -401,7 +401,9 @@ struct SCfg {
     static constexpr int NB1 = MC_ * (NOPAD_ ? 3 : 1) * (STK1_ ? 2 : 1), NB2 = NC2_ * (STK2_ ? 2 : 1);
     static_assert(!(NOPAD_ && STK1_), "no-pad conv1 is 3 MC wide already");
     static_assert(!(STK1_ || STK2_) || PM_ == 2, "stacking is an f16x3 layout");
-    static_assert(!STK2_ || (!HST_ && !RES_), "stacked conv2: plain-width coupling epilogue only");
+    // stacked conv2: only the plain-width epilogue (widths of 8 / 16 / 32 / 48 columns per warp half)
+    static_assert(!STK2_ || (!HST_ && (NC2_ / 2 == 8 || (NC2_ / 2 <= 48 && (NC2_ / 2) % 16 == 0))),
+                  "stacked conv2: plain-width epilogue only");
     static constexpr bool HST = HST_ != 0;
     static constexpr bool RES = RES_ != 0;   // residual blocks / ELU / fixed-point replays compiled in
     static constexpr int HC = HST_ ? (C_ + 7) / 8 * 8 : 0;   // == StagePlan::hc
@@ -2162,6 +2164,8 @@ static const TunedPlan kTuned[] = {
     {4, 4, 96, 256, 2, 128, 1, 1, 4, 0},   // stage 3 f16x3
     {16, 16, 12, 64, 0, 32, 5, 2, 4, 1},   // CR (residual, f1) stage 1 bf16: wide hst (N = 48)
     {16, 16, 12, 64, 0, 64, 5, 1, 4, 0},   // CR stage 1 bf16, plain conv2 (CI_NO_WIDE_HST)
+    {16, 16, 12, 64, 2, 32, 7, 1, 3, 0, 0, 1},   // CR stage 1 f16x3, stacked conv2 (CI_NO_STK: unstacked)
+    {8, 8, 48, 128, 2, 64, 2, 1, 4, 0, 1, 0},    // CR stage 2 f16x3, stacked conv1
     {16, 16, 12, 64, 2, 32, 7, 1, 3, 0},   // CR stage 1 f16x3
 };
 
@@ -2431,8 +2435,6 @@ static const SpecEntry kSpecs[] = {
     CI_SPEC_XS(5, 96, 128, 96, 1, 2, 16384, 4, 96, 0, 0, 0, 1, 1),  // C stage 3, f16x3, stacked conv1 + conv2
     CI_SPEC_XN(4, 96, 64, 288, 1, 2, 18432, 4, 96, 0, 1, 0, 0, 0, 1),   // C stage 3, f16x3, no-pad raster
     CI_SPEC_XS(17, 64, 32, 64, 3, 2, 16384, 16, 64, 0, 0, 0, 1, 0), // encoder tail, f16x3, stacked conv1
-    CI_SPEC(17, 8, 16, 32, 5, 2, 16384, 16, 6, 1),   // C stage 1, f16x3, MC = 16, nhd = 2 (A/B)
-    CI_SPEC(17, 8, 32, 32, 3, 2, 16384, 16, 6, 1),   // C stage 1, f16x3, T = 3, I = 1, nhd = 2 (A/B)
     CI_SPEC(17, 64, 32, 64, 5, 0, 16384, 16, 64, 0),  // learned-encoder tail (E2, E3), bf16
     CI_SPEC(17, 64, 32, 64, 3, 2, 16384, 16, 64, 0),  // learned-encoder tail (E2, E3), f16x3
     // i-ResNet variant of Arch C (f1, config C3R): residual blocks on 12 / 48 / 192 channels
@@ -2443,6 +2445,8 @@ static const SpecEntry kSpecs[] = {
     CI_SPEC_R(17, 16, 32, 16, 7, 2, 16384, 16, 12, 0),    // CR stage 1, f16x3
     CI_SPEC_R(9, 48, 64, 48, 2, 2, 16384, 8, 48, 1),      // CR stage 2, f16x3
     CI_SPEC_R(5, 192, 128, 192, 1, 2, 16384, 4, 192, 0),  // CR stage 3, f16x3
+    CI_SPEC_XS(17, 16, 32, 16, 7, 2, 16384, 16, 12, 0, 0, 1, 0, 1),   // CR stage 1, f16x3, stacked conv2
+    CI_SPEC_XS(9, 48, 64, 48, 2, 2, 16384, 8, 48, 1, 0, 1, 1, 0),     // CR stage 2, f16x3, stacked conv1
 };
 
 // Coupling specialisations carry no residual / ELU code (it would cost them registers); residual
@@ -2466,7 +2470,8 @@ static StageKernel pick_kernel(const StagePlan& p, const StageArgs& a) {
 }
 // plan a stage; a stacked plan without a specialised kernel falls back to the unstacked plan
 static bool make_plan_spec(const StageInfo& S, int pm, StagePlan& p, int residual, int act) {
-    if (!make_plan(S, pm, p)) return false;
+    // a stacked / no-pad table entry that does not fit, or has no specialised kernel: plan without it
+    if (!make_plan(S, pm, p)) return make_plan(S, pm, p, false);
     if ((p.stk1 || p.stk2 || p.nopad) && !find_spec(p, residual, act)) return make_plan(S, pm, p, false);
     return true;
 }
