@@ -2434,6 +2434,7 @@ static const SpecEntry kSpecs[] = {
     CI_SPEC_XS(17, 8, 32, 32, 5, 2, 16384, 16, 6, 1, 1, 0, 1, 0),   // C stage 1, f16x3, stacked conv1
     CI_SPEC_XS(5, 96, 128, 96, 1, 2, 16384, 4, 96, 0, 0, 0, 1, 1),  // C stage 3, f16x3, stacked conv1 + conv2
     CI_SPEC_XN(4, 96, 64, 288, 1, 2, 18432, 4, 96, 0, 1, 0, 0, 0, 1),   // C stage 3, f16x3, no-pad raster
+    CI_SPEC_XS(9, 32, 64, 80, 2, 2, 16384, 8, 24, 0, 1, 0, 1, 0),   // C stage 2, f16x3, MC = 64 stacked (A/B)
     CI_SPEC_XS(17, 64, 32, 64, 3, 2, 16384, 16, 64, 0, 0, 0, 1, 0), // encoder tail, f16x3, stacked conv1
     CI_SPEC(17, 64, 32, 64, 5, 0, 16384, 16, 64, 0),  // learned-encoder tail (E2, E3), bf16
     CI_SPEC(17, 64, 32, 64, 3, 2, 16384, 16, 64, 0),  // learned-encoder tail (E2, E3), f16x3
