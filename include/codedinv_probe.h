@@ -45,6 +45,19 @@ CI_API ci_status_t ci_test_umma_gemm(const uint16_t* A, int32_t RA, int32_t KA, 
 CI_API ci_status_t ci_test_umma_rate(int32_t N, int32_t iters, int32_t nblocks, int64_t* cycles,
                                      ci_stream_t stream);
 
+/* TS-mode UMMA GEMM (A in tensor memory): D[128][N] (fp32) = sum over nk K=16 steps of
+ * A[:, 16j:16j+16] x B[:, 16j:16j+16]^T.  A [128][8 nk] uint32 words, row r = TMEM lane r,
+ * word 8j+i = K elements 16j+2i (low half) and 16j+2i+1 (high half), stored at TMEM columns
+ * acol + 8j + i; B [N][16 nk] 16-bit row-major in shared memory; f16 != 0: fp16 operands, else
+ * bf16.  Requires 16 <= N <= 256, N % 16 == 0, N <= acol, acol + 8 nk <= 512. */
+CI_API ci_status_t ci_test_umma_ts_gemm(const uint32_t* A, const uint16_t* B, int32_t N, int32_t nk,
+                                        int32_t acol, int32_t f16, float* D, ci_stream_t stream);
+
+/* TS-mode issue rate: `nblocks` CTAs each issue `iters` back-to-back 128 x N x 16 fp16 MMAs with
+ * A in tensor memory; cycles[nblocks] (int64) = issue-to-completion SM cycles. */
+CI_API ci_status_t ci_test_umma_ts_rate(int32_t N, int32_t iters, int32_t nblocks, int64_t* cycles,
+                                        ci_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -243,6 +243,100 @@ __global__ void __launch_bounds__(512) k_tmem_ld_rate(int iters, int batch, long
     if (warp == 0) tmem_dealloc(tmem_base, 512);
 }
 
+
+// TS-mode (A in tensor memory) GEMM: thread r of 128 writes row r of A (K = 16 nk 16-bit values,
+// two per 32-bit column, even k in the low half) into TMEM lane r, columns acol + 8j + (k%16)/2;
+// one thread then issues nk MMAs D = sum_j A_j B_j^T with B from shared memory (one plane per 8
+// K, LBO = N*16 B).  mode bit 30: fp16 operands.
+__global__ void __launch_bounds__(128) k_umma_ts_gemm(const uint32_t* __restrict__ A, const uint16_t* __restrict__ B,
+                                                      int N, int nk, int acol, int f16, float* __restrict__ D) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tmem_base;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int KB = 16 * nk, pb = KB / 8;
+    uint8_t* sB = smem;
+    for (int i = tid; i < N * pb; i += 128) {
+        int r = i / pb, p = i % pb;
+        *reinterpret_cast<uint4*>(sB + ((size_t)p * N + r) * 16) = *reinterpret_cast<const uint4*>(B + (size_t)r * KB + p * 8);
+    }
+    fence_proxy_async();
+    if (warp == 0) tmem_alloc(&tmem_base, 512);
+    if (tid == 0) { mbar_init(&bar, 1); fence_mbar_init(); }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = tmem_base;
+    const uint32_t lane_addr = (uint32_t)(warp * 32) << 16;
+    for (int j = 0; j < nk; j++) {
+        float v[8];
+        for (int i = 0; i < 8; i++) v[i] = __uint_as_float(A[(size_t)tid * (8 * nk) + 8 * j + i]);
+        tmem_st8(tmem + lane_addr + (uint32_t)(acol + 8 * j), v);
+    }
+    tmem_wait_st();
+    fence_before();
+    __syncthreads();
+    fence_after();
+    if (warp == 0 && elect_one()) {
+        const uint32_t idesc = idesc_of(128, N, f16 != 0);
+        for (int j = 0; j < nk; j++) {
+            const uint64_t bd = smem_desc(smem_u32(sB) + (uint32_t)(2 * j * N) * 16, N * 16, 128);
+            mma_ts(tmem, tmem + (uint32_t)(acol + 8 * j), bd, idesc, j > 0);
+        }
+        commit(&bar);
+    }
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    fence_after();
+    for (int c = 0; c < N; c += 8) {
+        float v[8];
+        tmem_ld8(tmem + lane_addr + c, v);
+        tmem_wait_ld();
+        for (int q = 0; q < 8; q++) D[(size_t)tid * N + c + q] = v[q];
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+// TS-mode issue rate: one elected thread issues `iters` back-to-back 128 x N x 16 MMAs with A read
+// from TMEM (columns 320 + 8 (j % 8)), D at column 0, B fixed in shared memory.
+__global__ void __launch_bounds__(128) k_umma_ts_rate(int N, int iters, long long* __restrict__ cycles) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tmem_base;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int i = tid; i < 256 * 2 * 4; i += 128) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+    fence_proxy_async();
+    if (warp == 0) tmem_alloc(&tmem_base, 512);
+    if (tid == 0) { mbar_init(&bar, 1); fence_mbar_init(); }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = tmem_base;
+    {
+        float z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int j = 0; j < 8; j++) tmem_st8(tmem + ((uint32_t)(warp * 32) << 16) + 320u + (uint32_t)(8 * j), z);
+        tmem_wait_st();
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    if (warp == 0 && elect_one()) {
+        const uint32_t idesc = idesc_f16(128, N);
+        const uint64_t bd = smem_desc(smem_u32(smem), N * 16, 128);
+        long long t0 = clock64();
+        for (int j = 0; j < iters; j++) mma_ts(tmem, tmem + 320u + (uint32_t)((j & 7) * 8), bd, idesc, 1);
+        commit(&bar);
+        mbar_wait(&bar, 0);
+        cycles[blockIdx.x] = clock64() - t0;
+    }
+    __syncwarp();
+    fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
 }  // namespace ci
 
 using namespace ci;
@@ -297,6 +391,28 @@ ci_status_t ci_test_umma_rate(int32_t N, int32_t iters, int32_t nblocks, int64_t
     CI_CUDA(cudaFuncSetAttribute(k_umma_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_umma_rate<<<nblocks, 128, smem, (cudaStream_t)stream>>>(N, iters, ntile, variant, (long long*)cycles);
     CI_CHECK_LAUNCH("k_umma_rate");
+    return CI_OK;
+}
+
+ci_status_t ci_test_umma_ts_gemm(const uint32_t* A, const uint16_t* B, int32_t N, int32_t nk, int32_t acol,
+                                 int32_t f16, float* D, ci_stream_t stream) {
+    if (N < 16 || N > 256 || N % 16 || nk < 1 || acol < N || acol + 8 * nk > 512) {
+        set_error("bad probe shape");
+        return CI_ERR_INVALID_ARG;
+    }
+    size_t smem = (size_t)2 * nk * N * 16;
+    CI_CUDA(cudaFuncSetAttribute(k_umma_ts_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_umma_ts_gemm<<<1, 128, smem, (cudaStream_t)stream>>>(A, B, N, nk, acol, f16, D);
+    CI_CHECK_LAUNCH("k_umma_ts_gemm");
+    return CI_OK;
+}
+
+ci_status_t ci_test_umma_ts_rate(int32_t N, int32_t iters, int32_t nblocks, int64_t* cycles, ci_stream_t stream) {
+    if (N < 16 || N > 256 || N % 16 || iters < 1 || nblocks < 1) { set_error("bad probe shape"); return CI_ERR_INVALID_ARG; }
+    size_t sm = 256 * 2 * 16;
+    CI_CUDA(cudaFuncSetAttribute(k_umma_ts_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k_umma_ts_rate<<<nblocks, 128, sm, (cudaStream_t)stream>>>(N, iters, (long long*)cycles);
+    CI_CHECK_LAUNCH("k_umma_ts_rate");
     return CI_OK;
 }
 

@@ -139,3 +139,45 @@ def test_umma_issue_rate_report(ci):
         print(f"[umma rate] N={N}: {c:.1f} cyc/MMA (compute floor N/2 = {N / 2:.0f}, "
               f"SS model max(N/2, 32+N/4) = {max(N / 2, 32 + N / 4):.0f})")
         assert c >= N / 2 * 0.95
+
+
+def _ts_probe(ci):
+    P, I32 = ctypes.c_void_p, ctypes.c_int32
+    ci.lib.ci_test_umma_ts_gemm.restype = I32
+    ci.lib.ci_test_umma_ts_gemm.argtypes = [P, P, I32, I32, I32, I32, P, P]
+    ci.lib.ci_test_umma_ts_rate.restype = I32
+    ci.lib.ci_test_umma_ts_rate.argtypes = [I32, I32, I32, P, P]
+    return ci.lib
+
+
+@pytest.mark.parametrize("N,nk,acol", [(16, 1, 256), (80, 4, 256), (96, 2, 128), (128, 4, 384), (256, 3, 256)])
+@pytest.mark.parametrize("f16", [0, 1])
+def test_umma_ts_gemm_a_in_tmem(ci, N, nk, acol, f16):
+    """TS mode (A operand in tensor memory, the stage-1 conv2 of DESIGN.md 7.2): lane r = row r,
+    K pairs (2i, 2i+1) packed low / high in column 8j + i; exact on small integers."""
+    lib = _ts_probe(ci)
+    rng = np.random.default_rng(N * 10 + nk + f16)
+    A = bf16_small_ints(rng, (128, 16 * nk))
+    B = bf16_small_ints(rng, (N, 16 * nk))
+    dt = torch.float16 if f16 else torch.bfloat16
+    a16 = torch.from_numpy(A).to(dt).view(torch.int16).view(torch.int32).cuda()   # pairs -> one word, even k low
+    b16 = torch.from_numpy(B).to(dt).view(torch.int16).cuda()
+    D = torch.empty(128, N, device="cuda")
+    st = lib.ci_test_umma_ts_gemm(a16.data_ptr(), b16.data_ptr(), N, nk, acol, f16, D.data_ptr(), ci._s())
+    assert st == 0, ci.lib.ci_probe_last_error().decode()
+    torch.cuda.synchronize()
+    assert np.array_equal(D.cpu().numpy(), A @ B.T)
+
+
+def test_umma_ts_issue_rate_report(ci):
+    """Reports the TS-mode tcgen05 rate (A from TMEM: only B crosses the shared-memory port); sanity only."""
+    lib = _ts_probe(ci)
+    for N in (16, 32, 48, 64, 80, 96, 128, 160, 256):
+        cyc = torch.zeros(148, dtype=torch.int64, device="cuda")
+        st = lib.ci_test_umma_ts_rate(N, 2048, 148, cyc.data_ptr(), ci._s())
+        assert st == 0
+        torch.cuda.synchronize()
+        c = cyc.cpu().numpy().astype(np.float64).mean() / 2048
+        print(f"[umma ts rate] N={N}: {c:.1f} cyc/MMA (compute floor N/2 = {N / 2:.0f}, "
+              f"SS model max(N/2, 32+N/4) = {max(N / 2, 32 + N / 4):.0f})")
+        assert c >= N / 2 * 0.95
