@@ -134,4 +134,23 @@ ci_status_t umma_stage(const Model* m, int stage, float* state, int64_t n, bool 
 ci_status_t umma_encoder_tail(const Model* m, float* zbuf, int64_t n, int* ctr, cudaStream_t s);
 bool umma_has_encoder(const Model* m);   // the encoder tail has a tcgen05 plan
 
+// TS-mode stage kernel (k_stage_ts.cu): Arch C stage 1 (16x16, c = 6, m = 64, coupling + ReLU)
+// with the hidden activation kept in tensor memory
+struct TsArgs {
+    float* state;            // [n][C][H][W] fp32, updated in place
+    int64_t n;               // images
+    const uint8_t* wpack;    // stage stream: block t at t * blk_bytes (pack_block, StagePlan::ts)
+    int64_t blk_bytes;
+    const float* bias;       // block t at t * bias_stride: [64] b1 (folded, unused), then b2 by channel
+    int bias_stride;
+    int nb, first_orient, inverse;
+    int* ctr;                // zeroed batch counter of this launch, or null
+};
+bool stage_ts_shape(int H, int W, int C, int c, int m, int residual, int act);
+int64_t stage_ts_block_bytes(int pm);
+int stage_ts_n2();
+void stage_ts_col(int n, int& tap, int& o);   // conv2 column -> (tap, output channel), tap -1 = padding
+cudaError_t stage_ts_prepare();
+cudaError_t launch_stage_ts(const TsArgs& a, int pm, cudaStream_t st);
+
 }  // namespace ci

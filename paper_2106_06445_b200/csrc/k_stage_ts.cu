@@ -1,0 +1,519 @@
+// Stage 1 of Arch C (16x16 images, c = 6 coupling channels, m = 64 hidden) as a TS-mode kernel:
+// the hidden activation never leaves tensor memory.  DESIGN.md 7.2b.
+//
+// One additive-coupling block (Eq. 1):  s_out <- s_out (+|-) F(s_in),
+//   F = conv3x3(W2) o ReLU o conv3x3(W1)   (cross-correlation, zero padding, as oracle_conv3x3).
+//
+//  * Raster WITHOUT pad column or pad band: one image = 256 rows = exactly two 128-row M-tiles
+//    (100% of the MMA rows are pixels; the padded raster of k_stage holds 2 images in 5 tiles).
+//    Horizontal taps can no longer be row shifts (they would wrap into the next image row), so
+//    the conv1 input is kept in three views: Xc (the input), Xl[p] = X[p-1] (0 at x = 0) and
+//    Xr[p] = X[p+1] (0 at x = W-1).  Tap (u, v) of row p is row p + u W of view v: vertical
+//    shifts only, and the pair-mode k-step order of k_stage is kept (9 taps x 8 channels in 5
+//    K = 16 steps, the two 8-channel K halves of a step LBO bytes apart: l|c views, or two
+//    rows of Xr 16 rows apart).
+//  * conv1 (SS mode, A = X views in shared memory, B = W1 streamed by the TMA engine) writes
+//    acc1[row][h]; the epilogue applies ReLU, splits into fp16 hi + lo and stores the result
+//    back into TMEM (tcgen05.st) as the A operand of conv2: lane = pixel row, two 16-bit
+//    channels per 32-bit column (tests/test_gpu_umma.py pins the layout).
+//  * conv2 (TS mode: A from TMEM, only B crosses the 128 B/clk shared-memory port; measured at
+//    the compute floor N/2 cycles) computes all 9 taps at once: N = 64 columns = 9 taps x 4
+//    outputs (warp half 0: channels 0-3) + 9 taps x 2 outputs (half 1: channels 4-5), K = the
+//    64 hidden channels.  The epilogue forms out[p] = sum_{u,v} Z_{u,v}[p + u W + v]: the
+//    horizontal part with lane shuffles (image rows are 16-aligned inside a warp), the vertical
+//    part with one xor-16 shuffle (two image rows per warp) plus one 16-B shared-memory exchange
+//    with the neighbouring warp row.
+//  * Two images ("slots" A and B) per CTA in flight: TMEM columns [0,256) and [256,512), so
+//    the MMA issue order per block, conv1(A) conv1(B) conv2(A) conv2(B), lets the tensor core run
+//    one image's convolutions while the epilogue warps work on the other's (ping-pong).
+//  * The batch's fp32 state lives in shared memory for the whole stage.
+// Precisions as k_stage (PM: 0 bf16, 1 f16x2, 2 f16x3 with the stacked conv1).
+#include <stdio.h>
+
+#include "ci_internal.h"
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "umma.cuh"
+
+namespace ci {
+using namespace umma;
+
+namespace ts {
+constexpr int kThreads = 320;      // warp 0 producer, warp 1 MMA, warps 2..9 epilogue
+constexpr int kEpi = 256;
+constexpr int H = 16, W = 16, HW = 256, C = 12, c = 6, M = 64;
+constexpr int G = 16;                       // guard rows above the image (one image row)
+constexpr int RT = G + HW + 32;             // rows per view plane (32 guard rows below)
+constexpr int PB = RT * 16;                 // plane bytes
+constexpr int N1 = 64, N2 = 64;             // conv1 / conv2 MMA widths
+constexpr int K1 = 5, K2 = 4;               // k-steps
+constexpr int NSLOT = 4, SLOTB = 20480;     // weight ring
+constexpr int ST_BYTES = C * HW * 4;        // fp32 state of one image
+constexpr int XCH_BYTES = 2 * HW * 16;      // vertical exchange [half][row] float4
+__host__ __device__ constexpr int kstep(int N, int pm) { return N * 32 * (pm == 2 ? 2 : 1); }
+__host__ __device__ constexpr int nplanes(int pm) { return pm ? 6 : 3; }
+__host__ __device__ constexpr int slot_bytes(int pm) { return nplanes(pm) * PB + ST_BYTES + XCH_BYTES; }
+__host__ __device__ constexpr int smem_bytes(int pm) { return NSLOT * SLOTB + 2 * slot_bytes(pm) + 512; }
+}  // namespace ts
+
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, float (&v)[4]) {
+    uint32_t r[4];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(taddr));
+#pragma unroll
+    for (int i = 0; i < 4; i++) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_ld2(uint32_t taddr, float (&v)[2]) {
+    uint32_t r[2];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "r"(taddr));
+    v[0] = __uint_as_float(r[0]);
+    v[1] = __uint_as_float(r[1]);
+}
+__device__ __forceinline__ void tmem_st16u(uint32_t taddr, const uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
+
+// two fp32 -> packed 16-bit pair (a in the low half): fp16 hi / lo split, or bf16
+__device__ __forceinline__ void ts_split(float a, float b, uint32_t& hi, uint32_t& lo) {
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(b), "f"(a));
+    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&hi));
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(b - f.y), "f"(a - f.x));
+}
+__device__ __forceinline__ uint32_t ts_bf16x2(float a, float b) {
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+    return r;
+}
+
+template <int PM>
+__global__ void __launch_bounds__(ts::kThreads, 1) k_stage_ts(TsArgs a) {
+    using namespace ts;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    uint8_t* ring = smem;
+    uint8_t* slots = ring + NSLOT * SLOTB;   // [2] x { X planes [hi l c r][lo l c r], state, xch }
+    auto xplanes = [&](int s) { return slots + (size_t)s * slot_bytes(PM); };
+    auto sstate = [&](int s) { return reinterpret_cast<float*>(slots + (size_t)s * slot_bytes(PM) + nplanes(PM) * PB); };
+    auto sxch = [&](int s) {
+        return reinterpret_cast<float4*>(slots + (size_t)s * slot_bytes(PM) + nplanes(PM) * PB + ST_BYTES);
+    };
+    uint64_t* bars = reinterpret_cast<uint64_t*>(slots + 2 * slot_bytes(PM));
+    uint64_t* full = bars;            // [4]
+    uint64_t* empty = bars + 4;       // [4]
+    uint64_t* bqf = bars + 8;         // [4] batch queue entry published
+    uint64_t* bqe = bars + 12;        // [4] entry consumed (MMA thread + every epilogue thread)
+    uint64_t* x_rdy = bars + 16;      // [2] X views of slot s final for the next conv1 (epilogue)
+    uint64_t* a1t = bars + 18;        // [2][2] conv1 of (slot, tile) done (commit)
+    uint64_t* hdt = bars + 22;        // [2][2] hidden of (slot, tile) in TMEM (epilogue)
+    uint64_t* a2t = bars + 26;        // [2][2] conv2 of (slot, tile) done (commit)
+    volatile int64_t* bq = reinterpret_cast<volatile int64_t*>(bars + 30);   // [4]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 34);
+
+    {   // X views: zero guards, x = 0 column of Xl, x = W-1 column of Xr (never written later)
+        uint4 z = make_uint4(0, 0, 0, 0);
+        for (int s = 0; s < 2; s++)
+            for (int i = tid; i < nplanes(PM) * PB / 16; i += kThreads) reinterpret_cast<uint4*>(xplanes(s))[i] = z;
+    }
+    fence_proxy_async();
+    if (warp == 1) tmem_alloc(tmem_slot, 512);
+    if (tid == 0) {
+        for (int i = 0; i < 4; i++) {
+            mbar_init(&full[i], 1); mbar_init(&empty[i], 1);
+            mbar_init(&bqf[i], 1); mbar_init(&bqe[i], 1 + kEpi);
+        }
+        for (int i = 0; i < 2; i++) mbar_init(&x_rdy[i], kEpi);
+        for (int i = 0; i < 4; i++) { mbar_init(&a1t[i], 1); mbar_init(&hdt[i], kEpi); mbar_init(&a2t[i], 1); }
+        fence_mbar_init();
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int64_t nbatch = a.n;   // one image per batch
+    auto bq_read = [&](int i) -> int64_t {
+        mbar_wait(&bqf[i & 3], (uint32_t)((i >> 2) & 1));
+        return bq[i & 3];
+    };
+    const int SEG1 = K1 * kstep(N1, PM), SEG2 = K2 * kstep(N2, PM);
+
+    if (warp == 0) {
+        // ================= producer: claims batches in pairs, streams packed weights =========
+        if (lane == 0) {
+            int slot = 0;
+            uint32_t phase = 0;
+            int64_t claimed = 0;
+            auto next = [&]() -> int64_t {
+                const int64_t k = claimed++;
+                if (k == 0) return blockIdx.x;
+                return a.ctr ? (int64_t)gridDim.x + atomicAdd(a.ctr, 1) : (int64_t)blockIdx.x + k * gridDim.x;
+            };
+            auto publish = [&](int i, int64_t v) {
+                mbar_wait(&bqe[i & 3], (uint32_t)(((i >> 2) & 1) ^ 1));
+                bq[i & 3] = v;
+                mbar_arrive(&bqf[i & 3]);
+            };
+            for (int pi = 0;; pi++) {
+                const int64_t b0 = next();
+                publish(2 * pi, b0);
+                if (b0 >= nbatch) break;
+                const int64_t b1 = next();
+                publish(2 * pi + 1, b1);
+                for (int tt = 0; tt < a.nb; tt++) {
+                    const int t = a.inverse ? a.nb - 1 - tt : tt;
+                    const uint8_t* src = a.wpack + (int64_t)t * a.blk_bytes;
+                    for (int sg = 0; sg < 2; sg++) {
+                        const uint32_t bytes = sg == 0 ? SEG1 : SEG2;
+                        mbar_wait(&empty[slot], phase ^ 1);
+                        mbar_arrive_expect_tx(&full[slot], bytes);
+                        bulk_g2s(ring + (size_t)slot * SLOTB, src, bytes, &full[slot]);
+                        src += bytes;
+                        if (++slot == NSLOT) { slot = 0; phase ^= 1; }
+                    }
+                }
+                if (b1 >= nbatch) break;
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // ================= MMA issuer ========================================================
+        if (elect_one()) {
+            int slot = 0;
+            uint32_t phase = 0, kb = 0;
+            const uint32_t rb = smem_u32(ring);
+            const uint32_t id1w = idesc_of(128, PM == 2 ? 2 * N1 : N1, PM != 0);
+            const uint32_t id1 = idesc_of(128, N1, PM != 0);
+            const uint32_t id2 = idesc_of(128, N2, PM != 0);
+            constexpr uint32_t LOA = (uint32_t)(3 * PB / 16);     // lo views, descriptor units
+            constexpr uint32_t B1LBO = (uint32_t)((PM == 2 ? 2 : 1) * N1 * 16);
+            for (int pi = 0;; pi++) {
+                const int64_t b0 = bq_read(2 * pi);
+                mbar_arrive(&bqe[(2 * pi) & 3]);
+                if (b0 >= nbatch) break;
+                const int64_t b1 = bq_read(2 * pi + 1);
+                mbar_arrive(&bqe[(2 * pi + 1) & 3]);
+                const int ns = b1 < nbatch ? 2 : 1;
+                for (int tt = 0; tt < a.nb; tt++, kb++) {
+                    const uint32_t par = kb & 1;
+                    // conv1 of both slots: one weight segment
+                    mbar_wait(&full[slot], phase);
+                    fence_after();
+                    const uint32_t w1 = rb + (uint32_t)slot * SLOTB;
+                    for (int s = 0; s < ns; s++) {
+                        mbar_wait(&x_rdy[s], par);
+                        fence_after();
+                        const uint32_t xs = smem_u32(xplanes(s));
+#pragma unroll
+                        for (int t = 0; t < 2; t++) {
+                            const uint32_t d = tmem + (uint32_t)(s * 256 + t * 128);
+#pragma unroll
+                            for (int ks = 0; ks < K1; ks++) {
+                                // k-step ks (pair order): views l|c at row shift (ks-1) W, or two rows
+                                // of Xr 16 apart (taps (-1,+1)|(0,+1), then (+1,+1)|zero weights)
+                                const uint32_t base = ks < 3 ? xs : xs + 2 * PB;
+                                const int row = G + t * 128 + (ks < 3 ? (ks - 1) * W : (ks == 3 ? -W : W));
+                                const uint32_t lbo = ks < 3 ? (uint32_t)PB : (uint32_t)(W * 16);
+                                const uint64_t ad = smem_desc(base + (uint32_t)row * 16u, lbo, 128);
+                                const uint64_t bd = smem_desc(w1 + (uint32_t)(ks * kstep(N1, PM)), B1LBO, 128);
+                                const uint32_t acc = ks > 0 ? 1u : 0u;
+                                if (PM == 2) {   // hi(x) [W_hi | W_lo] (2N wide), then lo(x) W_hi
+                                    mma_bf16(d, ad, bd, id1w, acc);
+                                    mma_bf16(d, ad + LOA, bd, id1, 1u);
+                                } else {
+                                    mma_bf16(d, ad, bd, id1, acc);
+                                    if (PM == 1) mma_bf16(d, ad + LOA, bd, id1, 1u);
+                                }
+                            }
+                            commit(&a1t[s * 2 + t]);
+                        }
+                    }
+                    commit(&empty[slot]);
+                    if (++slot == NSLOT) { slot = 0; phase ^= 1; }
+                    // conv2 of both slots (TS mode: A = the hidden in TMEM)
+                    mbar_wait(&full[slot], phase);
+                    fence_after();
+                    const uint32_t w2 = rb + (uint32_t)slot * SLOTB;
+                    for (int s = 0; s < ns; s++) {
+#pragma unroll
+                        for (int t = 0; t < 2; t++) {
+                            mbar_wait(&hdt[s * 2 + t], par);
+                            fence_after();
+                            const uint32_t tb = tmem + (uint32_t)(s * 256 + t * 128);
+#pragma unroll
+                            for (int ks = 0; ks < K2; ks++) {
+                                // hidden channels 16 ks..16 ks+15: warp half ks/2's words 8 (ks%2)..+7
+                                const uint32_t ahi = tb + (uint32_t)(32 * (ks >> 1) + 8 * (ks & 1));
+                                const uint64_t bd = smem_desc(w2 + (uint32_t)(ks * kstep(N2, PM)), N2 * 16, 128);
+                                const uint32_t acc = ks > 0 ? 1u : 0u;
+                                mma_ts(tb + 64, ahi, bd, id2, acc);
+                                if (PM >= 1) mma_ts(tb + 64, ahi + 16, bd, id2, 1u);                       // lo(h) W
+                                if (PM == 2) mma_ts(tb + 64, ahi, bd + (uint64_t)(N2 * 32 / 16), id2, 1u);  // hi(h) W_lo
+                            }
+                            commit(&a2t[s * 2 + t]);
+                        }
+                    }
+                    commit(&empty[slot]);
+                    if (++slot == NSLOT) { slot = 0; phase ^= 1; }
+                }
+                if (ns == 1) break;
+            }
+        }
+        __syncwarp();
+    } else {
+        // ================= epilogue warps ===================================================
+        // warp w reads TMEM lanes 32 (w % 4)..+31; warps w and w+4 share a lane quarter: half 0
+        // takes hidden channels 0-31 / outputs 0-3, half 1 hidden 32-63 / outputs 4-5 (+ the
+        // constant-1 channel 6 of the X views, which carries the folded conv1 bias)
+        const int ew = warp - 2, quarter = warp & 3, half = ew >> 2, et = ew * 32 + lane;
+        const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
+        const int x = lane & 15;
+        uint32_t kb = 0;
+        // X views of slot s at row p, this half's 4 channel slots (8 bytes of the 16-byte row)
+        auto write_x = [&](int s, int p, const float (&v)[4]) {
+            uint8_t* xs = xplanes(s);
+            uint2 hi, lo;
+            if (PM) {
+                ts_split(v[0], v[1], hi.x, lo.x);
+                ts_split(v[2], v[3], hi.y, lo.y);
+            } else {
+                hi = make_uint2(ts_bf16x2(v[0], v[1]), ts_bf16x2(v[2], v[3]));
+                lo = hi;
+            }
+            const size_t off = (size_t)(G + p) * 16 + half * 8;
+            auto put = [&](int view, int row_delta) {
+                *reinterpret_cast<uint2*>(xs + (size_t)view * PB + off + row_delta * 16) = hi;
+                if (PM) *reinterpret_cast<uint2*>(xs + (size_t)(3 + view) * PB + off + row_delta * 16) = lo;
+            };
+            put(1, 0);                  // Xc[p]
+            if (x < W - 1) put(0, 1);   // Xl[p+1] = X[p]
+            if (x > 0) put(2, -1);      // Xr[p-1] = X[p]
+        };
+        auto in_half = [&](int t) { return ((a.first_orient + t) & 1) == 0 ? 0 : c; };
+        for (int pi = 0;; pi++) {
+            const int64_t b0 = bq_read(2 * pi);
+            mbar_arrive(&bqe[(2 * pi) & 3]);
+            if (b0 >= nbatch) break;
+            const int64_t b1 = bq_read(2 * pi + 1);
+            mbar_arrive(&bqe[(2 * pi + 1) & 3]);
+            const int ns = b1 < nbatch ? 2 : 1;
+            // ---- batch state -> shared memory, first block's input half -> X views
+            for (int s = 0; s < ns; s++) {
+                const float4* src = reinterpret_cast<const float4*>(a.state + (s ? b1 : b0) * (int64_t)C * HW);
+                float4* dst = reinterpret_cast<float4*>(sstate(s));
+                for (int i = et; i < C * HW / 4; i += kEpi) dst[i] = __ldcg(src + i);
+            }
+            asm volatile("bar.sync 1, %0;" ::"n"(kEpi) : "memory");
+            {
+                const int t0 = a.inverse ? a.nb - 1 : 0, ioff = in_half(t0) + 4 * half;
+                for (int s = 0; s < ns; s++) {
+                    const float* st = sstate(s);
+#pragma unroll
+                    for (int t = 0; t < 2; t++) {
+                        const int p = t * 128 + quarter * 32 + lane;
+                        float v[4];
+                        if (half == 0) {
+#pragma unroll
+                            for (int o = 0; o < 4; o++) v[o] = st[(ioff + o) * HW + p];
+                        } else {
+                            v[0] = st[ioff * HW + p];
+                            v[1] = st[(ioff + 1) * HW + p];
+                            v[2] = 1.f;
+                            v[3] = 0.f;
+                        }
+                        write_x(s, p, v);
+                    }
+                    fence_proxy_async();
+                    mbar_arrive(&x_rdy[s]);
+                }
+            }
+            for (int tt = 0; tt < a.nb; tt++, kb++) {
+                const uint32_t par = kb & 1;
+                const int t = a.inverse ? a.nb - 1 - tt : tt;
+                const int out_off = c - in_half(t);
+                const bool write_next = tt + 1 < a.nb;
+                // ---- conv1 epilogue: acc1 -> ReLU -> fp16 hi / lo (or bf16) words back into TMEM,
+                // into the same columns this thread read (half h: columns [32h, 32h+32))
+                for (int s = 0; s < ns; s++) {
+#pragma unroll
+                    for (int tl = 0; tl < 2; tl++) {
+                        mbar_wait(&a1t[s * 2 + tl], par);
+                        fence_after();
+                        const uint32_t col = tmem + lane_addr + (uint32_t)(s * 256 + tl * 128 + 32 * half);
+                        float v[32];
+                        {
+                            float (&v0)[16] = *reinterpret_cast<float (*)[16]>(&v[0]);
+                            float (&v1)[16] = *reinterpret_cast<float (*)[16]>(&v[16]);
+                            tmem_ld16(col, v0);
+                            tmem_ld16(col + 16, v1);
+                        }
+                        if (PM == 2) {   // stacked: hi(x) W_lo columns at +64
+                            float w[32];
+                            float (&w0)[16] = *reinterpret_cast<float (*)[16]>(&w[0]);
+                            float (&w1)[16] = *reinterpret_cast<float (*)[16]>(&w[16]);
+                            tmem_ld16(col + 64, w0);
+                            tmem_ld16(col + 80, w1);
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int e = 0; e < 32; e++) v[e] += w[e];
+                        } else {
+                            tmem_wait_ld();
+                        }
+                        uint32_t hw[16], lw[16];
+#pragma unroll
+                        for (int e = 0; e < 16; e++) {
+                            const float p0 = fmaxf(v[2 * e], 0.f), p1 = fmaxf(v[2 * e + 1], 0.f);
+                            if (PM) ts_split(p0, p1, hw[e], lw[e]);
+                            else hw[e] = ts_bf16x2(p0, p1);
+                        }
+                        tmem_st16u(col, hw);
+                        if (PM) tmem_st16u(col + 16, lw);
+                        tmem_wait_st();
+                        fence_before();
+                        mbar_arrive(&hdt[s * 2 + tl]);
+                    }
+                }
+                // ---- conv2 epilogue: col2im of the 9 tap groups, s_out (+|-)= F + b2
+                const float* b2 = a.bias + (int64_t)t * a.bias_stride + M;
+                for (int s = 0; s < ns; s++) {
+                    float mid[2][4];
+                    float4* xch = sxch(s);
+#pragma unroll
+                    for (int tl = 0; tl < 2; tl++) {
+                        mbar_wait(&a2t[s * 2 + tl], par);
+                        fence_after();
+                        const uint32_t col = tmem + lane_addr + (uint32_t)(s * 256 + tl * 128 + 64 + 36 * half);
+                        float z[9][4];
+                        if (half == 0) {   // column 4 tap + o
+                            float za[16], zb[16], zc[4];
+                            tmem_ld16(col, za);
+                            tmem_ld16(col + 16, zb);
+                            tmem_ld4(col + 32, zc);
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int q = 0; q < 36; q++) z[q / 4][q % 4] = q < 16 ? za[q] : (q < 32 ? zb[q - 16] : zc[q - 32]);
+                        } else {           // column 36 + 2 tap + (o - 4)
+                            float za[16], zb[2];
+                            tmem_ld16(col, za);
+                            tmem_ld2(col + 16, zb);
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int q = 0; q < 18; q++) z[q / 2][q % 2] = q < 16 ? za[q] : zb[q - 16];
+#pragma unroll
+                            for (int q = 0; q < 9; q++) z[q][2] = z[q][3] = 0.f;
+                        }
+                        // horizontal: H_u[r] = Z_{u,-1}[r-1] + Z_{u,0}[r] + Z_{u,+1}[r+1] (masked at x = 0 / W-1)
+                        float hsum[3][4];
+#pragma unroll
+                        for (int u = 0; u < 3; u++)
+#pragma unroll
+                            for (int o = 0; o < 4; o++) {
+                                const float l = __shfl_up_sync(0xffffffffu, z[u * 3 + 0][o], 1);
+                                const float r = __shfl_down_sync(0xffffffffu, z[u * 3 + 2][o], 1);
+                                hsum[u][o] = z[u * 3 + 1][o] + (x > 0 ? l : 0.f) + (x < W - 1 ? r : 0.f);
+                            }
+                        // vertical: out[p] = H_-1[p-W] + H_0[p] + H_+1[p+W].  Lanes l < 16 (even y) take
+                        // H_+1 of lane l+16 and publish their H_+1 for the warp row above; lanes >= 16
+                        // take H_-1 of lane l-16 and publish their H_-1 for the warp row below.
+                        const int p = tl * 128 + quarter * 32 + lane;
+                        float pub[4];
+#pragma unroll
+                        for (int o = 0; o < 4; o++) {
+                            const float send = lane < 16 ? hsum[0][o] : hsum[2][o];
+                            const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
+                            mid[tl][o] = hsum[1][o] + recv;
+                            pub[o] = lane < 16 ? hsum[2][o] : hsum[0][o];
+                        }
+                        xch[half * HW + p] = make_float4(pub[0], pub[1], pub[2], pub[3]);
+                    }
+                    fence_before();
+                    asm volatile("bar.sync 1, %0;" ::"n"(kEpi) : "memory");
+                    float* st = sstate(s);
+                    float bb[4];
+#pragma unroll
+                    for (int o = 0; o < 4; o++) bb[o] = (half == 0 || o < 2) ? __ldg(b2 + 4 * half + o) : 0.f;
+#pragma unroll
+                    for (int tl = 0; tl < 2; tl++) {
+                        const int p = tl * 128 + quarter * 32 + lane, y = p >> 4;
+                        float4 oth = make_float4(0.f, 0.f, 0.f, 0.f);
+                        if (lane < 16 && y > 0) oth = xch[half * HW + p - W];
+                        if (lane >= 16 && y < H - 1) oth = xch[half * HW + p + W];
+                        const float ov[4] = {oth.x, oth.y, oth.z, oth.w};
+                        float nv[4];
+#pragma unroll
+                        for (int o = 0; o < 4; o++) {
+                            const int ch = 4 * half + o;
+                            if (ch < c) {
+                                const float f = mid[tl][o] + ov[o] + bb[o];
+                                float* sp = st + (out_off + ch) * HW + p;
+                                const float old = *sp;
+                                nv[o] = a.inverse ? old - f : old + f;
+                                *sp = nv[o];
+                            } else {
+                                nv[o] = ch == c ? 1.f : 0.f;   // constant-1 channel (folded conv1 bias)
+                            }
+                        }
+                        if (write_next) write_x(s, p, nv);
+                    }
+                    if (write_next) {
+                        fence_proxy_async();
+                        mbar_arrive(&x_rdy[s]);
+                    }
+                }
+            }
+            // ---- state back to global memory
+            asm volatile("bar.sync 1, %0;" ::"n"(kEpi) : "memory");
+            for (int s = 0; s < ns; s++) {
+                float4* dst = reinterpret_cast<float4*>(a.state + (s ? b1 : b0) * (int64_t)C * HW);
+                const float4* src = reinterpret_cast<const float4*>(sstate(s));
+                for (int i = et; i < C * HW / 4; i += kEpi) __stcg(dst + i, src[i]);
+            }
+            asm volatile("bar.sync 1, %0;" ::"n"(kEpi) : "memory");
+            if (ns == 1) break;
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+bool stage_ts_shape(int H, int W, int C, int c, int m, int residual, int act) {
+    return H == ts::H && W == ts::W && C == ts::C && c == ts::c && m == ts::M && !residual && act == 0 &&
+           !getenv("CI_NO_TS");
+}
+int64_t stage_ts_block_bytes(int pm) { return (int64_t)ts::K1 * ts::kstep(ts::N1, pm) + ts::K2 * ts::kstep(ts::N2, pm); }
+int stage_ts_n2() { return ts::N2; }
+
+// conv2 column n of the TS layout -> (tap, output channel), or tap = -1 for padding columns
+void stage_ts_col(int n, int& tap, int& o) {
+    if (n < 36) { tap = n / 4; o = n % 4; return; }
+    if (n < 54) { tap = (n - 36) / 2; o = 4 + (n - 36) % 2; return; }
+    tap = -1; o = -1;
+}
+
+static void* ts_kernel(int pm) {
+    return pm == 2 ? (void*)k_stage_ts<2> : (pm == 1 ? (void*)k_stage_ts<1> : (void*)k_stage_ts<0>);
+}
+
+cudaError_t stage_ts_prepare() {
+    cudaError_t e = cudaSuccess;
+    for (int pm = 0; pm < 3 && e == cudaSuccess; pm++)
+        e = cudaFuncSetAttribute(ts_kernel(pm), cudaFuncAttributeMaxDynamicSharedMemorySize, ts::smem_bytes(pm));
+    return e;
+}
+
+cudaError_t launch_stage_ts(const TsArgs& a, int pm, cudaStream_t st) {
+    const int grid = (int)std::min<int64_t>((a.n + 1) / 2, 148);
+    if (a.n <= 0) return cudaSuccess;
+    const size_t sm = ts::smem_bytes(pm);
+    if (pm == 2) k_stage_ts<2><<<grid, ts::kThreads, sm, st>>>(a);
+    else if (pm == 1) k_stage_ts<1><<<grid, ts::kThreads, sm, st>>>(a);
+    else k_stage_ts<0><<<grid, ts::kThreads, sm, st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace ci

@@ -82,6 +82,8 @@ struct StagePlan {
     int nopad;             // raster without pad column (Wp = W): conv1's horizontal taps stacked in
                            // N as well (3 MC columns, masked col2im in the epilogue), conv2 hst
     int n1;                // conv1 segment width: MC, or 3 MC with nopad
+    int ts;                // TS-mode stage kernel (k_stage_ts.cu): no-pad raster with l/c/r views,
+                           // hidden in TMEM, conv2 over all 9 taps stacked in N
 };
 
 struct StageArgs {
@@ -2380,7 +2382,11 @@ static void pack_block(const StagePlan& p, const float* W1, const float* b1, con
             for (int n = 0; n < p.Nc2; n++)
                 for (int kk = 0; kk < 16; kk++) {
                     const int h = j * p.MC + kc * 16 + kk;
-                    if (p.hst)   // column n = (v+1)*hc + o, k-step row u = tap-1
+                    if (p.ts) {   // all 9 taps stacked in N (stage_ts_col), k-step s = hidden 16 s..16 s+15
+                        int tp, o;
+                        stage_ts_col(n, tp, o);
+                        tile[(size_t)n * 16 + kk] = tp >= 0 ? w2(o, 16 * s + kk, tp / 3 - 1, tp % 3 - 1) : 0.f;
+                    } else if (p.hst)   // column n = (v+1)*hc + o, k-step row u = tap-1
                         tile[(size_t)n * 16 + kk] = n < 3 * p.hc ? w2(n % p.hc, h, tap - 1, n / p.hc - 1) : 0.f;
                     else
                         tile[(size_t)n * 16 + kk] = w2(conv2_col_channel(p, n), h, tap / 3 - 1, tap % 3 - 1);
@@ -2471,6 +2477,21 @@ static StageKernel pick_kernel(const StagePlan& p, const StageArgs& a) {
 }
 // plan a stage; a stacked plan without a specialised kernel falls back to the unstacked plan
 static bool make_plan_spec(const StageInfo& S, int pm, StagePlan& p, int residual, int act) {
+    if (stage_ts_shape(S.H, S.W, S.C, S.c, S.m, residual, act)) {
+        p = StagePlan{};
+        p.ts = 1;
+        p.H = S.H; p.W = S.W; p.Wp = S.W; p.G = S.W;
+        p.c = S.c; p.m = S.m; p.Cp = 8; p.Mp = 64; p.MC = 64; p.nch = 1; p.n1 = 64;
+        p.Nc2 = stage_ts_n2();
+        p.T = 2; p.I = 1; p.pair = 1; p.fold = 1; p.pm = pm;
+        p.k1 = kPairK1; p.k2 = 4;
+        p.stk1 = pm == 2 ? 1 : 0;
+        p.blk_bytes = stage_ts_block_bytes(pm);
+        p.tmem_cols = 512;
+        p.nslot = 4;
+        p.slot_bytes = 20480;
+        return true;
+    }
     // a stacked / no-pad table entry that does not fit, or has no specialised kernel: plan without it
     if (!make_plan(S, pm, p)) return make_plan(S, pm, p, false);
     if ((p.stk1 || p.stk2 || p.nopad) && !find_spec(p, residual, act)) return make_plan(S, pm, p, false);
@@ -2495,10 +2516,11 @@ ci_status_t umma_prepare(Model* m, const float* host_params) {
         if (getenv("CI_DEBUG_PLAN"))
             fprintf(stderr,
                     "[ci plan] stage %d %dx%d c=%d m=%d pm=%d: Cp=%d Mp=%d MC=%d nch=%d Nc2=%d T=%d I=%d "
-                    "k1=%d k2=%d slots=%dx%d smem=%zu tmem=%d blk_bytes=%lld M-eff=%.3f nhd=%d sst=%d stk=%d%d est=%.0f cyc/img/blk\n",
+                    "k1=%d k2=%d slots=%dx%d smem=%zu tmem=%d blk_bytes=%lld M-eff=%.3f nhd=%d sst=%d stk=%d%d est=%.0f cyc/img/blk%s\n",
                     s, p.H, p.W, p.c, p.m, p.pm, p.Cp, p.Mp, p.MC, p.nch, p.Nc2, p.T, p.I, p.k1, p.k2,
                     p.nslot, p.slot_bytes, p.smem, p.tmem_cols, (long long)p.blk_bytes,
-                    (double)p.I * p.H * p.W / (p.T * 128.0), p.nhd, p.sstate, p.stk1, p.stk2, p.est_cycles);
+                    (double)p.I * p.H * p.W / (p.T * 128.0), p.nhd, p.sstate, p.stk1, p.stk2, p.est_cycles,
+                    p.ts ? " [TS kernel]" : "");
         // align each stage stream to 128 B
         while ((pack.size() * 2) % 128) pack.push_back(0);
         U->wpack_off[s] = (int64_t)pack.size() * 2;
@@ -2518,7 +2540,7 @@ ci_status_t umma_prepare(Model* m, const float* host_params) {
             }
             for (int i = 0; i < p.Mp; i++) bias.push_back(i < S.m ? b1[i] : 0.f);
             for (int i = 0; i < p.Nc2; i++) {   // conv2 bias: by channel (hst) or by column
-                const int o = p.hst ? (i < S.c ? i : -1) : conv2_col_channel(p, i);
+                const int o = (p.hst || p.ts) ? (i < S.c ? i : -1) : conv2_col_channel(p, i);
                 bias.push_back(o >= 0 ? b2[o] : 0.f);
             }
         }
@@ -2559,6 +2581,7 @@ ci_status_t umma_prepare(Model* m, const float* host_params) {
     if (e == cudaSuccess) e = cudaMalloc(&m->d_bias, std::max<size_t>(bias.size(), 1) * 4);
     if (e == cudaSuccess) e = cudaMemcpy(m->d_bias, bias.data(), bias.size() * 4, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_stage<SDyn>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap);
+    if (e == cudaSuccess) e = stage_ts_prepare();
     for (const auto& sp : kSpecs)
         if (e == cudaSuccess) e = cudaFuncSetAttribute(sp.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap);
     if (e != cudaSuccess) { delete U; return cuda_status(e, "umma_prepare"); }
@@ -2684,6 +2707,25 @@ ci_status_t umma_stage(const Model* m, int s, float* state, int64_t n, bool inve
     a.ctr = ctr;
     a.residual = m->arch.block_kind == 1 ? 1 : 0;
     a.fp_iters = a.residual ? m->arch.fp_iters : 1;
+    if (a.p.ts) {
+        TsArgs t;
+        t.state = state;
+        t.n = n;
+        t.wpack = a.wpack;
+        t.blk_bytes = a.p.blk_bytes;
+        t.bias = a.bias;
+        t.bias_stride = a.p.Mp + a.p.Nc2;
+        t.nb = a.nb;
+        t.first_orient = a.first_orient;
+        t.inverse = a.inverse;
+        t.ctr = ctr;
+        const StageInfo& S = m->st[s];
+        prof_begin(st);
+        CI_CUDA(launch_stage_ts(t, a.p.pm, st));
+        count_launch();
+        prof_end(st, s, (double)n * S.nb * 36.0 * S.H * S.W * S.c * S.m);
+        return CI_OK;
+    }
     a.dbg = cycles_buffer(st);
     int64_t nbatch = (n + a.p.I - 1) / a.p.I;
     int dev_sms = 148;
