@@ -17,16 +17,17 @@
 //    back into TMEM (tcgen05.st) as the A operand of conv2: lane = pixel row, two 16-bit
 //    channels per 32-bit column (tests/test_gpu_umma.py pins the layout).
 //  * conv2 (TS mode: A from TMEM, only B crosses the 128 B/clk shared-memory port; measured at
-//    the compute floor N/2 cycles) computes all 9 taps at once: N = 64 columns = 9 taps x 4
-//    outputs (warp half 0: channels 0-3) + 9 taps x 2 outputs (half 1: channels 4-5), K = the
-//    64 hidden channels.  The epilogue forms out[p] = sum_{u,v} Z_{u,v}[p + u W + v]: the
-//    horizontal part with lane shuffles (image rows are 16-aligned inside a warp), the vertical
-//    part with one xor-16 shuffle (two image rows per warp) plus one 16-B shared-memory exchange
-//    with the neighbouring warp row.
-//  * Two images ("slots" A and B) per CTA in flight: TMEM columns [0,256) and [256,512), so
-//    the MMA issue order per block, conv1(A) conv1(B) conv2(A) conv2(B), lets the tensor core run
-//    one image's convolutions while the epilogue warps work on the other's (ping-pong).
-//  * The batch's fp32 state lives in shared memory for the whole stage.
+//    the compute floor N/2 cycles) computes all 9 taps at once: N = 64 columns = 9 taps x 6
+//    outputs (column 6 tap + o) + padding, K = the 64 hidden channels.  The epilogue forms
+//    out[p] = sum_{u,v} Z_{u,v}[p + u W + v]: the horizontal part with lane shuffles (image rows
+//    are 16-aligned inside a warp), the vertical part with one xor-16 shuffle (two image rows per
+//    warp) plus one 32-B shared-memory exchange with the neighbouring warp row.
+//  * Two images ("slots") per CTA in flight: TMEM columns [0,256) and [256,512), each served by
+//    its own group of 8 epilogue warps.  The MMA issue order per block, conv1(A) conv1(B)
+//    conv2(A) conv2(B), lets the tensor core run one image's convolutions while the other
+//    image's group is in its epilogue; the groups are otherwise independent (own barriers,
+//    own batch-queue entries, own state load / store).
+//  * The image's fp32 state lives in shared memory for the whole stage.
 // Precisions as k_stage (PM: 0 bf16, 1 f16x2, 2 f16x3 with the stacked conv1).
 #include <stdio.h>
 
@@ -40,8 +41,8 @@ namespace ci {
 using namespace umma;
 
 namespace ts {
-constexpr int kThreads = 320;      // warp 0 producer, warp 1 MMA, warps 2..9 epilogue
-constexpr int kEpi = 256;
+constexpr int kThreads = 576;      // warp 0 producer, warp 1 MMA, warps 2..17 epilogue (2 groups)
+constexpr int kEpi = 256;          // threads of one epilogue group (one image slot)
 constexpr int H = 16, W = 16, HW = 256, C = 12, c = 6, M = 64;
 constexpr int G = 16;                       // guard rows above the image (one image row)
 constexpr int RT = G + HW + 32;             // rows per view plane (32 guard rows below)
@@ -50,7 +51,7 @@ constexpr int N1 = 64, N2 = 64;             // conv1 / conv2 MMA widths
 constexpr int K1 = 5, K2 = 4;               // k-steps
 constexpr int NSLOT = 4, SLOTB = 20480;     // weight ring
 constexpr int ST_BYTES = C * HW * 4;        // fp32 state of one image
-constexpr int XCH_BYTES = 2 * HW * 16;      // vertical exchange [half][row] float4
+constexpr int XCH_BYTES = 2 * HW * 32;      // vertical exchange [block parity][row][8] fp32
 __host__ __device__ constexpr int kstep(int N, int pm) { return N * 32 * (pm == 2 ? 2 : 1); }
 __host__ __device__ constexpr int nplanes(int pm) { return pm ? 6 : 3; }
 __host__ __device__ constexpr int slot_bytes(int pm) { return nplanes(pm) * PB + ST_BYTES + XCH_BYTES; }
@@ -127,7 +128,7 @@ __global__ void __launch_bounds__(ts::kThreads, 1) k_stage_ts(TsArgs a) {
             mbar_init(&full[i], 1); mbar_init(&empty[i], 1);
             mbar_init(&bqf[i], 1); mbar_init(&bqe[i], 1 + kEpi);
         }
-        for (int i = 0; i < 2; i++) mbar_init(&x_rdy[i], kEpi);
+        for (int i = 0; i < 2; i++) mbar_init(&x_rdy[i], kEpi);   // one epilogue group each
         for (int i = 0; i < 4; i++) { mbar_init(&a1t[i], 1); mbar_init(&hdt[i], kEpi); mbar_init(&a2t[i], 1); }
         fence_mbar_init();
     }
@@ -160,10 +161,10 @@ __global__ void __launch_bounds__(ts::kThreads, 1) k_stage_ts(TsArgs a) {
             };
             for (int pi = 0;; pi++) {
                 const int64_t b0 = next();
+                const int64_t b1 = b0 < nbatch ? next() : nbatch;
                 publish(2 * pi, b0);
+                publish(2 * pi + 1, b1);   // group B reads its entry even when the queue is done
                 if (b0 >= nbatch) break;
-                const int64_t b1 = next();
-                publish(2 * pi + 1, b1);
                 for (int tt = 0; tt < a.nb; tt++) {
                     const int t = a.inverse ? a.nb - 1 - tt : tt;
                     const uint8_t* src = a.wpack + (int64_t)t * a.blk_bytes;
@@ -176,7 +177,10 @@ __global__ void __launch_bounds__(ts::kThreads, 1) k_stage_ts(TsArgs a) {
                         if (++slot == NSLOT) { slot = 0; phase ^= 1; }
                     }
                 }
-                if (b1 >= nbatch) break;
+                if (b1 >= nbatch) {   // group A's next entry: terminator
+                    publish(2 * pi + 2, nbatch);
+                    break;
+                }
             }
         }
         __syncwarp();
@@ -265,71 +269,64 @@ __global__ void __launch_bounds__(ts::kThreads, 1) k_stage_ts(TsArgs a) {
         }
         __syncwarp();
     } else {
-        // ================= epilogue warps ===================================================
-        // warp w reads TMEM lanes 32 (w % 4)..+31; warps w and w+4 share a lane quarter: half 0
-        // takes hidden channels 0-31 / outputs 0-3, half 1 hidden 32-63 / outputs 4-5 (+ the
-        // constant-1 channel 6 of the X views, which carries the folded conv1 bias)
-        const int ew = warp - 2, quarter = warp & 3, half = ew >> 2, et = ew * 32 + lane;
+        // ================= epilogue: two independent groups of 8 warps, group g = image slot g ==
+        // warp w reads TMEM lanes 32 (w % 4)..+31; in a group, warps w and w+4 share a lane quarter:
+        // conv1 epilogue: half 0 takes hidden channels 0-31, half 1 hidden 32-63 (both tiles);
+        // conv2 epilogue: half h takes M-tile h (all 6 outputs of its pixel rows)
+        const int g = (warp - 2) >> 3, ew = (warp - 2) & 7, quarter = warp & 3, half = ew >> 2, et = ew * 32 + lane;
         const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
         const int x = lane & 15;
-        uint32_t kb = 0;
-        // X views of slot s at row p, this half's 4 channel slots (8 bytes of the 16-byte row)
-        auto write_x = [&](int s, int p, const float (&v)[4]) {
-            uint8_t* xs = xplanes(s);
-            uint2 hi, lo;
+        const uint32_t bar_id = 1 + g;
+        auto gsync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "n"(kEpi) : "memory"); };
+        uint8_t* xs = xplanes(g);
+        float* st = sstate(g);
+        float* xch0 = reinterpret_cast<float*>(sxch(g));
+        // X views at row p: 8 channels (one 16-byte row per view and precision plane)
+        auto write_x = [&](int p, const float (&v)[8]) {
+            uint4 hi, lo;
             if (PM) {
                 ts_split(v[0], v[1], hi.x, lo.x);
                 ts_split(v[2], v[3], hi.y, lo.y);
+                ts_split(v[4], v[5], hi.z, lo.z);
+                ts_split(v[6], v[7], hi.w, lo.w);
             } else {
-                hi = make_uint2(ts_bf16x2(v[0], v[1]), ts_bf16x2(v[2], v[3]));
+                hi = make_uint4(ts_bf16x2(v[0], v[1]), ts_bf16x2(v[2], v[3]), ts_bf16x2(v[4], v[5]), ts_bf16x2(v[6], v[7]));
                 lo = hi;
             }
-            const size_t off = (size_t)(G + p) * 16 + half * 8;
+            const int xx = p & 15;
+            const size_t off = (size_t)(G + p) * 16;
             auto put = [&](int view, int row_delta) {
-                *reinterpret_cast<uint2*>(xs + (size_t)view * PB + off + row_delta * 16) = hi;
-                if (PM) *reinterpret_cast<uint2*>(xs + (size_t)(3 + view) * PB + off + row_delta * 16) = lo;
+                *reinterpret_cast<uint4*>(xs + (size_t)view * PB + off + row_delta * 16) = hi;
+                if (PM) *reinterpret_cast<uint4*>(xs + (size_t)(3 + view) * PB + off + row_delta * 16) = lo;
             };
-            put(1, 0);                  // Xc[p]
-            if (x < W - 1) put(0, 1);   // Xl[p+1] = X[p]
-            if (x > 0) put(2, -1);      // Xr[p-1] = X[p]
+            put(1, 0);                   // Xc[p]
+            if (xx < W - 1) put(0, 1);   // Xl[p+1] = X[p]
+            if (xx > 0) put(2, -1);      // Xr[p-1] = X[p]
         };
         auto in_half = [&](int t) { return ((a.first_orient + t) & 1) == 0 ? 0 : c; };
-        for (int pi = 0;; pi++) {
-            const int64_t b0 = bq_read(2 * pi);
-            mbar_arrive(&bqe[(2 * pi) & 3]);
-            if (b0 >= nbatch) break;
-            const int64_t b1 = bq_read(2 * pi + 1);
-            mbar_arrive(&bqe[(2 * pi + 1) & 3]);
-            const int ns = b1 < nbatch ? 2 : 1;
-            // ---- batch state -> shared memory, first block's input half -> X views
-            for (int s = 0; s < ns; s++) {
-                const float4* src = reinterpret_cast<const float4*>(a.state + (s ? b1 : b0) * (int64_t)C * HW);
-                float4* dst = reinterpret_cast<float4*>(sstate(s));
-                for (int i = et; i < C * HW / 4; i += kEpi) dst[i] = __ldcg(src + i);
-            }
-            asm volatile("bar.sync 1, %0;" ::"n"(kEpi) : "memory");
+        uint32_t kb = 0;
+        for (int i = 0;; i++) {
+            const int qe = 2 * i + g;
+            const int64_t b = bq_read(qe);
+            mbar_arrive(&bqe[qe & 3]);
+            if (b >= nbatch) break;
+            float* gst = a.state + b * (int64_t)C * HW;
+            // ---- image state -> shared memory, first block's input half -> X views
             {
-                const int t0 = a.inverse ? a.nb - 1 : 0, ioff = in_half(t0) + 4 * half;
-                for (int s = 0; s < ns; s++) {
-                    const float* st = sstate(s);
+                const float4* src = reinterpret_cast<const float4*>(gst);
+                float4* dst = reinterpret_cast<float4*>(st);
+                for (int q = et; q < C * HW / 4; q += kEpi) dst[q] = __ldcg(src + q);
+            }
+            gsync();
+            {
+                const int ioff = in_half(a.inverse ? a.nb - 1 : 0);
+                const int p = half * 128 + quarter * 32 + lane;
+                float v[8];
 #pragma unroll
-                    for (int t = 0; t < 2; t++) {
-                        const int p = t * 128 + quarter * 32 + lane;
-                        float v[4];
-                        if (half == 0) {
-#pragma unroll
-                            for (int o = 0; o < 4; o++) v[o] = st[(ioff + o) * HW + p];
-                        } else {
-                            v[0] = st[ioff * HW + p];
-                            v[1] = st[(ioff + 1) * HW + p];
-                            v[2] = 1.f;
-                            v[3] = 0.f;
-                        }
-                        write_x(s, p, v);
-                    }
-                    fence_proxy_async();
-                    mbar_arrive(&x_rdy[s]);
-                }
+                for (int o = 0; o < 8; o++) v[o] = o < c ? st[(ioff + o) * HW + p] : (o == c ? 1.f : 0.f);
+                write_x(p, v);
+                fence_proxy_async();
+                mbar_arrive(&x_rdy[g]);
             }
             for (int tt = 0; tt < a.nb; tt++, kb++) {
                 const uint32_t par = kb & 1;
@@ -338,142 +335,123 @@ __global__ void __launch_bounds__(ts::kThreads, 1) k_stage_ts(TsArgs a) {
                 const bool write_next = tt + 1 < a.nb;
                 // ---- conv1 epilogue: acc1 -> ReLU -> fp16 hi / lo (or bf16) words back into TMEM,
                 // into the same columns this thread read (half h: columns [32h, 32h+32))
-                for (int s = 0; s < ns; s++) {
 #pragma unroll
-                    for (int tl = 0; tl < 2; tl++) {
-                        mbar_wait(&a1t[s * 2 + tl], par);
-                        fence_after();
-                        const uint32_t col = tmem + lane_addr + (uint32_t)(s * 256 + tl * 128 + 32 * half);
-                        float v[32];
-                        {
-                            float (&v0)[16] = *reinterpret_cast<float (*)[16]>(&v[0]);
-                            float (&v1)[16] = *reinterpret_cast<float (*)[16]>(&v[16]);
-                            tmem_ld16(col, v0);
-                            tmem_ld16(col + 16, v1);
-                        }
-                        if (PM == 2) {   // stacked: hi(x) W_lo columns at +64
-                            float w[32];
-                            float (&w0)[16] = *reinterpret_cast<float (*)[16]>(&w[0]);
-                            float (&w1)[16] = *reinterpret_cast<float (*)[16]>(&w[16]);
-                            tmem_ld16(col + 64, w0);
-                            tmem_ld16(col + 80, w1);
-                            tmem_wait_ld();
-#pragma unroll
-                            for (int e = 0; e < 32; e++) v[e] += w[e];
-                        } else {
-                            tmem_wait_ld();
-                        }
-                        uint32_t hw[16], lw[16];
-#pragma unroll
-                        for (int e = 0; e < 16; e++) {
-                            const float p0 = fmaxf(v[2 * e], 0.f), p1 = fmaxf(v[2 * e + 1], 0.f);
-                            if (PM) ts_split(p0, p1, hw[e], lw[e]);
-                            else hw[e] = ts_bf16x2(p0, p1);
-                        }
-                        tmem_st16u(col, hw);
-                        if (PM) tmem_st16u(col + 16, lw);
-                        tmem_wait_st();
-                        fence_before();
-                        mbar_arrive(&hdt[s * 2 + tl]);
+                for (int tl = 0; tl < 2; tl++) {
+                    mbar_wait(&a1t[g * 2 + tl], par);
+                    fence_after();
+                    const uint32_t col = tmem + lane_addr + (uint32_t)(g * 256 + tl * 128 + 32 * half);
+                    float v[32];
+                    {
+                        float (&v0)[16] = *reinterpret_cast<float (*)[16]>(&v[0]);
+                        float (&v1)[16] = *reinterpret_cast<float (*)[16]>(&v[16]);
+                        tmem_ld16(col, v0);
+                        tmem_ld16(col + 16, v1);
                     }
+                    if (PM == 2) {   // stacked: hi(x) W_lo columns at +64
+                        float w[32];
+                        float (&w0)[16] = *reinterpret_cast<float (*)[16]>(&w[0]);
+                        float (&w1)[16] = *reinterpret_cast<float (*)[16]>(&w[16]);
+                        tmem_ld16(col + 64, w0);
+                        tmem_ld16(col + 80, w1);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int e = 0; e < 32; e++) v[e] += w[e];
+                    } else {
+                        tmem_wait_ld();
+                    }
+                    uint32_t hw[16], lw[16];
+#pragma unroll
+                    for (int e = 0; e < 16; e++) {
+                        const float p0 = fmaxf(v[2 * e], 0.f), p1 = fmaxf(v[2 * e + 1], 0.f);
+                        if (PM) ts_split(p0, p1, hw[e], lw[e]);
+                        else hw[e] = ts_bf16x2(p0, p1);
+                    }
+                    tmem_st16u(col, hw);
+                    if (PM) tmem_st16u(col + 16, lw);
+                    tmem_wait_st();
+                    fence_before();
+                    mbar_arrive(&hdt[g * 2 + tl]);
                 }
-                // ---- conv2 epilogue: col2im of the 9 tap groups, s_out (+|-)= F + b2
+                // ---- conv2 epilogue (tile `half`): col2im of the 9 tap groups, s_out (+|-)= F + b2
                 const float* b2 = a.bias + (int64_t)t * a.bias_stride + M;
-                for (int s = 0; s < ns; s++) {
-                    float mid[2][4];
-                    float4* xch = sxch(s);
+                const int p = half * 128 + quarter * 32 + lane, y = p >> 4;
+                float* xch = xch0 + (par ? HW * 8 : 0);   // double-buffered by block parity
+                float mid[c];
+                {
+                    mbar_wait(&a2t[g * 2 + half], par);
+                    fence_after();
+                    const uint32_t col = tmem + lane_addr + (uint32_t)(g * 256 + half * 128 + 64);
+                    float z[9][c];   // column tap * 6 + o
+                    {
+                        float za[16], zb[16], zc[16], zd[4], ze[2];
+                        tmem_ld16(col, za);
+                        tmem_ld16(col + 16, zb);
+                        tmem_ld16(col + 32, zc);
+                        tmem_ld4(col + 48, zd);
+                        tmem_ld2(col + 52, ze);
+                        tmem_wait_ld();
 #pragma unroll
-                    for (int tl = 0; tl < 2; tl++) {
-                        mbar_wait(&a2t[s * 2 + tl], par);
-                        fence_after();
-                        const uint32_t col = tmem + lane_addr + (uint32_t)(s * 256 + tl * 128 + 64 + 36 * half);
-                        float z[9][4];
-                        if (half == 0) {   // column 4 tap + o
-                            float za[16], zb[16], zc[4];
-                            tmem_ld16(col, za);
-                            tmem_ld16(col + 16, zb);
-                            tmem_ld4(col + 32, zc);
-                            tmem_wait_ld();
-#pragma unroll
-                            for (int q = 0; q < 36; q++) z[q / 4][q % 4] = q < 16 ? za[q] : (q < 32 ? zb[q - 16] : zc[q - 32]);
-                        } else {           // column 36 + 2 tap + (o - 4)
-                            float za[16], zb[2];
-                            tmem_ld16(col, za);
-                            tmem_ld2(col + 16, zb);
-                            tmem_wait_ld();
-#pragma unroll
-                            for (int q = 0; q < 18; q++) z[q / 2][q % 2] = q < 16 ? za[q] : zb[q - 16];
-#pragma unroll
-                            for (int q = 0; q < 9; q++) z[q][2] = z[q][3] = 0.f;
-                        }
-                        // horizontal: H_u[r] = Z_{u,-1}[r-1] + Z_{u,0}[r] + Z_{u,+1}[r+1] (masked at x = 0 / W-1)
-                        float hsum[3][4];
-#pragma unroll
-                        for (int u = 0; u < 3; u++)
-#pragma unroll
-                            for (int o = 0; o < 4; o++) {
-                                const float l = __shfl_up_sync(0xffffffffu, z[u * 3 + 0][o], 1);
-                                const float r = __shfl_down_sync(0xffffffffu, z[u * 3 + 2][o], 1);
-                                hsum[u][o] = z[u * 3 + 1][o] + (x > 0 ? l : 0.f) + (x < W - 1 ? r : 0.f);
-                            }
-                        // vertical: out[p] = H_-1[p-W] + H_0[p] + H_+1[p+W].  Lanes l < 16 (even y) take
-                        // H_+1 of lane l+16 and publish their H_+1 for the warp row above; lanes >= 16
-                        // take H_-1 of lane l-16 and publish their H_-1 for the warp row below.
-                        const int p = tl * 128 + quarter * 32 + lane;
-                        float pub[4];
-#pragma unroll
-                        for (int o = 0; o < 4; o++) {
-                            const float send = lane < 16 ? hsum[0][o] : hsum[2][o];
-                            const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
-                            mid[tl][o] = hsum[1][o] + recv;
-                            pub[o] = lane < 16 ? hsum[2][o] : hsum[0][o];
-                        }
-                        xch[half * HW + p] = make_float4(pub[0], pub[1], pub[2], pub[3]);
+                        for (int q = 0; q < 54; q++)
+                            z[q / c][q % c] = q < 16 ? za[q] : q < 32 ? zb[q - 16] : q < 48 ? zc[q - 32] : q < 52 ? zd[q - 48] : ze[q - 52];
                     }
                     fence_before();
-                    asm volatile("bar.sync 1, %0;" ::"n"(kEpi) : "memory");
-                    float* st = sstate(s);
-                    float bb[4];
+                    // horizontal: H_u[r] = Z_{u,-1}[r-1] + Z_{u,0}[r] + Z_{u,+1}[r+1] (masked at x = 0 / W-1)
+                    float hsum[3][c];
 #pragma unroll
-                    for (int o = 0; o < 4; o++) bb[o] = (half == 0 || o < 2) ? __ldg(b2 + 4 * half + o) : 0.f;
+                    for (int u = 0; u < 3; u++)
 #pragma unroll
-                    for (int tl = 0; tl < 2; tl++) {
-                        const int p = tl * 128 + quarter * 32 + lane, y = p >> 4;
-                        float4 oth = make_float4(0.f, 0.f, 0.f, 0.f);
-                        if (lane < 16 && y > 0) oth = xch[half * HW + p - W];
-                        if (lane >= 16 && y < H - 1) oth = xch[half * HW + p + W];
-                        const float ov[4] = {oth.x, oth.y, oth.z, oth.w};
-                        float nv[4];
-#pragma unroll
-                        for (int o = 0; o < 4; o++) {
-                            const int ch = 4 * half + o;
-                            if (ch < c) {
-                                const float f = mid[tl][o] + ov[o] + bb[o];
-                                float* sp = st + (out_off + ch) * HW + p;
-                                const float old = *sp;
-                                nv[o] = a.inverse ? old - f : old + f;
-                                *sp = nv[o];
-                            } else {
-                                nv[o] = ch == c ? 1.f : 0.f;   // constant-1 channel (folded conv1 bias)
-                            }
+                        for (int o = 0; o < c; o++) {
+                            const float l = __shfl_up_sync(0xffffffffu, z[u * 3 + 0][o], 1);
+                            const float r = __shfl_down_sync(0xffffffffu, z[u * 3 + 2][o], 1);
+                            hsum[u][o] = z[u * 3 + 1][o] + (x > 0 ? l : 0.f) + (x < W - 1 ? r : 0.f);
                         }
-                        if (write_next) write_x(s, p, nv);
+                    // vertical: out[p] = H_-1[p-W] + H_0[p] + H_+1[p+W].  Lanes l < 16 (even y) take
+                    // H_+1 of lane l+16 and publish their H_+1 for the warp row above; lanes >= 16
+                    // take H_-1 of lane l-16 and publish their H_-1 for the warp row below.
+                    float pub[8];
+#pragma unroll
+                    for (int o = 0; o < c; o++) {
+                        const float send = lane < 16 ? hsum[0][o] : hsum[2][o];
+                        const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
+                        mid[o] = hsum[1][o] + recv + __ldg(b2 + o);
+                        pub[o] = lane < 16 ? hsum[2][o] : hsum[0][o];
                     }
+                    pub[6] = pub[7] = 0.f;
+                    reinterpret_cast<float4*>(xch)[2 * p] = make_float4(pub[0], pub[1], pub[2], pub[3]);
+                    reinterpret_cast<float4*>(xch)[2 * p + 1] = make_float4(pub[4], pub[5], pub[6], pub[7]);
+                }
+                gsync();
+                {
+                    const int q = lane < 16 ? (y > 0 ? p - W : -1) : (y < H - 1 ? p + W : -1);
+                    float4 o0 = make_float4(0.f, 0.f, 0.f, 0.f), o1 = o0;
+                    if (q >= 0) { o0 = reinterpret_cast<const float4*>(xch)[2 * q]; o1 = reinterpret_cast<const float4*>(xch)[2 * q + 1]; }
+                    const float ov[6] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y};
+                    float nv[8];
+#pragma unroll
+                    for (int o = 0; o < c; o++) {
+                        const float f = mid[o] + ov[o];
+                        float* sp = st + (out_off + o) * HW + p;
+                        const float old = *sp;
+                        nv[o] = a.inverse ? old - f : old + f;
+                        *sp = nv[o];
+                    }
+                    nv[6] = 1.f;   // constant-1 channel (folded conv1 bias)
+                    nv[7] = 0.f;
                     if (write_next) {
+                        write_x(p, nv);
                         fence_proxy_async();
-                        mbar_arrive(&x_rdy[s]);
+                        mbar_arrive(&x_rdy[g]);
                     }
                 }
             }
             // ---- state back to global memory
-            asm volatile("bar.sync 1, %0;" ::"n"(kEpi) : "memory");
-            for (int s = 0; s < ns; s++) {
-                float4* dst = reinterpret_cast<float4*>(a.state + (s ? b1 : b0) * (int64_t)C * HW);
-                const float4* src = reinterpret_cast<const float4*>(sstate(s));
-                for (int i = et; i < C * HW / 4; i += kEpi) __stcg(dst + i, src[i]);
+            gsync();
+            {
+                float4* dst = reinterpret_cast<float4*>(gst);
+                const float4* src = reinterpret_cast<const float4*>(st);
+                for (int q = et; q < C * HW / 4; q += kEpi) __stcg(dst + q, src[q]);
             }
-            asm volatile("bar.sync 1, %0;" ::"n"(kEpi) : "memory");
-            if (ns == 1) break;
+            gsync();
         }
     }
     fence_before();
@@ -490,8 +468,7 @@ int stage_ts_n2() { return ts::N2; }
 
 // conv2 column n of the TS layout -> (tap, output channel), or tap = -1 for padding columns
 void stage_ts_col(int n, int& tap, int& o) {
-    if (n < 36) { tap = n / 4; o = n % 4; return; }
-    if (n < 54) { tap = (n - 36) / 2; o = 4 + (n - 36) % 2; return; }
+    if (n < 9 * ts::c) { tap = n / ts::c; o = n % ts::c; return; }
     tap = -1; o = -1;
 }
 
