@@ -151,6 +151,7 @@ int64_t stage_ts_block_bytes(int pm);
 int stage_ts_n2();
 void stage_ts_col(int n, int& tap, int& o);   // conv2 column -> (tap, output channel), tap -1 = padding
 cudaError_t stage_ts_prepare();
-cudaError_t launch_stage_ts(const TsArgs& a, int pm, cudaStream_t st);
+bool stage_ts_stacked(int pm);   // f16x3: stacked conv1 (CI_TS_UNSTK=1: three N = 64 MMAs per k-step)
+cudaError_t launch_stage_ts(const TsArgs& a, int pm, int stk, cudaStream_t st);
 
 }  // namespace ci

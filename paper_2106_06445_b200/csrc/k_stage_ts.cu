@@ -50,11 +50,11 @@ constexpr int PB = RT * 16;                 // plane bytes
 constexpr int N1 = 64, N2 = 64;             // conv1 / conv2 MMA widths
 constexpr int K1 = 5, K2 = 4;               // k-steps
 constexpr int NSLOT = 4, SLOTB = 20480;     // weight ring
-constexpr int ST_BYTES = C * HW * 4;        // fp32 state of one image
+constexpr int ST_BYTES = C * HW * 4;        // fp32 state of one image (two buffers per slot: cp.async prefetch)
 constexpr int XCH_BYTES = 2 * HW * 32;      // vertical exchange [block parity][row][8] fp32
 __host__ __device__ constexpr int kstep(int N, int pm) { return N * 32 * (pm == 2 ? 2 : 1); }
 __host__ __device__ constexpr int nplanes(int pm) { return pm ? 6 : 3; }
-__host__ __device__ constexpr int slot_bytes(int pm) { return nplanes(pm) * PB + ST_BYTES + XCH_BYTES; }
+__host__ __device__ constexpr int slot_bytes(int pm) { return nplanes(pm) * PB + 2 * ST_BYTES + XCH_BYTES; }
 __host__ __device__ constexpr int smem_bytes(int pm) { return NSLOT * SLOTB + 2 * slot_bytes(pm) + 512; }
 }  // namespace ts
 
@@ -80,11 +80,37 @@ __device__ __forceinline__ void tmem_st16u(uint32_t taddr, const uint32_t (&v)[1
         : "memory");
 }
 
+// f32x2 arithmetic (sm_100 FADD2 / FFMA2): two lanes of a float2 per instruction
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+    float2 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(*reinterpret_cast<unsigned long long*>(&r))
+        : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
+    return r;
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+    float2 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(*reinterpret_cast<unsigned long long*>(&r))
+        : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
+    return r;
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+    float2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(*reinterpret_cast<unsigned long long*>(&r))
+        : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+          "l"(*reinterpret_cast<unsigned long long*>(&c)));
+    return r;
+}
+
+__device__ __forceinline__ void tmem_st8u(uint32_t taddr, const uint32_t (&v)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
+                 "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
 // two fp32 -> packed 16-bit pair (a in the low half): fp16 hi / lo split, or bf16
 __device__ __forceinline__ void ts_split(float a, float b, uint32_t& hi, uint32_t& lo) {
     asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(b), "f"(a));
-    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&hi));
-    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(b - f.y), "f"(a - f.x));
+    const float2 d = sub2(make_float2(a, b), __half22float2(*reinterpret_cast<const __half2*>(&hi)));
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(d.y), "f"(d.x));
 }
 __device__ __forceinline__ uint32_t ts_bf16x2(float a, float b) {
     uint32_t r;
@@ -92,7 +118,8 @@ __device__ __forceinline__ uint32_t ts_bf16x2(float a, float b) {
     return r;
 }
 
-template <int PM>
+// PM: precision; STK (PM == 2 only): stacked conv1, hi(x) [W_hi | W_lo] as one 2N-wide MMA
+template <int PM, int STK>
 __global__ void __launch_bounds__(ts::kThreads, 1) k_stage_ts(TsArgs a) {
     using namespace ts;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -102,7 +129,7 @@ __global__ void __launch_bounds__(ts::kThreads, 1) k_stage_ts(TsArgs a) {
     auto xplanes = [&](int s) { return slots + (size_t)s * slot_bytes(PM); };
     auto sstate = [&](int s) { return reinterpret_cast<float*>(slots + (size_t)s * slot_bytes(PM) + nplanes(PM) * PB); };
     auto sxch = [&](int s) {
-        return reinterpret_cast<float4*>(slots + (size_t)s * slot_bytes(PM) + nplanes(PM) * PB + ST_BYTES);
+        return reinterpret_cast<float4*>(slots + (size_t)s * slot_bytes(PM) + nplanes(PM) * PB + 2 * ST_BYTES);
     };
     uint64_t* bars = reinterpret_cast<uint64_t*>(slots + 2 * slot_bytes(PM));
     uint64_t* full = bars;            // [4]
@@ -190,11 +217,11 @@ __global__ void __launch_bounds__(ts::kThreads, 1) k_stage_ts(TsArgs a) {
             int slot = 0;
             uint32_t phase = 0, kb = 0;
             const uint32_t rb = smem_u32(ring);
-            const uint32_t id1w = idesc_of(128, PM == 2 ? 2 * N1 : N1, PM != 0);
+            const uint32_t id1w = idesc_of(128, STK ? 2 * N1 : N1, PM != 0);
             const uint32_t id1 = idesc_of(128, N1, PM != 0);
             const uint32_t id2 = idesc_of(128, N2, PM != 0);
             constexpr uint32_t LOA = (uint32_t)(3 * PB / 16);     // lo views, descriptor units
-            constexpr uint32_t B1LBO = (uint32_t)((PM == 2 ? 2 : 1) * N1 * 16);
+            constexpr uint32_t B1LBO = (uint32_t)((STK ? 2 : 1) * N1 * 16);
             for (int pi = 0;; pi++) {
                 const int64_t b0 = bq_read(2 * pi);
                 mbar_arrive(&bqe[(2 * pi) & 3]);
@@ -225,9 +252,13 @@ __global__ void __launch_bounds__(ts::kThreads, 1) k_stage_ts(TsArgs a) {
                                 const uint64_t ad = smem_desc(base + (uint32_t)row * 16u, lbo, 128);
                                 const uint64_t bd = smem_desc(w1 + (uint32_t)(ks * kstep(N1, PM)), B1LBO, 128);
                                 const uint32_t acc = ks > 0 ? 1u : 0u;
-                                if (PM == 2) {   // hi(x) [W_hi | W_lo] (2N wide), then lo(x) W_hi
+                                if (STK) {   // hi(x) [W_hi | W_lo] (2N wide), then lo(x) W_hi
                                     mma_bf16(d, ad, bd, id1w, acc);
                                     mma_bf16(d, ad + LOA, bd, id1, 1u);
+                                } else if (PM == 2) {   // hi(x) W_hi + lo(x) W_hi + hi(x) W_lo
+                                    mma_bf16(d, ad, bd, id1, acc);
+                                    mma_bf16(d, ad + LOA, bd, id1, 1u);
+                                    mma_bf16(d, ad, bd + (uint64_t)(N1 * 32 / 16), id1, 1u);
                                 } else {
                                     mma_bf16(d, ad, bd, id1, acc);
                                     if (PM == 1) mma_bf16(d, ad + LOA, bd, id1, 1u);
@@ -250,12 +281,12 @@ __global__ void __launch_bounds__(ts::kThreads, 1) k_stage_ts(TsArgs a) {
                             const uint32_t tb = tmem + (uint32_t)(s * 256 + t * 128);
 #pragma unroll
                             for (int ks = 0; ks < K2; ks++) {
-                                // hidden channels 16 ks..16 ks+15: warp half ks/2's words 8 (ks%2)..+7
-                                const uint32_t ahi = tb + (uint32_t)(32 * (ks >> 1) + 8 * (ks & 1));
+                                // hidden channels 16 ks..16 ks+15: hi words at column 16 ks, lo at 16 ks + 8
+                                const uint32_t ahi = tb + (uint32_t)(16 * ks);
                                 const uint64_t bd = smem_desc(w2 + (uint32_t)(ks * kstep(N2, PM)), N2 * 16, 128);
                                 const uint32_t acc = ks > 0 ? 1u : 0u;
                                 mma_ts(tb + 64, ahi, bd, id2, acc);
-                                if (PM >= 1) mma_ts(tb + 64, ahi + 16, bd, id2, 1u);                       // lo(h) W
+                                if (PM >= 1) mma_ts(tb + 64, ahi + 8, bd, id2, 1u);                        // lo(h) W
                                 if (PM == 2) mma_ts(tb + 64, ahi, bd + (uint64_t)(N2 * 32 / 16), id2, 1u);  // hi(h) W_lo
                             }
                             commit(&a2t[s * 2 + t]);
@@ -279,9 +310,11 @@ __global__ void __launch_bounds__(ts::kThreads, 1) k_stage_ts(TsArgs a) {
         const uint32_t bar_id = 1 + g;
         auto gsync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "n"(kEpi) : "memory"); };
         uint8_t* xs = xplanes(g);
-        float* st = sstate(g);
         float* xch0 = reinterpret_cast<float*>(sxch(g));
-        // X views at row p: 8 channels (one 16-byte row per view and precision plane)
+        const float2 ml = make_float2(x > 0 ? 1.f : 0.f, x > 0 ? 1.f : 0.f);          // left tap inside the image
+        const float2 mr = make_float2(x < W - 1 ? 1.f : 0.f, x < W - 1 ? 1.f : 0.f);  // right tap inside the image
+        // X views at row p: 8 channels (one 16-byte row per view and precision plane).  Branch-free:
+        // the Xl / Xr rows a border pixel would feed are written as zeros (they must stay zero).
         auto write_x = [&](int p, const float (&v)[8]) {
             uint4 hi, lo;
             if (PM) {
@@ -294,31 +327,40 @@ __global__ void __launch_bounds__(ts::kThreads, 1) k_stage_ts(TsArgs a) {
                 lo = hi;
             }
             const int xx = p & 15;
+            const uint4 z4 = make_uint4(0, 0, 0, 0);
             const size_t off = (size_t)(G + p) * 16;
-            auto put = [&](int view, int row_delta) {
-                *reinterpret_cast<uint4*>(xs + (size_t)view * PB + off + row_delta * 16) = hi;
-                if (PM) *reinterpret_cast<uint4*>(xs + (size_t)(3 + view) * PB + off + row_delta * 16) = lo;
+            auto put = [&](int view, int row_delta, bool keep) {
+                *reinterpret_cast<uint4*>(xs + (size_t)view * PB + off + row_delta * 16) = keep ? hi : z4;
+                if (PM) *reinterpret_cast<uint4*>(xs + (size_t)(3 + view) * PB + off + row_delta * 16) = keep ? lo : z4;
             };
-            put(1, 0);                   // Xc[p]
-            if (xx < W - 1) put(0, 1);   // Xl[p+1] = X[p]
-            if (xx > 0) put(2, -1);      // Xr[p-1] = X[p]
+            put(1, 0, true);         // Xc[p]
+            put(0, 1, xx < W - 1);   // Xl[p+1] = X[p]
+            put(2, -1, xx > 0);      // Xr[p-1] = X[p]
+        };
+        // image state -> shared-memory buffer (16-B cp.async, completes on wait_all)
+        auto fetch_state = [&](int64_t bb, float* dst) {
+            const float* src = a.state + bb * (int64_t)C * HW;
+            for (int q = et; q < C * HW / 4; q += kEpi)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst + 4 * q)), "l"(src + 4 * q)
+                             : "memory");
+            asm volatile("cp.async.commit_group;" ::: "memory");
         };
         auto in_half = [&](int t) { return ((a.first_orient + t) & 1) == 0 ? 0 : c; };
         uint32_t kb = 0;
+        bool prefetched = false;
         for (int i = 0;; i++) {
             const int qe = 2 * i + g;
             const int64_t b = bq_read(qe);
             mbar_arrive(&bqe[qe & 3]);
             if (b >= nbatch) break;
             float* gst = a.state + b * (int64_t)C * HW;
-            // ---- image state -> shared memory, first block's input half -> X views
-            {
-                const float4* src = reinterpret_cast<const float4*>(gst);
-                float4* dst = reinterpret_cast<float4*>(st);
-                for (int q = et; q < C * HW / 4; q += kEpi) dst[q] = __ldcg(src + q);
-            }
+            float* st = sstate(g) + (i & 1) * (C * HW);
+            // ---- image state -> shared memory (prefetched during the previous image's last blocks)
+            if (!prefetched) fetch_state(b, st);
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            prefetched = false;
             gsync();
-            {
+            {   // first block's input half -> X views
                 const int ioff = in_half(a.inverse ? a.nb - 1 : 0);
                 const int p = half * 128 + quarter * 32 + lane;
                 float v[8];
@@ -333,6 +375,19 @@ __global__ void __launch_bounds__(ts::kThreads, 1) k_stage_ts(TsArgs a) {
                 const int t = a.inverse ? a.nb - 1 - tt : tt;
                 const int out_off = c - in_half(t);
                 const bool write_next = tt + 1 < a.nb;
+                float bb[c];   // conv2 bias of this block (loads in flight during the conv1 epilogue)
+                {
+                    const float* b2 = a.bias + (int64_t)t * a.bias_stride + M;
+#pragma unroll
+                    for (int o = 0; o < c; o++) bb[o] = __ldg(b2 + o);
+                }
+                if (tt == a.nb - 2 || (a.nb == 1 && tt == 0)) {   // prefetch the group's next image state
+                    const int64_t bn = bq_read(qe + 2);
+                    if (bn < nbatch) {
+                        fetch_state(bn, sstate(g) + ((i + 1) & 1) * (C * HW));
+                        prefetched = true;
+                    }
+                }
                 // ---- conv1 epilogue: acc1 -> ReLU -> fp16 hi / lo (or bf16) words back into TMEM,
                 // into the same columns this thread read (half h: columns [32h, 32h+32))
 #pragma unroll
@@ -340,48 +395,49 @@ __global__ void __launch_bounds__(ts::kThreads, 1) k_stage_ts(TsArgs a) {
                     mbar_wait(&a1t[g * 2 + tl], par);
                     fence_after();
                     const uint32_t col = tmem + lane_addr + (uint32_t)(g * 256 + tl * 128 + 32 * half);
-                    float v[32];
-                    {
-                        float (&v0)[16] = *reinterpret_cast<float (*)[16]>(&v[0]);
-                        float (&v1)[16] = *reinterpret_cast<float (*)[16]>(&v[16]);
-                        tmem_ld16(col, v0);
-                        tmem_ld16(col + 16, v1);
-                    }
-                    if (PM == 2) {   // stacked: hi(x) W_lo columns at +64
-                        float w[32];
-                        float (&w0)[16] = *reinterpret_cast<float (*)[16]>(&w[0]);
-                        float (&w1)[16] = *reinterpret_cast<float (*)[16]>(&w[16]);
-                        tmem_ld16(col + 64, w0);
-                        tmem_ld16(col + 80, w1);
-                        tmem_wait_ld();
+                    // two rounds of 16 hidden channels (register pressure: 18 warps leave 96 per thread)
 #pragma unroll
-                        for (int e = 0; e < 32; e++) v[e] += w[e];
-                    } else {
-                        tmem_wait_ld();
-                    }
-                    uint32_t hw[16], lw[16];
+                    for (int rd = 0; rd < 2; rd++) {
+                        float v[16];
+                        tmem_ld16(col + 16 * rd, v);
+                        if (STK) {   // stacked: hi(x) W_lo columns at +64
+                            float w[16];
+                            tmem_ld16(col + 64 + 16 * rd, w);
+                            tmem_wait_ld();
 #pragma unroll
-                    for (int e = 0; e < 16; e++) {
-                        const float p0 = fmaxf(v[2 * e], 0.f), p1 = fmaxf(v[2 * e + 1], 0.f);
-                        if (PM) ts_split(p0, p1, hw[e], lw[e]);
-                        else hw[e] = ts_bf16x2(p0, p1);
+                            for (int e = 0; e < 8; e++) {
+                                const float2 r = add2(make_float2(v[2 * e], v[2 * e + 1]), make_float2(w[2 * e], w[2 * e + 1]));
+                                v[2 * e] = r.x;
+                                v[2 * e + 1] = r.y;
+                            }
+                        } else {
+                            tmem_wait_ld();
+                        }
+                        uint32_t hw[8], lw[8];
+#pragma unroll
+                        for (int e = 0; e < 8; e++) {
+                            const float p0 = fmaxf(v[2 * e], 0.f), p1 = fmaxf(v[2 * e + 1], 0.f);
+                            if (PM) ts_split(p0, p1, hw[e], lw[e]);
+                            else hw[e] = ts_bf16x2(p0, p1);
+                        }
+                        // hidden channels 16 k..16 k+15 (k = 2 half + rd): hi words at column 16 k, lo
+                        // words at 16 k + 8 -- only columns this round has already read
+                        tmem_st8u(col + 16 * rd, hw);
+                        if (PM) tmem_st8u(col + 16 * rd + 8, lw);
                     }
-                    tmem_st16u(col, hw);
-                    if (PM) tmem_st16u(col + 16, lw);
                     tmem_wait_st();
                     fence_before();
                     mbar_arrive(&hdt[g * 2 + tl]);
                 }
                 // ---- conv2 epilogue (tile `half`): col2im of the 9 tap groups, s_out (+|-)= F + b2
-                const float* b2 = a.bias + (int64_t)t * a.bias_stride + M;
                 const int p = half * 128 + quarter * 32 + lane, y = p >> 4;
                 float* xch = xch0 + (par ? HW * 8 : 0);   // double-buffered by block parity
-                float mid[c];
+                float2 mid[c / 2];
                 {
                     mbar_wait(&a2t[g * 2 + half], par);
                     fence_after();
                     const uint32_t col = tmem + lane_addr + (uint32_t)(g * 256 + half * 128 + 64);
-                    float z[9][c];   // column tap * 6 + o
+                    float2 z[9][c / 2];   // column tap * 6 + o
                     {
                         float za[16], zb[16], zc[16], zd[4], ze[2];
                         tmem_ld16(col, za);
@@ -390,50 +446,57 @@ __global__ void __launch_bounds__(ts::kThreads, 1) k_stage_ts(TsArgs a) {
                         tmem_ld4(col + 48, zd);
                         tmem_ld2(col + 52, ze);
                         tmem_wait_ld();
+                        auto zq = [&](int q) -> float {
+                            return q < 16 ? za[q] : q < 32 ? zb[q - 16] : q < 48 ? zc[q - 32] : q < 52 ? zd[q - 48] : ze[q - 52];
+                        };
 #pragma unroll
-                        for (int q = 0; q < 54; q++)
-                            z[q / c][q % c] = q < 16 ? za[q] : q < 32 ? zb[q - 16] : q < 48 ? zc[q - 32] : q < 52 ? zd[q - 48] : ze[q - 52];
+                        for (int q = 0; q < 27; q++) z[q / 3][q % 3] = make_float2(zq(2 * q), zq(2 * q + 1));
                     }
                     fence_before();
                     // horizontal: H_u[r] = Z_{u,-1}[r-1] + Z_{u,0}[r] + Z_{u,+1}[r+1] (masked at x = 0 / W-1)
-                    float hsum[3][c];
+                    float2 hsum[3][c / 2];
 #pragma unroll
                     for (int u = 0; u < 3; u++)
 #pragma unroll
-                        for (int o = 0; o < c; o++) {
-                            const float l = __shfl_up_sync(0xffffffffu, z[u * 3 + 0][o], 1);
-                            const float r = __shfl_down_sync(0xffffffffu, z[u * 3 + 2][o], 1);
-                            hsum[u][o] = z[u * 3 + 1][o] + (x > 0 ? l : 0.f) + (x < W - 1 ? r : 0.f);
+                        for (int o = 0; o < c / 2; o++) {
+                            const float2 zl = z[u * 3 + 0][o], zr = z[u * 3 + 2][o];
+                            const float2 l = make_float2(__shfl_up_sync(0xffffffffu, zl.x, 1), __shfl_up_sync(0xffffffffu, zl.y, 1));
+                            const float2 r = make_float2(__shfl_down_sync(0xffffffffu, zr.x, 1), __shfl_down_sync(0xffffffffu, zr.y, 1));
+                            hsum[u][o] = fma2(l, ml, fma2(r, mr, z[u * 3 + 1][o]));
                         }
                     // vertical: out[p] = H_-1[p-W] + H_0[p] + H_+1[p+W].  Lanes l < 16 (even y) take
                     // H_+1 of lane l+16 and publish their H_+1 for the warp row above; lanes >= 16
                     // take H_-1 of lane l-16 and publish their H_-1 for the warp row below.
-                    float pub[8];
+                    float2 pub[c / 2];
 #pragma unroll
-                    for (int o = 0; o < c; o++) {
-                        const float send = lane < 16 ? hsum[0][o] : hsum[2][o];
-                        const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
-                        mid[o] = hsum[1][o] + recv + __ldg(b2 + o);
+                    for (int o = 0; o < c / 2; o++) {
+                        const float2 send = lane < 16 ? hsum[0][o] : hsum[2][o];
+                        const float2 recv = make_float2(__shfl_xor_sync(0xffffffffu, send.x, 16), __shfl_xor_sync(0xffffffffu, send.y, 16));
+                        mid[o] = add2(add2(hsum[1][o], recv), make_float2(bb[2 * o], bb[2 * o + 1]));
                         pub[o] = lane < 16 ? hsum[2][o] : hsum[0][o];
                     }
-                    pub[6] = pub[7] = 0.f;
-                    reinterpret_cast<float4*>(xch)[2 * p] = make_float4(pub[0], pub[1], pub[2], pub[3]);
-                    reinterpret_cast<float4*>(xch)[2 * p + 1] = make_float4(pub[4], pub[5], pub[6], pub[7]);
+                    reinterpret_cast<float4*>(xch)[p] = make_float4(pub[0].x, pub[0].y, pub[1].x, pub[1].y);
+                    reinterpret_cast<float2*>(xch + 4 * HW)[p] = pub[2];
                 }
                 gsync();
                 {
+                    float* st = sstate(g) + (i & 1) * (C * HW);
                     const int q = lane < 16 ? (y > 0 ? p - W : -1) : (y < H - 1 ? p + W : -1);
-                    float4 o0 = make_float4(0.f, 0.f, 0.f, 0.f), o1 = o0;
-                    if (q >= 0) { o0 = reinterpret_cast<const float4*>(xch)[2 * q]; o1 = reinterpret_cast<const float4*>(xch)[2 * q + 1]; }
-                    const float ov[6] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y};
+                    float4 o0 = make_float4(0.f, 0.f, 0.f, 0.f);
+                    float2 o1 = make_float2(0.f, 0.f);
+                    if (q >= 0) { o0 = reinterpret_cast<const float4*>(xch)[q]; o1 = reinterpret_cast<const float2*>(xch + 4 * HW)[q]; }
+                    const float2 ov[3] = {make_float2(o0.x, o0.y), make_float2(o0.z, o0.w), o1};
                     float nv[8];
 #pragma unroll
-                    for (int o = 0; o < c; o++) {
-                        const float f = mid[o] + ov[o];
-                        float* sp = st + (out_off + o) * HW + p;
-                        const float old = *sp;
-                        nv[o] = a.inverse ? old - f : old + f;
-                        *sp = nv[o];
+                    for (int o2 = 0; o2 < c / 2; o2++) {
+                        const float2 f = add2(mid[o2], ov[o2]);
+                        float* sp = st + (out_off + 2 * o2) * HW + p;
+                        const float2 old = make_float2(sp[0], sp[HW]);
+                        const float2 n2 = a.inverse ? sub2(old, f) : add2(old, f);
+                        sp[0] = n2.x;
+                        sp[HW] = n2.y;
+                        nv[2 * o2] = n2.x;
+                        nv[2 * o2 + 1] = n2.y;
                     }
                     nv[6] = 1.f;   // constant-1 channel (folded conv1 bias)
                     nv[7] = 0.f;
@@ -448,10 +511,9 @@ __global__ void __launch_bounds__(ts::kThreads, 1) k_stage_ts(TsArgs a) {
             gsync();
             {
                 float4* dst = reinterpret_cast<float4*>(gst);
-                const float4* src = reinterpret_cast<const float4*>(st);
+                const float4* src = reinterpret_cast<const float4*>(sstate(g) + (i & 1) * (C * HW));
                 for (int q = et; q < C * HW / 4; q += kEpi) __stcg(dst + q, src[q]);
             }
-            gsync();
         }
     }
     fence_before();
@@ -472,24 +534,25 @@ void stage_ts_col(int n, int& tap, int& o) {
     tap = -1; o = -1;
 }
 
-static void* ts_kernel(int pm) {
-    return pm == 2 ? (void*)k_stage_ts<2> : (pm == 1 ? (void*)k_stage_ts<1> : (void*)k_stage_ts<0>);
+typedef void (*TsKernel)(TsArgs);
+static TsKernel ts_kernel(int pm, int stk) {
+    return pm == 2 ? (stk ? k_stage_ts<2, 1> : k_stage_ts<2, 0>) : (pm == 1 ? k_stage_ts<1, 0> : k_stage_ts<0, 0>);
 }
 
 cudaError_t stage_ts_prepare() {
     cudaError_t e = cudaSuccess;
     for (int pm = 0; pm < 3 && e == cudaSuccess; pm++)
-        e = cudaFuncSetAttribute(ts_kernel(pm), cudaFuncAttributeMaxDynamicSharedMemorySize, ts::smem_bytes(pm));
+        for (int stk = 0; stk < (pm == 2 ? 2 : 1) && e == cudaSuccess; stk++)
+            e = cudaFuncSetAttribute(ts_kernel(pm, stk), cudaFuncAttributeMaxDynamicSharedMemorySize, ts::smem_bytes(pm));
     return e;
 }
 
-cudaError_t launch_stage_ts(const TsArgs& a, int pm, cudaStream_t st) {
+bool stage_ts_stacked(int pm) { return pm == 2 && !getenv("CI_TS_UNSTK"); }
+
+cudaError_t launch_stage_ts(const TsArgs& a, int pm, int stk, cudaStream_t st) {
     const int grid = (int)std::min<int64_t>((a.n + 1) / 2, 148);
     if (a.n <= 0) return cudaSuccess;
-    const size_t sm = ts::smem_bytes(pm);
-    if (pm == 2) k_stage_ts<2><<<grid, ts::kThreads, sm, st>>>(a);
-    else if (pm == 1) k_stage_ts<1><<<grid, ts::kThreads, sm, st>>>(a);
-    else k_stage_ts<0><<<grid, ts::kThreads, sm, st>>>(a);
+    ts_kernel(pm, stk)<<<grid, ts::kThreads, ts::smem_bytes(pm), st>>>(a);
     return cudaGetLastError();
 }
 

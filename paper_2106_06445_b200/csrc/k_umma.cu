@@ -2485,7 +2485,7 @@ static bool make_plan_spec(const StageInfo& S, int pm, StagePlan& p, int residua
         p.Nc2 = stage_ts_n2();
         p.T = 2; p.I = 1; p.pair = 1; p.fold = 1; p.pm = pm;
         p.k1 = kPairK1; p.k2 = 4;
-        p.stk1 = pm == 2 ? 1 : 0;
+        p.stk1 = stage_ts_stacked(pm) ? 1 : 0;
         p.blk_bytes = stage_ts_block_bytes(pm);
         p.tmem_cols = 512;
         p.nslot = 4;
@@ -2721,7 +2721,7 @@ ci_status_t umma_stage(const Model* m, int s, float* state, int64_t n, bool inve
         t.ctr = ctr;
         const StageInfo& S = m->st[s];
         prof_begin(st);
-        CI_CUDA(launch_stage_ts(t, a.p.pm, st));
+        CI_CUDA(launch_stage_ts(t, a.p.pm, a.p.stk1, st));
         count_launch();
         prof_end(st, s, (double)n * S.nb * 36.0 * S.H * S.W * S.c * S.m);
         return CI_OK;
