@@ -1,0 +1,108 @@
+"""The TS-mode stage-1 kernel (csrc/k_stage_ts.cu) against the f64 oracle and
+against the padded-raster k_stage (CI_NO_TS=1, independently pinned by the round-1 tests).
+
+Arch C's first stage (16x16, c = 6, m = 64) runs on k_stage_ts whenever the model is created
+without CI_NO_TS.  Image counts cover: one image (the pair's second slot absent), an odd count,
+exactly one image per CTA pair, more images than 2 x 148 (dynamic claiming, two passes), and
+the inverse direction (blocks in reverse order, subtraction)."""
+import os
+
+import numpy as np
+import pytest
+
+import fixtures as fx
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = {"fp32": 1e-3, "f16x2": 5e-3, "bf16": 3e-2}
+
+
+@pytest.fixture(scope="module")
+def ci():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2106_06445_b200 import codedinv
+    return codedinv
+
+
+def relerr(a, ref):
+    a = np.asarray(a, np.float64).reshape(-1, np.shape(ref)[-1])
+    r = np.asarray(ref, np.float64).reshape(-1, np.shape(ref)[-1])
+    return float(np.max(np.max(np.abs(a - r), 1) / np.maximum(np.max(np.abs(r), 1), 1e-30)))
+
+
+def make_model(ci, arch, params, prec, ts):
+    old = os.environ.pop("CI_NO_TS", None)
+    if not ts:
+        os.environ["CI_NO_TS"] = "1"
+    try:
+        return ci.Model(arch, params, prec)
+    finally:
+        os.environ.pop("CI_NO_TS", None)
+        if old is not None:
+            os.environ["CI_NO_TS"] = old
+
+
+def run_h(m, x, n, d, inverse=False):
+    xt = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    ws = m.workspace(1, n)
+    if inverse:
+        out = torch.empty(n, 3, 32, 32, device="cuda")
+        m.ci_inverse_h(xt.view(n, d), out, ws)
+    else:
+        out = torch.empty(n, d, device="cuda")
+        m.ci_forward_h(xt.view(n, 3, 32, 32), out, ws)
+    torch.cuda.synchronize()
+    return out.cpu().numpy().reshape(n, -1)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "f16x2", "bf16"])
+@pytest.mark.parametrize("n", [1, 3, 296, 301])
+def test_ts_forward_vs_oracle(ci, prec, n):
+    arch = fx.ARCH_C
+    params = fx.make_weights(arch, 13)
+    x = fx.make_inputs(arch, 1, n, 7 + n)[0]
+    got = run_h(make_model(ci, arch, params, prec, True), x, n, arch.d)
+    idx = np.unique(np.array([0, n - 1, n // 2]))
+    ref = oracle.forward_h(arch, params, x[idx]).reshape(len(idx), -1)
+    e = relerr(got[idx], ref)
+    print(f"[ts fwd {prec} n={n}] {e:.3g}")
+    assert e < TOL[prec]
+
+
+@pytest.mark.parametrize("prec", ["fp32", "f16x2"])
+def test_ts_matches_padded_kernel(ci, prec):
+    """Same h from the TS kernel and from the padded-raster k_stage (different MMA and epilogue
+    order, same precision): agreement far inside the contract tolerance, forward and inverse."""
+    arch = fx.ARCH_C
+    params = fx.make_weights(arch, 13)
+    n = 157
+    x = fx.make_inputs(arch, 1, n, 99)[0]
+    a = make_model(ci, arch, params, prec, True)
+    b = make_model(ci, arch, params, prec, False)
+    ha, hb = run_h(a, x, n, arch.d), run_h(b, x, n, arch.d)
+    e_f = relerr(ha, hb)
+    xa, xb = run_h(a, ha, n, arch.d, inverse=True), run_h(b, ha, n, arch.d, inverse=True)
+    e_i = relerr(xa, xb)
+    e_rt = relerr(xa, x.reshape(n, -1))
+    print(f"[ts vs padded {prec}] forward {e_f:.3g} inverse {e_i:.3g} round trip {e_rt:.3g}")
+    assert e_f < 1e-4 and e_i < 1e-4 and e_rt < 1e-5
+
+
+def test_ts_inverse_vs_oracle_and_determinism(ci):
+    arch = fx.ARCH_C
+    params = fx.make_weights(arch, 13)
+    n = 149
+    x = fx.make_inputs(arch, 1, n, 5)[0]
+    m = make_model(ci, arch, params, "fp32", True)
+    h1 = run_h(m, x, n, arch.d)
+    h2 = run_h(m, x, n, arch.d)
+    assert np.array_equal(h1, h2)   # dynamic batch claiming does not change any result
+    idx = np.array([0, 74, 148])
+    ref = oracle.inverse_h(arch, params, h1[idx].astype(np.float64)).reshape(len(idx), -1)
+    xr = run_h(m, h1, n, arch.d, inverse=True)
+    e = relerr(xr[idx], ref)
+    print(f"[ts inverse fp32] {e:.3g}")
+    assert e < 1e-3
