@@ -153,5 +153,10 @@ void stage_ts_col(int n, int& tap, int& o);   // conv2 column -> (tap, output ch
 cudaError_t stage_ts_prepare();
 bool stage_ts_stacked(int pm);   // f16x3: stacked conv1 (CI_TS_UNSTK=1: three N = 64 MMAs per k-step)
 cudaError_t launch_stage_ts(const TsArgs& a, int pm, int stk, cudaStream_t st);
+// TS-mode kernel for Arch C stage 2 (8x8, c = 24, m = 128; k_stage_ts2.cu)
+bool stage_ts2_shape(int H, int W, int C, int c, int m, int residual, int act);
+int64_t stage_ts2_block_bytes(int pm);
+cudaError_t stage_ts2_prepare();
+cudaError_t launch_stage_ts2(const TsArgs& a, int pm, cudaStream_t st);
 
 }  // namespace ci

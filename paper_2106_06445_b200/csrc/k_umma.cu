@@ -2326,6 +2326,36 @@ static void put_tile(std::vector<uint16_t>& out, const std::vector<float>& w, in
 static void pack_block(const StagePlan& p, const float* W1, const float* b1, const float* W2, int pm,
                        std::vector<uint16_t>& out) {
     const int c = p.c, m = p.m;
+    if (p.ts == 2) {   // k_stage_ts2: conv1 over the 28 view planes, conv2 in two 112-column passes
+        std::vector<float> tile;
+        for (int s = 0; s < 14; s++) {   // plane L = 2s + kk/8: tap L/3, channels 8 (L%3)..; L = 27: bias
+            tile.assign((size_t)128 * 16, 0.f);
+            for (int h = 0; h < m; h++)
+                for (int kk = 0; kk < 16; kk++) {
+                    const int L = 2 * s + kk / 8, e = kk % 8;
+                    float v = 0.f;
+                    if (L < 27) {
+                        const int tap = L / 3, ci = 8 * (L % 3) + e;
+                        v = W1[(((size_t)h * c + ci) * 3 + tap / 3) * 3 + tap % 3];
+                    } else if (e == 0) {
+                        v = b1[h];
+                    }
+                    tile[(size_t)h * 16 + kk] = v;
+                }
+            put_tile(out, tile, 128, pm);
+        }
+        for (int pass = 0; pass < 2; pass++)
+            for (int s = 0; s < 8; s++) {   // column n = 54 half + 6 tap + o' -> output 12 pass + 6 half + o'
+                tile.assign((size_t)112 * 16, 0.f);
+                for (int n = 0; n < 108; n++) {
+                    const int hh = n / 54, tap = (n % 54) / 6, o = 12 * pass + 6 * hh + n % 6;
+                    for (int kk = 0; kk < 16; kk++)
+                        tile[(size_t)n * 16 + kk] = W2[(((size_t)o * m + 16 * s + kk) * 3 + tap / 3) * 3 + tap % 3];
+                }
+                put_tile(out, tile, 112, pm);
+            }
+        return;
+    }
     auto w1 = [&](int h, int ci, int u, int v) -> float {  // u, v in -1..1
         // folded bias: X channel c is 1 on every valid pixel, so its centre-tap weight is b1
         if (p.fold && h < m && ci == c && u == 0 && v == 0) return b1[h];
@@ -2477,6 +2507,20 @@ static StageKernel pick_kernel(const StagePlan& p, const StageArgs& a) {
 }
 // plan a stage; a stacked plan without a specialised kernel falls back to the unstacked plan
 static bool make_plan_spec(const StageInfo& S, int pm, StagePlan& p, int residual, int act) {
+    if (stage_ts2_shape(S.H, S.W, S.C, S.c, S.m, residual, act)) {
+        p = StagePlan{};
+        p.ts = 2;
+        p.H = S.H; p.W = S.W; p.Wp = S.W; p.G = 0;
+        p.c = S.c; p.m = S.m; p.Cp = 32; p.Mp = 128; p.MC = 128; p.nch = 1; p.n1 = 128;
+        p.Nc2 = 112;
+        p.T = 1; p.I = 2; p.fold = 1; p.pm = pm;
+        p.k1 = 14; p.k2 = 8;
+        p.blk_bytes = stage_ts2_block_bytes(pm);
+        p.tmem_cols = 512;
+        p.nslot = 3;
+        p.slot_bytes = 16384;
+        return true;
+    }
     if (stage_ts_shape(S.H, S.W, S.C, S.c, S.m, residual, act)) {
         p = StagePlan{};
         p.ts = 1;
@@ -2520,7 +2564,7 @@ ci_status_t umma_prepare(Model* m, const float* host_params) {
                     s, p.H, p.W, p.c, p.m, p.pm, p.Cp, p.Mp, p.MC, p.nch, p.Nc2, p.T, p.I, p.k1, p.k2,
                     p.nslot, p.slot_bytes, p.smem, p.tmem_cols, (long long)p.blk_bytes,
                     (double)p.I * p.H * p.W / (p.T * 128.0), p.nhd, p.sstate, p.stk1, p.stk2, p.est_cycles,
-                    p.ts ? " [TS kernel]" : "");
+                    p.ts == 2 ? " [TS2 kernel]" : (p.ts ? " [TS kernel]" : ""));
         // align each stage stream to 128 B
         while ((pack.size() * 2) % 128) pack.push_back(0);
         U->wpack_off[s] = (int64_t)pack.size() * 2;
@@ -2582,6 +2626,7 @@ ci_status_t umma_prepare(Model* m, const float* host_params) {
     if (e == cudaSuccess) e = cudaMemcpy(m->d_bias, bias.data(), bias.size() * 4, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_stage<SDyn>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap);
     if (e == cudaSuccess) e = stage_ts_prepare();
+    if (e == cudaSuccess) e = stage_ts2_prepare();
     for (const auto& sp : kSpecs)
         if (e == cudaSuccess) e = cudaFuncSetAttribute(sp.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap);
     if (e != cudaSuccess) { delete U; return cuda_status(e, "umma_prepare"); }
@@ -2721,7 +2766,8 @@ ci_status_t umma_stage(const Model* m, int s, float* state, int64_t n, bool inve
         t.ctr = ctr;
         const StageInfo& S = m->st[s];
         prof_begin(st);
-        CI_CUDA(launch_stage_ts(t, a.p.pm, a.p.stk1, st));
+        if (a.p.ts == 2) CI_CUDA(launch_stage_ts2(t, a.p.pm, st));
+        else CI_CUDA(launch_stage_ts(t, a.p.pm, a.p.stk1, st));
         count_launch();
         prof_end(st, s, (double)n * S.nb * 36.0 * S.H * S.W * S.c * S.m);
         return CI_OK;

@@ -1,8 +1,9 @@
-"""The TS-mode stage-1 kernel (csrc/k_stage_ts.cu) against the f64 oracle and
-against the padded-raster k_stage (CI_NO_TS=1, independently pinned by the round-1 tests).
+"""The TS-mode stage kernels (csrc/k_stage_ts.cu stage 1, csrc/k_stage_ts2.cu stage 2; DESIGN.md
+7.2b/c) against the f64 oracle and against the padded-raster k_stage (CI_NO_TS=1, CI_NO_TS2=1,
+independently pinned by the round-1 tests).
 
-Arch C's first stage (16x16, c = 6, m = 64) runs on k_stage_ts whenever the model is created
-without CI_NO_TS.  Image counts cover: one image (the pair's second slot absent), an odd count,
+Arch C's first two stages (16x16, c = 6, m = 64; 8x8, c = 24, m = 128) run on the TS kernels
+whenever the model is created without those switches.  Image counts cover: one image (the pair's second slot absent), an odd count,
 exactly one image per CTA pair, more images than 2 x 148 (dynamic claiming, two passes), and
 the inverse direction (blocks in reverse order, subtraction)."""
 import os
@@ -34,15 +35,19 @@ def relerr(a, ref):
 
 
 def make_model(ci, arch, params, prec, ts):
-    old = os.environ.pop("CI_NO_TS", None)
+    """ts=False: both TS kernels off (CI_NO_TS, CI_NO_TS2: stages 1-2 on the padded k_stage)."""
+    keys = ("CI_NO_TS", "CI_NO_TS2")
+    old = {k: os.environ.pop(k, None) for k in keys}
     if not ts:
-        os.environ["CI_NO_TS"] = "1"
+        for k in keys:
+            os.environ[k] = "1"
     try:
         return ci.Model(arch, params, prec)
     finally:
-        os.environ.pop("CI_NO_TS", None)
-        if old is not None:
-            os.environ["CI_NO_TS"] = old
+        for k in keys:
+            os.environ.pop(k, None)
+            if old[k] is not None:
+                os.environ[k] = old[k]
 
 
 def run_h(m, x, n, d, inverse=False):
