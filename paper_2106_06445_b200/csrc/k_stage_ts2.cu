@@ -3,22 +3,22 @@
 //   s_out <- s_out (+|-) F(s_in),  F = conv3x3(W2) o ReLU o conv3x3(W1).
 //
 //  * Two images per 128-row M-tile with no pad rows or columns (100% of the MMA rows are
-//    pixels; k_stage's padded raster held 3 images in 2 tiles = 75%).  A row shift would cross
-//    image and row borders, so conv1's input is kept as nine masked VIEWS, one per tap:
-//    V_{u,v}[p] = X[y+u][x+v] (0 outside the image).  conv1 is then a plain K-major GEMM over
-//    27 planes of 8 channels (+ the constant-1 plane that carries the folded conv1 bias): 14
-//    K = 16 steps, the two K halves of a step two adjacent planes (LBO = one plane).
+//    pixels; k_stage's padded raster held 3 images in 2 tiles = 75%), rows interleaved by image
+//    row: r = 16 y + 8 img + x.  A vertical tap is then a row shift of 16 that stays inside the
+//    image (rows beyond the tile are zero guard rows), and a horizontal tap uses one of three
+//    views of the input, Xc, Xl[r] = X[r-1] (0 at x = 0), Xr[r] = X[r+1] (0 at x = 7).  conv1 runs
+//    14 K = 16 steps over (vertical shift, view, 8-channel plane) pairs + the constant-1 plane
+//    (folded conv1 bias), the two K halves of a step LBO bytes apart.
 //  * The hidden (128 channels, ReLU, fp16 hi + lo) is written back into TMEM over acc1 and read
 //    by conv2 in TS mode (A from TMEM).  conv2 stacks all 9 taps in N: two passes over the
 //    outputs (channels 0-11 then 12-23; N = 108 -> 112 each: column 54 half + 6 tap + o), so a
-//    slot needs 128 + 112 TMEM columns.  The epilogue forms out[p] = sum_{u,v} Z_{u,v}[p + 8u + v]:
-//    horizontal neighbours are lanes +-1 (image rows are 8-aligned in a warp), vertical ones lanes
-//    +-8, except across the two warps of an image (one 32-B exchange per border row).
-//  * Two slots (tiles) per CTA, each served by its own group of 8 epilogue warps; per block the
-//    MMA thread issues conv1(A) conv1(B) conv2a(A) conv2a(B) conv2b(A) conv2b(B).  The views are
-//    ONE shared buffer (112 KB): group A writes its views for block k+1 once conv1(B, k) has
-//    completed, group B once conv1(A, k+1) has completed.  Weight segments are streamed per
-//    slot (the ring cannot hold a whole 112 KB conv1 segment).
+//    slot needs 128 + 112 TMEM columns.  The epilogue forms out[r] = sum_{u,v} Z_{u,v}[r + 16u + v]:
+//    horizontal neighbours are lanes +-1 (masked at x = 0 / 7), vertical ones lanes +-16 (one
+//    xor-16 shuffle) or the neighbouring warp's rows (one exchange through shared memory).
+//  * Two slots (tiles) per CTA with their own views, state and group of 8 epilogue warps.  The
+//    MMA thread runs slot B half a block behind slot A: conv1(A,k) conv2(B,k-1) conv2(A,k)
+//    conv1(B,k), so every hand-off between a slot's epilogue and its next MMA step is covered by
+//    at least one conv1 or two conv2 passes of the other slot.
 //  * The fp32 state of the slot's two images stays in shared memory for the whole stage.
 #include <stdio.h>
 
@@ -35,19 +35,25 @@ namespace ts2 {
 constexpr int kThreads = 576;      // warp 0 producer, warp 1 MMA, warps 2..17 epilogue (2 groups)
 constexpr int kEpi = 256;
 constexpr int H = 8, W = 8, HW = 64, C = 48, c = 24, M = 128;
-constexpr int NP1 = 28;                     // conv1 K planes: 9 taps x 3 + the constant-1 plane
-constexpr int PB = 128 * 16;                // plane bytes (one tile, no guards)
+constexpr int NPL = 10;                     // view planes: 3 views x 3 planes of 8 channels + constant-1
+constexpr int G = 16;                       // guard rows above / below the 128 tile rows (one row shift)
+constexpr int RT = G + 128 + G;
+constexpr int PB = RT * 16;                 // plane bytes
 constexpr int N1 = 128, N2 = 112;           // conv1 / conv2-pass MMA widths
 constexpr int K1 = 14, K2 = 8;              // k-steps
 constexpr int NSLOT = 3, SLOTB = 16384;     // weight ring
 constexpr int ST_BYTES = 2 * C * HW * 4;    // fp32 state of the slot's two images
-constexpr int XCH_BYTES = 2 * 2 * 32 * 32;  // vertical exchange [pass][half][32 border rows][8] fp32
+constexpr int XCH_BYTES = 2 * 2 * 128 * 24; // vertical exchange [pass][half][row][6] fp32
 __host__ __device__ constexpr int kstep(int N, int pm) { return N * 32 * (pm == 2 ? 2 : 1); }
 __host__ __device__ constexpr int per_slot(int N, int pm) { return SLOTB / kstep(N, pm); }
-__host__ __device__ constexpr int view_bytes(int pm) { return (pm ? 2 : 1) * NP1 * PB; }
-__host__ __device__ constexpr int smem_bytes(int pm) {
-    return NSLOT * SLOTB + view_bytes(pm) + 2 * (ST_BYTES + XCH_BYTES) + 512;
+__host__ __device__ constexpr int view_bytes(int pm) { return (pm ? 2 : 1) * NPL * PB; }
+__host__ __device__ constexpr int slot_bytes(int pm) { return view_bytes(pm) + ST_BYTES + XCH_BYTES; }
+__host__ __device__ constexpr int smem_bytes(int pm) { return NSLOT * SLOTB + 2 * slot_bytes(pm) + 512; }
+// conv1 k-step s: A start (bytes from the plane base of the views) and LBO (bytes)
+__host__ __device__ constexpr int k1_start(int s) {
+    return s < 12 ? 2 * (s % 4) * PB + (G + 16 * (s / 4 - 1)) * 16 : 8 * PB + (G + (s == 12 ? -16 : 16)) * 16;
 }
+__host__ __device__ constexpr int k1_lbo(int s) { return s < 12 ? PB : (s == 12 ? 256 : PB - 256); }
 }  // namespace ts2
 
 namespace {
@@ -108,30 +114,33 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     uint8_t* ring = smem;
-    uint8_t* views = ring + NSLOT * SLOTB;                 // [hi: 28 planes][lo: 28 planes]
-    uint8_t* gbase = views + view_bytes(PM);               // [2] x { state, xch }
-    auto sstate = [&](int s) { return reinterpret_cast<float*>(gbase + (size_t)s * (ST_BYTES + XCH_BYTES)); };
-    auto sxch = [&](int s) { return reinterpret_cast<float*>(gbase + (size_t)s * (ST_BYTES + XCH_BYTES) + ST_BYTES); };
-    uint64_t* bars = reinterpret_cast<uint64_t*>(gbase + 2 * (ST_BYTES + XCH_BYTES));
+    uint8_t* slots = ring + NSLOT * SLOTB;   // [2] x { views [hi: 10 planes][lo: 10 planes], state, xch }
+    auto sviews = [&](int s) { return slots + (size_t)s * slot_bytes(PM); };
+    auto sstate = [&](int s) { return reinterpret_cast<float*>(slots + (size_t)s * slot_bytes(PM) + view_bytes(PM)); };
+    auto sxch = [&](int s) {
+        return reinterpret_cast<float*>(slots + (size_t)s * slot_bytes(PM) + view_bytes(PM) + ST_BYTES);
+    };
+    uint64_t* bars = reinterpret_cast<uint64_t*>(slots + 2 * slot_bytes(PM));
     uint64_t* full = bars;            // [3]
     uint64_t* empty = bars + 4;       // [3]
     uint64_t* bqf = bars + 8;         // [4]
     uint64_t* bqe = bars + 12;        // [4]
-    uint64_t* x_rdy = bars + 16;      // [2] the shared views hold slot s's input for its next conv1
-    uint64_t* a1t = bars + 18;        // [2] conv1 of slot s done (commit; also frees the views)
+    uint64_t* x_rdy = bars + 16;      // [2] views of slot s final for its next conv1
+    uint64_t* a1t = bars + 18;        // [2] conv1 of slot s done (commit)
     uint64_t* hdt = bars + 20;        // [2] hidden of slot s in TMEM
     uint64_t* a2t = bars + 22;        // [2] conv2 pass of slot s done (commit; twice per block)
     uint64_t* a2r = bars + 24;        // [2] pass-a accumulator of slot s read (pass b may overwrite)
     volatile int64_t* bq = reinterpret_cast<volatile int64_t*>(bars + 26);   // [4]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 30);
 
-    {   // views: zero (masked taps, never written later); constant-1 plane: channel 0 = 1.0 (hi)
+    {   // views: zero (guards, x borders of Xl / Xr); constant-1 plane: channel 0 = 1.0 on the tile rows
         uint4 z = make_uint4(0, 0, 0, 0);
-        for (int i = tid; i < view_bytes(PM) / 16; i += kThreads) reinterpret_cast<uint4*>(views)[i] = z;
+        for (int s = 0; s < 2; s++)
+            for (int i = tid; i < view_bytes(PM) / 16; i += kThreads) reinterpret_cast<uint4*>(sviews(s))[i] = z;
         __syncthreads();
         const uint32_t one = PM ? 0x3C00u : 0x3F80u;   // fp16 / bf16 1.0 in the low half
-        for (int r = tid; r < 128; r += kThreads)
-            *reinterpret_cast<uint4*>(views + (size_t)27 * PB + r * 16) = make_uint4(one, 0, 0, 0);
+        for (int i = tid; i < 2 * 128; i += kThreads)
+            *reinterpret_cast<uint4*>(sviews(i >> 7) + (size_t)9 * PB + (size_t)(G + (i & 127)) * 16) = make_uint4(one, 0, 0, 0);
     }
     fence_proxy_async();
     if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -155,6 +164,17 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
     };
     const int SEG1 = K1 * kstep(N1, PM), SEG2 = K2 * kstep(N2, PM);
     constexpr int G1 = per_slot(N1, PM), G2 = per_slot(N2, PM);   // k-steps per ring slot
+    // MMA order of one image pair (slot B half a block behind slot A), as (segment, block, slot):
+    //   conv1(A,k) [conv2a(B,k-1) conv2b(B,k-1)] conv2a(A,k) conv2b(A,k) [conv1(B,k)], k = 0..nb-1,
+    //   then [conv2a(B,nb-1) conv2b(B,nb-1)]; segment 0 = conv1, 1 = conv2 pass a, 2 = pass b
+    auto for_each_step = [&](int ns, auto&& f) {
+        for (int k = 0; k <= a.nb; k++) {
+            if (k < a.nb) f(0, k, 0);
+            if (ns == 2 && k >= 1) { f(1, k - 1, 1); f(2, k - 1, 1); }
+            if (k < a.nb) { f(1, k, 0); f(2, k, 0); }
+            if (ns == 2 && k < a.nb) f(0, k, 1);
+        }
+    };
 
     if (warp == 0) {
         // ================= producer ==========================================================
@@ -172,29 +192,24 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
                 bq[i & 3] = v;
                 mbar_arrive(&bqf[i & 3]);
             };
-            auto stream = [&](const uint8_t* src, int K, int G, int kb) {
-                for (int s0 = 0; s0 < K; s0 += G) {
-                    const uint32_t bytes = (uint32_t)(min(G, K - s0) * kb);
-                    mbar_wait(&empty[slot], phase ^ 1);
-                    mbar_arrive_expect_tx(&full[slot], bytes);
-                    bulk_g2s(ring + (size_t)slot * SLOTB, src + (size_t)s0 * kb, bytes, &full[slot]);
-                    if (++slot == NSLOT) { slot = 0; phase ^= 1; }
-                }
-            };
             for (int pi = 0;; pi++) {
                 const int64_t b0 = next();
                 const int64_t b1 = b0 < nbatch ? next() : nbatch;
                 publish(2 * pi, b0);
                 publish(2 * pi + 1, b1);
                 if (b0 >= nbatch) break;
-                const int ns = b1 < nbatch ? 2 : 1;
-                for (int tt = 0; tt < a.nb; tt++) {
-                    const int t = a.inverse ? a.nb - 1 - tt : tt;
-                    const uint8_t* src = a.wpack + (int64_t)t * a.blk_bytes;
-                    for (int s = 0; s < ns; s++) stream(src, K1, G1, kstep(N1, PM));
-                    for (int pass = 0; pass < 2; pass++)
-                        for (int s = 0; s < ns; s++) stream(src + SEG1 + pass * SEG2, K2, G2, kstep(N2, PM));
-                }
+                for_each_step(b1 < nbatch ? 2 : 1, [&](int seg, int k, int) {
+                    const int t = a.inverse ? a.nb - 1 - k : k;
+                    const uint8_t* src = a.wpack + (int64_t)t * a.blk_bytes + (seg == 0 ? 0 : SEG1 + (seg - 1) * SEG2);
+                    const int K = seg == 0 ? K1 : K2, Gs = seg == 0 ? G1 : G2, kb = seg == 0 ? kstep(N1, PM) : kstep(N2, PM);
+                    for (int s0 = 0; s0 < K; s0 += Gs) {
+                        const uint32_t bytes = (uint32_t)(min(Gs, K - s0) * kb);
+                        mbar_wait(&empty[slot], phase ^ 1);
+                        mbar_arrive_expect_tx(&full[slot], bytes);
+                        bulk_g2s(ring + (size_t)slot * SLOTB, src + (size_t)s0 * kb, bytes, &full[slot]);
+                        if (++slot == NSLOT) { slot = 0; phase ^= 1; }
+                    }
+                });
                 if (b1 >= nbatch) {
                     publish(2 * pi + 2, nbatch);
                     break;
@@ -206,11 +221,12 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
         // ================= MMA issuer ========================================================
         if (elect_one()) {
             int slot = 0;
-            uint32_t phase = 0, kb = 0;
-            const uint32_t rb = smem_u32(ring), vb = smem_u32(views);
+            uint32_t phase = 0;
+            uint32_t kbs[2] = {0, 0};   // blocks completed per slot (barrier phases)
+            const uint32_t rb = smem_u32(ring);
             const uint32_t id1 = idesc_of(128, N1, PM != 0);
             const uint32_t id2 = idesc_of(128, N2, PM != 0);
-            constexpr uint32_t LOA = (uint32_t)(NP1 * PB / 16);   // lo planes, descriptor units
+            constexpr uint32_t LOA = (uint32_t)(NPL * PB / 16);   // lo planes, descriptor units
             auto acquire = [&]() -> uint32_t {
                 mbar_wait(&full[slot], phase);
                 fence_after();
@@ -227,79 +243,73 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
                 const int64_t b1 = bq_read(2 * pi + 1);
                 mbar_arrive(&bqe[(2 * pi + 1) & 3]);
                 const int ns = b1 < nbatch ? 2 : 1;
-                for (int tt = 0; tt < a.nb; tt++, kb++) {
-                    const uint32_t par = kb & 1;
-                    // conv1 (SS: A = the nine views, one K-major operand of 28 planes)
-                    for (int s = 0; s < 2; s++) {
-                        if (s >= ns) { commit(&a1t[s]); continue; }   // keeps the views hand-off regular
+                for_each_step(ns, [&](int seg, int, int s) {
+                    const uint32_t par = kbs[s] & 1;
+                    const uint32_t tb = tmem + (uint32_t)(s * 256);
+                    if (seg == 0) {   // conv1 (SS: A = the views, vertical taps as row shifts of 16)
                         mbar_wait(&x_rdy[s], par);
                         fence_after();
-                        const uint32_t d = tmem + (uint32_t)(s * 256);
+                        const uint32_t vb = smem_u32(sviews(s));
                         for (int s0 = 0; s0 < K1; s0 += G1) {
                             const uint32_t w = acquire();
 #pragma unroll
                             for (int q = 0; q < G1; q++) {
                                 const int ks = s0 + q;
                                 if (ks >= K1) break;
-                                const uint64_t ad = smem_desc(vb + (uint32_t)(2 * ks * PB), PB, 128);
+                                const uint64_t ad = smem_desc(vb + (uint32_t)k1_start(ks), (uint32_t)k1_lbo(ks), 128);
                                 const uint64_t bd = smem_desc(w + (uint32_t)(q * kstep(N1, PM)), N1 * 16, 128);
                                 const uint32_t acc = ks > 0 ? 1u : 0u;
-                                mma_bf16(d, ad, bd, id1, acc);
-                                if (PM >= 1) mma_bf16(d, ad + LOA, bd, id1, 1u);
-                                if (PM == 2) mma_bf16(d, ad, bd + (uint64_t)(N1 * 32 / 16), id1, 1u);
+                                mma_bf16(tb, ad, bd, id1, acc);
+                                if (PM >= 1) mma_bf16(tb, ad + LOA, bd, id1, 1u);
+                                if (PM == 2) mma_bf16(tb, ad, bd + (uint64_t)(N1 * 32 / 16), id1, 1u);
                             }
                             release();
                         }
                         commit(&a1t[s]);
-                    }
-                    // conv2, two passes over the outputs (TS: A = the hidden in TMEM)
-                    for (int pass = 0; pass < 2; pass++)
-                        for (int s = 0; s < ns; s++) {
-                            if (pass == 0) mbar_wait(&hdt[s], par);
-                            else mbar_wait(&a2r[s], par);
-                            fence_after();
-                            const uint32_t tb = tmem + (uint32_t)(s * 256);
-                            for (int s0 = 0; s0 < K2; s0 += G2) {
-                                const uint32_t w = acquire();
+                    } else {          // conv2 pass (TS: A = the hidden in TMEM)
+                        mbar_wait(seg == 1 ? &hdt[s] : &a2r[s], par);
+                        fence_after();
+                        for (int s0 = 0; s0 < K2; s0 += G2) {
+                            const uint32_t w = acquire();
 #pragma unroll
-                                for (int q = 0; q < G2; q++) {
-                                    const int ks = s0 + q;
-                                    if (ks >= K2) break;
-                                    const uint32_t ahi = tb + (uint32_t)(16 * ks);   // hidden 16 ks..+15: hi | lo
-                                    const uint64_t bd = smem_desc(w + (uint32_t)(q * kstep(N2, PM)), N2 * 16, 128);
-                                    const uint32_t acc = ks > 0 ? 1u : 0u;
-                                    mma_ts(tb + 128, ahi, bd, id2, acc);
-                                    if (PM >= 1) mma_ts(tb + 128, ahi + 8, bd, id2, 1u);
-                                    if (PM == 2) mma_ts(tb + 128, ahi, bd + (uint64_t)(N2 * 32 / 16), id2, 1u);
-                                }
-                                release();
+                            for (int q = 0; q < G2; q++) {
+                                const int ks = s0 + q;
+                                if (ks >= K2) break;
+                                const uint32_t ahi = tb + (uint32_t)(16 * ks);   // hidden 16 ks..+15: hi | lo
+                                const uint64_t bd = smem_desc(w + (uint32_t)(q * kstep(N2, PM)), N2 * 16, 128);
+                                const uint32_t acc = ks > 0 ? 1u : 0u;
+                                mma_ts(tb + 128, ahi, bd, id2, acc);
+                                if (PM >= 1) mma_ts(tb + 128, ahi + 8, bd, id2, 1u);
+                                if (PM == 2) mma_ts(tb + 128, ahi, bd + (uint64_t)(N2 * 32 / 16), id2, 1u);
                             }
-                            commit(&a2t[s]);
+                            release();
                         }
-                }
+                        commit(&a2t[s]);
+                        if (seg == 2) kbs[s]++;
+                    }
+                });
                 if (ns == 1) break;
             }
         }
         __syncwarp();
     } else {
         // ================= epilogue: group g = slot g (8 warps) ================================
-        // row p = 32 quarter + lane of the tile: image p / 64, y = (p % 64) / 8, x = p % 8.  Warps w
-        // and w+4 share a lane quarter: conv1 epilogue half h = hidden 64h..64h+63; conv2 epilogue
-        // half h = outputs 12 pass + 6h..+5; view writes half 0 = taps 0-4, half 1 = taps 5-8.
+        // row r = 32 quarter + lane: y = r / 16, image (r / 8) % 2, x = r % 8.  Warps w and w+4 share
+        // a lane quarter: conv1 epilogue half h = hidden 64h..64h+63; conv2 epilogue half h =
+        // outputs 12 pass + 6h..+5; view writes: half 0 = (view, plane) combos 0-4, half 1 = 5-8.
         const int g = (warp - 2) >> 3, ew = (warp - 2) & 7, quarter = warp & 3, half = ew >> 2, et = ew * 32 + lane;
         const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
-        const int p = quarter * 32 + lane, img = p >> 6, pp = p & 63, y = pp >> 3, x = pp & 7;
+        const int r = quarter * 32 + lane, y = r >> 4, img = (r >> 3) & 1, x = r & 7, pp = 8 * y + x;
         const uint32_t bar_id = 1 + g;
         auto gsync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "n"(kEpi) : "memory"); };
+        uint8_t* views = sviews(g);
         float* st = sstate(g);
         float* xch0 = sxch(g);
         const float2 ml = make_float2(x > 0 ? 1.f : 0.f, x > 0 ? 1.f : 0.f);
         const float2 mr = make_float2(x < W - 1 ? 1.f : 0.f, x < W - 1 ? 1.f : 0.f);
-        // cross-warp vertical neighbours: the second warp of an image (odd quarter) lanes 0-7 need
-        // H_-1 of the first warp's lanes 24-31 and vice versa (H_+1)
-        const bool xtop = (quarter & 1) && lane < 8, xbot = !(quarter & 1) && lane >= 24;
         auto in_half = [&](int t) { return ((a.first_orient + t) & 1) == 0 ? 0 : c; };
-        // views <- this pixel's 24 channels at offset ch0 of the state (the next conv1's input)
+        // views <- this pixel's 24 channels at offset ch0 of the state (the next conv1's input).
+        // Branch-free: a border pixel writes zeros into the Xl / Xr rows it would otherwise feed.
         auto write_views = [&](int ch0, int nimg) {
             const bool present = img < nimg;
             float v[c];
@@ -311,20 +321,19 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
                 if (PM) t2_split(v[2 * e], v[2 * e + 1], hi[e], lo[e]);
                 else { hi[e] = t2_bf16x2(v[2 * e], v[2 * e + 1]); lo[e] = 0; }
             }
+            const uint4 z4 = make_uint4(0, 0, 0, 0);
 #pragma unroll
-            for (int tap = 0; tap < 9; tap++) {
-                if ((tap < 5) != (half == 0)) continue;
-                const int u = tap / 3 - 1, vv = tap % 3 - 1;
-                // V_{u,v}[q] = X[q + 8u + v]: this pixel feeds row q = p - 8u - v when that pixel exists
-                if (y - u < 0 || y - u > H - 1 || x - vv < 0 || x - vv > W - 1) continue;
-                const int q = p - 8 * u - vv;
-#pragma unroll
-                for (int pl = 0; pl < 3; pl++) {
-                    const size_t off = (size_t)(tap * 3 + pl) * PB + (size_t)q * 16;
-                    *reinterpret_cast<uint4*>(views + off) = make_uint4(hi[4 * pl], hi[4 * pl + 1], hi[4 * pl + 2], hi[4 * pl + 3]);
-                    if (PM)
-                        *reinterpret_cast<uint4*>(views + (size_t)NP1 * PB + off) =
-                            make_uint4(lo[4 * pl], lo[4 * pl + 1], lo[4 * pl + 2], lo[4 * pl + 3]);
+            for (int cb = 0; cb < 9; cb++) {
+                if ((cb < 5) != (half == 0)) continue;
+                const int view = cb / 3, pl = cb % 3;   // view 0 = l (row r+1), 1 = c (row r), 2 = r (row r-1)
+                const int row = r + 1 - view;
+                const bool keep = view == 1 || (view == 0 ? x < W - 1 : x > 0);
+                const size_t off = (size_t)(view * 3 + pl) * PB + (size_t)(G + row) * 16;
+                const uint4 h4 = make_uint4(hi[4 * pl], hi[4 * pl + 1], hi[4 * pl + 2], hi[4 * pl + 3]);
+                *reinterpret_cast<uint4*>(views + off) = keep ? h4 : z4;
+                if (PM) {
+                    const uint4 l4 = make_uint4(lo[4 * pl], lo[4 * pl + 1], lo[4 * pl + 2], lo[4 * pl + 3]);
+                    *reinterpret_cast<uint4*>(views + (size_t)NPL * PB + off) = keep ? l4 : z4;
                 }
             }
         };
@@ -343,9 +352,6 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
                 for (int q = et; q < nimg * C * HW / 4; q += kEpi) dst[q] = __ldcg(src + q);
             }
             gsync();
-            // first block's views: A after conv1(B) of the previous block, B after conv1(A) of this one
-            if (g == 0) { if (kb > 0) mbar_wait(&a1t[1], (kb - 1) & 1); }
-            else mbar_wait(&a1t[0], kb & 1);
             write_views(in_half(a.inverse ? a.nb - 1 : 0), nimg);
             fence_proxy_async();
             mbar_arrive(&x_rdy[g]);
@@ -412,35 +418,28 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
                         for (int o = 0; o < 3; o++) {
                             const float2 zl = z[u * 3 + 0][o], zr = z[u * 3 + 2][o];
                             const float2 l = make_float2(__shfl_up_sync(0xffffffffu, zl.x, 1), __shfl_up_sync(0xffffffffu, zl.y, 1));
-                            const float2 r = make_float2(__shfl_down_sync(0xffffffffu, zr.x, 1), __shfl_down_sync(0xffffffffu, zr.y, 1));
-                            hs[u][o] = t2_fma2(l, ml, t2_fma2(r, mr, z[u * 3 + 1][o]));
+                            const float2 rr = make_float2(__shfl_down_sync(0xffffffffu, zr.x, 1), __shfl_down_sync(0xffffffffu, zr.y, 1));
+                            hs[u][o] = t2_fma2(l, ml, t2_fma2(rr, mr, z[u * 3 + 1][o]));
                         }
-                    // vertical: out[p] = H_-1[p-8] + H_0[p] + H_+1[p+8]; rows +-8 are lanes +-8 except
-                    // across the two warps of an image (exchange); image borders = warp borders
-                    float* xch = xch0 + (pass * 2 + half) * (32 * 8);   // 32 border rows per tile
-                    float2 mid[3];
+                    // vertical: out[r] = H_-1[r-16] + H_0[r] + H_+1[r+16].  Lanes < 16 (even y) take H_+1 of
+                    // lane +16 and publish their H_+1 for the warp above; lanes >= 16 take H_-1 of lane
+                    // -16 and publish their H_-1 for the warp below.
+                    float* xch = xch0 + (pass * 2 + half) * (128 * 6);
+                    float2 mid[3], pub[3];
 #pragma unroll
                     for (int o = 0; o < 3; o++) {
-                        const float2 up = make_float2(__shfl_up_sync(0xffffffffu, hs[0][o].x, 8), __shfl_up_sync(0xffffffffu, hs[0][o].y, 8));
-                        const float2 dn = make_float2(__shfl_down_sync(0xffffffffu, hs[2][o].x, 8), __shfl_down_sync(0xffffffffu, hs[2][o].y, 8));
-                        const float2 mu = make_float2(lane >= 8 ? 1.f : 0.f, lane >= 8 ? 1.f : 0.f);
-                        const float2 md = make_float2(lane < 24 ? 1.f : 0.f, lane < 24 ? 1.f : 0.f);
-                        mid[o] = t2_add2(t2_fma2(up, mu, t2_fma2(dn, md, hs[1][o])), bb[o]);
+                        const float2 send = lane < 16 ? hs[0][o] : hs[2][o];
+                        const float2 recv = make_float2(__shfl_xor_sync(0xffffffffu, send.x, 16), __shfl_xor_sync(0xffffffffu, send.y, 16));
+                        mid[o] = t2_add2(t2_add2(hs[1][o], recv), bb[o]);
+                        pub[o] = lane < 16 ? hs[2][o] : hs[0][o];
                     }
-                    if (xbot || xtop) {   // publish H_-1 (first warp, lanes 24-31) / H_+1 (second warp, lanes 0-7)
-                        const int u = xbot ? 0 : 2;
-                        const int e = img * 16 + (xbot ? lane - 24 : 8 + lane);
-                        reinterpret_cast<float4*>(xch)[2 * e] = make_float4(hs[u][0].x, hs[u][0].y, hs[u][1].x, hs[u][1].y);
-                        reinterpret_cast<float2*>(xch)[4 * e + 2] = hs[u][2];
-                    }
+#pragma unroll
+                    for (int o = 0; o < 3; o++) reinterpret_cast<float2*>(xch)[3 * r + o] = pub[o];
                     gsync();
-                    if (xbot || xtop) {   // the row 8 above (xtop) / below (xbot), published by the other warp
-                        const int q = img * 16 + (xtop ? lane : 8 + lane - 24);
-                        const float4 o0 = reinterpret_cast<const float4*>(xch)[2 * q];
-                        const float2 o1 = reinterpret_cast<const float2*>(xch)[4 * q + 2];
-                        mid[0] = t2_add2(mid[0], make_float2(o0.x, o0.y));
-                        mid[1] = t2_add2(mid[1], make_float2(o0.z, o0.w));
-                        mid[2] = t2_add2(mid[2], o1);
+                    const int q = lane < 16 ? (y > 0 ? r - 16 : -1) : (y < H - 1 ? r + 16 : -1);
+                    if (q >= 0) {
+#pragma unroll
+                        for (int o = 0; o < 3; o++) mid[o] = t2_add2(mid[o], reinterpret_cast<const float2*>(xch)[3 * q + o]);
                     }
 #pragma unroll
                     for (int o = 0; o < 3; o++) {
@@ -453,9 +452,6 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
                 }
                 if (write_next) {
                     gsync();   // the pixel's 24 updated channels come from both halves and both passes
-                    // the shared views are free once the other slot's conv1 has completed
-                    if (g == 0) mbar_wait(&a1t[1], par);
-                    else mbar_wait(&a1t[0], (kb + 1) & 1);
                     write_views(out_off, nimg);
                     fence_proxy_async();
                     mbar_arrive(&x_rdy[g]);

@@ -2326,20 +2326,23 @@ static void put_tile(std::vector<uint16_t>& out, const std::vector<float>& w, in
 static void pack_block(const StagePlan& p, const float* W1, const float* b1, const float* W2, int pm,
                        std::vector<uint16_t>& out) {
     const int c = p.c, m = p.m;
-    if (p.ts == 2) {   // k_stage_ts2: conv1 over the 28 view planes, conv2 in two 112-column passes
+    if (p.ts == 2) {   // k_stage_ts2: conv1 over (row shift, view, plane) pairs, conv2 in two 112-column passes
         std::vector<float> tile;
-        for (int s = 0; s < 14; s++) {   // plane L = 2s + kk/8: tap L/3, channels 8 (L%3)..; L = 27: bias
+        // conv1 k-step s (k_stage_ts2 k1_start / k1_lbo): s < 12: vertical tap u = s/4 - 1, view planes
+        // P = 2 (s%4) + half (view v = P/3 - 1, channels 8 (P%3)..); s = 12: plane 8 at u = -1 | u = 0;
+        // s = 13: plane 8 at u = +1 | the constant-1 plane (the folded bias b1)
+        for (int s = 0; s < 14; s++) {
             tile.assign((size_t)128 * 16, 0.f);
             for (int h = 0; h < m; h++)
                 for (int kk = 0; kk < 16; kk++) {
-                    const int L = 2 * s + kk / 8, e = kk % 8;
-                    float v = 0.f;
-                    if (L < 27) {
-                        const int tap = L / 3, ci = 8 * (L % 3) + e;
-                        v = W1[(((size_t)h * c + ci) * 3 + tap / 3) * 3 + tap % 3];
-                    } else if (e == 0) {
-                        v = b1[h];
-                    }
+                    const int hf = kk / 8, e = kk % 8;
+                    int u, P;
+                    if (s < 12) { u = s / 4 - 1; P = 2 * (s % 4) + hf; }
+                    else if (s == 12) { u = hf - 1; P = 8; }
+                    else { u = 1; P = hf ? 9 : 8; }
+                    float v;
+                    if (P == 9) v = e == 0 ? b1[h] : 0.f;
+                    else v = W1[(((size_t)h * c + 8 * (P % 3) + e) * 3 + (u + 1)) * 3 + P / 3];
                     tile[(size_t)h * 16 + kk] = v;
                 }
             put_tile(out, tile, 128, pm);
