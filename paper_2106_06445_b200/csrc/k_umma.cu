@@ -79,7 +79,9 @@ struct StagePlan {
     uint32_t sstate_off;   // byte offset of the fp32 state region in dynamic smem
     int stk1, stk2;        // stacked f16x3 for conv1 / conv2 (mma_prec): B tiles of 2N rows, 2N
                            // accumulator columns per tile (specialised kernels only)
-    int nopad;             // raster without pad column (Wp = W): conv1's horizontal taps stacked in
+    int nopad;             // 2: image-row-interleaved raster (see row_pixel): Wp = I W (one tile of
+                           //    I = 128 / (H W) images), 16 guard rows shared between planes
+                           // 1: raster without pad column (Wp = W): conv1's horizontal taps stacked in
                            // N as well (3 MC columns, masked col2im in the epilogue), conv2 hst
     int n1;                // conv1 segment width: MC, or 3 MC with nopad
     int ts;                // TS-mode stage kernel (k_stage_ts.cu): no-pad raster with l/c/r views,
@@ -147,6 +149,13 @@ __device__ __forceinline__ float bf16_val(uint32_t b) {
 
 // pixel row r of a batch -> (image in batch, y, x), or false for pad/zero rows
 __device__ __forceinline__ bool row_pixel(int r, const StagePlan& p, int& ii, int& y, int& x) {
+    if (p.nopad == 2) {   // interleaved: r = Wp y + W ii + x, no pad rows
+        y = r / p.Wp;
+        const int rem = r - y * p.Wp;
+        ii = rem / p.W;
+        x = rem - ii * p.W;
+        return y < p.H;
+    }
     int band = r / p.Wp;
     x = r - band * p.Wp;
     ii = band / (p.H + 1);
@@ -397,6 +406,10 @@ struct SCfg {
     // no-pad raster (StagePlan::nopad): Wp = W, both convolutions take their horizontal taps as
     // N-stacked column groups and the epilogues do a masked col2im
     static constexpr bool NOPAD = NOPAD_ != 0;
+    // NOPAD_ == 2: image-row-interleaved raster, row r = WP y + W img + x (WP = I W), so a vertical
+    // tap is a shift of WP rows that never leaves the image; 16 guard rows per plane side, shared
+    // with the neighbouring plane (a shift of WP = 32 rows reads the neighbour's guard)
+    static constexpr bool ILV = NOPAD_ == 2;
     static_assert(!NOPAD_ || (HST_ && !RES_), "no-pad raster: horizontal taps stacked in both convolutions");
     // stacked f16x3 (mma_prec): conv1 / conv2 B tiles of 2N rows, accumulators 2N columns per tile
     static constexpr int STK1 = STK1_, STK2 = STK2_;
@@ -411,10 +424,10 @@ struct SCfg {
     static constexpr int HC = HST_ ? (C_ + 7) / 8 * 8 : 0;   // == StagePlan::hc
     static constexpr bool kStatic = WP_ > 0;
     static constexpr int WP = WP_, CP = CP_, MC = MC_, NC2 = NC2_, T = T_, SLOT = SLOT_;
-    static constexpr int H = H_, W = NOPAD_ ? WP_ : WP_ - 1, C = C_, SST = SST_;
+    static constexpr int H = H_, W = NOPAD_ == 2 ? H_ : (NOPAD_ ? WP_ : WP_ - 1), C = C_, SST = SST_;
     static constexpr int PM = PM_;            // StagePlan::pm
     static constexpr bool P3 = PM_ != 0;      // activations split into fp16 hi + lo planes
-    static constexpr int G = WP + 2;
+    static constexpr int G = ILV ? 16 : WP + 2;
     static constexpr int RTOT = T * 128 + 2 * G;
     static constexpr int PLANE16 = RTOT;                 // plane bytes / 16
     static constexpr bool PAIR = CP == 8;
@@ -496,11 +509,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
 
     // ---- shared memory carve-up
     uint8_t* ring = smem;                                           // nslot * slot_bytes
-    uint8_t* xbuf = ring + (size_t)p.nslot * p.slot_bytes;          // P * Cp/8 planes
+    const size_t ilv_pad = p.nopad == 2 ? 256 : 0;                   // zero rows a -WP shift of plane 0 reads
+    uint8_t* xbuf = ring + (size_t)p.nslot * p.slot_bytes + ilv_pad;  // P * Cp/8 planes
     const uint32_t plane_bytes = (uint32_t)p.Rtot * 16;
     uint8_t* hbuf = xbuf + (size_t)P * (p.Cp / 8) * plane_bytes;    // nhd x (P * MC/8 planes)
     const size_t hbuf_stride = (size_t)P * (p.MC / 8) * plane_bytes;
-    float* xchg = reinterpret_cast<float*>(hbuf + (size_t)p.nhd * hbuf_stride);     // hst exchange
+    float* xchg = reinterpret_cast<float*>(hbuf + (size_t)p.nhd * hbuf_stride + ilv_pad);   // hst exchange
     uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(xchg) + p.xchg_bytes);
     uint64_t* full = bars;                  // [kMaxSlots]
     uint64_t* empty = bars + kMaxSlots;     // [kMaxSlots]
@@ -531,8 +545,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
     // ---- zero the activation buffers (pads and guards must read as 0)
     {
         uint4 z = make_uint4(0, 0, 0, 0);
-        size_t nbytes = (size_t)P * ((p.Cp + p.nhd * p.MC) / 8) * plane_bytes;
-        for (size_t i = tid; i < nbytes / 16; i += kThreads) reinterpret_cast<uint4*>(xbuf)[i] = z;
+        size_t nbytes = (size_t)P * ((p.Cp + p.nhd * p.MC) / 8) * plane_bytes + 2 * ilv_pad;
+        for (size_t i = tid; i < nbytes / 16; i += kThreads) reinterpret_cast<uint4*>(xbuf - ilv_pad)[i] = z;
     }
     fence_proxy_async();
     if (warp == 1) tmem_alloc(tmem_slot, p.tmem_cols);
@@ -928,6 +942,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
         const bool any2 = cb2 < ec;                    // this half owns at least one real channel
         unsigned long long w_a1 = 0, w_he = 0, w_a2 = 0, t_ld = 0, t_e1 = 0, t_e2 = 0, t_start = CLK();
         auto rowpix = [&](int r, int& ii, int& y, int& x) -> bool {
+            if ((S && CFG::ILV) || (!S && p.nopad == 2)) {   // interleaved: r = Wp y + W ii + x
+                y = r / eWp;
+                const int rem = r - y * eWp;
+                ii = rem / eW;
+                x = rem - ii * eW;
+                return y < eH;
+            }
             const int band = r / eWp;
             x = r - band * eWp;
             ii = band / (eH + 1);
@@ -2160,6 +2181,7 @@ static const TunedPlan kTuned[] = {
     {8, 8, 24, 128, 2, 128, 2, 1, 3, 1},   // stage 2 f16x3
     {16, 16, 6, 64, 2, 32, 5, 1, 4, 1, 1, 0},    // stage 1 f16x3, stacked conv1 (CI_NO_STK: unstacked)
     {16, 16, 6, 64, 2, 32, 5, 1, 4, 1},    // stage 1 f16x3
+    {4, 4, 96, 256, 2, 64, 1, 2, 4, 1, 0, 0, 2},  // stage 3 f16x3, interleaved raster, 8 images per tile (CI_NO_ILV)
     {4, 4, 96, 256, 2, 64, 1, 2, 4, 1, 0, 0, 1},  // stage 3 f16x3, no-pad raster (CI_NO_NOPAD: padded)
     {4, 4, 96, 256, 2, 128, 1, 1, 4, 0, 1, 1},   // stage 3 f16x3, stacked conv1 + conv2
     {16, 16, 64, 64, 2, 32, 3, 1, 4, 0, 1, 0},   // learned-encoder tail f16x3, stacked conv1
@@ -2179,6 +2201,7 @@ static bool make_plan(const StageInfo& S, int pm, StagePlan& best, bool allow_st
     static const bool no_tuned = getenv("CI_NO_TUNED") != nullptr;         // A/B switch: cost model only
     static const bool no_stk = getenv("CI_NO_STK") != nullptr;             // A/B switch: unstacked f16x3
     static const bool no_nopad = getenv("CI_NO_NOPAD") != nullptr;         // A/B switch: padded raster
+    static const bool no_ilv = getenv("CI_NO_ILV") != nullptr;             // A/B switch: no interleaved raster
     // CI_TUNE="H,W,c,m,pm,MC,T,nhd,nslot,hst;..." overrides the table (same-box plan A/B)
     static const std::vector<TunedPlan> env_tuned = [] {
         std::vector<TunedPlan> v;
@@ -2199,11 +2222,16 @@ static bool make_plan(const StageInfo& S, int pm, StagePlan& best, bool allow_st
     if (!no_tuned)
     for (const auto& tp : kTuned)   // first match wins
         if (!tuned && tp.H == S.H && tp.W == S.W && tp.c == S.c && tp.m == S.m && tp.pm == pm &&
-            !((no_stk || !allow_stk) && (tp.stk1 || tp.stk2)) && !((no_nopad || !allow_stk) && tp.nopad) && !(no_wide_hst && tp.hst && tp.c > 8) && !(tp.c == 24 && !tp.pm && tp.MC == 64 && tp.hst && s1_mc32) &&
+            !((no_stk || !allow_stk) && (tp.stk1 || tp.stk2)) && !((no_nopad || !allow_stk) && tp.nopad) && !(no_ilv && tp.nopad == 2) && !(no_wide_hst && tp.hst && tp.c > 8) && !(tp.c == 24 && !tp.pm && tp.MC == 64 && tp.hst && s1_mc32) &&
             !(tp.c == 24 && !tp.pm && tp.MC == 128 && tp.hst && (s1_mc64 || s1_mc32)))
             tuned = &tp;
     p.nopad = (tuned && allow_stk) ? tuned->nopad : 0;
     p.H = S.H; p.W = S.W; p.Wp = p.nopad ? S.W : S.W + 1; p.G = p.Wp + 2;
+    if (p.nopad == 2) {   // one tile of 128 / (H W) images, rows interleaved by image row
+        if (128 % (S.H * S.W)) return false;
+        p.Wp = (128 / (S.H * S.W)) * S.W;
+        p.G = 16;
+    }
     p.c = S.c; p.m = S.m;
     p.Cp = S.c <= 8 ? 8 : rup(S.c, 16);
     p.Mp = rup(S.m, 16);
@@ -2213,7 +2241,7 @@ static bool make_plan(const StageInfo& S, int pm, StagePlan& best, bool allow_st
     p.pm = pm;
     const int P = pm ? 2 : 1;
     const double P3f = 1.0 + pm;   // MMAs per k-step: f16x2 hi(A)*B + lo(A)*B, f16x3 + hi(A)*lo(B)
-    const int img_rows = (p.H + 1) * p.Wp;
+    const int img_rows = p.nopad == 2 ? p.H * p.W : (p.H + 1) * p.Wp;
     if (p.nopad) p.pair = p.tri = 0;
     const int k1 = p.nopad ? 3 * (p.Cp / 16) : (p.pair ? kPairK1 : (p.tri ? kTriK1 : 9 * (p.Cp / 16)));
     p.stk1 = (tuned && pm == 2 && allow_stk) ? tuned->stk1 : 0;
@@ -2240,6 +2268,7 @@ static bool make_plan(const StageInfo& S, int pm, StagePlan& best, bool allow_st
         for (int T = 1; T <= 8; T++) {
             if (T * (n1 * (1 + p.stk1) + p.Nc2 * (1 + p.stk2)) > 512) break;
             if (tuned && T != tuned->T) continue;
+            if (p.nopad == 2 && T != 1) continue;   // interleaved raster: one tile
             const int I = (T * 128) / img_rows;
             if (I < 1) continue;
             for (int nhd = (nch >= 2 ? 2 : 1); nhd >= 1; nhd--) {
@@ -2250,6 +2279,7 @@ static bool make_plan(const StageInfo& S, int pm, StagePlan& best, bool allow_st
                     const int Rtot = T * 128 + 2 * p.G;
                     const int xchg = (p.hst && !p.nopad) ? T * 4 * 2 * p.hc * 4 : 0;   // no-pad: rows 4-aligned, no exchange
                     const size_t smem0 = (size_t)nslot * slot_bytes + (size_t)P * ((p.Cp + nhd * MC) / 8) * Rtot * 16 +
+                                         (p.nopad == 2 ? 512 : 0) +
                                          kBarBytes + (size_t)rup(xchg, 16);
                     if (smem0 > kSmemCap) continue;
                     const size_t state_bytes = (size_t)I * S.C * p.H * p.W * 4;
@@ -2473,6 +2503,7 @@ static const SpecEntry kSpecs[] = {
     CI_SPEC_XS(17, 8, 32, 32, 5, 2, 16384, 16, 6, 1, 1, 0, 1, 0),   // C stage 1, f16x3, stacked conv1
     CI_SPEC_XS(5, 96, 128, 96, 1, 2, 16384, 4, 96, 0, 0, 0, 1, 1),  // C stage 3, f16x3, stacked conv1 + conv2
     CI_SPEC_XN(4, 96, 64, 288, 1, 2, 18432, 4, 96, 0, 1, 0, 0, 0, 1),   // C stage 3, f16x3, no-pad raster
+    CI_SPEC_XN(32, 96, 64, 288, 1, 2, 18432, 4, 96, 0, 1, 0, 0, 0, 2),  // C stage 3, f16x3, interleaved raster
     CI_SPEC_XS(9, 32, 64, 80, 2, 2, 16384, 8, 24, 0, 1, 0, 1, 0),   // C stage 2, f16x3, MC = 64 stacked (A/B)
     CI_SPEC_XS(17, 64, 32, 64, 3, 2, 16384, 16, 64, 0, 0, 0, 1, 0), // encoder tail, f16x3, stacked conv1
     CI_SPEC(17, 64, 32, 64, 5, 0, 16384, 16, 64, 0),  // learned-encoder tail (E2, E3), bf16
