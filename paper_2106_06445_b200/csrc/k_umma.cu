@@ -2171,12 +2171,14 @@ static const TunedPlan kTuned[] = {
     {8, 8, 24, 128, 0, 64, 3, 2, 3, 1},    // stage 2 bf16: wide hst, N = 64 conv1, T = 3 (CI_S1_MC64)
     {8, 8, 24, 128, 0, 32, 4, 2, 3, 1},    // stage 2 bf16: wide hst, N = 32 conv1, T = 4 (CI_S1_MC32)
     {8, 8, 24, 128, 0, 32, 7, 2, 3, 0},    // stage 2 bf16, plain conv2 (CI_NO_WIDE_HST)
+    {4, 4, 96, 256, 0, 64, 1, 2, 4, 1, 0, 0, 2},  // stage 3 bf16, interleaved raster (CI_NO_ILV: padded)
     {4, 4, 96, 256, 0, 128, 2, 1, 4, 0},   // stage 3 bf16
     // split-activation precisions (f16x2, f16x3: two SMEM planes per 8 channels): the cost
     // model's picks, measured 18-22% per stage faster than the round-1 bf16x3 plans (MC = 16 /
     // 64 / 64) -- MMA count, not SMEM, bounds these stages
     {16, 16, 6, 64, 1, 32, 5, 1, 4, 1},    // stage 1 f16x2: MC = 32, T = 5, SMEM state
     {8, 8, 24, 128, 1, 128, 2, 1, 3, 1},   // stage 2 f16x2: wide hst, one N = 128 conv1 chunk
+    {4, 4, 96, 256, 1, 64, 1, 2, 4, 1, 0, 0, 2},  // stage 3 f16x2, interleaved raster (CI_NO_ILV: padded)
     {4, 4, 96, 256, 1, 128, 1, 1, 4, 0},   // stage 3 f16x2: N = 128 conv1 chunks, T = 1
     {8, 8, 24, 128, 2, 128, 2, 1, 3, 1},   // stage 2 f16x3
     {16, 16, 6, 64, 2, 32, 5, 1, 4, 1, 1, 0},    // stage 1 f16x3, stacked conv1 (CI_NO_STK: unstacked)
@@ -2504,6 +2506,8 @@ static const SpecEntry kSpecs[] = {
     CI_SPEC_XS(5, 96, 128, 96, 1, 2, 16384, 4, 96, 0, 0, 0, 1, 1),  // C stage 3, f16x3, stacked conv1 + conv2
     CI_SPEC_XN(4, 96, 64, 288, 1, 2, 18432, 4, 96, 0, 1, 0, 0, 0, 1),   // C stage 3, f16x3, no-pad raster
     CI_SPEC_XN(32, 96, 64, 288, 1, 2, 18432, 4, 96, 0, 1, 0, 0, 0, 2),  // C stage 3, f16x3, interleaved raster
+    CI_SPEC_XN(32, 96, 64, 288, 1, 1, 16384, 4, 96, 0, 1, 0, 0, 0, 2),  // C stage 3, f16x2, interleaved raster
+    CI_SPEC_XN(32, 96, 64, 288, 1, 0, 16384, 4, 96, 0, 1, 0, 0, 0, 2),  // C stage 3, bf16, interleaved raster
     CI_SPEC_XS(9, 32, 64, 80, 2, 2, 16384, 8, 24, 0, 1, 0, 1, 0),   // C stage 2, f16x3, MC = 64 stacked (A/B)
     CI_SPEC_XS(17, 64, 32, 64, 3, 2, 16384, 16, 64, 0, 0, 0, 1, 0), // encoder tail, f16x3, stacked conv1
     CI_SPEC(17, 64, 32, 64, 5, 0, 16384, 16, 64, 0),  // learned-encoder tail (E2, E3), bf16
