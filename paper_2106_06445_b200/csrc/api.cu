@@ -85,9 +85,35 @@ static T* at(void* ws, size_t off) { return reinterpret_cast<T*>(reinterpret_cas
 // ---------------------------------------------------------------------------
 // h / h^-1 orchestration (both precisions share the stage-boundary permutations)
 // ---------------------------------------------------------------------------
+// Stage-boundary permutations fused into the TS stage kernels' load / store (stage_io.cuh): possible
+// when every psi between two stages -- and the copy of x into the first stage -- is adjacent to a
+// TS stage.  Then h runs in place in one buffer and no k_permute pass is launched.
+static bool fused_io_forward(const Model* m) {
+    static const bool off = getenv("CI_NO_FUSED_IO") != nullptr;   // A/B switch: separate k_permute passes
+    if (off) return false;
+    const int S = m->n_stages;
+    if (!umma_stage_fuses_io(m, 0)) return false;
+    for (int s = 1; s < S; s++)
+        if (m->st[s].squeeze && !umma_stage_fuses_io(m, s - 1) && !umma_stage_fuses_io(m, s)) return false;
+    return true;
+}
+static bool fused_io_inverse(const Model* m) { return fused_io_forward(m); }   // same boundaries, reversed
+
 static ci_status_t forward_impl(const Model* m, const float* x, float* h, int64_t n, void* ws,
                                 const WsLayout& L, cudaStream_t st) {
     if (n == 0) return CI_OK;
+    if (fused_io_forward(m)) {
+        const int S = m->n_stages;
+        for (int s = 0; s < S; s++) {
+            const bool ts = umma_stage_fuses_io(m, s);
+            // layouts (stage_io.cuh): 1 = the previous stage's (psi on load), 2 = the next stage's (psi on store)
+            const int in_mode = ts && m->st[s].squeeze && (s == 0 || !umma_stage_fuses_io(m, s - 1)) ? 1 : 0;
+            const int out_mode = ts && s + 1 < S && m->st[s + 1].squeeze ? 2 : 0;
+            ci_status_t r = umma_stage_io(m, s, s == 0 ? x : h, in_mode, h, out_mode, n, false, next_ctr(ws, L), st);
+            if (r != CI_OK) return r;
+        }
+        return CI_OK;
+    }
     float* scratch = at<float>(ws, L.scratch);
     // stage s starts with a copy (psi or identity) into buffer buf[s]; last buffer = h
     const int S = m->n_stages;
@@ -111,6 +137,27 @@ static ci_status_t inverse_impl(const Model* m, const float* h, float* x, int64_
     if (n == 0) return CI_OK;
     float* scratch = at<float>(ws, L.scratch);
     const int S = m->n_stages;
+    if (fused_io_inverse(m)) {
+        // cur: the working buffer (h itself when the caller hands it over); the last stage reads h
+        // directly when it is a TS stage, otherwise h is copied into cur first
+        float* cur = consume_h ? const_cast<float*>(h) : scratch;
+        const bool ts_last = umma_stage_fuses_io(m, S - 1);
+        if (!consume_h && !ts_last) {
+            const StageInfo& L3 = m->st[S - 1];
+            CI_CUDA(launch_permute(h, cur, n, L3.C, L3.H, L3.W, 0, st));
+        }
+        for (int s = S - 1; s >= 0; s--) {
+            const bool ts = umma_stage_fuses_io(m, s);
+            const float* src = (s == S - 1 && ts) ? h : cur;
+            float* dst = s == 0 ? x : cur;
+            // layouts: 2 = the next stage's (psi^-1 on load), 1 = the previous stage's (psi^-1 on store)
+            const int in_mode = ts && s + 1 < S && m->st[s + 1].squeeze && !umma_stage_fuses_io(m, s + 1) ? 2 : 0;
+            const int out_mode = ts && m->st[s].squeeze ? 1 : 0;
+            ci_status_t r = umma_stage_io(m, s, src, in_mode, dst, out_mode, n, true, next_ctr(ws, L), st);
+            if (r != CI_OK) return r;
+        }
+        return CI_OK;
+    }
     // copies: [1 initial] + 1 after each stage, the last one lands in x
     int ncopy = consume_h ? S : S + 1, ci = 0;
     auto target = [&](int i) { return ((ncopy - 1 - i) % 2 == 0) ? x : scratch; };

@@ -127,6 +127,11 @@ ci_status_t umma_prepare(Model* m, const float* host_params);
 void umma_release(Model* m);
 // Runs one stage (all blocks) on the fp32 NCHW state `state` [n][C][H][W] in place.
 // ctr: a zeroed int the launch claims batches from (null: static round-robin batches).
+// TS stages can read their input from src (layout in_mode) and write to dst (layout out_mode),
+// stage_io.cuh; every other stage runs in place in its own layout (src == dst, modes 0).
+bool umma_stage_fuses_io(const Model* m, int stage);
+ci_status_t umma_stage_io(const Model* m, int stage, const float* src, int in_mode, float* dst, int out_mode,
+                          int64_t n, bool inverse, int* ctr, cudaStream_t s);
 ci_status_t umma_stage(const Model* m, int stage, float* state, int64_t n, bool inverse,
                        int* ctr, cudaStream_t s);
 // Learned-encoder tail: zbuf [n][2*4c1][H/2][W/2]; channels [0,4c1) = psi(mean first layer) in,
@@ -137,7 +142,13 @@ bool umma_has_encoder(const Model* m);   // the encoder tail has a tcgen05 plan
 // TS-mode stage kernel (k_stage_ts.cu): Arch C stage 1 (16x16, c = 6, m = 64, coupling + ReLU)
 // with the hidden activation kept in tensor memory
 struct TsArgs {
-    float* state;            // [n][C][H][W] fp32, updated in place
+    // images in global memory: read from src in layout in_mode, written to dst in layout out_mode
+    // (stage_io.cuh: 0 = the stage's own [C][H][W], 1 = the previous stage's, 2 = the next
+    // stage's, i.e. psi / psi^-1 fused into the load / store).  src == dst is allowed (each image
+    // is read completely before it is written; all layouts have the same size).
+    const float* src;
+    float* dst;
+    int in_mode, out_mode;
     int64_t n;               // images
     const uint8_t* wpack;    // stage stream: block t at t * blk_bytes (pack_block, StagePlan::ts)
     int64_t blk_bytes;

@@ -35,6 +35,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include "stage_io.cuh"
 #include "umma.cuh"
 
 namespace ci {
@@ -337,13 +338,9 @@ __global__ void __launch_bounds__(ts::kThreads, 1) k_stage_ts(TsArgs a) {
             put(0, 1, xx < W - 1);   // Xl[p+1] = X[p]
             put(2, -1, xx > 0);      // Xr[p-1] = X[p]
         };
-        // image state -> shared-memory buffer (16-B cp.async, completes on wait_all)
+        // image state (src, layout in_mode) -> shared-memory buffer (cp.async, completes on wait_all)
         auto fetch_state = [&](int64_t bb, float* dst) {
-            const float* src = a.state + bb * (int64_t)C * HW;
-            for (int q = et; q < C * HW / 4; q += kEpi)
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst + 4 * q)), "l"(src + 4 * q)
-                             : "memory");
-            asm volatile("cp.async.commit_group;" ::: "memory");
+            io_fetch_async<C, H, W>(a.src + bb * (int64_t)C * HW, a.in_mode, dst, et, kEpi);
         };
         auto in_half = [&](int t) { return ((a.first_orient + t) & 1) == 0 ? 0 : c; };
         uint32_t kb = 0;
@@ -353,7 +350,7 @@ __global__ void __launch_bounds__(ts::kThreads, 1) k_stage_ts(TsArgs a) {
             const int64_t b = bq_read(qe);
             mbar_arrive(&bqe[qe & 3]);
             if (b >= nbatch) break;
-            float* gst = a.state + b * (int64_t)C * HW;
+            float* gst = a.dst + b * (int64_t)C * HW;
             float* st = sstate(g) + (i & 1) * (C * HW);
             // ---- image state -> shared memory (prefetched during the previous image's last blocks)
             if (!prefetched) fetch_state(b, st);
@@ -509,11 +506,7 @@ __global__ void __launch_bounds__(ts::kThreads, 1) k_stage_ts(TsArgs a) {
             }
             // ---- state back to global memory
             gsync();
-            {
-                float4* dst = reinterpret_cast<float4*>(gst);
-                const float4* src = reinterpret_cast<const float4*>(sstate(g) + (i & 1) * (C * HW));
-                for (int q = et; q < C * HW / 4; q += kEpi) __stcg(dst + q, src[q]);
-            }
+            io_store<C, H, W>(gst, a.out_mode, sstate(g) + (i & 1) * (C * HW), et, kEpi);   // layout out_mode
         }
     }
     fence_before();

@@ -26,6 +26,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include "stage_io.cuh"
 #include "umma.cuh"
 
 namespace ci {
@@ -345,12 +346,10 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
             if (b >= nbatch) break;
             const int64_t img0 = 2 * b;
             const int nimg = a.n - img0 < 2 ? 1 : 2;
-            float* gst = a.state + img0 * (int64_t)C * HW;
-            {   // the slot's state -> shared memory
-                const float4* src = reinterpret_cast<const float4*>(gst);
-                float4* dst = reinterpret_cast<float4*>(st);
-                for (int q = et; q < nimg * C * HW / 4; q += kEpi) dst[q] = __ldcg(src + q);
-            }
+            float* gst = a.dst + img0 * (int64_t)C * HW;
+            // the slot's state (src, layout in_mode) -> shared memory
+            for (int ii = 0; ii < nimg; ii++)
+                io_load<C, H, W>(a.src + (img0 + ii) * (int64_t)C * HW, a.in_mode, st + ii * C * HW, et, kEpi);
             gsync();
             write_views(in_half(a.inverse ? a.nb - 1 : 0), nimg);
             fence_proxy_async();
@@ -459,11 +458,8 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
             }
             // ---- state back to global memory
             gsync();
-            {
-                float4* dst = reinterpret_cast<float4*>(gst);
-                const float4* src = reinterpret_cast<const float4*>(st);
-                for (int q = et; q < nimg * C * HW / 4; q += kEpi) __stcg(dst + q, src[q]);
-            }
+            for (int ii = 0; ii < nimg; ii++)   // layout out_mode
+                io_store<C, H, W>(gst + ii * C * HW, a.out_mode, st + ii * C * HW, et, kEpi);
             gsync();
         }
     }

@@ -2772,9 +2772,24 @@ ci_status_t umma_encoder_tail(const Model* m, float* zbuf, int64_t n, int* ctr, 
     return CI_OK;
 }
 
+bool umma_stage_fuses_io(const Model* m, int s) {
+    const UmmaState* U = reinterpret_cast<const UmmaState*>(m->umma_state);
+    return U && U->plan[s].ts != 0;
+}
+
 ci_status_t umma_stage(const Model* m, int s, float* state, int64_t n, bool inverse, int* ctr, cudaStream_t st) {
+    return umma_stage_io(m, s, state, 0, state, 0, n, inverse, ctr, st);
+}
+
+ci_status_t umma_stage_io(const Model* m, int s, const float* src, int in_mode, float* dst, int out_mode, int64_t n,
+                          bool inverse, int* ctr, cudaStream_t st) {
     if (n == 0) return CI_OK;
     const UmmaState* U = reinterpret_cast<const UmmaState*>(m->umma_state);
+    if (!U->plan[s].ts && (src != dst || in_mode || out_mode)) {
+        set_error("internal: stage %d runs in place in its own layout only", s);
+        return CI_ERR_UNSUPPORTED;
+    }
+    float* state = dst;
     StageArgs a;
     a.p = U->plan[s];
     a.state = state;
@@ -2792,7 +2807,10 @@ ci_status_t umma_stage(const Model* m, int s, float* state, int64_t n, bool inve
     a.fp_iters = a.residual ? m->arch.fp_iters : 1;
     if (a.p.ts) {
         TsArgs t;
-        t.state = state;
+        t.src = src;
+        t.dst = dst;
+        t.in_mode = in_mode;
+        t.out_mode = out_mode;
         t.n = n;
         t.wpack = a.wpack;
         t.blk_bytes = a.p.blk_bytes;
