@@ -356,6 +356,18 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
             mbar_arrive(&x_rdy[g]);
             for (int tt = 0; tt < a.nb; tt++, kb++) {
                 const uint32_t par = kb & 1;
+                if (tt == a.nb - 3) {   // L2 prefetch of the group's next batch, if the producer has published it
+                    const int qn = qe + 2;
+                    if (mbar_test(&bqf[qn & 3], (uint32_t)((qn >> 2) & 1))) {
+                        const int64_t bn = bq[qn & 3];
+                        if (bn < nbatch) {
+                            const int64_t in0 = 2 * bn, nb_img = a.n - in0 < 2 ? 1 : 2;
+                            const char* pf = reinterpret_cast<const char*>(a.src + in0 * (int64_t)C * HW);
+                            for (int off = et * 128; off < nb_img * C * HW * 4; off += kEpi * 128)
+                                asm volatile("prefetch.global.L2 [%0];" ::"l"(pf + off));
+                        }
+                    }
+                }
                 const int t = a.inverse ? a.nb - 1 - tt : tt;
                 const int out_off = c - in_half(t);
                 const bool write_next = tt + 1 < a.nb;
