@@ -194,8 +194,13 @@ struct AOff {
     int shift, poff16;   // A start: row shift, plane offset (16-B units)
     uint32_t lbo_add;    // added to the descriptor low word: LBO field delta (bits 16-29)
 };
+// conv1 of the interleaved raster (am 3): k-steps channel-group major, in the order the conv2
+// epilogue finishes the groups (16-channel group kc = ilv_group(s / 3), vertical tap u = s % 3 - 1),
+// so the next block's conv1 starts once the first groups of X are final (x_grp barriers)
+__host__ __device__ constexpr int ilv_group(int j) { return (j >> 1) + (j & 1) * 3; }
 __host__ __device__ constexpr AOff a_off(int s, int am, bool hstk, int per, int wp, int plane16) {
     if (am == 1) return AOff{pair_shift(s, wp), 0, pair_lbo_add(s, wp)};
+    if (am == 3) return AOff{(s % 3 - 1) * wp, 2 * ilv_group(s / 3) * plane16, 0u};
     if (am == 2) {
         if (s < 9) return AOff{(s / 3 - 1) * wp + (s % 3 - 1), 0, 0u};
         const int q = s - 9;
@@ -247,7 +252,8 @@ template <int K, int PER, int AM, int WP, int PLANE16, int G, int KB16, int T, i
           int LOA16, int ACC0, int DSTRIDE, bool HSTK = false, int STK = 0>
 __device__ __forceinline__ void issue_static(uint32_t tmem, uint32_t alo0, uint32_t ringlo, uint32_t slot16,
                                              uint32_t idesc, uint32_t acc_first, int& slot, uint32_t& phase,
-                                             int nslot, uint64_t* full, uint64_t* empty, uint32_t idescw = 0) {
+                                             int nslot, uint64_t* full, uint64_t* empty, uint32_t idescw = 0,
+                                             uint64_t* xgrp = nullptr, uint32_t xgph = 0) {
     constexpr uint32_t HI = 0x4008u;   // SBO = 128 B, descriptor version 1
     uint32_t bl = 0;
     // opaque to the optimiser: keeps ptxas from hoisting every k-step's descriptor constant out
@@ -255,6 +261,10 @@ __device__ __forceinline__ void issue_static(uint32_t tmem, uint32_t alo0, uint3
     asm volatile("" : "+r"(alo0), "+r"(ringlo));
 #pragma unroll
     for (int s = 0; s < K; s++) {
+        if (AM == 3 && xgrp && s % 6 == 0) {   // channel groups ilv_group(2i), ilv_group(2i+1) of X final
+            mbar_wait(&xgrp[s / 6], xgph);
+            fence_after();
+        }
         if (s % G == 0) {
             mbar_wait(&full[slot], phase);
             fence_after();
@@ -435,7 +445,8 @@ struct SCfg {
     static constexpr bool SPLIT = !HST && C_ % 8 == 0 && C_ / 2 < NC2_ / 2 &&
                                   (NC2_ / 2 == 8 || NC2_ / 2 == 16 || NC2_ / 2 == 32 || NC2_ / 2 == 48);
     static constexpr bool TRI = CP_ == 32 && C_ == 24;   // == StagePlan::tri
-    static constexpr int AM1 = PAIR ? 1 : (TRI ? 2 : 0);  // conv1 A-operand mode (a_off)
+    static constexpr int AM1 = PAIR ? 1 : (TRI ? 2 : (NOPAD_ == 2 && CP_ == 96 ? 3 : 0));  // conv1 A mode (a_off)
+    static constexpr bool XGRP = AM1 == 3;   // per-channel-group X hand-off (x_grp) for conv1 chunk 0
     static constexpr int PER1 = PAIR ? 2 : CP / 16;
     static constexpr int K1 = NOPAD ? 3 * (CP / 16) : (PAIR ? kPairK1 : (TRI ? kTriK1 : 9 * (CP / 16)));
     static constexpr int N1 = NOPAD ? 3 * MC : MC;   // conv1 columns per tile: 3 tap groups when no-pad
@@ -481,7 +492,7 @@ constexpr bool kXPrefetch = false;   // A/B switch
 constexpr bool kXPrefetch = true;    // cross-batch X prefetch (epilogue, see x_pref)
 #endif
 constexpr int kMaxTiles = 8;                     // T <= 8 (512 TMEM columns / >= 64 per tile)
-constexpr int kBarBytes = 1088;                  // mbarriers, TMEM slot, batch queue, staged conv2 bias
+constexpr int kBarBytes = 1152;                  // mbarriers, TMEM slot, batch queue, staged conv2 bias
 
 // Cycle instrumentation (CI_DEBUG_CYCLES; inactive unless requested).  -DCI_NO_CYCLES
 // compiles it out; same-box A/B showed no gain from that (s2 got slower), so it stays in.
@@ -541,6 +552,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
     // tcgen05.commit per tile), so the next chunk's conv1 epilogue may overwrite the hidden rows of
     // tile t-1 once tile t is done, instead of waiting for the whole chunk (hd_empty)
     uint64_t* h2t = x_full + 116;      // [kMaxTiles]
+    // interleaved stage 3 (SCfg::XGRP): x_grp[i] = 16-channel groups ilv_group(2i), ilv_group(2i+1) of
+    // the X planes are final (conv2 epilogue iteration i), so conv1 chunk 0 streams in behind it
+    uint64_t* x_grp = x_full + 124;    // [3]
 
     // ---- zero the activation buffers (pads and guards must read as 0)
     {
@@ -553,6 +567,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
     if (tid == 0) {
         for (int i = 0; i < p.nslot; i++) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
         for (int i = 0; i < kMaxTiles; i++) mbar_init(&x_tile[i], kEpiThreads);
+        for (int i = 0; i < 3; i++) mbar_init(&x_grp[i], kEpiThreads);
         mbar_init(acc1_full, 1);
         for (int i = 0; i < 2; i++) { mbar_init(&hd_full[i], kEpiThreads); mbar_init(&hd_empty[i], 1); }
         mbar_init(acc2_full, 1);
@@ -676,7 +691,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                             issue_static<CFG::K1, CFG::PER1, CFG::AM1, CFG::WP, CFG::PLANE16, CFG::G1, CFG::KB1 / 16,
                                          CFG::T, CFG::N1, CFG::PM, CFG::LOX16, CFG::ACC1, CFG::NB1, CFG::NOPAD, CFG::STK1>(
                                 tmem, alo0, ringlo, (uint32_t)CFG::SLOT / 16u, id1, CFG::FOLD ? 0u : 1u, slot, phase,
-                                p.nslot, full, empty, id1w);
+                                p.nslot, full, empty, id1w, (CFG::XGRP && j == 0) ? x_grp : nullptr, xph);
                         } else
                                                 {
                             int tap = 0, kc = 0, q = 0;
@@ -868,8 +883,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                         }
                     }
                     if (!tiles_first) {
-                        TWAIT(w_x, mbar_wait(&x_tile[p.T - 1], xph));
-                        fence_after();
+                        if (!CFG::XGRP) {   // XGRP: do_conv1(0) waits for X channel group by group
+                            TWAIT(w_x, mbar_wait(&x_tile[p.T - 1], xph));
+                            fence_after();
+                        }
                         do_conv1(0);
                     }
                     xph ^= 1;
@@ -1141,6 +1158,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
             }
             fence_proxy_async();
             for (int t = 0; t < eT; t++) mbar_arrive(&x_tile[t]);
+            if constexpr (CFG::XGRP)
+                for (int q = 0; q < 3; q++) mbar_arrive(&x_grp[q]);
         };
         // Cross-batch X prefetch: once the last block's last conv1 chunk has completed (its epilogue
         // has waited for it) nothing reads the X planes of this batch any more, so the next batch's
@@ -1569,6 +1588,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 tmem_st8(tmem + lane_addr + col + (uint32_t)((g + u) * 8), bz);
                                 tmem_st8(tmem + lane_addr + col + (uint32_t)(HCW + (g + u) * 8), bc);
                                 tmem_st8(tmem + lane_addr + col + (uint32_t)(2 * HCW + (g + u) * 8), bz);
+                            }
+                            if constexpr (CFG::XGRP) {   // 16-channel groups g/2 and 3 + g/2 of X are final
+                                if (write_x) {
+                                    fence_proxy_async();
+                                    mbar_arrive(&x_grp[g / 2]);
+                                }
                             }
                         }
                         x_ready(tile);
@@ -2414,7 +2439,9 @@ static void pack_block(const StagePlan& p, const float* W1, const float* b1, con
                 int h = j * p.MC + n % p.MC;
                 for (int kk = 0; kk < 16; kk++) {
                     float v;
-                    if (p.nopad) {
+                    if (p.nopad == 2 && p.Cp == 96) {   // channel-group-major order (a_off mode 3)
+                        v = w1(h, ilv_group(s / 3) * 16 + kk, s % 3 - 1, n / p.MC - 1);
+                    } else if (p.nopad) {
                         const int per = p.Cp / 16;
                         v = w1(h, (s % per) * 16 + kk, s / per - 1, n / p.MC - 1);
                     } else if (p.pair) {   // k-step order of pair_shift / pair_lbo_add
@@ -2537,7 +2564,7 @@ static StageKernel find_spec(const StagePlan& p, int residual, int act) {
 }
 // stacked plans exist only as specialisations (umma_prepare re-plans unstacked otherwise)
 static StageKernel pick_kernel(const StagePlan& p, const StageArgs& a) {
-    if (!getenv("CI_NO_STATIC") || p.stk1 || p.stk2) {
+    if (!getenv("CI_NO_STATIC") || p.stk1 || p.stk2 || p.nopad) {   // stacked / no-pad plans: specialised only
         StageKernel f = find_spec(p, a.residual, a.act);
         if (f) return f;
     }
