@@ -156,6 +156,7 @@ struct TsArgs {
     int bias_stride;
     int nb, first_orient, inverse;
     int* ctr;                // zeroed batch counter of this launch, or null
+    unsigned long long* dbg; // optional per-CTA cycle counters (CI_DEBUG_CYCLES), 16 per CTA
 };
 bool stage_ts_shape(int H, int W, int C, int c, int m, int residual, int act);
 int64_t stage_ts_block_bytes(int pm);

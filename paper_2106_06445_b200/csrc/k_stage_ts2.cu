@@ -38,16 +38,16 @@ constexpr int kEpi = 256;
 constexpr int H = 8, W = 8, HW = 64, C = 48, c = 24, M = 128;
 constexpr int NPL = 10;                     // view planes: 3 views x 3 planes of 8 channels + constant-1
 constexpr int G = 16;                       // guard rows above / below the 128 tile rows (one row shift)
-constexpr int RT = G + 128 + G;
-constexpr int PB = RT * 16;                 // plane bytes
+constexpr int PB = (128 + G) * 16;          // plane stride: 128 rows + 16 guard rows shared with the next plane
+constexpr int LOB = (G + NPL * (128 + G)) * 16;   // one precision's planes (leading guard + 10 strides)
 constexpr int N1 = 128, N2 = 112;           // conv1 / conv2-pass MMA widths
 constexpr int K1 = 14, K2 = 8;              // k-steps
-constexpr int NSLOT = 3, SLOTB = 16384;     // weight ring
+constexpr int NSLOT = 4, SLOTB = 16384;     // weight ring (bytes in flight bound the L2 -> SMEM stream)
 constexpr int ST_BYTES = 2 * C * HW * 4;    // fp32 state of the slot's two images
-constexpr int XCH_BYTES = 2 * 2 * 128 * 24; // vertical exchange [pass][half][row][6] fp32
+constexpr int XCH_BYTES = 2 * 128 * 24;     // vertical exchange [half][row][6] fp32 (both passes)
 __host__ __device__ constexpr int kstep(int N, int pm) { return N * 32 * (pm == 2 ? 2 : 1); }
 __host__ __device__ constexpr int per_slot(int N, int pm) { return SLOTB / kstep(N, pm); }
-__host__ __device__ constexpr int view_bytes(int pm) { return (pm ? 2 : 1) * NPL * PB; }
+__host__ __device__ constexpr int view_bytes(int pm) { return (pm ? 2 : 1) * LOB; }
 __host__ __device__ constexpr int slot_bytes(int pm) { return view_bytes(pm) + ST_BYTES + XCH_BYTES; }
 __host__ __device__ constexpr int smem_bytes(int pm) { return NSLOT * SLOTB + 2 * slot_bytes(pm) + 512; }
 // conv1 k-step s: A start (bytes from the plane base of the views) and LBO (bytes)
@@ -58,6 +58,25 @@ __host__ __device__ constexpr int k1_lbo(int s) { return s < 12 ? PB : (s == 12 
 }  // namespace ts2
 
 namespace {
+// cycle counters (CI_DEBUG_CYCLES): time spent in `call` added to acc when a.dbg is set.  The MMA
+// thread's are always compiled in; the epilogue's only with -DCI_TS_EPI_CYCLES (they cost registers).
+#ifdef CI_TS_EPI_CYCLES
+constexpr bool kEpiCycles = true;
+#else
+constexpr bool kEpiCycles = false;
+#endif
+#define T2_WAIT(acc, call)                                             \
+    do {                                                               \
+        const long long t0_ = a.dbg ? clock64() : 0;                   \
+        call;                                                          \
+        if (a.dbg) acc += (unsigned long long)(clock64() - t0_);       \
+    } while (0)
+#define T2_EWAIT(acc, call)                                                        \
+    do {                                                                           \
+        const long long t0_ = (kEpiCycles && a.dbg) ? clock64() : 0;               \
+        call;                                                                      \
+        if (kEpiCycles && a.dbg) acc += (unsigned long long)(clock64() - t0_);     \
+    } while (0)
 __device__ __forceinline__ void t2_ld16(uint32_t taddr, float (&v)[16]) { tmem_ld16(taddr, v); }
 __device__ __forceinline__ void t2_ld4(uint32_t taddr, float (&v)[4]) {
     uint32_t r[4];
@@ -227,9 +246,11 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
             const uint32_t rb = smem_u32(ring);
             const uint32_t id1 = idesc_of(128, N1, PM != 0);
             const uint32_t id2 = idesc_of(128, N2, PM != 0);
-            constexpr uint32_t LOA = (uint32_t)(NPL * PB / 16);   // lo planes, descriptor units
+            constexpr uint32_t LOA = (uint32_t)(LOB / 16);   // lo planes, descriptor units
+            unsigned long long c_x = 0, c_h = 0, c_f = 0;
+            const long long c_t0 = clock64();
             auto acquire = [&]() -> uint32_t {
-                mbar_wait(&full[slot], phase);
+                T2_WAIT(c_f, mbar_wait(&full[slot], phase));
                 fence_after();
                 return rb + (uint32_t)slot * SLOTB;
             };
@@ -248,7 +269,7 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
                     const uint32_t par = kbs[s] & 1;
                     const uint32_t tb = tmem + (uint32_t)(s * 256);
                     if (seg == 0) {   // conv1 (SS: A = the views, vertical taps as row shifts of 16)
-                        mbar_wait(&x_rdy[s], par);
+                        T2_WAIT(c_x, mbar_wait(&x_rdy[s], par));
                         fence_after();
                         const uint32_t vb = smem_u32(sviews(s));
                         for (int s0 = 0; s0 < K1; s0 += G1) {
@@ -268,7 +289,7 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
                         }
                         commit(&a1t[s]);
                     } else {          // conv2 pass (TS: A = the hidden in TMEM)
-                        mbar_wait(seg == 1 ? &hdt[s] : &a2r[s], par);
+                        T2_WAIT(c_h, mbar_wait(seg == 1 ? &hdt[s] : &a2r[s], par));
                         fence_after();
                         for (int s0 = 0; s0 < K2; s0 += G2) {
                             const uint32_t w = acquire();
@@ -290,6 +311,10 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
                     }
                 });
                 if (ns == 1) break;
+            }
+            if (a.dbg) {
+                unsigned long long* o = a.dbg + blockIdx.x * 16;
+                o[0] = clock64() - c_t0; o[1] = c_x; o[2] = c_h; o[3] = c_f;
             }
         }
         __syncwarp();
@@ -334,11 +359,13 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
                 *reinterpret_cast<uint4*>(views + off) = keep ? h4 : z4;
                 if (PM) {
                     const uint4 l4 = make_uint4(lo[4 * pl], lo[4 * pl + 1], lo[4 * pl + 2], lo[4 * pl + 3]);
-                    *reinterpret_cast<uint4*>(views + (size_t)NPL * PB + off) = keep ? l4 : z4;
+                    *reinterpret_cast<uint4*>(views + (size_t)LOB + off) = keep ? l4 : z4;
                 }
             }
         };
         uint32_t kb = 0;
+        unsigned long long c_a1 = 0, c_a2 = 0, c_e1 = 0, c_e2 = 0, c_v = 0, c_io = 0;
+        const long long c_t0 = clock64();
         for (int i = 0;; i++) {
             const int qe = 2 * i + g;
             const int64_t b = bq_read(qe);
@@ -347,6 +374,7 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
             const int64_t img0 = 2 * b;
             const int nimg = a.n - img0 < 2 ? 1 : 2;
             float* gst = a.dst + img0 * (int64_t)C * HW;
+            const long long c_ios = (kEpiCycles && a.dbg) ? clock64() : 0;
             // the slot's state (src, layout in_mode) -> shared memory
             for (int ii = 0; ii < nimg; ii++)
                 io_load<C, H, W>(a.src + (img0 + ii) * (int64_t)C * HW, a.in_mode, st + ii * C * HW, et, kEpi);
@@ -354,6 +382,7 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
             write_views(in_half(a.inverse ? a.nb - 1 : 0), nimg);
             fence_proxy_async();
             mbar_arrive(&x_rdy[g]);
+            if (kEpiCycles && a.dbg) c_io += (unsigned long long)(clock64() - c_ios);
             for (int tt = 0; tt < a.nb; tt++, kb++) {
                 const uint32_t par = kb & 1;
                 if (tt == a.nb - 3) {   // L2 prefetch of the group's next batch, if the producer has published it
@@ -373,8 +402,9 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
                 const bool write_next = tt + 1 < a.nb;
                 const float* b2 = a.bias + (int64_t)t * a.bias_stride + M;
                 // ---- conv1 epilogue: acc1 -> ReLU -> fp16 hi | lo words over the columns just read
-                mbar_wait(&a1t[g], par);
+                T2_EWAIT(c_a1, mbar_wait(&a1t[g], par));
                 fence_after();
+                const long long c_e1s = (kEpiCycles && a.dbg) ? clock64() : 0;
 #pragma unroll
                 for (int rd = 0; rd < 4; rd++) {
                     const uint32_t col = tmem + lane_addr + (uint32_t)(g * 256 + 64 * half + 16 * rd);
@@ -394,6 +424,9 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
                 tmem_wait_st();
                 fence_before();
                 mbar_arrive(&hdt[g]);
+                if (kEpiCycles && a.dbg) c_e1 += (unsigned long long)(clock64() - c_e1s);
+                const long long c_e2s = (kEpiCycles && a.dbg) ? clock64() : 0;
+                unsigned long long c_a2b = 0;
                 // ---- conv2 epilogue, two passes: col2im of the 9 tap groups, s_out (+|-)= F + b2
 #pragma unroll 1
                 for (int pass = 0; pass < 2; pass++) {
@@ -401,7 +434,7 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
                     float2 bb[3];
 #pragma unroll
                     for (int o = 0; o < 3; o++) bb[o] = make_float2(__ldg(b2 + ch0 + 2 * o), __ldg(b2 + ch0 + 2 * o + 1));
-                    mbar_wait(&a2t[g], (uint32_t)pass);
+                    T2_EWAIT(c_a2b, mbar_wait(&a2t[g], (uint32_t)pass));
                     fence_after();
                     float2 z[9][3];   // column 54 half + 6 tap + o
                     {
@@ -435,7 +468,8 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
                     // vertical: out[r] = H_-1[r-16] + H_0[r] + H_+1[r+16].  Lanes < 16 (even y) take H_+1 of
                     // lane +16 and publish their H_+1 for the warp above; lanes >= 16 take H_-1 of lane
                     // -16 and publish their H_-1 for the warp below.
-                    float* xch = xch0 + (pass * 2 + half) * (128 * 6);
+                    float* xch = xch0 + half * (128 * 6);
+                    if (pass == 1) gsync();   // every thread has read pass a's exchange values
                     float2 mid[3], pub[3];
 #pragma unroll
                     for (int o = 0; o < 3; o++) {
@@ -461,11 +495,14 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
                         sp[HW] = nv.y;
                     }
                 }
+                if (kEpiCycles && a.dbg) { c_a2 += c_a2b; c_e2 += (unsigned long long)(clock64() - c_e2s) - c_a2b; }
                 if (write_next) {
+                    const long long c_vs = (kEpiCycles && a.dbg) ? clock64() : 0;
                     gsync();   // the pixel's 24 updated channels come from both halves and both passes
                     write_views(out_off, nimg);
                     fence_proxy_async();
                     mbar_arrive(&x_rdy[g]);
+                    if (kEpiCycles && a.dbg) c_v += (unsigned long long)(clock64() - c_vs);
                 }
             }
             // ---- state back to global memory
@@ -473,6 +510,10 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
             for (int ii = 0; ii < nimg; ii++)   // layout out_mode
                 io_store<C, H, W>(gst + ii * C * HW, a.out_mode, st + ii * C * HW, et, kEpi);
             gsync();
+        }
+        if (kEpiCycles && a.dbg && g == 0 && et == 0) {
+            unsigned long long* o = a.dbg + blockIdx.x * 16;
+            o[6] = clock64() - c_t0; o[7] = c_a1; o[8] = c_a2; o[9] = c_e1; o[10] = c_e2; o[11] = c_v; o[12] = c_io;
         }
     }
     fence_before();

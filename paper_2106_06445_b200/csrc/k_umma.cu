@@ -2847,12 +2847,27 @@ ci_status_t umma_stage_io(const Model* m, int s, const float* src, int in_mode, 
         t.first_orient = a.first_orient;
         t.inverse = a.inverse;
         t.ctr = ctr;
+        t.dbg = a.p.ts == 2 ? cycles_buffer(st) : nullptr;
         const StageInfo& S = m->st[s];
         prof_begin(st);
         if (a.p.ts == 2) CI_CUDA(launch_stage_ts2(t, a.p.pm, st));
         else CI_CUDA(launch_stage_ts(t, a.p.pm, a.p.stk1, st));
         count_launch();
         prof_end(st, s, (double)n * S.nb * 36.0 * S.H * S.W * S.c * S.m);
+        if (t.dbg) {   // per-role cycles of the TS2 kernel
+            unsigned long long h[148 * 16];
+            cudaMemcpyAsync(h, t.dbg, sizeof(h), cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            const int grid = (int)std::min<int64_t>(((n + 1) / 2 + 1) / 2, 148);
+            double acc[16] = {0};
+            for (int b = 0; b < grid; b++)
+                for (int i = 0; i < 16; i++) acc[i] += (double)h[b * 16 + i] / grid;
+            fprintf(stderr,
+                    "[ci cycles] ts2 stage %d n=%lld inv=%d | mma total %.0f wait_x %.0f wait_h %.0f wait_full %.0f | "
+                    "epi total %.0f wait_a1 %.0f wait_a2 %.0f epi1 %.0f epi2 %.0f views %.0f io %.0f\n",
+                    s, (long long)n, inverse ? 1 : 0, acc[0], acc[1], acc[2], acc[3], acc[6], acc[7], acc[8], acc[9],
+                    acc[10], acc[11], acc[12]);
+        }
         return CI_OK;
     }
     a.dbg = cycles_buffer(st);
