@@ -157,6 +157,7 @@ struct TsArgs {
     int nb, first_orient, inverse;
     int* ctr;                // zeroed batch counter of this launch, or null
     unsigned long long* dbg; // optional per-CTA cycle counters (CI_DEBUG_CYCLES), 16 per CTA
+    int sched;               // k_stage_ts2 MMA schedule: 0 lockstep, shared weight stream; 1 offset slots
 };
 bool stage_ts_shape(int H, int W, int C, int c, int m, int residual, int act);
 int64_t stage_ts_block_bytes(int pm);

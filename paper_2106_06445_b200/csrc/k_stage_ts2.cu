@@ -184,10 +184,17 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
     };
     const int SEG1 = K1 * kstep(N1, PM), SEG2 = K2 * kstep(N2, PM);
     constexpr int G1 = per_slot(N1, PM), G2 = per_slot(N2, PM);   // k-steps per ring slot
-    // MMA order of one image pair (slot B half a block behind slot A), as (segment, block, slot):
-    //   conv1(A,k) [conv2a(B,k-1) conv2b(B,k-1)] conv2a(A,k) conv2b(A,k) [conv1(B,k)], k = 0..nb-1,
-    //   then [conv2a(B,nb-1) conv2b(B,nb-1)]; segment 0 = conv1, 1 = conv2 pass a, 2 = pass b
+    // MMA order of one image pair as (segment, block, slot); segment 0 = conv1, 1 = conv2 pass a,
+    // 2 = pass b.  Default (a.sched == 1): slot B half a block behind slot A, each segment streamed
+    // per slot: conv1(A,k) conv2a/b(B,k-1) conv2a/b(A,k) conv1(B,k).  a.sched == 0 (CI_TS2_LOCKSTEP):
+    // per block conv1, conv2a, conv2b for both slots with their k-steps interleaved per ring piece
+    // (slot -1), every weight byte streamed once per pair -- measured 12% slower: the ring waits
+    // drop (0.90M -> 0.31M cycles) but each slot's epilogue is no longer covered by the other's MMAs.
     auto for_each_step = [&](int ns, auto&& f) {
+        if (a.sched == 0) {
+            for (int k = 0; k < a.nb; k++) { f(0, k, -1); f(1, k, -1); f(2, k, -1); }
+            return;
+        }
         for (int k = 0; k <= a.nb; k++) {
             if (k < a.nb) f(0, k, 0);
             if (ns == 2 && k >= 1) { f(1, k - 1, 1); f(2, k - 1, 1); }
@@ -265,48 +272,51 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
                 const int64_t b1 = bq_read(2 * pi + 1);
                 mbar_arrive(&bqe[(2 * pi + 1) & 3]);
                 const int ns = b1 < nbatch ? 2 : 1;
-                for_each_step(ns, [&](int seg, int, int s) {
-                    const uint32_t par = kbs[s] & 1;
-                    const uint32_t tb = tmem + (uint32_t)(s * 256);
-                    if (seg == 0) {   // conv1 (SS: A = the views, vertical taps as row shifts of 16)
-                        T2_WAIT(c_x, mbar_wait(&x_rdy[s], par));
-                        fence_after();
-                        const uint32_t vb = smem_u32(sviews(s));
-                        for (int s0 = 0; s0 < K1; s0 += G1) {
-                            const uint32_t w = acquire();
-#pragma unroll
-                            for (int q = 0; q < G1; q++) {
-                                const int ks = s0 + q;
-                                if (ks >= K1) break;
-                                const uint64_t ad = smem_desc(vb + (uint32_t)k1_start(ks), (uint32_t)k1_lbo(ks), 128);
-                                const uint64_t bd = smem_desc(w + (uint32_t)(q * kstep(N1, PM)), N1 * 16, 128);
-                                const uint32_t acc = ks > 0 ? 1u : 0u;
-                                mma_bf16(tb, ad, bd, id1, acc);
-                                if (PM >= 1) mma_bf16(tb, ad + LOA, bd, id1, 1u);
-                                if (PM == 2) mma_bf16(tb, ad, bd + (uint64_t)(N1 * 32 / 16), id1, 1u);
+                for_each_step(ns, [&](int seg, int, int sl) {
+                    // slots this step runs (sl = -1: both, k-steps interleaved per ring piece)
+                    const int s_lo = sl < 0 ? 0 : sl, s_hi = sl < 0 ? ns : sl + 1;
+                    const int K = seg == 0 ? K1 : K2, Gs = seg == 0 ? G1 : G2;
+                    for (int s0 = 0; s0 < K; s0 += Gs) {
+                        const uint32_t w = acquire();
+                        for (int s = s_lo; s < s_hi; s++) {
+                            const uint32_t par = kbs[s] & 1;
+                            const uint32_t tb = tmem + (uint32_t)(s * 256);
+                            if (s0 == 0) {   // the slot's operand is ready: views (conv1), hidden (pass a), pass a read (b)
+                                if (seg == 0) T2_WAIT(c_x, mbar_wait(&x_rdy[s], par));
+                                else T2_WAIT(c_h, mbar_wait(seg == 1 ? &hdt[s] : &a2r[s], par));
+                                fence_after();
                             }
-                            release();
-                        }
-                        commit(&a1t[s]);
-                    } else {          // conv2 pass (TS: A = the hidden in TMEM)
-                        T2_WAIT(c_h, mbar_wait(seg == 1 ? &hdt[s] : &a2r[s], par));
-                        fence_after();
-                        for (int s0 = 0; s0 < K2; s0 += G2) {
-                            const uint32_t w = acquire();
+                            if (seg == 0) {   // conv1 (SS: A = the views, vertical taps as row shifts of 16)
+                                const uint32_t vb = smem_u32(sviews(s));
 #pragma unroll
-                            for (int q = 0; q < G2; q++) {
-                                const int ks = s0 + q;
-                                if (ks >= K2) break;
-                                const uint32_t ahi = tb + (uint32_t)(16 * ks);   // hidden 16 ks..+15: hi | lo
-                                const uint64_t bd = smem_desc(w + (uint32_t)(q * kstep(N2, PM)), N2 * 16, 128);
-                                const uint32_t acc = ks > 0 ? 1u : 0u;
-                                mma_ts(tb + 128, ahi, bd, id2, acc);
-                                if (PM >= 1) mma_ts(tb + 128, ahi + 8, bd, id2, 1u);
-                                if (PM == 2) mma_ts(tb + 128, ahi, bd + (uint64_t)(N2 * 32 / 16), id2, 1u);
+                                for (int q = 0; q < G1; q++) {
+                                    const int ks = s0 + q;
+                                    if (ks >= K1) break;
+                                    const uint64_t ad = smem_desc(vb + (uint32_t)k1_start(ks), (uint32_t)k1_lbo(ks), 128);
+                                    const uint64_t bd = smem_desc(w + (uint32_t)(q * kstep(N1, PM)), N1 * 16, 128);
+                                    const uint32_t acc = ks > 0 ? 1u : 0u;
+                                    mma_bf16(tb, ad, bd, id1, acc);
+                                    if (PM >= 1) mma_bf16(tb, ad + LOA, bd, id1, 1u);
+                                    if (PM == 2) mma_bf16(tb, ad, bd + (uint64_t)(N1 * 32 / 16), id1, 1u);
+                                }
+                            } else {          // conv2 pass (TS: A = the hidden in TMEM)
+#pragma unroll
+                                for (int q = 0; q < G2; q++) {
+                                    const int ks = s0 + q;
+                                    if (ks >= K2) break;
+                                    const uint32_t ahi = tb + (uint32_t)(16 * ks);   // hidden 16 ks..+15: hi | lo
+                                    const uint64_t bd = smem_desc(w + (uint32_t)(q * kstep(N2, PM)), N2 * 16, 128);
+                                    const uint32_t acc = ks > 0 ? 1u : 0u;
+                                    mma_ts(tb + 128, ahi, bd, id2, acc);
+                                    if (PM >= 1) mma_ts(tb + 128, ahi + 8, bd, id2, 1u);
+                                    if (PM == 2) mma_ts(tb + 128, ahi, bd + (uint64_t)(N2 * 32 / 16), id2, 1u);
+                                }
                             }
-                            release();
                         }
-                        commit(&a2t[s]);
+                        release();
+                    }
+                    for (int s = s_lo; s < s_hi; s++) {
+                        commit(seg == 0 ? &a1t[s] : &a2t[s]);
                         if (seg == 2) kbs[s]++;
                     }
                 });

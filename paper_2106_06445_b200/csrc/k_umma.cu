@@ -2848,6 +2848,8 @@ ci_status_t umma_stage_io(const Model* m, int s, const float* src, int in_mode, 
         t.inverse = a.inverse;
         t.ctr = ctr;
         t.dbg = a.p.ts == 2 ? cycles_buffer(st) : nullptr;
+        static const int ts2_sched = getenv("CI_TS2_LOCKSTEP") ? 0 : 1;   // A/B switch (lockstep: -12%)
+        t.sched = ts2_sched;
         const StageInfo& S = m->st[s];
         prof_begin(st);
         if (a.p.ts == 2) CI_CUDA(launch_stage_ts2(t, a.p.pm, st));
