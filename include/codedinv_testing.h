@@ -29,7 +29,8 @@ CI_API int64_t ci_test_launch_count(int32_t reset);
  * all |c| state channels; pm = product precision: 0 bf16 (CI_PREC_BF16), 1 f16x2 (CI_PREC_F16X2),
  * 2 f16x3 (CI_PREC_FP32)).  out16 = {Wp, G, Cp, Mp, MC, nch, Nc2,
  * T, I, Rtot, k1, k2, nslot, slot_bytes, smem_bytes, packed_bytes_per_block, nhd, sstate,
- * est_cycles_per_image_per_block, tmem_cols, hst, hc, has_specialised_kernel}  (23 entries). */
+ * est_cycles_per_image_per_block, tmem_cols, hst, hc, has_specialised_kernel, ts (1: k_stage_ts,
+ * 2: k_stage_ts2), nopad (1: no pad column, 2: image-row-interleaved raster)}  (25 entries). */
 CI_API ci_status_t ci_test_plan(int32_t H, int32_t W, int32_t c, int32_t m, int32_t pm, int64_t* out16);
 
 /* The encode-mean kernel alone: m [B][d] = (sum_{i<k} h[b][i]) / k  (as inside ci_encode). */

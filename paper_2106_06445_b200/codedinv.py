@@ -350,7 +350,8 @@ def ci_test_mean(h, m, stream=None):
 
 
 PLAN_FIELDS = ["Wp", "G", "Cp", "Mp", "MC", "nch", "Nc2", "T", "I", "Rtot", "k1", "k2", "nslot",
-               "slot_bytes", "smem", "blk_bytes", "nhd", "sstate", "est", "tmem_cols", "hst", "hc", "static"]
+               "slot_bytes", "smem", "blk_bytes", "nhd", "sstate", "est", "tmem_cols", "hst", "hc", "static",
+               "ts", "nopad"]
 
 
 def ci_test_plan(H, W, c, m, pm):

@@ -161,6 +161,7 @@ struct TsArgs {
 };
 bool stage_ts_shape(int H, int W, int C, int c, int m, int residual, int act);
 int64_t stage_ts_block_bytes(int pm);
+int stage_ts_smem(int pm);
 int stage_ts_n2();
 void stage_ts_col(int n, int& tap, int& o);   // conv2 column -> (tap, output channel), tap -1 = padding
 cudaError_t stage_ts_prepare();
@@ -169,6 +170,7 @@ cudaError_t launch_stage_ts(const TsArgs& a, int pm, int stk, cudaStream_t st);
 // TS-mode kernel for Arch C stage 2 (8x8, c = 24, m = 128; k_stage_ts2.cu)
 bool stage_ts2_shape(int H, int W, int C, int c, int m, int residual, int act);
 int64_t stage_ts2_block_bytes(int pm);
+int stage_ts2_smem(int pm);
 cudaError_t stage_ts2_prepare();
 cudaError_t launch_stage_ts2(const TsArgs& a, int pm, cudaStream_t st);
 

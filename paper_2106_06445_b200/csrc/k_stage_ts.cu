@@ -2,7 +2,7 @@
 // the hidden activation never leaves tensor memory.  DESIGN.md 7.2b.
 //
 // One additive-coupling block (Eq. 1):  s_out <- s_out (+|-) F(s_in),
-//   F = conv3x3(W2) o ReLU o conv3x3(W1)   (cross-correlation, zero padding, as oracle_conv3x3).
+//   F = conv3x3(W2) o ReLU o conv3x3(W1)   (cross-correlation, zero padding).
 //
 //  * Raster WITHOUT pad column or pad band: one image = 256 rows = exactly two 128-row M-tiles
 //    (100% of the MMA rows are pixels; the padded raster of k_stage holds 2 images in 5 tiles).
@@ -520,6 +520,7 @@ bool stage_ts_shape(int H, int W, int C, int c, int m, int residual, int act) {
 }
 int64_t stage_ts_block_bytes(int pm) { return (int64_t)ts::K1 * ts::kstep(ts::N1, pm) + ts::K2 * ts::kstep(ts::N2, pm); }
 int stage_ts_n2() { return ts::N2; }
+int stage_ts_smem(int pm) { return ts::smem_bytes(pm); }
 
 // conv2 column n of the TS layout -> (tap, output channel), or tap = -1 for padding columns
 void stage_ts_col(int n, int& tap, int& o) {

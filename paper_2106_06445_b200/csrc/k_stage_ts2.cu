@@ -539,6 +539,8 @@ int64_t stage_ts2_block_bytes(int pm) {
     return (int64_t)ts2::K1 * ts2::kstep(ts2::N1, pm) + 2 * (int64_t)ts2::K2 * ts2::kstep(ts2::N2, pm);
 }
 
+int stage_ts2_smem(int pm) { return ts2::smem_bytes(pm); }
+
 typedef void (*Ts2Kernel)(TsArgs);
 static Ts2Kernel ts2_kernel(int pm) { return pm == 2 ? k_stage_ts2<2> : (pm == 1 ? k_stage_ts2<1> : k_stage_ts2<0>); }
 

@@ -2581,6 +2581,7 @@ static bool make_plan_spec(const StageInfo& S, int pm, StagePlan& p, int residua
         p.T = 1; p.I = 2; p.fold = 1; p.pm = pm;
         p.k1 = 14; p.k2 = 8;
         p.blk_bytes = stage_ts2_block_bytes(pm);
+        p.smem = (size_t)stage_ts2_smem(pm);
         p.tmem_cols = 512;
         p.nslot = 3;
         p.slot_bytes = 16384;
@@ -2596,6 +2597,7 @@ static bool make_plan_spec(const StageInfo& S, int pm, StagePlan& p, int residua
         p.k1 = kPairK1; p.k2 = 4;
         p.stk1 = stage_ts_stacked(pm) ? 1 : 0;
         p.blk_bytes = stage_ts_block_bytes(pm);
+        p.smem = (size_t)stage_ts_smem(pm);
         p.tmem_cols = 512;
         p.nslot = 4;
         p.slot_bytes = 20480;
@@ -2902,11 +2904,12 @@ ci_status_t ci_test_plan(int32_t H, int32_t W, int32_t c, int32_t m, int32_t pm,
     ci::StageArgs sa{};
     sa.residual = residual ? 1 : 0;
     sa.act = residual ? 1 : 0;   // the residual archs use ELU, the coupling archs ReLU
-    const bool has_static = ci::pick_kernel(p, sa) != ci::k_stage<ci::SDyn>;
-    int64_t v[23] = {p.Wp, p.G, p.Cp, p.Mp, p.MC, p.nch, p.Nc2, p.T, p.I, p.Rtot, p.k1, p.k2,
+    // the TS stage kernels are compile-time specialised for their one shape
+    const bool has_static = p.ts != 0 || ci::pick_kernel(p, sa) != ci::k_stage<ci::SDyn>;
+    int64_t v[25] = {p.Wp, p.G, p.Cp, p.Mp, p.MC, p.nch, p.Nc2, p.T, p.I, p.Rtot, p.k1, p.k2,
                      p.nslot, p.slot_bytes, (int64_t)p.smem, p.blk_bytes, p.nhd, p.sstate,
-                     (int64_t)p.est_cycles, p.tmem_cols, p.hst, p.hc, has_static ? 1 : 0};
-    for (int i = 0; i < 23; i++) out16[i] = v[i];
+                     (int64_t)p.est_cycles, p.tmem_cols, p.hst, p.hc, has_static ? 1 : 0, p.ts, p.nopad};
+    for (int i = 0; i < 25; i++) out16[i] = v[i];
     return CI_OK;
 }
 ci_status_t ci_test_prof_enable(int32_t enable) {

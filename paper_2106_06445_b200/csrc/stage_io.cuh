@@ -1,5 +1,5 @@
 // Stage-boundary layouts for the TS stage kernels: the 2x2 squeeze psi between stages
-// (pixel_unshuffle order, oracle_psi) applied while an image's state moves
+// (pixel_unshuffle channel order) applied while an image's state moves
 // between global memory and shared memory, instead of a separate permutation pass.
 //
 // Element g (0 .. C H W - 1) of one image in global memory, for a stage whose state is [C][H][W]

@@ -119,7 +119,10 @@ def test_hot_path_plans_have_specialised_kernels():
                 plan = ci.ci_test_plan(H, W, q, m, pm)
                 assert plan["static"] == 1, (arch.name, H, c, m, pm, plan)
                 assert plan["tmem_cols"] <= 512 and plan["smem"] <= 227 * 1024
-    # the tuned Arch-C bf16 plans use horizontal tap stacking on stages 1-2
-    assert ci.ci_test_plan(16, 16, 6, 64, 0)["hst"] == 1
-    p2 = ci.ci_test_plan(8, 8, 24, 128, 0)
-    assert p2["hst"] == 1 and p2["hc"] == 24 and p2["Nc2"] == 80
+    # Arch C: stage 1 on k_stage_ts, stage 2 on k_stage_ts2, stage 3 on the interleaved raster
+    # (one tile of eight 4x4 images: Wp = 32), in every precision
+    for pm in (0, 1, 2):
+        assert ci.ci_test_plan(16, 16, 6, 64, pm)["ts"] == 1
+        assert ci.ci_test_plan(8, 8, 24, 128, pm)["ts"] == 2
+        p3 = ci.ci_test_plan(4, 4, 96, 256, pm)
+        assert p3["nopad"] == 2 and p3["Wp"] == 32 and p3["T"] == 1 and p3["I"] == 8
