@@ -42,7 +42,9 @@ constexpr int PB = (128 + G) * 16;          // plane stride: 128 rows + 16 guard
 constexpr int LOB = (G + NPL * (128 + G)) * 16;   // one precision's planes (leading guard + 10 strides)
 constexpr int N1 = 128, N2 = 112;           // conv1 / conv2-pass MMA widths
 constexpr int K1 = 14, K2 = 8;              // k-steps
-constexpr int NSLOT = 4, SLOTB = 16384;     // weight ring (bytes in flight bound the L2 -> SMEM stream)
+// weight ring: three k-steps per slot in f16x3 (conv1 24 KB, conv2 21 KB).  Measured: the stream is
+// bound by the per-copy latency, not the bytes in flight (8 x 8 KB slots: s1 +30%, 4 x 16 KB: 0.69 ms)
+constexpr int NSLOT = 3, SLOTB = 24576;
 constexpr int ST_BYTES = 2 * C * HW * 4;    // fp32 state of the slot's two images
 constexpr int XCH_BYTES = 2 * 128 * 24;     // vertical exchange [half][row][6] fp32 (both passes)
 __host__ __device__ constexpr int kstep(int N, int pm) { return N * 32 * (pm == 2 ? 2 : 1); }
@@ -141,17 +143,17 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
         return reinterpret_cast<float*>(slots + (size_t)s * slot_bytes(PM) + view_bytes(PM) + ST_BYTES);
     };
     uint64_t* bars = reinterpret_cast<uint64_t*>(slots + 2 * slot_bytes(PM));
-    uint64_t* full = bars;            // [3]
-    uint64_t* empty = bars + 4;       // [3]
-    uint64_t* bqf = bars + 8;         // [4]
-    uint64_t* bqe = bars + 12;        // [4]
-    uint64_t* x_rdy = bars + 16;      // [2] views of slot s final for its next conv1
-    uint64_t* a1t = bars + 18;        // [2] conv1 of slot s done (commit)
-    uint64_t* hdt = bars + 20;        // [2] hidden of slot s in TMEM
-    uint64_t* a2t = bars + 22;        // [2] conv2 pass of slot s done (commit; twice per block)
-    uint64_t* a2r = bars + 24;        // [2] pass-a accumulator of slot s read (pass b may overwrite)
-    volatile int64_t* bq = reinterpret_cast<volatile int64_t*>(bars + 26);   // [4]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 30);
+    uint64_t* full = bars;            // [NSLOT]
+    uint64_t* empty = bars + 8;       // [NSLOT]
+    uint64_t* bqf = bars + 16;        // [4]
+    uint64_t* bqe = bars + 20;        // [4]
+    uint64_t* x_rdy = bars + 24;      // [2] views of slot s final for its next conv1
+    uint64_t* a1t = bars + 26;        // [2] conv1 of slot s done (commit)
+    uint64_t* hdt = bars + 28;        // [2] hidden of slot s in TMEM
+    uint64_t* a2t = bars + 30;        // [2] conv2 pass of slot s done (commit; twice per block)
+    uint64_t* a2r = bars + 32;        // [2] pass-a accumulator of slot s read (pass b may overwrite)
+    volatile int64_t* bq = reinterpret_cast<volatile int64_t*>(bars + 34);   // [4]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 38);
 
     {   // views: zero (guards, x borders of Xl / Xr); constant-1 plane: channel 0 = 1.0 on the tile rows
         uint4 z = make_uint4(0, 0, 0, 0);
