@@ -120,6 +120,13 @@ __device__ __forceinline__ uint32_t ts_bf16x2(float a, float b) {
 }
 
 // PM: precision; STK (PM == 2 only): stacked conv1, hi(x) [W_hi | W_lo] as one 2N-wide MMA
+#define TS_WAIT(acc, call)                                             \
+    do {                                                               \
+        const long long t0_ = a.dbg ? clock64() : 0;                   \
+        call;                                                          \
+        if (a.dbg) acc += (unsigned long long)(clock64() - t0_);       \
+    } while (0)
+
 template <int PM, int STK>
 __global__ void __launch_bounds__(ts::kThreads, 1) k_stage_ts(TsArgs a) {
     using namespace ts;
@@ -217,6 +224,8 @@ __global__ void __launch_bounds__(ts::kThreads, 1) k_stage_ts(TsArgs a) {
         if (elect_one()) {
             int slot = 0;
             uint32_t phase = 0, kb = 0;
+            unsigned long long c_x = 0, c_h = 0, c_f = 0;   // CI_DEBUG_CYCLES: MMA-thread waits
+            const long long c_t0 = clock64();
             const uint32_t rb = smem_u32(ring);
             const uint32_t id1w = idesc_of(128, STK ? 2 * N1 : N1, PM != 0);
             const uint32_t id1 = idesc_of(128, N1, PM != 0);
@@ -233,11 +242,11 @@ __global__ void __launch_bounds__(ts::kThreads, 1) k_stage_ts(TsArgs a) {
                 for (int tt = 0; tt < a.nb; tt++, kb++) {
                     const uint32_t par = kb & 1;
                     // conv1 of both slots: one weight segment
-                    mbar_wait(&full[slot], phase);
+                    TS_WAIT(c_f, mbar_wait(&full[slot], phase));
                     fence_after();
                     const uint32_t w1 = rb + (uint32_t)slot * SLOTB;
                     for (int s = 0; s < ns; s++) {
-                        mbar_wait(&x_rdy[s], par);
+                        TS_WAIT(c_x, mbar_wait(&x_rdy[s], par));
                         fence_after();
                         const uint32_t xs = smem_u32(xplanes(s));
 #pragma unroll
@@ -271,13 +280,13 @@ __global__ void __launch_bounds__(ts::kThreads, 1) k_stage_ts(TsArgs a) {
                     commit(&empty[slot]);
                     if (++slot == NSLOT) { slot = 0; phase ^= 1; }
                     // conv2 of both slots (TS mode: A = the hidden in TMEM)
-                    mbar_wait(&full[slot], phase);
+                    TS_WAIT(c_f, mbar_wait(&full[slot], phase));
                     fence_after();
                     const uint32_t w2 = rb + (uint32_t)slot * SLOTB;
                     for (int s = 0; s < ns; s++) {
 #pragma unroll
                         for (int t = 0; t < 2; t++) {
-                            mbar_wait(&hdt[s * 2 + t], par);
+                            TS_WAIT(c_h, mbar_wait(&hdt[s * 2 + t], par));
                             fence_after();
                             const uint32_t tb = tmem + (uint32_t)(s * 256 + t * 128);
 #pragma unroll
@@ -297,6 +306,10 @@ __global__ void __launch_bounds__(ts::kThreads, 1) k_stage_ts(TsArgs a) {
                     if (++slot == NSLOT) { slot = 0; phase ^= 1; }
                 }
                 if (ns == 1) break;
+            }
+            if (a.dbg) {
+                unsigned long long* o = a.dbg + blockIdx.x * 16;
+                o[0] = clock64() - c_t0; o[1] = c_x; o[2] = c_h; o[3] = c_f;
             }
         }
         __syncwarp();

@@ -2849,7 +2849,7 @@ ci_status_t umma_stage_io(const Model* m, int s, const float* src, int in_mode, 
         t.first_orient = a.first_orient;
         t.inverse = a.inverse;
         t.ctr = ctr;
-        t.dbg = a.p.ts == 2 ? cycles_buffer(st) : nullptr;
+        t.dbg = cycles_buffer(st);
         static const int ts2_sched = getenv("CI_TS2_LOCKSTEP") ? 0 : 1;   // A/B switch (lockstep: -12%)
         t.sched = ts2_sched;
         const StageInfo& S = m->st[s];
@@ -2862,14 +2862,14 @@ ci_status_t umma_stage_io(const Model* m, int s, const float* src, int in_mode, 
             unsigned long long h[148 * 16];
             cudaMemcpyAsync(h, t.dbg, sizeof(h), cudaMemcpyDeviceToHost, st);
             cudaStreamSynchronize(st);
-            const int grid = (int)std::min<int64_t>(((n + 1) / 2 + 1) / 2, 148);
+            const int grid = (int)std::min<int64_t>(a.p.ts == 2 ? ((n + 1) / 2 + 1) / 2 : (n + 1) / 2, 148);
             double acc[16] = {0};
             for (int b = 0; b < grid; b++)
                 for (int i = 0; i < 16; i++) acc[i] += (double)h[b * 16 + i] / grid;
             fprintf(stderr,
-                    "[ci cycles] ts2 stage %d n=%lld inv=%d | mma total %.0f wait_x %.0f wait_h %.0f wait_full %.0f | "
+                    "[ci cycles] ts%d stage %d n=%lld inv=%d | mma total %.0f wait_x %.0f wait_h %.0f wait_full %.0f | "
                     "epi total %.0f wait_a1 %.0f wait_a2 %.0f epi1 %.0f epi2 %.0f views %.0f io %.0f\n",
-                    s, (long long)n, inverse ? 1 : 0, acc[0], acc[1], acc[2], acc[3], acc[6], acc[7], acc[8], acc[9],
+                    a.p.ts, s, (long long)n, inverse ? 1 : 0, acc[0], acc[1], acc[2], acc[3], acc[6], acc[7], acc[8], acc[9],
                     acc[10], acc[11], acc[12]);
         }
         return CI_OK;
