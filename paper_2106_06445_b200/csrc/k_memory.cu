@@ -1,3 +1,4 @@
+#include <stdlib.h>
 // HBM-bound kernels of the coded path: encode-mean (K7), decode (K8), linear heads +
 // argmax (K9) and the device drop-index generator (K12).
 //
@@ -267,6 +268,79 @@ __global__ void __launch_bounds__(256) k_classify_smem(const float* __restrict__
     }
 }
 
+// Heads with the whole weight matrix resident in shared memory (C d floats <= kClsResident): one
+// persistent CTA of 16 warps per SM, loaded once; each warp streams 4 rows of z (float4, two
+// iterations in flight per row) and keeps their C partial dot products in registers, then one
+// warp reduction per logit.  No per-chunk barriers, so the z stream is never interrupted.
+constexpr int kClsResident = 160 * 1024;
+__global__ void __launch_bounds__(512) k_classify_resident(const float* __restrict__ z, int64_t n, int64_t d,
+                                                           const float* __restrict__ W, const float* __restrict__ bias,
+                                                           int C, float* __restrict__ logits, int32_t* __restrict__ labels) {
+    extern __shared__ float4 wres[];   // [C][d/4]
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int64_t d4 = d >> 2;
+    const float4* W4 = reinterpret_cast<const float4*>(W);
+    for (int64_t i = threadIdx.x; i < (int64_t)C * d4; i += blockDim.x) wres[i] = __ldg(W4 + i);
+    __syncthreads();
+    for (int64_t rb = ((int64_t)blockIdx.x * nw + wid) * CLS_ROWS; rb < n; rb += (int64_t)gridDim.x * nw * CLS_ROWS) {
+        float acc[CLS_ROWS][CLS_CMAX];
+#pragma unroll
+        for (int r = 0; r < CLS_ROWS; r++)
+#pragma unroll
+            for (int c = 0; c < CLS_CMAX; c++) acc[r][c] = 0.f;
+        const float4* zr[CLS_ROWS];
+#pragma unroll
+        for (int r = 0; r < CLS_ROWS; r++) zr[r] = reinterpret_cast<const float4*>(z + (rb + r < n ? rb + r : rb) * d);
+#pragma unroll 2
+        for (int64_t e = lane; e < d4; e += 32) {
+            float4 zv[CLS_ROWS];
+#pragma unroll
+            for (int r = 0; r < CLS_ROWS; r++) zv[r] = ld_stream(zr[r] + e);
+#pragma unroll
+            for (int c = 0; c < CLS_CMAX; c++) {
+                if (c >= C) break;
+                const float4 w = wres[(int64_t)c * d4 + e];
+#pragma unroll
+                for (int r = 0; r < CLS_ROWS; r++) {
+                    float a = acc[r][c];
+                    a = fmaf(w.x, zv[r].x, a);
+                    a = fmaf(w.y, zv[r].y, a);
+                    a = fmaf(w.z, zv[r].z, a);
+                    a = fmaf(w.w, zv[r].w, a);
+                    acc[r][c] = a;
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < CLS_ROWS; r++)
+#pragma unroll
+            for (int c = 0; c < CLS_CMAX; c++) {
+                if (c >= C) break;
+                float v = acc[r][c];
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+                acc[r][c] = v;
+            }
+        if (lane == 0) {
+#pragma unroll
+            for (int r = 0; r < CLS_ROWS; r++) {
+                const int64_t row = rb + r;
+                if (row >= n) break;
+                int best = 0;
+                float bv = 0.f;
+#pragma unroll
+                for (int c = 0; c < CLS_CMAX; c++) {
+                    if (c >= C) break;
+                    const float v = acc[r][c] + __ldg(bias + c);
+                    if (logits) logits[row * C + c] = v;
+                    if (c == 0 || v > bv) { bv = v; best = c; }
+                }
+                if (labels) labels[row] = best;
+            }
+        }
+    }
+}
+
 __global__ void k_classify_scalar(const float* __restrict__ z, int64_t n, int64_t d, const float* __restrict__ W,
                                   const float* __restrict__ bias, int C, float* __restrict__ logits,
                                   int32_t* __restrict__ labels) {
@@ -289,6 +363,21 @@ cudaError_t launch_classify(const float* z, int64_t n, int64_t d, const float* W
     if (n == 0) return cudaSuccess;
     if (d % 4) {
         k_classify_scalar<<<grid_for(n, 128), 128, 0, s>>>(z, n, d, W, b, C, logits, labels);
+        count_launch();
+        return cudaGetLastError();
+    }
+    const size_t wbytes = (size_t)C * d * sizeof(float);
+    static const bool no_resident = getenv("CI_NO_CLS_RESIDENT") != nullptr;   // A/B switch
+    if (!no_resident && C <= CLS_CMAX && wbytes <= (size_t)kClsResident) {
+        static bool attr = false;
+        if (!attr) {
+            cudaError_t e = cudaFuncSetAttribute(k_classify_resident, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 kClsResident);
+            if (e != cudaSuccess) return e;
+            attr = true;
+        }
+        const int64_t need = (n + 16 * CLS_ROWS - 1) / (16 * CLS_ROWS);
+        k_classify_resident<<<(unsigned)(need < 148 ? need : 148), 512, wbytes, s>>>(z, n, d, W, b, C, logits, labels);
         count_launch();
         return cudaGetLastError();
     }
