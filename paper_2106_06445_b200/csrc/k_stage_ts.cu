@@ -405,28 +405,30 @@ __global__ void __launch_bounds__(ts::kThreads, 1) k_stage_ts(TsArgs a) {
                     mbar_wait(&a1t[g * 2 + tl], par);
                     fence_after();
                     const uint32_t col = tmem + lane_addr + (uint32_t)(g * 256 + tl * 128 + 32 * half);
-                    // two rounds of 16 hidden channels (register pressure: 18 warps leave 96 per thread)
+                    // two rounds of 16 hidden channels; round 1's loads are in flight while round 0 is
+                    // converted (round 0 only writes columns it read, round 1 reads other columns)
+                    float v[2][16], w[2][STK ? 16 : 1];
+                    tmem_ld16(col, v[0]);
+                    if constexpr (STK != 0) tmem_ld16(col + 64, *reinterpret_cast<float (*)[16]>(&w[0][0]));
+                    tmem_wait_ld();
+                    tmem_ld16(col + 16, v[1]);
+                    if constexpr (STK != 0) tmem_ld16(col + 80, *reinterpret_cast<float (*)[16]>(&w[1][0]));
 #pragma unroll
                     for (int rd = 0; rd < 2; rd++) {
-                        float v[16];
-                        tmem_ld16(col + 16 * rd, v);
-                        if (STK) {   // stacked: hi(x) W_lo columns at +64
-                            float w[16];
-                            tmem_ld16(col + 64 + 16 * rd, w);
-                            tmem_wait_ld();
+                        if (rd == 1) tmem_wait_ld();
+                        if constexpr (STK != 0) {   // stacked: hi(x) W_lo columns at +64
 #pragma unroll
                             for (int e = 0; e < 8; e++) {
-                                const float2 r = add2(make_float2(v[2 * e], v[2 * e + 1]), make_float2(w[2 * e], w[2 * e + 1]));
-                                v[2 * e] = r.x;
-                                v[2 * e + 1] = r.y;
+                                const float2 r = add2(make_float2(v[rd][2 * e], v[rd][2 * e + 1]),
+                                                      make_float2(w[rd][2 * e], w[rd][2 * e + 1]));
+                                v[rd][2 * e] = r.x;
+                                v[rd][2 * e + 1] = r.y;
                             }
-                        } else {
-                            tmem_wait_ld();
                         }
                         uint32_t hw[8], lw[8];
 #pragma unroll
                         for (int e = 0; e < 8; e++) {
-                            const float p0 = fmaxf(v[2 * e], 0.f), p1 = fmaxf(v[2 * e + 1], 0.f);
+                            const float p0 = fmaxf(v[rd][2 * e], 0.f), p1 = fmaxf(v[rd][2 * e + 1], 0.f);
                             if (PM) ts_split(p0, p1, hw[e], lw[e]);
                             else hw[e] = ts_bf16x2(p0, p1);
                         }
