@@ -27,7 +27,9 @@
 //    conv2(A) conv2(B), lets the tensor core run one image's convolutions while the other
 //    image's group is in its epilogue; the groups are otherwise independent (own barriers,
 //    own batch-queue entries, own state load / store).
-//  * The image's fp32 state lives in shared memory for the whole stage.
+//  * The image's fp32 state lives in shared memory for the whole stage; the group prefetches its
+//    next image with cp.async into a second buffer.  Images are read / written in the layout the
+//    caller names (stage_io.cuh), so the squeeze psi / psi^-1 at the stage boundaries costs no pass.
 // Precisions as k_stage (PM: 0 bf16, 1 f16x2, 2 f16x3 with the stacked conv1).
 #include <stdio.h>
 
