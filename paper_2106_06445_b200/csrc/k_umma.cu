@@ -1119,14 +1119,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
         auto init_acc1_nopad = [&](const float* b1src, uint32_t col) {
             if constexpr (S && CFG::NOPAD) {
 #pragma unroll
-                for (int v = 0; v < 3; v++)
+                for (int v = 0; v < 3; v++) {
+                    if constexpr (CFG::MC / 2 == 8) {   // MC = 16: 8 columns per half
+                        float v8[8];
 #pragma unroll
-                    for (int g = 0; g < CFG::MC / 2; g += 16) {
-                        float v16[16];
+                        for (int e = 0; e < 8; e++) v8[e] = v == 1 ? __ldg(b1src + e) : 0.f;
+                        tmem_st8(tmem + lane_addr + col + (uint32_t)(v * CFG::MC), v8);
+                    } else {
 #pragma unroll
-                        for (int e = 0; e < 16; e++) v16[e] = v == 1 ? __ldg(b1src + g + e) : 0.f;
-                        tmem_st16(tmem + lane_addr + col + (uint32_t)(v * CFG::MC + g), v16);
+                        for (int g = 0; g < CFG::MC / 2; g += 16) {
+                            float v16[16];
+#pragma unroll
+                            for (int e = 0; e < 16; e++) v16[e] = v == 1 ? __ldg(b1src + g + e) : 0.f;
+                            tmem_st16(tmem + lane_addr + col + (uint32_t)(v * CFG::MC + g), v16);
+                        }
                     }
+                }
             }
         };
         for (int tile = 0; tile < eT; tile++) {
@@ -1252,6 +1260,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 float zl[2][8], zc[2][8], zr[2][8];
 #pragma unroll
                                 for (int u = 0; u < 2; u++) {
+                                    if ((g + u) * 8 >= CW) break;   // MC = 16: one 8-channel group per half
                                     tmem_ld8(tmem + lane_addr + col + (uint32_t)((g + u) * 8), zl[u]);
                                     tmem_ld8(tmem + lane_addr + col + (uint32_t)(CFG::MC + (g + u) * 8), zc[u]);
                                     tmem_ld8(tmem + lane_addr + col + (uint32_t)(2 * CFG::MC + (g + u) * 8), zr[u]);
@@ -1259,6 +1268,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stage(StageArgs a) {
                                 tmem_wait_ld();
 #pragma unroll
                                 for (int u = 0; u < 2; u++) {
+                                    if ((g + u) * 8 >= CW) break;
                                     float h8[8];
 #pragma unroll
                                     for (int o = 0; o < 8; o++) {
@@ -2211,7 +2221,8 @@ static const TunedPlan kTuned[] = {
     {4, 4, 96, 256, 2, 64, 1, 2, 4, 1, 0, 0, 2},  // stage 3 f16x3, interleaved raster, 8 images per tile (CI_NO_ILV)
     {4, 4, 96, 256, 2, 64, 1, 2, 4, 1, 0, 0, 1},  // stage 3 f16x3, no-pad raster (CI_NO_NOPAD: padded)
     {4, 4, 96, 256, 2, 128, 1, 1, 4, 0, 1, 1},   // stage 3 f16x3, stacked conv1 + conv2
-    {16, 16, 64, 64, 2, 32, 3, 1, 4, 0, 1, 0},   // learned-encoder tail f16x3, stacked conv1
+    {16, 16, 64, 64, 2, 16, 2, 2, 4, 1, 0, 0, 2},  // learned-encoder tail f16x3, one image in 2 tiles, no pad
+    {16, 16, 64, 64, 2, 32, 3, 1, 4, 0, 1, 0},   // learned-encoder tail f16x3, stacked conv1 (CI_NO_ILV)
     {4, 4, 96, 256, 2, 128, 1, 1, 4, 0},   // stage 3 f16x3
     {16, 16, 12, 64, 0, 32, 5, 2, 4, 1},   // CR (residual, f1) stage 1 bf16: wide hst (N = 48)
     {16, 16, 12, 64, 0, 64, 5, 1, 4, 0},   // CR stage 1 bf16, plain conv2 (CI_NO_WIDE_HST)
@@ -2254,10 +2265,16 @@ static bool make_plan(const StageInfo& S, int pm, StagePlan& best, bool allow_st
             tuned = &tp;
     p.nopad = (tuned && allow_stk) ? tuned->nopad : 0;
     p.H = S.H; p.W = S.W; p.Wp = p.nopad ? S.W : S.W + 1; p.G = p.Wp + 2;
-    if (p.nopad == 2) {   // one tile of 128 / (H W) images, rows interleaved by image row
-        if (128 % (S.H * S.W)) return false;
-        p.Wp = (128 / (S.H * S.W)) * S.W;
+    int ilv_T = 1;
+    if (p.nopad == 2) {   // 128 / (H W) images per tile rows interleaved by image row, or one image of
+                          // H W / 128 tiles (r = W y + x); vertical taps are Wp-row shifts
+        const int hw = S.H * S.W;
+        if (hw < 128 ? 128 % hw : hw % 128) return false;
+        const int I = hw < 128 ? 128 / hw : 1;
+        p.Wp = I * S.W;
         p.G = 16;
+        ilv_T = hw < 128 ? 1 : hw / 128;
+        if (p.Wp > 2 * p.G) return false;   // a Wp-row shift reads this plane's and the neighbour's guard
     }
     p.c = S.c; p.m = S.m;
     p.Cp = S.c <= 8 ? 8 : rup(S.c, 16);
@@ -2295,7 +2312,7 @@ static bool make_plan(const StageInfo& S, int pm, StagePlan& best, bool allow_st
         for (int T = 1; T <= 8; T++) {
             if (T * (n1 * (1 + p.stk1) + p.Nc2 * (1 + p.stk2)) > 512) break;
             if (tuned && T != tuned->T) continue;
-            if (p.nopad == 2 && T != 1) continue;   // interleaved raster: one tile
+            if (p.nopad == 2 && T != ilv_T) continue;   // interleaved raster: its tile count
             const int I = (T * 128) / img_rows;
             if (I < 1) continue;
             for (int nhd = (nch >= 2 ? 2 : 1); nhd >= 1; nhd--) {
@@ -2535,6 +2552,7 @@ static const SpecEntry kSpecs[] = {
     CI_SPEC_XN(32, 96, 64, 288, 1, 2, 18432, 4, 96, 0, 1, 0, 0, 0, 2),  // C stage 3, f16x3, interleaved raster
     CI_SPEC_XN(32, 96, 64, 288, 1, 1, 16384, 4, 96, 0, 1, 0, 0, 0, 2),  // C stage 3, f16x2, interleaved raster
     CI_SPEC_XN(32, 96, 64, 288, 1, 0, 16384, 4, 96, 0, 1, 0, 0, 0, 2),  // C stage 3, bf16, interleaved raster
+    CI_SPEC_XN(16, 64, 16, 192, 2, 2, 16384, 16, 64, 0, 1, 0, 0, 0, 2), // encoder tail, f16x3, no-pad 2-tile raster
     CI_SPEC_XS(9, 32, 64, 80, 2, 2, 16384, 8, 24, 0, 1, 0, 1, 0),   // C stage 2, f16x3, MC = 64 stacked (A/B)
     CI_SPEC_XS(17, 64, 32, 64, 3, 2, 16384, 16, 64, 0, 0, 0, 1, 0), // encoder tail, f16x3, stacked conv1
     CI_SPEC(17, 64, 32, 64, 5, 0, 16384, 16, 64, 0),  // learned-encoder tail (E2, E3), bf16
