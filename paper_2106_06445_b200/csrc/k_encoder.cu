@@ -137,39 +137,41 @@ __global__ void __launch_bounds__(kEncThreads, 2) k_enc_out(const float* __restr
                                                            const __grid_constant__ E4Params<CI, C1> p,
                                                            float* __restrict__ xp) {
     extern __shared__ __align__(16) float us[];
-    constexpr int RS = EncTile<W>::RS, WQ = W / kEncPx, W2 = W / 2;
+    constexpr int RS = EncTile<W>::RS, WQ = W / kEncPx;
     const int plane = EncTile<W>::plane(H), tileN = C1 * plane;
     const int HW = H * W, Ho = H / 2, Wo = W / 2;
     const int r = threadIdx.x / WQ, x0 = (threadIdx.x % WQ) * kEncPx;
     for (int e = threadIdx.x; e < tileN; e += kEncThreads) us[e] = 0.f;   // halo (and interior)
-    const int npair = C1 * H * W2;   // pixel pairs (x even, x + 1): one float2 of m, one float of each z plane
+    constexpr int W4 = W / 4;
+    const int nquad = C1 * H * W4;   // 4-pixel runs (x % 4 == 0): one float4 of m, one float2 of each z plane
     for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
         const float* zb = z + b * zstride;
         const float* mb = m + b * (int64_t)C1 * HW;
         __syncthreads();   // the previous group's readers are done
-        constexpr int U = 8;   // loads in flight per thread
-        for (int v0 = threadIdx.x; v0 < npair; v0 += U * kEncThreads) {
-            float2 mv[U];
-            float z0[U], z1[U];
+        constexpr int U = 8;   // runs in flight per thread (3 loads each)
+        for (int v0 = threadIdx.x; v0 < nquad; v0 += U * kEncThreads) {
+            float4 mv[U];
+            float2 z0[U], z1[U];
 #pragma unroll
             for (int j = 0; j < U; j++) {
                 const int v = v0 + j * kEncThreads;
-                if (v < npair) {
-                    const int c = v / (H * W2), rem = v - c * (H * W2), y = rem / W2, xh = rem - y * W2;
-                    mv[j] = *reinterpret_cast<const float2*>(mb + c * HW + y * W + 2 * xh);
-                    const float* zr = zb + ((int64_t)(c * 4 + 2 * (y & 1)) * Ho + (y >> 1)) * Wo + xh;
-                    z0[j] = zr[0];
-                    z1[j] = zr[(int64_t)Ho * Wo];
+                if (v < nquad) {
+                    const int c = v / (H * W4), rem = v - c * (H * W4), y = rem / W4, xq = rem - y * W4;
+                    mv[j] = *reinterpret_cast<const float4*>(mb + c * HW + y * W + 4 * xq);
+                    // psi^-1: pixel (y, x) of channel c is z[4c + 2(y&1) + (x&1)][y/2][x/2]
+                    const float* zr = zb + ((int64_t)(c * 4 + 2 * (y & 1)) * Ho + (y >> 1)) * Wo + 2 * xq;
+                    z0[j] = *reinterpret_cast<const float2*>(zr);                       // x even
+                    z1[j] = *reinterpret_cast<const float2*>(zr + (int64_t)Ho * Wo);    // x odd
                 }
             }
 #pragma unroll
             for (int j = 0; j < U; j++) {
                 const int v = v0 + j * kEncThreads;
-                if (v < npair) {
-                    const int c = v / (H * W2), rem = v - c * (H * W2), y = rem / W2, xh = rem - y * W2;
-                    float* d = us + c * plane + (y + 1) * RS + 4 + 2 * xh;
-                    d[0] = z0[j] + mv[j].x;
-                    d[1] = z1[j] + mv[j].y;
+                if (v < nquad) {
+                    const int c = v / (H * W4), rem = v - c * (H * W4), y = rem / W4, xq = rem - y * W4;
+                    float* d = us + c * plane + (y + 1) * RS + 4 + 4 * xq;
+                    *reinterpret_cast<float4*>(d) =
+                        make_float4(z0[j].x + mv[j].x, z1[j].x + mv[j].y, z0[j].y + mv[j].z, z1[j].y + mv[j].w);
                 }
             }
         }
