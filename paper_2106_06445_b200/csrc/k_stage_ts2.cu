@@ -19,7 +19,11 @@
 //    MMA thread runs slot B half a block behind slot A: conv1(A,k) conv2(B,k-1) conv2(A,k)
 //    conv1(B,k), so every hand-off between a slot's epilogue and its next MMA step is covered by
 //    at least one conv1 or two conv2 passes of the other slot.
-//  * The fp32 state of the slot's two images stays in shared memory for the whole stage.
+//  * The fp32 state of the slot's two images stays in shared memory for the whole stage; it is read
+//    and written in the layouts the caller names (stage_io.cuh: the squeeze psi / psi^-1 at the
+//    stage boundaries fused into the load / store).
+//  * Weights stream through a 3 x 24 KB ring per slot-block; at the MMA rate that is the chip's
+//    whole L2 -> SM bulk-copy throughput, so the ring is this kernel's bound.
 #include <stdio.h>
 
 #include "ci_internal.h"
