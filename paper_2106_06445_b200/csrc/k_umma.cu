@@ -2317,7 +2317,7 @@ static bool make_plan(const StageInfo& S, int pm, StagePlan& best, bool allow_st
             if (I < 1) continue;
             for (int nhd = (nch >= 2 ? 2 : 1); nhd >= 1; nhd--) {
                 if (tuned && nhd != tuned->nhd) continue;
-                for (int nslot = 4; nslot >= 2; nslot--) {
+                for (int nslot = tuned ? std::min(std::max(tuned->nslot, 4), kMaxSlots) : 4; nslot >= 2; nslot--) {
                     if (tuned && nslot != tuned->nslot) continue;
                     const int slot_bytes = std::max(16384, std::max(kstep_bytes(n1, pm), kstep_bytes(p.Nc2, pm)));
                     const int Rtot = T * 128 + 2 * p.G;
