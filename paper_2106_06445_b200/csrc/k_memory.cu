@@ -280,7 +280,23 @@ __global__ void __launch_bounds__(512) k_classify_resident(const float* __restri
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int64_t d4 = d >> 2;
     const float4* W4 = reinterpret_cast<const float4*>(W);
-    for (int64_t i = threadIdx.x; i < (int64_t)C * d4; i += blockDim.x) wres[i] = __ldg(W4 + i);
+    {   // W -> shared memory with 8 loads in flight per thread (a serial load / store loop pays the
+        // memory latency once per element)
+        const int64_t nw = (int64_t)C * d4;
+        for (int64_t i0 = threadIdx.x; i0 < nw; i0 += 8 * (int64_t)blockDim.x) {
+            float4 t[8];
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                const int64_t i = i0 + (int64_t)j * blockDim.x;
+                if (i < nw) t[j] = __ldg(W4 + i);
+            }
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                const int64_t i = i0 + (int64_t)j * blockDim.x;
+                if (i < nw) wres[i] = t[j];
+            }
+        }
+    }
     __syncthreads();
     for (int64_t rb = ((int64_t)blockIdx.x * nw + wid) * CLS_ROWS; rb < n; rb += (int64_t)gridDim.x * nw * CLS_ROWS) {
         float acc[CLS_ROWS][CLS_CMAX];
@@ -291,7 +307,7 @@ __global__ void __launch_bounds__(512) k_classify_resident(const float* __restri
         const float4* zr[CLS_ROWS];
 #pragma unroll
         for (int r = 0; r < CLS_ROWS; r++) zr[r] = reinterpret_cast<const float4*>(z + (rb + r < n ? rb + r : rb) * d);
-#pragma unroll 2
+#pragma unroll 4
         for (int64_t e = lane; e < d4; e += 32) {
             float4 zv[CLS_ROWS];
 #pragma unroll
