@@ -111,3 +111,30 @@ def test_ts_inverse_vs_oracle_and_determinism(ci):
     e = relerr(xr[idx], ref)
     print(f"[ts inverse fp32] {e:.3g}")
     assert e < 1e-3
+
+
+@pytest.mark.parametrize("k", [1, 10])
+def test_ts_degenerate_single_group(ci, k):
+    """One group through ci_serve_group on Arch C (the parity path is a single image: the TS
+    kernels' second slot and the second image of a TS2 slot are absent; k = 1 is repetition, so
+    x_p = x up to the round trip)."""
+    arch = fx.ARCH_C
+    params = fx.make_weights(arch, 13)
+    x = fx.make_inputs(arch, 1, k, 21)
+    drop = np.zeros(1, np.int32)
+    ref = oracle.serve_group(arch, params, x, drop)
+    m = make_model(ci, arch, params, "fp32", True)
+    xt = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    h = torch.empty(1, k, arch.d, device="cuda")
+    p = torch.empty(1, arch.d, device="cuda")
+    xp = torch.empty(1, arch.in_c, arch.in_h, arch.in_w, device="cuda")
+    ws = m.workspace(k, 1)
+    m.ci_serve_group(xt, torch.from_numpy(drop).cuda(), h, p, ws, x_parity=xp)
+    m.ci_check(ws)
+    torch.cuda.synchronize()
+    e = {key: relerr(g, ref[key]) for key, g in (("R", h.cpu().numpy()), ("P", p.cpu().numpy()),
+                                                 ("xp", xp.cpu().numpy()))}
+    print(f"[ts single group k={k}] " + " ".join(f"{a}={b:.3g}" for a, b in e.items()))
+    assert max(e.values()) < 1e-3
+    if k == 1:
+        assert relerr(xp.cpu().numpy().reshape(1, -1), x.reshape(1, -1)) < 1e-5
