@@ -395,8 +395,25 @@ def timed_run(ci, wl, model, steps, warmup, nin, dist=None, measure=True, prof=F
     return dict(ms=ms, clocks=clocks, launches=launches, kms=kms, klaunch=kl, kflops=kfl, ws=wss[0])
 
 
-def stage_roofline(run, peaks, peak_src, precision, step_ms, measured_in):
-    """Roofline of the dominant kernel (the fused tcgen05 stage kernel) from live CUDA events."""
+def stage_kernel_names(ci, arch, precision):
+    """The kernel each stage of h runs on (planner query: TS kernels / interleaved raster / k_stage)."""
+    pm = {"bf16": 0, "f16x2": 1, "fp32": 2}[precision]
+    names = []
+    for (C, H, W, c, m, nb) in arch.stage_shapes():
+        q = -c if arch.block == "residual" else c
+        try:
+            p = ci.ci_test_plan(H, W, q, m, pm)
+        except Exception:
+            names.append("k_stage")
+            continue
+        names.append({1: "k_stage_ts", 2: "k_stage_ts2"}.get(p.get("ts", 0), "k_stage") +
+                     (" (interleaved raster)" if p.get("nopad") == 2 else ""))
+    return names
+
+
+def stage_roofline(run, peaks, peak_src, precision, step_ms, measured_in, names=None):
+    """Roofline of the dominant kernels (the fused tcgen05 stage kernels of h, summed) from live
+    CUDA events."""
     kms, kfl, kl = run["kms"], run["kflops"], run["klaunch"]
     stage_ms, stage_fl = sum(kms), sum(kfl)
     if stage_ms <= 0:
@@ -411,7 +428,8 @@ def stage_roofline(run, peaks, peak_src, precision, step_ms, measured_in):
         except Exception:
             traffic = None
     mult = MMAS[precision]
-    roof = {"bound": "tensor", "kernel": "k_stage (fused coupling stage, tcgen05)",
+    label = " + ".join(dict.fromkeys(n.split(" (")[0] for n in names)) if names else "k_stage"
+    roof = {"bound": "tensor", "kernel": f"fused tcgen05 stage kernels of h ({label}), summed",
             "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "peak_source": f"{peak_src} bf16_tflops_sustained (dense bf16 cuBLAS, 4 s loop); fp16 runs at the "
                            f"same kind::f16 rate",
@@ -422,7 +440,8 @@ def stage_roofline(run, peaks, peak_src, precision, step_ms, measured_in):
     kernels = {}
     for s in range(4):
         if kl[s]:
-            kernels[f"k_stage[s{s}]"] = {"launches": kl[s], "ms_per_launch": kms[s] / kl[s],
+            kernels[f"k_stage[s{s}]"] = {"kernel": names[s] if names and s < len(names) else "k_stage",
+                                         "launches": kl[s], "ms_per_launch": kms[s] / kl[s],
                                          "tflops": kfl[s] / (kms[s] / 1e3) / 1e12,
                                          "frac_of_peak": kfl[s] / (kms[s] / 1e3) / 1e12 / peak}
     return roof, kernels
@@ -446,7 +465,8 @@ def measure_workload(ci, wl, precision, args, dist, local, peaks, peak_src, nin,
                        "p90": float(np.percentile(vals, 90)), "steps_per_rep": args.steps}
     prof = timed_run(ci, wl, model, max(3, args.steps // 2), 3, 1, dist=dist, measure=False, prof=True, local=local)
     res["roofline"], res["kernels"] = stage_roofline(prof, peaks, peak_src, precision, prof["ms"],
-                                                     "single-stream pass" if nin > 1 or graph else "timed region")
+                                                     "single-stream pass" if nin > 1 or graph else "timed region",
+                                                     names=stage_kernel_names(ci, wl.cfg.arch, precision))
     res["model"], res["ws"] = model, run["ws"]
     return res
 

@@ -101,7 +101,7 @@ txt = f"""# Round-2 profile summary (B200, `scripts/gpu_refresh.sh {tag}` + `scr
 
 All numbers come from one `gpurun` call: `pytest -m gpu` ({npass}), the bench lines committed
 next to this file (`{tag}_bench*.json`), the ncu launch list, one `ncu --set full` capture of the
-fused stage kernel in the contract precision and the DRAM counters of the HBM-bound kernels.
+fused stage kernels (k_stage_ts, k_stage_ts2, k_stage) in the contract precision and the DRAM counters of the HBM-bound kernels.
 
 ## Live bench (CUDA events; 2 request batches in flight; numerics vs the f64 oracle on sampled groups)
 Contract precision = `fp32` (CI_PREC_FP32: f16x3 products, fp32 state): max relative error <= 1e-3.
@@ -122,7 +122,7 @@ C3 fp32 numerics ({num['groups_checked']} groups): features {num['max_rel_err_fe
 parity {num['max_rel_err_parity']:.2g}, x_p {num['max_rel_err_parity_input']:.2g}, logits {num['max_rel_err_logits']:.2g}, labels {num['label_agreement'] * 100:.1f}%.
 
 Per-stage fused kernel (C3 fp32, single-stream profiled pass, avg over the 3 launch sizes; algorithmic FLOPs,
-3 MMAs issued per product): """ + ", ".join(f"{kk[-3:-1]} {v['tflops']:.0f} TFLOP/s ({v['frac_of_peak'] * 100:.1f}%)" for kk, v in k.items()) + f"""
+3 MMAs issued per product): """ + ", ".join(f"{kk[-3:-1]} [{v.get('kernel', 'k_stage')}] {v['tflops']:.0f} TFLOP/s ({v['frac_of_peak'] * 100:.1f}%)" for kk, v in k.items()) + f"""
 
 HBM-bound kernels (standalone, 8192 groups = 1.1 GB, L2 flushed): decode {hb['decode']['achieved']:.0f} GB/s
 ({hb['decode']['frac'] * 100:.1f}% of measured {hb['decode']['peak']:.0f}), mean {hb['mean']['achieved']:.0f} GB/s ({hb['mean']['frac'] * 100:.1f}%).
