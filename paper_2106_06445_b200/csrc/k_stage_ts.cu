@@ -1,7 +1,8 @@
 // Stage 1 of Arch C (16x16 images, c = 6 coupling channels, m = 64 hidden) as a TS-mode kernel:
 // the hidden activation never leaves tensor memory.  DESIGN.md 7.2b.
 //
-// One additive-coupling block (Eq. 1):  s_out <- s_out (+|-) F(s_in),
+// One additive-coupling block (i-RevNet style; reading Q1 of DESIGN.md 2):
+//   s_out <- s_out (+|-) F(s_in),
 //   F = conv3x3(W2) o ReLU o conv3x3(W1)   (cross-correlation, zero padding).
 //
 //  * Raster WITHOUT pad column or pad band: one image = 256 rows = exactly two 128-row M-tiles

@@ -1,5 +1,6 @@
 // Stage 2 of Arch C (8x8 images, c = 24 coupling channels, m = 128 hidden) as a TS-mode kernel.
-// DESIGN.md 7.2c.  Same block as k_stage / k_stage_ts (Eq. 1):
+// DESIGN.md 7.2c.  Same block as k_stage / k_stage_ts (i-RevNet-style additive coupling, PAPER.md:168;
+// reading Q1 of DESIGN.md 2):
 //   s_out <- s_out (+|-) F(s_in),  F = conv3x3(W2) o ReLU o conv3x3(W1).
 //
 //  * Two images per 128-row M-tile with no pad rows or columns (100% of the MMA rows are
