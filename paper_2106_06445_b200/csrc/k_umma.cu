@@ -2226,6 +2226,7 @@ static const TunedPlan kTuned[] = {
     {4, 4, 96, 256, 2, 128, 1, 1, 4, 0},   // stage 3 f16x3
     {16, 16, 12, 64, 0, 32, 5, 2, 4, 1},   // CR (residual, f1) stage 1 bf16: wide hst (N = 48)
     {16, 16, 12, 64, 0, 64, 5, 1, 4, 0},   // CR stage 1 bf16, plain conv2 (CI_NO_WIDE_HST)
+    {16, 16, 12, 64, 2, 32, 5, 1, 4, 1},   // CR stage 1 f16x3: wide hst (N = 3 x 16 -> 48), T = 5, SMEM state
     {16, 16, 12, 64, 2, 32, 7, 1, 3, 0, 0, 1},   // CR stage 1 f16x3, stacked conv2 (CI_NO_STK: unstacked)
     {8, 8, 48, 128, 2, 64, 2, 1, 4, 0, 1, 0},    // CR stage 2 f16x3, stacked conv1
     {16, 16, 12, 64, 2, 32, 7, 1, 3, 0},   // CR stage 1 f16x3
@@ -2560,6 +2561,7 @@ static const SpecEntry kSpecs[] = {
     // i-ResNet variant of Arch C (f1, config C3R): residual blocks on 12 / 48 / 192 channels
     CI_SPEC_R(17, 16, 64, 16, 5, 0, 16384, 16, 12, 1),    // CR stage 1, bf16 (plain conv2)
     CI_SPEC_X(17, 16, 32, 48, 5, 0, 16384, 16, 12, 1, 1, 1),   // CR stage 1, bf16, wide hst
+    CI_SPEC_X(17, 16, 32, 48, 5, 2, 16384, 16, 12, 1, 1, 1),   // CR stage 1, f16x3, wide hst
     CI_SPEC_R(9, 48, 128, 48, 2, 0, 16384, 8, 48, 1),     // CR stage 2, bf16
     CI_SPEC_R(5, 192, 64, 192, 2, 0, 16384, 4, 192, 0),   // CR stage 3, bf16
     CI_SPEC_R(17, 16, 32, 16, 7, 2, 16384, 16, 12, 0),    // CR stage 1, f16x3
