@@ -126,3 +126,7 @@ def test_hot_path_plans_have_specialised_kernels():
         assert ci.ci_test_plan(8, 8, 24, 128, pm)["ts"] == 2
         p3 = ci.ci_test_plan(4, 4, 96, 256, pm)
         assert p3["nopad"] == 2 and p3["Wp"] == 32 and p3["T"] == 1 and p3["I"] == 8
+    # C3R stage 1 in the contract precision: the wide-hst plan (conv2 as 3 x 16 = 48 columns over
+    # the hidden map in shared memory, 5 tiles, state in SMEM)
+    p1 = ci.ci_test_plan(16, 16, -12, 64, 2)
+    assert p1["hst"] == 1 and p1["Nc2"] == 48 and p1["T"] == 5 and p1["static"] == 1
