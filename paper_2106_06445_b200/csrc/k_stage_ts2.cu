@@ -23,8 +23,9 @@
 //  * The fp32 state of the slot's two images stays in shared memory for the whole stage; it is read
 //    and written in the layouts the caller names (stage_io.cuh: the squeeze psi / psi^-1 at the
 //    stage boundaries fused into the load / store).
-//  * Weights stream through a 3 x 24 KB ring per slot-block; at the MMA rate that is the chip's
-//    whole L2 -> SM bulk-copy throughput, so the ring is this kernel's bound.
+//  * Weights stream through a 3 x 24 KB ring per slot-block; the ring's depth (per-piece latency,
+//    not the chip's L2 -> SM bytes: halving those with cluster multicast, MC below, did not help)
+//    is this kernel's bound.
 #include <stdio.h>
 
 #include "ci_internal.h"
@@ -135,7 +136,11 @@ __device__ __forceinline__ uint32_t t2_bf16x2(float a, float b) {
 }
 }  // namespace
 
-template <int PM>
+// MC: launched as clusters of two CTAs that stream the same weight sequence; each CTA copies half
+// of every ring piece and multicasts it to both (one L2 read per pair: half the per-SM L2 -> SM
+// bytes), and a piece is refilled only after both CTAs' MMAs released it (empty count 2, commits
+// multicast to the pair).  Batches are assigned statically, four per cluster and iteration.
+template <int PM, bool MC>
 __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
     using namespace ts2;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -172,7 +177,7 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
     fence_proxy_async();
     if (warp == 1) tmem_alloc(tmem_slot, 512);
     if (tid == 0) {
-        for (int i = 0; i < NSLOT; i++) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+        for (int i = 0; i < NSLOT; i++) { mbar_init(&full[i], 1); mbar_init(&empty[i], MC ? 2 : 1); }
         for (int i = 0; i < 4; i++) { mbar_init(&bqf[i], 1); mbar_init(&bqe[i], 1 + kEpi); }
         for (int i = 0; i < 2; i++) {
             mbar_init(&x_rdy[i], kEpi); mbar_init(&a1t[i], 1); mbar_init(&hdt[i], kEpi);
@@ -182,8 +187,12 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
     }
     fence_before();
     __syncthreads();
+    if (MC) cluster_sync();   // the peer's barriers are initialised before any multicast reaches them
     fence_after();
     const uint32_t tmem = *tmem_slot;
+    const int crank = MC ? (int)cluster_rank() : 0;
+    const int64_t ncl = gridDim.x >> 1, cid = blockIdx.x >> 1;
+    auto mc_base = [&](int pi) -> int64_t { return 4 * (cid + (int64_t)pi * ncl); };   // MC: the cluster's first batch
     const int64_t nbatch = (a.n + 1) / 2;   // two images per slot batch
     auto bq_read = [&](int i) -> int64_t {
         mbar_wait(&bqf[i & 3], (uint32_t)((i >> 2) & 1));
@@ -226,7 +235,31 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
                 bq[i & 3] = v;
                 mbar_arrive(&bqf[i & 3]);
             };
-            for (int pi = 0;; pi++) {
+            for (int pi = 0; MC; pi++) {
+                const int64_t base = mc_base(pi), b0 = base + 2 * crank, b1 = b0 + 1;
+                publish(2 * pi, b0 < nbatch ? b0 : nbatch);
+                publish(2 * pi + 1, b1 < nbatch ? b1 : nbatch);
+                if (base >= nbatch) break;
+                for_each_step(2, [&](int seg, int k, int) {
+                    const int t = a.inverse ? a.nb - 1 - k : k;
+                    const uint8_t* src = a.wpack + (int64_t)t * a.blk_bytes + (seg == 0 ? 0 : SEG1 + (seg - 1) * SEG2);
+                    const int K = seg == 0 ? K1 : K2, Gs = seg == 0 ? G1 : G2, kb = seg == 0 ? kstep(N1, PM) : kstep(N2, PM);
+                    for (int s0 = 0; s0 < K; s0 += Gs) {
+                        const uint32_t bytes = (uint32_t)(min(Gs, K - s0) * kb), hb = bytes / 2;
+                        mbar_wait(&empty[slot], phase ^ 1);   // both CTAs released the piece
+                        mbar_arrive_expect_tx(&full[slot], bytes);
+                        bulk_g2s_mc(ring + (size_t)slot * SLOTB + crank * hb, src + (size_t)s0 * kb + crank * hb, hb,
+                                    &full[slot], (uint16_t)3);
+                        if (++slot == NSLOT) { slot = 0; phase ^= 1; }
+                    }
+                });
+            }
+            if (MC)   // every release (ours and the peer's) has arrived before the CTA may exit
+                for (int i = 0; i < NSLOT; i++) {
+                    mbar_wait(&empty[slot], phase ^ 1);
+                    if (++slot == NSLOT) { slot = 0; phase ^= 1; }
+                }
+            for (int pi = 0; !MC; pi++) {
                 const int64_t b0 = next();
                 const int64_t b1 = b0 < nbatch ? next() : nbatch;
                 publish(2 * pi, b0);
@@ -269,16 +302,20 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
                 return rb + (uint32_t)slot * SLOTB;
             };
             auto release = [&]() {
-                commit(&empty[slot]);
+                if (MC) commit_mc(&empty[slot], (uint16_t)3);
+                else commit(&empty[slot]);
                 if (++slot == NSLOT) { slot = 0; phase ^= 1; }
             };
             for (int pi = 0;; pi++) {
                 const int64_t b0 = bq_read(2 * pi);
                 mbar_arrive(&bqe[(2 * pi) & 3]);
-                if (b0 >= nbatch) break;
+                if (!MC && b0 >= nbatch) break;
                 const int64_t b1 = bq_read(2 * pi + 1);
                 mbar_arrive(&bqe[(2 * pi + 1) & 3]);
-                const int ns = b1 < nbatch ? 2 : 1;
+                if (MC && mc_base(pi) >= nbatch) break;
+                // MC: the pair streams both slots' weights whether or not this CTA has the batches
+                const int ns = (MC || b1 < nbatch) ? 2 : 1;
+                const bool valid[2] = {b0 < nbatch, b1 < nbatch};
                 for_each_step(ns, [&](int seg, int, int sl) {
                     // slots this step runs (sl = -1: both, k-steps interleaved per ring piece)
                     const int s_lo = sl < 0 ? 0 : sl, s_hi = sl < 0 ? ns : sl + 1;
@@ -286,6 +323,7 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
                     for (int s0 = 0; s0 < K; s0 += Gs) {
                         const uint32_t w = acquire();
                         for (int s = s_lo; s < s_hi; s++) {
+                            if (MC && !valid[s]) continue;
                             const uint32_t par = kbs[s] & 1;
                             const uint32_t tb = tmem + (uint32_t)(s * 256);
                             if (s0 == 0) {   // the slot's operand is ready: views (conv1), hidden (pass a), pass a read (b)
@@ -323,11 +361,12 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
                         release();
                     }
                     for (int s = s_lo; s < s_hi; s++) {
+                        if (MC && !valid[s]) continue;
                         commit(seg == 0 ? &a1t[s] : &a2t[s]);
                         if (seg == 2) kbs[s]++;
                     }
                 });
-                if (ns == 1) break;
+                if (!MC && ns == 1) break;
             }
             if (a.dbg) {
                 unsigned long long* o = a.dbg + blockIdx.x * 16;
@@ -535,6 +574,7 @@ __global__ void __launch_bounds__(ts2::kThreads, 1) k_stage_ts2(TsArgs a) {
     }
     fence_before();
     __syncthreads();
+    if (MC) cluster_sync();   // no multicast or remote arrival still in flight towards either CTA
     if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
@@ -549,20 +589,58 @@ int64_t stage_ts2_block_bytes(int pm) {
 int stage_ts2_smem(int pm) { return ts2::smem_bytes(pm); }
 
 typedef void (*Ts2Kernel)(TsArgs);
-static Ts2Kernel ts2_kernel(int pm) { return pm == 2 ? k_stage_ts2<2> : (pm == 1 ? k_stage_ts2<1> : k_stage_ts2<0>); }
+static Ts2Kernel ts2_kernel(int pm, bool mc) {
+    if (mc) return pm == 2 ? k_stage_ts2<2, true> : (pm == 1 ? k_stage_ts2<1, true> : k_stage_ts2<0, true>);
+    return pm == 2 ? k_stage_ts2<2, false> : (pm == 1 ? k_stage_ts2<1, false> : k_stage_ts2<0, false>);
+}
+static bool ts2_mc() { static const bool on = getenv("CI_TS2_MC") != nullptr; return on; }   // A/B switch
+static int ts2_max_clusters[3] = {0, 0, 0};
+
+static cudaLaunchConfig_t ts2_config(int pm, int grid, cudaStream_t st, cudaLaunchAttribute* attr) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(ts2::kThreads);
+    cfg.dynamicSmemBytes = ts2::smem_bytes(pm);
+    cfg.stream = st;
+    attr->id = cudaLaunchAttributeClusterDimension;
+    attr->val.clusterDim.x = 2;
+    attr->val.clusterDim.y = 1;
+    attr->val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cfg;
+}
 
 cudaError_t stage_ts2_prepare() {
     cudaError_t e = cudaSuccess;
     for (int pm = 0; pm < 3 && e == cudaSuccess; pm++)
-        e = cudaFuncSetAttribute(ts2_kernel(pm), cudaFuncAttributeMaxDynamicSharedMemorySize, ts2::smem_bytes(pm));
+        for (int mc = 0; mc < 2 && e == cudaSuccess; mc++)
+            e = cudaFuncSetAttribute(ts2_kernel(pm, mc), cudaFuncAttributeMaxDynamicSharedMemorySize, ts2::smem_bytes(pm));
+    for (int pm = 0; pm < 3 && e == cudaSuccess; pm++) {   // pairs of SMs the cluster launch can hold at once
+        cudaLaunchAttribute attr;
+        cudaLaunchConfig_t cfg = ts2_config(pm, 2, nullptr, &attr);
+        if (cudaOccupancyMaxActiveClusters(&ts2_max_clusters[pm], (const void*)ts2_kernel(pm, true), &cfg) != cudaSuccess) {
+            ts2_max_clusters[pm] = 0;   // no cluster launch: the single-CTA kernel runs
+            (void)cudaGetLastError();
+        }
+    }
+    if (getenv("CI_DEBUG_PLAN"))
+        fprintf(stderr, "[ci plan] ts2 cluster pairs resident: %d %d %d\n", ts2_max_clusters[0], ts2_max_clusters[1],
+                ts2_max_clusters[2]);
     return e;
 }
 
 cudaError_t launch_stage_ts2(const TsArgs& a, int pm, cudaStream_t st) {
     if (a.n <= 0) return cudaSuccess;
     const int64_t nbatch = (a.n + 1) / 2;
+    if (ts2_mc() && ts2_max_clusters[pm] > 0) {
+        const int grid = 2 * (int)std::min<int64_t>((nbatch + 3) / 4, ts2_max_clusters[pm]);
+        cudaLaunchAttribute attr;
+        cudaLaunchConfig_t cfg = ts2_config(pm, grid, st, &attr);
+        return cudaLaunchKernelEx(&cfg, ts2_kernel(pm, true), a);
+    }
     const int grid = (int)std::min<int64_t>((nbatch + 1) / 2, 148);
-    ts2_kernel(pm)<<<grid, ts2::kThreads, ts2::smem_bytes(pm), st>>>(a);
+    ts2_kernel(pm, false)<<<grid, ts2::kThreads, ts2::smem_bytes(pm), st>>>(a);
     return cudaGetLastError();
 }
 
