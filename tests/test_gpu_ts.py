@@ -138,3 +138,45 @@ def test_ts_degenerate_single_group(ci, k):
     assert max(e.values()) < 1e-3
     if k == 1:
         assert relerr(xp.cpu().numpy().reshape(1, -1), x.reshape(1, -1)) < 1e-5
+
+
+_MC_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, ".")
+import fixtures as fx
+from paper_2106_06445_b200 import codedinv as ci
+arch = fx.ARCH_C
+m = ci.Model(arch, fx.make_weights(arch, 13), sys.argv[2])
+n = int(sys.argv[3])
+x = torch.from_numpy(np.ascontiguousarray(fx.make_inputs(arch, 1, n, 41)[0])).cuda()
+h = torch.empty(n, arch.d, device="cuda")
+ws = m.workspace(1, n)
+m.ci_forward_h(x.view(n, 3, 32, 32), h, ws)
+xr = torch.empty(n, 3, 32, 32, device="cuda")
+m.ci_inverse_h(h, xr, ws)
+torch.cuda.synchronize()
+np.savez(sys.argv[1], h=h.cpu().numpy(), xr=xr.cpu().numpy())
+"""
+
+
+@pytest.mark.parametrize("n", [5, 301, 1187])
+def test_ts2_cluster_multicast_bit_exact(ci, tmp_path, n):
+    """The cluster-multicast weight stream of k_stage_ts2 (CI_TS2_MC, read once per process: run in
+    a subprocess) changes only where the weights come from and which CTA takes which batch: h and
+    h^-1 are bit-identical to the default kernel, including the tails where one CTA of a pair has
+    no batch (n = 5: 3 batches for one cluster; 1187: a partial last iteration)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for mc in (False, True):
+        env = dict(os.environ)
+        env.pop("CI_TS2_MC", None)
+        if mc:
+            env["CI_TS2_MC"] = "1"
+        f = str(tmp_path / f"mc{int(mc)}.npz")
+        subprocess.run([sys.executable, "-c", _MC_SCRIPT, f, "fp32", str(n)], cwd=root, env=env, check=True,
+                       timeout=300)
+        out[mc] = np.load(f)
+    assert np.array_equal(out[False]["h"], out[True]["h"])
+    assert np.array_equal(out[False]["xr"], out[True]["xr"])
